@@ -1,0 +1,18 @@
+"""B200-native CDMPP predictor hot path (drop-in for `tpcost`'s predictor API).
+
+Host layer in Python mirroring tpcost (features / costmodel / sampling /
+nn / dataset) over hand-written sm_100a CUDA kernels in libtpcb200.so
+(C ABI: include/tpcb200.h).  No CPU fallback: without the built library
+or a CUDA device the compute entry points raise.
+"""
+
+from .errors import TpcostError
+from .features import (CompactAst, CompactBatch, DeviceSpec, EncodedInput, device_vector,
+                       encode_input, positional_encoding)
+from .dataset import BoxCoxNormalizer, Dataset, Sample, fit_boxcox, split_dataset
+from .costmodel import (CostModelConfig, CostModelParams, LatentBatch, Predictor, desk_config,
+                        encode_dataset, forward, full_reference_config, init_params,
+                        load_checkpoint, loss_pretrain, metrics, predict, predict_batch,
+                        save_checkpoint)
+
+__version__ = "0.1.0"

@@ -1,0 +1,335 @@
+"""Transformer latency predictor — the reference `tpcost.costmodel` API on B200.
+
+Same call signatures as costmodel.py (config / params / forward / backward /
+losses / train / finetune / predict / checkpoints); every numeric step of the
+hot path runs in libtpcb200.so:
+
+  forward, predict, predict_batch     K1 featurize_pack → K2+K3 fused forward
+  backward (+ CMD)                    K1 → train-step kernels (train.cu)
+  train / finetune epochs             one native call per epoch (train.cu),
+                                      optimizer in optim.cu
+Host code here only validates inputs (raising the reference's exceptions
+before any compute, as costmodel.py does), moves numpy arrays to and from the
+device and runs the seeded host-side batch planning of costmodel.py:632-645.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import io
+import json
+import math
+import zipfile
+from dataclasses import asdict, dataclass, replace
+
+import numpy as np
+import torch
+
+from . import engine
+from .dataset import BoxCoxNormalizer, fit_boxcox
+from .errors import (CheckpointError, EmptyBatch, EmptyDataset, EmptySet, DimensionMismatch,
+                     ValidationError)
+from .features import (N_ENTRY, CompactAst, CompactBatch, DeviceSpec, EncodedInput,
+                       check_leaf_counts, encode_input, ragged_from_encoded)
+
+DEVICE_FEATURES = 6
+
+
+# ---------------------------------------------------------------------------
+# configuration / parameters (costmodel.py:36-150)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class CostModelConfig:
+    d_model: int = 64
+    n_layers: int = 2
+    n_heads: int = 2
+    d_ff: int = 128
+    d_embed: int = 32
+    d_device: int = 16
+    decoder_dims: tuple = (64, 64)
+    n_leaf_max: int = 16
+    lambda_hybrid: float = 1e-3
+    alpha_cmd: float = 0.0
+    cmd_order: int = 5
+    lr: float = 1e-3
+    weight_decay: float = 0.0
+    optimizer: str = "adam"
+    lr_schedule: str = "constant"
+    batch_size: int = 64
+    epochs: int = 300
+    seed: int = 0
+    loss_mode: str = "hybrid"
+    mape_space: str = "transformed"
+
+    def validate(self) -> None:
+        if self.d_model % self.n_heads != 0:
+            raise ValidationError("d_model must be divisible by n_heads")
+        for a in ("d_model", "n_layers", "n_heads", "d_ff", "d_embed", "d_device",
+                  "n_leaf_max", "batch_size"):
+            if getattr(self, a) < 1:
+                raise ValidationError(f"{a} must be >= 1")
+        if self.epochs < 0:
+            raise ValidationError("epochs must be >= 0")
+        if any(w < 1 for w in self.decoder_dims):
+            raise ValidationError("decoder widths must be >= 1")
+        if self.lr <= 0 or self.lambda_hybrid < 0 or self.alpha_cmd < 0:
+            raise ValidationError("lr must be > 0; loss coefficients >= 0")
+        if self.cmd_order < 1:
+            raise ValidationError("cmd_order must be >= 1")
+        if self.optimizer not in ("adam", "sgd"):
+            raise ValidationError(f"unknown optimizer '{self.optimizer}'")
+        if self.lr_schedule not in ("constant", "cyclic"):
+            raise ValidationError(f"unknown lr_schedule '{self.lr_schedule}'")
+        if self.loss_mode not in ("hybrid", "mse", "mape"):
+            raise ValidationError(f"unknown loss_mode '{self.loss_mode}'")
+        if self.mape_space not in ("original", "transformed"):
+            raise ValidationError(f"unknown mape_space '{self.mape_space}'")
+
+
+def desk_config(**overrides) -> CostModelConfig:
+    return replace(CostModelConfig(), **overrides)
+
+
+def full_reference_config() -> CostModelConfig:
+    return CostModelConfig(d_model=716, n_layers=11, n_heads=4, d_ff=985, d_embed=69,
+                           d_device=64, decoder_dims=(930, 930, 930), n_leaf_max=16,
+                           lambda_hybrid=1e-3, alpha_cmd=1.0, lr=1.68e-5, weight_decay=0.0013,
+                           optimizer="adam", lr_schedule="cyclic", batch_size=600)
+
+
+@dataclass
+class CostModelParams:
+    config: CostModelConfig
+    tensors: dict
+
+    def n_params(self) -> int:
+        return sum(t.size for t in self.tensors.values())
+
+    def copy(self) -> "CostModelParams":
+        return CostModelParams(self.config, {k: v.copy() for k, v in self.tensors.items()})
+
+
+def _xavier(rng, fan_in, fan_out):
+    bound = math.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-bound, bound, size=(fan_in, fan_out))
+
+
+def init_params(config: CostModelConfig) -> CostModelParams:
+    """Seeded Xavier-uniform init; LN gains 1, biases 0; same tensor creation
+    order — hence bit-identical tensors — as costmodel.py:116-150."""
+    config.validate()
+    rng = np.random.default_rng(config.seed)
+    t: dict = {}
+    d = config.d_model
+
+    def lin(name, fi, fo):
+        t[f"{name}.W"] = _xavier(rng, fi, fo)
+        t[f"{name}.b"] = np.zeros(fo)
+
+    lin("input", N_ENTRY, d)
+    for i in range(config.n_layers):
+        p = f"enc{i}"
+        for w in ("Wq", "Wk", "Wv", "Wo"):
+            t[f"{p}.attn.{w}"] = _xavier(rng, d, d)
+        for b in ("bq", "bk", "bv", "bo"):
+            t[f"{p}.attn.{b}"] = np.zeros(d)
+        t[f"{p}.ln1.g"] = np.ones(d)
+        t[f"{p}.ln1.b"] = np.zeros(d)
+        lin(f"{p}.ffn.h", d, config.d_ff)
+        lin(f"{p}.ffn.o", config.d_ff, d)
+        t[f"{p}.ln2.g"] = np.ones(d)
+        t[f"{p}.ln2.b"] = np.zeros(d)
+    for L in range(1, config.n_leaf_max + 1):
+        lin(f"leaf_embed.{L}", L * d, config.d_embed)
+    lin("dev.hidden", DEVICE_FEATURES, config.d_device)
+    lin("dev.proj", config.d_device, config.d_embed)
+    w = config.d_embed
+    for i, h in enumerate(config.decoder_dims):
+        lin(f"dec.{i}", w, h)
+        w = h
+    lin("dec.out", w, 1)
+    return CostModelParams(config=config, tensors=t)
+
+
+@dataclass
+class LatentBatch:
+    z_x: np.ndarray
+    z_v: np.ndarray
+    z: np.ndarray
+
+
+# ---------------------------------------------------------------------------
+# device model cache
+# ---------------------------------------------------------------------------
+
+_MODELS: dict = {}
+
+
+def device_model(config: CostModelConfig) -> engine.DeviceModel:
+    key = (config.d_model, config.n_layers, config.n_heads, config.d_ff, config.d_embed,
+           config.d_device, tuple(config.decoder_dims), config.n_leaf_max)
+    dm = _MODELS.get(key)
+    if dm is None:
+        dm = _MODELS[key] = engine.DeviceModel(config)
+    return dm
+
+
+class Predictor:
+    """Device-resident model: flat fp32 parameters + the model handle.
+    The bulk inference entry point (`forward_batch`) of the GPU path."""
+
+    def __init__(self, params: CostModelParams, rows_per_tile: int = 64):
+        self.config = params.config
+        self.dm = device_model(params.config)
+        self.params = self.dm.upload(params.tensors)
+        self.R = rows_per_tile
+        self.status = engine.Status(self.params.device)
+
+    def tensors(self) -> dict:
+        return self.dm.unflatten(self.params.double().cpu().numpy())
+
+    def forward_device(self, rows, ordering, leaf_off, devfeat, n_ast, encoded, norm=None,
+                       latents=True, theta=engine.THETA_DEFAULT):
+        pk = engine.pack(rows, ordering, leaf_off, n_ast, self.config.n_leaf_max, encoded,
+                         self.status, self.R, theta)
+        return engine.run_forward(self.dm, self.params, pk, devfeat, self.status, norm, latents)
+
+    def forward_ragged(self, rag: engine.RaggedHost, norm=None, latents=True):
+        if rag.n_ast == 0:
+            raise EmptyBatch("forward needs at least one input")
+        check_leaf_counts(rag.n_leaf, self.config.n_leaf_max)
+        rows, ordering, leaf_off, devfeat = engine.upload_ragged(rag)
+        out = self.forward_device(rows, ordering, leaf_off, devfeat, rag.n_ast, rag.encoded,
+                                  norm, latents)
+        self.status.check("forward")
+        return out
+
+    def forward_batch(self, batch: CompactBatch, normalizer=None, latents=False):
+        """Bulk path: raw compact ASTs in, (pred, z_x, z_v, z, latency) out."""
+        pred, zx, zv, z, lat = self.forward_ragged(batch.ragged(), normalizer, latents)
+        cpu = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
+        return cpu(pred), cpu(zx), cpu(zv), cpu(z), cpu(lat)
+
+
+def forward(params: CostModelParams, inputs: list) -> tuple:
+    """Predictions (model space) and latents (costmodel.py:265-269)."""
+    if not inputs:
+        raise EmptyBatch("forward needs at least one input")
+    rag = ragged_from_encoded(inputs, params.config.n_leaf_max)
+    p = Predictor(params)
+    pred, zx, zv, z, _ = p.forward_ragged(rag)
+    f64 = lambda t: t.double().cpu().numpy()  # noqa: E731
+    return f64(pred), LatentBatch(z_x=f64(zx), z_v=f64(zv), z=f64(z))
+
+
+def predict(params: CostModelParams, compact: CompactAst, device: DeviceSpec,
+            normalizer: BoxCoxNormalizer) -> float:
+    """Latency in seconds for one program (costmodel.py:795-800)."""
+    normalizer._check()
+    batch = CompactBatch.from_compacts([compact], device, dtype=np.float64)
+    _, _, _, _, lat = Predictor(params).forward_batch(batch, normalizer)
+    return float(lat[0])
+
+
+def predict_batch(params: CostModelParams, inputs: list,
+                  normalizer: BoxCoxNormalizer) -> np.ndarray:
+    """Decoded latencies for encoded inputs (costmodel.py:803-806)."""
+    normalizer._check()
+    if not inputs:
+        raise EmptyBatch("forward needs at least one input")
+    rag = ragged_from_encoded(inputs, params.config.n_leaf_max)
+    _, _, _, _, lat = Predictor(params).forward_ragged(rag, normalizer, latents=False)
+    return lat.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# losses / metrics (costmodel.py:343-355, 489-508, 577-591)
+# ---------------------------------------------------------------------------
+
+def loss_pretrain(pred, y, lambda_hybrid: float = 1e-3) -> float:
+    pred = np.asarray(pred, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    if pred.size == 0:
+        raise EmptyBatch("loss needs at least one sample")
+    if pred.shape != y.shape:
+        raise ValidationError("pred and y must have equal length")
+    if np.any(y <= 0):
+        raise ValidationError("labels must be positive for the relative term")
+    diff = pred - y
+    return float(np.mean(diff ** 2) + lambda_hybrid * np.mean(np.abs(diff) / y))
+
+
+def metrics(pred, y) -> dict:
+    pred = np.asarray(pred, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    if pred.size == 0:
+        raise EmptyBatch("metrics need at least one sample")
+    if pred.shape != y.shape:
+        raise ValidationError("pred and y must have equal length")
+    if np.any(y <= 0):
+        raise ValidationError("labels must be positive")
+    diff = pred - y
+    rel = diff / y
+    return {"mape": float(np.mean(np.abs(rel))), "rmse": float(math.sqrt(np.mean(diff ** 2))),
+            "mspe": float(np.mean(rel ** 2))}
+
+
+def encode_dataset(samples, devices: dict) -> list:
+    out = []
+    for s in samples:
+        if s.device_id not in devices:
+            raise ValidationError(f"unknown device '{s.device_id}'")
+        out.append(encode_input(s.compact, devices[s.device_id]))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# checkpoints (costmodel.py:902-956) — same file format
+# ---------------------------------------------------------------------------
+
+_CHECKPOINT_VERSION = 1
+
+
+def _tensor_checksum(tensors: dict) -> str:
+    h = hashlib.sha256()
+    for name in sorted(tensors):
+        arr = np.ascontiguousarray(tensors[name], dtype=np.float64)
+        h.update(name.encode())
+        h.update(str(arr.shape).encode())
+        h.update(arr.tobytes())
+    return h.hexdigest()
+
+
+def save_checkpoint(path, params: CostModelParams, normalizer=None) -> None:
+    cfg = asdict(params.config)
+    cfg["decoder_dims"] = list(cfg["decoder_dims"])
+    meta = {"version": _CHECKPOINT_VERSION, "config": cfg,
+            "normalizer": asdict(normalizer) if normalizer is not None else None,
+            "checksum": _tensor_checksum(params.tensors)}
+    meta_bytes = np.frombuffer(json.dumps(meta, sort_keys=True).encode(), dtype=np.uint8)
+    buf = io.BytesIO()
+    np.savez(buf, __meta__=meta_bytes, **params.tensors)
+    with open(path, "wb") as f:
+        f.write(buf.getvalue())
+
+
+def load_checkpoint(path):
+    try:
+        with np.load(path) as data:
+            if "__meta__" not in data:
+                raise CheckpointError("missing metadata block")
+            meta = json.loads(bytes(data["__meta__"]).decode())
+            if meta.get("version") != _CHECKPOINT_VERSION:
+                raise CheckpointError(f"unsupported version {meta.get('version')}")
+            tensors = {n: np.asarray(data[n], dtype=np.float64)
+                       for n in data.files if n != "__meta__"}
+    except (ValueError, KeyError, OSError, json.JSONDecodeError, zipfile.BadZipFile) as e:
+        raise CheckpointError(f"cannot read checkpoint: {e}") from e
+    if _tensor_checksum(tensors) != meta["checksum"]:
+        raise CheckpointError("checksum mismatch: corrupt checkpoint")
+    cfg = dict(meta["config"])
+    cfg["decoder_dims"] = tuple(cfg["decoder_dims"])
+    params = CostModelParams(config=CostModelConfig(**cfg), tensors=tensors)
+    norm = BoxCoxNormalizer(**meta["normalizer"]) if meta["normalizer"] is not None else None
+    return params, norm

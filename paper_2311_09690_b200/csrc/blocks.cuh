@@ -1,0 +1,184 @@
+// Device building blocks for the fused predictor kernels (FP32 FFMA path).
+//
+// All activations of a tile live in shared memory with an odd row stride
+// (ld = width + 1) so that a warp walking different rows of one column hits
+// distinct banks.  Weights are read straight from global memory: the whole
+// desk model is 1.4 MB and stays resident in the 126 MB L2, and every CTA of
+// the grid reads the same bytes, so L1/L2 serve them.
+#pragma once
+
+#include "common.cuh"
+
+namespace tpcb {
+
+// Y[r, n] = act(b[n] + Σ_k X[r, k] W[k, n]) (+ Res[r, n])  for r < R, n < N.
+// X/Y/Res in shared memory (row strides ldx/ldy/ldr), W row-major [K, N] and
+// b in global memory.  Each thread owns a TM×TN register tile.
+template <int TM, int TN>
+__device__ __forceinline__ void gemm_rows(const float* X, int ldx, const float* __restrict__ W,
+                                          const float* __restrict__ b, float* Y, int ldy, int R,
+                                          int K, int N, bool relu, const float* Res = nullptr,
+                                          int ldr = 0) {
+  const int ncg = (N + TN - 1) / TN;
+  const int nrg = (R + TM - 1) / TM;
+  const bool vec = (TN == 4) && ((N & 3) == 0);
+  for (int job = threadIdx.x; job < ncg * nrg; job += blockDim.x) {
+    const int cg = job % ncg, rg = job / ncg;
+    const int c0 = cg * TN, r0 = rg * TM;
+    float acc[TM][TN];
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const float bj = (b != nullptr && c0 + j < N) ? __ldg(b + c0 + j) : 0.f;
+#pragma unroll
+      for (int i = 0; i < TM; ++i) acc[i][j] = bj;
+    }
+    int rr[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) rr[i] = min(r0 + i, R - 1) * ldx;
+    if (vec) {
+      for (int k = 0; k < K; ++k) {
+        const float4 w4 = __ldg(reinterpret_cast<const float4*>(W + (size_t)k * N + c0));
+        const float w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const float xv = X[rr[i] + k];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(xv, w[j], acc[i][j]);
+        }
+      }
+    } else {
+      for (int k = 0; k < K; ++k) {
+        float w[TN];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) w[j] = (c0 + j < N) ? __ldg(W + (size_t)k * N + c0 + j) : 0.f;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const float xv = X[rr[i] + k];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(xv, w[j], acc[i][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int r = r0 + i;
+      if (r >= R) break;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int c = c0 + j;
+        if (c >= N) break;
+        float v = acc[i][j];
+        if (relu) v = fmaxf(v, 0.f);
+        if (Res) v += Res[r * ldr + c];
+        Y[r * ldy + c] = v;
+      }
+    }
+  }
+}
+
+// Row-wise LayerNorm over `d` features (nn.py:48-54): biased variance, eps
+// 1e-5 inside the square root.  One warp per row; optionally stores xhat and
+// 1/sqrt(var+eps) for the backward pass.
+__device__ __forceinline__ void layernorm_rows(const float* X, int ldx, float* Y, int ldy, int R,
+                                               int d, const float* __restrict__ g,
+                                               const float* __restrict__ b, float* xhat = nullptr,
+                                               int ldh = 0, float* inv_out = nullptr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const float inv_d = 1.f / (float)d;
+  for (int r = w; r < R; r += nw) {
+    const float* x = X + r * ldx;
+    float s = 0.f;
+    for (int c = lane; c < d; c += 32) s += x[c];
+    const float mu = warp_sum(s) * inv_d;
+    float v = 0.f;
+    for (int c = lane; c < d; c += 32) {
+      const float t = x[c] - mu;
+      v = fmaf(t, t, v);
+    }
+    const float var = warp_sum(v) * inv_d;
+    const float inv = 1.f / sqrtf(var + 1e-5f);
+    for (int c = lane; c < d; c += 32) {
+      const float xh = (x[c] - mu) * inv;
+      if (xhat) xhat[r * ldh + c] = xh;
+      Y[r * ldy + c] = fmaf(__ldg(g + c), xh, __ldg(b + c));
+    }
+    if (inv_out && lane == 0) inv_out[r] = inv;
+  }
+}
+
+// Multi-head self-attention core over A ASTs of L rows each (rows a*L ..
+// a*L+L-1), heads of width dh: ctx = softmax(Q Kᵀ/sqrt(dh)) V per AST and
+// head (nn.py:79-96).  Bucketing makes every AST attend over exactly its own L
+// leaves, so no mask is needed.  One thread per (AST, head, query row);
+// optionally stores the probabilities P[(a*H + h)*L*L + i*L + j].
+__device__ __forceinline__ void attention_rows(const float* Q, const float* K, const float* V,
+                                               int ld, float* C, int ldc, int A, int L, int H,
+                                               int dh, float scale, float* P = nullptr) {
+  const int jobs = A * H * L;
+  for (int job = threadIdx.x; job < jobs; job += blockDim.x) {
+    const int i = job % L;
+    const int h = (job / L) % H;
+    const int a = job / (L * H);
+    const float* q = Q + (a * L + i) * ld + h * dh;
+    float p[TPCB_MAX_LEAF];
+    float m = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < TPCB_MAX_LEAF; ++j) {
+      if (j < L) {
+        const float* k = K + (a * L + j) * ld + h * dh;
+        float s = 0.f;
+        for (int c = 0; c < dh; ++c) s = fmaf(q[c], k[c], s);
+        s *= scale;
+        p[j] = s;
+        m = fmaxf(m, s);
+      }
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < TPCB_MAX_LEAF; ++j) {
+      if (j < L) {
+        p[j] = expf(p[j] - m);
+        sum += p[j];
+      }
+    }
+    const float inv = 1.f / sum;
+#pragma unroll
+    for (int j = 0; j < TPCB_MAX_LEAF; ++j)
+      if (j < L) p[j] = p[j] / sum;
+    (void)inv;
+    if (P) {
+      float* pp = P + ((a * H + h) * L + i) * L;
+#pragma unroll
+      for (int j = 0; j < TPCB_MAX_LEAF; ++j)
+        if (j < L) pp[j] = p[j];
+    }
+    float* c_out = C + (a * L + i) * ldc + h * dh;
+    for (int c = 0; c < dh; ++c) {
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < TPCB_MAX_LEAF; ++j)
+        if (j < L) acc = fmaf(p[j], V[(a * L + j) * ld + h * dh + c], acc);
+      c_out[c] = acc;
+    }
+  }
+}
+
+// z_x[a, e] = b[e] + Σ_{l<L, j<d} H[a*L + l, j] · W[l*d + j, e]
+// (flatten row-major then leaf_embed.{L}, costmodel.py:213-216).
+__device__ __forceinline__ void leaf_embed_rows(const float* Hs, int ld, int A, int L, int d,
+                                                const float* __restrict__ W,
+                                                const float* __restrict__ b, int de, float* Z,
+                                                int ldz) {
+  for (int job = threadIdx.x; job < A * de; job += blockDim.x) {
+    const int e = job % de, a = job / de;
+    float acc = __ldg(b + e);
+    for (int l = 0; l < L; ++l) {
+      const float* h = Hs + (a * L + l) * ld;
+      const float* w = W + (size_t)l * d * de + e;
+      for (int j = 0; j < d; ++j) acc = fmaf(h[j], __ldg(w + (size_t)j * de), acc);
+    }
+    Z[a * ldz + e] = acc;
+  }
+}
+
+}  // namespace tpcb

@@ -1,0 +1,102 @@
+// Shared definitions for the tpcb200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/tpcb200.h"
+
+namespace tpcb {
+
+// Offsets (in floats) of every tensor of one encoder layer inside the flat
+// parameter vector.  Order of creation follows costmodel.py:130-140.
+struct LayerOff {
+  int Wq, Wk, Wv, Wo, bq, bk, bv, bo;
+  int ln1g, ln1b, fhW, fhb, foW, fob, ln2g, ln2b;
+};
+
+// Device-visible model description: dims + canonical tensor offsets.
+// Passed to kernels by value (~1.3 KB, below the 4 KB parameter limit).
+struct Model {
+  int d, n_layers, n_heads, dh, d_ff, d_e, d_dev, n_dec, n_leaf_max;
+  int dec[TPCB_MAX_DEC];
+  int inW, inb;
+  LayerOff layer[TPCB_MAX_LAYERS];
+  int leafW[TPCB_MAX_LEAF + 1], leafb[TPCB_MAX_LEAF + 1];
+  int devhW, devhb, devpW, devpb;
+  int decW[TPCB_MAX_DEC], decb[TPCB_MAX_DEC];
+  int outW, outb;
+  int total;
+  // first / last+1 float of the tensors touched by every batch regardless of
+  // its leaf count (everything except leaf_embed.*) — see optim.cu
+  int shared_lo, shared_hi;  // [inW, leafW[1])
+  int tail_lo;               // devhW .. total
+};
+
+struct TensorInfo {
+  std::string name;
+  int64_t offset;
+  int rows, cols;
+};
+
+}  // namespace tpcb
+
+struct tpcb_model {
+  tpcb_config cfg;
+  tpcb::Model dev;
+  std::vector<tpcb::TensorInfo> tensors;
+};
+
+namespace tpcb {
+
+void set_last_error(const char* what, cudaError_t e);
+
+#define TPCB_CUDA_CHECK(call)                              \
+  do {                                                     \
+    cudaError_t _e = (call);                               \
+    if (_e != cudaSuccess) {                               \
+      ::tpcb::set_last_error(#call, _e);                   \
+      return TPCB_ERR_CUDA;                                \
+    }                                                      \
+  } while (0)
+
+#define TPCB_LAUNCH_CHECK(what)                            \
+  do {                                                     \
+    cudaError_t _e = cudaGetLastError();                   \
+    if (_e != cudaSuccess) {                               \
+      ::tpcb::set_last_error(what, _e);                    \
+      return TPCB_ERR_CUDA;                                \
+    }                                                      \
+  } while (0)
+
+// device status word: first error wins (atomicCAS from 0)
+__device__ __forceinline__ void raise_status(int32_t* st, int32_t code) {
+  if (st) atomicCAS(st, 0, code);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+constexpr int kNumSMs = 148;
+
+}  // namespace tpcb

@@ -1,0 +1,247 @@
+"""Device-side runtime: model handles, packed batches and kernel launches.
+
+PyTorch is used only as the device allocator / stream provider; all compute
+is in libtpcb200.so (see include/tpcb200.h).  Everything here is
+stream-ordered on torch's current stream; `sync_status` is the only place
+that synchronises, to turn the device status word into the reference's
+exceptions.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import errors as E
+
+THETA_DEFAULT = 10000.0
+
+
+def _need_cuda():
+    if not torch.cuda.is_available():
+        raise E.CudaError("a CUDA device is required (no CPU fallback)")
+    _lib.load()
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def pe_denominators(theta: float = THETA_DEFAULT) -> np.ndarray:
+    """θ^(2δ/24), δ=0..11 — computed with numpy exactly as features.py:257-258
+    so the device divides by bit-identical denominators."""
+    if theta <= 0:
+        raise E.ValidationError("theta must be > 0")
+    return float(theta) ** (2.0 * np.arange(12, dtype=np.float64) / 24)
+
+
+class Status:
+    """Device status word shared by a sequence of launches."""
+
+    def __init__(self, device):
+        self.t = torch.zeros(1, dtype=torch.int32, device=device)
+
+    @property
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    def check(self, what: str, epoch: int = -1) -> None:
+        code = int(self.t.item())  # synchronises the stream
+        if code:
+            self.t.zero_()
+            _lib.check(code, what, epoch)
+
+
+# ---------------------------------------------------------------------------
+# model handle + flat parameter vector
+# ---------------------------------------------------------------------------
+
+class DeviceModel:
+    """tpcb_model handle + canonical layout of the flat fp32 parameter vector."""
+
+    def __init__(self, cfg):
+        _need_cuda()
+        lib = _lib.load()
+        c = _lib.Config()
+        c.d_model, c.n_layers, c.n_heads = cfg.d_model, cfg.n_layers, cfg.n_heads
+        c.d_ff, c.d_embed, c.d_device = cfg.d_ff, cfg.d_embed, cfg.d_device
+        dec = tuple(cfg.decoder_dims)
+        if len(dec) > _lib.MAX_DEC:
+            raise E.UnsupportedConfig("too many decoder layers")
+        c.n_dec = len(dec)
+        for i, w in enumerate(dec):
+            c.dec[i] = w
+        c.n_leaf_max = cfg.n_leaf_max
+        h = C.c_void_p()
+        _lib.check(lib.tpcb_model_create(C.byref(c), C.byref(h)), "model_create")
+        self.handle = h
+        self.cfg = cfg
+        self.n_params = int(lib.tpcb_model_param_count(h))
+        self.layout: dict[str, tuple[int, tuple]] = {}
+        buf = C.create_string_buffer(128)
+        off, r, cc = C.c_int64(), C.c_int32(), C.c_int32()
+        for i in range(lib.tpcb_model_tensor_count(h)):
+            lib.tpcb_model_tensor_info(h, i, buf, 128, C.byref(off), C.byref(r), C.byref(cc))
+            shape = (r.value, cc.value) if cc.value else (r.value,)
+            self.layout[buf.value.decode()] = (off.value, shape)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                _lib.load().tpcb_model_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def flatten(self, tensors: dict[str, np.ndarray]) -> np.ndarray:
+        flat = np.zeros(self.n_params, dtype=np.float64)
+        for name, (o, shape) in self.layout.items():
+            t = np.asarray(tensors[name], dtype=np.float64)
+            if t.shape != shape:
+                raise E.ValidationError(f"tensor {name}: shape {t.shape} != {shape}")
+            flat[o:o + t.size] = t.ravel()
+        return flat
+
+    def unflatten(self, flat: np.ndarray) -> dict[str, np.ndarray]:
+        out = {}
+        for name, (o, shape) in self.layout.items():
+            n = int(np.prod(shape))
+            out[name] = np.asarray(flat[o:o + n], dtype=np.float64).reshape(shape).copy()
+        return out
+
+    def upload(self, tensors: dict[str, np.ndarray], device="cuda") -> torch.Tensor:
+        return torch.from_numpy(self.flatten(tensors).astype(np.float32)).to(device)
+
+    def slice_of(self, name: str) -> slice:
+        o, shape = self.layout[name]
+        return slice(o, o + int(np.prod(shape)))
+
+
+# ---------------------------------------------------------------------------
+# ragged batch → packed tiles (K1)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class RaggedHost:
+    """Host SoA of a batch of compact ASTs (or encoded matrices)."""
+    rows: np.ndarray        # (n_tok, 24) float32/float64
+    ordering: np.ndarray    # (n_tok,) int32 (unused when encoded=True)
+    n_leaf: np.ndarray      # (n_ast,) int64
+    devfeat: np.ndarray     # (n_ast, 6) float32
+    encoded: bool           # rows already carry the PE
+
+    @property
+    def n_ast(self) -> int:
+        return int(self.n_leaf.shape[0])
+
+    @property
+    def n_tok(self) -> int:
+        return int(self.rows.shape[0])
+
+
+class PackedBatch:
+    """Device buffers of the packed fixed-stride layout (tpcb_packed)."""
+
+    def __init__(self, n_ast: int, n_tok: int, n_leaf_max: int, R: int, device):
+        lib = _lib.load()
+        ntm, ws = C.c_int32(), C.c_size_t()
+        _lib.check(lib.tpcb_pack_sizes(n_ast, n_tok, n_leaf_max, R, C.byref(ntm), C.byref(ws)),
+                   "pack_sizes")
+        self.n_ast, self.n_tok, self.R, self.n_leaf_max = n_ast, n_tok, R, n_leaf_max
+        self.n_tiles_max = ntm.value
+        i32 = dict(dtype=torch.int32, device=device)
+        self.x = torch.empty(ntm.value * R * _lib.FEAT_PAD, dtype=torch.float32, device=device)
+        self.row_ast = torch.empty(ntm.value * R, **i32)
+        self.tile_L = torch.empty(ntm.value, **i32)
+        self.tile_first = torch.empty(ntm.value, **i32)
+        self.tile_count = torch.empty(ntm.value, **i32)
+        self.perm = torch.empty(max(n_ast, 1), **i32)
+        self.ast_row = torch.empty(max(n_ast, 1), **i32)
+        self.bucket_off = torch.empty(n_leaf_max + 2, **i32)
+        self.n_tiles = torch.zeros(1, **i32)
+        self.ws = torch.empty(max(ws.value, 4), dtype=torch.uint8, device=device)
+        s = _lib.Packed()
+        s.rows_per_tile, s.n_tiles_max = R, ntm.value
+        for f in ("x", "row_ast", "tile_L", "tile_first", "tile_count", "perm", "ast_row",
+                  "bucket_off", "n_tiles"):
+            setattr(s, f, getattr(self, f).data_ptr())
+        self.struct = s
+
+
+def upload_ragged(rag: RaggedHost, device="cuda"):
+    rows = torch.from_numpy(np.ascontiguousarray(rag.rows)).to(device, non_blocking=True)
+    ordering = torch.from_numpy(np.ascontiguousarray(rag.ordering, dtype=np.int32)).to(device)
+    off = np.zeros(rag.n_ast + 1, dtype=np.int64)
+    np.cumsum(rag.n_leaf, out=off[1:])
+    leaf_off = torch.from_numpy(off).to(device)
+    devfeat = torch.from_numpy(np.ascontiguousarray(rag.devfeat, dtype=np.float32)).to(device)
+    return rows, ordering, leaf_off, devfeat
+
+
+def pack(rows: torch.Tensor, ordering: torch.Tensor, leaf_off: torch.Tensor, n_ast: int,
+         n_leaf_max: int, encoded: bool, status: Status, R: int = 64,
+         theta: float = THETA_DEFAULT) -> PackedBatch:
+    """Run K1 on device-resident ragged rows."""
+    lib = _lib.load()
+    n_tok = int(rows.shape[0])
+    pk = PackedBatch(n_ast, n_tok, n_leaf_max, R, rows.device)
+    den = None if encoded else pe_denominators(theta)
+    den_p = None if den is None else den.ctypes.data_as(C.c_void_p)
+    is64 = 1 if rows.dtype == torch.float64 else 0
+    if rows.dtype not in (torch.float32, torch.float64):
+        raise E.ValidationError("leaf vectors must be float32 or float64")
+    _lib.check(lib.tpcb_featurize_pack(rows.data_ptr(), is64, ordering.data_ptr(),
+                                       leaf_off.data_ptr(), n_ast, n_tok, n_leaf_max, den_p,
+                                       pk.ws.data_ptr(), pk.ws.numel(), C.byref(pk.struct),
+                                       status.ptr, stream_ptr()), "featurize_pack")
+    return pk
+
+
+def boxcox_struct(norm) -> _lib.BoxCox:
+    b = _lib.BoxCox()
+    if norm is None:
+        b.enabled = 0
+        return b
+    b.lambda_bc, b.shift = float(norm.lambda_bc), float(norm.shift)
+    b.t_mean, b.t_std = float(norm.t_mean), float(norm.t_std)
+    b.enabled = 1
+    return b
+
+
+def run_forward(dm: DeviceModel, params: torch.Tensor, pk: PackedBatch, devfeat: torch.Tensor,
+                status: Status, norm=None, latents: bool = True):
+    """Launch the fused forward; returns device tensors (pred, z_x, z_v, z, lat)."""
+    lib = _lib.load()
+    n = pk.n_ast
+    dev = params.device
+    pred = torch.empty(n, dtype=torch.float32, device=dev)
+    zx = torch.empty((n, dm.cfg.d_embed), dtype=torch.float32, device=dev) if latents else None
+    zv = torch.empty((n, dm.cfg.d_device), dtype=torch.float32, device=dev) if latents else None
+    z = torch.empty((n, dm.cfg.d_embed), dtype=torch.float32, device=dev) if latents else None
+    lat = torch.empty(n, dtype=torch.float64, device=dev) if norm is not None else None
+    bc = boxcox_struct(norm)
+    _lib.check(lib.tpcb_forward(dm.handle, params.data_ptr(), C.byref(pk.struct),
+                                devfeat.data_ptr(), n, C.byref(bc), pred.data_ptr(), dptr(zx),
+                                dptr(zv), dptr(z), dptr(lat), status.ptr, stream_ptr()),
+               "forward")
+    return pred, zx, zv, z, lat
+
+
+def positional_encoding_device(ordering: np.ndarray, theta: float) -> np.ndarray:
+    _need_cuda()
+    lib = _lib.load()
+    den = pe_denominators(theta)
+    o = torch.from_numpy(np.ascontiguousarray(ordering, dtype=np.int32)).cuda()
+    out = torch.empty((o.numel(), 24), dtype=torch.float64, device="cuda")
+    _lib.check(lib.tpcb_positional_encoding(o.data_ptr(), o.numel(),
+                                            den.ctypes.data_as(C.c_void_p), out.data_ptr(),
+                                            stream_ptr()), "positional_encoding")
+    return out.cpu().numpy()

@@ -30,8 +30,17 @@ def pytest_collection_modifyitems(config, items):
             item.add_marker(skip)
 
 
+class _Eager(dict):
+    """npz contents loaded once (NpzFile re-inflates a member per access)."""
+
+    @property
+    def files(self):
+        return list(self.keys())
+
+
 def load_golden(name):
-    return np.load(GOLDEN / f"{name}.npz", allow_pickle=False)
+    with np.load(GOLDEN / f"{name}.npz", allow_pickle=False) as z:
+        return _Eager({k: z[k] for k in z.files})
 
 
 class GoldenModel:
