@@ -137,6 +137,85 @@ int tpcb_forward(const tpcb_model* m, const float* d_params, const tpcb_packed* 
                  float* d_pred, float* d_zx, float* d_zv, float* d_z, double* d_latency,
                  int32_t* d_status, void* stream);
 
+/* ---- K4–K7: training ------------------------------------------------------
+ * Loss selection (costmodel.LossSpec, costmodel.py:511-526). */
+typedef struct {
+  int32_t mode;           /* 0 hybrid, 1 mse, 2 mape */
+  int32_t original_space; /* relative term on decoded latencies (needs norm) */
+  double lambda_hybrid, offset, alpha_cmd;
+  int32_t cmd_order;      /* K <= 8 */
+  tpcb_boxcox norm;
+} tpcb_loss;
+
+/* one dataset on the device: packed rows from tpcb_featurize_pack + per-sample data */
+typedef struct {
+  const float* x;          /* packed rows [*, 32] */
+  const int32_t* ast_row;  /* [n] first packed row of each sample */
+  const int32_t* n_leaf;   /* [n] */
+  const float* devfeat;    /* [n, 6] */
+  const double* y;         /* [n] model-space targets (source set only) */
+} tpcb_samples;
+
+/* optimizer (nn.Adam / nn.Sgd, nn.py:127-167) */
+typedef struct {
+  int32_t kind; /* 0 none, 1 adam, 2 sgd */
+  double beta1, beta2, eps, weight_decay;
+} tpcb_optim;
+
+/* caller-allocated training workspace (sizes from tpcb_train_ws_sizes) */
+typedef struct {
+  float* partial;       /* [n_slots * slot_stride] per-CTA gradient slots */
+  int64_t slot_stride;
+  int32_t n_slots;
+  uint32_t* touched;    /* [n_slots] */
+  float* zall;          /* [max_rows * d_embed] */
+  double* terms;        /* [max_rows * 2] */
+  double* scalars;      /* [8]: [0] CMD value, [1] loss value */
+} tpcb_train_ws;
+
+/* epoch plan: steps[s] = {offset into d_batch, n_src, n_tgt, 0} (int32 x4);
+ * d_batch holds each step's source sample indices then its target indices */
+typedef struct {
+  const int32_t* d_batch;
+  const int32_t* d_steps;
+  int32_t n_steps;
+} tpcb_plan;
+
+int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t* n_slots,
+                        int64_t* slot_stride, int64_t* zall_floats, int64_t* terms_doubles);
+/* refresh the transposed copy of every 2-D weight (read by the backward) */
+int tpcb_transpose_params(const tpcb_model* m, const float* d_params, float* d_params_t,
+                          void* stream);
+/* costmodel.backward (costmodel.py:529-570): loss value → ws->scalars[1],
+ * CMD value → ws->scalars[0], gradient of every parameter → d_grad [P]
+ * (zeros for tensors the batch does not touch), predictions → d_pred. */
+int tpcb_loss_backward(const tpcb_model* m, const float* d_params, const float* d_params_t,
+                       const tpcb_samples* src, const tpcb_samples* tgt, const int32_t* d_batch,
+                       int32_t n_src, int32_t n_tgt, const tpcb_loss* loss,
+                       const tpcb_train_ws* ws, void* d_step_scratch /* 16 B */, float* d_grad,
+                       float* d_pred, int32_t* d_status, void* stream);
+/* nn.Adam.step / nn.Sgd.step over a flat vector of n floats (t = 1-based
+ * step count).  With a model handle n is its parameter count and d_params_t
+ * (when non-NULL) is refreshed; m may be NULL for a bare vector. */
+int tpcb_optimizer_step(const tpcb_model* m, int64_t n, float* d_params, float* d_params_t,
+                        const float* d_grad, float* d_m, float* d_v, const tpcb_optim* opt,
+                        double lr, int64_t t, void* stream);
+/* the train/finetune inner loop (costmodel.py:700-706, 759-773) for one
+ * epoch: per step backward (+CMD) → reduce → optimizer → transpose.
+ * lr and the step count before the epoch are read from device memory;
+ * per-step loss / CMD values land in d_step_loss / d_step_cmd. */
+int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_params_t, float* d_m,
+                     float* d_v, const tpcb_samples* src, const tpcb_samples* tgt,
+                     const tpcb_plan* plan, const tpcb_loss* loss, const tpcb_optim* opt,
+                     const double* d_lr, const int64_t* d_t0, const tpcb_train_ws* ws,
+                     double* d_step_loss, double* d_step_cmd, int32_t* d_status, void* stream);
+
+/* ---- K6: CMD between two sets (costmodel.cmd, costmodel.py:489-503) ------
+ * d_z = [zs; zt] row-major [(ns+nt), de] (f32 or f64); value → d_value[0];
+ * when d_grad != NULL, dCMD/dz for every row (fp64, same layout). */
+int tpcb_cmd(const void* d_z, int32_t z_is_f64, int64_t ns, int64_t nt, int32_t de, int32_t k,
+             double* d_value, double* d_grad, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

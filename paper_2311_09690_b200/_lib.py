@@ -46,9 +46,22 @@ class LossCfg(C.Structure):
                 ("norm", BoxCox)]
 
 
-class AdamCfg(C.Structure):
+class OptimCfg(C.Structure):
     _fields_ = [("kind", i32), ("beta1", f64), ("beta2", f64), ("eps", f64),
                 ("weight_decay", f64)]
+
+
+class Samples(C.Structure):
+    _fields_ = [("x", vp), ("ast_row", vp), ("n_leaf", vp), ("devfeat", vp), ("y", vp)]
+
+
+class TrainWs(C.Structure):
+    _fields_ = [("partial", vp), ("slot_stride", i64), ("n_slots", i32), ("touched", vp),
+                ("zall", vp), ("terms", vp), ("scalars", vp)]
+
+
+class Plan(C.Structure):
+    _fields_ = [("d_batch", vp), ("d_steps", vp), ("n_steps", i32)]
 
 
 # name -> (restype, argtypes)
@@ -67,6 +80,18 @@ SIGNATURES = {
     "tpcb_positional_encoding": (i32, [vp, i64, vp, vp, vp]),
     "tpcb_forward": (i32, [vp, vp, C.POINTER(Packed), vp, i64, C.POINTER(BoxCox), vp, vp, vp,
                            vp, vp, vp, vp]),
+    "tpcb_cmd": (i32, [vp, i32, i64, i64, i32, i32, vp, vp, vp]),
+    "tpcb_train_ws_sizes": (i32, [vp, i32, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64),
+                                  C.POINTER(i64)]),
+    "tpcb_transpose_params": (i32, [vp, vp, vp, vp]),
+    "tpcb_loss_backward": (i32, [vp, vp, vp, C.POINTER(Samples), C.POINTER(Samples), vp, i32,
+                                 i32, C.POINTER(LossCfg), C.POINTER(TrainWs), vp, vp, vp, vp,
+                                 vp]),
+    "tpcb_optimizer_step": (i32, [vp, i64, vp, vp, vp, vp, vp, C.POINTER(OptimCfg), f64, i64,
+                                  vp]),
+    "tpcb_train_epoch": (i32, [vp, vp, vp, vp, vp, C.POINTER(Samples), C.POINTER(Samples),
+                               C.POINTER(Plan), C.POINTER(LossCfg), C.POINTER(OptimCfg), vp, vp,
+                               C.POINTER(TrainWs), vp, vp, vp, vp]),
 }
 
 STATUS_EXC = {

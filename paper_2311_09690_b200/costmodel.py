@@ -27,8 +27,8 @@ import torch
 
 from . import engine
 from .dataset import BoxCoxNormalizer, fit_boxcox
-from .errors import (CheckpointError, EmptyBatch, EmptyDataset, EmptySet, DimensionMismatch,
-                     ValidationError)
+from .errors import (CheckpointError, DimensionMismatch, DomainError, EmptyBatch,
+                     EmptyDataset, EmptySet, NonFiniteLoss, ValidationError)
 from .features import (N_ENTRY, CompactAst, CompactBatch, DeviceSpec, EncodedInput,
                        check_leaf_counts, encode_input, ragged_from_encoded)
 
@@ -282,6 +282,128 @@ def encode_dataset(samples, devices: dict) -> list:
             raise ValidationError(f"unknown device '{s.device_id}'")
         out.append(encode_input(s.compact, devices[s.device_id]))
     return out
+
+
+# ---------------------------------------------------------------------------
+# CMD (costmodel.py:489-508, 783-788)
+# ---------------------------------------------------------------------------
+
+def _cmd_device(zs, zt, k: int, want_grad: bool):
+    zs = np.atleast_2d(np.asarray(zs, dtype=np.float64))
+    zt = np.atleast_2d(np.asarray(zt, dtype=np.float64))
+    if zs.shape[0] == 0 or zt.shape[0] == 0:
+        raise EmptySet("cmd needs non-empty sets")
+    if zs.shape[1] != zt.shape[1]:
+        raise DimensionMismatch(f"column mismatch: {zs.shape[1]} vs {zt.shape[1]}")
+    engine._need_cuda()
+    z = torch.from_numpy(np.ascontiguousarray(np.vstack([zs, zt]))).cuda()
+    val = torch.zeros(1, dtype=torch.float64, device=z.device)
+    grad = torch.empty_like(z) if want_grad else None
+    lib = engine._lib.load()
+    engine._lib.check(lib.tpcb_cmd(z.data_ptr(), 1, zs.shape[0], zt.shape[0], zs.shape[1], int(k),
+                                   val.data_ptr(), engine.dptr(grad), engine.stream_ptr()), "cmd")
+    value = float(val.item())
+    if not want_grad:
+        return value
+    g = grad.cpu().numpy()
+    return value, g[:zs.shape[0]], g[zs.shape[0]:]
+
+
+def cmd(zs, zt, k: int = 5) -> float:
+    """Central moment discrepancy between two sample sets, fp64 on the GPU."""
+    return _cmd_device(zs, zt, k, False)
+
+
+def cmd_grad(zs, zt, k: int = 5):
+    """(value, dCMD/dzs, dCMD/dzt) — `_cmd_forward_backward` (costmodel.py:426-486)."""
+    return _cmd_device(zs, zt, k, True)
+
+
+def loss_finetune(pred, y, zs, zt, lambda_hybrid: float = 1e-3, alpha_cmd: float = 1.0,
+                  k: int = 5) -> float:
+    return loss_pretrain(pred, y, lambda_hybrid) + alpha_cmd * cmd(zs, zt, k)
+
+
+def cmd_between(params: CostModelParams, source_inputs: list, target_inputs: list,
+                k: int = 5) -> float:
+    """CMD between the aggregated latents of two full input sets."""
+    _, ls = forward(params, source_inputs)
+    _, lt = forward(params, target_inputs)
+    return cmd(ls.z, lt.z, k)
+
+
+# ---------------------------------------------------------------------------
+# backward (costmodel.py:511-570)
+# ---------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class LossSpec:
+    mode: str = "hybrid"
+    lambda_hybrid: float = 1e-3
+    alpha_cmd: float = 0.0
+    cmd_order: int = 5
+    offset: float = 0.0
+    mape_space: str = "transformed"
+    normalizer: BoxCoxNormalizer | None = None
+
+
+def _check_loss(loss: LossSpec, targets: np.ndarray) -> None:
+    if loss.mode not in ("hybrid", "mse", "mape"):
+        raise ValidationError(f"unknown loss mode '{loss.mode}'")
+    if loss.mode == "mse":
+        return
+    if loss.mape_space == "original":
+        if loss.normalizer is None:
+            raise ValidationError("original-space relative loss needs a fitted normalizer")
+        loss.normalizer._check()
+        t = np.asarray(targets) * loss.normalizer.t_std + loss.normalizer.t_mean
+        if abs(loss.normalizer.lambda_bc) >= 1e-9 and np.any(loss.normalizer.lambda_bc * t + 1.0 <= 0):
+            raise DomainError("no positive preimage: lambda*t + 1 <= 0")
+    elif np.any(np.asarray(targets) + loss.offset <= 0):
+        raise ValidationError("shifted labels must be positive")
+
+
+def _loss_struct(loss: LossSpec):
+    return engine.loss_struct(loss.mode, loss.lambda_hybrid, loss.offset, loss.alpha_cmd,
+                              loss.cmd_order, loss.mape_space, loss.normalizer)
+
+
+def backward(params: CostModelParams, batch: list, targets, loss: LossSpec,
+             target_batch: list | None = None):
+    """Loss value and d(objective)/d(every parameter) (costmodel.py:529-570),
+    computed by the fused train-step kernels; with alpha_cmd > 0 and a target
+    batch the CMD term couples both forward passes."""
+    targets = np.asarray(targets, dtype=np.float64)
+    if not batch:
+        raise EmptyBatch("forward needs at least one input")
+    cfg = params.config
+    rag = ragged_from_encoded(batch, cfg.n_leaf_max)
+    if targets.shape != (len(batch),):
+        raise ValidationError("batch and targets must have equal length")
+    _check_loss(loss, targets)
+    use_cmd = loss.alpha_cmd > 0.0 and target_batch is not None
+    trag = None
+    if use_cmd:
+        if not target_batch:
+            raise EmptyBatch("forward needs at least one input")
+        trag = ragged_from_encoded(target_batch, cfg.n_leaf_max)
+    dm = device_model(cfg)
+    P = dm.upload(params.tensors)
+    PT = torch.empty_like(P)
+    engine.transpose_params(dm, P, PT)
+    st = engine.Status(P.device)
+    src = engine.DeviceSamples(rag, cfg.n_leaf_max, st, y=targets)
+    tgt = engine.DeviceSamples(trag, cfg.n_leaf_max, st) if use_cmd else None
+    ws = engine.TrainWorkspace(dm, src.n + (tgt.n if tgt else 0))
+    grad, pred = engine.run_backward(dm, P, PT, src, tgt, _loss_struct(loss), ws, st)
+    st.check("backward")
+    sc = ws.scalars.cpu().numpy()
+    value = float(sc[1])
+    cmd_value = float(sc[0]) if use_cmd else 0.0
+    grads = dm.unflatten(grad.double().cpu().numpy())
+    if not math.isfinite(value):
+        raise NonFiniteLoss(-1)
+    return value, grads, {"pred": pred.double().cpu().numpy(), "cmd": cmd_value}
 
 
 # ---------------------------------------------------------------------------

@@ -181,4 +181,123 @@ __device__ __forceinline__ void leaf_embed_rows(const float* Hs, int ld, int A, 
   }
 }
 
+// ---------------------------------------------------------------------------
+// backward helpers
+// ---------------------------------------------------------------------------
+
+// first ? G[i] = v : G[i] += v — gradient slots of one CTA are written by the
+// first work item that touches them and accumulated afterwards (fixed order).
+__device__ __forceinline__ void gstore(float* G, size_t i, float v, bool first) {
+  if (first)
+    G[i] = v;
+  else
+    G[i] += v;
+}
+
+// G[k*N + n] (+)= Σ_r X[r, k] · dY[r, n]   (weight gradient, nn.py:30-34)
+__device__ __forceinline__ void wgrad_rows(const float* X, int ldx, const float* dY, int ldy,
+                                           int R, int K, int N, float* G, bool first) {
+  for (int e = threadIdx.x; e < K * N; e += blockDim.x) {
+    const int k = e / N, n = e - k * N;
+    float acc = 0.f;
+    for (int r = 0; r < R; ++r) acc = fmaf(X[r * ldx + k], dY[r * ldy + n], acc);
+    gstore(G, e, acc, first);
+  }
+}
+
+// G[n] (+)= Σ_r dY[r, n] (· S[r, n] when S is given)   (bias / LN gains)
+__device__ __forceinline__ void colsum_rows(const float* dY, int ldy, int R, int N, float* G,
+                                            bool first, const float* S = nullptr, int lds = 0) {
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    float acc = 0.f;
+    for (int r = 0; r < R; ++r) acc += S ? dY[r * ldy + n] * S[r * lds + n] : dY[r * ldy + n];
+    gstore(G, n, acc, first);
+  }
+}
+
+// LayerNorm backward (nn.py:57-66): dX = inv (gx - mean(gx) - xhat mean(gx xhat)),
+// gx = dY ⊙ g.  One warp per row.
+__device__ __forceinline__ void layernorm_back_rows(const float* dY, int ldy, const float* Xh,
+                                                    int ldh, const float* inv, int R, int d,
+                                                    const float* __restrict__ g, float* dX,
+                                                    int ldx) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const float inv_d = 1.f / (float)d;
+  for (int r = w; r < R; r += nw) {
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = lane; c < d; c += 32) {
+      const float gx = dY[r * ldy + c] * __ldg(g + c);
+      s1 += gx;
+      s2 = fmaf(gx, Xh[r * ldh + c], s2);
+    }
+    const float m1 = warp_sum(s1) * inv_d, m2 = warp_sum(s2) * inv_d;
+    const float iv = inv[r];
+    for (int c = lane; c < d; c += 32) {
+      const float gx = dY[r * ldy + c] * __ldg(g + c);
+      dX[r * ldx + c] = iv * (gx - m1 - Xh[r * ldh + c] * m2);
+    }
+  }
+}
+
+// Y[r, c] = g[c] · Xh[r, c] + b[c]  (recompute an LN output from its cache)
+__device__ __forceinline__ void ln_apply_rows(const float* Xh, int ldh, int R, int d,
+                                              const float* __restrict__ g,
+                                              const float* __restrict__ b, float* Y, int ldy) {
+  for (int e = threadIdx.x; e < R * d; e += blockDim.x) {
+    const int r = e / d, c = e - r * d;
+    Y[r * ldy + c] = fmaf(__ldg(g + c), Xh[r * ldh + c], __ldg(b + c));
+  }
+}
+
+// Attention backward for A ASTs × H heads (nn.py:99-120) given the cached
+// probabilities P and dCtx: dP = dCtx Vᵀ, dV = Pᵀ dCtx,
+// dS = P ⊙ (dP − Σ_j dP P) · scale, dQ = dS K, dK = dSᵀ Q.
+// Uses S as scratch for dS (same layout as P).
+__device__ __forceinline__ void attention_back_rows(const float* Q, const float* K,
+                                                    const float* V, int ld, const float* P,
+                                                    const float* dC, int ldc, float* dQ,
+                                                    float* dK, float* dV, float* S, int A, int L,
+                                                    int H, int dh, float scale) {
+  // dS rows: one thread per (a, h, i)
+  for (int job = threadIdx.x; job < A * H * L; job += blockDim.x) {
+    const int i = job % L, h = (job / L) % H, a = job / (L * H);
+    const float* pp = P + ((a * H + h) * L + i) * L;
+    const float* dc = dC + (a * L + i) * ldc + h * dh;
+    float dp[TPCB_MAX_LEAF];
+    float dot = 0.f;
+#pragma unroll
+    for (int j = 0; j < TPCB_MAX_LEAF; ++j) {
+      if (j < L) {
+        const float* v = V + (a * L + j) * ld + h * dh;
+        float s = 0.f;
+        for (int c = 0; c < dh; ++c) s = fmaf(dc[c], v[c], s);
+        dp[j] = s;
+        dot = fmaf(s, pp[j], dot);
+      }
+    }
+    float* ss = S + ((a * H + h) * L + i) * L;
+#pragma unroll
+    for (int j = 0; j < TPCB_MAX_LEAF; ++j)
+      if (j < L) ss[j] = pp[j] * (dp[j] - dot) * scale;
+  }
+  __syncthreads();
+  // dQ[i] = Σ_j dS[i,j] K[j];  dK[j] = Σ_i dS[i,j] Q[i];  dV[j] = Σ_i P[i,j] dC[i]
+  for (int e = threadIdx.x; e < A * L * H * dh; e += blockDim.x) {
+    const int c = e % dh, h = (e / dh) % H, i = (e / (dh * H)) % L, a = e / (dh * H * L);
+    const float* sr = S + (a * H + h) * L * L;
+    const float* pr = P + (a * H + h) * L * L;
+    float q = 0.f, k = 0.f, v = 0.f;
+    for (int j = 0; j < L; ++j) {
+      const int rj = (a * L + j) * ld + h * dh + c;
+      q = fmaf(sr[i * L + j], K[rj], q);
+      k = fmaf(sr[j * L + i], Q[rj], k);
+      v = fmaf(pr[j * L + i], dC[(a * L + j) * ldc + h * dh + c], v);
+    }
+    const int ri = (a * L + i) * ld + h * dh + c;
+    dQ[ri] = q;
+    dK[ri] = k;
+    dV[ri] = v;
+  }
+}
+
 }  // namespace tpcb

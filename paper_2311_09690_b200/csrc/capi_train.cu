@@ -1,0 +1,181 @@
+// C ABI of the training path: single backward (costmodel.backward), the
+// optimizer (nn.Adam / nn.Sgd), and the native epoch loop (train/finetune
+// inner loops, costmodel.py:697-707 and :755-773).
+#include <vector>
+
+#include "common.cuh"
+#include "train.cuh"
+
+using namespace tpcb;
+
+namespace {
+
+SampleSetDev to_dev(const tpcb_samples* s) {
+  SampleSetDev d{};
+  if (s) {
+    d.x = s->x;
+    d.ast_row = s->ast_row;
+    d.n_leaf = s->n_leaf;
+    d.devfeat = s->devfeat;
+    d.y = s->y;
+  }
+  return d;
+}
+
+LossDev to_dev(const tpcb_loss* l, bool has_tgt) {
+  LossDev d{};
+  d.mode = l->mode;
+  d.original = l->original_space;
+  d.lambda = l->lambda_hybrid;
+  d.offset = l->offset;
+  d.alpha = l->alpha_cmd;
+  d.cmd_order = l->cmd_order;
+  d.use_cmd = (l->alpha_cmd > 0.0 && has_tgt) ? 1 : 0;
+  d.norm = l->norm;
+  return d;
+}
+
+TrainWs to_dev(const tpcb_train_ws* w) {
+  TrainWs d{};
+  d.partial = w->partial;
+  d.slot_stride = (size_t)w->slot_stride;
+  d.n_slots = w->n_slots;
+  d.touched = w->touched;
+  d.zall = w->zall;
+  d.terms = w->terms;
+  d.scalars = w->scalars;
+  return d;
+}
+
+OptDev to_dev(const tpcb_optim* o) {
+  OptDev d{};
+  if (o) {
+    d.kind = o->kind;
+    d.beta1 = o->beta1;
+    d.beta2 = o->beta2;
+    d.eps = o->eps;
+    d.weight_decay = o->weight_decay;
+  }
+  return d;
+}
+
+int check_loss(const tpcb_loss* l) {
+  if (!l) return TPCB_ERR_VALIDATION;
+  if (l->mode < 0 || l->mode > 2) return TPCB_ERR_VALIDATION;
+  if (l->cmd_order < 1) return TPCB_ERR_VALIDATION;
+  if (l->cmd_order > kMaxCmdOrder) return TPCB_ERR_UNSUPPORTED;
+  return TPCB_OK;
+}
+
+// one training step on an already uploaded step table
+int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
+             const SampleSetDev& src, const SampleSetDev& tgt, const int32_t* batch,
+             const int4* steps, int step, int grid, const LossDev& loss, const OptDev& opt,
+             const double* lr, const int64_t* t0, const TrainWs& ws, float* grad_out,
+             double* step_loss, double* step_cmd, float* pred_out, int32_t* status,
+             cudaStream_t stream) {
+  int st;
+  if (loss.use_cmd) {
+    st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 0, ws, nullptr,
+                      status, stream);
+    if (st) return st;
+  }
+  st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 1, ws, pred_out,
+                    status, stream);
+  if (st) return st;
+  st = launch_reduce_apply(m->dev, ws, steps, step, loss.use_cmd, grad_out, P, mb, vb, opt, lr, t0,
+                           loss, step_loss, step_cmd, stream);
+  if (st) return st;
+  if (opt.kind != kOptNone && PT) st = launch_transpose(m, P, PT, stream);
+  return st;
+}
+
+}  // namespace
+
+extern "C" int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t* n_slots,
+                                   int64_t* slot_stride, int64_t* zall_floats,
+                                   int64_t* terms_doubles) {
+  if (!m || max_rows < 1) return TPCB_ERR_VALIDATION;
+  const int slots = std::min<int32_t>(max_rows, 1024);
+  if (n_slots) *n_slots = slots;
+  // 64-float (256 B) aligned slots
+  if (slot_stride) *slot_stride = ((int64_t)m->dev.total + 63) / 64 * 64;
+  if (zall_floats) *zall_floats = (int64_t)max_rows * m->dev.d_e;
+  if (terms_doubles) *terms_doubles = (int64_t)max_rows * 2;
+  TrainPlan tp = make_train_plan(m->dev);
+  if ((size_t)tp.total * sizeof(float) > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
+  return TPCB_OK;
+}
+
+extern "C" int tpcb_transpose_params(const tpcb_model* m, const float* d_params, float* d_params_t,
+                                     void* stream) {
+  if (!m || !d_params || !d_params_t) return TPCB_ERR_VALIDATION;
+  return launch_transpose(m, d_params, d_params_t, (cudaStream_t)stream);
+}
+
+extern "C" int tpcb_loss_backward(const tpcb_model* m, const float* d_params,
+                                  const float* d_params_t, const tpcb_samples* src,
+                                  const tpcb_samples* tgt, const int32_t* d_batch, int32_t n_src,
+                                  int32_t n_tgt, const tpcb_loss* loss, const tpcb_train_ws* ws,
+                                  void* d_step_scratch_, float* d_grad, float* d_pred,
+                                  int32_t* d_status, void* stream_) {
+  int4* d_step_scratch = static_cast<int4*>(d_step_scratch_);
+  if (!m || !d_params || !d_params_t || !src || !ws || !d_batch || !d_step_scratch)
+    return TPCB_ERR_VALIDATION;
+  if (n_src < 1) return TPCB_ERR_EMPTY_BATCH;
+  int st = check_loss(loss);
+  if (st) return st;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const LossDev ld = to_dev(loss, tgt != nullptr && n_tgt > 0);
+  if (ld.use_cmd && !tgt) return TPCB_ERR_VALIDATION;
+  const int n_all = n_src + (ld.use_cmd ? n_tgt : 0);
+  int4 h{0, n_src, ld.use_cmd ? n_tgt : 0, 0};
+  TPCB_CUDA_CHECK(cudaMemcpyAsync(d_step_scratch, &h, sizeof(int4), cudaMemcpyHostToDevice, stream));
+  OptDev none{};
+  TrainWs w = to_dev(ws);
+  return run_step(m, const_cast<float*>(d_params), const_cast<float*>(d_params_t), nullptr, nullptr,
+                  to_dev(src), to_dev(tgt), d_batch, d_step_scratch, 0, n_all, ld, none, nullptr,
+                  nullptr, w, d_grad, ws->scalars + 1, nullptr, d_pred, d_status, stream);
+}
+
+extern "C" int tpcb_optimizer_step(const tpcb_model* m, int64_t n, float* d_params,
+                                   float* d_params_t, const float* d_grad, float* d_m, float* d_v,
+                                   const tpcb_optim* opt, double lr, int64_t t, void* stream_) {
+  if (!d_params || !d_grad || !opt || t < 1) return TPCB_ERR_VALIDATION;
+  if (opt->kind == kOptAdam && (!d_m || !d_v)) return TPCB_ERR_VALIDATION;
+  if (d_params_t && !m) return TPCB_ERR_VALIDATION;
+  if (m) n = m->dev.total;
+  if (n < 0 || n > 0x7fffffff) return TPCB_ERR_VALIDATION;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  int st = launch_optimizer((int)n, d_grad, d_params, d_m, d_v, to_dev(opt), lr, (double)t,
+                            stream);
+  if (st) return st;
+  if (d_params_t) st = launch_transpose(m, d_params, d_params_t, stream);
+  return st;
+}
+
+extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_params_t,
+                                float* d_m, float* d_v, const tpcb_samples* src,
+                                const tpcb_samples* tgt, const tpcb_plan* plan,
+                                const tpcb_loss* loss, const tpcb_optim* opt, const double* d_lr,
+                                const int64_t* d_t0, const tpcb_train_ws* ws,
+                                double* d_step_loss, double* d_step_cmd, int32_t* d_status,
+                                void* stream_) {
+  if (!m || !d_params || !d_params_t || !src || !plan || !opt || !ws) return TPCB_ERR_VALIDATION;
+  int st = check_loss(loss);
+  if (st) return st;
+  if (plan->n_steps < 0) return TPCB_ERR_VALIDATION;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const LossDev ld = to_dev(loss, tgt != nullptr);
+  const OptDev od = to_dev(opt);
+  const TrainWs w = to_dev(ws);
+  const SampleSetDev s = to_dev(src), t = to_dev(tgt);
+  const int4* steps = reinterpret_cast<const int4*>(plan->d_steps);
+  for (int k = 0; k < plan->n_steps; ++k) {
+    st = run_step(m, d_params, d_params_t, d_m, d_v, s, t, plan->d_batch, steps, k, ws->n_slots,
+                  ld, od, d_lr, d_t0, w, nullptr, d_step_loss, d_step_cmd, nullptr, d_status,
+                  stream);
+    if (st) return st;
+  }
+  return TPCB_OK;
+}

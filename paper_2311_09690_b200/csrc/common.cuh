@@ -36,6 +36,13 @@ struct Model {
   int tail_lo;               // devhW .. total
 };
 
+// 2-D tensors of the flat parameter vector (for the transposed copy)
+constexpr int kMaxT2 = 160;
+struct T2Table {
+  int n;
+  int off[kMaxT2], rows[kMaxT2], cols[kMaxT2], cum[kMaxT2 + 1];
+};
+
 struct TensorInfo {
   std::string name;
   int64_t offset;
@@ -47,6 +54,7 @@ struct TensorInfo {
 struct tpcb_model {
   tpcb_config cfg;
   tpcb::Model dev;
+  tpcb::T2Table t2;
   std::vector<tpcb::TensorInfo> tensors;
 };
 

@@ -120,6 +120,20 @@ extern "C" int tpcb_model_create(const tpcb_config* c, tpcb_model** out) {
     return TPCB_ERR_UNSUPPORTED;
   }
   M.total = (int)off;
+  m->t2.n = 0;
+  m->t2.cum[0] = 0;
+  for (const TensorInfo& t : m->tensors) {
+    if (t.cols == 0) continue;
+    if (m->t2.n >= tpcb::kMaxT2) {
+      delete m;
+      return TPCB_ERR_UNSUPPORTED;
+    }
+    const int i = m->t2.n++;
+    m->t2.off[i] = (int)t.offset;
+    m->t2.rows[i] = t.rows;
+    m->t2.cols[i] = t.cols;
+    m->t2.cum[i + 1] = m->t2.cum[i] + t.rows * t.cols;
+  }
   M.shared_lo = M.inW;
   M.shared_hi = M.leafW[1];
   M.tail_lo = M.devhW;

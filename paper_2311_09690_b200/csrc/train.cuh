@@ -1,0 +1,73 @@
+// Shared declarations of the training-step kernels (train.cu, optim.cu, capi).
+#pragma once
+
+#include "common.cuh"
+
+namespace tpcb {
+
+constexpr int kMaxCmdOrder = 8;
+constexpr double kCmdSupportFloor = 1e-6;  // costmodel.py:29
+enum { kLossHybrid = 0, kLossMse = 1, kLossMape = 2 };
+enum { kOptNone = 0, kOptAdam = 1, kOptSgd = 2 };
+
+struct OptDev {
+  int kind;
+  double beta1, beta2, eps, weight_decay;
+};
+
+// shared-memory plan of one training CTA (one sample of ≤ n_leaf_max rows)
+struct TrainPlan {
+  int R, ld, ldf;
+  int oQ, oK, oV, oC, oX1, oX2, oF, oI1, oI2, oP, layer_stride, layer_base;
+  int X0, H0, Hout, T1, T2, dH, dA, dB, dQ, dK, dV, dF, S;
+  int uw, dv, zx, zv, zp, u, du0, du1, dzx, dzp, dzv, dflat, misc;
+  int cmd, cmd_cols;
+  int total;  // floats
+};
+
+TrainPlan make_train_plan(const Model& M);
+
+// one dataset on the device (packed rows from K1 + per-sample data)
+struct SampleSetDev {
+  const float* x;          // packed rows [*, 32]
+  const int32_t* ast_row;  // first packed row of each sample
+  const int32_t* n_leaf;   // leaf count of each sample
+  const float* devfeat;    // [n, 6]
+  const double* y;         // model-space targets (source only)
+};
+
+struct LossDev {
+  int mode;      // kLoss*
+  int original;  // relative term in original (decoded) space
+  double lambda, offset, alpha;
+  int cmd_order;
+  int use_cmd;
+  tpcb_boxcox norm;
+};
+
+struct TrainWs {
+  float* partial;      // [n_slots][slot_stride]
+  size_t slot_stride;  // >= param count
+  int n_slots;
+  uint32_t* touched;   // [n_slots] region bitmask (bit 0 shared, bit L leaf_embed.L)
+  float* zall;         // [max rows][d_embed]
+  double* terms;       // [max src][2] per-sample (sq, rel)
+  double* scalars;     // [8] cmd value, loss value, ...
+};
+
+// steps[s] = {offset of step s in batch, n_src, n_tgt, 0}; batch holds the
+// source sample indices of the step followed by its target sample indices.
+int launch_train(const Model& M, const float* P, const float* PT, const SampleSetDev& src,
+                 const SampleSetDev& tgt, const int32_t* batch, const int4* steps, int step,
+                 int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
+                 int32_t* status, cudaStream_t stream);
+int launch_reduce_apply(const Model& M, const TrainWs& ws, const int4* steps, int step, int use_cmd,
+                        float* grad_out, float* P, float* m, float* v, const OptDev& opt,
+                        const double* lr, const int64_t* t, const LossDev& loss, double* step_loss,
+                        double* step_cmd, cudaStream_t stream);
+int launch_transpose(const tpcb_model* m, const float* P, float* PT, cudaStream_t stream);
+int launch_optimizer(int n, const float* grad, float* P, float* m, float* v, const OptDev& opt,
+                     double lr, double t, cudaStream_t stream);
+
+
+}  // namespace tpcb

@@ -245,3 +245,113 @@ def positional_encoding_device(ordering: np.ndarray, theta: float) -> np.ndarray
                                             den.ctypes.data_as(C.c_void_p), out.data_ptr(),
                                             stream_ptr()), "positional_encoding")
     return out.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# training
+# ---------------------------------------------------------------------------
+
+LOSS_MODES = {"hybrid": 0, "mse": 1, "mape": 2}
+OPT_KINDS = {None: 0, "adam": 1, "sgd": 2}
+
+
+class DeviceSamples:
+    """A dataset resident on the device: K1-packed rows + per-sample data
+    (tpcb_samples).  Built once per training run / backward call."""
+
+    def __init__(self, rag: RaggedHost, n_leaf_max: int, status: Status, y=None, R: int = 64,
+                 device="cuda", theta: float = THETA_DEFAULT):
+        rows, ordering, leaf_off, devfeat = upload_ragged(rag, device)
+        self.pk = pack(rows, ordering, leaf_off, rag.n_ast, n_leaf_max, rag.encoded, status, R,
+                       theta)
+        self.n = rag.n_ast
+        self.n_leaf_host = np.asarray(rag.n_leaf, dtype=np.int64)
+        self.n_leaf = torch.from_numpy(self.n_leaf_host.astype(np.int32)).to(device)
+        self.devfeat = devfeat
+        self.y = None
+        if y is not None:
+            self.y = torch.from_numpy(np.ascontiguousarray(y, dtype=np.float64)).to(device)
+        s = _lib.Samples()
+        s.x, s.ast_row = self.pk.x.data_ptr(), self.pk.ast_row.data_ptr()
+        s.n_leaf, s.devfeat = self.n_leaf.data_ptr(), devfeat.data_ptr()
+        s.y = self.y.data_ptr() if self.y is not None else None
+        self.struct = s
+
+    def set_targets(self, y):
+        self.y = torch.from_numpy(np.ascontiguousarray(y, dtype=np.float64)).to(self.devfeat.device)
+        self.struct.y = self.y.data_ptr()
+
+
+class TrainWorkspace:
+    def __init__(self, dm: DeviceModel, max_rows: int, device="cuda"):
+        lib = _lib.load()
+        ns, stride, zf, tf = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
+        _lib.check(lib.tpcb_train_ws_sizes(dm.handle, max_rows, C.byref(ns), C.byref(stride),
+                                           C.byref(zf), C.byref(tf)), "train_ws_sizes")
+        self.max_rows = max_rows
+        self.partial = torch.empty(ns.value * stride.value, dtype=torch.float32, device=device)
+        self.touched = torch.zeros(ns.value, dtype=torch.int32, device=device)
+        self.zall = torch.empty(max(zf.value, 1), dtype=torch.float32, device=device)
+        self.terms = torch.zeros(max(tf.value, 2), dtype=torch.float64, device=device)
+        self.scalars = torch.zeros(8, dtype=torch.float64, device=device)
+        self.step_scratch = torch.zeros(4, dtype=torch.int32, device=device)
+        w = _lib.TrainWs()
+        w.partial, w.slot_stride, w.n_slots = self.partial.data_ptr(), stride.value, ns.value
+        w.touched, w.zall = self.touched.data_ptr(), self.zall.data_ptr()
+        w.terms, w.scalars = self.terms.data_ptr(), self.scalars.data_ptr()
+        self.struct = w
+
+
+def loss_struct(mode="hybrid", lambda_hybrid=1e-3, offset=0.0, alpha_cmd=0.0, cmd_order=5,
+                mape_space="transformed", normalizer=None) -> _lib.LossCfg:
+    c = _lib.LossCfg()
+    c.mode = LOSS_MODES[mode]
+    c.original_space = 1 if mape_space == "original" else 0
+    c.lambda_hybrid, c.offset, c.alpha_cmd = float(lambda_hybrid), float(offset), float(alpha_cmd)
+    c.cmd_order = int(cmd_order)
+    c.norm = boxcox_struct(normalizer)
+    return c
+
+
+def optim_struct(kind, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0) -> _lib.OptimCfg:
+    o = _lib.OptimCfg()
+    o.kind = OPT_KINDS[kind]
+    o.beta1, o.beta2, o.eps, o.weight_decay = beta1, beta2, eps, float(weight_decay)
+    return o
+
+
+def transpose_params(dm: DeviceModel, params: torch.Tensor, params_t: torch.Tensor) -> None:
+    _lib.check(_lib.load().tpcb_transpose_params(dm.handle, params.data_ptr(),
+                                                 params_t.data_ptr(), stream_ptr()), "transpose")
+
+
+def run_backward(dm: DeviceModel, params: torch.Tensor, params_t: torch.Tensor,
+                 src: DeviceSamples, tgt: DeviceSamples | None, loss: _lib.LossCfg,
+                 ws: TrainWorkspace, status: Status):
+    """One costmodel.backward over all of src (and tgt when CMD is on).
+    Returns device (grad [P], pred [n_src]); loss/CMD values in ws.scalars."""
+    lib = _lib.load()
+    n_src = src.n
+    n_tgt = tgt.n if tgt is not None else 0
+    dev = params.device
+    batch = torch.cat([torch.arange(n_src, dtype=torch.int32, device=dev),
+                       torch.arange(n_tgt, dtype=torch.int32, device=dev)])
+    grad = torch.empty(dm.n_params, dtype=torch.float32, device=dev)
+    pred = torch.empty(n_src, dtype=torch.float32, device=dev)
+    _lib.check(lib.tpcb_loss_backward(dm.handle, params.data_ptr(), params_t.data_ptr(),
+                                      C.byref(src.struct),
+                                      C.byref(tgt.struct) if tgt is not None else None,
+                                      batch.data_ptr(), n_src, n_tgt, C.byref(loss),
+                                      C.byref(ws.struct), ws.step_scratch.data_ptr(),
+                                      grad.data_ptr(), pred.data_ptr(), status.ptr,
+                                      stream_ptr()), "loss_backward")
+    return grad, pred
+
+
+def optimizer_step(dm: DeviceModel | None, params, params_t, grad, m, v, opt: _lib.OptimCfg,
+                   lr: float, t: int) -> None:
+    """nn.Adam/Sgd step on the device; dm=None steps a bare flat vector."""
+    _lib.check(_lib.load().tpcb_optimizer_step(dm.handle if dm is not None else None,
+                                               params.numel(), params.data_ptr(), dptr(params_t),
+                                               grad.data_ptr(), dptr(m), dptr(v), C.byref(opt),
+                                               float(lr), int(t), stream_ptr()), "optimizer")
