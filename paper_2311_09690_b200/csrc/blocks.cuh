@@ -21,7 +21,7 @@ __device__ __forceinline__ void gemm_rows(const float* X, int ldx, const float* 
                                           int ldr = 0) {
   const int ncg = (N + TN - 1) / TN;
   const int nrg = (R + TM - 1) / TM;
-  const bool vec = (TN == 4) && ((N & 3) == 0);
+  const bool vec = (TN == 4) && ((N & 3) == 0) && ((reinterpret_cast<uintptr_t>(W) & 15) == 0);
   for (int job = threadIdx.x; job < ncg * nrg; job += blockDim.x) {
     const int cg = job % ncg, rg = job / ncg;
     const int c0 = cg * TN, r0 = rg * TM;

@@ -68,7 +68,10 @@ extern "C" int tpcb_model_create(const tpcb_config* c, tpcb_model** out) {
   for (int i = 0; i < c->n_dec; ++i) M.dec[i] = c->dec[i];
 
   int64_t off = 0;
+  // every tensor starts on a 16-byte boundary so the kernels can use 128-bit
+  // loads on any weight matrix (padding floats stay 0 through training)
   auto add = [&](const std::string& name, int rows, int cols) -> int {
+    off = (off + 3) & ~(int64_t)3;
     int at = (int)off;
     m->tensors.push_back(TensorInfo{name, off, rows, cols});
     off += (int64_t)rows * (cols ? cols : 1);
@@ -115,6 +118,7 @@ extern "C" int tpcb_model_create(const tpcb_config* c, tpcb_model** out) {
   }
   M.outW = add("dec.out.W", w, 1);
   M.outb = add("dec.out.b", 1, 0);
+  off = (off + 3) & ~(int64_t)3;
   if (off > (int64_t)0x7fffffff) {
     delete m;
     return TPCB_ERR_UNSUPPORTED;

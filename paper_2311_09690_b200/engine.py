@@ -289,7 +289,8 @@ class TrainWorkspace:
         _lib.check(lib.tpcb_train_ws_sizes(dm.handle, max_rows, C.byref(ns), C.byref(stride),
                                            C.byref(zf), C.byref(tf)), "train_ws_sizes")
         self.max_rows = max_rows
-        self.partial = torch.empty(ns.value * stride.value, dtype=torch.float32, device=device)
+        # zero-filled once: alignment padding between tensors is never written
+        self.partial = torch.zeros(ns.value * stride.value, dtype=torch.float32, device=device)
         self.touched = torch.zeros(ns.value, dtype=torch.int32, device=device)
         self.zall = torch.empty(max(zf.value, 1), dtype=torch.float32, device=device)
         self.terms = torch.zeros(max(tf.value, 2), dtype=torch.float64, device=device)
