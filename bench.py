@@ -1,0 +1,415 @@
+"""Benchmark: CDMPP predictor training throughput on B200 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (configs[1]): one training epoch over 262,144 synthetic compact ASTs
+(327,680 generated, 8:1:1 split — SURVEY §8d C2), desk model
+(init_params(desk_config(seed=0)), 354,577 parameters), batch size 64
+(the reference's), hybrid loss, Adam, fp32 accumulate.  A bench "step" is one
+epoch (≈4,096 optimizer steps).  Synthetic data: `synth.generate`, the
+reference's generative model drawn with vectorised numpy (data="synthetic").
+
+Printed JSON line (rank 0):
+  value      training samples/s, device time of the timed epochs (CUDA events
+             on the training stream, L2 flushed between epochs, max over ranks)
+  e2e        the same metric through the public API per epoch: pinned-host
+             H2D of the training set → K1 pack → plan upload → epoch →
+             validation → D2H of per-step losses + metrics
+  roofline   dominant kernel (train_kernel, fused fwd+bwd) from an uncaptured
+             profiled epoch: algorithmic FLOPs / device time
+  cpu_baseline  the oracle restatement of the reference step (float64 numpy)
+             on this host, single thread, bounded sample
+  extra      inference ASTs/s on the C1 (4,096) and 1M-AST batches
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_GEN = 327_680
+METRIC = "predictor training samples/sec (train epoch, 256K synthetic ASTs)"
+
+
+def desk_fwd_flops(L):
+    """Algorithmic forward FLOPs/AST for the desk config:
+    138,240·L + 512·L² + 13,664."""
+    L = np.asarray(L, dtype=np.float64)
+    return 138_240.0 * L + 512.0 * L * L + 13_664.0
+
+
+# --------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- helpers
+
+def dist_setup(n_gpus: int):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def make_data():
+    from paper_2311_09690_b200 import synth
+    data = synth.generate(N_GEN, seed=0)
+    tr, va, _ = synth.split(N_GEN, seed=0)
+    return data, data.take(np.sort(tr)), data.take(np.sort(va))
+
+
+def rag_of(s, device_feat):
+    from paper_2311_09690_b200 import engine
+    dev = np.tile(device_feat.astype(np.float32), (s.n, 1))
+    return engine.RaggedHost(rows=s.vectors.astype(np.float32), ordering=s.ordering,
+                             n_leaf=s.n_leaf, devfeat=dev, encoded=False)
+
+
+# --------------------------------------------------------------- CPU baseline
+
+def cpu_baseline(train, device_feat, offset, norm, budget_s: float = 12.0, batch: int = 64):
+    """Oracle restatement of the reference train step (float64 numpy), single
+    thread, bounded sample: as many bs-64 steps of the planned epoch as fit in
+    `budget_s`."""
+    from threadpoolctl import threadpool_limits
+    from oracle import featurize as of
+    from oracle import predictor as op
+    from oracle import trainer as ot
+    import paper_2311_09690_b200 as pb
+    from paper_2311_09690_b200.training import epoch_batches
+    cfg = pb.desk_config(seed=0)
+    T = {k: v.copy() for k, v in pb.init_params(cfg).tensors.items()}
+    dm = op.Dims(cfg.d_model, cfg.n_layers, cfg.n_heads, cfg.d_ff, cfg.d_embed, cfg.d_device,
+                 tuple(cfg.decoder_dims), cfg.n_leaf_max)
+    off = train.offsets()
+    y = norm.encode(train.latency)
+    batches = epoch_batches(np.random.default_rng(0), train.n_leaf, batch)
+    opt = ot.AdamState(T)
+    n_done, t_used, steps = 0, 0.0, 0
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        for b in batches:
+            L = int(train.n_leaf[b[0]])
+            x = np.stack([of.encode_rows(train.vectors[off[i]:off[i] + L],
+                                         train.ordering[off[i]:off[i] + L]) for i in b])
+            dev = np.tile(device_feat, (len(b), 1))
+            ot.train_step(T, dm, x, dev, y[b], opt, 1e-3, offset)
+            n_done += len(b)
+            steps += 1
+            t_used = time.perf_counter() - t0
+            if t_used >= budget_s and steps >= 8:
+                break
+    return {"value": n_done / t_used, "unit": "samples/s", "cores": 1, "kind": "port",
+            "sample": f"{steps} reference train steps (bs {batch}, encode+backward+Adam, "
+                      f"{n_done} samples, {t_used:.1f} s) of the same epoch plan, float64 "
+                      f"numpy oracle, 1 thread"}
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference algorithm (oracle port, float64) on the
+    host cores; each step = a bounded sample of the epoch."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2311_09690_b200 as pb
+    data, train, valid = make_data()
+    from paper_2311_09690_b200.dataset import fit_boxcox
+    norm = fit_boxcox(train.latency)
+    dv = pb.device_vector(pb.DeviceSpec("synth0", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0))
+    for _ in range(args.warmup):
+        cpu_baseline(train, dv, norm.loss_offset, norm, budget_s=1.0)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(train, dv, norm.loss_offset, norm, budget_s=6.0))
+    elapsed = time.perf_counter() - t0
+    v = float(np.mean([r["value"] for r in vals]))
+    line = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed * 1e3 / max(args.steps, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "train epoch, 262,144 synthetic ASTs, desk model, bs 64",
+                       "model": "desk (354,577 params)", "global_batch": 64, "seq_len": "1..6 leaves",
+                       "parallelism": "host, 1 thread"},
+            "cpu_baseline": {**vals[-1], "value": v},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+    import paper_2311_09690_b200 as pb
+    from paper_2311_09690_b200 import _lib, engine
+    from paper_2311_09690_b200.dataset import fit_boxcox
+    from paper_2311_09690_b200.training import Trainer, epoch_batches
+
+    world, rank, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    lib = _lib.load()
+    cfg = pb.desk_config(seed=0, batch_size=args.batch_size)
+    data, train, valid = make_data()
+    norm = fit_boxcox(train.latency)
+    targets = norm.encode(train.latency)
+    dspec = pb.DeviceSpec("synth0", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0)
+    dv = pb.device_vector(dspec)
+    if world > 1:  # weak scaling: every rank trains on its own shard at bs 64
+        sel = np.arange(train.n)[rank::world]
+        train = train.take(sel)
+        targets = targets[sel]
+    params = pb.init_params(cfg)
+    loss = engine.loss_struct("hybrid", cfg.lambda_hybrid, norm.loss_offset, 0.0, 5,
+                              "transformed", norm)
+    tr = Trainer(cfg, params.tensors, rag_of(train, dv), targets, loss, rag_of(valid, dv),
+                 valid.latency, norm, device=dev)
+    rng = np.random.default_rng(cfg.seed)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def flush_l2():
+        with torch.cuda.stream(tr.stream):
+            _lib.check(lib.tpcb_flush_l2(flush.data_ptr(), flush.numel(), engine.stream_ptr()),
+                       "flush")
+
+    # warm-up epochs (first one captures the epoch graph)
+    for w in range(max(args.warmup, 1)):
+        flat, steps = tr.plan(rng)
+        n = tr.run_epoch(cfg.lr, flat, steps)
+        tr.evaluate_async()
+        tr.collect(n, w)
+    plans = [tr.plan(rng) for _ in range(args.steps)]
+    n_steps = plans[0][1].shape[0]
+    # timed: K epochs, device time per epoch, L2 flushed in between
+    barrier(world)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for k, (flat, steps) in enumerate(plans):
+            flush_l2()
+            with torch.cuda.stream(tr.stream):
+                ev[k][0].record()
+            tr.run_epoch(cfg.lr, flat, steps)
+            with torch.cuda.stream(tr.stream):
+                ev[k][1].record()
+        tr.stream.synchronize()
+    barrier(world)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    ms = max_over_ranks(ms, world)
+    tr.collect(n_steps, 0)
+    samples = train.n * args.steps * world
+    value = samples / (ms / 1e3)
+
+    # ------------------------------------------------ e2e through the public API
+    # per epoch: pinned-host H2D of the training set + K1 pack, plan upload,
+    # epoch, validation, D2H of losses and metrics
+    pinned = {
+        "rows": torch.from_numpy(train.vectors.astype(np.float32)).pin_memory(),
+        "ordering": torch.from_numpy(train.ordering.astype(np.int32)).pin_memory(),
+        "leaf_off": torch.from_numpy(train.offsets()).pin_memory(),
+        "y": torch.from_numpy(np.asarray(targets, dtype=np.float64)).pin_memory(),
+    }
+    h2d = sum(t.numel() * t.element_size() for t in pinned.values())
+    e2e_k = max(1, min(args.steps, 3))
+    barrier(world)
+    t0 = time.perf_counter()
+    for k in range(e2e_k):
+        with torch.cuda.stream(tr.stream):
+            rows_d = pinned["rows"].to(dev, non_blocking=True)
+            ord_d = pinned["ordering"].to(dev, non_blocking=True)
+            off_d = pinned["leaf_off"].to(dev, non_blocking=True)
+            tr.src.y.copy_(pinned["y"], non_blocking=True)
+            engine.pack(rows_d, ord_d, off_d, train.n, cfg.n_leaf_max, False, tr.status,
+                        out=tr.src.pk)
+        flat, steps = plans[k % len(plans)]
+        n = tr.run_epoch(cfg.lr, flat, steps)
+        tr.evaluate_async()
+        losses, _, met = tr.collect(n, k)
+    barrier(world)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    d2h = n_steps * 8 + 3 * 8 + 4
+    plan_bytes = plans[0][0].nbytes + plans[0][1].nbytes
+    e2e = {"value": train.n * e2e_k * world / e2e_s, "unit": "samples/s",
+           "h2d_bytes_per_step": int(h2d + plan_bytes), "d2h_bytes_per_step": int(d2h),
+           "steps": e2e_k, "includes": "H2D of training set + K1 + epoch + validation"}
+
+    # --------------------------------------- roofline of the dominant kernel
+    prof = np.zeros(3)
+    flat, steps = plans[0]
+    tr.run_epoch(cfg.lr, flat, steps, profile=prof)
+    tr.collect(n_steps, 0)
+    launches = n_steps
+    flops_epoch = 3.0 * float(desk_fwd_flops(train.n_leaf).sum())
+    avg_ms = prof[0] / launches
+    achieved = flops_epoch / launches / (avg_ms / 1e3) / 1e12
+    import ctypes as C
+    scratch = torch.empty(4096, dtype=torch.float32, device=dev)
+    tf = C.c_double()
+    _lib.check(lib.tpcb_probe_ffma(scratch.data_ptr(), C.byref(tf), engine.stream_ptr()), "probe")
+    ffma = tf.value
+    peaks = {}
+    pk_path = ROOT / "MEASURED_PEAKS.json"
+    if pk_path.exists():
+        peaks = json.loads(pk_path.read_text())
+    bf16 = peaks.get("bf16_tflops", 1590.0)
+    roofline = {"bound": "tensor", "kernel": "train_kernel (fused fwd+bwd per sample)",
+                "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                "frac": achieved / bf16, "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else
+                               "fallback 1.59 PFLOP/s",
+                "fp32_ffma_peak_measured": ffma, "frac_of_fp32_ffma": achieved / ffma,
+                "share_of_step": prof[0] / prof.sum(),
+                "per_launch": {"flops": flops_epoch / launches, "avg_ms": avg_ms},
+                "other_kernels_ms_per_epoch": {"reduce_adam": prof[1], "transpose": prof[2]}}
+
+    # ----------------------------------------------- inference (extra keys)
+    infer = {}
+    if rank == 0:
+        p = pb.Predictor(params)
+        for n in (4096, 1 << 20):
+            sub = data.take(np.arange(n) % data.n)
+            rows, ordering, leaf_off, devfeat = engine.upload_ragged(rag_of(sub, dv), dev)
+            for _ in range(3):
+                p.forward_device(rows, ordering, leaf_off, devfeat, n, False, norm, latents=False)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = 20 if n <= 4096 else 5
+            a.record()
+            for _ in range(reps):
+                p.forward_device(rows, ordering, leaf_off, devfeat, n, False, norm, latents=False)
+            b.record()
+            torch.cuda.synchronize()
+            infer[f"infer_asts_per_s_{n}"] = n * reps / (a.elapsed_time(b) / 1e3)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(train, dv, norm.loss_offset, norm)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": "train epoch, 262,144 synthetic ASTs (configs[1])",
+                           "model": "desk_config (354,577 params), init seed 0",
+                           "global_batch": args.batch_size * world, "seq_len": "1..6 leaves",
+                           "parallelism": f"dp{world}" if world > 1 else "single GPU",
+                           "optimizer_steps_per_epoch": int(n_steps),
+                           "l2": "flushed (256 MiB write) between timed epochs"},
+                "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+                "gpu_launches": int(args.steps * n_steps * 3),
+                "clocks": clk.summary(), "extra": infer,
+                "final_val_mape": float(met[0]), "final_train_loss": float(np.mean(losses))}
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch-size", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

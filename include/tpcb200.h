@@ -137,6 +137,9 @@ int tpcb_forward(const tpcb_model* m, const float* d_params, const tpcb_packed* 
                  float* d_pred, float* d_zx, float* d_zv, float* d_z, double* d_latency,
                  int32_t* d_status, void* stream);
 
+/* costmodel.metrics (costmodel.py:577-591): d_out = {MAPE, RMSE, MSPE} (fp64) */
+int tpcb_metrics(const double* d_pred, const double* d_y, int64_t n, double* d_out, void* stream);
+
 /* ---- K4–K7: training ------------------------------------------------------
  * Loss selection (costmodel.LossSpec, costmodel.py:511-526). */
 typedef struct {
@@ -200,21 +203,37 @@ int tpcb_loss_backward(const tpcb_model* m, const float* d_params, const float* 
 int tpcb_optimizer_step(const tpcb_model* m, int64_t n, float* d_params, float* d_params_t,
                         const float* d_grad, float* d_m, float* d_v, const tpcb_optim* opt,
                         double lr, int64_t t, void* stream);
+/* captured-epoch cache (a CUDA graph replayed while the arguments match) */
+typedef struct tpcb_graph tpcb_graph;
+int tpcb_graph_create(tpcb_graph** out);
+void tpcb_graph_destroy(tpcb_graph* g);
+
 /* the train/finetune inner loop (costmodel.py:700-706, 759-773) for one
  * epoch: per step backward (+CMD) → reduce → optimizer → transpose.
  * lr and the step count before the epoch are read from device memory;
- * per-step loss / CMD values land in d_step_loss / d_step_cmd. */
+ * per-step loss / CMD values land in d_step_loss / d_step_cmd.  With a
+ * graph handle the whole epoch is captured once and replayed (the stream
+ * must then be a non-legacy stream).  prof_ms (host, [3], nullable) runs the
+ * epoch uncaptured and returns the summed device time of the fwd/bwd kernels,
+ * the reduce+optimizer kernels and the transpose kernels (synchronises). */
 int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_params_t, float* d_m,
                      float* d_v, const tpcb_samples* src, const tpcb_samples* tgt,
                      const tpcb_plan* plan, const tpcb_loss* loss, const tpcb_optim* opt,
                      const double* d_lr, const int64_t* d_t0, const tpcb_train_ws* ws,
-                     double* d_step_loss, double* d_step_cmd, int32_t* d_status, void* stream);
+                     double* d_step_loss, double* d_step_cmd, int32_t* d_status,
+                     tpcb_graph* graph, double* prof_ms, void* stream);
 
 /* ---- K6: CMD between two sets (costmodel.cmd, costmodel.py:489-503) ------
  * d_z = [zs; zt] row-major [(ns+nt), de] (f32 or f64); value → d_value[0];
  * when d_grad != NULL, dCMD/dz for every row (fp64, same layout). */
 int tpcb_cmd(const void* d_z, int32_t z_is_f64, int64_t ns, int64_t nt, int32_t de, int32_t k,
              double* d_value, double* d_grad, void* stream);
+
+/* ---- measurement helpers (bench.py) -------------------------------------
+ * FP32 FFMA throughput of this GPU in TFLOP/s (d_scratch: >= 1184 floats);
+ * L2 flush by overwriting a caller buffer larger than L2. */
+int tpcb_probe_ffma(float* d_scratch, double* tflops_out, void* stream);
+int tpcb_flush_l2(void* d_buf, size_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -10,9 +10,11 @@ from .errors import TpcostError
 from .features import (CompactAst, CompactBatch, DeviceSpec, EncodedInput, device_vector,
                        encode_input, positional_encoding)
 from .dataset import BoxCoxNormalizer, Dataset, Sample, fit_boxcox, split_dataset
-from .costmodel import (CostModelConfig, CostModelParams, LatentBatch, Predictor, desk_config,
-                        encode_dataset, forward, full_reference_config, init_params,
-                        load_checkpoint, loss_pretrain, metrics, predict, predict_batch,
-                        save_checkpoint)
+from .costmodel import (CostModelConfig, CostModelParams, LatentBatch, LossSpec, Predictor,
+                        TrainResult, backward, cmd, cmd_between, desk_config, encode_dataset,
+                        finetune, forward, full_reference_config, init_params, load_checkpoint,
+                        loss_finetune, loss_pretrain, metrics, predict, predict_batch,
+                        save_checkpoint, train)
+from .nn import Adam, Sgd
 
 __version__ = "0.1.0"

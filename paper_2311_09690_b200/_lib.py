@@ -80,6 +80,7 @@ SIGNATURES = {
     "tpcb_positional_encoding": (i32, [vp, i64, vp, vp, vp]),
     "tpcb_forward": (i32, [vp, vp, C.POINTER(Packed), vp, i64, C.POINTER(BoxCox), vp, vp, vp,
                            vp, vp, vp, vp]),
+    "tpcb_metrics": (i32, [vp, vp, i64, vp, vp]),
     "tpcb_cmd": (i32, [vp, i32, i64, i64, i32, i32, vp, vp, vp]),
     "tpcb_train_ws_sizes": (i32, [vp, i32, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64),
                                   C.POINTER(i64)]),
@@ -91,7 +92,11 @@ SIGNATURES = {
                                   vp]),
     "tpcb_train_epoch": (i32, [vp, vp, vp, vp, vp, C.POINTER(Samples), C.POINTER(Samples),
                                C.POINTER(Plan), C.POINTER(LossCfg), C.POINTER(OptimCfg), vp, vp,
-                               C.POINTER(TrainWs), vp, vp, vp, vp]),
+                               C.POINTER(TrainWs), vp, vp, vp, vp, vp, vp]),
+    "tpcb_graph_create": (i32, [C.POINTER(vp)]),
+    "tpcb_probe_ffma": (i32, [vp, C.POINTER(f64), vp]),
+    "tpcb_flush_l2": (i32, [vp, sz, vp]),
+    "tpcb_graph_destroy": (None, [vp]),
 }
 
 STATUS_EXC = {

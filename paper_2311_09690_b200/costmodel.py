@@ -407,6 +407,13 @@ def backward(params: CostModelParams, batch: list, targets, loss: LossSpec,
 
 
 # ---------------------------------------------------------------------------
+# training loops (costmodel.py:598-780) — device resident, see training.py
+# ---------------------------------------------------------------------------
+
+from .training import EpochLog, TrainResult, Trainer, epoch_batches, finetune, lr_at, train  # noqa: E402,F401
+
+
+# ---------------------------------------------------------------------------
 # checkpoints (costmodel.py:902-956) — same file format
 # ---------------------------------------------------------------------------
 

@@ -1,12 +1,21 @@
 // C ABI of the training path: single backward (costmodel.backward), the
 // optimizer (nn.Adam / nn.Sgd), and the native epoch loop (train/finetune
 // inner loops, costmodel.py:697-707 and :755-773).
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
 #include "train.cuh"
 
 using namespace tpcb;
+
+// Captured epoch: every launch of one epoch recorded once and replayed; all
+// per-epoch inputs (plan contents, lr, step count) are read from device
+// memory, so the same graph serves every epoch of a training run.
+struct tpcb_graph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<uint8_t> key;
+};
 
 namespace {
 
@@ -67,6 +76,21 @@ int check_loss(const tpcb_loss* l) {
   return TPCB_OK;
 }
 
+// optional per-kernel-class timing of an uncaptured epoch (bench.py roofline)
+struct StepProfiler {
+  std::vector<cudaEvent_t> ev;  // pairs: (start, end), class = index % 3
+  int pos = 0;
+  void mark(cudaStream_t s) {
+    if (pos >= (int)ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    cudaEventRecord(ev[pos++], s);
+  }
+};
+thread_local StepProfiler* g_prof = nullptr;
+
 // one training step on an already uploaded step table
 int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
              const SampleSetDev& src, const SampleSetDev& tgt, const int32_t* batch,
@@ -75,6 +99,7 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
              double* step_loss, double* step_cmd, float* pred_out, int32_t* status,
              cudaStream_t stream) {
   int st;
+  if (g_prof) g_prof->mark(stream);
   if (loss.use_cmd) {
     st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 0, ws, nullptr,
                       status, stream);
@@ -83,10 +108,13 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
   st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 1, ws, pred_out,
                     status, stream);
   if (st) return st;
+  if (g_prof) g_prof->mark(stream);
   st = launch_reduce_apply(m->dev, ws, steps, step, loss.use_cmd, grad_out, P, mb, vb, opt, lr, t0,
                            loss, step_loss, step_cmd, stream);
   if (st) return st;
+  if (g_prof) g_prof->mark(stream);
   if (opt.kind != kOptNone && PT) st = launch_transpose(m, P, PT, stream);
+  if (g_prof) g_prof->mark(stream);
   return st;
 }
 
@@ -154,13 +182,35 @@ extern "C" int tpcb_optimizer_step(const tpcb_model* m, int64_t n, float* d_para
   return st;
 }
 
+extern "C" int tpcb_graph_create(tpcb_graph** out) {
+  if (!out) return TPCB_ERR_VALIDATION;
+  *out = new tpcb_graph();
+  return TPCB_OK;
+}
+
+extern "C" void tpcb_graph_destroy(tpcb_graph* g) {
+  if (!g) return;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  delete g;
+}
+
+namespace {
+
+template <typename T>
+void key_add(std::vector<uint8_t>& k, const T& v) {
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(&v);
+  k.insert(k.end(), p, p + sizeof(T));
+}
+
+}  // namespace
+
 extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_params_t,
                                 float* d_m, float* d_v, const tpcb_samples* src,
                                 const tpcb_samples* tgt, const tpcb_plan* plan,
                                 const tpcb_loss* loss, const tpcb_optim* opt, const double* d_lr,
                                 const int64_t* d_t0, const tpcb_train_ws* ws,
                                 double* d_step_loss, double* d_step_cmd, int32_t* d_status,
-                                void* stream_) {
+                                tpcb_graph* graph, double* prof_ms, void* stream_) {
   if (!m || !d_params || !d_params_t || !src || !plan || !opt || !ws) return TPCB_ERR_VALIDATION;
   int st = check_loss(loss);
   if (st) return st;
@@ -171,11 +221,79 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
   const TrainWs w = to_dev(ws);
   const SampleSetDev s = to_dev(src), t = to_dev(tgt);
   const int4* steps = reinterpret_cast<const int4*>(plan->d_steps);
-  for (int k = 0; k < plan->n_steps; ++k) {
-    st = run_step(m, d_params, d_params_t, d_m, d_v, s, t, plan->d_batch, steps, k, ws->n_slots,
-                  ld, od, d_lr, d_t0, w, nullptr, d_step_loss, d_step_cmd, nullptr, d_status,
-                  stream);
+  auto enqueue = [&]() -> int {
+    for (int k = 0; k < plan->n_steps; ++k) {
+      int r = run_step(m, d_params, d_params_t, d_m, d_v, s, t, plan->d_batch, steps, k,
+                       ws->n_slots, ld, od, d_lr, d_t0, w, nullptr, d_step_loss, d_step_cmd,
+                       nullptr, d_status, stream);
+      if (r) return r;
+    }
+    return TPCB_OK;
+  };
+  if (prof_ms) {  // uncaptured, timed per kernel class
+    StepProfiler prof;
+    g_prof = &prof;
+    st = enqueue();
+    g_prof = nullptr;
     if (st) return st;
+    TPCB_CUDA_CHECK(cudaStreamSynchronize(stream));
+    prof_ms[0] = prof_ms[1] = prof_ms[2] = 0.0;
+    for (int i = 0; i + 3 < prof.pos; i += 4) {
+      for (int c = 0; c < 3; ++c) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, prof.ev[i + c], prof.ev[i + c + 1]);
+        prof_ms[c] += ms;
+      }
+    }
+    for (cudaEvent_t e : prof.ev) cudaEventDestroy(e);
+    return TPCB_OK;
   }
+  if (!graph || plan->n_steps == 0) return enqueue();
+  std::vector<uint8_t> key;
+  key_add(key, m);
+  key_add(key, d_params);
+  key_add(key, d_params_t);
+  key_add(key, d_m);
+  key_add(key, d_v);
+  key_add(key, *src);
+  if (tgt) key_add(key, *tgt);
+  key_add(key, *plan);
+  key_add(key, *loss);
+  key_add(key, *opt);
+  key_add(key, d_lr);
+  key_add(key, d_t0);
+  key_add(key, *ws);
+  key_add(key, d_step_loss);
+  key_add(key, d_step_cmd);
+  key_add(key, d_status);
+  if (!graph->exec || graph->key != key) {
+    if (graph->exec) {
+      cudaGraphExecDestroy(graph->exec);
+      graph->exec = nullptr;
+    }
+    st = prepare_train_kernels(m->dev);  // function attributes are set outside capture
+    if (st) return st;
+    TPCB_CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    st = enqueue();
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(stream, &g);
+    if (st) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (e != cudaSuccess) {
+      set_last_error("cudaStreamEndCapture", e);
+      return TPCB_ERR_CUDA;
+    }
+    e = cudaGraphInstantiate(&graph->exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+      set_last_error("cudaGraphInstantiate", e);
+      graph->exec = nullptr;
+      return TPCB_ERR_CUDA;
+    }
+    graph->key = key;
+  }
+  TPCB_CUDA_CHECK(cudaGraphLaunch(graph->exec, stream));
   return TPCB_OK;
 }

@@ -188,9 +188,58 @@ __global__ void __launch_bounds__(256) forward_kernel(
   }
 }
 
+// MAPE / RMSE / MSPE of decoded predictions (costmodel.metrics,
+// costmodel.py:577-591) in fp64, fixed-order block reduction (1 CTA).
+__global__ void __launch_bounds__(1024) metrics_kernel(const double* __restrict__ pred,
+                                                       const double* __restrict__ y, int64_t n,
+                                                       double* __restrict__ out) {
+  __shared__ double red[3][32];
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = pred[i] - y[i];
+    const double r = d / y[i];
+    a += fabs(r);
+    b += d * d;
+    c += r * r;
+  }
+  a = warp_sum_d(a);
+  b = warp_sum_d(b);
+  c = warp_sum_d(c);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+    red[0][w] = a;
+    red[1][w] = b;
+    red[2][w] = c;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    a = lane < nw ? red[0][lane] : 0.0;
+    b = lane < nw ? red[1][lane] : 0.0;
+    c = lane < nw ? red[2][lane] : 0.0;
+    a = warp_sum_d(a);
+    b = warp_sum_d(b);
+    c = warp_sum_d(c);
+    if (lane == 0) {
+      out[0] = a / (double)n;
+      out[1] = sqrt(b / (double)n);
+      out[2] = c / (double)n;
+    }
+  }
+}
+
 }  // namespace tpcb
 
 using namespace tpcb;
+
+extern "C" int tpcb_metrics(const double* d_pred, const double* d_y, int64_t n, double* d_out,
+                            void* stream) {
+  if (!d_pred || !d_y || !d_out) return TPCB_ERR_VALIDATION;
+  if (n < 1) return TPCB_ERR_EMPTY_BATCH;
+  metrics_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(d_pred, d_y, n, d_out);
+  TPCB_LAUNCH_CHECK("metrics_kernel");
+  return TPCB_OK;
+}
 
 extern "C" int tpcb_forward(const tpcb_model* m, const float* d_params, const tpcb_packed* pk,
                             const float* d_devfeat, int64_t n_ast, const tpcb_boxcox* norm,

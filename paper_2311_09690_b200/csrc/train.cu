@@ -428,6 +428,19 @@ __global__ void __launch_bounds__(256) train_kernel(
 
 }  // namespace
 
+int prepare_train_kernels(const Model& M) {
+  TrainPlan tp = make_train_plan(M);
+  const size_t smem = (size_t)tp.total * sizeof(float);
+  if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
+  static size_t set_for = 0;
+  if (smem > set_for) {
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         227 * 1024));
+    set_for = 227 * 1024;
+  }
+  return TPCB_OK;
+}
+
 int launch_train(const Model& M, const float* P, const float* PT, const SampleSetDev& src,
                  const SampleSetDev& tgt, const int32_t* batch, const int4* steps, int step,
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
@@ -436,8 +449,8 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
   const size_t smem = (size_t)tp.total * sizeof(float);
   if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
   if (loss.cmd_order > kMaxCmdOrder) return TPCB_ERR_UNSUPPORTED;
-  TPCB_CUDA_CHECK(
-      cudaFuncSetAttribute(train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int st = prepare_train_kernels(M);
+  if (st) return st;
   grid = std::max(1, std::min(grid, ws.n_slots));
   train_kernel<<<grid, 256, smem, stream>>>(M, P, PT, src, tgt, batch, steps, step, loss, phase,
                                             tp, ws.zall, ws.partial, ws.slot_stride, ws.touched,

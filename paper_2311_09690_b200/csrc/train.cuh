@@ -61,6 +61,7 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
                  const SampleSetDev& tgt, const int32_t* batch, const int4* steps, int step,
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                  int32_t* status, cudaStream_t stream);
+int prepare_train_kernels(const Model& M);
 int launch_reduce_apply(const Model& M, const TrainWs& ws, const int4* steps, int step, int use_cmd,
                         float* grad_out, float* P, float* m, float* v, const OptDev& opt,
                         const double* lr, const int64_t* t, const LossDev& loss, double* step_loss,

@@ -188,11 +188,15 @@ def upload_ragged(rag: RaggedHost, device="cuda"):
 
 def pack(rows: torch.Tensor, ordering: torch.Tensor, leaf_off: torch.Tensor, n_ast: int,
          n_leaf_max: int, encoded: bool, status: Status, R: int = 64,
-         theta: float = THETA_DEFAULT) -> PackedBatch:
-    """Run K1 on device-resident ragged rows."""
+         theta: float = THETA_DEFAULT, out: PackedBatch | None = None) -> PackedBatch:
+    """Run K1 on device-resident ragged rows (into `out` when given: same
+    buffers, so captured graphs that read them stay valid)."""
     lib = _lib.load()
     n_tok = int(rows.shape[0])
-    pk = PackedBatch(n_ast, n_tok, n_leaf_max, R, rows.device)
+    if out is not None and (out.n_ast, out.n_tok, out.n_leaf_max) == (n_ast, n_tok, n_leaf_max):
+        pk, R = out, out.R
+    else:
+        pk = PackedBatch(n_ast, n_tok, n_leaf_max, R, rows.device)
     den = None if encoded else pe_denominators(theta)
     den_p = None if den is None else den.ctypes.data_as(C.c_void_p)
     is64 = 1 if rows.dtype == torch.float64 else 0

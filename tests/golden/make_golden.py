@@ -211,6 +211,16 @@ def main():
                         split=np.array([{"train": 0, "valid": 1, "test": 2}[
                             sp.splits[s.id]] for s in ds4k.samples]))
 
+    # batch planning: the reference's own _epoch_batches on the C1 train split
+    tr_nleaf = [s.compact.n_leaf for s in sp.subset("train")]
+    prng = np.random.default_rng(0)
+    plan = {}
+    for ep in range(2):
+        bl = cm._epoch_batches(prng, tr_nleaf, 64)
+        plan[f"ep{ep}.flat"] = np.concatenate(bl)
+        plan[f"ep{ep}.len"] = np.array([len(b) for b in bl])
+    np.savez_compressed(OUT / "plan.npz", n_leaf=np.array(tr_nleaf), **plan)
+
     # ---------------------------------------------------------------- CMD
     out = {}
     crng = np.random.default_rng(2)

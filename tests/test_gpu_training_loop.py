@@ -1,0 +1,99 @@
+"""GPU training / fine-tuning loops (costmodel.train / finetune) against the
+reference's recorded 10-epoch desk run, plus the reference's determinism and
+edge-case contracts.
+
+Tolerance: the reference trains in float64, this path in fp32 with the same
+batches (identical host RNG plan), so the epoch losses track the reference
+run closely: per-epoch mean training loss within 2 % relative for the 10
+epochs, best epoch identical."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _pb():
+    import paper_2311_09690_b200 as pb
+    return pb
+
+
+def c1_dataset():
+    pb = _pb()
+    g = load_golden("c1_4096")
+    off = np.concatenate([[0], np.cumsum(g["n_leaf"])])
+    samples, splits = [], {}
+    names = ("train", "valid", "test")
+    for i in range(len(g["n_leaf"])):
+        comp = pb.CompactAst(g["vectors"][off[i]:off[i + 1]],
+                             tuple(g["ordering"][off[i]:off[i + 1]].tolist()), (), int(g["n_leaf"][i]))
+        s = pb.Sample(f"s{i}", f"t{g['task'][i]}", f"m{g['model'][i]}", "synth0", comp,
+                      float(g["latency"][i]))
+        samples.append(s)
+        splits[s.id] = names[int(g["split"][i])]
+    return pb.Dataset(samples=samples, splits=splits)
+
+
+SYNTH = None
+
+
+def devices():
+    pb = _pb()
+    return {"synth0": pb.DeviceSpec("synth0", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0)}
+
+
+def test_train_tracks_reference_desk_run():
+    pb = _pb()
+    gm = load_golden("model_desk")
+    ds = c1_dataset()
+    res = pb.train(pb.desk_config(epochs=10, seed=0), ds, devices())
+    ref = gm["train_log"]  # [epoch] = (train_loss, val_mape, val_rmse)
+    got = np.array([[e.train_loss, e.val_mape, e.val_rmse] for e in res.log])
+    rel = np.abs(got[:, 0] - ref[:, 0]) / ref[:, 0]
+    assert rel.max() <= 0.02, rel
+    lam, shift, tm, ts, off = gm["norm"]
+    assert res.normalizer.lambda_bc == pytest.approx(lam, abs=1e-12)
+    assert res.best_epoch == int(gm["best_epoch"])
+
+
+def test_train_deterministic_and_zero_epochs():
+    pb = _pb()
+    ds = c1_dataset()
+    cfg = pb.desk_config(epochs=3, seed=11, d_model=16, d_ff=32, d_embed=8, batch_size=16)
+    a = pb.train(cfg, ds, devices())
+    b = pb.train(cfg, ds, devices())
+    assert [r.__dict__ for r in a.log] == [r.__dict__ for r in b.log]
+    for k in a.params.tensors:
+        assert np.array_equal(a.params.tensors[k], b.params.tensors[k])
+    z = pb.train(pb.desk_config(epochs=0, seed=3), ds, devices())
+    fresh = pb.init_params(pb.desk_config(epochs=0, seed=3))
+    assert z.log == []
+    for k in fresh.tensors:
+        assert np.array_equal(z.params.tensors[k], fresh.tensors[k])
+
+
+def test_finetune_cmd_runs_and_is_deterministic():
+    pb = _pb()
+    ds = c1_dataset()
+    cfg = pb.desk_config(epochs=2, seed=10, d_model=16, d_ff=32, d_embed=8, d_device=4,
+                         decoder_dims=(8,), batch_size=32)
+    pre = pb.train(cfg, ds, devices())
+    shift = np.where((np.arange(24) >= 10) & (np.arange(24) < 16), 2.0, 0.0)
+    test = ds.subset("test")
+    dv = pb.device_vector(devices()["synth0"])
+    from oracle import featurize as of
+    tgt = [pb.EncodedInput(of.encode_rows(s.compact.leaf_vectors, s.compact.ordering) + shift, dv)
+           for s in test]
+    ft_cfg = pb.desk_config(epochs=2, seed=10, d_model=16, d_ff=32, d_embed=8, d_device=4,
+                            decoder_dims=(8,), batch_size=32, alpha_cmd=1.0)
+    f1 = pb.finetune(pre.params, ds, tgt, ft_cfg, devices(), pre.normalizer)
+    f2 = pb.finetune(pre.params, ds, tgt, ft_cfg, devices(), pre.normalizer)
+    assert [r.__dict__ for r in f1.log] == [r.__dict__ for r in f2.log]
+    assert all(e.cmd > 0 for e in f1.log)
+    for k in f1.params.tensors:
+        assert np.array_equal(f1.params.tensors[k], f2.params.tensors[k])
+    from paper_2311_09690_b200.errors import EmptyDataset
+    with pytest.raises(EmptyDataset):
+        pb.finetune(pre.params, ds, [], ft_cfg, devices(), pre.normalizer)
