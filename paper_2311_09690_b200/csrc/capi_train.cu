@@ -113,7 +113,7 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
                            loss, step_loss, step_cmd, stream);
   if (st) return st;
   if (g_prof) g_prof->mark(stream);
-  if (opt.kind != kOptNone && PT) st = launch_transpose(m, P, PT, stream);
+  // (the staged backward reads W with a transposed index: no transposed copy)
   if (g_prof) g_prof->mark(stream);
   return st;
 }

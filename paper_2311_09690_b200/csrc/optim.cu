@@ -27,7 +27,8 @@ __device__ __forceinline__ int region_bit(const Model& M, int p, const int* leaf
 }
 
 __global__ void __launch_bounds__(256) reduce_apply_kernel(
-    Model M, const float* __restrict__ partial, size_t stride, const uint32_t* __restrict__ touched,
+    const __grid_constant__ Model M, const float* __restrict__ partial, size_t stride,
+    const uint32_t* __restrict__ touched,
     const int4* __restrict__ steps, int step, int n_slots, int use_cmd, float* __restrict__ grad_out,
     float* __restrict__ P, float* __restrict__ mbuf, float* __restrict__ vbuf, OptDev opt,
     const double* __restrict__ lr_p, const int64_t* __restrict__ t_p,
@@ -80,29 +81,63 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(
   const float b1 = (float)opt.beta1, b2 = (float)opt.beta2, eps = (float)opt.eps,
               wd = (float)opt.weight_decay;
   const float omb1 = (float)(1.0 - opt.beta1), omb2 = (float)(1.0 - opt.beta2);
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < M.total; p += gridDim.x * blockDim.x) {
-    const int bit = region_bit(M, p, s_leaf);
-    const uint32_t want = 1u << bit;
-    float g = 0.f;
-    for (int c = 0; c < G; ++c)
-      if (s_touch[c] & want) g += partial[(size_t)c * stride + p];
-    if (grad_out) grad_out[p] = g;
-    if (opt.kind == kOptNone) continue;
-    float w = P[p];
-    if (wd != 0.f) g = g + wd * w;
-    if (opt.kind == kOptSgd) {
-      w = w - lr * g;
-    } else {
-      float m = mbuf[p], v = vbuf[p];
-      m = __fmul_rn(m, b1);
-      m = __fadd_rn(m, __fmul_rn(omb1, g));
-      v = __fmul_rn(v, b2);
-      v = __fadd_rn(v, __fmul_rn(__fmul_rn(omb2, g), g));
-      mbuf[p] = m;
-      vbuf[p] = v;
-      w = w - __fdiv_rn(__fmul_rn(lr, __fdiv_rn(m, bc1)), __fadd_rn(sqrtf(__fdiv_rn(v, bc2)), eps));
+  // 4 parameters per thread: tensors start on 16-byte boundaries, so a group
+  // never straddles two tensors and shares one region bit
+  const int n4 = M.total >> 2;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += gridDim.x * blockDim.x) {
+    const int p = q << 2;
+    const uint32_t want = 1u << region_bit(M, p, s_leaf);
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* src = reinterpret_cast<const float4*>(partial + p);
+    const size_t st4 = stride >> 2;
+    int c = 0;
+    for (; c + 4 <= G; c += 4) {  // 4 slots in flight, summed in slot order
+      float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0, v2 = v0, v3 = v0;
+      if (s_touch[c] & want) v0 = src[(size_t)c * st4];
+      if (s_touch[c + 1] & want) v1 = src[(size_t)(c + 1) * st4];
+      if (s_touch[c + 2] & want) v2 = src[(size_t)(c + 2) * st4];
+      if (s_touch[c + 3] & want) v3 = src[(size_t)(c + 3) * st4];
+      g.x += v0.x; g.y += v0.y; g.z += v0.z; g.w += v0.w;
+      g.x += v1.x; g.y += v1.y; g.z += v1.z; g.w += v1.w;
+      g.x += v2.x; g.y += v2.y; g.z += v2.z; g.w += v2.w;
+      g.x += v3.x; g.y += v3.y; g.z += v3.z; g.w += v3.w;
     }
-    P[p] = w;
+    for (; c < G; ++c) {
+      if (s_touch[c] & want) {
+        const float4 v = src[(size_t)c * st4];
+        g.x += v.x; g.y += v.y; g.z += v.z; g.w += v.w;
+      }
+    }
+    if (grad_out) *reinterpret_cast<float4*>(grad_out + p) = g;
+    if (opt.kind == kOptNone) continue;
+    float4 w = *reinterpret_cast<float4*>(P + p);
+    float gg[4] = {g.x, g.y, g.z, g.w};
+    float ww[4] = {w.x, w.y, w.z, w.w};
+    if (opt.kind == kOptSgd) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float gj = gg[j];
+        if (wd != 0.f) gj = gj + wd * ww[j];
+        ww[j] = ww[j] - lr * gj;
+      }
+    } else {
+      const float4 m4 = *reinterpret_cast<float4*>(mbuf + p);
+      const float4 v4 = *reinterpret_cast<float4*>(vbuf + p);
+      float mm[4] = {m4.x, m4.y, m4.z, m4.w};
+      float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float gj = gg[j];
+        if (wd != 0.f) gj = gj + wd * ww[j];
+        mm[j] = __fadd_rn(__fmul_rn(mm[j], b1), __fmul_rn(omb1, gj));
+        vv[j] = __fadd_rn(__fmul_rn(vv[j], b2), __fmul_rn(__fmul_rn(omb2, gj), gj));
+        ww[j] = ww[j] - __fdiv_rn(__fmul_rn(lr, __fdiv_rn(mm[j], bc1)),
+                                  __fadd_rn(sqrtf(__fdiv_rn(vv[j], bc2)), eps));
+      }
+      *reinterpret_cast<float4*>(mbuf + p) = make_float4(mm[0], mm[1], mm[2], mm[3]);
+      *reinterpret_cast<float4*>(vbuf + p) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    }
+    *reinterpret_cast<float4*>(P + p) = make_float4(ww[0], ww[1], ww[2], ww[3]);
   }
 }
 
@@ -155,7 +190,7 @@ int launch_reduce_apply(const Model& M, const TrainWs& ws, const int4* steps, in
                         float* grad_out, float* P, float* m, float* v, const OptDev& opt,
                         const double* lr, const int64_t* t, const LossDev& loss, double* step_loss,
                         double* step_cmd, cudaStream_t stream) {
-  const int grid = min(ceil_div(M.total, 256), kNumSMs * 4);
+  const int grid = min(ceil_div(M.total / 4, 256), kNumSMs * 8);
   reduce_apply_kernel<<<grid, 256, 0, stream>>>(M, ws.partial, ws.slot_stride, ws.touched, steps,
                                                 step, ws.n_slots, use_cmd, grad_out, P, m, v, opt,
                                                 lr, t, ws.terms, ws.scalars, loss, step_loss,

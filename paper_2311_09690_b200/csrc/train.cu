@@ -10,11 +10,13 @@
 // Work decomposition: one work item = one sample (its L ≤ 16 leaf rows); a
 // CTA keeps every activation of its sample in shared memory, so forward and
 // backward never touch HBM except for weights (L2-resident) and the CTA's
-// private gradient slot.  Weight gradients of a CTA go to slot blockIdx.x of
-// `partial`; optim.cu sums the slots in slot order — deterministic, no float
-// atomics (SPEC determinism contract).  dX products use a transposed copy of
-// every weight matrix (PT, refreshed after each optimizer step) so all
-// products are coalesced row-major GEMMs.
+// private gradient slot.  Weights are streamed op by op into a double-
+// buffered shared-memory stage with cp.async, one op ahead of use
+// (smallmm.cuh), so the L2 latency of the next weight matrix hides behind the
+// current op; the transposed products of the backward read the same staged
+// copy with a transposed index.  Weight gradients of a CTA go to slot
+// blockIdx.x of `partial`; optim.cu sums the slots in slot order —
+// deterministic, no float atomics (SPEC determinism contract).
 //
 // CMD couples the samples of a step through batch statistics, so a CMD step
 // runs the kernel twice: phase 0 writes every sample's z, phase 1 recomputes
@@ -26,16 +28,74 @@
 #include "blocks.cuh"
 #include "common.cuh"
 #include "cmd.cuh"
+#include "smallmm.cuh"
 #include "train.cuh"
 
 namespace tpcb {
+
+
+__host__ __device__ inline int round4(int v) { return (v + 3) & ~3; }
+
+// ---------------------------------------------------------------------------
+// weight stream: the fixed order in which the fwd+bwd of one sample consumes
+// weight matrices
+// ---------------------------------------------------------------------------
+
+__host__ __device__ inline int n_fwd_entries(const Model& M, int L) {
+  return 1 + 6 * M.n_layers + L + 2 + M.n_dec + 1;
+}
+__host__ __device__ inline int n_all_entries(const Model& M, int L) {
+  return n_fwd_entries(M, L) + M.n_dec + 1 + L + 6 * M.n_layers;
+}
+
+__host__ __device__ inline void entry_shape(const Model& M, int L, int idx, int* K, int* N,
+                                            int* off) {
+  const int nl = M.n_layers, nd = M.n_dec, d = M.d;
+  auto dec_in = [&](int j) { return j == 0 ? M.d_e : M.dec[j - 1]; };
+  const int nf = n_fwd_entries(M, L);
+  auto layer_mat = [&](int li, int kind) {  // 0 Wq 1 Wk 2 Wv 3 Wo 4 fhW 5 foW
+    const LayerOff& lo = M.layer[li];
+    switch (kind) {
+      case 0: *K = d; *N = d; *off = lo.Wq; break;
+      case 1: *K = d; *N = d; *off = lo.Wk; break;
+      case 2: *K = d; *N = d; *off = lo.Wv; break;
+      case 3: *K = d; *N = d; *off = lo.Wo; break;
+      case 4: *K = d; *N = M.d_ff; *off = lo.fhW; break;
+      default: *K = M.d_ff; *N = d; *off = lo.foW; break;
+    }
+  };
+  if (idx < nf) {
+    if (idx == 0) { *K = TPCB_FEAT; *N = d; *off = M.inW; return; }
+    int q = idx - 1;
+    if (q < 6 * nl) { layer_mat(q / 6, q % 6); return; }
+    q -= 6 * nl;
+    if (q < L) { *K = d; *N = M.d_e; *off = M.leafW[L] + q * d * M.d_e; return; }
+    q -= L;
+    if (q == 0) { *K = TPCB_DEV_FEAT; *N = M.d_dev; *off = M.devhW; return; }
+    if (q == 1) { *K = M.d_dev; *N = M.d_e; *off = M.devpW; return; }
+    q -= 2;
+    if (q < nd) { *K = dec_in(q); *N = M.dec[q]; *off = M.decW[q]; return; }
+    *K = dec_in(nd); *N = 1; *off = M.outW;
+    return;
+  }
+  int b = idx - nf;
+  if (b < nd) { const int j = nd - 1 - b; *K = dec_in(j); *N = M.dec[j]; *off = M.decW[j]; return; }
+  b -= nd;
+  if (b == 0) { *K = M.d_dev; *N = M.d_e; *off = M.devpW; return; }
+  b -= 1;
+  if (b < L) { *K = d; *N = M.d_e; *off = M.leafW[L] + b * d * M.d_e; return; }
+  b -= L;
+  const int li = nl - 1 - b / 6;
+  const int order[6] = {5, 4, 3, 0, 1, 2};  // foW, fhW, Wo, Wq, Wk, Wv
+  layer_mat(li, order[b % 6]);
+}
 
 TrainPlan make_train_plan(const Model& M) {
   TrainPlan p;
   const int R = M.n_leaf_max;
   p.R = R;
-  p.ld = M.d + 1;
-  p.ldf = M.d_ff + 1;
+  p.ld = round4(M.d) + 4;
+  p.ldf = round4(M.d_ff) + 4;
   const int blk = R * p.ld;
   int o = 0;
   p.oQ = o; o += blk;
@@ -45,13 +105,13 @@ TrainPlan make_train_plan(const Model& M) {
   p.oX1 = o; o += blk;
   p.oX2 = o; o += blk;
   p.oF = o; o += R * p.ldf;
-  p.oI1 = o; o += R;
-  p.oI2 = o; o += R;
-  p.oP = o; o += M.n_heads * R * R;
+  p.oI1 = o; o += round4(R);
+  p.oI2 = o; o += round4(R);
+  p.oP = o; o += round4(M.n_heads * R * R);
   p.layer_stride = o;
   o = 0;
   p.layer_base = o; o += M.n_layers * p.layer_stride;
-  p.X0 = o; o += R * (TPCB_FEAT + 1);
+  p.X0 = o; o += R * 28;
   p.H0 = o; o += blk;
   p.Hout = o; o += blk;
   p.T1 = o; o += blk;
@@ -63,31 +123,44 @@ TrainPlan make_train_plan(const Model& M) {
   p.dK = o; o += blk;
   p.dV = o; o += blk;
   p.dF = o; o += R * p.ldf;
-  p.S = o; o += M.n_heads * R * R;
-  int uw = 1, usum = M.d_e;
+  int uw = M.d_e, usum = round4(M.d_e);
   for (int i = 0; i < M.n_dec; ++i) {
     uw = max(uw, M.dec[i]);
-    usum += M.dec[i];
+    usum += round4(M.dec[i]);
   }
-  uw = max(uw, M.d_e);
-  p.uw = uw;
+  p.uw = round4(max(uw, max(M.d_dev, M.d)));
   p.dv = o; o += 8;
-  p.zx = o; o += M.d_e;
-  p.zv = o; o += M.d_dev;
-  p.zp = o; o += M.d_e;
-  p.u = o; o += usum;  // u[0] = z, u[j+1] = output of decoder layer j
-  p.du0 = o; o += uw;
-  p.du1 = o; o += uw;
-  p.dzx = o; o += M.d_e;
-  p.dzp = o; o += M.d_e;
-  p.dzv = o; o += M.d_dev;
-  p.dflat = o; o += R * M.d;
+  p.zx = o; o += round4(M.d_e);
+  p.zv = o; o += round4(M.d_dev);
+  p.zp = o; o += round4(M.d_e);
+  p.u = o; o += usum;  // u[0] = z, u[j+1] = output of decoder layer j (each 4-aligned)
+  p.du0 = o; o += p.uw;
+  p.du1 = o; o += p.uw;
+  p.dzx = o; o += round4(M.d_e);
+  p.dzp = o; o += round4(M.d_e);
+  p.dzv = o; o += round4(M.d_dev);
+  p.dflat = o; o += round4(M.d_e) + 4;
   p.misc = o; o += 8;
+  // split-K partials of small_mm and the attention dS scratch share a region
+  p.S = o; o += max(256 * R, M.n_heads * R * R);
   o = (o + 1) & ~1;  // 8-byte align the fp64 CMD scratch
   p.cmd = o;
-  // per column: lo, hi, mus, mut, s, u, ds + amin, amax (stored as double) + ms[K+1], mt[K+1]
   p.cmd_cols = M.d_e;
   o += 2 * cmd_scratch_doubles(M.d_e) + 8;
+  // weight stage: two buffers of the largest entry (ld = N + 1)
+  int cap = 0;
+  for (int L = 1; L <= M.n_leaf_max; ++L) {
+    const int n = n_all_entries(M, L);
+    for (int i = 0; i < n; ++i) {
+      int K, N, off;
+      entry_shape(M, L, i, &K, &N, &off);
+      cap = max(cap, K * (N + 1));
+    }
+  }
+  p.stage_cap = round4(cap);
+  o = round4(o);
+  p.stage0 = o; o += p.stage_cap;
+  p.stage1 = o; o += p.stage_cap;
   p.total = o;
   return p;
 }
@@ -127,17 +200,57 @@ __device__ double decode_plain(double e, const tpcb_boxcox& n) {
 
 __device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
 
-}  // namespace
+// op-ahead weight prefetch over the entries of one sample
+struct WStream {
+  const Model* M;
+  const float* P;
+  float* buf[2];
+  int L, idx, n;
 
-namespace {
+  __device__ void stage(int i) {
+    int K, N, off;
+    entry_shape(*M, L, i, &K, &N, &off);
+    WEntry e;
+    e.p[0] = P + off;
+    e.K = K;
+    e.Nb = N;
+    e.nb = 1;
+    stage_entry(e, buf[i & 1]);
+  }
+  __device__ void begin(int L_, int n_) {
+    L = L_;
+    n = n_;
+    idx = 0;
+    stage(0);
+    cp_async_commit();
+  }
+  // staged copy of entry idx (row stride N+1); prefetches entry idx+1.
+  // Every caller must have passed a block barrier since the previous use of
+  // the buffer being refilled.
+  __device__ const float* acquire(int* ldw) {
+    int K, N, off;
+    entry_shape(*M, L, idx, &K, &N, &off);
+    *ldw = N + 1;
+    if (idx + 1 < n) stage(idx + 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    return buf[(idx++) & 1];
+  }
+  __device__ void drain() {
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+};
 
 __global__ void __launch_bounds__(256) train_kernel(
-    Model M, const float* __restrict__ Pw, const float* __restrict__ PT, SampleSetDev src,
-    SampleSetDev tgt, const int32_t* __restrict__ batch_all, const int4* __restrict__ steps,
-    int step, LossDev loss, int phase, TrainPlan tp, float* __restrict__ zall, float* __restrict__ partial,
+    const __grid_constant__ Model M, const float* __restrict__ Pw, SampleSetDev src, SampleSetDev tgt,
+    const int32_t* __restrict__ batch_all, const int4* __restrict__ steps, int step, LossDev loss,
+    int phase, const __grid_constant__ TrainPlan tp, float* __restrict__ zall,
+    float* __restrict__ partial,
     size_t slot_stride, uint32_t* __restrict__ touched, double* __restrict__ terms,
     double* __restrict__ scalars, float* __restrict__ pred_out, int32_t* status) {
-  extern __shared__ float sm[];
+  extern __shared__ __align__(16) float sm[];
   const int4 sd = steps[step];
   const int32_t* batch = batch_all + sd.x;
   const int n_src = sd.y, n_tgt = sd.z;
@@ -166,76 +279,83 @@ __global__ void __launch_bounds__(256) train_kernel(
   float* uall = sm + tp.u;
   float* misc = sm + tp.misc;
   double* cmds = reinterpret_cast<double*>(sm + tp.cmd);
+  WStream ws;
+  ws.M = &M;
+  ws.P = Pw;
+  ws.buf[0] = sm + tp.stage0;
+  ws.buf[1] = sm + tp.stage1;
+  int uoff[TPCB_MAX_DEC + 1], uw[TPCB_MAX_DEC + 1];
+  uoff[0] = 0;
+  uw[0] = de;
+  for (int j = 0; j < M.n_dec; ++j) {
+    uoff[j + 1] = uoff[j] + round4(uw[j]);
+    uw[j + 1] = M.dec[j];
+  }
+  const int nd = M.n_dec;
+  int ldw;
 
   for (int w = blockIdx.x; w < n_all; w += gridDim.x) {
     const bool is_t = w >= n_src;
     const SampleSetDev& set = is_t ? tgt : src;
     const int idx = batch[w];
     const int L = set.n_leaf[idx];
+    ws.begin(L, phase == 0 ? n_fwd_entries(M, L) : n_all_entries(M, L));
     const float* xr = set.x + (size_t)set.ast_row[idx] * TPCB_FEAT_PAD;
     for (int e = threadIdx.x; e < L * TPCB_FEAT; e += blockDim.x) {
       const int r = e / TPCB_FEAT, c = e - r * TPCB_FEAT;
-      X0[r * (TPCB_FEAT + 1) + c] = __ldg(xr + r * TPCB_FEAT_PAD + c);
+      X0[r * 28 + c] = __ldg(xr + r * TPCB_FEAT_PAD + c);
     }
     if (threadIdx.x < TPCB_DEV_FEAT)
       dv[threadIdx.x] = __ldg(set.devfeat + (size_t)idx * TPCB_DEV_FEAT + threadIdx.x);
-    __syncthreads();
     // ------------------------------------------------------------ forward
-    gemm_rows<4, 4>(X0, TPCB_FEAT + 1, Pw + M.inW, Pw + M.inb, H0, ld, L, TPCB_FEAT, d, false);
-    __syncthreads();
+    const float* W = ws.acquire(&ldw);  // input.W (barrier inside covers X0/dv)
+    small_mm<false>(X0, 28, W, ldw, L, TPCB_FEAT, d, Pw + M.inb, false, nullptr, 0, H0, ld, S);
     const float* Hin = H0;
     for (int li = 0; li < M.n_layers; ++li) {
       const LayerOff& lo = M.layer[li];
       Ptrs c = layer_ptrs(sm, tp, li);
-      gemm_rows<4, 4>(Hin, ld, Pw + lo.Wq, Pw + lo.bq, c.Q, ld, L, d, d, false);
-      gemm_rows<4, 4>(Hin, ld, Pw + lo.Wk, Pw + lo.bk, c.K, ld, L, d, d, false);
-      gemm_rows<4, 4>(Hin, ld, Pw + lo.Wv, Pw + lo.bv, c.V, ld, L, d, d, false);
-      __syncthreads();
+      W = ws.acquire(&ldw);
+      small_mm<false>(Hin, ld, W, ldw, L, d, d, Pw + lo.bq, false, nullptr, 0, c.Q, ld, S);
+      W = ws.acquire(&ldw);
+      small_mm<false>(Hin, ld, W, ldw, L, d, d, Pw + lo.bk, false, nullptr, 0, c.K, ld, S);
+      W = ws.acquire(&ldw);
+      small_mm<false>(Hin, ld, W, ldw, L, d, d, Pw + lo.bv, false, nullptr, 0, c.V, ld, S);
       attention_rows(c.Q, c.K, c.V, ld, c.C, ld, 1, L, H, dh, scale, c.P);
-      __syncthreads();
-      gemm_rows<4, 4>(c.C, ld, Pw + lo.Wo, Pw + lo.bo, T1, ld, L, d, d, false, Hin, ld);
-      __syncthreads();
+      W = ws.acquire(&ldw);  // (its barrier also orders the attention output)
+      small_mm<false>(c.C, ld, W, ldw, L, d, d, Pw + lo.bo, false, Hin, ld, T1, ld, S);
       layernorm_rows(T1, ld, T2, ld, L, d, Pw + lo.ln1g, Pw + lo.ln1b, c.X1, ld, c.I1);
-      __syncthreads();
-      gemm_rows<4, 4>(T2, ld, Pw + lo.fhW, Pw + lo.fhb, c.F, ldf, L, d, M.d_ff, true);
-      __syncthreads();
-      gemm_rows<4, 4>(c.F, ldf, Pw + lo.foW, Pw + lo.fob, T1, ld, L, M.d_ff, d, false, T2, ld);
-      __syncthreads();
+      W = ws.acquire(&ldw);
+      small_mm<false>(T2, ld, W, ldw, L, d, M.d_ff, Pw + lo.fhb, true, nullptr, 0, c.F, ldf, S);
+      W = ws.acquire(&ldw);
+      small_mm<false>(c.F, ldf, W, ldw, L, M.d_ff, d, Pw + lo.fob, false, T2, ld, T1, ld, S);
       layernorm_rows(T1, ld, Hout, ld, L, d, Pw + lo.ln2g, Pw + lo.ln2b, c.X2, ld, c.I2);
       __syncthreads();
       Hin = Hout;
     }
-    // head forward (one sample ⇒ row vectors)
-    leaf_embed_rows(Hout, ld, 1, L, d, Pw + M.leafW[L], Pw + M.leafb[L], de, zx, de);
-    gemm_rows<1, 4>(dv, TPCB_DEV_FEAT, Pw + M.devhW, Pw + M.devhb, zv, M.d_dev, 1,
-                    TPCB_DEV_FEAT, M.d_dev, true);
-    __syncthreads();
-    gemm_rows<1, 4>(zv, M.d_dev, Pw + M.devpW, Pw + M.devpb, zp, de, 1, M.d_dev, de, false);
-    __syncthreads();
-    for (int e = threadIdx.x; e < de; e += blockDim.x) uall[e] = zx[e] * zp[e];
-    __syncthreads();
-    {
-      int off = 0, wdt = de;
-      for (int j = 0; j < M.n_dec; ++j) {
-        gemm_rows<1, 4>(uall + off, wdt, Pw + M.decW[j], Pw + M.decb[j], uall + off + wdt,
-                        M.dec[j], 1, wdt, M.dec[j], true);
-        __syncthreads();
-        off += wdt;
-        wdt = M.dec[j];
-      }
-      if (threadIdx.x < 32) {
-        float s = 0.f;
-        for (int c = threadIdx.x; c < wdt; c += 32)
-          s = fmaf(uall[off + c], __ldg(Pw + M.outW + c), s);
-        s = warp_sum(s) + __ldg(Pw + M.outb);
-        if (threadIdx.x == 0) misc[0] = s;
-      }
-      __syncthreads();
+    // head: z_x = b_L + Σ_l Hout[l] · W_L[l]   (leaf_embed.{L}, chunk per leaf)
+    for (int l = 0; l < L; ++l) {
+      W = ws.acquire(&ldw);
+      small_mm<false>(Hout + l * ld, ld, W, ldw, 1, d, de, l == 0 ? Pw + M.leafb[L] : nullptr,
+                      false, l == 0 ? nullptr : zx, 0, zx, 0, S);
     }
+    W = ws.acquire(&ldw);
+    small_mm<false>(dv, 8, W, ldw, 1, TPCB_DEV_FEAT, M.d_dev, Pw + M.devhb, true, nullptr, 0, zv,
+                    0, S);
+    W = ws.acquire(&ldw);
+    small_mm<false>(zv, 0, W, ldw, 1, M.d_dev, de, Pw + M.devpb, false, nullptr, 0, zp, 0, S);
+    for (int e = threadIdx.x; e < de; e += blockDim.x) uall[e] = zx[e] * zp[e];
+    for (int j = 0; j < nd; ++j) {
+      W = ws.acquire(&ldw);
+      small_mm<false>(uall + uoff[j], 0, W, ldw, 1, uw[j], M.dec[j], Pw + M.decb[j], true,
+                      nullptr, 0, uall + uoff[j + 1], 0, S);
+    }
+    W = ws.acquire(&ldw);
+    small_mm<false>(uall + uoff[nd], 0, W, ldw, 1, uw[nd], 1, Pw + M.outb, false, nullptr, 0,
+                    misc, 0, S);
     const float pred = misc[0];
     if (phase == 0) {
       for (int e = threadIdx.x; e < de; e += blockDim.x) zall[(size_t)w * de + e] = uall[e];
-      __syncthreads();
+      ws.drain();
       continue;
     }
     // ------------------------------------------------------- loss gradient
@@ -272,50 +392,35 @@ __global__ void __launch_bounds__(256) train_kernel(
       }
       misc[1] = (float)dpred;
     }
-    float* dz = sm + tp.du0;  // dz lives in du0 until the decoder backward is done
     __syncthreads();
     // ------------------------------------------------------------ backward
     const bool fs = !(mask & 1u);
     const bool fl = !(mask & (1u << L));
-    // decoder: du = dpred · Wout ; dWout += u_n dpred
+    float* du = sm + tp.du0;
+    float* du2 = sm + tp.du1;
     {
-      int offs[TPCB_MAX_DEC + 1];
-      int wdt[TPCB_MAX_DEC + 1];
-      offs[0] = 0;
-      wdt[0] = de;
-      for (int j = 0; j < M.n_dec; ++j) {
-        offs[j + 1] = offs[j] + wdt[j];
-        wdt[j + 1] = M.dec[j];
-      }
-      const int nd = M.n_dec;
       const float dpred = misc[1];
-      float* du = sm + tp.du0;
-      float* du2 = sm + tp.du1;
-      for (int c = threadIdx.x; c < wdt[nd]; c += blockDim.x) {
-        gstore(G, M.outW + c, uall[offs[nd] + c] * dpred, fs);
+      for (int c = threadIdx.x; c < uw[nd]; c += blockDim.x) {
+        gstore(G, M.outW + c, uall[uoff[nd] + c] * dpred, fs);
         du[c] = __ldg(Pw + M.outW + c) * dpred;
       }
       if (threadIdx.x == 0) gstore(G, M.outb, dpred, fs);
       __syncthreads();
       for (int j = nd - 1; j >= 0; --j) {
-        const float* uin = uall + offs[j];
-        const float* uout = uall + offs[j + 1];
-        const int win = wdt[j], wout = wdt[j + 1];
-        for (int c = threadIdx.x; c < wout; c += blockDim.x)
+        const float* uout = uall + uoff[j + 1];
+        for (int c = threadIdx.x; c < uw[j + 1]; c += blockDim.x)
           if (!(uout[c] > 0.f)) du[c] = 0.f;
         __syncthreads();
-        wgrad_rows(uin, win, du, wout, 1, win, wout, G + M.decW[j], fs);
-        for (int c = threadIdx.x; c < wout; c += blockDim.x) gstore(G, M.decb[j] + c, du[c], fs);
-        // du_prev = du · W_jᵀ
-        gemm_rows<1, 4>(du, wout, PT + M.decW[j], nullptr, du2, win, 1, wout, win, false);
-        __syncthreads();
+        wgrad_v(uall + uoff[j], 0, du, 0, 1, uw[j], uw[j + 1], G + M.decW[j], fs);
+        for (int c = threadIdx.x; c < uw[j + 1]; c += blockDim.x) gstore(G, M.decb[j] + c, du[c], fs);
+        W = ws.acquire(&ldw);
+        small_mm<true>(du, 0, W, ldw, 1, uw[j + 1], uw[j], nullptr, false, nullptr, 0, du2, 0, S);
         float* t = du;
         du = du2;
         du2 = t;
       }
-      dz = du;
     }
-    // CMD term
+    float* dz = du;
     if (loss.use_cmd) {
       const double v = cmd_stats(zall, n_src, n_tgt, de, loss.cmd_order, cmds);
       if (blockIdx.x == 0 && threadIdx.x == 0 && w == 0) scalars[0] = v;
@@ -332,70 +437,53 @@ __global__ void __launch_bounds__(256) train_kernel(
       dzp[e] = dz[e] * zx[e];
     }
     __syncthreads();
-    // device MLP
-    wgrad_rows(zv, M.d_dev, dzp, de, 1, M.d_dev, de, G + M.devpW, fs);
+    wgrad_v(zv, 0, dzp, 0, 1, M.d_dev, de, G + M.devpW, fs);
     for (int e = threadIdx.x; e < de; e += blockDim.x) gstore(G, M.devpb + e, dzp[e], fs);
-    gemm_rows<1, 4>(dzp, de, PT + M.devpW, nullptr, dzv, M.d_dev, 1, de, M.d_dev, false);
-    __syncthreads();
+    W = ws.acquire(&ldw);
+    small_mm<true>(dzp, 0, W, ldw, 1, de, M.d_dev, nullptr, false, nullptr, 0, dzv, 0, S);
     for (int e = threadIdx.x; e < M.d_dev; e += blockDim.x)
       if (!(zv[e] > 0.f)) dzv[e] = 0.f;
     __syncthreads();
-    wgrad_rows(dv, TPCB_DEV_FEAT, dzv, M.d_dev, 1, TPCB_DEV_FEAT, M.d_dev, G + M.devhW, fs);
+    wgrad_v(dv, 0, dzv, 0, 1, TPCB_DEV_FEAT, M.d_dev, G + M.devhW, fs);
     for (int e = threadIdx.x; e < M.d_dev; e += blockDim.x) gstore(G, M.devhb + e, dzv[e], fs);
-    // leaf_embed.{L}: dW = flat ⊗ dzx ; dflat = dzx · W_Lᵀ → dH rows
-    for (int e = threadIdx.x; e < L * d * de; e += blockDim.x) {
-      const int k = e / de, n = e - k * de;
-      const int l = k / d, j = k - l * d;
-      gstore(G, M.leafW[L] + e, Hout[l * ld + j] * dzx[n], fl);
+    // leaf_embed.{L}: dW rows l = Hout[l] ⊗ dzx ; dH[l] = dzx · W_L[l]ᵀ
+    for (int l = 0; l < L; ++l) {
+      wgrad_v(Hout + l * ld, 0, dzx, 0, 1, d, de, G + M.leafW[L] + l * d * de, fl);
+      W = ws.acquire(&ldw);
+      small_mm<true>(dzx, 0, W, ldw, 1, de, d, nullptr, false, nullptr, 0, dH + l * ld, 0, S);
     }
     for (int e = threadIdx.x; e < de; e += blockDim.x) gstore(G, M.leafb[L] + e, dzx[e], fl);
-    {
-      float* dflat = sm + tp.dflat;
-      gemm_rows<1, 4>(dzx, de, PT + M.leafW[L], nullptr, dflat, L * d, 1, de, L * d, false);
-      __syncthreads();
-      for (int e = threadIdx.x; e < L * d; e += blockDim.x) {
-        const int r = e / d, c = e - r * d;
-        dH[r * ld + c] = dflat[e];
-      }
-      __syncthreads();
-    }
     // encoder layers, last to first
     for (int li = M.n_layers - 1; li >= 0; --li) {
       const LayerOff& lo = M.layer[li];
       Ptrs c = layer_ptrs(sm, tp, li);
-      // LN2
       layernorm_back_rows(dH, ld, c.X2, ld, c.I2, L, d, Pw + lo.ln2g, dA, ld);
       colsum_rows(dH, ld, L, d, G + lo.ln2g, fs, c.X2, ld);
       colsum_rows(dH, ld, L, d, G + lo.ln2b, fs);
       __syncthreads();
-      // FFN out: dW_fo = Fᵀ dA ; dF = dA W_foᵀ ⊙ (F > 0)
-      wgrad_rows(c.F, ldf, dA, ld, L, M.d_ff, d, G + lo.foW, fs);
+      wgrad_v(c.F, ldf, dA, ld, L, M.d_ff, d, G + lo.foW, fs);
       colsum_rows(dA, ld, L, d, G + lo.fob, fs);
-      gemm_rows<4, 4>(dA, ld, PT + lo.foW, nullptr, dF, ldf, L, d, M.d_ff, false);
       ln_apply_rows(c.X1, ld, L, d, Pw + lo.ln1g, Pw + lo.ln1b, T1, ld);  // h1
-      __syncthreads();
+      W = ws.acquire(&ldw);  // foW
+      small_mm<true>(dA, ld, W, ldw, L, d, M.d_ff, nullptr, false, nullptr, 0, dF, ldf, S);
       for (int e = threadIdx.x; e < L * M.d_ff; e += blockDim.x) {
         const int r = e / M.d_ff, k = e - r * M.d_ff;
         if (!(c.F[r * ldf + k] > 0.f)) dF[r * ldf + k] = 0.f;
       }
       __syncthreads();
-      wgrad_rows(T1, ld, dF, ldf, L, d, M.d_ff, G + lo.fhW, fs);
+      wgrad_v(T1, ld, dF, ldf, L, d, M.d_ff, G + lo.fhW, fs);
       colsum_rows(dF, ldf, L, M.d_ff, G + lo.fhb, fs);
-      // dh1 = dA + dF W_fhᵀ → dB
-      gemm_rows<4, 4>(dF, ldf, PT + lo.fhW, nullptr, dB, ld, L, M.d_ff, d, false, dA, ld);
-      __syncthreads();
-      // LN1
+      W = ws.acquire(&ldw);  // fhW: dh1 = dA + dF W_fhᵀ → dB
+      small_mm<true>(dF, ldf, W, ldw, L, M.d_ff, d, nullptr, false, dA, ld, dB, ld, S);
       layernorm_back_rows(dB, ld, c.X1, ld, c.I1, L, d, Pw + lo.ln1g, dA, ld);
       colsum_rows(dB, ld, L, d, G + lo.ln1g, fs, c.X1, ld);
       colsum_rows(dB, ld, L, d, G + lo.ln1b, fs);
       __syncthreads();
-      // O projection: dW_o = Cᵀ dA ; dC = dA W_oᵀ → dB
-      wgrad_rows(c.C, ld, dA, ld, L, d, d, G + lo.Wo, fs);
+      wgrad_v(c.C, ld, dA, ld, L, d, d, G + lo.Wo, fs);
       colsum_rows(dA, ld, L, d, G + lo.bo, fs);
-      gemm_rows<4, 4>(dA, ld, PT + lo.Wo, nullptr, dB, ld, L, d, d, false);
-      __syncthreads();
+      W = ws.acquire(&ldw);  // Wo: dC = dA W_oᵀ → dB
+      small_mm<true>(dA, ld, W, ldw, L, d, d, nullptr, false, nullptr, 0, dB, ld, S);
       attention_back_rows(c.Q, c.K, c.V, ld, c.P, dB, ld, dQ, dK, dV, S, 1, L, H, dh, scale);
-      // layer input (recomputed for li > 0)
       const float* hin = H0;
       if (li > 0) {
         const LayerOff& lp = M.layer[li - 1];
@@ -404,24 +492,24 @@ __global__ void __launch_bounds__(256) train_kernel(
         hin = T1;
       }
       __syncthreads();
-      wgrad_rows(hin, ld, dQ, ld, L, d, d, G + lo.Wq, fs);
-      wgrad_rows(hin, ld, dK, ld, L, d, d, G + lo.Wk, fs);
-      wgrad_rows(hin, ld, dV, ld, L, d, d, G + lo.Wv, fs);
+      wgrad_v(hin, ld, dQ, ld, L, d, d, G + lo.Wq, fs);
+      wgrad_v(hin, ld, dK, ld, L, d, d, G + lo.Wk, fs);
+      wgrad_v(hin, ld, dV, ld, L, d, d, G + lo.Wv, fs);
       colsum_rows(dQ, ld, L, d, G + lo.bq, fs);
       colsum_rows(dK, ld, L, d, G + lo.bk, fs);
       colsum_rows(dV, ld, L, d, G + lo.bv, fs);
       // dHin = dA + dQ Wqᵀ + dK Wkᵀ + dV Wvᵀ → dH
-      gemm_rows<4, 4>(dQ, ld, PT + lo.Wq, nullptr, dH, ld, L, d, d, false, dA, ld);
-      __syncthreads();
-      gemm_rows<4, 4>(dK, ld, PT + lo.Wk, nullptr, dH, ld, L, d, d, false, dH, ld);
-      __syncthreads();
-      gemm_rows<4, 4>(dV, ld, PT + lo.Wv, nullptr, dH, ld, L, d, d, false, dH, ld);
-      __syncthreads();
+      W = ws.acquire(&ldw);
+      small_mm<true>(dQ, ld, W, ldw, L, d, d, nullptr, false, dA, ld, dH, ld, S);
+      W = ws.acquire(&ldw);
+      small_mm<true>(dK, ld, W, ldw, L, d, d, nullptr, false, dH, ld, dH, ld, S);
+      W = ws.acquire(&ldw);
+      small_mm<true>(dV, ld, W, ldw, L, d, d, nullptr, false, dH, ld, dH, ld, S);
     }
-    wgrad_rows(X0, TPCB_FEAT + 1, dH, ld, L, TPCB_FEAT, d, G + M.inW, fs);
+    wgrad_v(X0, 28, dH, ld, L, TPCB_FEAT, d, G + M.inW, fs);
     colsum_rows(dH, ld, L, d, G + M.inb, fs);
     mask |= 1u | (1u << L);
-    __syncthreads();
+    ws.drain();
   }
   if (threadIdx.x == 0) touched[blockIdx.x] = mask;
 }
@@ -432,11 +520,11 @@ int prepare_train_kernels(const Model& M) {
   TrainPlan tp = make_train_plan(M);
   const size_t smem = (size_t)tp.total * sizeof(float);
   if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
-  static size_t set_for = 0;
-  if (smem > set_for) {
+  static bool done = false;
+  if (!done) {
     TPCB_CUDA_CHECK(cudaFuncSetAttribute(train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          227 * 1024));
-    set_for = 227 * 1024;
+    done = true;
   }
   return TPCB_OK;
 }
@@ -445,6 +533,7 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
                  const SampleSetDev& tgt, const int32_t* batch, const int4* steps, int step,
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                  int32_t* status, cudaStream_t stream) {
+  (void)PT;
   TrainPlan tp = make_train_plan(M);
   const size_t smem = (size_t)tp.total * sizeof(float);
   if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
@@ -452,8 +541,8 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
   int st = prepare_train_kernels(M);
   if (st) return st;
   grid = std::max(1, std::min(grid, ws.n_slots));
-  train_kernel<<<grid, 256, smem, stream>>>(M, P, PT, src, tgt, batch, steps, step, loss, phase,
-                                            tp, ws.zall, ws.partial, ws.slot_stride, ws.touched,
+  train_kernel<<<grid, 256, smem, stream>>>(M, P, src, tgt, batch, steps, step, loss, phase, tp,
+                                            ws.zall, ws.partial, ws.slot_stride, ws.touched,
                                             ws.terms, ws.scalars, pred_out, status);
   TPCB_LAUNCH_CHECK("train_kernel");
   return TPCB_OK;

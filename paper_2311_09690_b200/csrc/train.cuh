@@ -22,6 +22,7 @@ struct TrainPlan {
   int X0, H0, Hout, T1, T2, dH, dA, dB, dQ, dK, dV, dF, S;
   int uw, dv, zx, zv, zp, u, du0, du1, dzx, dzp, dzv, dflat, misc;
   int cmd, cmd_cols;
+  int stage_cap, stage0, stage1;  // double-buffered weight stage
   int total;  // floats
 };
 
