@@ -21,26 +21,36 @@ __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(src));
 }
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// one staged weight block list: `nb` column blocks of K × Nb (row-major in
-// global memory) placed side by side → smem [K × nb·Nb], row stride nb·Nb+1
-struct WEntry {
-  const float* p[3];
-  int K, Nb, nb;
-};
+// staged stride of a weight matrix with N columns: 16-byte rows, and an odd
+// multiple of 4 floats so 8 consecutive 128-bit row reads hit distinct banks
+__host__ __device__ __forceinline__ int stage_ld(int N) { return ((N + 3) & ~3) + 4; }
 
-__device__ __forceinline__ void stage_entry(const WEntry& e, float* dst) {
-  const int ncol = e.nb * e.Nb, ld = ncol + 1;
-  const int total = e.K * ncol;
-  for (int t = threadIdx.x; t < total; t += blockDim.x) {
-    const int k = t / ncol, c = t - k * ncol;
-    const int b = c / e.Nb, n = c - b * e.Nb;
-    cp_async4(dst + k * ld + c, e.p[b] + (size_t)k * e.Nb + n);
+// stage W [K × N] (row-major, global) into dst with row stride stage_ld(N)
+__device__ __forceinline__ void stage_matrix(const float* __restrict__ W, int K, int N, float* dst) {
+  const int ld = stage_ld(N);
+  if ((N & 3) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0) {
+    const int n4 = N >> 2;
+    const int total = K * n4;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int k = t / n4, c4 = t - k * n4;
+      cp_async16(dst + k * ld + 4 * c4, W + (size_t)k * N + 4 * c4);
+    }
+  } else {
+    const int total = K * N;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int k = t / N, c = t - k * N;
+      cp_async4(dst + k * ld + c, W + (size_t)k * N + c);
+    }
   }
 }
 
@@ -64,53 +74,61 @@ __device__ __forceinline__ void small_mm(const float* A, int lda, const float* S
   for (int t = threadIdx.x; t < C * G; t += nt) {
     const int c = t % C, g = t / C;
     const int i0 = g * slice, i1 = min(I, i0 + slice);
-    float acc[kMaxRows];
-#pragma unroll
-    for (int r = 0; r < kMaxRows; ++r) acc[r] = 0.f;
-    if (vec) {
-      for (int i = i0; i < i1; i += 4) {
-        float w0, w1, w2, w3;
-        if (TRANS) {
-          const float* s = SW + c * ldw + i;
-          w0 = s[0]; w1 = s[1]; w2 = s[2]; w3 = s[3];
-        } else {
-          const float* s = SW + i * ldw + c;
-          w0 = s[0]; w1 = s[ldw]; w2 = s[2 * ldw]; w3 = s[3 * ldw];
-        }
-#pragma unroll
-        for (int r = 0; r < kMaxRows; ++r) {
-          if (r < R) {
-            const float4 a = *reinterpret_cast<const float4*>(A + r * lda + i);
-            acc[r] = fmaf(a.x, w0, acc[r]);
-            acc[r] = fmaf(a.y, w1, acc[r]);
-            acc[r] = fmaf(a.z, w2, acc[r]);
-            acc[r] = fmaf(a.w, w3, acc[r]);
+    for (int r0 = 0; r0 < R; r0 += 4) {  // rows in groups of 4 (R is usually ≤ 6)
+      const int nr = min(4, R - r0);
+      const float* a0 = A + r0 * lda;
+      float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+      if (vec) {
+        for (int i = i0; i < i1; i += 4) {
+          float4 w;
+          if (TRANS) {
+            w = *reinterpret_cast<const float4*>(SW + c * ldw + i);
+          } else {
+            const float* s = SW + i * ldw + c;
+            w = make_float4(s[0], s[ldw], s[2 * ldw], s[3 * ldw]);
+          }
+          float4 x = *reinterpret_cast<const float4*>(a0 + i);
+          acc0 = fmaf(x.x, w.x, fmaf(x.y, w.y, fmaf(x.z, w.z, fmaf(x.w, w.w, acc0))));
+          if (nr > 1) {
+            x = *reinterpret_cast<const float4*>(a0 + lda + i);
+            acc1 = fmaf(x.x, w.x, fmaf(x.y, w.y, fmaf(x.z, w.z, fmaf(x.w, w.w, acc1))));
+          }
+          if (nr > 2) {
+            x = *reinterpret_cast<const float4*>(a0 + 2 * lda + i);
+            acc2 = fmaf(x.x, w.x, fmaf(x.y, w.y, fmaf(x.z, w.z, fmaf(x.w, w.w, acc2))));
+          }
+          if (nr > 3) {
+            x = *reinterpret_cast<const float4*>(a0 + 3 * lda + i);
+            acc3 = fmaf(x.x, w.x, fmaf(x.y, w.y, fmaf(x.z, w.z, fmaf(x.w, w.w, acc3))));
           }
         }
-      }
-    } else {
-      for (int i = i0; i < i1; ++i) {
-        const float w = TRANS ? SW[c * ldw + i] : SW[i * ldw + c];
-#pragma unroll
-        for (int r = 0; r < kMaxRows; ++r)
-          if (r < R) acc[r] = fmaf(A[r * lda + i], w, acc[r]);
-      }
-    }
-    if (G == 1) {
-      const float bc = bias ? __ldg(bias + c) : 0.f;
-#pragma unroll
-      for (int r = 0; r < kMaxRows; ++r) {
-        if (r < R) {
-          float v = acc[r] + bc;
-          if (relu) v = fmaxf(v, 0.f);
-          if (Res) v += Res[r * ldr + c];
-          out[r * ldo + c] = v;
+      } else {
+        for (int i = i0; i < i1; ++i) {
+          const float w = TRANS ? SW[c * ldw + i] : SW[i * ldw + c];
+          acc0 = fmaf(a0[i], w, acc0);
+          if (nr > 1) acc1 = fmaf(a0[lda + i], w, acc1);
+          if (nr > 2) acc2 = fmaf(a0[2 * lda + i], w, acc2);
+          if (nr > 3) acc3 = fmaf(a0[3 * lda + i], w, acc3);
         }
       }
-    } else {
+      const float accs[4] = {acc0, acc1, acc2, acc3};
+      if (G == 1) {
+        const float bc = bias ? __ldg(bias + c) : 0.f;
 #pragma unroll
-      for (int r = 0; r < kMaxRows; ++r)
-        if (r < R) scratch[(g * R + r) * C + c] = acc[r];
+        for (int j = 0; j < 4; ++j) {
+          if (j < nr) {
+            const int r = r0 + j;
+            float v = accs[j] + bc;
+            if (relu) v = fmaxf(v, 0.f);
+            if (Res) v += Res[r * ldr + c];
+            out[r * ldo + c] = v;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j < nr) scratch[(g * R + r0 + j) * C + c] = accs[j];
+      }
     }
   }
   __syncthreads();

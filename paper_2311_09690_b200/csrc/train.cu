@@ -154,7 +154,7 @@ TrainPlan make_train_plan(const Model& M) {
     for (int i = 0; i < n; ++i) {
       int K, N, off;
       entry_shape(M, L, i, &K, &N, &off);
-      cap = max(cap, K * (N + 1));
+      cap = max(cap, K * stage_ld(N));
     }
   }
   p.stage_cap = round4(cap);
@@ -210,12 +210,7 @@ struct WStream {
   __device__ void stage(int i) {
     int K, N, off;
     entry_shape(*M, L, i, &K, &N, &off);
-    WEntry e;
-    e.p[0] = P + off;
-    e.K = K;
-    e.Nb = N;
-    e.nb = 1;
-    stage_entry(e, buf[i & 1]);
+    stage_matrix(P + off, K, N, buf[i & 1]);
   }
   __device__ void begin(int L_, int n_) {
     L = L_;
@@ -230,7 +225,7 @@ struct WStream {
   __device__ const float* acquire(int* ldw) {
     int K, N, off;
     entry_shape(*M, L, idx, &K, &N, &off);
-    *ldw = N + 1;
+    *ldw = stage_ld(N);
     if (idx + 1 < n) stage(idx + 1);
     cp_async_commit();
     cp_async_wait<1>();
