@@ -107,7 +107,9 @@ class Trainer:
         self.n_train = train_rag.n_ast
         self.n_leaf = np.asarray(train_rag.n_leaf)
         # plan buffers (fixed sizes: every epoch visits every training sample once)
-        self.max_entries = self.n_train + (self.n_train if self.use_cmd else 0)
+        n_steps_max = int(sum(-(-int(c) // config.batch_size)
+                              for c in np.bincount(self.n_leaf)[1:]))
+        self.max_entries = self.n_train + (n_steps_max * config.batch_size if self.use_cmd else 0)
         self.batch_dev = torch.zeros(max(self.max_entries, 1), dtype=torch.int32, device=device)
         self.batch_host = torch.zeros(max(self.max_entries, 1), dtype=torch.int32).pin_memory()
         self.hyper_dev = torch.zeros(2, dtype=torch.float64, device=device)  # lr, t0 (as f64)

@@ -221,6 +221,13 @@ def main():
         plan[f"ep{ep}.len"] = np.array([len(b) for b in bl])
     np.savez_compressed(OUT / "plan.npz", n_leaf=np.array(tr_nleaf), **plan)
 
+    # acceptance criterion 6 dataset (test_acceptance.py:232-257)
+    ds6 = split_dataset(generate_synthetic(2000, [DEFAULT_SYNTH_DEVICE],
+                                           SynthOracleConfig(noise_sigma=0.0), seed=11), seed=1)
+    np.savez_compressed(OUT / "crit6.npz", **compacts_blob(ds6.samples),
+                        split=np.array([{"train": 0, "valid": 1, "test": 2}[ds6.splits[s.id]]
+                                        for s in ds6.samples]))
+
     # ---------------------------------------------------------------- CMD
     out = {}
     crng = np.random.default_rng(2)
