@@ -36,7 +36,7 @@ __device__ __forceinline__ void cp_async_wait() {
 __host__ __device__ __forceinline__ int stage_ld(int N) { return ((N + 3) & ~3) + 4; }
 
 // stage W [K × N] (row-major, global) into dst with row stride stage_ld(N)
-__device__ __forceinline__ void stage_matrix(const float* __restrict__ W, int K, int N, float* dst) {
+static __device__ __noinline__ void stage_matrix(const float* __restrict__ W, int K, int N, float* dst) {
   const int ld = stage_ld(N);
   if ((N & 3) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0) {
     const int n4 = N >> 2;
@@ -60,7 +60,7 @@ __device__ __forceinline__ void stage_matrix(const float* __restrict__ W, int K,
 // Rows of A: stride lda (multiple of 4, 16-B aligned base) when I % 4 == 0.
 // `scratch` (≥ blockDim·R floats) holds split-K partials.  Ends with a barrier.
 template <bool TRANS>
-__device__ __forceinline__ void small_mm(const float* A, int lda, const float* SW, int ldw, int R,
+static __device__ __noinline__ void small_mm(const float* A, int lda, const float* SW, int ldw, int R,
                                          int I, int C, const float* __restrict__ bias,
                                          bool relu, const float* Res, int ldr, float* out,
                                          int ldo, float* scratch) {
@@ -147,7 +147,7 @@ __device__ __forceinline__ void small_mm(const float* A, int lda, const float* S
 
 // G[k*N + n] (+)= Σ_r X[r, k] · dY[r, n]  — weight gradient into the CTA's
 // gradient slot (global), 4 columns per thread with 128-bit stores.
-__device__ __forceinline__ void wgrad_v(const float* X, int ldx, const float* dY, int ldy, int R,
+static __device__ __noinline__ void wgrad_v(const float* X, int ldx, const float* dY, int ldy, int R,
                                         int K, int N, float* G, bool first) {
   if ((N & 3) == 0 && (ldy & 3) == 0 && ((reinterpret_cast<uintptr_t>(G) & 15) == 0)) {
     const int n4 = N >> 2;

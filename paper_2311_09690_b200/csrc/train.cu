@@ -167,6 +167,39 @@ TrainPlan make_train_plan(const Model& M) {
 
 namespace {
 
+// out-of-line copies of the row blocks: the training kernel calls each one
+// dozens of times per sample; one copy keeps the kernel in the I-cache
+__device__ __noinline__ void layernorm_rows_nl(const float* X, int ldx, float* Y, int ldy, int R,
+                                               int d, const float* g, const float* b,
+                                               float* xhat, int ldh, float* inv_out) {
+  layernorm_rows(X, ldx, Y, ldy, R, d, g, b, xhat, ldh, inv_out);
+}
+__device__ __noinline__ void attention_rows_nl(const float* Q, const float* K, const float* V,
+                                               int ld, float* C, int ldc, int A, int L, int H,
+                                               int dh, float scale, float* P) {
+  attention_rows(Q, K, V, ld, C, ldc, A, L, H, dh, scale, P);
+}
+__device__ __noinline__ void colsum_rows_nl(const float* dY, int ldy, int R, int N, float* G,
+                                            bool first, const float* S, int lds) {
+  colsum_rows(dY, ldy, R, N, G, first, S, lds);
+}
+__device__ __noinline__ void layernorm_back_rows_nl(const float* dY, int ldy, const float* Xh,
+                                                    int ldh, const float* inv, int R, int d,
+                                                    const float* g, float* dX, int ldx) {
+  layernorm_back_rows(dY, ldy, Xh, ldh, inv, R, d, g, dX, ldx);
+}
+__device__ __noinline__ void ln_apply_rows_nl(const float* Xh, int ldh, int R, int d,
+                                              const float* g, const float* b, float* Y, int ldy) {
+  ln_apply_rows(Xh, ldh, R, d, g, b, Y, ldy);
+}
+__device__ __noinline__ void attention_back_rows_nl(const float* Q, const float* K,
+                                                    const float* V, int ld, const float* P,
+                                                    const float* dC, int ldc, float* dQ,
+                                                    float* dK, float* dV, float* S, int A, int L,
+                                                    int H, int dh, float scale) {
+  attention_back_rows(Q, K, V, ld, P, dC, ldc, dQ, dK, dV, S, A, L, H, dh, scale);
+}
+
 struct Ptrs {
   float *Q, *K, *V, *C, *X1, *X2, *F, *I1, *I2, *P;
 };
@@ -315,15 +348,15 @@ __global__ void __launch_bounds__(256) train_kernel(
       small_mm<false>(Hin, ld, W, ldw, L, d, d, Pw + lo.bk, false, nullptr, 0, c.K, ld, S);
       W = ws.acquire(&ldw);
       small_mm<false>(Hin, ld, W, ldw, L, d, d, Pw + lo.bv, false, nullptr, 0, c.V, ld, S);
-      attention_rows(c.Q, c.K, c.V, ld, c.C, ld, 1, L, H, dh, scale, c.P);
+      attention_rows_nl(c.Q, c.K, c.V, ld, c.C, ld, 1, L, H, dh, scale, c.P);
       W = ws.acquire(&ldw);  // (its barrier also orders the attention output)
       small_mm<false>(c.C, ld, W, ldw, L, d, d, Pw + lo.bo, false, Hin, ld, T1, ld, S);
-      layernorm_rows(T1, ld, T2, ld, L, d, Pw + lo.ln1g, Pw + lo.ln1b, c.X1, ld, c.I1);
+      layernorm_rows_nl(T1, ld, T2, ld, L, d, Pw + lo.ln1g, Pw + lo.ln1b, c.X1, ld, c.I1);
       W = ws.acquire(&ldw);
       small_mm<false>(T2, ld, W, ldw, L, d, M.d_ff, Pw + lo.fhb, true, nullptr, 0, c.F, ldf, S);
       W = ws.acquire(&ldw);
       small_mm<false>(c.F, ldf, W, ldw, L, M.d_ff, d, Pw + lo.fob, false, T2, ld, T1, ld, S);
-      layernorm_rows(T1, ld, Hout, ld, L, d, Pw + lo.ln2g, Pw + lo.ln2b, c.X2, ld, c.I2);
+      layernorm_rows_nl(T1, ld, Hout, ld, L, d, Pw + lo.ln2g, Pw + lo.ln2b, c.X2, ld, c.I2);
       __syncthreads();
       Hin = Hout;
     }
@@ -452,13 +485,13 @@ __global__ void __launch_bounds__(256) train_kernel(
     for (int li = M.n_layers - 1; li >= 0; --li) {
       const LayerOff& lo = M.layer[li];
       Ptrs c = layer_ptrs(sm, tp, li);
-      layernorm_back_rows(dH, ld, c.X2, ld, c.I2, L, d, Pw + lo.ln2g, dA, ld);
-      colsum_rows(dH, ld, L, d, G + lo.ln2g, fs, c.X2, ld);
-      colsum_rows(dH, ld, L, d, G + lo.ln2b, fs);
+      layernorm_back_rows_nl(dH, ld, c.X2, ld, c.I2, L, d, Pw + lo.ln2g, dA, ld);
+      colsum_rows_nl(dH, ld, L, d, G + lo.ln2g, fs, c.X2, ld);
+      colsum_rows_nl(dH, ld, L, d, G + lo.ln2b, fs, nullptr, 0);
       __syncthreads();
       wgrad_v(c.F, ldf, dA, ld, L, M.d_ff, d, G + lo.foW, fs);
-      colsum_rows(dA, ld, L, d, G + lo.fob, fs);
-      ln_apply_rows(c.X1, ld, L, d, Pw + lo.ln1g, Pw + lo.ln1b, T1, ld);  // h1
+      colsum_rows_nl(dA, ld, L, d, G + lo.fob, fs, nullptr, 0);
+      ln_apply_rows_nl(c.X1, ld, L, d, Pw + lo.ln1g, Pw + lo.ln1b, T1, ld);  // h1
       W = ws.acquire(&ldw);  // foW
       small_mm<true>(dA, ld, W, ldw, L, d, M.d_ff, nullptr, false, nullptr, 0, dF, ldf, S);
       for (int e = threadIdx.x; e < L * M.d_ff; e += blockDim.x) {
@@ -467,32 +500,32 @@ __global__ void __launch_bounds__(256) train_kernel(
       }
       __syncthreads();
       wgrad_v(T1, ld, dF, ldf, L, d, M.d_ff, G + lo.fhW, fs);
-      colsum_rows(dF, ldf, L, M.d_ff, G + lo.fhb, fs);
+      colsum_rows_nl(dF, ldf, L, M.d_ff, G + lo.fhb, fs, nullptr, 0);
       W = ws.acquire(&ldw);  // fhW: dh1 = dA + dF W_fhᵀ → dB
       small_mm<true>(dF, ldf, W, ldw, L, M.d_ff, d, nullptr, false, dA, ld, dB, ld, S);
-      layernorm_back_rows(dB, ld, c.X1, ld, c.I1, L, d, Pw + lo.ln1g, dA, ld);
-      colsum_rows(dB, ld, L, d, G + lo.ln1g, fs, c.X1, ld);
-      colsum_rows(dB, ld, L, d, G + lo.ln1b, fs);
+      layernorm_back_rows_nl(dB, ld, c.X1, ld, c.I1, L, d, Pw + lo.ln1g, dA, ld);
+      colsum_rows_nl(dB, ld, L, d, G + lo.ln1g, fs, c.X1, ld);
+      colsum_rows_nl(dB, ld, L, d, G + lo.ln1b, fs, nullptr, 0);
       __syncthreads();
       wgrad_v(c.C, ld, dA, ld, L, d, d, G + lo.Wo, fs);
-      colsum_rows(dA, ld, L, d, G + lo.bo, fs);
+      colsum_rows_nl(dA, ld, L, d, G + lo.bo, fs, nullptr, 0);
       W = ws.acquire(&ldw);  // Wo: dC = dA W_oᵀ → dB
       small_mm<true>(dA, ld, W, ldw, L, d, d, nullptr, false, nullptr, 0, dB, ld, S);
-      attention_back_rows(c.Q, c.K, c.V, ld, c.P, dB, ld, dQ, dK, dV, S, 1, L, H, dh, scale);
+      attention_back_rows_nl(c.Q, c.K, c.V, ld, c.P, dB, ld, dQ, dK, dV, S, 1, L, H, dh, scale);
       const float* hin = H0;
       if (li > 0) {
         const LayerOff& lp = M.layer[li - 1];
         Ptrs cp = layer_ptrs(sm, tp, li - 1);
-        ln_apply_rows(cp.X2, ld, L, d, Pw + lp.ln2g, Pw + lp.ln2b, T1, ld);
+        ln_apply_rows_nl(cp.X2, ld, L, d, Pw + lp.ln2g, Pw + lp.ln2b, T1, ld);
         hin = T1;
       }
       __syncthreads();
       wgrad_v(hin, ld, dQ, ld, L, d, d, G + lo.Wq, fs);
       wgrad_v(hin, ld, dK, ld, L, d, d, G + lo.Wk, fs);
       wgrad_v(hin, ld, dV, ld, L, d, d, G + lo.Wv, fs);
-      colsum_rows(dQ, ld, L, d, G + lo.bq, fs);
-      colsum_rows(dK, ld, L, d, G + lo.bk, fs);
-      colsum_rows(dV, ld, L, d, G + lo.bv, fs);
+      colsum_rows_nl(dQ, ld, L, d, G + lo.bq, fs, nullptr, 0);
+      colsum_rows_nl(dK, ld, L, d, G + lo.bk, fs, nullptr, 0);
+      colsum_rows_nl(dV, ld, L, d, G + lo.bv, fs, nullptr, 0);
       // dHin = dA + dQ Wqᵀ + dK Wkᵀ + dV Wvᵀ → dH
       W = ws.acquire(&ldw);
       small_mm<true>(dQ, ld, W, ldw, L, d, d, nullptr, false, dA, ld, dH, ld, S);
@@ -502,7 +535,7 @@ __global__ void __launch_bounds__(256) train_kernel(
       small_mm<true>(dV, ld, W, ldw, L, d, d, nullptr, false, dH, ld, dH, ld, S);
     }
     wgrad_v(X0, 28, dH, ld, L, TPCB_FEAT, d, G + M.inW, fs);
-    colsum_rows(dH, ld, L, d, G + M.inb, fs);
+    colsum_rows_nl(dH, ld, L, d, G + M.inb, fs, nullptr, 0);
     mask |= 1u | (1u << L);
     ws.drain();
   }
