@@ -203,24 +203,11 @@ __device__ __forceinline__ void small_mm(const float* A, int lda, const float* S
     mm_fixed<TRANS, II, CC>(A, lda, SW, R, bias, relu, Res, ldr, out, ldo, scratch);   \
     return;                                                                            \
   }
-  if (!TRANS) {
-    TPCB_MM_CASE(24, 64)
-    TPCB_MM_CASE(64, 64)
-    TPCB_MM_CASE(64, 128)
-    TPCB_MM_CASE(128, 64)
-    TPCB_MM_CASE(64, 32)
-    TPCB_MM_CASE(6, 16)
-    TPCB_MM_CASE(16, 32)
-    TPCB_MM_CASE(32, 64)
-    TPCB_MM_CASE(64, 1)
-  } else {
-    TPCB_MM_CASE(64, 64)
-    TPCB_MM_CASE(64, 32)
-    TPCB_MM_CASE(32, 16)
-    TPCB_MM_CASE(32, 64)
-    TPCB_MM_CASE(64, 128)
-    TPCB_MM_CASE(128, 64)
-  }
+  // the encoder shapes of the desk model get specialised copies; the rest
+  // (head vectors, other configs) share one generic body (I-cache budget)
+  TPCB_MM_CASE(64, 64)
+  TPCB_MM_CASE(64, 128)
+  TPCB_MM_CASE(128, 64)
 #undef TPCB_MM_CASE
   mm_generic<TRANS>(A, lda, SW, R, I, C, bias, relu, Res, ldr, out, ldo, scratch);
 }

@@ -200,6 +200,105 @@ __device__ __noinline__ void attention_back_rows_nl(const float* Q, const float*
   attention_back_rows(Q, K, V, ld, P, dC, ldc, dQ, dK, dV, S, A, L, H, dh, scale);
 }
 
+// Attention of one sample (L ≤ 16 rows) spread over the whole block:
+// scores one thread per (head, i, j), softmax one thread per (head, i),
+// context one thread per (i, feature) — three short barrier-separated
+// phases instead of one long serial loop per query row (nn.py:79-96).
+__device__ __noinline__ void attn_fwd_sample(const float* Q, const float* K, const float* V,
+                                             int ld, float* C, int L, int H, int dh, float scale,
+                                             float* P) {
+  const int nt = blockDim.x, LL = L * L;
+  for (int e = threadIdx.x; e < H * LL; e += nt) {
+    const int h = e / LL, ij = e - h * LL, i = ij / L, j = ij - i * L;
+    const float* q = Q + i * ld + h * dh;
+    const float* k = K + j * ld + h * dh;
+    float s = 0.f;
+    if ((dh & 3) == 0) {
+      for (int c = 0; c < dh; c += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(q + c);
+        const float4 b = *reinterpret_cast<const float4*>(k + c);
+        s = fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, fmaf(a.w, b.w, s))));
+      }
+    } else {
+      for (int c = 0; c < dh; ++c) s = fmaf(q[c], k[c], s);
+    }
+    P[e] = s * scale;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < H * L; e += nt) {
+    float* p = P + e * L;
+    float m = -INFINITY;
+    for (int j = 0; j < L; ++j) m = fmaxf(m, p[j]);
+    float sum = 0.f;
+    for (int j = 0; j < L; ++j) {
+      const float v = expf(p[j] - m);
+      p[j] = v;
+      sum += v;
+    }
+    for (int j = 0; j < L; ++j) p[j] = p[j] / sum;
+  }
+  __syncthreads();
+  const int D = H * dh;
+  for (int e = threadIdx.x; e < L * D; e += nt) {
+    const int i = e / D, f = e - i * D, h = f / dh;
+    const float* p = P + (h * L + i) * L;
+    float acc = 0.f;
+    for (int j = 0; j < L; ++j) acc = fmaf(p[j], V[j * ld + f], acc);
+    C[i * ld + f] = acc;
+  }
+  __syncthreads();
+}
+
+// backward of attn_fwd_sample (nn.py:99-120): dS = P ⊙ (dP − Σ_j dP P)·scale
+// with dP = dC Vᵀ; dQ = dS K, dK = dSᵀ Q, dV = Pᵀ dC.  S: H·L·L scratch.
+__device__ __noinline__ void attn_bwd_sample(const float* Q, const float* K, const float* V,
+                                             int ld, const float* P, const float* dC,
+                                             float* dQ, float* dK, float* dV, float* S, int L,
+                                             int H, int dh, float scale) {
+  const int nt = blockDim.x, LL = L * L;
+  for (int e = threadIdx.x; e < H * LL; e += nt) {
+    const int h = e / LL, ij = e - h * LL, i = ij / L, j = ij - i * L;
+    const float* a = dC + i * ld + h * dh;
+    const float* b = V + j * ld + h * dh;
+    float s = 0.f;
+    if ((dh & 3) == 0) {
+      for (int c = 0; c < dh; c += 4) {
+        const float4 x = *reinterpret_cast<const float4*>(a + c);
+        const float4 y = *reinterpret_cast<const float4*>(b + c);
+        s = fmaf(x.x, y.x, fmaf(x.y, y.y, fmaf(x.z, y.z, fmaf(x.w, y.w, s))));
+      }
+    } else {
+      for (int c = 0; c < dh; ++c) s = fmaf(a[c], b[c], s);
+    }
+    S[e] = s;  // dP
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < H * L; e += nt) {
+    float* s = S + e * L;
+    const float* p = P + e * L;
+    float dot = 0.f;
+    for (int j = 0; j < L; ++j) dot = fmaf(s[j], p[j], dot);
+    for (int j = 0; j < L; ++j) s[j] = p[j] * (s[j] - dot) * scale;
+  }
+  __syncthreads();
+  const int D = H * dh;
+  for (int e = threadIdx.x; e < L * D; e += nt) {
+    const int r = e / D, f = e - r * D, h = f / dh;
+    const float* s = S + h * LL;
+    const float* p = P + h * LL;
+    float q = 0.f, k = 0.f, v = 0.f;
+    for (int j = 0; j < L; ++j) {
+      q = fmaf(s[r * L + j], K[j * ld + f], q);
+      k = fmaf(s[j * L + r], Q[j * ld + f], k);
+      v = fmaf(p[j * L + r], dC[j * ld + f], v);
+    }
+    dQ[r * ld + f] = q;
+    dK[r * ld + f] = k;
+    dV[r * ld + f] = v;
+  }
+  __syncthreads();
+}
+
 struct Ptrs {
   float *Q, *K, *V, *C, *X1, *X2, *F, *I1, *I2, *P;
 };
@@ -348,7 +447,7 @@ __global__ void __launch_bounds__(256) train_kernel(
       small_mm<false>(Hin, ld, W, ldw, L, d, d, Pw + lo.bk, false, nullptr, 0, c.K, ld, S);
       W = ws.acquire(&ldw);
       small_mm<false>(Hin, ld, W, ldw, L, d, d, Pw + lo.bv, false, nullptr, 0, c.V, ld, S);
-      attention_rows_nl(c.Q, c.K, c.V, ld, c.C, ld, 1, L, H, dh, scale, c.P);
+      attn_fwd_sample(c.Q, c.K, c.V, ld, c.C, L, H, dh, scale, c.P);
       W = ws.acquire(&ldw);  // (its barrier also orders the attention output)
       small_mm<false>(c.C, ld, W, ldw, L, d, d, Pw + lo.bo, false, Hin, ld, T1, ld, S);
       layernorm_rows_nl(T1, ld, T2, ld, L, d, Pw + lo.ln1g, Pw + lo.ln1b, c.X1, ld, c.I1);
@@ -511,7 +610,7 @@ __global__ void __launch_bounds__(256) train_kernel(
       colsum_rows_nl(dA, ld, L, d, G + lo.bo, fs, nullptr, 0);
       W = ws.acquire(&ldw);  // Wo: dC = dA W_oᵀ → dB
       small_mm<true>(dA, ld, W, ldw, L, d, d, nullptr, false, nullptr, 0, dB, ld, S);
-      attention_back_rows_nl(c.Q, c.K, c.V, ld, c.P, dB, ld, dQ, dK, dV, S, 1, L, H, dh, scale);
+      attn_bwd_sample(c.Q, c.K, c.V, ld, c.P, dB, dQ, dK, dV, S, L, H, dh, scale);
       const float* hin = H0;
       if (li > 0) {
         const LayerOff& lp = M.layer[li - 1];
