@@ -229,6 +229,10 @@ int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_params_t, fl
 int tpcb_cmd(const void* d_z, int32_t z_is_f64, int64_t ns, int64_t nt, int32_t de, int32_t k,
              double* d_value, double* d_grad, void* stream);
 
+/* debug: per-weight-op timestamps (clock64 pairs) of CTA 0 of the training
+ * kernel into d_trace[512] (NULL disables) — tools/trace_train.py */
+int tpcb_debug_train_trace(long long* d_trace);
+
 /* ---- measurement helpers (bench.py) -------------------------------------
  * FP32 FFMA throughput of this GPU in TFLOP/s (d_scratch: >= 1184 floats);
  * L2 flush by overwriting a caller buffer larger than L2. */

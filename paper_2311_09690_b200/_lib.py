@@ -95,6 +95,7 @@ SIGNATURES = {
                                C.POINTER(TrainWs), vp, vp, vp, vp, vp, vp]),
     "tpcb_graph_create": (i32, [C.POINTER(vp)]),
     "tpcb_probe_ffma": (i32, [vp, C.POINTER(f64), vp]),
+    "tpcb_debug_train_trace": (i32, [vp]),
     "tpcb_flush_l2": (i32, [vp, sz, vp]),
     "tpcb_graph_destroy": (None, [vp]),
 }

@@ -182,6 +182,13 @@ extern "C" int tpcb_optimizer_step(const tpcb_model* m, int64_t n, float* d_para
   return st;
 }
 
+namespace tpcb {
+int set_train_trace(long long* d_trace);
+}
+
+/* debug: per-op timestamps of CTA 0 of the training kernel (NULL disables) */
+extern "C" int tpcb_debug_train_trace(long long* d_trace) { return tpcb::set_train_trace(d_trace); }
+
 extern "C" int tpcb_graph_create(tpcb_graph** out) {
   if (!out) return TPCB_ERR_VALIDATION;
   *out = new tpcb_graph();

@@ -333,6 +333,10 @@ __device__ double decode_plain(double e, const tpcb_boxcox& n) {
 __device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
 
 // op-ahead weight prefetch over the entries of one sample
+// optional per-op timestamps of CTA 0 (tools/trace_train.py): pairs of
+// (clock64 at acquire entry, clock64 after its barrier) per weight entry
+__device__ long long* g_trace = nullptr;
+
 struct WStream {
   const Model* M;
   const float* P;
@@ -355,6 +359,9 @@ struct WStream {
   // Every caller must have passed a block barrier since the previous use of
   // the buffer being refilled.
   __device__ const float* acquire(int* ldw) {
+    long long* tr = g_trace;
+    const bool rec = tr != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && idx < 256;
+    if (rec) tr[2 * idx] = clock64();
     int K, N, off;
     entry_shape(*M, L, idx, &K, &N, &off);
     *ldw = stage_ld(N);
@@ -362,6 +369,7 @@ struct WStream {
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
+    if (rec) tr[2 * idx + 1] = clock64();
     return buf[(idx++) & 1];
   }
   __device__ void drain() {
@@ -642,6 +650,11 @@ __global__ void __launch_bounds__(256) train_kernel(
 }
 
 }  // namespace
+
+int set_train_trace(long long* d_trace) {
+  TPCB_CUDA_CHECK(cudaMemcpyToSymbol(g_trace, &d_trace, sizeof(d_trace)));
+  return TPCB_OK;
+}
 
 int prepare_train_kernels(const Model& M) {
   TrainPlan tp = make_train_plan(M);
