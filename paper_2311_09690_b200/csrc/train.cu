@@ -341,14 +341,15 @@ struct WStream {
   const Model* M;
   const float* P;
   float* buf[2];
-  int L, idx, n;
+  int L, idx, n, rep;
 
   __device__ void stage(int i) {
     int K, N, off;
     entry_shape(*M, L, i, &K, &N, &off);
     stage_matrix(P + off, K, N, buf[i & 1]);
   }
-  __device__ void begin(int L_, int n_) {
+  __device__ void begin(int L_, int n_, int rep_ = 0) {
+    rep = rep_;
     L = L_;
     n = n_;
     idx = 0;
@@ -360,8 +361,8 @@ struct WStream {
   // the buffer being refilled.
   __device__ const float* acquire(int* ldw) {
     long long* tr = g_trace;
-    const bool rec = tr != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && idx < 256;
-    if (rec) tr[2 * idx] = clock64();
+    const bool rec = tr != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && idx < 128 && rep < 2;
+    if (rec) tr[2 * idx + 256 * rep] = clock64();
     int K, N, off;
     entry_shape(*M, L, idx, &K, &N, &off);
     *ldw = stage_ld(N);
@@ -369,7 +370,7 @@ struct WStream {
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    if (rec) tr[2 * idx + 1] = clock64();
+    if (rec) tr[2 * idx + 1 + 256 * rep] = clock64();
     return buf[(idx++) & 1];
   }
   __device__ void drain() {
@@ -434,7 +435,8 @@ __global__ void __launch_bounds__(256) train_kernel(
     const SampleSetDev& set = is_t ? tgt : src;
     const int idx = batch[w];
     const int L = set.n_leaf[idx];
-    ws.begin(L, phase == 0 ? n_fwd_entries(M, L) : n_all_entries(M, L));
+    ws.begin(L, phase == 0 ? n_fwd_entries(M, L) : n_all_entries(M, L),
+             (w - (int)blockIdx.x) / (int)gridDim.x);
     const float* xr = set.x + (size_t)set.ast_row[idx] * TPCB_FEAT_PAD;
     for (int e = threadIdx.x; e < L * TPCB_FEAT; e += blockDim.x) {
       const int r = e / TPCB_FEAT, c = e - r * TPCB_FEAT;

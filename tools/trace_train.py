@@ -20,6 +20,8 @@ rag = engine.RaggedHost(rows=data.vectors.astype(np.float32), ordering=data.orde
                         encoded=False)
 loss = engine.loss_struct("hybrid", 1e-3, norm.loss_offset, 0.0, 5, "transformed", norm)
 tr = Trainer(cfg, pb.init_params(cfg).tensors, rag, y, loss, use_graph=False)
+if len(sys.argv) > 1:  # fewer gradient slots → several samples per CTA
+    tr.ws = engine.TrainWorkspace(tr.dm, int(sys.argv[1]))
 flat, steps = tr.plan(np.random.default_rng(0))
 tr.run_epoch(1e-3, flat, steps[:3].copy())
 tr.stream.synchronize()
@@ -30,18 +32,21 @@ for k in range(3, 8):
     buf.zero_()
     tr.run_epoch(1e-3, flat, steps[k:k + 1].copy())
     tr.stream.synchronize()
-    b = buf.cpu().numpy().reshape(-1, 2)
-    n = int(np.count_nonzero(b[:, 0]))
-    L = int(data.n_leaf[flat[steps[k][0]]])
-    t0 = b[0, 0]
-    rows = []
-    for i in range(n):
-        wait = b[i, 1] - b[i, 0]
-        work = (b[i + 1, 0] - b[i, 1]) if i + 1 < n else 0
-        rows.append((i, wait, work))
-    tot = b[n - 1, 1] - t0
-    print(f"step {k} L={L}: {n} ops, span {tot} cycles ({tot/1.965e3:.1f} us); wait sum {sum(r[1] for r in rows)}, work sum {sum(r[2] for r in rows)}")
-    if k == 3:
-        for r in rows:
-            print("   op %2d  wait %6d  work %6d" % r)
+    for rep in (0, 1):
+        b = buf.cpu().numpy()[256 * rep:256 * rep + 256].reshape(-1, 2)
+        n = int(np.count_nonzero(b[:, 0]))
+        if n == 0:
+            continue
+        L = int(data.n_leaf[flat[steps[k][0]]])
+        t0 = b[0, 0]
+        rows = []
+        for i in range(n):
+            wait = b[i, 1] - b[i, 0]
+            work = (b[i + 1, 0] - b[i, 1]) if i + 1 < n else 0
+            rows.append((i, wait, work))
+        tot = b[n - 1, 1] - t0
+        print(f"rep {rep} step {k} L={L}: {n} ops, span {tot} cycles ({tot/1.965e3:.1f} us); wait sum {sum(r[1] for r in rows)}, work sum {sum(r[2] for r in rows)}")
+        if k == 3 and rep == 1:
+            for r in rows:
+                print("   op %2d  wait %6d  work %6d" % r)
 lib.tpcb_debug_train_trace(None)
