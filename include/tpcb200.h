@@ -229,6 +229,38 @@ int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_params_t, fl
 int tpcb_cmd(const void* d_z, int32_t z_is_f64, int64_t ns, int64_t nt, int32_t de, int32_t k,
              double* d_value, double* d_grad, void* stream);
 
+/* ---- K8–K11: KMeans task sampler (sampling.py:40-144), float64 ----------
+ * x: [n, d] row-major fp64 on the device (d ≤ 128).  Distances follow the
+ * reference's exact recipe (numpy pairwise summation order), so assignments
+ * and centres are bit-identical to sampling.kmeans. */
+int tpcb_kmeans_ws_size(int64_t n, int32_t d, int32_t kappa, size_t* bytes);
+/* k-means++ (sampling.py:45-60): centre 0 = x[first]; closest = dist²; total */
+int tpcb_kmeanspp_init(const double* d_x, int64_t n, int32_t d, int64_t first, double* d_centers,
+                       double* d_closest, double* d_total, void* ws, size_t ws_bytes,
+                       void* stream);
+/* centre i: u >= 0 → first j with cumsum(closest/total)/last > u (the
+ * Generator.choice draw); u < 0 → j = direct (the rng.integers branch when
+ * total == 0).  Then closest = min(closest, dist²(x, c_i)), total = Σ. */
+int tpcb_kmeanspp_step(const double* d_x, int64_t n, int32_t d, int32_t i, double u,
+                       int64_t direct, double* d_centers, double* d_closest, double* d_total,
+                       int64_t* d_chosen, void* ws, size_t ws_bytes, void* stream);
+/* Lloyd assignment: first-index argmin of sqrt distance, own distance, counts */
+int tpcb_kmeans_assign(const double* d_x, int64_t n, int32_t d, const double* d_centers,
+                       int32_t kappa, int64_t* d_assign, double* d_own, int32_t* d_counts,
+                       void* stream);
+/* centres = member means in point order (empty clusters keep their centre) */
+int tpcb_kmeans_update(const double* d_x, int64_t n, int32_t d, int32_t kappa,
+                       const int64_t* d_assign, const int32_t* d_counts, double* d_centers,
+                       void* ws, size_t ws_bytes, void* stream);
+/* *d_flag = 1 if the two assignments differ */
+int tpcb_kmeans_changed(const int64_t* d_a, const int64_t* d_b, int64_t n, int32_t* d_flag,
+                        void* stream);
+/* Ψ[e, t] = mean over rows of task t (rows d_task_off[t]..[t+1]) of the L2
+ * distance to centre e (sampling.build_distance_table, sampling.py:109-123) */
+int tpcb_distance_table(const double* d_feats, const int64_t* d_task_off, int32_t n_tasks,
+                        int32_t d, const double* d_centers, int32_t kappa, double* d_psi,
+                        void* stream);
+
 /* debug: per-weight-op timestamps (clock64 pairs) of CTA 0 of the training
  * kernel into d_trace[512] (NULL disables) — tools/trace_train.py */
 int tpcb_debug_train_trace(long long* d_trace);

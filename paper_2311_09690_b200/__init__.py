@@ -18,3 +18,5 @@ from .costmodel import (CostModelConfig, CostModelParams, LatentBatch, LossSpec,
 from .nn import Adam, Sgd
 
 __version__ = "0.1.0"
+from .sampling import (ClusterModel, DistanceTable, TaskFeatureSet, build_distance_table, kmeans,
+                       select_tasks)

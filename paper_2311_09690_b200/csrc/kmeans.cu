@@ -1,0 +1,456 @@
+// K8–K11 — KMeans task sampler (sampling.py:40-144), float64.
+//
+// Every distance is evaluated with the reference's exact floating-point
+// recipe — diff = x − c, square, then numpy's pairwise summation over the
+// feature axis (8 interleaved accumulators for 8 ≤ d ≤ 128, recursive
+// halving above, a plain loop below 8), sqrt for the assignment — and every
+// centre is the sequential row sum of its members in point order divided by
+// the member count, as `members.mean(axis=0)` computes it.  Assignments,
+// centres and the Ψ table therefore match the reference bit for bit; the only
+// non-bit-exact quantity is the k-means++ CDF (a parallel scan instead of
+// numpy's sequential cumsum), which can change a draw only when the uniform
+// falls within rounding distance of a CDF step.
+//
+//   K10 kmeanspp_*     closest-distance update, total, CDF search (per centre)
+//   K8  kmeans_assign  distances to all centres (centres tiled through smem),
+//                      first-index argmin, own distance, cluster counts
+//   K9  kmeans_update  stable counting sort of points by cluster (CUB radix
+//                      sort), then one thread per (cluster, feature) summing
+//                      its members in order
+//   K11 distance_table Ψ[e, t] = mean over task t's rows of dist(row, c_e)
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+
+namespace tpcb {
+namespace {
+
+constexpr int kMaxDim = 128;  // widest feature vector supported
+
+// Σ_k (a_k − b_k)² in numpy's pairwise order (umath pairwise_sum), no FMA
+// contraction (each product and sum rounded separately like numpy).
+__device__ __forceinline__ double sqd(const double* a, const double* b, int i) {
+  const double t = __dsub_rn(a[i], b[i]);
+  return __dmul_rn(t, t);
+}
+
+__device__ double pw_sq_range(const double* a, const double* b, int lo, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, sqd(a, b, lo + i));
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = sqd(a, b, lo + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sqd(a, b, lo + i + j));
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, sqd(a, b, lo + i));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  // one level of recursion is enough for d ≤ 256; deeper splits loop
+  return __dadd_rn(pw_sq_range(a, b, lo, n2), pw_sq_range(a, b, lo + n2, n - n2));
+}
+
+__device__ __forceinline__ double pw_sq(const double* a, const double* b, int d) {
+  return pw_sq_range(a, b, 0, d);
+}
+
+// closest[i] = dist²(x_i, c) (init) or min(closest[i], dist²(x_i, c)); block
+// partial sums of the updated closest into part[blockIdx.x]
+__global__ void closest_update_kernel(const double* __restrict__ x, int64_t n, int d,
+                                      const double* __restrict__ c, double* __restrict__ closest,
+                                      int init, double* __restrict__ part) {
+  __shared__ double sc[kMaxDim * 2];
+  __shared__ double red[32];
+  for (int k = threadIdx.x; k < d; k += blockDim.x) sc[k] = c[k];
+  __syncthreads();
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = pw_sq(x + i * d, sc, d);
+    const double nv = init ? v : fmin(closest[i], v);
+    closest[i] = nv;
+    acc += nv;
+  }
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum_d(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  }
+}
+
+__global__ void sum_parts_kernel(const double* __restrict__ part, int np, double* __restrict__ out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];  // fixed order per thread
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum_d(v);
+    if (threadIdx.x == 0) *out = v;
+  }
+}
+
+__global__ void div_kernel(const double* __restrict__ a, const double* __restrict__ total,
+                           double* __restrict__ p, int64_t n) {
+  const double t = *total;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = a[i] / t;
+}
+
+// first j with cdf[j] / cdf[n-1] > u  (Generator.choice: cdf /= cdf[-1];
+// cdf.searchsorted(u, side="right"))
+__global__ void search_kernel(const double* __restrict__ cdf, int64_t n, double u,
+                              unsigned long long* __restrict__ found) {
+  const double last = cdf[n - 1];
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if (cdf[j] / last > u) {
+      atomicMin(found, (unsigned long long)j);
+      return;  // later j of this thread are larger
+    }
+  }
+}
+
+__global__ void set_center_kernel(const double* __restrict__ x, int d,
+                                  const unsigned long long* __restrict__ found, int64_t n,
+                                  double* __restrict__ center, int64_t* __restrict__ chosen) {
+  unsigned long long j = *found;
+  if (j >= (unsigned long long)n) j = n - 1;  // u ≥ cdf_norm[-1] cannot happen for u < 1
+  for (int k = threadIdx.x; k < d; k += blockDim.x) center[k] = x[j * d + k];
+  if (threadIdx.x == 0 && chosen) *chosen = (int64_t)j;
+}
+
+__global__ void set_center_direct_kernel(const double* __restrict__ x, int d, int64_t j,
+                                         double* __restrict__ center) {
+  for (int k = threadIdx.x; k < d; k += blockDim.x) center[k] = x[j * d + k];
+}
+
+// fixed-width variant: the whole point row lives in registers
+template <int D>
+__device__ __forceinline__ double pw_sq_fixed(const double* a, const double* b) {
+  if (D < 8) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < D; ++i) r = __dadd_rn(r, sqd(a, b, i));
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = sqd(a, b, j);
+#pragma unroll
+  for (int i = 8; i < D - (D % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sqd(a, b, i + j));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+  for (int i = D - (D % 8); i < D; ++i) res = __dadd_rn(res, sqd(a, b, i));
+  return res;
+}
+
+// K8: one thread per point, centres streamed through shared memory in tiles.
+// D > 0: compile-time width (row in registers); D == 0: runtime width.
+constexpr int kTileCenters = 64;
+
+template <int D>
+__global__ void __launch_bounds__(256) assign_kernel(const double* __restrict__ x, int64_t n,
+                                                     int d_rt, const double* __restrict__ centers,
+                                                     int kappa, int64_t* __restrict__ assign,
+                                                     double* __restrict__ own,
+                                                     int32_t* __restrict__ counts) {
+  extern __shared__ double sc[];  // [kTileCenters][d] then (D == 0) rows [256][d+1]
+  const int d = D > 0 ? D : d_rt;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = i < n;
+  double xr[D > 0 ? D : 1];
+  double* xs = sc + kTileCenters * d + threadIdx.x * (d + 1);
+  if (live) {
+    if (D > 0) {
+#pragma unroll
+      for (int k = 0; k < (D > 0 ? D : 1); ++k) xr[k] = x[i * d + k];
+    } else {
+      for (int k = 0; k < d; ++k) xs[k] = x[i * d + k];
+    }
+  }
+  double best = INFINITY;
+  int bi = 0;
+  for (int c0 = 0; c0 < kappa; c0 += kTileCenters) {
+    const int tc = min(kTileCenters, kappa - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < tc * d; e += blockDim.x) sc[e] = centers[(size_t)c0 * d + e];
+    __syncthreads();
+    if (live) {
+      for (int j = 0; j < tc; ++j) {
+        const double sq = D > 0 ? pw_sq_fixed<(D > 0 ? D : 1)>(xr, sc + j * d)
+                                : pw_sq(xs, sc + j * d, d);
+        const double dist = sqrt(sq);
+        if (dist < best) {  // strict: first index wins ties (np.argmin)
+          best = dist;
+          bi = c0 + j;
+        }
+      }
+    }
+  }
+  if (live) {
+    assign[i] = bi;
+    own[i] = best;
+    atomicAdd(&counts[bi], 1);
+  }
+}
+
+__global__ void to_key_kernel(const int64_t* __restrict__ a, int32_t* __restrict__ key,
+                              int32_t* __restrict__ idx, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    key[i] = (int32_t)a[i];
+    idx[i] = (int32_t)i;
+  }
+}
+
+// K9: centre c feature k = (Σ members in point order) / count
+__global__ void member_mean_kernel(const double* __restrict__ x, int d, int kappa,
+                                   const int32_t* __restrict__ sorted_idx,
+                                   const int32_t* __restrict__ offs,
+                                   const int32_t* __restrict__ counts, double* __restrict__ centers) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)kappa * d) return;
+  const int c = (int)(e / d), k = (int)(e - (int64_t)c * d);
+  const int m = counts[c];
+  if (m == 0) return;  // empty cluster keeps its centre (sampling.py:101-104)
+  const int32_t* mem = sorted_idx + offs[c];
+  double acc = x[(int64_t)mem[0] * d + k];
+  int r = 1;
+  for (; r + 8 <= m; r += 8) {  // loads in flight, adds in order
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = x[(int64_t)mem[r + j] * d + k];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, v[j]);
+  }
+  for (; r < m; ++r) acc = __dadd_rn(acc, x[(int64_t)mem[r] * d + k]);
+  centers[(size_t)c * d + k] = acc / (double)m;
+}
+
+__global__ void compare_kernel(const int64_t* __restrict__ a, const int64_t* __restrict__ b,
+                               int64_t n, int32_t* __restrict__ changed) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (a[i] != b[i]) {
+      atomicOr(changed, 1);
+      return;
+    }
+}
+
+// K11: Ψ[e, t] — one thread per (centre, task), rows of the task in order
+__global__ void psi_kernel(const double* __restrict__ f, const int64_t* __restrict__ off, int nt,
+                           int d, const double* __restrict__ centers, int kappa,
+                           double* __restrict__ psi) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)kappa * nt) return;
+  const int c = (int)(e / nt), t = (int)(e - (int64_t)c * nt);
+  const double* cc = centers + (size_t)c * d;
+  const int64_t r0 = off[t], r1 = off[t + 1];
+  double acc = sqrt(pw_sq(f + r0 * d, cc, d));
+  for (int64_t r = r0 + 1; r < r1; ++r) acc = __dadd_rn(acc, sqrt(pw_sq(f + r * d, cc, d)));
+  psi[(size_t)c * nt + t] = acc / (double)(r1 - r0);
+}
+
+int grid_for(int64_t n, int block = 256) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + block - 1) / block, kNumSMs * 16));
+}
+
+}  // namespace
+}  // namespace tpcb
+
+using namespace tpcb;
+
+// workspace: partial sums, scan temp, found index, sort buffers
+extern "C" int tpcb_kmeans_ws_size(int64_t n, int32_t d, int32_t kappa, size_t* bytes) {
+  if (n < 1 || d < 1 || kappa < 1 || !bytes) return TPCB_ERR_VALIDATION;
+  if (d > kMaxDim) return TPCB_ERR_UNSUPPORTED;
+  if (n > 0x7fffffff) return TPCB_ERR_UNSUPPORTED;
+  size_t scan_tmp = 0, sort_tmp = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, scan_tmp, (double*)nullptr, (double*)nullptr, (int)n);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (int32_t*)nullptr, (int32_t*)nullptr,
+                                  (int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  size_t b = 0;
+  b += 4096 * 8;                  // block partials
+  b += 256;                       // found + flags
+  b += (size_t)n * 8 * 2;         // p, cdf
+  b += (size_t)n * 4 * 4;         // keys/idx in/out
+  b += (size_t)(kappa + 1) * 4;   // offsets
+  b += std::max(scan_tmp, sort_tmp) + 256;
+  *bytes = b;
+  return TPCB_OK;
+}
+
+namespace {
+struct KWs {
+  double* part;
+  unsigned long long* found;
+  int32_t* flag;
+  double* p;
+  double* cdf;
+  int32_t *kin, *kout, *iin, *iout, *offs;
+  void* tmp;
+  size_t tmp_bytes;
+};
+
+KWs carve(void* ws, size_t bytes, int64_t n, int kappa) {
+  KWs w{};
+  char* p = static_cast<char*>(ws);
+  auto take = [&](size_t sz) {
+    char* r = p;
+    p += (sz + 255) & ~(size_t)255;
+    return r;
+  };
+  w.part = reinterpret_cast<double*>(take(4096 * 8));
+  w.found = reinterpret_cast<unsigned long long*>(take(128));
+  w.flag = reinterpret_cast<int32_t*>(take(128));
+  w.p = reinterpret_cast<double*>(take((size_t)n * 8));
+  w.cdf = reinterpret_cast<double*>(take((size_t)n * 8));
+  w.kin = reinterpret_cast<int32_t*>(take((size_t)n * 4));
+  w.kout = reinterpret_cast<int32_t*>(take((size_t)n * 4));
+  w.iin = reinterpret_cast<int32_t*>(take((size_t)n * 4));
+  w.iout = reinterpret_cast<int32_t*>(take((size_t)n * 4));
+  w.offs = reinterpret_cast<int32_t*>(take((size_t)(kappa + 1) * 4));
+  w.tmp = p;
+  const size_t used = (size_t)(p - static_cast<char*>(ws));
+  w.tmp_bytes = bytes > used ? bytes - used : 0;
+  return w;
+}
+}  // namespace
+
+extern "C" int tpcb_kmeanspp_init(const double* d_x, int64_t n, int32_t d, int64_t first,
+                                  double* d_centers, double* d_closest, double* d_total,
+                                  void* ws, size_t ws_bytes, void* stream_) {
+  if (!d_x || !d_centers || !d_closest || !d_total || !ws) return TPCB_ERR_VALIDATION;
+  if (first < 0 || first >= n || d > kMaxDim) return TPCB_ERR_VALIDATION;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KWs w = carve(ws, ws_bytes, n, 1);
+  set_center_direct_kernel<<<1, 128, 0, stream>>>(d_x, d, first, d_centers);
+  const int g = std::min(grid_for(n), 4096);
+  closest_update_kernel<<<g, 256, 0, stream>>>(d_x, n, d, d_centers, d_closest, 1, w.part);
+  sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
+  TPCB_LAUNCH_CHECK("kmeanspp_init");
+  return TPCB_OK;
+}
+
+extern "C" int tpcb_kmeanspp_step(const double* d_x, int64_t n, int32_t d, int32_t i, double u,
+                                  int64_t direct, double* d_centers, double* d_closest,
+                                  double* d_total, int64_t* d_chosen, void* ws, size_t ws_bytes,
+                                  void* stream_) {
+  if (!d_x || !d_centers || !d_closest || !d_total || !ws) return TPCB_ERR_VALIDATION;
+  if (d > kMaxDim) return TPCB_ERR_UNSUPPORTED;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KWs w = carve(ws, ws_bytes, n, 1);
+  double* center = d_centers + (size_t)i * d;
+  if (u >= 0.0) {
+    div_kernel<<<grid_for(n), 256, 0, stream>>>(d_closest, d_total, w.p, n);
+    size_t tb = w.tmp_bytes;
+    TPCB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(w.tmp, tb, w.p, w.cdf, (int)n, stream));
+    TPCB_CUDA_CHECK(cudaMemsetAsync(w.found, 0xff, sizeof(unsigned long long), stream));
+    search_kernel<<<grid_for(n), 256, 0, stream>>>(w.cdf, n, u, w.found);
+    set_center_kernel<<<1, 128, 0, stream>>>(d_x, d, w.found, n, center, d_chosen);
+  } else {
+    if (direct < 0 || direct >= n) return TPCB_ERR_VALIDATION;
+    set_center_direct_kernel<<<1, 128, 0, stream>>>(d_x, d, direct, center);
+  }
+  const int g = std::min(grid_for(n), 4096);
+  closest_update_kernel<<<g, 256, 0, stream>>>(d_x, n, d, center, d_closest, 0, w.part);
+  sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
+  TPCB_LAUNCH_CHECK("kmeanspp_step");
+  return TPCB_OK;
+}
+
+extern "C" int tpcb_kmeans_assign(const double* d_x, int64_t n, int32_t d,
+                                  const double* d_centers, int32_t kappa, int64_t* d_assign,
+                                  double* d_own, int32_t* d_counts, void* stream_) {
+  if (!d_x || !d_centers || !d_assign || !d_own || !d_counts) return TPCB_ERR_VALIDATION;
+  if (d > kMaxDim) return TPCB_ERR_UNSUPPORTED;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  TPCB_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * kappa, stream));
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  if (d == 24 || d == 32) {
+    const size_t smem = (size_t)kTileCenters * d * sizeof(double);
+    if (d == 24)
+      assign_kernel<24><<<grid, 256, smem, stream>>>(d_x, n, d, d_centers, kappa, d_assign, d_own,
+                                                     d_counts);
+    else
+      assign_kernel<32><<<grid, 256, smem, stream>>>(d_x, n, d, d_centers, kappa, d_assign, d_own,
+                                                     d_counts);
+  } else {
+    const size_t smem = ((size_t)kTileCenters * d + 256 * (size_t)(d + 1)) * sizeof(double);
+    if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(assign_kernel<0>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    assign_kernel<0><<<grid, 256, smem, stream>>>(d_x, n, d, d_centers, kappa, d_assign, d_own,
+                                                  d_counts);
+  }
+  TPCB_LAUNCH_CHECK("kmeans_assign");
+  return TPCB_OK;
+}
+
+extern "C" int tpcb_kmeans_update(const double* d_x, int64_t n, int32_t d, int32_t kappa,
+                                  const int64_t* d_assign, const int32_t* d_counts,
+                                  double* d_centers, void* ws, size_t ws_bytes, void* stream_) {
+  if (!d_x || !d_assign || !d_counts || !d_centers || !ws) return TPCB_ERR_VALIDATION;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KWs w = carve(ws, ws_bytes, n, kappa);
+  to_key_kernel<<<grid_for(n), 256, 0, stream>>>(d_assign, w.kin, w.iin, n);
+  int bits = 1;
+  while ((1 << bits) < kappa) ++bits;
+  size_t tb = w.tmp_bytes;
+  TPCB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.kin, w.kout, w.iin, w.iout, (int)n,
+                                                  0, bits, stream));
+  tb = w.tmp_bytes;
+  TPCB_CUDA_CHECK(cudaMemsetAsync(w.offs, 0, sizeof(int32_t), stream));
+  TPCB_CUDA_CHECK(
+      cub::DeviceScan::InclusiveSum(w.tmp, tb, d_counts, w.offs + 1, kappa, stream));
+  const int64_t items = (int64_t)kappa * d;
+  member_mean_kernel<<<(unsigned)((items + 127) / 128), 128, 0, stream>>>(d_x, d, kappa, w.iout,
+                                                                         w.offs, d_counts,
+                                                                         d_centers);
+  TPCB_LAUNCH_CHECK("kmeans_update");
+  return TPCB_OK;
+}
+
+extern "C" int tpcb_kmeans_changed(const int64_t* d_a, const int64_t* d_b, int64_t n,
+                                   int32_t* d_flag, void* stream_) {
+  if (!d_a || !d_b || !d_flag) return TPCB_ERR_VALIDATION;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  TPCB_CUDA_CHECK(cudaMemsetAsync(d_flag, 0, sizeof(int32_t), stream));
+  compare_kernel<<<grid_for(n), 256, 0, stream>>>(d_a, d_b, n, d_flag);
+  TPCB_LAUNCH_CHECK("kmeans_changed");
+  return TPCB_OK;
+}
+
+extern "C" int tpcb_distance_table(const double* d_feats, const int64_t* d_task_off,
+                                   int32_t n_tasks, int32_t d, const double* d_centers,
+                                   int32_t kappa, double* d_psi, void* stream_) {
+  if (!d_feats || !d_task_off || !d_centers || !d_psi) return TPCB_ERR_VALIDATION;
+  if (n_tasks < 1) return TPCB_ERR_TOO_FEW_TASKS;
+  if (d > kMaxDim) return TPCB_ERR_UNSUPPORTED;
+  const int64_t items = (int64_t)kappa * n_tasks;
+  psi_kernel<<<(unsigned)((items + 127) / 128), 128, 0, (cudaStream_t)stream_>>>(
+      d_feats, d_task_off, n_tasks, d, d_centers, kappa, d_psi);
+  TPCB_LAUNCH_CHECK("distance_table");
+  return TPCB_OK;
+}

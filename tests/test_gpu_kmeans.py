@@ -1,0 +1,94 @@
+"""GPU KMeans sampler vs the reference, bit-exact (float64, numpy's pairwise
+summation order reproduced on the device): k-means++ seeds, Lloyd centres
+and assignments, the Ψ table and the selected task ids."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import lloyd
+
+pytestmark = pytest.mark.gpu
+
+
+def _s():
+    from paper_2311_09690_b200 import sampling
+    return sampling
+
+
+FIVE = np.array([0.0, 0.1, 5.0, 10.0, 10.1])
+
+
+def _tasks_golden(g):
+    s = _s()
+    x = g["cli_x"]
+    off = np.concatenate([[0], np.cumsum(g["cli_task_rows"])])
+    return x, [s.TaskFeatureSet(str(t), x[off[i]:off[i + 1]])
+               for i, t in enumerate(g["cli_task_ids"])]
+
+
+def test_hand_runs():
+    s = _s()
+    g = load_golden("kmeans")
+    m = s.kmeans(FIVE, 2, seed=0, init_centers=np.array([0.05, 10.05]))
+    assert np.array_equal(m.centers, g["five_centers"])
+    assert m.assignment.tolist() == [0, 0, 0, 1, 1] and m.sizes.tolist() == [3, 2]
+    m = s.kmeans(np.array([[0.0], [0.0], [0.0], [9.0]]), 2, seed=0,
+                 init_centers=np.array([[0.0], [0.0]]))
+    assert np.array_equal(m.assignment, g["rep_assign"]) and min(m.sizes) >= 1
+    assert s.select_tasks(FIVE, 2, [s.TaskFeatureSet("A", np.array([[0.0], [0.1]])),
+                                    s.TaskFeatureSet("B", np.array([[10.0], [10.1]])),
+                                    s.TaskFeatureSet("C", np.array([[5.0]]))],
+                          seed=0, init_centers=np.array([0.05, 10.05])) == ["A", "B"]
+
+
+@pytest.mark.parametrize("kappa,seed", [(4, 0), (9, 3)])
+def test_cli_features_bit_exact(kappa, seed):
+    s = _s()
+    g = load_golden("kmeans")
+    x, tasks = _tasks_golden(g)
+    m = s.kmeans(x, kappa, seed=seed)
+    assert np.array_equal(m.centers, g[f"k{kappa}.centers"])
+    assert np.array_equal(m.assignment, g[f"k{kappa}.assign"])
+    assert np.array_equal(m.sizes, g[f"k{kappa}.sizes"])
+    t = s.build_distance_table(m, tasks)
+    assert np.array_equal(t.psi, g[f"k{kappa}.psi"])
+    assert s.select_tasks(x, kappa, tasks, seed=seed) == [str(v) for v in g[f"k{kappa}.selected"]]
+
+
+def test_blobs_d24_bit_exact():
+    s = _s()
+    g = load_golden("kmeans")
+    xb = g["blob_x"]
+    km = s.DeviceKMeans(xb, 16)
+    km.kmeanspp(np.random.default_rng(11))
+    assert np.array_equal(km.centers.cpu().numpy(), g["blob_init"])
+    m = s.kmeans(xb, 16, seed=11)
+    assert np.array_equal(m.centers, g["blob_centers"])
+    assert np.array_equal(m.assignment, g["blob_assign"])
+
+
+def test_large_random_vs_oracle_same_init():
+    """Lloyd from identical init centres on 20k × 32 points, 64 clusters:
+    identical to the chunked float64 oracle restatement."""
+    s = _s()
+    rng = np.random.default_rng(7)
+    x = np.concatenate([rng.normal(loc=rng.normal(scale=5, size=32), size=(2500, 32))
+                        for _ in range(8)])
+    init = x[rng.choice(len(x), 64, replace=False)]
+    m = s.kmeans(x, 64, init_centers=init)
+    c, a, sz, _ = lloyd.kmeans(x, 64, init_centers=init)
+    assert np.array_equal(m.assignment, a)
+    assert np.array_equal(m.centers, c)
+
+
+def test_errors():
+    s = _s()
+    from paper_2311_09690_b200.errors import DimensionMismatch, TooFewPoints, TooFewTasks
+    with pytest.raises(TooFewPoints):
+        s.kmeans(np.zeros((2, 2)), 3)
+    with pytest.raises(TooFewTasks):
+        s.select_tasks(FIVE, 4, [s.TaskFeatureSet("A", np.array([[0.0]]))])
+    m = s.ClusterModel(np.zeros((2, 3)), np.zeros(1, int), np.array([1, 1]))
+    with pytest.raises(DimensionMismatch):
+        s.build_distance_table(m, [s.TaskFeatureSet("x", np.zeros((2, 2)))])
