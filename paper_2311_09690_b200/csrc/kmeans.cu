@@ -296,7 +296,7 @@ extern "C" int tpcb_kmeans_ws_size(int64_t n, int32_t d, int32_t kappa, size_t* 
   b += (size_t)n * 8 * 2;         // p, cdf
   b += (size_t)n * 4 * 4;         // keys/idx in/out
   b += (size_t)(kappa + 1) * 4;   // offsets
-  b += std::max(scan_tmp, sort_tmp) + 256;
+  b += std::max(scan_tmp, sort_tmp) + 16 * 256;  // + per-region 256-B alignment slack
   *bytes = b;
   return TPCB_OK;
 }
