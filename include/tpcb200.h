@@ -174,10 +174,14 @@ typedef struct {
   float* zall;          /* [max_rows * d_embed] */
   double* terms;        /* [max_rows * 2] */
   double* scalars;      /* [8]: [0] CMD value, [1] loss value */
+  int64_t zall_floats;  /* size of zall (global rows × d_embed) */
 } tpcb_train_ws;
 
-/* epoch plan: steps[s] = {offset into d_batch, n_src, n_tgt, 0} (int32 x4);
- * d_batch holds each step's source sample indices then its target indices */
+/* epoch plan: steps[s] = 8 × int32 {offset into d_batch, n_src, n_tgt,
+ * n_norm, src_pos, ns_glob, tgt_pos, nt_glob}: this rank's source / target
+ * counts, the batch size the loss is normalised by (the global batch under
+ * data parallelism) and where this rank's rows sit in the global [zs; zt]
+ * CMD matrix.  d_batch holds each step's source indices then target indices. */
 typedef struct {
   const int32_t* d_batch;
   const int32_t* d_steps;
@@ -203,6 +207,17 @@ int tpcb_loss_backward(const tpcb_model* m, const float* d_params, const float* 
 int tpcb_optimizer_step(const tpcb_model* m, int64_t n, float* d_params, float* d_params_t,
                         const float* d_grad, float* d_m, float* d_v, const tpcb_optim* opt,
                         double lr, int64_t t, void* stream);
+/* ---- data parallel: NCCL communicator (one process per GPU) --------------
+ * rank 0 creates the id, the host broadcasts it (torch.distributed), every
+ * rank creates its communicator; tpcb_train_epoch all-reduces each step's
+ * gradient (and the CMD latents) on the training stream. */
+typedef struct tpcb_comm tpcb_comm;
+int tpcb_nccl_unique_id(void* out, int32_t cap /* >= 128 */);
+int tpcb_nccl_comm_create(const void* id, int32_t nranks, int32_t rank, tpcb_comm** out);
+void tpcb_nccl_comm_destroy(tpcb_comm* c);
+int tpcb_nccl_allreduce_sum(tpcb_comm* c, void* d_buf, int64_t count, int32_t is_f64,
+                            void* stream);
+
 /* captured-epoch cache (a CUDA graph replayed while the arguments match) */
 typedef struct tpcb_graph tpcb_graph;
 int tpcb_graph_create(tpcb_graph** out);
@@ -215,13 +230,16 @@ void tpcb_graph_destroy(tpcb_graph* g);
  * graph handle the whole epoch is captured once and replayed (the stream
  * must then be a non-legacy stream).  prof_ms (host, [3], nullable) runs the
  * epoch uncaptured and returns the summed device time of the fwd/bwd kernels,
- * the reduce+optimizer kernels and the transpose kernels (synchronises). */
+ * the reduce+optimizer kernels and the transpose kernels (synchronises).
+ * comm (nullable): data-parallel communicator; then d_grad [param_count]
+ * receives the all-reduced gradient each step. */
 int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_params_t, float* d_m,
                      float* d_v, const tpcb_samples* src, const tpcb_samples* tgt,
                      const tpcb_plan* plan, const tpcb_loss* loss, const tpcb_optim* opt,
                      const double* d_lr, const int64_t* d_t0, const tpcb_train_ws* ws,
                      double* d_step_loss, double* d_step_cmd, int32_t* d_status,
-                     tpcb_graph* graph, double* prof_ms, void* stream);
+                     tpcb_graph* graph, double* prof_ms, tpcb_comm* comm, float* d_grad,
+                     void* stream);
 
 /* ---- K6: CMD between two sets (costmodel.cmd, costmodel.py:489-503) ------
  * d_z = [zs; zt] row-major [(ns+nt), de] (f32 or f64); value → d_value[0];

@@ -57,7 +57,7 @@ class Samples(C.Structure):
 
 class TrainWs(C.Structure):
     _fields_ = [("partial", vp), ("slot_stride", i64), ("n_slots", i32), ("touched", vp),
-                ("zall", vp), ("terms", vp), ("scalars", vp)]
+                ("zall", vp), ("terms", vp), ("scalars", vp), ("zall_floats", i64)]
 
 
 class Plan(C.Structure):
@@ -92,7 +92,11 @@ SIGNATURES = {
                                   vp]),
     "tpcb_train_epoch": (i32, [vp, vp, vp, vp, vp, C.POINTER(Samples), C.POINTER(Samples),
                                C.POINTER(Plan), C.POINTER(LossCfg), C.POINTER(OptimCfg), vp, vp,
-                               C.POINTER(TrainWs), vp, vp, vp, vp, vp, vp]),
+                               C.POINTER(TrainWs), vp, vp, vp, vp, vp, vp, vp, vp]),
+    "tpcb_nccl_unique_id": (i32, [vp, i32]),
+    "tpcb_nccl_comm_create": (i32, [vp, i32, i32, C.POINTER(vp)]),
+    "tpcb_nccl_comm_destroy": (None, [vp]),
+    "tpcb_nccl_allreduce_sum": (i32, [vp, vp, i64, i32, vp]),
     "tpcb_graph_create": (i32, [C.POINTER(vp)]),
     "tpcb_probe_ffma": (i32, [vp, C.POINTER(f64), vp]),
     "tpcb_debug_train_trace": (i32, [vp]),

@@ -25,8 +25,18 @@ BUILD = ROOT / "build" / "tpcb200"
 LIB = PKG / "libtpcb200.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_dir() -> Path:
+    """NCCL 2.28 shipped with torch (nvidia-nccl wheel), same image on every box."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("nvidia.nccl (torch's NCCL) not found")
+    return Path(list(spec.submodule_search_locations)[0])
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-              "--expt-relaxed-constexpr", "-Xptxas", "-v", f"-I{ROOT / 'include'}"]
+              "--expt-relaxed-constexpr", "-Xptxas", "-v", f"-I{ROOT / 'include'}",
+              f"-I{_nccl_dir() / 'include'}", "-diag-suppress", "128,177"]
 
 
 def nvcc() -> str:
@@ -64,7 +74,9 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             if log:
                 print(log, file=sys.stderr)
     if force or not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcuda"]
+        nccl_lib = _nccl_dir() / "lib"
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcuda",
+               f"-L{nccl_lib}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "dist.cuh"
 #include "train.cuh"
 
 using namespace tpcb;
@@ -53,6 +54,7 @@ TrainWs to_dev(const tpcb_train_ws* w) {
   d.zall = w->zall;
   d.terms = w->terms;
   d.scalars = w->scalars;
+  d.zall_bytes = 0;
   return d;
 }
 
@@ -91,29 +93,56 @@ struct StepProfiler {
 };
 thread_local StepProfiler* g_prof = nullptr;
 
-// one training step on an already uploaded step table
+// one training step on an already uploaded step table.  With a
+// communicator (data parallel): local fwd/bwd → local gradient sum into
+// `gbuf` → all-reduce(gradient, step loss) → optimizer from the gradient.
 int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
              const SampleSetDev& src, const SampleSetDev& tgt, const int32_t* batch,
-             const int4* steps, int step, int grid, const LossDev& loss, const OptDev& opt,
+             const StepDesc* steps, int step, int grid, const LossDev& loss, const OptDev& opt,
              const double* lr, const int64_t* t0, const TrainWs& ws, float* grad_out,
              double* step_loss, double* step_cmd, float* pred_out, int32_t* status,
-             cudaStream_t stream) {
+             cudaStream_t stream, tpcb_comm* comm = nullptr, float* gbuf = nullptr) {
+  (void)PT;
   int st;
+  const bool dp = comm != nullptr;  // (a 1-rank communicator exercises the same path)
   if (g_prof) g_prof->mark(stream);
   if (loss.use_cmd) {
+    if (dp) {  // every rank fills its own rows; the all-reduce assembles [zs; zt]
+      TPCB_CUDA_CHECK(cudaMemsetAsync(ws.zall, 0, ws.zall_bytes, stream));
+    }
     st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 0, ws, nullptr,
                       status, stream);
     if (st) return st;
+    if (dp) {
+      st = allreduce_sum(comm, ws.zall, (int64_t)(ws.zall_bytes / sizeof(float)), 0, stream);
+      if (st) return st;
+    }
   }
   st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 1, ws, pred_out,
                     status, stream);
   if (st) return st;
   if (g_prof) g_prof->mark(stream);
-  st = launch_reduce_apply(m->dev, ws, steps, step, loss.use_cmd, grad_out, P, mb, vb, opt, lr, t0,
-                           loss, step_loss, step_cmd, stream);
-  if (st) return st;
+  if (!dp) {
+    st = launch_reduce_apply(m->dev, ws, steps, step, loss.use_cmd, 1, grad_out, P, mb, vb, opt,
+                             lr, t0, loss, step_loss, step_cmd, stream);
+    if (st) return st;
+  } else {
+    OptDev none{};
+    st = launch_reduce_apply(m->dev, ws, steps, step, loss.use_cmd, comm->rank == 0, gbuf,
+                             nullptr, nullptr, nullptr, none, nullptr, nullptr, loss, step_loss,
+                             step_cmd, stream);
+    if (st) return st;
+    if ((st = group_start())) return st;
+    st = allreduce_sum(comm, gbuf, m->dev.total, 0, stream);
+    if (!st && step_loss) st = allreduce_sum(comm, step_loss + step, 1, 1, stream);
+    int st2 = group_end();
+    if (st || st2) return st ? st : st2;
+    if (opt.kind != kOptNone) {
+      st = launch_opt_from_grad(m->dev, gbuf, P, mb, vb, opt, lr, t0, step, stream);
+      if (st) return st;
+    }
+  }
   if (g_prof) g_prof->mark(stream);
-  // (the staged backward reads W with a transposed index: no transposed copy)
   if (g_prof) g_prof->mark(stream);
   return st;
 }
@@ -147,7 +176,7 @@ extern "C" int tpcb_loss_backward(const tpcb_model* m, const float* d_params,
                                   int32_t n_tgt, const tpcb_loss* loss, const tpcb_train_ws* ws,
                                   void* d_step_scratch_, float* d_grad, float* d_pred,
                                   int32_t* d_status, void* stream_) {
-  int4* d_step_scratch = static_cast<int4*>(d_step_scratch_);
+  StepDesc* d_step_scratch = static_cast<StepDesc*>(d_step_scratch_);
   if (!m || !d_params || !d_params_t || !src || !ws || !d_batch || !d_step_scratch)
     return TPCB_ERR_VALIDATION;
   if (n_src < 1) return TPCB_ERR_EMPTY_BATCH;
@@ -157,8 +186,10 @@ extern "C" int tpcb_loss_backward(const tpcb_model* m, const float* d_params,
   const LossDev ld = to_dev(loss, tgt != nullptr && n_tgt > 0);
   if (ld.use_cmd && !tgt) return TPCB_ERR_VALIDATION;
   const int n_all = n_src + (ld.use_cmd ? n_tgt : 0);
-  int4 h{0, n_src, ld.use_cmd ? n_tgt : 0, 0};
-  TPCB_CUDA_CHECK(cudaMemcpyAsync(d_step_scratch, &h, sizeof(int4), cudaMemcpyHostToDevice, stream));
+  const int nt = ld.use_cmd ? n_tgt : 0;
+  StepDesc h{0, n_src, nt, n_src, 0, n_src, 0, nt};
+  TPCB_CUDA_CHECK(
+      cudaMemcpyAsync(d_step_scratch, &h, sizeof(StepDesc), cudaMemcpyHostToDevice, stream));
   OptDev none{};
   TrainWs w = to_dev(ws);
   return run_step(m, const_cast<float*>(d_params), const_cast<float*>(d_params_t), nullptr, nullptr,
@@ -217,8 +248,10 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
                                 const tpcb_loss* loss, const tpcb_optim* opt, const double* d_lr,
                                 const int64_t* d_t0, const tpcb_train_ws* ws,
                                 double* d_step_loss, double* d_step_cmd, int32_t* d_status,
-                                tpcb_graph* graph, double* prof_ms, void* stream_) {
-  if (!m || !d_params || !d_params_t || !src || !plan || !opt || !ws) return TPCB_ERR_VALIDATION;
+                                tpcb_graph* graph, double* prof_ms, tpcb_comm* comm,
+                                float* d_grad, void* stream_) {
+  if (!m || !d_params || !src || !plan || !opt || !ws) return TPCB_ERR_VALIDATION;
+  if (comm && !d_grad) return TPCB_ERR_VALIDATION;
   int st = check_loss(loss);
   if (st) return st;
   if (plan->n_steps < 0) return TPCB_ERR_VALIDATION;
@@ -227,12 +260,12 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
   const OptDev od = to_dev(opt);
   const TrainWs w = to_dev(ws);
   const SampleSetDev s = to_dev(src), t = to_dev(tgt);
-  const int4* steps = reinterpret_cast<const int4*>(plan->d_steps);
+  const StepDesc* steps = reinterpret_cast<const StepDesc*>(plan->d_steps);
   auto enqueue = [&]() -> int {
     for (int k = 0; k < plan->n_steps; ++k) {
       int r = run_step(m, d_params, d_params_t, d_m, d_v, s, t, plan->d_batch, steps, k,
                        ws->n_slots, ld, od, d_lr, d_t0, w, nullptr, d_step_loss, d_step_cmd,
-                       nullptr, d_status, stream);
+                       nullptr, d_status, stream, comm, d_grad);
       if (r) return r;
     }
     return TPCB_OK;
@@ -273,6 +306,8 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
   key_add(key, d_step_loss);
   key_add(key, d_step_cmd);
   key_add(key, d_status);
+  key_add(key, comm);
+  key_add(key, d_grad);
   if (!graph->exec || graph->key != key) {
     if (graph->exec) {
       cudaGraphExecDestroy(graph->exec);

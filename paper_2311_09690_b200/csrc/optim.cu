@@ -29,15 +29,16 @@ __device__ __forceinline__ int region_bit(const Model& M, int p, const int* leaf
 __global__ void __launch_bounds__(256) reduce_apply_kernel(
     const __grid_constant__ Model M, const float* __restrict__ partial, size_t stride,
     const uint32_t* __restrict__ touched,
-    const int4* __restrict__ steps, int step, int n_slots, int use_cmd, float* __restrict__ grad_out,
+    const StepDesc* __restrict__ steps, int step, int n_slots, int use_cmd, int add_cmd,
+    float* __restrict__ grad_out,
     float* __restrict__ P, float* __restrict__ mbuf, float* __restrict__ vbuf, OptDev opt,
     const double* __restrict__ lr_p, const int64_t* __restrict__ t_p,
     const double* __restrict__ terms, const double* __restrict__ scalars, LossDev loss,
     double* __restrict__ step_loss, double* __restrict__ step_cmd) {
   __shared__ uint32_t s_touch[1024];
   __shared__ int s_leaf[TPCB_MAX_LEAF + 2];
-  const int4 sd = steps[step];
-  const int n_src = sd.y, n_tgt = sd.z;
+  const StepDesc sd = steps[step];
+  const int n_src = sd.n_src, n_tgt = sd.n_tgt;
   const int n_all = n_src + (use_cmd ? n_tgt : 0);
   const int G = min(n_all, n_slots);
   for (int c = threadIdx.x; c < G; c += blockDim.x) s_touch[c] = touched[c];
@@ -55,14 +56,14 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(
     sq = warp_sum_d(sq);
     rel = warp_sum_d(rel);
     if (threadIdx.x == 0 && step_loss) {
-      const double n = (double)n_src;
+      const double n = (double)sd.n_norm;
       double v = loss.mode == kLossMse ? sq / n
                  : loss.mode == kLossMape ? rel / n
                                           : sq / n + loss.lambda * (rel / n);
       double cmdv = 0.0;
       if (use_cmd) {
         cmdv = scalars[0];
-        v += loss.alpha * cmdv;
+        if (add_cmd) v += loss.alpha * cmdv;  // once across data-parallel ranks
       }
       step_loss[step] = v;
       if (step_cmd) step_cmd[step] = cmdv;
@@ -166,6 +167,34 @@ __global__ void optimizer_kernel(int n, const float* __restrict__ grad, float* _
   }
 }
 
+// Adam / SGD from a (data-parallel all-reduced) gradient vector; lr and the
+// step count before the epoch in device memory (graph replay across epochs)
+__global__ void opt_from_grad_kernel(int n, const float* __restrict__ grad, float* __restrict__ P,
+                                     float* __restrict__ mbuf, float* __restrict__ vbuf,
+                                     OptDev opt, const double* __restrict__ lr_p,
+                                     const int64_t* __restrict__ t_p, int step) {
+  const float lr = (float)lr_p[0];
+  const double t = (double)(t_p[0] + step + 1);
+  const float bc1 = (float)(1.0 - pow(opt.beta1, t)), bc2 = (float)(1.0 - pow(opt.beta2, t));
+  const float b1 = (float)opt.beta1, b2 = (float)opt.beta2, eps = (float)opt.eps,
+              wd = (float)opt.weight_decay;
+  const float omb1 = (float)(1.0 - opt.beta1), omb2 = (float)(1.0 - opt.beta2);
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    float g = grad[p], w = P[p];
+    if (wd != 0.f) g = g + wd * w;
+    if (opt.kind == kOptSgd) {
+      P[p] = w - lr * g;
+      continue;
+    }
+    float m = mbuf[p], v = vbuf[p];
+    m = __fadd_rn(__fmul_rn(m, b1), __fmul_rn(omb1, g));
+    v = __fadd_rn(__fmul_rn(v, b2), __fmul_rn(__fmul_rn(omb2, g), g));
+    mbuf[p] = m;
+    vbuf[p] = v;
+    P[p] = w - __fdiv_rn(__fmul_rn(lr, __fdiv_rn(m, bc1)), __fadd_rn(sqrtf(__fdiv_rn(v, bc2)), eps));
+  }
+}
+
 __global__ void transpose_kernel(const float* __restrict__ P, float* __restrict__ PT, T2Table tt) {
   const int total = tt.cum[tt.n];
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -186,16 +215,26 @@ __global__ void transpose_kernel(const float* __restrict__ P, float* __restrict_
 
 }  // namespace
 
-int launch_reduce_apply(const Model& M, const TrainWs& ws, const int4* steps, int step, int use_cmd,
-                        float* grad_out, float* P, float* m, float* v, const OptDev& opt,
-                        const double* lr, const int64_t* t, const LossDev& loss, double* step_loss,
-                        double* step_cmd, cudaStream_t stream) {
+int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps, int step,
+                        int use_cmd, int add_cmd, float* grad_out, float* P, float* m, float* v,
+                        const OptDev& opt, const double* lr, const int64_t* t,
+                        const LossDev& loss, double* step_loss, double* step_cmd,
+                        cudaStream_t stream) {
   const int grid = min(ceil_div(M.total / 4, 256), kNumSMs * 8);
   reduce_apply_kernel<<<grid, 256, 0, stream>>>(M, ws.partial, ws.slot_stride, ws.touched, steps,
-                                                step, ws.n_slots, use_cmd, grad_out, P, m, v, opt,
-                                                lr, t, ws.terms, ws.scalars, loss, step_loss,
-                                                step_cmd);
+                                                step, ws.n_slots, use_cmd, add_cmd, grad_out, P, m,
+                                                v, opt, lr, t, ws.terms, ws.scalars, loss,
+                                                step_loss, step_cmd);
   TPCB_LAUNCH_CHECK("reduce_apply");
+  return TPCB_OK;
+}
+
+int launch_opt_from_grad(const Model& M, const float* grad, float* P, float* m, float* v,
+                         const OptDev& opt, const double* lr, const int64_t* t, int step,
+                         cudaStream_t stream) {
+  const int grid = min(ceil_div(M.total, 256), kNumSMs * 8);
+  opt_from_grad_kernel<<<grid, 256, 0, stream>>>(M.total, grad, P, m, v, opt, lr, t, step);
+  TPCB_LAUNCH_CHECK("opt_from_grad");
   return TPCB_OK;
 }
 

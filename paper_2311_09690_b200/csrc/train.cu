@@ -381,16 +381,17 @@ struct WStream {
 
 __global__ void __launch_bounds__(256) train_kernel(
     const __grid_constant__ Model M, const float* __restrict__ Pw, SampleSetDev src, SampleSetDev tgt,
-    const int32_t* __restrict__ batch_all, const int4* __restrict__ steps, int step, LossDev loss,
+    const int32_t* __restrict__ batch_all, const StepDesc* __restrict__ steps, int step, LossDev loss,
     int phase, const __grid_constant__ TrainPlan tp, float* __restrict__ zall,
     float* __restrict__ partial,
     size_t slot_stride, uint32_t* __restrict__ touched, double* __restrict__ terms,
     double* __restrict__ scalars, float* __restrict__ pred_out, int32_t* status) {
   extern __shared__ __align__(16) float sm[];
-  const int4 sd = steps[step];
-  const int32_t* batch = batch_all + sd.x;
-  const int n_src = sd.y, n_tgt = sd.z;
+  const StepDesc sd = steps[step];
+  const int32_t* batch = batch_all + sd.off;
+  const int n_src = sd.n_src, n_tgt = sd.n_tgt;
   const int n_all = n_src + (loss.use_cmd ? n_tgt : 0);
+  const int ns_g = sd.ns_glob, nt_g = sd.nt_glob;
   const int ld = tp.ld, ldf = tp.ldf, d = M.d, H = M.n_heads, dh = M.dh, de = M.d_e;
   const float scale = 1.f / sqrtf((float)dh);
   float* G = partial + (size_t)blockIdx.x * slot_stride;
@@ -490,8 +491,10 @@ __global__ void __launch_bounds__(256) train_kernel(
     small_mm<false>(uall + uoff[nd], 0, W, ldw, 1, uw[nd], 1, Pw + M.outb, false, nullptr, 0,
                     misc, 0, S);
     const float pred = misc[0];
+    // row of this sample in the global [zs; zt] matrix
+    const int zrow = is_t ? ns_g + sd.tgt_pos + (w - n_src) : sd.src_pos + w;
     if (phase == 0) {
-      for (int e = threadIdx.x; e < de; e += blockDim.x) zall[(size_t)w * de + e] = uall[e];
+      for (int e = threadIdx.x; e < de; e += blockDim.x) zall[(size_t)zrow * de + e] = uall[e];
       ws.drain();
       continue;
     }
@@ -501,7 +504,7 @@ __global__ void __launch_bounds__(256) train_kernel(
       if (!is_t) {
         const double y = set.y[idx];
         const double dd = (double)pred - y;
-        const double n = (double)n_src;
+        const double n = (double)sd.n_norm;
         double rel = 0.0, relg = 0.0;
         if (loss.mode != kLossMse) {
           if (loss.original) {
@@ -559,11 +562,11 @@ __global__ void __launch_bounds__(256) train_kernel(
     }
     float* dz = du;
     if (loss.use_cmd) {
-      const double v = cmd_stats(zall, n_src, n_tgt, de, loss.cmd_order, cmds);
-      if (blockIdx.x == 0 && threadIdx.x == 0 && w == 0) scalars[0] = v;
+      const double v = cmd_stats(zall, ns_g, nt_g, de, loss.cmd_order, cmds);
+      if (blockIdx.x == 0 && threadIdx.x == 0 && w == (int)blockIdx.x) scalars[0] = v;
       for (int e = threadIdx.x; e < de; e += blockDim.x)
-        dz[e] += (float)(loss.alpha * cmd_grad_elem(cmds, n_src, n_tgt, de, loss.cmd_order, w, e,
-                                                    (double)zall[(size_t)w * de + e]));
+        dz[e] += (float)(loss.alpha * cmd_grad_elem(cmds, ns_g, nt_g, de, loss.cmd_order, zrow, e,
+                                                    (double)zall[(size_t)zrow * de + e]));
       __syncthreads();
     }
     float* dzx = sm + tp.dzx;
@@ -672,7 +675,7 @@ int prepare_train_kernels(const Model& M) {
 }
 
 int launch_train(const Model& M, const float* P, const float* PT, const SampleSetDev& src,
-                 const SampleSetDev& tgt, const int32_t* batch, const int4* steps, int step,
+                 const SampleSetDev& tgt, const int32_t* batch, const StepDesc* steps, int step,
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                  int32_t* status, cudaStream_t stream) {
   (void)PT;

@@ -10,6 +10,15 @@ constexpr double kCmdSupportFloor = 1e-6;  // costmodel.py:29
 enum { kLossHybrid = 0, kLossMse = 1, kLossMape = 2 };
 enum { kOptNone = 0, kOptAdam = 1, kOptSgd = 2 };
 
+// one optimizer step of an epoch plan (8 int32, host layout in training.py):
+// the step's sample indices are batch[off .. off+n_src+n_tgt); the loss is
+// normalised by n_norm (the global batch under data parallelism); z rows of
+// this rank's source/target samples sit at src_pos / ns_glob+tgt_pos of the
+// global [zs; zt] matrix the CMD statistics run over.
+struct StepDesc {
+  int off, n_src, n_tgt, n_norm, src_pos, ns_glob, tgt_pos, nt_glob;
+};
+
 struct OptDev {
   int kind;
   double beta1, beta2, eps, weight_decay;
@@ -54,19 +63,25 @@ struct TrainWs {
   float* zall;         // [max rows][d_embed]
   double* terms;       // [max src][2] per-sample (sq, rel)
   double* scalars;     // [8] cmd value, loss value, ...
+  size_t zall_bytes;   // size of zall (zeroed before phase 0 under data parallelism)
 };
 
 // steps[s] = {offset of step s in batch, n_src, n_tgt, 0}; batch holds the
 // source sample indices of the step followed by its target sample indices.
 int launch_train(const Model& M, const float* P, const float* PT, const SampleSetDev& src,
-                 const SampleSetDev& tgt, const int32_t* batch, const int4* steps, int step,
+                 const SampleSetDev& tgt, const int32_t* batch, const StepDesc* steps, int step,
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                  int32_t* status, cudaStream_t stream);
 int prepare_train_kernels(const Model& M);
-int launch_reduce_apply(const Model& M, const TrainWs& ws, const int4* steps, int step, int use_cmd,
-                        float* grad_out, float* P, float* m, float* v, const OptDev& opt,
-                        const double* lr, const int64_t* t, const LossDev& loss, double* step_loss,
-                        double* step_cmd, cudaStream_t stream);
+int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps, int step,
+                        int use_cmd, int add_cmd, float* grad_out, float* P, float* m, float* v,
+                        const OptDev& opt, const double* lr, const int64_t* t,
+                        const LossDev& loss, double* step_loss, double* step_cmd,
+                        cudaStream_t stream);
+// optimizer step from a reduced gradient with lr / step count in device memory
+int launch_opt_from_grad(const Model& M, const float* grad, float* P, float* m, float* v,
+                         const OptDev& opt, const double* lr, const int64_t* t, int step,
+                         cudaStream_t stream);
 int launch_transpose(const tpcb_model* m, const float* P, float* PT, cudaStream_t stream);
 int launch_optimizer(int n, const float* grad, float* P, float* m, float* v, const OptDev& opt,
                      double lr, double t, cudaStream_t stream);

@@ -287,11 +287,15 @@ class DeviceSamples:
 
 
 class TrainWorkspace:
-    def __init__(self, dm: DeviceModel, max_rows: int, device="cuda"):
+    """max_rows: samples this rank handles per step (gradient slots);
+    z_rows: rows of the global [zs; zt] CMD matrix (≥ max_rows)."""
+
+    def __init__(self, dm: DeviceModel, max_rows: int, device="cuda", z_rows: int = 0):
         lib = _lib.load()
         ns, stride, zf, tf = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
         _lib.check(lib.tpcb_train_ws_sizes(dm.handle, max_rows, C.byref(ns), C.byref(stride),
                                            C.byref(zf), C.byref(tf)), "train_ws_sizes")
+        zf = C.c_int64(max(zf.value, z_rows * dm.cfg.d_embed))
         self.max_rows = max_rows
         # zero-filled once: alignment padding between tensors is never written
         self.partial = torch.zeros(ns.value * stride.value, dtype=torch.float32, device=device)
@@ -304,6 +308,7 @@ class TrainWorkspace:
         w.partial, w.slot_stride, w.n_slots = self.partial.data_ptr(), stride.value, ns.value
         w.touched, w.zall = self.touched.data_ptr(), self.zall.data_ptr()
         w.terms, w.scalars = self.terms.data_ptr(), self.scalars.data_ptr()
+        w.zall_floats = self.zall.numel()
         self.struct = w
 
 
@@ -343,6 +348,7 @@ def run_backward(dm: DeviceModel, params: torch.Tensor, params_t: torch.Tensor,
                        torch.arange(n_tgt, dtype=torch.int32, device=dev)])
     grad = torch.empty(dm.n_params, dtype=torch.float32, device=dev)
     pred = torch.empty(n_src, dtype=torch.float32, device=dev)
+    ws.step_scratch = torch.zeros(8, dtype=torch.int32, device=dev)
     _lib.check(lib.tpcb_loss_backward(dm.handle, params.data_ptr(), params_t.data_ptr(),
                                       C.byref(src.struct),
                                       C.byref(tgt.struct) if tgt is not None else None,
@@ -360,3 +366,39 @@ def optimizer_step(dm: DeviceModel | None, params, params_t, grad, m, v, opt: _l
                                                params.numel(), params.data_ptr(), dptr(params_t),
                                                grad.data_ptr(), dptr(m), dptr(v), C.byref(opt),
                                                float(lr), int(t), stream_ptr()), "optimizer")
+
+
+class Comm:
+    """NCCL communicator (tpcb_comm) bootstrapped over an initialised
+    torch.distributed process group: rank 0's unique id is broadcast with
+    broadcast_object_list, then every rank joins."""
+
+    def __init__(self, rank: int, world: int, uid: bytes | None = None):
+        lib = _lib.load()
+        self.rank, self.world = rank, world
+        if uid is None:
+            import torch.distributed as dist
+            buf = C.create_string_buffer(128)
+            obj = [None]
+            if rank == 0:
+                _lib.check(lib.tpcb_nccl_unique_id(buf, 128), "nccl_unique_id")
+                obj = [bytes(buf.raw)]
+            if world > 1:
+                dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        self._uid = C.create_string_buffer(uid, 128)
+        h = C.c_void_p()
+        _lib.check(lib.tpcb_nccl_comm_create(self._uid, world, rank, C.byref(h)), "nccl_comm")
+        self.handle = h
+
+    @classmethod
+    def single(cls) -> "Comm":
+        lib = _lib.load()
+        buf = C.create_string_buffer(128)
+        _lib.check(lib.tpcb_nccl_unique_id(buf, 128), "nccl_unique_id")
+        return cls(0, 1, bytes(buf.raw))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.load().tpcb_nccl_comm_destroy(self.handle)
+            self.handle = None

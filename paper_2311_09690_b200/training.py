@@ -71,6 +71,40 @@ def epoch_batches(rng: np.random.Generator, n_leaves: np.ndarray, batch_size: in
     return [batches[i] for i in perm]
 
 
+def plan_epoch(rng: np.random.Generator, n_leaf: np.ndarray, batch_size: int, world: int = 1,
+               rank: int = 0, tgt_buckets: dict | None = None, n_tgt: int = 0):
+    """One epoch's batch plan for `rank` of `world` data-parallel ranks.
+
+    Every rank draws the same global plan — `epoch_batches` with
+    batch_size × world (costmodel.py:632-645) and, for fine-tuning, the
+    same-leaf-count target draw per batch (costmodel.py:762-766) — and keeps
+    its contiguous share (np.array_split) of each batch.  Returns (flat int32
+    sample indices, int32 [n_steps, 8] step table: offset, n_src, n_tgt,
+    n_norm = global batch, src_pos, ns_glob, tgt_pos, nt_glob)."""
+    gbs = batch_size * world
+    batches = epoch_batches(rng, n_leaf, gbs)
+    parts, steps, off = [], [], 0
+    for b in batches:
+        tsel = np.zeros(0, dtype=np.int64)
+        if tgt_buckets is not None:
+            pool = tgt_buckets.get(int(n_leaf[b[0]]))
+            if pool is None or len(pool) == 0:
+                pool = np.arange(n_tgt)
+            take = min(gbs, len(pool))
+            picked = rng.choice(len(pool), size=take, replace=False)
+            tsel = pool[np.sort(picked)]
+        sb = np.array_split(b, world)
+        st = np.array_split(tsel, world)
+        sp = int(sum(len(c) for c in sb[:rank]))
+        tp = int(sum(len(c) for c in st[:rank]))
+        parts.append(sb[rank])
+        parts.append(st[rank])
+        steps.append((off, len(sb[rank]), len(st[rank]), len(b), sp, len(b), tp, len(tsel)))
+        off += len(sb[rank]) + len(st[rank])
+    flat = np.concatenate(parts).astype(np.int32) if parts else np.zeros(0, np.int32)
+    return flat, np.asarray(steps, dtype=np.int32).reshape(-1, 8)
+
+
 class Trainer:
     """Training state resident on cuda:0 (or the current device)."""
 
@@ -78,7 +112,7 @@ class Trainer:
                  targets: np.ndarray, loss_struct, valid_rag: engine.RaggedHost | None = None,
                  valid_latency: np.ndarray | None = None, normalizer=None,
                  target_rag: engine.RaggedHost | None = None, device="cuda",
-                 use_graph: bool = True):
+                 use_graph: bool = True, comm: "engine.Comm | None" = None):
         from .costmodel import device_model
         self.config = config
         self.dm = device_model(config)
@@ -102,13 +136,20 @@ class Trainer:
             self.tgt_buckets = {k: np.asarray(v) for k, v in self.tgt_buckets.items()}
         self.loss = loss_struct
         self.opt = engine.optim_struct(config.optimizer, weight_decay=config.weight_decay)
+        # data parallel (weak scaling): every rank takes a contiguous share of
+        # each global batch of batch_size × world samples (the reference's
+        # semantics at that batch size); gradients all-reduced every step
+        self.comm = comm
+        self.world = comm.world if comm is not None else 1
+        self.rank = comm.rank if comm is not None else 0
         rows = config.batch_size * (2 if self.use_cmd else 1)
-        self.ws = engine.TrainWorkspace(self.dm, rows, device)
+        self.ws = engine.TrainWorkspace(self.dm, rows, device, z_rows=rows * self.world)
+        self.grad = torch.zeros_like(self.P) if comm is not None else None
         self.n_train = train_rag.n_ast
         self.n_leaf = np.asarray(train_rag.n_leaf)
         # plan buffers (fixed sizes: every epoch visits every training sample once)
         n_steps_max = int(sum(-(-int(c) // config.batch_size)
-                              for c in np.bincount(self.n_leaf)[1:]))
+                              for c in np.bincount(self.n_leaf)[1:]))  # ≥ global steps
         self.max_entries = self.n_train + (n_steps_max * config.batch_size if self.use_cmd else 0)
         self.batch_dev = torch.zeros(max(self.max_entries, 1), dtype=torch.int32, device=device)
         self.batch_host = torch.zeros(max(self.max_entries, 1), dtype=torch.int32).pin_memory()
@@ -146,26 +187,10 @@ class Trainer:
 
     # ------------------------------------------------------------ planning
     def plan(self, rng: np.random.Generator):
-        """Host batch plan of one epoch → (flat int32 sample list, steps table)."""
-        bs = self.config.batch_size
-        batches = epoch_batches(rng, self.n_leaf, bs)
-        parts, steps, off = [], [], 0
-        for b in batches:
-            tsel = np.zeros(0, dtype=np.int64)
-            if self.use_cmd:
-                L = int(self.n_leaf[b[0]])
-                pool = self.tgt_buckets.get(L)
-                if pool is None or len(pool) == 0:
-                    pool = np.arange(len(self.tgt_leaf))
-                take = min(bs, len(pool))
-                picked = rng.choice(len(pool), size=take, replace=False)
-                tsel = pool[np.sort(picked)]
-            parts.append(b)
-            parts.append(tsel)
-            steps.append((off, len(b), len(tsel), 0))
-            off += len(b) + len(tsel)
-        flat = np.concatenate(parts).astype(np.int32) if parts else np.zeros(0, np.int32)
-        return flat, np.asarray(steps, dtype=np.int32).reshape(-1, 4)
+        """Host batch plan of this rank for one epoch (see plan_epoch)."""
+        return plan_epoch(rng, self.n_leaf, self.config.batch_size, self.world, self.rank,
+                          self.tgt_buckets if self.use_cmd else None,
+                          len(self.tgt_leaf) if self.use_cmd else 0)
 
     # ------------------------------------------------------------ one epoch
     def run_epoch(self, lr: float, flat: np.ndarray, steps: np.ndarray, profile=None):
@@ -181,7 +206,7 @@ class Trainer:
         self.batch_host[:flat.size].copy_(torch.from_numpy(flat))
         self.batch_dev[:flat.size].copy_(self.batch_host[:flat.size], non_blocking=True)
         if self.steps_dev is None or self.steps_dev.shape[0] < n_steps:
-            self.steps_dev = torch.zeros((max(n_steps, 1), 4), dtype=torch.int32, device=self.dev)
+            self.steps_dev = torch.zeros((max(n_steps, 1), 8), dtype=torch.int32, device=self.dev)
             self.step_loss = torch.zeros(max(n_steps, 1), dtype=torch.float64, device=self.dev)
             self.step_cmd = torch.zeros(max(n_steps, 1), dtype=torch.float64, device=self.dev)
         self.steps_dev[:n_steps].copy_(torch.from_numpy(steps))
@@ -199,6 +224,8 @@ class Trainer:
             self.t0_dev.data_ptr(), C.byref(self.ws.struct), self.step_loss.data_ptr(),
             self.step_cmd.data_ptr(), self.status.ptr, self.graph,
             None if profile is None else profile.ctypes.data_as(C.c_void_p),
+            self.comm.handle if self.comm is not None else None,
+            self.grad.data_ptr() if self.grad is not None else None,
             engine.stream_ptr()), "train_epoch")
         self.t += n_steps
         return n_steps

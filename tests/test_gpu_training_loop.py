@@ -99,7 +99,7 @@ def test_steps_track_oracle_short_horizon():
     opt = ot.AdamState(T)
     off = data.offsets()
     want = []
-    for (o, n, _, _) in steps:
+    for (o, n, *_rest) in steps:
         b = flat[o:o + n]
         L = int(data.n_leaf[b[0]])
         x = np.stack([of.encode_rows(data.vectors[off[i]:off[i] + L],
@@ -128,7 +128,7 @@ def test_single_step_matches_oracle():
     tr.run_epoch(1e-3, flat, steps[:1].copy())
     got = tr.tensors()
     T = {k: v.copy() for k, v in params.tensors.items()}
-    o, n, _, _ = steps[0]
+    o, n = steps[0][:2]
     b = flat[o:o + n]
     L = int(data.n_leaf[b[0]])
     off = data.offsets()
@@ -210,3 +210,33 @@ def test_finetune_cmd_runs_and_is_deterministic():
     from paper_2311_09690_b200.errors import EmptyDataset
     with pytest.raises(EmptyDataset):
         pb.finetune(pre.params, ds, [], ft_cfg, devices(), pre.normalizer)
+
+
+def test_data_parallel_path_single_rank_matches():
+    """The data-parallel step (local gradient → NCCL all-reduce → optimizer
+    from the gradient) on a 1-rank communicator reproduces the fused
+    single-GPU step bit for bit, CMD included."""
+    pb = _pb()
+    from paper_2311_09690_b200 import engine
+    from paper_2311_09690_b200.training import Trainer
+    data, norm, y, dv, rag, loss = _oracle_setup(n=1024)
+    cfg = pb.desk_config(seed=0, alpha_cmd=1.0, d_model=16, d_ff=32, d_embed=8)
+    params = pb.init_params(cfg)
+    tgt = engine.RaggedHost(rows=rag.rows + 0.5, ordering=rag.ordering, n_leaf=rag.n_leaf,
+                            devfeat=rag.devfeat, encoded=False)
+    loss = engine.loss_struct("hybrid", 1e-3, norm.loss_offset, 1.0, 5, "transformed", norm)
+    comm = engine.Comm.single()
+    runs = []
+    for c in (None, comm):
+        tr = Trainer(cfg, params.tensors, rag, y, loss, target_rag=tgt, comm=c)
+        rng = np.random.default_rng(0)
+        for _ in range(2):
+            flat, steps = tr.plan(rng)
+            n = tr.run_epoch(1e-3, flat, steps)
+            losses, cmds, _ = tr.collect(n, 0)
+        runs.append((losses, cmds, tr.tensors()))
+    comm.close()
+    assert np.array_equal(runs[0][0], runs[1][0])
+    assert np.array_equal(runs[0][1], runs[1][1])
+    for k in runs[0][2]:
+        assert np.array_equal(runs[0][2][k], runs[1][2][k]), k

@@ -26,7 +26,7 @@ dm = op.Dims(64, 2, 2, 128, 32, 16, (64, 64), 16)
 opt = ot.AdamState(T)
 off = data.offsets()
 for s in range(NS):
-    o, n, _, _ = steps[s]
+    o, n = steps[s][:2]
     b = flat[o:o + n]
     L = int(data.n_leaf[b[0]])
     # device: one step
