@@ -16,6 +16,7 @@
 namespace tpcb {
 
 constexpr int kMaxRows = TPCB_MAX_LEAF;
+constexpr int kTrainThreads = 512;  // threads per training CTA
 
 __device__ __forceinline__ void cp_async4(float* dst, const float* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -82,7 +83,7 @@ __device__ __forceinline__ void mm_body(const float* A, int lda, const float* SW
                                         int C, const float* __restrict__ bias, bool relu,
                                         const float* Res, int ldr, float* out, int ldo,
                                         float* scratch) {
-  constexpr int NT = 256;
+  constexpr int NT = kTrainThreads;
   const int ldw = stage_ld(TRANS ? I : C);
   const bool vec = (I & 3) == 0 && (lda & 3) == 0;
   if (R * C >= 128 || I < 16) {

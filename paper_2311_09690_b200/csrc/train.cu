@@ -142,7 +142,7 @@ TrainPlan make_train_plan(const Model& M) {
   p.dflat = o; o += round4(M.d_e) + 4;
   p.misc = o; o += 8;
   // split-K partials of small_mm and the attention dS scratch share a region
-  p.S = o; o += max(256 * R, M.n_heads * R * R);
+  p.S = o; o += max(kTrainThreads * R, M.n_heads * R * R);
   o = (o + 1) & ~1;  // 8-byte align the fp64 CMD scratch
   p.cmd = o;
   p.cmd_cols = M.d_e;
@@ -379,7 +379,7 @@ struct WStream {
   }
 };
 
-__global__ void __launch_bounds__(256) train_kernel(
+__global__ void __launch_bounds__(kTrainThreads) train_kernel(
     const __grid_constant__ Model M, const float* __restrict__ Pw, SampleSetDev src, SampleSetDev tgt,
     const int32_t* __restrict__ batch_all, const StepDesc* __restrict__ steps, int step, LossDev loss,
     int phase, const __grid_constant__ TrainPlan tp, float* __restrict__ zall,
@@ -686,7 +686,7 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
   int st = prepare_train_kernels(M);
   if (st) return st;
   grid = std::max(1, std::min(grid, ws.n_slots));
-  train_kernel<<<grid, 256, smem, stream>>>(M, P, src, tgt, batch, steps, step, loss, phase, tp,
+  train_kernel<<<grid, kTrainThreads, smem, stream>>>(M, P, src, tgt, batch, steps, step, loss, phase, tp,
                                             ws.zall, ws.partial, ws.slot_stride, ws.touched,
                                             ws.terms, ws.scalars, pred_out, status);
   TPCB_LAUNCH_CHECK("train_kernel");
