@@ -175,6 +175,7 @@ typedef struct {
   double* terms;        /* [max_rows * 2] */
   double* scalars;      /* [8]: [0] CMD value, [1] loss value */
   int64_t zall_floats;  /* size of zall (global rows × d_embed) */
+  int32_t l_cap;        /* largest leaf count among the samples (≤ n_leaf_max) */
 } tpcb_train_ws;
 
 /* epoch plan: steps[s] = 8 × int32 {offset into d_batch, n_src, n_tgt,
@@ -188,7 +189,7 @@ typedef struct {
   int32_t n_steps;
 } tpcb_plan;
 
-int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t* n_slots,
+int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t l_cap, int32_t* n_slots,
                         int64_t* slot_stride, int64_t* zall_floats, int64_t* terms_doubles);
 /* refresh the transposed copy of every 2-D weight (read by the backward) */
 int tpcb_transpose_params(const tpcb_model* m, const float* d_params, float* d_params_t,

@@ -57,7 +57,8 @@ class Samples(C.Structure):
 
 class TrainWs(C.Structure):
     _fields_ = [("partial", vp), ("slot_stride", i64), ("n_slots", i32), ("touched", vp),
-                ("zall", vp), ("terms", vp), ("scalars", vp), ("zall_floats", i64)]
+                ("zall", vp), ("terms", vp), ("scalars", vp), ("zall_floats", i64),
+                ("l_cap", i32)]
 
 
 class Plan(C.Structure):
@@ -82,8 +83,8 @@ SIGNATURES = {
                            vp, vp, vp, vp]),
     "tpcb_metrics": (i32, [vp, vp, i64, vp, vp]),
     "tpcb_cmd": (i32, [vp, i32, i64, i64, i32, i32, vp, vp, vp]),
-    "tpcb_train_ws_sizes": (i32, [vp, i32, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64),
-                                  C.POINTER(i64)]),
+    "tpcb_train_ws_sizes": (i32, [vp, i32, i32, C.POINTER(i32), C.POINTER(i64),
+                                  C.POINTER(i64), C.POINTER(i64)]),
     "tpcb_transpose_params": (i32, [vp, vp, vp, vp]),
     "tpcb_loss_backward": (i32, [vp, vp, vp, C.POINTER(Samples), C.POINTER(Samples), vp, i32,
                                  i32, C.POINTER(LossCfg), C.POINTER(TrainWs), vp, vp, vp, vp,

@@ -55,6 +55,7 @@ TrainWs to_dev(const tpcb_train_ws* w) {
   d.terms = w->terms;
   d.scalars = w->scalars;
   d.zall_bytes = 0;
+  d.l_cap = w->l_cap;
   return d;
 }
 
@@ -149,8 +150,8 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
 
 }  // namespace
 
-extern "C" int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t* n_slots,
-                                   int64_t* slot_stride, int64_t* zall_floats,
+extern "C" int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t l_cap,
+                                   int32_t* n_slots, int64_t* slot_stride, int64_t* zall_floats,
                                    int64_t* terms_doubles) {
   if (!m || max_rows < 1) return TPCB_ERR_VALIDATION;
   const int slots = std::min<int32_t>(max_rows, 1024);
@@ -159,7 +160,7 @@ extern "C" int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_
   if (slot_stride) *slot_stride = ((int64_t)m->dev.total + 63) / 64 * 64;
   if (zall_floats) *zall_floats = (int64_t)max_rows * m->dev.d_e;
   if (terms_doubles) *terms_doubles = (int64_t)max_rows * 2;
-  TrainPlan tp = make_train_plan(m->dev);
+  TrainPlan tp = make_train_plan(m->dev, l_cap);
   if ((size_t)tp.total * sizeof(float) > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
   return TPCB_OK;
 }
@@ -313,7 +314,7 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
       cudaGraphExecDestroy(graph->exec);
       graph->exec = nullptr;
     }
-    st = prepare_train_kernels(m->dev);  // function attributes are set outside capture
+    st = prepare_train_kernels(m->dev, ws->l_cap);  // attributes are set outside capture
     if (st) return st;
     TPCB_CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     st = enqueue();

@@ -90,9 +90,9 @@ __host__ __device__ inline void entry_shape(const Model& M, int L, int idx, int*
   layer_mat(li, order[b % 6]);
 }
 
-TrainPlan make_train_plan(const Model& M) {
+TrainPlan make_train_plan(const Model& M, int l_cap) {
   TrainPlan p;
-  const int R = M.n_leaf_max;
+  const int R = (l_cap >= 1 && l_cap <= M.n_leaf_max) ? l_cap : M.n_leaf_max;
   p.R = R;
   p.ld = round4(M.d) + 4;
   p.ldf = round4(M.d_ff) + 4;
@@ -149,7 +149,7 @@ TrainPlan make_train_plan(const Model& M) {
   o += 2 * cmd_scratch_doubles(M.d_e) + 8;
   // weight stage: two buffers of the largest entry (ld = N + 1)
   int cap = 0;
-  for (int L = 1; L <= M.n_leaf_max; ++L) {
+  for (int L = 1; L <= R; ++L) {
     const int n = n_all_entries(M, L);
     for (int i = 0; i < n; ++i) {
       int K, N, off;
@@ -436,6 +436,10 @@ __global__ void __launch_bounds__(kTrainThreads) train_kernel(
     const SampleSetDev& set = is_t ? tgt : src;
     const int idx = batch[w];
     const int L = set.n_leaf[idx];
+    if (L < 1 || L > tp.R) {  // the plan was sized for the trainer's datasets
+      raise_status(status, TPCB_ERR_LEAF_COUNT);
+      continue;
+    }
     ws.begin(L, phase == 0 ? n_fwd_entries(M, L) : n_all_entries(M, L),
              (w - (int)blockIdx.x) / (int)gridDim.x);
     const float* xr = set.x + (size_t)set.ast_row[idx] * TPCB_FEAT_PAD;
@@ -661,8 +665,8 @@ int set_train_trace(long long* d_trace) {
   return TPCB_OK;
 }
 
-int prepare_train_kernels(const Model& M) {
-  TrainPlan tp = make_train_plan(M);
+int prepare_train_kernels(const Model& M, int l_cap) {
+  TrainPlan tp = make_train_plan(M, l_cap);
   const size_t smem = (size_t)tp.total * sizeof(float);
   if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
   static bool done = false;
@@ -679,11 +683,11 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                  int32_t* status, cudaStream_t stream) {
   (void)PT;
-  TrainPlan tp = make_train_plan(M);
+  TrainPlan tp = make_train_plan(M, ws.l_cap);
   const size_t smem = (size_t)tp.total * sizeof(float);
   if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
   if (loss.cmd_order > kMaxCmdOrder) return TPCB_ERR_UNSUPPORTED;
-  int st = prepare_train_kernels(M);
+  int st = prepare_train_kernels(M, ws.l_cap);
   if (st) return st;
   grid = std::max(1, std::min(grid, ws.n_slots));
   train_kernel<<<grid, kTrainThreads, smem, stream>>>(M, P, src, tgt, batch, steps, step, loss, phase, tp,

@@ -35,7 +35,7 @@ struct TrainPlan {
   int total;  // floats
 };
 
-TrainPlan make_train_plan(const Model& M);
+TrainPlan make_train_plan(const Model& M, int l_cap);
 
 // one dataset on the device (packed rows from K1 + per-sample data)
 struct SampleSetDev {
@@ -64,6 +64,7 @@ struct TrainWs {
   double* terms;       // [max src][2] per-sample (sq, rel)
   double* scalars;     // [8] cmd value, loss value, ...
   size_t zall_bytes;   // size of zall (zeroed before phase 0 under data parallelism)
+  int l_cap;           // largest leaf count of any sample (sizes the smem plan)
 };
 
 // steps[s] = {offset of step s in batch, n_src, n_tgt, 0}; batch holds the
@@ -72,7 +73,7 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
                  const SampleSetDev& tgt, const int32_t* batch, const StepDesc* steps, int step,
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                  int32_t* status, cudaStream_t stream);
-int prepare_train_kernels(const Model& M);
+int prepare_train_kernels(const Model& M, int l_cap);
 int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps, int step,
                         int use_cmd, int add_cmd, float* grad_out, float* P, float* m, float* v,
                         const OptDev& opt, const double* lr, const int64_t* t,

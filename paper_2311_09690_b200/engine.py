@@ -290,11 +290,14 @@ class TrainWorkspace:
     """max_rows: samples this rank handles per step (gradient slots);
     z_rows: rows of the global [zs; zt] CMD matrix (≥ max_rows)."""
 
-    def __init__(self, dm: DeviceModel, max_rows: int, device="cuda", z_rows: int = 0):
+    def __init__(self, dm: DeviceModel, max_rows: int, device="cuda", z_rows: int = 0,
+                 l_cap: int = 0):
         lib = _lib.load()
         ns, stride, zf, tf = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
-        _lib.check(lib.tpcb_train_ws_sizes(dm.handle, max_rows, C.byref(ns), C.byref(stride),
-                                           C.byref(zf), C.byref(tf)), "train_ws_sizes")
+        self.l_cap = int(l_cap) if l_cap else dm.cfg.n_leaf_max
+        _lib.check(lib.tpcb_train_ws_sizes(dm.handle, max_rows, self.l_cap, C.byref(ns),
+                                           C.byref(stride), C.byref(zf), C.byref(tf)),
+                   "train_ws_sizes")
         zf = C.c_int64(max(zf.value, z_rows * dm.cfg.d_embed))
         self.max_rows = max_rows
         # zero-filled once: alignment padding between tensors is never written
@@ -309,6 +312,7 @@ class TrainWorkspace:
         w.touched, w.zall = self.touched.data_ptr(), self.zall.data_ptr()
         w.terms, w.scalars = self.terms.data_ptr(), self.scalars.data_ptr()
         w.zall_floats = self.zall.numel()
+        w.l_cap = self.l_cap
         self.struct = w
 
 
@@ -349,6 +353,9 @@ def run_backward(dm: DeviceModel, params: torch.Tensor, params_t: torch.Tensor,
     grad = torch.empty(dm.n_params, dtype=torch.float32, device=dev)
     pred = torch.empty(n_src, dtype=torch.float32, device=dev)
     ws.step_scratch = torch.zeros(8, dtype=torch.int32, device=dev)
+    need = max(int(src.n_leaf_host.max()), int(tgt.n_leaf_host.max()) if tgt is not None else 1)
+    if need > ws.l_cap:
+        raise E.ValidationError("workspace sized for fewer leaves than the batch holds")
     _lib.check(lib.tpcb_loss_backward(dm.handle, params.data_ptr(), params_t.data_ptr(),
                                       C.byref(src.struct),
                                       C.byref(tgt.struct) if tgt is not None else None,

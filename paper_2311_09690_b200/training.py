@@ -143,7 +143,11 @@ class Trainer:
         self.world = comm.world if comm is not None else 1
         self.rank = comm.rank if comm is not None else 0
         rows = config.batch_size * (2 if self.use_cmd else 1)
-        self.ws = engine.TrainWorkspace(self.dm, rows, device, z_rows=rows * self.world)
+        l_cap = int(np.max(train_rag.n_leaf))
+        if target_rag is not None:
+            l_cap = max(l_cap, int(np.max(target_rag.n_leaf)))
+        self.ws = engine.TrainWorkspace(self.dm, rows, device, z_rows=rows * self.world,
+                                        l_cap=l_cap)
         self.grad = torch.zeros_like(self.P) if comm is not None else None
         self.n_train = train_rag.n_ast
         self.n_leaf = np.asarray(train_rag.n_leaf)
