@@ -361,16 +361,18 @@ struct WStream {
   // the buffer being refilled.
   __device__ const float* acquire(int* ldw) {
     long long* tr = g_trace;
-    const bool rec = tr != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && idx < 128 && rep < 2;
-    if (rec) tr[2 * idx + 256 * rep] = clock64();
+    const bool rec = tr != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && idx < 64 && rep < 2;
+    if (rec) tr[4 * idx + 256 * rep] = clock64();
     int K, N, off;
     entry_shape(*M, L, idx, &K, &N, &off);
     *ldw = stage_ld(N);
     if (idx + 1 < n) stage(idx + 1);
     cp_async_commit();
+    if (rec) tr[4 * idx + 1 + 256 * rep] = clock64();
     cp_async_wait<1>();
+    if (rec) tr[4 * idx + 2 + 256 * rep] = clock64();
     __syncthreads();
-    if (rec) tr[2 * idx + 1 + 256 * rep] = clock64();
+    if (rec) tr[4 * idx + 3 + 256 * rep] = clock64();
     return buf[(idx++) & 1];
   }
   __device__ void drain() {

@@ -33,7 +33,8 @@ for k in range(3, 8):
     tr.run_epoch(1e-3, flat, steps[k:k + 1].copy())
     tr.stream.synchronize()
     for rep in (0, 1):
-        b = buf.cpu().numpy()[256 * rep:256 * rep + 256].reshape(-1, 2)
+        b4 = buf.cpu().numpy()[256 * rep:256 * rep + 256].reshape(-1, 4)
+        b = b4[:, [0, 3]]
         n = int(np.count_nonzero(b[:, 0]))
         if n == 0:
             continue
@@ -46,7 +47,8 @@ for k in range(3, 8):
             rows.append((i, wait, work))
         tot = b[n - 1, 1] - t0
         print(f"rep {rep} step {k} L={L}: {n} ops, span {tot} cycles ({tot/1.965e3:.1f} us); wait sum {sum(r[1] for r in rows)}, work sum {sum(r[2] for r in rows)}")
-        if k == 3 and rep == 1:
-            for r in rows:
-                print("   op %2d  wait %6d  work %6d" % r)
+        if k == 3 and rep == 0:
+            for i, r in enumerate(rows):
+                print("   op %2d  wait %6d  work %6d   (issue %5d, cp.async wait %5d, barrier %5d)"
+                      % (r + (b4[i, 1] - b4[i, 0], b4[i, 2] - b4[i, 1], b4[i, 3] - b4[i, 2])))
 lib.tpcb_debug_train_trace(None)
