@@ -48,8 +48,8 @@ __host__ __device__ inline int n_all_entries(const Model& M, int L) {
   return n_fwd_entries(M, L) + M.n_dec + 1 + L + 6 * M.n_layers;
 }
 
-__host__ __device__ inline void entry_shape(const Model& M, int L, int idx, int* K, int* N,
-                                            int* off) {
+__host__ __device__ __noinline__ void entry_shape(const Model& M, int L, int idx, int* K, int* N,
+                                                  int* off) {
   const int nl = M.n_layers, nd = M.n_dec, d = M.d;
   auto dec_in = [&](int j) { return j == 0 ? M.d_e : M.dec[j - 1]; };
   const int nf = n_fwd_entries(M, L);
@@ -343,7 +343,7 @@ struct WStream {
   float* buf[2];
   int L, idx, n, rep;
 
-  __device__ void stage(int i) {
+  __device__ __noinline__ void stage(int i) {
     int K, N, off;
     entry_shape(*M, L, i, &K, &N, &off);
     stage_matrix(P + off, K, N, buf[i & 1]);
@@ -359,7 +359,7 @@ struct WStream {
   // staged copy of entry idx (row stride N+1); prefetches entry idx+1.
   // Every caller must have passed a block barrier since the previous use of
   // the buffer being refilled.
-  __device__ const float* acquire(int* ldw) {
+  __device__ __noinline__ const float* acquire(int* ldw) {
     long long* tr = g_trace;
     const bool rec = tr != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && idx < 64 && rep < 2;
     if (rec) tr[4 * idx + 256 * rep] = clock64();
