@@ -48,8 +48,8 @@ __host__ __device__ inline int n_all_entries(const Model& M, int L) {
   return n_fwd_entries(M, L) + M.n_dec + 1 + L + 6 * M.n_layers;
 }
 
-__host__ __device__ __noinline__ void entry_shape(const Model& M, int L, int idx, int* K, int* N,
-                                                  int* off) {
+__host__ __device__ inline void entry_shape(const Model& M, int L, int idx, int* K, int* N,
+                                            int* off) {
   const int nl = M.n_layers, nd = M.n_dec, d = M.d;
   auto dec_in = [&](int j) { return j == 0 ? M.d_e : M.dec[j - 1]; };
   const int nf = n_fwd_entries(M, L);
@@ -337,35 +337,37 @@ __device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.
 // (clock64 at acquire entry, clock64 after its barrier) per weight entry
 __device__ long long* g_trace = nullptr;
 
+constexpr int kMaxEntries = 256;
+
+// op-ahead weight prefetch over the entries of one sample.  The entry table
+// (rows, cols, offset of every weight matrix in consumption order) is built
+// in shared memory at the start of each sample, so the hot path never reads
+// the kernel-parameter Model through a pointer (a generic load from param
+// space costs a global-memory round trip).
 struct WStream {
-  const Model* M;
   const float* P;
   float* buf[2];
-  int L, idx, n, rep;
+  const int* ent;  // smem [n][3]
+  int idx, n, rep;
 
-  __device__ __noinline__ void stage(int i) {
-    int K, N, off;
-    entry_shape(*M, L, i, &K, &N, &off);
-    stage_matrix(P + off, K, N, buf[i & 1]);
+  __device__ __forceinline__ void stage(int i) {
+    stage_matrix(P + ent[3 * i + 2], ent[3 * i], ent[3 * i + 1], buf[i & 1]);
   }
-  __device__ void begin(int L_, int n_, int rep_ = 0) {
+  __device__ void begin(int n_, int rep_ = 0) {
     rep = rep_;
-    L = L_;
     n = n_;
     idx = 0;
     stage(0);
     cp_async_commit();
   }
-  // staged copy of entry idx (row stride N+1); prefetches entry idx+1.
-  // Every caller must have passed a block barrier since the previous use of
-  // the buffer being refilled.
+  // staged copy of entry idx (row stride stage_ld(N)); prefetches entry
+  // idx+1.  Every caller must have passed a block barrier since the previous
+  // use of the buffer being refilled.
   __device__ __noinline__ const float* acquire(int* ldw) {
     long long* tr = g_trace;
     const bool rec = tr != nullptr && blockIdx.x == 0 && threadIdx.x == 0 && idx < 64 && rep < 2;
     if (rec) tr[4 * idx + 256 * rep] = clock64();
-    int K, N, off;
-    entry_shape(*M, L, idx, &K, &N, &off);
-    *ldw = stage_ld(N);
+    *ldw = stage_ld(ent[3 * idx + 1]);
     if (idx + 1 < n) stage(idx + 1);
     cp_async_commit();
     if (rec) tr[4 * idx + 1 + 256 * rep] = clock64();
@@ -418,9 +420,10 @@ __global__ void __launch_bounds__(kTrainThreads) train_kernel(
   float* uall = sm + tp.u;
   float* misc = sm + tp.misc;
   double* cmds = reinterpret_cast<double*>(sm + tp.cmd);
+  __shared__ int s_ent[3 * kMaxEntries];
   WStream ws;
-  ws.M = &M;
   ws.P = Pw;
+  ws.ent = s_ent;
   ws.buf[0] = sm + tp.stage0;
   ws.buf[1] = sm + tp.stage1;
   int uoff[TPCB_MAX_DEC + 1], uw[TPCB_MAX_DEC + 1];
@@ -435,15 +438,18 @@ __global__ void __launch_bounds__(kTrainThreads) train_kernel(
 
   for (int w = blockIdx.x; w < n_all; w += gridDim.x) {
     const bool is_t = w >= n_src;
-    const SampleSetDev& set = is_t ? tgt : src;
+    const SampleSetDev set = is_t ? tgt : src;  // by value: no generic loads from param space
     const int idx = batch[w];
     const int L = set.n_leaf[idx];
     if (L < 1 || L > tp.R) {  // the plan was sized for the trainer's datasets
       raise_status(status, TPCB_ERR_LEAF_COUNT);
       continue;
     }
-    ws.begin(L, phase == 0 ? n_fwd_entries(M, L) : n_all_entries(M, L),
-             (w - (int)blockIdx.x) / (int)gridDim.x);
+    const int n_ent = phase == 0 ? n_fwd_entries(M, L) : n_all_entries(M, L);
+    for (int i = threadIdx.x; i < n_ent; i += blockDim.x)
+      entry_shape(M, L, i, &s_ent[3 * i], &s_ent[3 * i + 1], &s_ent[3 * i + 2]);
+    __syncthreads();
+    ws.begin(n_ent, (w - (int)blockIdx.x) / (int)gridDim.x);
     const float* xr = set.x + (size_t)set.ast_row[idx] * TPCB_FEAT_PAD;
     for (int e = threadIdx.x; e < L * TPCB_FEAT; e += blockDim.x) {
       const int r = e / TPCB_FEAT, c = e - r * TPCB_FEAT;
