@@ -161,7 +161,7 @@ extern "C" int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_
   if (zall_floats) *zall_floats = (int64_t)max_rows * m->dev.d_e;
   if (terms_doubles) *terms_doubles = (int64_t)max_rows * 2;
   TrainPlan tp = make_train_plan(m->dev, l_cap);
-  if ((size_t)tp.total * sizeof(float) > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
+  if ((size_t)tp.total * sizeof(float) > 220 * 1024) return TPCB_ERR_UNSUPPORTED;
   return TPCB_OK;
 }
 

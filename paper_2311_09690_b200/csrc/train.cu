@@ -673,14 +673,26 @@ int set_train_trace(long long* d_trace) {
   return TPCB_OK;
 }
 
+// dynamic shared memory left next to the kernel's static tables
+static size_t train_dyn_smem_limit() {
+  static size_t lim = 0;
+  if (!lim) {
+    cudaFuncAttributes a{};
+    if (cudaFuncGetAttributes(&a, train_kernel) == cudaSuccess)
+      lim = 227 * 1024 - a.sharedSizeBytes;
+  }
+  return lim;
+}
+
 int prepare_train_kernels(const Model& M, int l_cap) {
   TrainPlan tp = make_train_plan(M, l_cap);
   const size_t smem = (size_t)tp.total * sizeof(float);
-  if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
+  const size_t lim = train_dyn_smem_limit();
+  if (smem > lim) return TPCB_ERR_UNSUPPORTED;
   static bool done = false;
   if (!done) {
     TPCB_CUDA_CHECK(cudaFuncSetAttribute(train_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024));
+                                         (int)lim));
     done = true;
   }
   return TPCB_OK;
@@ -693,7 +705,6 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
   (void)PT;
   TrainPlan tp = make_train_plan(M, ws.l_cap);
   const size_t smem = (size_t)tp.total * sizeof(float);
-  if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;
   if (loss.cmd_order > kMaxCmdOrder) return TPCB_ERR_UNSUPPORTED;
   int st = prepare_train_kernels(M, ws.l_cap);
   if (st) return st;
