@@ -218,6 +218,12 @@ namespace tpcb {
 int set_train_trace(long long* d_trace);
 }
 
+/* debug: force the generic (v2) training kernel */
+extern "C" int tpcb_debug_force_v2(int32_t on) {
+  tpcb::g_force_v2 = on != 0;
+  return TPCB_OK;
+}
+
 /* debug: per-op timestamps of CTA 0 of the training kernel (NULL disables) */
 extern "C" int tpcb_debug_train_trace(long long* d_trace) { return tpcb::set_train_trace(d_trace); }
 

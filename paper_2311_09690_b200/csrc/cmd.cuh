@@ -34,10 +34,21 @@ __host__ __device__ constexpr int cmd_scratch_doubles(int de) {
 // lo, hi, mus, mut, s, u, ds, amin, amax [de each], ms, mt [(K+1)·de],
 // norms [K+1]).  Returns the CMD value (valid in every thread after the
 // trailing barrier).  Must be called by the whole block.  costmodel.py:426-476.
+// group variant: the first `nthr` threads (nthr/32 warps) participate and
+// synchronise on named barrier `bar_id` (0 = whole block, __syncthreads)
+__device__ __forceinline__ void cmd_bar(int bar_id, int nthr) {
+  if (bar_id == 0)
+    __syncthreads();
+  else
+    asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nthr) : "memory");
+}
+
 template <typename T>
 static __device__ __noinline__ double cmd_stats(const T* __restrict__ Z, int ns, int nt, int de,
-                                                int K, double* cs) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+                                                int K, double* cs, int bar_id = 0,
+                                                int nthr = 0) {
+  if (nthr <= 0) nthr = blockDim.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = nthr >> 5;
   const int n = ns + nt;
   const int KM = kMaxCmdOrder + 1;
   double* lo = cs;
@@ -116,7 +127,7 @@ static __device__ __noinline__ double cmd_stats(const T* __restrict__ Z, int ns,
       s[c] = raw < kCmdSupportFloor ? -kCmdSupportFloor : raw;  // sign marks clamping
     }
   }
-  __syncthreads();
+  cmd_bar(bar_id, nthr);
   // norms over columns (warp 0)
   if (w == 0) {
     double acc = 0.0;
@@ -139,9 +150,9 @@ static __device__ __noinline__ double cmd_stats(const T* __restrict__ Z, int ns,
       if (lane == 0) norms[j] = sqrt(a2);
     }
   }
-  __syncthreads();
+  cmd_bar(bar_id, nthr);
   // support gradient per column
-  for (int c = threadIdx.x; c < de; c += blockDim.x) {
+  for (int c = threadIdx.x; c < de; c += nthr) {
     const double sc = fabs(s[c]);
     double d = 0.0;
     if (norms[1] > 0.0) d -= (u[c] / norms[1]) * u[c] / sc;
@@ -153,10 +164,10 @@ static __device__ __noinline__ double cmd_stats(const T* __restrict__ Z, int ns,
     }
     ds[c] = (s[c] < 0.0) ? 0.0 : d;
   }
-  __syncthreads();
+  cmd_bar(bar_id, nthr);
   double value = norms[1];
   for (int j = 2; j <= K; ++j) value += norms[j];
-  __syncthreads();
+  cmd_bar(bar_id, nthr);
   return value;
 }
 

@@ -37,6 +37,62 @@ struct TrainPlan {
 
 TrainPlan make_train_plan(const Model& M, int l_cap);
 
+__host__ __device__ inline int round4(int v) { return (v + 3) & ~3; }
+
+// weight stream: the fixed order in which the fwd+bwd of one sample consumes
+// weight matrices (shared by the v2 and v3 training kernels)
+
+__host__ __device__ inline int n_fwd_entries(const Model& M, int L) {
+  return 1 + 6 * M.n_layers + L + 2 + M.n_dec + 1;
+}
+__host__ __device__ inline int n_all_entries(const Model& M, int L) {
+  return n_fwd_entries(M, L) + M.n_dec + 1 + L + 6 * M.n_layers;
+}
+
+__host__ __device__ inline void entry_shape(const Model& M, int L, int idx, int* K, int* N,
+                                            int* off) {
+  const int nl = M.n_layers, nd = M.n_dec, d = M.d;
+  auto dec_in = [&](int j) { return j == 0 ? M.d_e : M.dec[j - 1]; };
+  const int nf = n_fwd_entries(M, L);
+  auto layer_mat = [&](int li, int kind) {  // 0 Wq 1 Wk 2 Wv 3 Wo 4 fhW 5 foW
+    const LayerOff& lo = M.layer[li];
+    switch (kind) {
+      case 0: *K = d; *N = d; *off = lo.Wq; break;
+      case 1: *K = d; *N = d; *off = lo.Wk; break;
+      case 2: *K = d; *N = d; *off = lo.Wv; break;
+      case 3: *K = d; *N = d; *off = lo.Wo; break;
+      case 4: *K = d; *N = M.d_ff; *off = lo.fhW; break;
+      default: *K = M.d_ff; *N = d; *off = lo.foW; break;
+    }
+  };
+  if (idx < nf) {
+    if (idx == 0) { *K = TPCB_FEAT; *N = d; *off = M.inW; return; }
+    int q = idx - 1;
+    if (q < 6 * nl) { layer_mat(q / 6, q % 6); return; }
+    q -= 6 * nl;
+    if (q < L) { *K = d; *N = M.d_e; *off = M.leafW[L] + q * d * M.d_e; return; }
+    q -= L;
+    if (q == 0) { *K = TPCB_DEV_FEAT; *N = M.d_dev; *off = M.devhW; return; }
+    if (q == 1) { *K = M.d_dev; *N = M.d_e; *off = M.devpW; return; }
+    q -= 2;
+    if (q < nd) { *K = dec_in(q); *N = M.dec[q]; *off = M.decW[q]; return; }
+    *K = dec_in(nd); *N = 1; *off = M.outW;
+    return;
+  }
+  int b = idx - nf;
+  if (b < nd) { const int j = nd - 1 - b; *K = dec_in(j); *N = M.dec[j]; *off = M.decW[j]; return; }
+  b -= nd;
+  if (b == 0) { *K = M.d_dev; *N = M.d_e; *off = M.devpW; return; }
+  b -= 1;
+  if (b < L) { *K = d; *N = M.d_e; *off = M.leafW[L] + b * d * M.d_e; return; }
+  b -= L;
+  const int li = nl - 1 - b / 6;
+  const int order[6] = {5, 4, 3, 0, 1, 2};  // foW, fhW, Wo, Wq, Wk, Wv
+  layer_mat(li, order[b % 6]);
+}
+
+
+
 // one dataset on the device (packed rows from K1 + per-sample data)
 struct SampleSetDev {
   const float* x;          // packed rows [*, 32]
@@ -74,6 +130,14 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                  int32_t* status, cudaStream_t stream);
 int prepare_train_kernels(const Model& M, int l_cap);
+// v3 (warp-group per sample, producer warp + mbarrier weight stream)
+bool v3_supported(const Model& M);
+size_t train3_smem(const Model& M, int l_cap);
+int launch_train3(const Model& M, const float* P, const SampleSetDev& src, const SampleSetDev& tgt,
+                  const int32_t* batch, const StepDesc* steps, int step, int grid,
+                  const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
+                  int32_t* status, cudaStream_t stream);
+extern bool g_force_v2;
 int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps, int step,
                         int use_cmd, int add_cmd, float* grad_out, float* P, float* m, float* v,
                         const OptDev& opt, const double* lr, const int64_t* t,
