@@ -225,7 +225,13 @@ extern "C" int tpcb_debug_force_v2(int32_t on) {
 }
 
 /* debug: per-op timestamps of CTA 0 of the training kernel (NULL disables) */
-extern "C" int tpcb_debug_train_trace(long long* d_trace) { return tpcb::set_train_trace(d_trace); }
+namespace tpcb {
+int set_train3_trace(long long* d_trace);
+}
+extern "C" int tpcb_debug_train_trace(long long* d_trace) {
+  int st = tpcb::set_train_trace(d_trace);
+  return st ? st : tpcb::set_train3_trace(d_trace);
+}
 
 extern "C" int tpcb_graph_create(tpcb_graph** out) {
   if (!out) return TPCB_ERR_VALIDATION;

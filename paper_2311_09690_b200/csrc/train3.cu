@@ -25,6 +25,13 @@
 
 namespace tpcb {
 
+__device__ long long* g_trace3 = nullptr;
+
+int set_train3_trace(long long* d) {
+  TPCB_CUDA_CHECK(cudaMemcpyToSymbol(g_trace3, &d, sizeof(d)));
+  return TPCB_OK;
+}
+
 namespace {
 
 constexpr int kG = 2;                 // compute warps per sample
@@ -515,9 +522,13 @@ __global__ void __launch_bounds__(kThreads3) train3_kernel(
   const int nd = M.n_dec;
   int J = 0;  // weight-stream position (matches the producer)
   int ldw = 0;
+  long long* trace = g_trace3;
+  const bool rec = trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
   auto acquire = [&](int N) -> const float* {
     const int b = J & 1;
+    if (rec && J < 128) trace[2 * J] = clock64();
     mbar_wait(&full[b], (J >> 1) & 1);
+    if (rec && J < 128) trace[2 * J + 1] = clock64();
     ldw = stage_ld3(N);
     return buf[b];
   };
