@@ -283,8 +283,11 @@ int tpcb_distance_table(const double* d_feats, const int64_t* d_task_off, int32_
 /* debug: per-weight-op timestamps (clock64 pairs) of CTA 0 of the training
  * kernel into d_trace[512] (NULL disables) — tools/trace_train.py */
 int tpcb_debug_train_trace(long long* d_trace);
-/* debug: 1 forces the generic (v2) training kernel instead of v3 */
-int tpcb_debug_force_v2(int32_t on);
+/* debug: training-kernel selection — 0 automatic (the desk fast path v4 where
+ * the config matches, else the generic v2), 2 generic, 3 warp-group, 4 fast path */
+int tpcb_debug_train_impl(int32_t impl);
+/* debug: cap the training grid so CTAs loop over several samples (0 = no cap) */
+int tpcb_debug_grid_cap(int32_t cap);
 
 /* ---- measurement helpers (bench.py) -------------------------------------
  * FP32 FFMA throughput of this GPU in TFLOP/s (d_scratch: >= 1184 floats);

@@ -64,3 +64,22 @@ __device__ __forceinline__ void group_bar(int id, int nthreads) {
 }
 
 }  // namespace tpcb
+
+namespace tpcb {
+
+// 2-D TMA tile load (tensor map in param/const/global space) → shared memory,
+// completion counted in bytes on `bar`; c0 = inner (column) coordinate
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+
+}  // namespace tpcb

@@ -218,19 +218,29 @@ namespace tpcb {
 int set_train_trace(long long* d_trace);
 }
 
-/* debug: force the generic (v2) training kernel */
-extern "C" int tpcb_debug_force_v2(int32_t on) {
-  tpcb::g_force_v2 = on != 0;
+/* debug: training-kernel selection (0 automatic, 2 generic, 3 warp-group, 4 desk fast path) */
+extern "C" int tpcb_debug_train_impl(int32_t impl) {
+  if (impl != 0 && impl != 2 && impl != 3 && impl != 4) return TPCB_ERR_VALIDATION;
+  tpcb::g_train_impl = impl;
+  return TPCB_OK;
+}
+
+/* debug: cap the training grid (CTAs then loop over several samples); 0 = no cap */
+extern "C" int tpcb_debug_grid_cap(int32_t cap) {
+  if (cap < 0) return TPCB_ERR_VALIDATION;
+  tpcb::g_grid_cap = cap;
   return TPCB_OK;
 }
 
 /* debug: per-op timestamps of CTA 0 of the training kernel (NULL disables) */
 namespace tpcb {
 int set_train3_trace(long long* d_trace);
+int set_train4_trace(long long* d_trace);
 }
 extern "C" int tpcb_debug_train_trace(long long* d_trace) {
   int st = tpcb::set_train_trace(d_trace);
-  return st ? st : tpcb::set_train3_trace(d_trace);
+  if (!st) st = tpcb::set_train3_trace(d_trace);
+  return st ? st : tpcb::set_train4_trace(d_trace);
 }
 
 extern "C" int tpcb_graph_create(tpcb_graph** out) {

@@ -137,7 +137,16 @@ int launch_train3(const Model& M, const float* P, const SampleSetDev& src, const
                   const int32_t* batch, const StepDesc* steps, int step, int grid,
                   const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                   int32_t* status, cudaStream_t stream);
-extern bool g_force_v2;
+// v4 (desk-shaped fast path)
+bool v4_supported(const Model& M);
+bool v4_fits(const Model& M, int l_cap);
+int launch_train4(const Model& M, const float* P, const SampleSetDev& src, const SampleSetDev& tgt,
+                  const int32_t* batch, const StepDesc* steps, int step, int grid,
+                  const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
+                  int32_t* status, cudaStream_t stream);
+// training-kernel selection: 0 automatic (v4 where it applies, else v2), 2/3/4 forced
+extern int g_train_impl;
+extern int g_grid_cap;  // debug: cap on the training grid (0 = none)
 int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps, int step,
                         int use_cmd, int add_cmd, float* grad_out, float* P, float* m, float* v,
                         const OptDev& opt, const double* lr, const int64_t* t,

@@ -34,7 +34,7 @@ int set_train3_trace(long long* d) {
 
 namespace {
 
-constexpr int kG = 2;                 // compute warps per sample
+constexpr int kG = 8;                 // compute warps per sample
 constexpr int kGT = 32 * kG;          // compute threads
 constexpr int kThreads3 = kGT + 32;   // + producer warp
 constexpr int kBarGroup = 1;          // named barrier id of the compute group
