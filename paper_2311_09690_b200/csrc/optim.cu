@@ -19,11 +19,50 @@ namespace tpcb {
 
 namespace {
 
-__device__ __forceinline__ int region_bit(const Model& M, int p, const int* leaf_lo) {
-  if (p < leaf_lo[1] || p >= M.tail_lo) return 0;
+// read-once gradient slots: evict-first
+__device__ __forceinline__ float4 ldg4_last_use(const float4* p) {
+  float4 v;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(pol));
+  return v;
+}
+
+// region of parameter p: 0 = touched by every batch, L = leaf_embed.L
+struct LeafLo {
+  const int* lo;
+};
+__device__ __forceinline__ LeafLo s_leaf_of(const Model& M) { return LeafLo{M.leafW}; }
+__device__ __forceinline__ int region_bit(const Model& M, int p, LeafLo t) {
+  if (p < t.lo[1] || p >= M.tail_lo) return 0;
   int L = 1;
-  while (L < M.n_leaf_max && p >= leaf_lo[L + 1]) ++L;
+  while (L < M.n_leaf_max && p >= t.lo[L + 1]) ++L;
   return L;
+}
+
+// SGD / Adam on parameter p with its preloaded w, m, v (nn.py:136-167, fp32,
+// same operation order as the oracle)
+__device__ __forceinline__ void apply1(int p, float g, float w, float m, float v,
+                                       float* __restrict__ grad_out, float* __restrict__ P,
+                                       float* __restrict__ mbuf, float* __restrict__ vbuf,
+                                       const OptDev& opt, float lr, float bc1, float bc2) {
+  if (grad_out) grad_out[p] = g;
+  if (opt.kind == kOptNone) return;
+  const float wd = (float)opt.weight_decay;
+  if (wd != 0.f) g = g + wd * w;
+  if (opt.kind == kOptSgd) {
+    P[p] = w - lr * g;
+    return;
+  }
+  const float b1 = (float)opt.beta1, b2 = (float)opt.beta2, eps = (float)opt.eps;
+  const float omb1 = (float)(1.0 - opt.beta1), omb2 = (float)(1.0 - opt.beta2);
+  m = __fadd_rn(__fmul_rn(m, b1), __fmul_rn(omb1, g));
+  v = __fadd_rn(__fmul_rn(v, b2), __fmul_rn(__fmul_rn(omb2, g), g));
+  mbuf[p] = m;
+  vbuf[p] = v;
+  P[p] = w - __fdiv_rn(__fmul_rn(lr, __fdiv_rn(m, bc1)), __fadd_rn(sqrtf(__fdiv_rn(v, bc2)), eps));
 }
 
 __global__ void __launch_bounds__(256) reduce_apply_kernel(
@@ -35,16 +74,23 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(
     const double* __restrict__ lr_p, const int64_t* __restrict__ t_p,
     const double* __restrict__ terms, const double* __restrict__ scalars, LossDev loss,
     double* __restrict__ step_loss, double* __restrict__ step_cmd) {
-  __shared__ uint32_t s_touch[1024];
-  __shared__ int s_leaf[TPCB_MAX_LEAF + 2];
+  // A block owns 64 float4 columns (4 parameters each: tensors start on
+  // 16-byte boundaries, so a column never straddles two tensors and has one
+  // region bit).  Its four 64-thread quarters each sum a contiguous quarter of
+  // the slots (8 loads in flight), the quarters are combined in fixed order
+  // (bitwise reproducible, no atomics), then every thread applies the
+  // optimizer to one parameter (coalesced).  All global loads of a thread —
+  // slots, p, m, v, step scalars — are issued before the block's single
+  // barrier, so a block costs about one memory latency.
+  __shared__ float4 s_part[4][64];
+  __shared__ float s_opt[3];
   const StepDesc sd = steps[step];
   const int n_src = sd.n_src, n_tgt = sd.n_tgt;
   const int n_all = n_src + (use_cmd ? n_tgt : 0);
   const int G = min(n_all, n_slots);
-  for (int c = threadIdx.x; c < G; c += blockDim.x) s_touch[c] = touched[c];
-  if (threadIdx.x <= M.n_leaf_max) s_leaf[threadIdx.x] = threadIdx.x ? M.leafW[threadIdx.x] : 0;
-  if (threadIdx.x == 0) s_leaf[M.n_leaf_max + 1] = M.tail_lo;
-  __syncthreads();
+  const int col = threadIdx.x & 63, quarter = threadIdx.x >> 6;
+  const int n4 = M.total >> 2;
+  const size_t st4 = stride >> 2;
 
   // loss value of the step (fixed order), costmodel.py:539-550
   if (blockIdx.x == 0 && threadIdx.x < 32) {
@@ -70,75 +116,103 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(
     }
   }
 
-  float lr = 0.f, bc1 = 1.f, bc2 = 1.f;
-  if (opt.kind != kOptNone) {
-    lr = (float)lr_p[0];
-    if (opt.kind == kOptAdam) {
-      const double t = (double)(t_p[0] + step + 1);
-      bc1 = (float)(1.0 - pow(opt.beta1, t));
-      bc2 = (float)(1.0 - pow(opt.beta2, t));
+  // slot masks: the fast path sums every slot unpredicated when all of them
+  // touched the column's region (the shared region, always; a leaf region when
+  // the batch is one bucket), and skips regions no slot touched
+  __shared__ uint32_t s_touch[1024];
+  __shared__ uint32_t s_and, s_or;
+  if (threadIdx.x < 32) {
+    uint32_t a = ~0u, o = 0u;
+    for (int c = threadIdx.x; c < G; c += 32) {
+      const uint32_t t = touched[c];
+      s_touch[c] = t;
+      a &= t;
+      o |= t;
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      a &= __shfl_xor_sync(0xffffffffu, a, d);
+      o |= __shfl_xor_sync(0xffffffffu, o, d);
+    }
+    if (threadIdx.x == 0) {
+      s_and = G > 0 ? a : 0u;
+      s_or = o;
     }
   }
-  const float b1 = (float)opt.beta1, b2 = (float)opt.beta2, eps = (float)opt.eps,
-              wd = (float)opt.weight_decay;
-  const float omb1 = (float)(1.0 - opt.beta1), omb2 = (float)(1.0 - opt.beta2);
-  // 4 parameters per thread: tensors start on 16-byte boundaries, so a group
-  // never straddles two tensors and shares one region bit
-  const int n4 = M.total >> 2;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += gridDim.x * blockDim.x) {
+  for (int base = blockIdx.x * 64; base < n4; base += gridDim.x * 64) {
+    // optimizer operands of this thread's parameter, in flight with the slots
+    const int pp = base * 4 + threadIdx.x;
+    const bool pv = pp < M.total && opt.kind != kOptNone;
+    float w = 0.f, m = 0.f, v = 0.f;
+    if (pv) {
+      w = P[pp];
+      if (opt.kind == kOptAdam) {
+        m = mbuf[pp];
+        v = vbuf[pp];
+      }
+    }
+    const int q = base + col;
+    const bool qv = q < n4;
     const int p = q << 2;
-    const uint32_t want = 1u << region_bit(M, p, s_leaf);
+    const uint32_t want = qv ? 1u << region_bit(M, p, s_leaf_of(M)) : 0u;
+    const int per_q = (G + 3) >> 2;
+    const int c_lo = min(G, quarter * per_q), c_hi = min(G, c_lo + per_q);
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4* src = reinterpret_cast<const float4*>(partial + p);
-    const size_t st4 = stride >> 2;
-    int c = 0;
-    for (; c + 4 <= G; c += 4) {  // 4 slots in flight, summed in slot order
-      float4 v0 = make_float4(0.f, 0.f, 0.f, 0.f), v1 = v0, v2 = v0, v3 = v0;
-      if (s_touch[c] & want) v0 = src[(size_t)c * st4];
-      if (s_touch[c + 1] & want) v1 = src[(size_t)(c + 1) * st4];
-      if (s_touch[c + 2] & want) v2 = src[(size_t)(c + 2) * st4];
-      if (s_touch[c + 3] & want) v3 = src[(size_t)(c + 3) * st4];
-      g.x += v0.x; g.y += v0.y; g.z += v0.z; g.w += v0.w;
-      g.x += v1.x; g.y += v1.y; g.z += v1.z; g.w += v1.w;
-      g.x += v2.x; g.y += v2.y; g.z += v2.z; g.w += v2.w;
-      g.x += v3.x; g.y += v3.y; g.z += v3.z; g.w += v3.w;
-    }
-    for (; c < G; ++c) {
-      if (s_touch[c] & want) {
-        const float4 v = src[(size_t)c * st4];
-        g.x += v.x; g.y += v.y; g.z += v.z; g.w += v.w;
-      }
-    }
-    if (grad_out) *reinterpret_cast<float4*>(grad_out + p) = g;
-    if (opt.kind == kOptNone) continue;
-    float4 w = *reinterpret_cast<float4*>(P + p);
-    float gg[4] = {g.x, g.y, g.z, g.w};
-    float ww[4] = {w.x, w.y, w.z, w.w};
-    if (opt.kind == kOptSgd) {
+    __syncthreads();  // s_touch / s_and / s_or (first iteration), s_part reuse (later ones)
+    if (qv && (s_or & want)) {
+      const float4* src = reinterpret_cast<const float4*>(partial + p) + (size_t)c_lo * st4;
+      const int n = c_hi - c_lo;
+      if (s_and & want) {  // every slot touched it: unpredicated, 8 loads in flight
+        int c = 0;
+        for (; c + 8 <= n; c += 8) {
+          float4 x[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float gj = gg[j];
-        if (wd != 0.f) gj = gj + wd * ww[j];
-        ww[j] = ww[j] - lr * gj;
-      }
-    } else {
-      const float4 m4 = *reinterpret_cast<float4*>(mbuf + p);
-      const float4 v4 = *reinterpret_cast<float4*>(vbuf + p);
-      float mm[4] = {m4.x, m4.y, m4.z, m4.w};
-      float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+          for (int u = 0; u < 8; ++u) x[u] = ldg4_last_use(src + (size_t)(c + u) * st4);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float gj = gg[j];
-        if (wd != 0.f) gj = gj + wd * ww[j];
-        mm[j] = __fadd_rn(__fmul_rn(mm[j], b1), __fmul_rn(omb1, gj));
-        vv[j] = __fadd_rn(__fmul_rn(vv[j], b2), __fmul_rn(__fmul_rn(omb2, gj), gj));
-        ww[j] = ww[j] - __fdiv_rn(__fmul_rn(lr, __fdiv_rn(mm[j], bc1)),
-                                  __fadd_rn(sqrtf(__fdiv_rn(vv[j], bc2)), eps));
+          for (int u = 0; u < 8; ++u) {
+            g.x += x[u].x; g.y += x[u].y; g.z += x[u].z; g.w += x[u].w;
+          }
+        }
+        for (; c < n; ++c) {
+          const float4 x = ldg4_last_use(src + (size_t)c * st4);
+          g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
+        }
+      } else {
+        for (int c = 0; c < n; ++c) {
+          if (s_touch[c_lo + c] & want) {
+            const float4 x = ldg4_last_use(src + (size_t)c * st4);
+            g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
+          }
+        }
       }
-      *reinterpret_cast<float4*>(mbuf + p) = make_float4(mm[0], mm[1], mm[2], mm[3]);
-      *reinterpret_cast<float4*>(vbuf + p) = make_float4(vv[0], vv[1], vv[2], vv[3]);
     }
-    *reinterpret_cast<float4*>(P + p) = make_float4(ww[0], ww[1], ww[2], ww[3]);
+    s_part[quarter][col] = g;
+    if (threadIdx.x == 0) {  // step scalars: one thread (fp64 pow is hundreds of instructions)
+      float lr = 0.f, bc1 = 1.f, bc2 = 1.f;
+      if (opt.kind != kOptNone) {
+        lr = (float)__ldg(lr_p);
+        if (opt.kind == kOptAdam) {
+          const double t = (double)(__ldg(t_p) + step + 1);
+          bc1 = (float)(1.0 - pow(opt.beta1, t));
+          bc2 = (float)(1.0 - pow(opt.beta2, t));
+        }
+      }
+      s_opt[0] = lr;
+      s_opt[1] = bc1;
+      s_opt[2] = bc2;
+    }
+    __syncthreads();
+    const float lr = s_opt[0], bc1 = s_opt[1], bc2 = s_opt[2];
+    if (pp < M.total) {
+      const int cc = threadIdx.x >> 2, comp = threadIdx.x & 3;
+      const float* part = reinterpret_cast<const float*>(s_part);
+      float gs = part[(0 * 64 + cc) * 4 + comp];
+      gs += part[(1 * 64 + cc) * 4 + comp];
+      gs += part[(2 * 64 + cc) * 4 + comp];
+      gs += part[(3 * 64 + cc) * 4 + comp];
+      apply1(pp, gs, w, m, v, grad_out, P, mbuf, vbuf, opt, lr, bc1, bc2);
+    }
+    __syncthreads();
   }
 }
 
@@ -220,7 +294,7 @@ int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps
                         const OptDev& opt, const double* lr, const int64_t* t,
                         const LossDev& loss, double* step_loss, double* step_cmd,
                         cudaStream_t stream) {
-  const int grid = min(ceil_div(M.total / 4, 256), kNumSMs * 8);
+  const int grid = min(ceil_div(M.total / 4, 64), kNumSMs * 16);
   reduce_apply_kernel<<<grid, 256, 0, stream>>>(M, ws.partial, ws.slot_stride, ws.touched, steps,
                                                 step, ws.n_slots, use_cmd, add_cmd, grad_out, P, m,
                                                 v, opt, lr, t, ws.terms, ws.scalars, loss,
