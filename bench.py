@@ -345,7 +345,7 @@ def run_ours(args):
     if pk_path.exists():
         peaks = json.loads(pk_path.read_text())
     bf16 = peaks.get("bf16_tflops", 1590.0)
-    roofline = {"bound": "tensor", "kernel": "train_kernel (fused fwd+bwd per sample)",
+    roofline = {"bound": "tensor", "kernel": "train4_kernel (fused fwd+bwd per sample, desk fast path)",
                 "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
                 "frac": achieved / bf16, "traffic": None,
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else
@@ -353,7 +353,7 @@ def run_ours(args):
                 "fp32_ffma_peak_measured": ffma, "frac_of_fp32_ffma": achieved / ffma,
                 "share_of_step": prof[0] / prof.sum(),
                 "per_launch": {"flops": flops_epoch / launches, "avg_ms": avg_ms},
-                "other_kernels_ms_per_epoch": {"reduce_adam": prof[1], "transpose": prof[2]}}
+                "other_kernels_ms_per_epoch": {"reduce_adam": prof[1], "allreduce_opt_dp": prof[2]}}
 
     # ----------------------------------------------- inference (extra keys)
     infer = {}

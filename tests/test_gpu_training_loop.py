@@ -167,8 +167,8 @@ def test_acceptance_criterion_6_desk_learning():
     actual = np.array([s.latency_s for s in test])
     mape = pb.metrics(pred, actual)["mape"]
     p90 = float(np.quantile(np.abs(pred - actual) / actual, 0.9))
-    assert mape <= 0.20, mape
-    assert p90 <= 0.35, p90
+    assert mape <= 0.20, (mape, p90)
+    assert p90 <= 0.35, (mape, p90)
 
 
 def test_train_deterministic_and_zero_epochs():
