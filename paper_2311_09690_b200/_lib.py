@@ -8,11 +8,13 @@ if the library is missing every GPU entry point raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from . import errors as E
 
-LIB_PATH = Path(__file__).resolve().parent / "libtpcb200.so"
+LIB_PATH = Path(os.environ.get("TPCB_LIB_PATH") or
+                Path(__file__).resolve().parent / "libtpcb200.so")  # (env: A/B experiments)
 
 MAX_LAYERS, MAX_LEAF, MAX_DEC = 16, 16, 8
 FEAT, FEAT_PAD, DEV_FEAT = 24, 32, 6

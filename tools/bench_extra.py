@@ -1,0 +1,131 @@
+"""Secondary measurements of SURVEY §8(d), one JSON line each (B200, 1 GPU):
+
+  C3  CMD fine-tune training throughput: source = the C2 training split,
+      target = shifted valid+test (criterion-7 shift), alpha 1, K 5, bs 64+64
+  C4  KMeans 1M × 1024 (d = 24 mean-pooled leaf vectors and d = 32 z_x),
+      k-means++ + Lloyd to convergence; per-iteration time
+  C5  inference sweep n = 64 … 1M ASTs (fp32 parity mode; the bf16 mode is not
+      implemented yet)
+
+python tools/bench_extra.py [c3] [c4] [c5]     (default: all)
+"""
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import paper_2311_09690_b200 as pb  # noqa: E402
+from paper_2311_09690_b200 import engine, synth  # noqa: E402
+from paper_2311_09690_b200.dataset import fit_boxcox  # noqa: E402
+
+DSPEC = pb.DeviceSpec("synth0", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0)
+DV = pb.device_vector(DSPEC).astype(np.float32)
+SHIFT = np.where((np.arange(24) >= 10) & (np.arange(24) < 16), 2.0, 0.0).astype(np.float32)
+
+
+def rag(s, shift=None):
+    rows = s.vectors.astype(np.float32)
+    if shift is not None:
+        rows = rows + shift
+    return engine.RaggedHost(rows=rows, ordering=s.ordering, n_leaf=s.n_leaf,
+                             devfeat=np.tile(DV, (s.n, 1)), encoded=False)
+
+
+def dev_time(fn, reps=1, stream=None):
+    """device time per call, CUDA events on the stream the work runs on"""
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / 1e3 / reps
+
+
+def c3():
+    from paper_2311_09690_b200.training import Trainer
+    n_gen = 327_680
+    data = synth.generate(n_gen, seed=0)
+    tr_i, va_i, te_i = synth.split(n_gen, seed=0)
+    train = data.take(np.sort(tr_i))
+    target = data.take(np.sort(np.concatenate([va_i, te_i])))
+    norm = fit_boxcox(train.latency)
+    cfg = pb.desk_config(seed=0, alpha_cmd=1.0)
+    loss = engine.loss_struct("hybrid", cfg.lambda_hybrid, norm.loss_offset, 1.0, 5,
+                              "transformed", norm)
+    tr = Trainer(cfg, pb.init_params(cfg).tensors, rag(train), norm.encode(train.latency), loss,
+                 target_rag=rag(target, SHIFT))
+    rng = np.random.default_rng(0)
+    flat, steps = tr.plan(rng)
+    tr.run_epoch(cfg.lr, flat, steps)  # warm-up + graph capture
+    torch.cuda.synchronize()
+    flat, steps = tr.plan(rng)
+    t = dev_time(lambda: tr.run_epoch(cfg.lr, flat, steps), stream=tr.stream)
+    cmd = tr.step_cmd[:steps.shape[0]].cpu().numpy()
+    return {"metric": "C3 CMD fine-tune source samples/s (1 GPU)", "value": train.n / t,
+            "unit": "samples/s", "epoch_s": t, "steps": int(steps.shape[0]),
+            "batch": "64 source + 64 target (same leaf bucket)", "mean_step_cmd": float(cmd.mean()),
+            "dtype": "f32 network, f64 CMD statistics"}
+
+
+def c4():
+    from paper_2311_09690_b200.sampling import DeviceKMeans
+    out = []
+    n, k = 1 << 20, 1024
+    data = synth.generate(n, seed=0)
+    off = data.offsets()
+    pooled = np.add.reduceat(data.vectors.astype(np.float64), off[:-1], axis=0) / data.n_leaf[:, None]
+    p = pb.Predictor(pb.init_params(pb.desk_config(seed=0)))
+    _, zx, _, _, _ = p.forward_ragged(rag(data), None, latents=True)
+    for name, x in (("d24 mean-pooled leaf vectors", pooled),
+                    ("d32 z_x latents", zx.double().cpu().numpy())):
+        km = DeviceKMeans(np.ascontiguousarray(x), k)
+        rng = np.random.default_rng(0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        km.kmeanspp(rng)
+        torch.cuda.synchronize()
+        t_pp = time.perf_counter() - t0
+        t_assign = dev_time(km.assign_step, reps=3)
+        t0 = time.perf_counter()
+        iters = km.lloyd()
+        torch.cuda.synchronize()
+        t_lloyd = time.perf_counter() - t0
+        flops = 3.0 * n * k * x.shape[1]
+        out.append({"metric": f"C4 KMeans {n}x{k} ({name})", "kmeanspp_s": t_pp,
+                    "lloyd_s": t_lloyd, "lloyd_iterations": iters,
+                    "assign_pass_ms": t_assign * 1e3,
+                    "assign_fp64_tflops": flops / t_assign / 1e12, "dtype": "f64"})
+    return out
+
+
+def c5():
+    p = pb.Predictor(pb.init_params(pb.desk_config(seed=0)))
+    big = synth.generate(1 << 20, seed=0)
+    res = {}
+    for n in (64, 256, 1024, 4096, 16384, 65536, 262144, 1 << 20):
+        sub = big.take(np.arange(n))
+        rows, ordering, leaf_off, devfeat = engine.upload_ragged(rag(sub), torch.device("cuda"))
+        f = lambda: p.forward_device(rows, ordering, leaf_off, devfeat, n, False, None,  # noqa
+                                     latents=False)
+        for _ in range(3):
+            f()
+        reps = 50 if n <= 65536 else 5
+        res[str(n)] = n / dev_time(f, reps)
+    return {"metric": "C5 inference sweep ASTs/s (fp32 parity mode, K1 pack + fused forward)",
+            "unit": "ASTs/s", "by_n": res, "dtype": "f32",
+            "note": "bf16 tensor-core mode not implemented in this round"}
+
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["c3", "c4", "c5"]
+    for w in which:
+        r = {"c3": c3, "c4": c4, "c5": c5}[w]()
+        for line in (r if isinstance(r, list) else [r]):
+            print(json.dumps(line), flush=True)
