@@ -137,6 +137,18 @@ int tpcb_forward(const tpcb_model* m, const float* d_params, const tpcb_packed* 
                  float* d_pred, float* d_zx, float* d_zv, float* d_z, double* d_latency,
                  int32_t* d_status, void* stream);
 
+/* bf16 tensor-core mode of tpcb_forward (the C5 sweep path):
+ * the desk encoder's GEMMs run on tcgen05 (bf16 operands, fp32 accumulation
+ * in TMEM); LayerNorm / softmax / head in fp32, decode in fp64.  Desk-shaped
+ * models only; pk->rows_per_tile must be 128.  d_img: device workspace of
+ * tpcb_forward_bf16_workspace() bytes (bf16 weight image, rebuilt per call).
+ * Accuracy is stated separately from the fp32 parity mode. */
+size_t tpcb_forward_bf16_workspace(void);
+int tpcb_forward_bf16(const tpcb_model* m, const float* d_params, const tpcb_packed* pk,
+                      const float* d_devfeat, int64_t n_ast, const tpcb_boxcox* norm, void* d_img,
+                      float* d_pred, float* d_zx, float* d_zv, float* d_z, double* d_latency,
+                      int32_t* d_status, void* stream);
+
 /* costmodel.metrics (costmodel.py:577-591): d_out = {MAPE, RMSE, MSPE} (fp64) */
 int tpcb_metrics(const double* d_pred, const double* d_y, int64_t n, double* d_out, void* stream);
 

@@ -83,6 +83,9 @@ SIGNATURES = {
     "tpcb_positional_encoding": (i32, [vp, i64, vp, vp, vp]),
     "tpcb_forward": (i32, [vp, vp, C.POINTER(Packed), vp, i64, C.POINTER(BoxCox), vp, vp, vp,
                            vp, vp, vp, vp]),
+    "tpcb_forward_bf16_workspace": (C.c_size_t, []),
+    "tpcb_forward_bf16": (i32, [vp, vp, C.POINTER(Packed), vp, i64, C.POINTER(BoxCox), vp, vp, vp,
+                                vp, vp, vp, vp, vp]),
     "tpcb_metrics": (i32, [vp, vp, i64, vp, vp]),
     "tpcb_cmd": (i32, [vp, i32, i64, i64, i32, i32, vp, vp, vp]),
     "tpcb_train_ws_sizes": (i32, [vp, i32, i32, C.POINTER(i32), C.POINTER(i64),

@@ -75,7 +75,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                 print(log, file=sys.stderr)
     if force or not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
         nccl_lib = _nccl_dir() / "lib"
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcuda",
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs),
                f"-L{nccl_lib}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:

@@ -179,11 +179,18 @@ class Predictor:
     """Device-resident model: flat fp32 parameters + the model handle.
     The bulk inference entry point (`forward_batch`) of the GPU path."""
 
-    def __init__(self, params: CostModelParams, rows_per_tile: int = 64):
+    def __init__(self, params: CostModelParams, rows_per_tile: int = 64, precision: str = "fp32"):
+        """precision "fp32": the parity mode (FP32 FFMA, decoded latency within
+        1e-3 of the float64 reference); "bf16": encoder GEMMs on the tcgen05
+        tensor cores with bf16 operands and fp32 accumulation (desk-shaped
+        models; packs 128-row tiles), accuracy stated in DESIGN.md."""
+        if precision not in ("fp32", "bf16"):
+            raise ValidationError(f"unknown precision {precision!r}")
         self.config = params.config
         self.dm = device_model(params.config)
         self.params = self.dm.upload(params.tensors)
-        self.R = rows_per_tile
+        self.precision = precision
+        self.R = 128 if precision == "bf16" else rows_per_tile
         self.status = engine.Status(self.params.device)
 
     def tensors(self) -> dict:
@@ -193,7 +200,8 @@ class Predictor:
                        latents=True, theta=engine.THETA_DEFAULT):
         pk = engine.pack(rows, ordering, leaf_off, n_ast, self.config.n_leaf_max, encoded,
                          self.status, self.R, theta)
-        return engine.run_forward(self.dm, self.params, pk, devfeat, self.status, norm, latents)
+        return engine.run_forward(self.dm, self.params, pk, devfeat, self.status, norm, latents,
+                                  self.precision)
 
     def forward_ragged(self, rag: engine.RaggedHost, norm=None, latents=True):
         if rag.n_ast == 0:

@@ -1,0 +1,565 @@
+// K2+K3, bf16 tensor-core mode (the C5 "bf16" inference path): the desk
+// encoder's GEMMs on the 5th-generation tensor cores (tcgen05.mma, fp32
+// accumulators in TMEM), everything else fused around them.
+//
+// Same network and outputs as forward.cu (reference: costmodel.py:193-269,
+// nn.py:26-96, dataset.py:97-115); only the encoder GEMM operands are rounded
+// to bf16 (fp32 accumulation).  LayerNorm, softmax, residuals, the leaf /
+// device / decoder head and the Box-Cox decode stay in fp32 / fp64.  The
+// accuracy of this mode is stated separately from the fp32 parity mode
+// (tests/test_gpu_forward_bf16.py).
+//
+// Layout.  One CTA (4 warps, thread r = row r) per 128-row packed tile
+// (rows_per_tile = 128: floor(128/L) whole ASTs of one leaf count),
+// persistent over tiles.  All encoder weights live in shared memory for the
+// CTA's lifetime as bf16 K-major, 128-byte-swizzled UMMA operand tiles
+// (136 KB, one bulk copy of an image prepared by prep_weights_kernel).  The
+// activation operand (128 rows × 64 bf16, same swizzle) is rewritten by the
+// epilogues; the accumulator tile is 128 TMEM lanes × up to 192 fp32 columns,
+// read back with tcgen05.ld (lane = row = thread) so LayerNorm needs no
+// cross-thread reduction.  Attention runs per query row on bf16 K/V rows of
+// its own AST.
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstring>
+
+#include "async.cuh"
+#include "common.cuh"
+
+namespace tpcb {
+
+namespace {
+
+constexpr int D = 64, FF = 128, DE = 32, DDEV = 16, DEC = 64, NLAY = 2, DH = 32;
+constexpr int TR = 128;   // rows per tile = TMEM lanes = threads
+constexpr int NTH = 128;
+
+// ---- weight image (bytes): bf16 B operands [N rows][64 k] K-major, SW128 ----
+constexpr int kTileB = 64 * 128;  // bytes per 64-row B tile (8 KB)
+constexpr int kImgIn = 0;                       // N=64, K=24 (zero-padded to 64)
+constexpr int kImgLayer = kTileB;               // + li * kImgLStride
+constexpr int kQKV = 0;                         // N=192 (Wq | Wk | Wv)
+constexpr int kWO = 3 * kTileB;                 // N=64
+constexpr int kFH = 4 * kTileB;                 // N=128
+constexpr int kFO0 = 6 * kTileB;                // N=64, k = 0..63 of foW
+constexpr int kFO1 = 7 * kTileB;                // N=64, k = 64..127
+constexpr int kImgLStride = 8 * kTileB;
+constexpr int kImgBytes = kImgLayer + NLAY * kImgLStride;  // 139,264
+
+// ---- shared memory (bytes, dynamic) ----
+constexpr int kSmA = kImgBytes;                 // A operand [128][64] bf16, SW128 (16 KB)
+constexpr int kSmKV = kSmA + TR * 128;          // K|V bf16 [128][128] row-major, later F (32 KB)
+constexpr int kSmH = kSmKV + TR * 256;          // encoder output fp32 [128][65]
+constexpr int kSmVec = kSmH + TR * 65 * 4;      // biases / LN vectors fp32
+constexpr int kVecIn = 0, kVecLayer = 64, kVecLStride = 704;  // (same order as train4)
+constexpr int kVBQKV = 0, kVBO = 192, kVLN1G = 256, kVLN1B = 320, kVFHB = 384, kVFOB = 512,
+              kVLN2G = 576, kVLN2B = 640;
+constexpr int kVecFloats = kVecLayer + NLAY * kVecLStride;
+constexpr int kSmTotal = kSmVec + kVecFloats * 4;
+
+__host__ __device__ inline uint32_t sw128(int r, int k) {  // bf16 element (row r, col k < 64)
+  return (r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) ^ (r & 7))) << 4) + (k & 7) * 2;
+}
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);  // start address
+  d |= (uint64_t)1 << 16;                 // leading byte offset (unused: SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // stride byte offset: 8-row swizzle atoms
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;                 // 128-byte swizzle
+  return d;
+}
+
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {  // bf16 × bf16 → fp32, K-major
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(m >> 4) << 24);
+}
+
+// D[tmem] (+)= A[128 × 64·ka] · B[n × 64·ka]ᵀ, k chunks of 64 (one SW128 tile each)
+__device__ __forceinline__ void mma_chain(uint32_t tmem, const uint32_t* a_tiles,
+                                          const uint32_t* b_tiles, int nchunks, int n) {
+  const uint32_t id = idesc_bf16(TR, n);
+  for (int c = 0; c < nchunks; ++c)
+    for (int k = 0; k < 4; ++k) {
+      const uint64_t a = sdesc(a_tiles[c] + k * 32), b = sdesc(b_tiles[c] + k * 32);
+      const uint32_t acc = (c | k) != 0;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+          "l"(a), "l"(b), "r"(id), "r"(acc));
+    }
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+      smem_u32(bar)));
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane (warp w owns lanes 32w..32w+31)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// this thread's 64 bf16 values → row r of a SW128 A tile
+__device__ __forceinline__ void store_row_bf16(uint8_t* tile, int r, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * c + 0], v[8 * c + 1]);
+    __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * c + 2], v[8 * c + 3]);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * c + 4], v[8 * c + 5]);
+    __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * c + 6], v[8 * c + 7]);
+    uint4 u;
+    u.x = *reinterpret_cast<uint32_t*>(&p0);
+    u.y = *reinterpret_cast<uint32_t*>(&p1);
+    u.z = *reinterpret_cast<uint32_t*>(&p2);
+    u.w = *reinterpret_cast<uint32_t*>(&p3);
+    *reinterpret_cast<uint4*>(tile + sw128(r, 8 * c)) = u;
+  }
+}
+
+// operand writes (generic proxy) → visible to the tensor cores; CTA barrier
+__device__ __forceinline__ void sync_for_mma() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
+  mbar_wait(bar, phase);
+  phase ^= 1;
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// LayerNorm of a row held by this thread (nn.py:48-54)
+__device__ __forceinline__ void ln_row(float* v, const float* g, const float* b) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < D; ++i) s += v[i];
+  const float mu = s * (1.f / D);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const float t = v[i] - mu;
+    q = fmaf(t, t, q);
+  }
+  const float inv = 1.f / sqrtf(q * (1.f / D) + 1e-5f);
+#pragma unroll
+  for (int i = 0; i < D; ++i) v[i] = fmaf(g[i], (v[i] - mu) * inv, b[i]);
+}
+
+__device__ __forceinline__ double boxcox_decode_tc(double e, const tpcb_boxcox& bc, bool* bad) {
+  const double t = e * bc.t_std + bc.t_mean;
+  if (fabs(bc.lambda_bc) < 1e-9) return exp(t) - bc.shift;
+  const double base = bc.lambda_bc * t + 1.0;
+  if (!(base > 0.0)) {
+    *bad = true;
+    return nan("");
+  }
+  return pow(base, 1.0 / bc.lambda_bc) - bc.shift;
+}
+
+// fp32 parameters → the bf16 weight image (see kImg*)
+__global__ void prep_weights_kernel(const Model M, const float* __restrict__ P,
+                                    uint8_t* __restrict__ img) {
+  const int total = kImgBytes / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int byte = e * 2;
+    // locate (tile base, n, k) from the byte offset: invert sw128 within 8-KB tiles
+    const int tile = byte / kTileB, in = byte - tile * kTileB;
+    const int atom = in >> 10, rr = (in >> 7) & 7, chunk = ((in >> 4) & 7) ^ rr;
+    const int n_local = atom * 8 + rr, k = chunk * 8 + ((in & 15) >> 1);
+    float v = 0.f;
+    if (tile == 0) {
+      v = k < TPCB_FEAT ? P[M.inW + k * D + n_local] : 0.f;
+    } else {
+      const int li = (tile - 1) / 8, t = (tile - 1) % 8;
+      const LayerOff& lo = M.layer[li];
+      if (t < 3) {
+        const int n = t * 64 + n_local;  // Q | K | V
+        const int off = n < 64 ? lo.Wq : (n < 128 ? lo.Wk : lo.Wv);
+        v = P[off + k * D + (n & 63)];
+      } else if (t == 3) {
+        v = P[lo.Wo + k * D + n_local];
+      } else if (t < 6) {
+        v = P[lo.fhW + k * FF + (t - 4) * 64 + n_local];
+      } else {
+        v = P[lo.foW + ((t - 6) * 64 + k) * D + n_local];
+      }
+    }
+    reinterpret_cast<__nv_bfloat16*>(img)[e] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
+    const __grid_constant__ Model M, const float* __restrict__ P,
+    const uint8_t* __restrict__ img, const float* __restrict__ x,
+    const int32_t* __restrict__ tile_L, const int32_t* __restrict__ tile_first,
+    const int32_t* __restrict__ tile_count, const int32_t* __restrict__ n_tiles_p,
+    const int32_t* __restrict__ perm, const float* __restrict__ devfeat, tpcb_boxcox bc,
+    float* __restrict__ pred_out, float* __restrict__ zx_out, float* __restrict__ zv_out,
+    float* __restrict__ z_out, double* __restrict__ lat_out, int32_t* status) {
+  extern __shared__ __align__(1024) uint8_t smb[];
+  __shared__ __align__(8) uint64_t bars[2];  // [0] weights landed, [1] MMA done
+  __shared__ uint32_t s_tmem;
+  const int t = threadIdx.x, warp = t >> 5;
+  const int n_tiles = *n_tiles_p;
+  uint8_t* sA = smb + kSmA;
+  uint8_t* sKV = smb + kSmKV;
+  float* sH = reinterpret_cast<float*>(smb + kSmH);
+  float* sv = reinterpret_cast<float*>(smb + kSmVec);
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  const uint32_t tlane = tmem + ((uint32_t)(32 * warp) << 16);  // this warp's lanes
+  if (t == 0 && (smem_u32(smb) & 1023u)) raise_status(status, TPCB_ERR_CUDA);  // swizzle atoms
+  if (t == 0) {  // the weight image: one bulk copy for the CTA's lifetime
+    mbar_arrive_expect_tx(&bars[0], (uint32_t)kImgBytes);
+    bulk_g2s(smb, img, (uint32_t)kImgBytes, &bars[0]);
+  }
+  // biases and LayerNorm vectors (fp32)
+  for (int i = t; i < D; i += NTH) sv[kVecIn + i] = __ldg(P + M.inb + i);
+  for (int li = 0; li < NLAY; ++li) {
+    const LayerOff& lo = M.layer[li];
+    float* b = sv + kVecLayer + li * kVecLStride;
+    for (int i = t; i < D; i += NTH) {
+      b[kVBQKV + i] = __ldg(P + lo.bq + i);
+      b[kVBQKV + D + i] = __ldg(P + lo.bk + i);
+      b[kVBQKV + 2 * D + i] = __ldg(P + lo.bv + i);
+      b[kVBO + i] = __ldg(P + lo.bo + i);
+      b[kVLN1G + i] = __ldg(P + lo.ln1g + i);
+      b[kVLN1B + i] = __ldg(P + lo.ln1b + i);
+      b[kVFOB + i] = __ldg(P + lo.fob + i);
+      b[kVLN2G + i] = __ldg(P + lo.ln2g + i);
+      b[kVLN2B + i] = __ldg(P + lo.ln2b + i);
+    }
+    for (int i = t; i < FF; i += NTH) b[kVFHB + i] = __ldg(P + lo.fhb + i);
+  }
+  mbar_wait(&bars[0], 0);
+  const uint32_t a_addr = smem_u32(sA), kv_addr = smem_u32(sKV), w_addr = smem_u32(smb);
+  const float scale = 1.f / sqrtf((float)DH);
+  uint32_t phase = 0;
+
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int L = tile_L[tile], first = tile_first[tile], A = tile_count[tile];
+    const int rows = A * L;
+    const bool live = t < rows;
+    float h[D];  // this row's residual stream (fp32)
+    {  // input rows → A operand (24 features, zero-padded to 64)
+      const float* xr = x + ((size_t)tile * TR + t) * TPCB_FEAT_PAD;
+      float v[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) v[i] = 0.f;
+      if (live)
+#pragma unroll
+        for (int i = 0; i < TPCB_FEAT; i += 4) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(xr + i));
+          v[i] = q.x; v[i + 1] = q.y; v[i + 2] = q.z; v[i + 3] = q.w;
+        }
+      store_row_bf16(sA, t, v);
+    }
+    sync_for_mma();
+    if (t == 0) {
+      const uint32_t at[1] = {a_addr}, bt[1] = {w_addr + kImgIn};
+      mma_chain(tmem, at, bt, 1, D);
+      mma_commit(&bars[1]);
+    }
+    wait_mma(&bars[1], phase);
+    tmem_ld32(tlane, h);
+    tmem_ld32(tlane + 32, h + 32);
+#pragma unroll
+    for (int i = 0; i < D; ++i) h[i] += sv[kVecIn + i];
+    store_row_bf16(sA, t, h);
+    sync_for_mma();
+
+    for (int li = 0; li < NLAY; ++li) {
+      const float* b = sv + kVecLayer + li * kVecLStride;
+      const uint32_t wl = w_addr + kImgLayer + li * kImgLStride;
+      if (t == 0) {  // Q | K | V
+        const uint32_t at[1] = {a_addr}, bt[1] = {wl + kQKV};
+        mma_chain(tmem, at, bt, 1, 3 * D);
+        mma_commit(&bars[1]);
+      }
+      wait_mma(&bars[1], phase);
+      float q[D];
+      tmem_ld32(tlane, q);
+      tmem_ld32(tlane + 32, q + 32);
+#pragma unroll
+      for (int i = 0; i < D; ++i) q[i] += b[kVBQKV + i];
+      {  // K, V rows → bf16 [row][K 0..63 | V 64..127]
+        float kv[D];
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(sKV) + t * 128;
+        for (int part = 0; part < 2; ++part) {
+          tmem_ld32(tlane + 64 + 64 * part, kv);
+          tmem_ld32(tlane + 96 + 64 * part, kv + 32);
+#pragma unroll
+          for (int i = 0; i < D; i += 2)
+            *reinterpret_cast<__nv_bfloat162*>(dst + 64 * part + i) = __floats2bfloat162_rn(
+                kv[i] + b[kVBQKV + (1 + part) * D + i], kv[i + 1] + b[kVBQKV + (1 + part) * D + i + 1]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      // attention of this query row over its AST's L keys (nn.py:79-96)
+      float c[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) c[i] = 0.f;
+      if (live) {
+        const int a = t / L, r0 = a * L;
+        const __nv_bfloat16* kvb = reinterpret_cast<const __nv_bfloat16*>(sKV);
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float s[16];
+          float m = -INFINITY;
+          for (int j = 0; j < L; ++j) {
+            const __nv_bfloat162* kr =
+                reinterpret_cast<const __nv_bfloat162*>(kvb + (r0 + j) * 128 + hh * DH);
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < DH / 2; ++i) {
+              const float2 kf = __bfloat1622float2(kr[i]);
+              acc = fmaf(q[hh * DH + 2 * i], kf.x, fmaf(q[hh * DH + 2 * i + 1], kf.y, acc));
+            }
+            s[j] = acc * scale;
+            m = fmaxf(m, s[j]);
+          }
+          float sum = 0.f;
+          for (int j = 0; j < L; ++j) {
+            s[j] = expf(s[j] - m);
+            sum += s[j];
+          }
+          const float inv = 1.f / sum;
+          for (int j = 0; j < L; ++j) {
+            const float p = s[j] * inv;
+            const __nv_bfloat162* vr =
+                reinterpret_cast<const __nv_bfloat162*>(kvb + (r0 + j) * 128 + D + hh * DH);
+#pragma unroll
+            for (int i = 0; i < DH / 2; ++i) {
+              const float2 vf = __bfloat1622float2(vr[i]);
+              c[hh * DH + 2 * i] = fmaf(p, vf.x, c[hh * DH + 2 * i]);
+              c[hh * DH + 2 * i + 1] = fmaf(p, vf.y, c[hh * DH + 2 * i + 1]);
+            }
+          }
+        }
+      }
+      store_row_bf16(sA, t, c);
+      sync_for_mma();
+      if (t == 0) {  // output projection
+        const uint32_t at[1] = {a_addr}, bt[1] = {wl + kWO};
+        mma_chain(tmem, at, bt, 1, D);
+        mma_commit(&bars[1]);
+      }
+      wait_mma(&bars[1], phase);
+      float h1[D];
+      tmem_ld32(tlane, h1);
+      tmem_ld32(tlane + 32, h1 + 32);
+#pragma unroll
+      for (int i = 0; i < D; ++i) h1[i] += b[kVBO + i] + h[i];
+      ln_row(h1, b + kVLN1G, b + kVLN1B);
+      store_row_bf16(sA, t, h1);
+      sync_for_mma();
+      if (t == 0) {  // FFN hidden (N = 128)
+        const uint32_t at[1] = {a_addr}, bt[1] = {wl + kFH};
+        mma_chain(tmem, at, bt, 1, FF);
+        mma_commit(&bars[1]);
+      }
+      wait_mma(&bars[1], phase);
+      {  // ReLU → F (two SW128 A tiles in the K|V region: the keys are dead)
+        float f[D];
+        for (int half = 0; half < 2; ++half) {
+          tmem_ld32(tlane + 64 * half, f);
+          tmem_ld32(tlane + 64 * half + 32, f + 32);
+#pragma unroll
+          for (int i = 0; i < D; ++i) f[i] = fmaxf(f[i] + b[kVFHB + 64 * half + i], 0.f);
+          store_row_bf16(sKV + half * TR * 128, t, f);
+        }
+      }
+      sync_for_mma();
+      if (t == 0) {  // FFN out (K = 128)
+        const uint32_t at[2] = {kv_addr, kv_addr + TR * 128},
+                       bt[2] = {wl + kFO0, wl + kFO1};
+        mma_chain(tmem, at, bt, 2, D);
+        mma_commit(&bars[1]);
+      }
+      wait_mma(&bars[1], phase);
+      tmem_ld32(tlane, h);
+      tmem_ld32(tlane + 32, h + 32);
+#pragma unroll
+      for (int i = 0; i < D; ++i) h[i] += b[kVFOB + i] + h1[i];
+      ln_row(h, b + kVLN2G, b + kVLN2B);
+      if (li + 1 < NLAY) {
+        store_row_bf16(sA, t, h);
+        sync_for_mma();
+      }
+    }
+    // ------------------------------------------------------------- head (fp32)
+#pragma unroll
+    for (int i = 0; i < D; ++i) sH[t * 65 + i] = h[i];
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (t < A) {  // thread = AST
+      const int a = t;
+      const float* W = P + M.leafW[L];
+      float zx[DE];
+#pragma unroll
+      for (int n = 0; n < DE; ++n) zx[n] = __ldg(P + M.leafb[L] + n);
+      for (int l = 0; l < L; ++l) {
+        const float* hr = sH + (a * L + l) * 65;
+        for (int k = 0; k < D; ++k) {
+          const float hv = hr[k];
+          const float4* wr = reinterpret_cast<const float4*>(W + (size_t)(l * D + k) * DE);
+#pragma unroll
+          for (int n4 = 0; n4 < DE / 4; ++n4) {
+            const float4 w4 = __ldg(wr + n4);
+            zx[4 * n4] = fmaf(hv, w4.x, zx[4 * n4]);
+            zx[4 * n4 + 1] = fmaf(hv, w4.y, zx[4 * n4 + 1]);
+            zx[4 * n4 + 2] = fmaf(hv, w4.z, zx[4 * n4 + 2]);
+            zx[4 * n4 + 3] = fmaf(hv, w4.w, zx[4 * n4 + 3]);
+          }
+        }
+      }
+      const int idx = perm[first + a];
+      float dv[TPCB_DEV_FEAT];
+#pragma unroll
+      for (int f = 0; f < TPCB_DEV_FEAT; ++f) dv[f] = __ldg(devfeat + (size_t)idx * TPCB_DEV_FEAT + f);
+      float zv[DDEV];
+#pragma unroll
+      for (int n = 0; n < DDEV; ++n) {
+        float s = __ldg(P + M.devhb + n);
+#pragma unroll
+        for (int f = 0; f < TPCB_DEV_FEAT; ++f) s = fmaf(dv[f], __ldg(P + M.devhW + f * DDEV + n), s);
+        zv[n] = fmaxf(s, 0.f);
+      }
+      float z[DE];
+#pragma unroll
+      for (int n = 0; n < DE; ++n) {
+        float s = __ldg(P + M.devpb + n);
+#pragma unroll
+        for (int k = 0; k < DDEV; ++k) s = fmaf(zv[k], __ldg(P + M.devpW + k * DE + n), s);
+        z[n] = zx[n] * s;
+      }
+      float u1[DEC];
+#pragma unroll
+      for (int n = 0; n < DEC; ++n) u1[n] = __ldg(P + M.decb[0] + n);
+      for (int k = 0; k < DE; ++k) {
+        const float zk = z[k];
+        const float4* wr = reinterpret_cast<const float4*>(P + M.decW[0] + k * DEC);
+#pragma unroll
+        for (int n4 = 0; n4 < DEC / 4; ++n4) {
+          const float4 w4 = __ldg(wr + n4);
+          u1[4 * n4] = fmaf(zk, w4.x, u1[4 * n4]);
+          u1[4 * n4 + 1] = fmaf(zk, w4.y, u1[4 * n4 + 1]);
+          u1[4 * n4 + 2] = fmaf(zk, w4.z, u1[4 * n4 + 2]);
+          u1[4 * n4 + 3] = fmaf(zk, w4.w, u1[4 * n4 + 3]);
+        }
+      }
+#pragma unroll
+      for (int n = 0; n < DEC; ++n) u1[n] = fmaxf(u1[n], 0.f);
+      float u2[DEC];
+#pragma unroll
+      for (int n = 0; n < DEC; ++n) u2[n] = __ldg(P + M.decb[1] + n);
+      for (int k = 0; k < DEC; ++k) {
+        const float uk = u1[k];
+        const float4* wr = reinterpret_cast<const float4*>(P + M.decW[1] + k * DEC);
+#pragma unroll
+        for (int n4 = 0; n4 < DEC / 4; ++n4) {
+          const float4 w4 = __ldg(wr + n4);
+          u2[4 * n4] = fmaf(uk, w4.x, u2[4 * n4]);
+          u2[4 * n4 + 1] = fmaf(uk, w4.y, u2[4 * n4 + 1]);
+          u2[4 * n4 + 2] = fmaf(uk, w4.z, u2[4 * n4 + 2]);
+          u2[4 * n4 + 3] = fmaf(uk, w4.w, u2[4 * n4 + 3]);
+        }
+      }
+      float pred = __ldg(P + M.outb);
+#pragma unroll
+      for (int k = 0; k < DEC; ++k) pred = fmaf(fmaxf(u2[k], 0.f), __ldg(P + M.outW + k), pred);
+      pred_out[idx] = pred;
+      if (lat_out) {
+        bool bad = false;
+        lat_out[idx] = bc.enabled ? boxcox_decode_tc((double)pred, bc, &bad) : (double)pred;
+        if (bad) raise_status(status, TPCB_ERR_DOMAIN);
+      }
+      if (zx_out)
+        for (int n = 0; n < DE; ++n) zx_out[(size_t)idx * DE + n] = zx[n];
+      if (z_out)
+        for (int n = 0; n < DE; ++n) z_out[(size_t)idx * DE + n] = z[n];
+      if (zv_out)
+        for (int n = 0; n < DDEV; ++n) zv_out[(size_t)idx * DDEV + n] = zv[n];
+    }
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+bool tc_supported(const Model& M) {
+  if (M.d != D || M.n_layers != NLAY || M.n_heads != 2 || M.dh != DH || M.d_ff != FF) return false;
+  if (M.d_e != DE || M.d_dev != DDEV || M.n_dec != 2 || M.dec[0] != DEC || M.dec[1] != DEC)
+    return false;
+  return M.n_leaf_max <= 16;
+}
+
+}  // namespace
+
+}  // namespace tpcb
+
+using namespace tpcb;
+
+/* bf16 tensor-core forward (C5 mode): same contract as tpcb_forward, desk-shaped
+ * models, rows_per_tile must be 128; d_img: caller workspace of
+ * tpcb_forward_bf16_workspace() bytes (the bf16 weight image, rebuilt per call). */
+extern "C" size_t tpcb_forward_bf16_workspace(void) { return (size_t)kImgBytes; }
+
+extern "C" int tpcb_forward_bf16(const tpcb_model* m, const float* d_params, const tpcb_packed* pk,
+                                 const float* d_devfeat, int64_t n_ast, const tpcb_boxcox* norm,
+                                 void* d_img, float* d_pred, float* d_zx, float* d_zv, float* d_z,
+                                 double* d_latency, int32_t* d_status, void* stream_) {
+  if (!m || !pk || !d_params || !d_pred || !d_devfeat || !d_img) return TPCB_ERR_VALIDATION;
+  if (n_ast < 1) return TPCB_ERR_EMPTY_BATCH;
+  if (!tc_supported(m->dev) || pk->rows_per_tile != TR) return TPCB_ERR_UNSUPPORTED;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  static bool attr = false;
+  if (!attr) {
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(forward_tc_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTotal));
+    attr = true;
+  }
+  prep_weights_kernel<<<2 * kNumSMs, 256, 0, stream>>>(m->dev, d_params,
+                                                       static_cast<uint8_t*>(d_img));
+  TPCB_LAUNCH_CHECK("prep_weights_kernel");
+  tpcb_boxcox bc{};
+  if (norm) bc = *norm;
+  const int grid = (int)std::min<int64_t>(pk->n_tiles_max, (int64_t)kNumSMs);
+  forward_tc_kernel<<<grid, NTH, kSmTotal, stream>>>(
+      m->dev, d_params, static_cast<const uint8_t*>(d_img), pk->x, pk->tile_L, pk->tile_first,
+      pk->tile_count, pk->n_tiles, pk->perm, d_devfeat, bc, d_pred, d_zx, d_zv, d_z, d_latency,
+      d_status);
+  TPCB_LAUNCH_CHECK("forward_tc_kernel");
+  return TPCB_OK;
+}

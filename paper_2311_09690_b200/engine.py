@@ -221,8 +221,10 @@ def boxcox_struct(norm) -> _lib.BoxCox:
 
 
 def run_forward(dm: DeviceModel, params: torch.Tensor, pk: PackedBatch, devfeat: torch.Tensor,
-                status: Status, norm=None, latents: bool = True):
-    """Launch the fused forward; returns device tensors (pred, z_x, z_v, z, lat)."""
+                status: Status, norm=None, latents: bool = True, precision: str = "fp32"):
+    """Launch the fused forward; returns device tensors (pred, z_x, z_v, z, lat).
+    precision "fp32": FP32 parity mode (tpcb_forward); "bf16": encoder GEMMs on
+    the tcgen05 tensor cores (tpcb_forward_bf16; desk config, 128-row tiles)."""
     lib = _lib.load()
     n = pk.n_ast
     dev = params.device
@@ -232,11 +234,32 @@ def run_forward(dm: DeviceModel, params: torch.Tensor, pk: PackedBatch, devfeat:
     z = torch.empty((n, dm.cfg.d_embed), dtype=torch.float32, device=dev) if latents else None
     lat = torch.empty(n, dtype=torch.float64, device=dev) if norm is not None else None
     bc = boxcox_struct(norm)
+    if precision == "bf16":
+        img = _bf16_image(dev)
+        _lib.check(lib.tpcb_forward_bf16(dm.handle, params.data_ptr(), C.byref(pk.struct),
+                                         devfeat.data_ptr(), n, C.byref(bc), img.data_ptr(),
+                                         pred.data_ptr(), dptr(zx), dptr(zv), dptr(z), dptr(lat),
+                                         status.ptr, stream_ptr()), "forward_bf16")
+        return pred, zx, zv, z, lat
+    if precision != "fp32":
+        raise E.ValidationError(f"unknown precision {precision!r}")
     _lib.check(lib.tpcb_forward(dm.handle, params.data_ptr(), C.byref(pk.struct),
                                 devfeat.data_ptr(), n, C.byref(bc), pred.data_ptr(), dptr(zx),
                                 dptr(zv), dptr(z), dptr(lat), status.ptr, stream_ptr()),
                "forward")
     return pred, zx, zv, z, lat
+
+
+_BF16_IMG = {}
+
+
+def _bf16_image(dev) -> torch.Tensor:
+    """Per-device workspace for the bf16 weight image (rebuilt on every call)."""
+    key = str(dev)
+    if key not in _BF16_IMG:
+        n = int(_lib.load().tpcb_forward_bf16_workspace())
+        _BF16_IMG[key] = torch.empty(n, dtype=torch.uint8, device=dev)
+    return _BF16_IMG[key]
 
 
 def positional_encoding_device(ordering: np.ndarray, theta: float) -> np.ndarray:
