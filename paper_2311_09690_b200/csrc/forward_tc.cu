@@ -5,9 +5,10 @@
 // Same network and outputs as forward.cu (reference: costmodel.py:193-269,
 // nn.py:26-96, dataset.py:97-115); only the encoder GEMM operands are rounded
 // to bf16 (fp32 accumulation).  LayerNorm, softmax, residuals, the leaf /
-// device / decoder head and the Box-Cox decode stay in fp32 / fp64.  The
+// device head and the Box-Cox decode stay in fp32 / fp64.  The
 // accuracy of this mode is stated separately from the fp32 parity mode
-// (tests/test_gpu_forward_bf16.py).
+// (tests/test_gpu_forward_bf16.py).  The decoder GEMMs (one AST per row)
+// also run on the tensor cores.
 //
 // Layout.  One CTA (4 warps, thread r = row r) per 128-row packed tile
 // (rows_per_tile = 128: floor(128/L) whole ASTs of one leaf count),
@@ -45,13 +46,15 @@ constexpr int kFH = 4 * kTileB;                 // N=128
 constexpr int kFO0 = 6 * kTileB;                // N=64, k = 0..63 of foW
 constexpr int kFO1 = 7 * kTileB;                // N=64, k = 64..127
 constexpr int kImgLStride = 8 * kTileB;
-constexpr int kImgBytes = kImgLayer + NLAY * kImgLStride;  // 139,264
+constexpr int kImgDec0 = kImgLayer + NLAY * kImgLStride;  // decoder 0: N=64, K=32 (zero-padded)
+constexpr int kImgDec1 = kImgDec0 + kTileB;              // decoder 1: N=64, K=64
+constexpr int kImgBytes = kImgDec1 + kTileB;              // 155,648
 
 // ---- shared memory (bytes, dynamic) ----
 constexpr int kSmA = kImgBytes;                 // A operand [128][64] bf16, SW128 (16 KB)
-constexpr int kSmKV = kSmA + TR * 128;          // K|V bf16 [128][128] row-major, later F (32 KB)
-constexpr int kSmH = kSmKV + TR * 256;          // encoder output fp32 [128][65]
-constexpr int kSmVec = kSmH + TR * 65 * 4;      // biases / LN vectors fp32
+constexpr int kKVLd = 136;                      // K|V row stride (bf16): 272 B, conflict-free 16-B accesses
+constexpr int kSmKV = kSmA + TR * 128;          // K|V bf16 [128][136], later F (two SW128 tiles)
+constexpr int kSmVec = kSmKV + TR * kKVLd * 2;  // biases / LN vectors fp32
 constexpr int kVecIn = 0, kVecLayer = 64, kVecLStride = 704;  // (same order as train4)
 constexpr int kVBQKV = 0, kVBO = 192, kVLN1G = 256, kVLN1B = 320, kVFHB = 384, kVFOB = 512,
               kVLN2G = 576, kVLN2B = 640;
@@ -186,6 +189,10 @@ __global__ void prep_weights_kernel(const Model M, const float* __restrict__ P,
     float v = 0.f;
     if (tile == 0) {
       v = k < TPCB_FEAT ? P[M.inW + k * D + n_local] : 0.f;
+    } else if (tile == kImgDec0 / kTileB) {
+      v = k < DE ? P[M.decW[0] + k * DEC + n_local] : 0.f;
+    } else if (tile == kImgDec1 / kTileB) {
+      v = P[M.decW[1] + k * DEC + n_local];
     } else {
       const int li = (tile - 1) / 8, t = (tile - 1) % 8;
       const LayerOff& lo = M.layer[li];
@@ -205,6 +212,14 @@ __global__ void prep_weights_kernel(const Model M, const float* __restrict__ P,
   }
 }
 
+__device__ long long* g_trace_tc = nullptr;
+// debug: per-phase timestamps of CTA 0 / thread 0 for its first 8 tiles
+#define TT(id)                                                                   \
+  do {                                                                           \
+    if (g_trace_tc && blockIdx.x == 0 && t == 0 && tcount < 8)                   \
+      g_trace_tc[tcount * 32 + (id)] = clock64();                                \
+  } while (0)
+
 __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     const __grid_constant__ Model M, const float* __restrict__ P,
     const uint8_t* __restrict__ img, const float* __restrict__ x,
@@ -220,7 +235,6 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
   const int n_tiles = *n_tiles_p;
   uint8_t* sA = smb + kSmA;
   uint8_t* sKV = smb + kSmKV;
-  float* sH = reinterpret_cast<float*>(smb + kSmH);
   float* sv = reinterpret_cast<float*>(smb + kSmVec);
   if (t == 0) {
     mbar_init(&bars[0], 1);
@@ -265,7 +279,10 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
   const float scale = 1.f / sqrtf((float)DH);
   uint32_t phase = 0;
 
+  int tcount = -1;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    ++tcount;
+    TT(0);
     const int L = tile_L[tile], first = tile_first[tile], A = tile_count[tile];
     const int rows = A * L;
     const bool live = t < rows;
@@ -284,18 +301,21 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       store_row_bf16(sA, t, v);
     }
     sync_for_mma();
+    TT(1);
     if (t == 0) {
       const uint32_t at[1] = {a_addr}, bt[1] = {w_addr + kImgIn};
       mma_chain(tmem, at, bt, 1, D);
       mma_commit(&bars[1]);
     }
     wait_mma(&bars[1], phase);
+    TT(2);
     tmem_ld32(tlane, h);
     tmem_ld32(tlane + 32, h + 32);
 #pragma unroll
     for (int i = 0; i < D; ++i) h[i] += sv[kVecIn + i];
     store_row_bf16(sA, t, h);
     sync_for_mma();
+    TT(3);
 
     for (int li = 0; li < NLAY; ++li) {
       const float* b = sv + kVecLayer + li * kVecLStride;
@@ -306,21 +326,32 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
         mma_commit(&bars[1]);
       }
       wait_mma(&bars[1], phase);
+      TT(4 + li * 12);
       float q[D];
       tmem_ld32(tlane, q);
       tmem_ld32(tlane + 32, q + 32);
 #pragma unroll
       for (int i = 0; i < D; ++i) q[i] += b[kVBQKV + i];
-      {  // K, V rows → bf16 [row][K 0..63 | V 64..127]
+      {  // K, V rows → bf16 [row][K 0..63 | V 64..127] (16-byte stores)
         float kv[D];
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(sKV) + t * 128;
+        uint8_t* dst = sKV + t * kKVLd * 2;
         for (int part = 0; part < 2; ++part) {
           tmem_ld32(tlane + 64 + 64 * part, kv);
           tmem_ld32(tlane + 96 + 64 * part, kv + 32);
 #pragma unroll
-          for (int i = 0; i < D; i += 2)
-            *reinterpret_cast<__nv_bfloat162*>(dst + 64 * part + i) = __floats2bfloat162_rn(
-                kv[i] + b[kVBQKV + (1 + part) * D + i], kv[i + 1] + b[kVBQKV + (1 + part) * D + i + 1]);
+          for (int c = 0; c < 8; ++c) {
+            const float* bb = b + kVBQKV + (1 + part) * D + 8 * c;
+            __nv_bfloat162 p0 = __floats2bfloat162_rn(kv[8 * c] + bb[0], kv[8 * c + 1] + bb[1]);
+            __nv_bfloat162 p1 = __floats2bfloat162_rn(kv[8 * c + 2] + bb[2], kv[8 * c + 3] + bb[3]);
+            __nv_bfloat162 p2 = __floats2bfloat162_rn(kv[8 * c + 4] + bb[4], kv[8 * c + 5] + bb[5]);
+            __nv_bfloat162 p3 = __floats2bfloat162_rn(kv[8 * c + 6] + bb[6], kv[8 * c + 7] + bb[7]);
+            uint4 u;
+            u.x = *reinterpret_cast<uint32_t*>(&p0);
+            u.y = *reinterpret_cast<uint32_t*>(&p1);
+            u.z = *reinterpret_cast<uint32_t*>(&p2);
+            u.w = *reinterpret_cast<uint32_t*>(&p3);
+            *reinterpret_cast<uint4*>(dst + (64 * part + 8 * c) * 2) = u;
+          }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -338,7 +369,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
           float m = -INFINITY;
           for (int j = 0; j < L; ++j) {
             const __nv_bfloat162* kr =
-                reinterpret_cast<const __nv_bfloat162*>(kvb + (r0 + j) * 128 + hh * DH);
+                reinterpret_cast<const __nv_bfloat162*>(kvb + (r0 + j) * kKVLd + hh * DH);
             float acc = 0.f;
 #pragma unroll
             for (int i = 0; i < DH / 2; ++i) {
@@ -357,7 +388,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
           for (int j = 0; j < L; ++j) {
             const float p = s[j] * inv;
             const __nv_bfloat162* vr =
-                reinterpret_cast<const __nv_bfloat162*>(kvb + (r0 + j) * 128 + D + hh * DH);
+                reinterpret_cast<const __nv_bfloat162*>(kvb + (r0 + j) * kKVLd + D + hh * DH);
 #pragma unroll
             for (int i = 0; i < DH / 2; ++i) {
               const float2 vf = __bfloat1622float2(vr[i]);
@@ -369,12 +400,14 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       }
       store_row_bf16(sA, t, c);
       sync_for_mma();
+      TT(5 + li * 12);
       if (t == 0) {  // output projection
         const uint32_t at[1] = {a_addr}, bt[1] = {wl + kWO};
         mma_chain(tmem, at, bt, 1, D);
         mma_commit(&bars[1]);
       }
       wait_mma(&bars[1], phase);
+      TT(6 + li * 12);
       float h1[D];
       tmem_ld32(tlane, h1);
       tmem_ld32(tlane + 32, h1 + 32);
@@ -383,12 +416,14 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       ln_row(h1, b + kVLN1G, b + kVLN1B);
       store_row_bf16(sA, t, h1);
       sync_for_mma();
+      TT(7 + li * 12);
       if (t == 0) {  // FFN hidden (N = 128)
         const uint32_t at[1] = {a_addr}, bt[1] = {wl + kFH};
         mma_chain(tmem, at, bt, 1, FF);
         mma_commit(&bars[1]);
       }
       wait_mma(&bars[1], phase);
+      TT(8 + li * 12);
       {  // ReLU → F (two SW128 A tiles in the K|V region: the keys are dead)
         float f[D];
         for (int half = 0; half < 2; ++half) {
@@ -400,6 +435,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
         }
       }
       sync_for_mma();
+      TT(9 + li * 12);
       if (t == 0) {  // FFN out (K = 128)
         const uint32_t at[2] = {kv_addr, kv_addr + TR * 128},
                        bt[2] = {wl + kFO0, wl + kFO1};
@@ -407,6 +443,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
         mma_commit(&bars[1]);
       }
       wait_mma(&bars[1], phase);
+      TT(10 + li * 12);
       tmem_ld32(tlane, h);
       tmem_ld32(tlane + 32, h + 32);
 #pragma unroll
@@ -415,95 +452,68 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       if (li + 1 < NLAY) {
         store_row_bf16(sA, t, h);
         sync_for_mma();
+        TT(11 + li * 12);
       }
     }
-    // ------------------------------------------------------------- head (fp32)
-#pragma unroll
-    for (int i = 0; i < D; ++i) sH[t * 65 + i] = h[i];
+    TT(30);
+    // ---------------------------------------------------------------- head
+    // leaf_embed: each row's partial H_l · W_L[l] (fp32, CUDA cores), summed
+    // in row order by the AST's first thread with the device MLP and the gate;
+    // the decoder then runs on the tensor cores with one AST per TMEM lane.
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (t < A) {  // thread = AST
-      const int a = t;
-      const float* W = P + M.leafW[L];
-      float zx[DE];
+    __syncthreads();  // (the last encoder epilogue may still read K|V / A)
+    float* s_part = reinterpret_cast<float*>(sKV);  // [128][33] leaf_embed partials
+    const int a = t / L, l = t - a * L;
+    if (live) {
+      const float* W = P + M.leafW[L] + (size_t)l * D * DE;
+      float part[DE];
 #pragma unroll
-      for (int n = 0; n < DE; ++n) zx[n] = __ldg(P + M.leafb[L] + n);
-      for (int l = 0; l < L; ++l) {
-        const float* hr = sH + (a * L + l) * 65;
-        for (int k = 0; k < D; ++k) {
-          const float hv = hr[k];
-          const float4* wr = reinterpret_cast<const float4*>(W + (size_t)(l * D + k) * DE);
+      for (int n = 0; n < DE; ++n) part[n] = 0.f;
+#pragma unroll 4
+      for (int k = 0; k < D; ++k) {
+        const float hv = h[k];
+        const float4* wr = reinterpret_cast<const float4*>(W + (size_t)k * DE);
 #pragma unroll
-          for (int n4 = 0; n4 < DE / 4; ++n4) {
-            const float4 w4 = __ldg(wr + n4);
-            zx[4 * n4] = fmaf(hv, w4.x, zx[4 * n4]);
-            zx[4 * n4 + 1] = fmaf(hv, w4.y, zx[4 * n4 + 1]);
-            zx[4 * n4 + 2] = fmaf(hv, w4.z, zx[4 * n4 + 2]);
-            zx[4 * n4 + 3] = fmaf(hv, w4.w, zx[4 * n4 + 3]);
-          }
+        for (int n4 = 0; n4 < DE / 4; ++n4) {
+          const float4 w4 = __ldg(wr + n4);
+          part[4 * n4] = fmaf(hv, w4.x, part[4 * n4]);
+          part[4 * n4 + 1] = fmaf(hv, w4.y, part[4 * n4 + 1]);
+          part[4 * n4 + 2] = fmaf(hv, w4.z, part[4 * n4 + 2]);
+          part[4 * n4 + 3] = fmaf(hv, w4.w, part[4 * n4 + 3]);
         }
       }
+#pragma unroll
+      for (int n = 0; n < DE; ++n) s_part[t * 33 + n] = part[n];
+    }
+    __syncthreads();
+    if (live && l == 0) {  // z_x (rows of the AST in order), device MLP, gate → decoder operand row a
       const int idx = perm[first + a];
+      float zx[DE], zv[DDEV], z[D];
+#pragma unroll
+      for (int n = 0; n < DE; ++n) zx[n] = __ldg(P + M.leafb[L] + n);
+      for (int j = 0; j < L; ++j)
+#pragma unroll
+        for (int n = 0; n < DE; ++n) zx[n] += s_part[(t + j) * 33 + n];
       float dv[TPCB_DEV_FEAT];
 #pragma unroll
       for (int f = 0; f < TPCB_DEV_FEAT; ++f) dv[f] = __ldg(devfeat + (size_t)idx * TPCB_DEV_FEAT + f);
-      float zv[DDEV];
 #pragma unroll
       for (int n = 0; n < DDEV; ++n) {
-        float s = __ldg(P + M.devhb + n);
+        float sacc = __ldg(P + M.devhb + n);
 #pragma unroll
-        for (int f = 0; f < TPCB_DEV_FEAT; ++f) s = fmaf(dv[f], __ldg(P + M.devhW + f * DDEV + n), s);
-        zv[n] = fmaxf(s, 0.f);
+        for (int f = 0; f < TPCB_DEV_FEAT; ++f) sacc = fmaf(dv[f], __ldg(P + M.devhW + f * DDEV + n), sacc);
+        zv[n] = fmaxf(sacc, 0.f);
       }
-      float z[DE];
 #pragma unroll
       for (int n = 0; n < DE; ++n) {
-        float s = __ldg(P + M.devpb + n);
+        float sacc = __ldg(P + M.devpb + n);
 #pragma unroll
-        for (int k = 0; k < DDEV; ++k) s = fmaf(zv[k], __ldg(P + M.devpW + k * DE + n), s);
-        z[n] = zx[n] * s;
-      }
-      float u1[DEC];
-#pragma unroll
-      for (int n = 0; n < DEC; ++n) u1[n] = __ldg(P + M.decb[0] + n);
-      for (int k = 0; k < DE; ++k) {
-        const float zk = z[k];
-        const float4* wr = reinterpret_cast<const float4*>(P + M.decW[0] + k * DEC);
-#pragma unroll
-        for (int n4 = 0; n4 < DEC / 4; ++n4) {
-          const float4 w4 = __ldg(wr + n4);
-          u1[4 * n4] = fmaf(zk, w4.x, u1[4 * n4]);
-          u1[4 * n4 + 1] = fmaf(zk, w4.y, u1[4 * n4 + 1]);
-          u1[4 * n4 + 2] = fmaf(zk, w4.z, u1[4 * n4 + 2]);
-          u1[4 * n4 + 3] = fmaf(zk, w4.w, u1[4 * n4 + 3]);
-        }
+        for (int k = 0; k < DDEV; ++k) sacc = fmaf(zv[k], __ldg(P + M.devpW + k * DE + n), sacc);
+        z[n] = zx[n] * sacc;
       }
 #pragma unroll
-      for (int n = 0; n < DEC; ++n) u1[n] = fmaxf(u1[n], 0.f);
-      float u2[DEC];
-#pragma unroll
-      for (int n = 0; n < DEC; ++n) u2[n] = __ldg(P + M.decb[1] + n);
-      for (int k = 0; k < DEC; ++k) {
-        const float uk = u1[k];
-        const float4* wr = reinterpret_cast<const float4*>(P + M.decW[1] + k * DEC);
-#pragma unroll
-        for (int n4 = 0; n4 < DEC / 4; ++n4) {
-          const float4 w4 = __ldg(wr + n4);
-          u2[4 * n4] = fmaf(uk, w4.x, u2[4 * n4]);
-          u2[4 * n4 + 1] = fmaf(uk, w4.y, u2[4 * n4 + 1]);
-          u2[4 * n4 + 2] = fmaf(uk, w4.z, u2[4 * n4 + 2]);
-          u2[4 * n4 + 3] = fmaf(uk, w4.w, u2[4 * n4 + 3]);
-        }
-      }
-      float pred = __ldg(P + M.outb);
-#pragma unroll
-      for (int k = 0; k < DEC; ++k) pred = fmaf(fmaxf(u2[k], 0.f), __ldg(P + M.outW + k), pred);
-      pred_out[idx] = pred;
-      if (lat_out) {
-        bool bad = false;
-        lat_out[idx] = bc.enabled ? boxcox_decode_tc((double)pred, bc, &bad) : (double)pred;
-        if (bad) raise_status(status, TPCB_ERR_DOMAIN);
-      }
+      for (int n = DE; n < D; ++n) z[n] = 0.f;
+      store_row_bf16(sA, a, z);
       if (zx_out)
         for (int n = 0; n < DE; ++n) zx_out[(size_t)idx * DE + n] = zx[n];
       if (z_out)
@@ -511,6 +521,48 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       if (zv_out)
         for (int n = 0; n < DDEV; ++n) zv_out[(size_t)idx * DDEV + n] = zv[n];
     }
+    sync_for_mma();
+    // decoder on the tensor cores, one AST per row / TMEM lane / thread
+    if (t == 0) {
+      const uint32_t at[1] = {a_addr}, bt[1] = {w_addr + kImgDec0};
+      mma_chain(tmem, at, bt, 1, DEC);
+      mma_commit(&bars[1]);
+    }
+    wait_mma(&bars[1], phase);
+    {
+      float u[DEC];
+      tmem_ld32(tlane, u);
+      tmem_ld32(tlane + 32, u + 32);
+#pragma unroll
+      for (int j = 0; j < DEC; ++j) u[j] = fmaxf(u[j] + __ldg(P + M.decb[0] + j), 0.f);
+      store_row_bf16(sA, t, u);
+    }
+    sync_for_mma();
+    if (t == 0) {
+      const uint32_t at[1] = {a_addr}, bt[1] = {w_addr + kImgDec1};
+      mma_chain(tmem, at, bt, 1, DEC);
+      mma_commit(&bars[1]);
+    }
+    wait_mma(&bars[1], phase);
+    {
+      float u[DEC];
+      tmem_ld32(tlane, u);
+      tmem_ld32(tlane + 32, u + 32);
+      if (t < A) {
+        float pred = __ldg(P + M.outb);
+#pragma unroll
+        for (int j = 0; j < DEC; ++j)
+          pred = fmaf(fmaxf(u[j] + __ldg(P + M.decb[1] + j), 0.f), __ldg(P + M.outW + j), pred);
+        const int idx = perm[first + t];
+        pred_out[idx] = pred;
+        if (lat_out) {
+          bool bad = false;
+          lat_out[idx] = bc.enabled ? boxcox_decode_tc((double)pred, bc, &bad) : (double)pred;
+          if (bad) raise_status(status, TPCB_ERR_DOMAIN);
+        }
+      }
+    }
+    TT(31);
     __syncthreads();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -535,6 +587,13 @@ using namespace tpcb;
  * models, rows_per_tile must be 128; d_img: caller workspace of
  * tpcb_forward_bf16_workspace() bytes (the bf16 weight image, rebuilt per call). */
 extern "C" size_t tpcb_forward_bf16_workspace(void) { return (size_t)kImgBytes; }
+
+namespace tpcb {
+int set_forward_tc_trace(long long* d) {
+  TPCB_CUDA_CHECK(cudaMemcpyToSymbol(g_trace_tc, &d, sizeof(d)));
+  return TPCB_OK;
+}
+}  // namespace tpcb
 
 extern "C" int tpcb_forward_bf16(const tpcb_model* m, const float* d_params, const tpcb_packed* pk,
                                  const float* d_devfeat, int64_t n_ast, const tpcb_boxcox* norm,

@@ -4,10 +4,9 @@
       target = shifted valid+test (criterion-7 shift), alpha 1, K 5, bs 64+64
   C4  KMeans 1M × 1024 (d = 24 mean-pooled leaf vectors and d = 32 z_x),
       k-means++ + Lloyd to convergence; per-iteration time
-  C5  inference sweep n = 64 … 1M ASTs (fp32 parity mode; the bf16 mode is not
-      implemented yet)
+  C5  inference sweep n = 64 … 1M ASTs, fp32 parity mode and bf16 tensor-core mode
 
-python tools/bench_extra.py [c3] [c4] [c5]     (default: all)
+python tools/bench_extra.py [c3] [c4] [c5] [c5bf16]     (default: all)
 """
 import json
 import sys
@@ -105,8 +104,8 @@ def c4():
     return out
 
 
-def c5():
-    p = pb.Predictor(pb.init_params(pb.desk_config(seed=0)))
+def c5(precision="fp32"):
+    p = pb.Predictor(pb.init_params(pb.desk_config(seed=0)), precision=precision)
     big = synth.generate(1 << 20, seed=0)
     res = {}
     for n in (64, 256, 1024, 4096, 16384, 65536, 262144, 1 << 20):
@@ -118,14 +117,15 @@ def c5():
             f()
         reps = 50 if n <= 65536 else 5
         res[str(n)] = n / dev_time(f, reps)
-    return {"metric": "C5 inference sweep ASTs/s (fp32 parity mode, K1 pack + fused forward)",
-            "unit": "ASTs/s", "by_n": res, "dtype": "f32",
-            "note": "bf16 tensor-core mode not implemented in this round"}
+    mode = {"fp32": "fp32 parity mode (FFMA)",
+            "bf16": "bf16 tensor-core mode (tcgen05, fp32 accumulate)"}[precision]
+    return {"metric": f"C5 inference sweep ASTs/s, {mode}, K1 pack + fused forward",
+            "unit": "ASTs/s", "by_n": res, "dtype": precision}
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c3", "c4", "c5"]
+    which = sys.argv[1:] or ["c3", "c4", "c5", "c5bf16"]
     for w in which:
-        r = {"c3": c3, "c4": c4, "c5": c5}[w]()
+        r = {"c3": c3, "c4": c4, "c5": c5, "c5bf16": lambda: c5("bf16")}[w]()
         for line in (r if isinstance(r, list) else [r]):
             print(json.dumps(line), flush=True)
