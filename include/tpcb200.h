@@ -280,6 +280,16 @@ int tpcb_kmeans_assign(const double* d_x, int64_t n, int32_t d, const double* d_
                        int32_t kappa, int64_t* d_assign, double* d_own, int32_t* d_counts,
                        void* stream);
 /* centres = member means in point order (empty clusters keep their centre) */
+/* K8, tensor-core mode: the same assignment (d <= 32) with the ranking score
+ * ||c||^2 - 2 x.c formed by a 3xTF32 tcgen05 GEMM, a fused per-point top-4 scan,
+ * and an exact float64 re-rank of the 4 candidates (numpy summation order).
+ * Equals tpcb_kmeans_assign whenever the true nearest centre is among the
+ * candidates (>= 99.9 % agreement required by the north_star; measured in
+ * tests/test_gpu_kmeans.py).  d_ws: tpcb_kmeans_assign_tc_ws(kappa) bytes. */
+size_t tpcb_kmeans_assign_tc_ws(int32_t kappa);
+int tpcb_kmeans_assign_tc(const double* d_x, int64_t n, int32_t d, const double* d_centers,
+                          int32_t kappa, int64_t* d_assign, double* d_own, int32_t* d_counts,
+                          void* d_ws, size_t ws_bytes, void* stream);
 int tpcb_kmeans_update(const double* d_x, int64_t n, int32_t d, int32_t kappa,
                        const int64_t* d_assign, const int32_t* d_counts, double* d_centers,
                        void* ws, size_t ws_bytes, void* stream);

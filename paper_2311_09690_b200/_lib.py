@@ -112,6 +112,8 @@ SIGNATURES = {
     "tpcb_kmeanspp_init": (i32, [vp, i64, i32, i64, vp, vp, vp, vp, sz, vp]),
     "tpcb_kmeanspp_step": (i32, [vp, i64, i32, i32, f64, i64, vp, vp, vp, vp, vp, sz, vp]),
     "tpcb_kmeans_assign": (i32, [vp, i64, i32, vp, i32, vp, vp, vp, vp]),
+    "tpcb_kmeans_assign_tc_ws": (C.c_size_t, [i32]),
+    "tpcb_kmeans_assign_tc": (i32, [vp, i64, i32, vp, i32, vp, vp, vp, vp, C.c_size_t, vp]),
     "tpcb_kmeans_update": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, sz, vp]),
     "tpcb_kmeans_changed": (i32, [vp, vp, i64, vp, vp]),
     "tpcb_distance_table": (i32, [vp, vp, i32, i32, vp, i32, vp, vp]),

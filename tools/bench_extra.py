@@ -3,10 +3,11 @@
   C3  CMD fine-tune training throughput: source = the C2 training split,
       target = shifted valid+test (criterion-7 shift), alpha 1, K 5, bs 64+64
   C4  KMeans 1M × 1024 (d = 24 mean-pooled leaf vectors and d = 32 z_x),
-      k-means++ + Lloyd to convergence; per-iteration time
+      k-means++ + Lloyd to convergence; per-iteration time; exact float64 and
+      tensor-core (3xTF32 + exact re-rank) assignment modes
   C5  inference sweep n = 64 … 1M ASTs, fp32 parity mode and bf16 tensor-core mode
 
-python tools/bench_extra.py [c3] [c4] [c5] [c5bf16]     (default: all)
+python tools/bench_extra.py [c3] [c4] [c4tc] [c5] [c5bf16]     (default: all)
 """
 import json
 import sys
@@ -73,7 +74,7 @@ def c3():
             "dtype": "f32 network, f64 CMD statistics"}
 
 
-def c4():
+def c4(assign="exact"):
     from paper_2311_09690_b200.sampling import DeviceKMeans
     out = []
     n, k = 1 << 20, 1024
@@ -84,7 +85,7 @@ def c4():
     _, zx, _, _, _ = p.forward_ragged(rag(data), None, latents=True)
     for name, x in (("d24 mean-pooled leaf vectors", pooled),
                     ("d32 z_x latents", zx.double().cpu().numpy())):
-        km = DeviceKMeans(np.ascontiguousarray(x), k)
+        km = DeviceKMeans(np.ascontiguousarray(x), k, assign=assign)
         rng = np.random.default_rng(0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -96,11 +97,21 @@ def c4():
         iters = km.lloyd()
         torch.cuda.synchronize()
         t_lloyd = time.perf_counter() - t0
-        flops = 3.0 * n * k * x.shape[1]
-        out.append({"metric": f"C4 KMeans {n}x{k} ({name})", "kmeanspp_s": t_pp,
-                    "lloyd_s": t_lloyd, "lloyd_iterations": iters,
-                    "assign_pass_ms": t_assign * 1e3,
-                    "assign_fp64_tflops": flops / t_assign / 1e12, "dtype": "f64"})
+        r = {"metric": f"C4 KMeans {n}x{k} ({name}), {assign} assignment", "kmeanspp_s": t_pp,
+             "lloyd_s": t_lloyd, "lloyd_iterations": iters, "assign_pass_ms": t_assign * 1e3}
+        if assign == "exact":
+            r["assign_fp64_tflops"] = 3.0 * n * k * x.shape[1] / t_assign / 1e12
+            r["dtype"] = "f64"
+        else:
+            r["assign_3xtf32_tflops"] = 3 * 2.0 * n * k * 32 / t_assign / 1e12
+            r["dtype"] = "3xTF32 candidates + f64 re-rank"
+            ex = DeviceKMeans(np.ascontiguousarray(x), k)
+            ex.centers.copy_(km.centers)
+            ex.assign_step()
+            km.assign_step()
+            r["agreement_vs_exact_same_centres"] = float(
+                (ex.assign == km.assign).double().mean().item())
+        out.append(r)
     return out
 
 
@@ -124,8 +135,9 @@ def c5(precision="fp32"):
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c3", "c4", "c5", "c5bf16"]
+    which = sys.argv[1:] or ["c3", "c4", "c4tc", "c5", "c5bf16"]
     for w in which:
-        r = {"c3": c3, "c4": c4, "c5": c5, "c5bf16": lambda: c5("bf16")}[w]()
+        r = {"c3": c3, "c4": c4, "c4tc": lambda: c4("tc"), "c5": c5,
+             "c5bf16": lambda: c5("bf16")}[w]()
         for line in (r if isinstance(r, list) else [r]):
             print(json.dumps(line), flush=True)
