@@ -294,6 +294,26 @@ int tpcb_kmeans_update(const double* d_x, int64_t n, int32_t d, int32_t kappa,
                        const int64_t* d_assign, const int32_t* d_counts, double* d_centers,
                        void* ws, size_t ws_bytes, void* stream);
 /* *d_flag = 1 if the two assignments differ */
+/* Data-parallel KMeans (point-sharded across ranks; sampling.kmeans_sharded,
+ * SURVEY 8(e)): the local pieces between the collectives.
+ *   closest: closest[i] = (init ? d : min(closest[i], d)) with d = dist^2(x_i, c);
+ *            d_total = sum of closest (fixed order)
+ *   cdf:     p = closest / *d_total (the global total), cdf = inclusive scan in
+ *            the workspace; *d_local_sum = cdf[n-1]
+ *   search:  first local j with (offset + cdf[j]) / total > u, -1 if none
+ *            (Generator.choice semantics over the concatenated shards)
+ *   partial: per-cluster member sums in point order [kappa, d] (the update
+ *            step's numerator; centres = all-reduced sums / all-reduced counts) */
+int tpcb_kmeanspp_closest(const double* d_x, int64_t n, int32_t d, const double* d_center,
+                          int32_t init, double* d_closest, double* d_total, void* ws,
+                          size_t ws_bytes, void* stream);
+int tpcb_kmeanspp_cdf(const double* d_closest, int64_t n, const double* d_total,
+                      double* d_local_sum, void* ws, size_t ws_bytes, void* stream);
+int tpcb_kmeanspp_search(int64_t n, double offset, double total, double u, int64_t* d_found,
+                         void* ws, size_t ws_bytes, void* stream);
+int tpcb_kmeans_partial(const double* d_x, int64_t n, int32_t d, int32_t kappa,
+                        const int64_t* d_assign, const int32_t* d_counts, double* d_sums,
+                        void* ws, size_t ws_bytes, void* stream);
 int tpcb_kmeans_changed(const int64_t* d_a, const int64_t* d_b, int64_t n, int32_t* d_flag,
                         void* stream);
 /* Ψ[e, t] = mean over rows of task t (rows d_task_off[t]..[t+1]) of the L2

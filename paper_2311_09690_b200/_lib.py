@@ -114,6 +114,11 @@ SIGNATURES = {
     "tpcb_kmeans_assign": (i32, [vp, i64, i32, vp, i32, vp, vp, vp, vp]),
     "tpcb_kmeans_assign_tc_ws": (C.c_size_t, [i32]),
     "tpcb_kmeans_assign_tc": (i32, [vp, i64, i32, vp, i32, vp, vp, vp, vp, C.c_size_t, vp]),
+    "tpcb_kmeanspp_closest": (i32, [vp, i64, i32, vp, i32, vp, vp, vp, C.c_size_t, vp]),
+    "tpcb_kmeanspp_cdf": (i32, [vp, i64, vp, vp, vp, C.c_size_t, vp]),
+    "tpcb_kmeanspp_search": (i32, [i64, C.c_double, C.c_double, C.c_double, vp, vp, C.c_size_t,
+                                   vp]),
+    "tpcb_kmeans_partial": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, C.c_size_t, vp]),
     "tpcb_kmeans_update": (i32, [vp, i64, i32, i32, vp, vp, vp, vp, sz, vp]),
     "tpcb_kmeans_changed": (i32, [vp, vp, i64, vp, vp]),
     "tpcb_distance_table": (i32, [vp, vp, i32, i32, vp, i32, vp, vp]),

@@ -248,6 +248,52 @@ __global__ void member_mean_kernel(const double* __restrict__ x, int d, int kapp
   centers[(size_t)c * d + k] = acc / (double)m;
 }
 
+// data-parallel k-means++: first local j with (offset + cdf[j]) / total > u
+__global__ void search_offset_kernel(const double* __restrict__ cdf, int64_t n, double offset,
+                                     double total, double u,
+                                     unsigned long long* __restrict__ found) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    if ((offset + cdf[j]) / total > u) {
+      atomicMin(found, (unsigned long long)j);
+      return;
+    }
+  }
+}
+
+__global__ void found_to_i64_kernel(const unsigned long long* __restrict__ found, int64_t n,
+                                    int64_t* __restrict__ out) {
+  const unsigned long long j = *found;
+  *out = j < (unsigned long long)n ? (int64_t)j : -1;
+}
+
+// data-parallel Lloyd: per-cluster member sums in point order (the partial
+// sums one rank contributes to the all-reduce; K9 without the division)
+__global__ void member_sum_kernel(const double* __restrict__ x, int d, int kappa,
+                                  const int32_t* __restrict__ sorted_idx,
+                                  const int32_t* __restrict__ offs,
+                                  const int32_t* __restrict__ counts, double* __restrict__ sums) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)kappa * d) return;
+  const int c = (int)(e / d), k = (int)(e - (int64_t)c * d);
+  const int m = counts[c];
+  double acc = 0.0;
+  if (m > 0) {  // same order as member_mean_kernel: first member, then in order
+    const int32_t* mem = sorted_idx + offs[c];
+    acc = x[(int64_t)mem[0] * d + k];
+    int r = 1;
+    for (; r + 8 <= m; r += 8) {
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = x[(int64_t)mem[r + j] * d + k];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, v[j]);
+    }
+    for (; r < m; ++r) acc = __dadd_rn(acc, x[(int64_t)mem[r] * d + k]);
+  }
+  sums[(size_t)c * d + k] = acc;
+}
+
 __global__ void compare_kernel(const int64_t* __restrict__ a, const int64_t* __restrict__ b,
                                int64_t n, int32_t* __restrict__ changed) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -439,6 +485,72 @@ extern "C" int tpcb_kmeans_changed(const int64_t* d_a, const int64_t* d_b, int64
   TPCB_CUDA_CHECK(cudaMemsetAsync(d_flag, 0, sizeof(int32_t), stream));
   compare_kernel<<<grid_for(n), 256, 0, stream>>>(d_a, d_b, n, d_flag);
   TPCB_LAUNCH_CHECK("kmeans_changed");
+  return TPCB_OK;
+}
+
+/* ---- data-parallel KMeans pieces (point-sharded; sampling.kmeans_sharded) ---- */
+
+extern "C" int tpcb_kmeanspp_closest(const double* d_x, int64_t n, int32_t d,
+                                     const double* d_center, int32_t init, double* d_closest,
+                                     double* d_total, void* ws, size_t ws_bytes, void* stream_) {
+  if (!d_x || !d_center || !d_closest || !d_total || !ws) return TPCB_ERR_VALIDATION;
+  if (d > kMaxDim) return TPCB_ERR_UNSUPPORTED;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KWs w = carve(ws, ws_bytes, n, 1);
+  const int g = std::min(grid_for(n), 4096);
+  closest_update_kernel<<<g, 256, 0, stream>>>(d_x, n, d, d_center, d_closest, init ? 1 : 0,
+                                               w.part);
+  sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
+  TPCB_LAUNCH_CHECK("kmeanspp_closest");
+  return TPCB_OK;
+}
+
+extern "C" int tpcb_kmeanspp_cdf(const double* d_closest, int64_t n, const double* d_total,
+                                 double* d_local_sum, void* ws, size_t ws_bytes, void* stream_) {
+  if (!d_closest || !d_total || !d_local_sum || !ws) return TPCB_ERR_VALIDATION;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KWs w = carve(ws, ws_bytes, n, 1);
+  div_kernel<<<grid_for(n), 256, 0, stream>>>(d_closest, d_total, w.p, n);
+  size_t tb = w.tmp_bytes;
+  TPCB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(w.tmp, tb, w.p, w.cdf, (int)n, stream));
+  TPCB_CUDA_CHECK(cudaMemcpyAsync(d_local_sum, w.cdf + (n - 1), sizeof(double),
+                                  cudaMemcpyDeviceToDevice, stream));
+  TPCB_LAUNCH_CHECK("kmeanspp_cdf");
+  return TPCB_OK;
+}
+
+extern "C" int tpcb_kmeanspp_search(int64_t n, double offset, double total, double u,
+                                    int64_t* d_found, void* ws, size_t ws_bytes, void* stream_) {
+  if (!d_found || !ws) return TPCB_ERR_VALIDATION;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KWs w = carve(ws, ws_bytes, n, 1);
+  TPCB_CUDA_CHECK(cudaMemsetAsync(w.found, 0xff, sizeof(unsigned long long), stream));
+  search_offset_kernel<<<grid_for(n), 256, 0, stream>>>(w.cdf, n, offset, total, u, w.found);
+  found_to_i64_kernel<<<1, 1, 0, stream>>>(w.found, n, d_found);
+  TPCB_LAUNCH_CHECK("kmeanspp_search");
+  return TPCB_OK;
+}
+
+extern "C" int tpcb_kmeans_partial(const double* d_x, int64_t n, int32_t d, int32_t kappa,
+                                   const int64_t* d_assign, const int32_t* d_counts,
+                                   double* d_sums, void* ws, size_t ws_bytes, void* stream_) {
+  if (!d_x || !d_assign || !d_counts || !d_sums || !ws) return TPCB_ERR_VALIDATION;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KWs w = carve(ws, ws_bytes, n, kappa);
+  to_key_kernel<<<grid_for(n), 256, 0, stream>>>(d_assign, w.kin, w.iin, n);
+  int bits = 1;
+  while ((1 << bits) < kappa) ++bits;
+  size_t tb = w.tmp_bytes;
+  TPCB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.kin, w.kout, w.iin, w.iout, (int)n,
+                                                  0, bits, stream));
+  tb = w.tmp_bytes;
+  TPCB_CUDA_CHECK(cudaMemsetAsync(w.offs, 0, sizeof(int32_t), stream));
+  TPCB_CUDA_CHECK(
+      cub::DeviceScan::InclusiveSum(w.tmp, tb, d_counts, w.offs + 1, kappa, stream));
+  const int64_t items = (int64_t)kappa * d;
+  member_sum_kernel<<<(unsigned)((items + 127) / 128), 128, 0, stream>>>(d_x, d, kappa, w.iout,
+                                                                        w.offs, d_counts, d_sums);
+  TPCB_LAUNCH_CHECK("kmeans_partial");
   return TPCB_OK;
 }
 

@@ -249,3 +249,264 @@ def select_tasks(x, kappa: int, tasks: list, seed: int = 0, init_centers=None) -
         selected.append(table.task_ids[best])
         taken[best] = True
     return selected
+
+
+# ---------------------------------------------------------------------------
+# Data-parallel KMeans (SURVEY 8(e), C4 multi-GPU): the points are sharded
+# across ranks (rank r holds a contiguous slice of the global point order),
+# the centres are replicated.  Per k-means++ centre: one gather of the local
+# closest-distance totals, one of the local CDF sums, one of the local search
+# hits and a broadcast of the chosen point; per Lloyd iteration: an
+# all-reduce of the int32 counts and of the changed flag and one all-gather
+# of the [kappa, d] member sums, added in rank order on every rank (so the
+# centres are bit-identical on all ranks and independent of the NCCL
+# algorithm).  At world size 1 every value is bit-identical to kmeans().
+# ---------------------------------------------------------------------------
+
+
+class _CudaShard:
+    """One rank's shard on its GPU: the local pieces between the collectives
+    (tpcb_kmeanspp_closest / _cdf / _search, tpcb_kmeans_assign[_tc] /
+    _changed / _partial)."""
+
+    def __init__(self, x: np.ndarray, kappa: int, device, assign: str):
+        self.km = DeviceKMeans(x, kappa, device, assign)
+        self.lib, self.n, self.d, self.kappa = self.km.lib, self.km.n, self.km.d, kappa
+        self.x_host, self.device = x, self.km.dev
+        self.local_sum = torch.zeros(1, dtype=torch.float64, device=self.device)
+        self.found = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.sums = torch.zeros((kappa, self.d), dtype=torch.float64, device=self.device)
+
+    @property
+    def assign(self):
+        return self.km.assign
+
+    @property
+    def assign_prev(self):
+        return self.km.assign_prev
+
+    @property
+    def counts(self):
+        return self.km.counts
+
+    @property
+    def own(self):
+        return self.km.own
+
+    def closest(self, center: torch.Tensor, init: bool) -> torch.Tensor:
+        k = self.km
+        _lib.check(self.lib.tpcb_kmeanspp_closest(k.x.data_ptr(), self.n, self.d,
+                                                  center.data_ptr(), int(init),
+                                                  k.closest.data_ptr(), k.total.data_ptr(),
+                                                  k.ws.ptr, k.ws.size, k.s()), "kmeanspp_closest")
+        return k.total
+
+    def cdf(self, total: torch.Tensor) -> torch.Tensor:
+        k = self.km
+        _lib.check(self.lib.tpcb_kmeanspp_cdf(k.closest.data_ptr(), self.n, total.data_ptr(),
+                                              self.local_sum.data_ptr(), k.ws.ptr, k.ws.size,
+                                              k.s()), "kmeanspp_cdf")
+        return self.local_sum
+
+    def search(self, offset: float, total: float, u: float) -> int:
+        k = self.km
+        _lib.check(self.lib.tpcb_kmeanspp_search(self.n, offset, total, u, self.found.data_ptr(),
+                                                 k.ws.ptr, k.ws.size, k.s()), "kmeanspp_search")
+        return int(self.found.item())
+
+    def point(self, j: int) -> torch.Tensor:
+        return self.km.x[j].clone()
+
+    def assign_step(self, centers: torch.Tensor) -> None:
+        self.km.centers.copy_(centers)
+        self.km.assign_step()
+
+    def changed(self) -> torch.Tensor:
+        k = self.km
+        _lib.check(self.lib.tpcb_kmeans_changed(k.assign.data_ptr(), k.assign_prev.data_ptr(),
+                                                self.n, k.flag.data_ptr(), k.s()), "kmeans_changed")
+        return k.flag
+
+    def save_prev(self) -> None:
+        self.km.assign_prev.copy_(self.km.assign)
+
+    def partial(self) -> torch.Tensor:
+        k = self.km
+        _lib.check(self.lib.tpcb_kmeans_partial(k.x.data_ptr(), self.n, self.d, self.kappa,
+                                                k.assign.data_ptr(), k.counts.data_ptr(),
+                                                self.sums.data_ptr(), k.ws.ptr, k.ws.size, k.s()),
+                   "kmeans_partial")
+        return self.sums
+
+    def set_assignment(self, a: np.ndarray, own: np.ndarray) -> None:
+        self.km.assign.copy_(torch.from_numpy(a))
+        self.km.own.copy_(torch.from_numpy(own))
+        self.km.counts.copy_(torch.from_numpy(np.bincount(a, minlength=self.kappa)
+                                              .astype(np.int32)))
+
+
+class ShardedKMeans:
+    """k-means++ and Lloyd over point shards with torch.distributed
+    collectives (NCCL for CUDA shards).  Every rank draws the same RNG
+    sequence (same seed), so the sequential choices of sampling.py:45-60 and
+    the empty-cluster repair of sampling.py:90-97 are replayed identically on
+    every rank over the concatenated point order."""
+
+    def __init__(self, shard, group=None):
+        import torch.distributed as dist
+        self.dist, self.group, self.shard = dist, group, shard
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.kappa, self.d, self.dev = shard.kappa, shard.d, shard.device
+        ns = self._gather(torch.tensor([shard.n], dtype=torch.int64, device=self.dev))
+        self.ns = [int(v) for v in ns]
+        if min(self.ns) < 1:
+            raise ValidationError("every rank needs at least one point")
+        self.start = [sum(self.ns[:r]) for r in range(self.world)]
+        self.n_global = sum(self.ns)
+        if self.n_global < self.kappa:
+            raise TooFewPoints(f"{self.n_global} points < kappa={self.kappa}")
+        self.centers = torch.zeros((self.kappa, self.d), dtype=torch.float64, device=self.dev)
+
+    # -- collectives -------------------------------------------------------
+    def _gather(self, t: torch.Tensor) -> list:
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t.contiguous(), group=self.group)
+        return [o.cpu() for o in out] if t.numel() == 1 else out
+
+    def _ordered_sum(self, parts: list) -> torch.Tensor:
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p
+        return acc
+
+    def _bcast_point(self, owner: int, j: int) -> torch.Tensor:
+        buf = (self.shard.point(j) if owner == self.rank
+               else torch.empty(self.d, dtype=torch.float64, device=self.dev))
+        src = owner if self.group is None else self.dist.get_global_rank(self.group, owner)
+        self.dist.broadcast(buf, src=src, group=self.group)
+        return buf
+
+    def _global_point(self, g: int) -> torch.Tensor:
+        owner = max(r for r in range(self.world) if self.start[r] <= g)
+        return self._bcast_point(owner, g - self.start[owner])
+
+    # -- k-means++ (sampling.py:45-60) -------------------------------------
+    def kmeanspp(self, rng: np.random.Generator) -> None:
+        c = self._global_point(int(rng.integers(0, self.n_global)))
+        self.centers[0] = c
+        total = self._ordered_sum(self._gather(self.shard.closest(self.centers[0], True)))
+        for i in range(1, self.kappa):
+            if float(total) == 0.0:
+                c = self._global_point(int(rng.integers(0, self.n_global)))
+            else:
+                u = float(rng.random())
+                sums = [float(s) for s in self._gather(self.shard.cdf(total.to(self.dev)))]
+                offset, tot_p = 0.0, sums[0]
+                for r in range(1, self.world):
+                    tot_p += sums[r]
+                for r in range(self.rank):
+                    offset = sums[r] if r == 0 else offset + sums[r]
+                j = self.shard.search(offset, tot_p, u)
+                found = [int(v) for v in self._gather(
+                    torch.tensor([j], dtype=torch.int64, device=self.dev))]
+                hits = [r for r in range(self.world) if found[r] >= 0]
+                # no hit (u at the rounding edge of the last CDF value): the
+                # last point, as the single-device search does
+                owner = hits[0] if hits else self.world - 1
+                c = self._bcast_point(owner, found[owner] if hits else self.ns[-1] - 1)
+            self.centers[i] = c
+            total = self._ordered_sum(self._gather(self.shard.closest(self.centers[i], False)))
+
+    # -- Lloyd (sampling.py:63-106) ----------------------------------------
+    def _counts_global(self) -> torch.Tensor:
+        g = self.shard.counts.clone()
+        self.dist.all_reduce(g, group=self.group)  # int32: exact in any order
+        return g
+
+    def repair_empty(self, counts: np.ndarray) -> None:
+        """Sequential steal of the globally farthest point from a cluster
+        with > 1 members (first point in global order on ties)."""
+        sh = self.shard
+        a = sh.assign.cpu().numpy()
+        own = sh.own.cpu().numpy()
+        centers = self.centers.cpu().numpy()
+        counts = counts.astype(np.int64).copy()
+        for c in range(self.kappa):
+            if counts[c] != 0:
+                continue
+            cand = np.flatnonzero(counts[a] > 1)
+            if cand.size:
+                j = int(cand[own[cand].argmax()])
+                mine = torch.tensor([1.0, own[j], float(j), float(a[j])], dtype=torch.float64)
+            else:
+                mine = torch.tensor([0.0, 0.0, 0.0, 0.0], dtype=torch.float64)
+            rows = [r.cpu().numpy() for r in
+                    self._gather_rows(mine.to(self.dev))]
+            best = -1
+            for r in range(self.world):  # strict >: the lowest rank wins ties
+                if rows[r][0] > 0 and (best < 0 or rows[r][1] > rows[best][1]):
+                    best = r
+            j, old = int(rows[best][2]), int(rows[best][3])
+            if best == self.rank:
+                a[j] = c
+                own[j] = _point_dist(sh.x_host[j], centers[c])
+            counts[c] += 1
+            counts[old] -= 1
+        sh.set_assignment(a, own)
+
+    def _gather_rows(self, t: torch.Tensor) -> list:
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return out
+
+    def lloyd(self, max_iter: int = KMEANS_MAX_ITER) -> int:
+        it = 0
+        for it in range(1, max_iter + 1):
+            self.shard.assign_step(self.centers)
+            counts = self._counts_global()
+            if int(counts.min().item()) == 0:
+                self.repair_empty(counts.cpu().numpy())
+                counts = self._counts_global()
+            flag = self.shard.changed().clone()
+            self.dist.all_reduce(flag, op=self.dist.ReduceOp.MAX, group=self.group)
+            if not int(flag.item()):
+                break
+            self.shard.save_prev()
+            sums = self._ordered_sum(self._gather_rows(self.shard.partial()))
+            live = counts > 0
+            self.centers[live] = sums[live] / counts[live].to(torch.float64)[:, None]
+        return it
+
+
+def kmeans_sharded(x_local, kappa: int, seed: int = 0, init_centers=None, assign: str = "exact",
+                   group=None, shard=None) -> ClusterModel:
+    """kmeans() over the points of all ranks (this rank holds `x_local`, a
+    contiguous slice of the global point order, in rank order).  Returns the
+    replicated centres, THIS rank's assignment and the global sizes.
+    `shard` overrides the local backend (default: this rank's GPU)."""
+    x_local = np.asarray(x_local, dtype=np.float64)
+    if x_local.ndim == 1:
+        x_local = x_local[:, None]
+    if kappa < 1:
+        raise ValidationError("kappa must be >= 1")
+    if shard is None:
+        shard = _CudaShard(np.ascontiguousarray(x_local), kappa,
+                           torch.device("cuda", torch.cuda.current_device()), assign)
+    km = ShardedKMeans(shard, group)
+    if init_centers is not None:
+        centers = np.asarray(init_centers, dtype=np.float64).copy()
+        if centers.ndim == 1:
+            centers = centers[:, None]
+        if centers.shape != (kappa, x_local.shape[1]):
+            raise DimensionMismatch("init_centers shape mismatch")
+        km.centers.copy_(torch.from_numpy(centers))
+    else:
+        km.kmeanspp(np.random.default_rng(seed))
+    km.lloyd()
+    a = shard.assign_prev.cpu().numpy()
+    if np.any(a < 0):
+        a = shard.assign.cpu().numpy()
+    sizes = torch.from_numpy(np.bincount(a, minlength=kappa).astype(np.int64)).to(shard.device)
+    km.dist.all_reduce(sizes, group=group)
+    return ClusterModel(centers=km.centers.cpu().numpy(), assignment=a, sizes=sizes.cpu().numpy())
