@@ -25,10 +25,10 @@ from dataclasses import asdict, dataclass, replace
 import numpy as np
 import torch
 
-from . import engine
+from . import _lib, engine
 from .dataset import BoxCoxNormalizer, fit_boxcox
 from .errors import (CheckpointError, DimensionMismatch, DomainError, EmptyBatch,
-                     EmptyDataset, EmptySet, NonFiniteLoss, ValidationError)
+                     EmptyDataset, EmptySet, NonFiniteLoss, UnsupportedConfig, ValidationError)
 from .features import (N_ENTRY, CompactAst, CompactBatch, DeviceSpec, EncodedInput,
                        check_leaf_counts, encode_input, ragged_from_encoded)
 
@@ -179,11 +179,17 @@ class Predictor:
     """Device-resident model: flat fp32 parameters + the model handle.
     The bulk inference entry point (`forward_batch`) of the GPU path."""
 
-    def __init__(self, params: CostModelParams, rows_per_tile: int = 64, precision: str = "fp32"):
+    def __init__(self, params: CostModelParams, rows_per_tile: int = 64, precision: str = "fp32",
+                 path: str = "auto"):
         """precision "fp32": the parity mode (FP32 FFMA, decoded latency within
         1e-3 of the float64 reference); "bf16": encoder GEMMs on the tcgen05
         tensor cores with bf16 operands and fp32 accumulation (desk-shaped
-        models; packs 128-row tiles), accuracy stated in DESIGN.md."""
+        models; packs 128-row tiles), accuracy stated in DESIGN.md.
+        path "auto" | "fused" | "large": the layer-by-layer tensor-core path
+        (csrc/large.cu) is taken automatically when the fused kernels cannot
+        hold the model; "large" forces it (tests)."""
+        if path not in ("auto", "fused", "large"):
+            raise ValidationError(f"unknown path {path!r}")
         if precision not in ("fp32", "bf16"):
             raise ValidationError(f"unknown precision {precision!r}")
         self.config = params.config
@@ -192,14 +198,29 @@ class Predictor:
         self.precision = precision
         self.R = 128 if precision == "bf16" else rows_per_tile
         self.status = engine.Status(self.params.device)
+        # configs the fused one-CTA-per-tile kernels cannot hold (e.g.
+        # full_reference_config) run layer by layer on the tensor cores
+        # (3xTF32 GEMMs, fp32-accumulate parity accuracy) in either precision
+        self.large = None
+        fits = bool(_lib.load().tpcb_forward_fits(self.dm.handle, self.R))
+        if path == "fused" and not fits:
+            raise UnsupportedConfig("the fused forward cannot hold this model")
+        if path == "large" or not fits:
+            self.large = engine.LargePath(self.dm, self.params)
 
     def tensors(self) -> dict:
         return self.dm.unflatten(self.params.double().cpu().numpy())
 
     def forward_device(self, rows, ordering, leaf_off, devfeat, n_ast, encoded, norm=None,
-                       latents=True, theta=engine.THETA_DEFAULT):
+                       latents=True, theta=engine.THETA_DEFAULT, n_leaf=None):
+        """n_leaf: host leaf counts (the large path plans its buckets on the
+        host; read back from leaf_off when not given)."""
         pk = engine.pack(rows, ordering, leaf_off, n_ast, self.config.n_leaf_max, encoded,
                          self.status, self.R, theta)
+        if self.large is not None:
+            if n_leaf is None:
+                n_leaf = np.diff(leaf_off.cpu().numpy())
+            return self.large.forward(pk, n_leaf, devfeat, self.status, norm, latents)
         return engine.run_forward(self.dm, self.params, pk, devfeat, self.status, norm, latents,
                                   self.precision)
 
@@ -209,7 +230,7 @@ class Predictor:
         check_leaf_counts(rag.n_leaf, self.config.n_leaf_max)
         rows, ordering, leaf_off, devfeat = engine.upload_ragged(rag)
         out = self.forward_device(rows, ordering, leaf_off, devfeat, rag.n_ast, rag.encoded,
-                                  norm, latents)
+                                  norm, latents, n_leaf=rag.n_leaf)
         self.status.check("forward")
         return out
 

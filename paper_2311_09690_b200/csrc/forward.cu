@@ -241,6 +241,11 @@ extern "C" int tpcb_metrics(const double* d_pred, const double* d_y, int64_t n, 
   return TPCB_OK;
 }
 
+extern "C" int32_t tpcb_forward_fits(const tpcb_model* m, int32_t R) {
+  if (!m || R < m->dev.n_leaf_max) return 0;
+  return (size_t)make_fwd_plan(m->dev, R).total * sizeof(float) <= 227 * 1024 ? 1 : 0;
+}
+
 extern "C" int tpcb_forward(const tpcb_model* m, const float* d_params, const tpcb_packed* pk,
                             const float* d_devfeat, int64_t n_ast, const tpcb_boxcox* norm,
                             float* d_pred, float* d_zx, float* d_zv, float* d_z,

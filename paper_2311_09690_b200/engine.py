@@ -250,6 +250,62 @@ def run_forward(dm: DeviceModel, params: torch.Tensor, pk: PackedBatch, devfeat:
     return pred, zx, zv, z, lat
 
 
+class LargePath:
+    """Layer-by-layer tensor-core forward (csrc/large.cu) for configs the
+    fused kernels do not fit, e.g. full_reference_config: the transposed
+    (hi, lo) weight image is built once per parameter version; the activation
+    workspace grows on demand."""
+
+    def __init__(self, dm: DeviceModel, params: torch.Tensor):
+        self.lib = _lib.load()
+        self.dm, self.params = dm, params
+        img, act = C.c_size_t(), C.c_size_t()
+        _lib.check(self.lib.tpcb_large_sizes(dm.handle, 1, 1, C.byref(img), C.byref(act)),
+                   "large_sizes")
+        self.image = torch.empty(img.value, dtype=torch.uint8, device=params.device)
+        self.act = torch.empty(0, dtype=torch.uint8, device=params.device)
+        self.prepare()
+
+    def prepare(self) -> None:
+        _lib.check(self.lib.tpcb_large_prepare(self.dm.handle, self.params.data_ptr(),
+                                               self.image.data_ptr(), stream_ptr()),
+                   "large_prepare")
+
+    @staticmethod
+    def order(n_leaf: np.ndarray):
+        """bucket order (the packed-index contract: stable argsort of n_leaf)
+        and the token offsets in that order"""
+        n_leaf = np.asarray(n_leaf, dtype=np.int64)
+        perm = np.argsort(n_leaf, kind="stable").astype(np.int32)
+        tok = np.zeros(len(n_leaf) + 1, dtype=np.int32)
+        np.cumsum(n_leaf[perm], out=tok[1:])
+        return perm, tok
+
+    def forward(self, pk: PackedBatch, n_leaf: np.ndarray, devfeat: torch.Tensor, status: Status,
+                norm=None, latents: bool = True):
+        n = pk.n_ast
+        perm, tok = self.order(n_leaf)
+        img, act = C.c_size_t(), C.c_size_t()
+        _lib.check(self.lib.tpcb_large_sizes(self.dm.handle, n, int(tok[-1]), C.byref(img),
+                                             C.byref(act)), "large_sizes")
+        if self.act.numel() < act.value:
+            self.act = torch.empty(act.value, dtype=torch.uint8, device=self.params.device)
+        dev = self.params.device
+        cfg = self.dm.cfg
+        pred = torch.empty(n, dtype=torch.float32, device=dev)
+        zx = torch.empty((n, cfg.d_embed), dtype=torch.float32, device=dev) if latents else None
+        zv = torch.empty((n, cfg.d_device), dtype=torch.float32, device=dev) if latents else None
+        z = torch.empty((n, cfg.d_embed), dtype=torch.float32, device=dev) if latents else None
+        lat = torch.empty(n, dtype=torch.float64, device=dev) if norm is not None else None
+        bc = boxcox_struct(norm)
+        _lib.check(self.lib.tpcb_large_forward(
+            self.dm.handle, self.params.data_ptr(), self.image.data_ptr(), C.byref(pk.struct),
+            perm.ctypes.data_as(C.c_void_p), tok.ctypes.data_as(C.c_void_p), devfeat.data_ptr(),
+            n, C.byref(bc), self.act.data_ptr(), self.act.numel(), pred.data_ptr(), dptr(zx),
+            dptr(zv), dptr(z), dptr(lat), status.ptr, stream_ptr()), "large_forward")
+        return pred, zx, zv, z, lat
+
+
 _BF16_IMG = {}
 
 
