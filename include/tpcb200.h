@@ -122,30 +122,6 @@ typedef struct {
   int32_t enabled; /* 0 = no decode */
 } tpcb_boxcox;
 
-/* ---- large-model path (SURVEY 8(f)1, full_reference_config) -------------
- * Layer-by-layer forward for configurations the fused kernels do not fit
- * (tpcb_forward_fits == 0): every product is a 3xTF32 tcgen05 GEMM (TMA-fed,
- * fp32 accumulation in TMEM); attention / LayerNorm / device MLP / output on
- * CUDA cores.  Replaces costmodel.forward (costmodel.py:193-269) for those
- * configs.  Image = transposed (hi, lo) weight operands, rebuilt by
- * tpcb_large_prepare after every parameter change.  h_perm / h_tok_off: the
- * HOST bucket order (stable argsort of n_leaf) and the token offsets in it. */
-int32_t tpcb_forward_fits(const tpcb_model* m, int32_t rows_per_tile);
-int tpcb_large_sizes(const tpcb_model* m, int64_t n_ast, int64_t n_tok, size_t* image_bytes,
-                     size_t* act_bytes);
-int tpcb_large_prepare(const tpcb_model* m, const float* d_params, void* d_image, void* stream);
-int tpcb_large_forward(const tpcb_model* m, const float* d_params, const void* d_image,
-                       const tpcb_packed* pk, const int32_t* h_perm, const int32_t* h_tok_off,
-                       const float* d_devfeat, int64_t n_ast, const tpcb_boxcox* norm,
-                       void* d_act, size_t act_bytes, float* d_pred, float* d_zx, float* d_zv,
-                       float* d_z, double* d_latency, int32_t* d_status, void* stream);
-/* the GEMM alone: C[M,N] = A[M,K] B[N,K]^T, fp32 row-major in/out (3xTF32) */
-size_t tpcb_gemm3_ws(int64_t M, int32_t N, int32_t K);
-int tpcb_gemm3(const float* d_a, const float* d_b, int64_t M, int32_t N, int32_t K, float* d_c,
-               int32_t ldc, void* d_ws, size_t ws_bytes, void* stream);
-int tpcb_gemm3_presplit(const float* a_hi, const float* a_lo, const float* b_hi,
-                        const float* b_lo, int64_t M, int32_t N, int32_t Kp, float* d_c,
-                        int32_t ldc, void* stream);
 
 
 /* ---- K2+K3: fused encoder + head forward (inference) ---------------------
@@ -187,6 +163,51 @@ typedef struct {
   int32_t cmd_order;      /* K <= 8 */
   tpcb_boxcox norm;
 } tpcb_loss;
+
+/* ---- large-model path (SURVEY 8(f)1, full_reference_config) -------------
+ * Layer-by-layer forward for configurations the fused kernels do not fit
+ * (tpcb_forward_fits == 0): every product is a 3xTF32 tcgen05 GEMM (TMA-fed,
+ * fp32 accumulation in TMEM); attention / LayerNorm / device MLP / output on
+ * CUDA cores.  Replaces costmodel.forward (costmodel.py:193-269) for those
+ * configs.  Image = transposed (hi, lo) weight operands (+ the plain ones the
+ * backward needs), rebuilt by tpcb_large_prepare after every parameter
+ * change; zero-fill it once at allocation.  h_perm / h_tok_off: the
+ * HOST bucket order (stable argsort of n_leaf) and the token offsets in it. */
+int32_t tpcb_forward_fits(const tpcb_model* m, int32_t rows_per_tile);
+int tpcb_large_sizes(const tpcb_model* m, int64_t n_ast, int64_t n_tok, size_t* image_bytes,
+                     size_t* act_bytes);
+/* flags: bit 0 = also the backward operands, bit 1 = entry table already
+ * resident in this image (skip its upload, which synchronises the stream) */
+int tpcb_large_prepare(const tpcb_model* m, const float* d_params, void* d_image,
+                       int32_t flags, void* stream);
+int tpcb_large_forward(const tpcb_model* m, const float* d_params, const void* d_image,
+                       const tpcb_packed* pk, const int32_t* h_perm, const int32_t* h_tok_off,
+                       const float* d_devfeat, int64_t n_ast, const tpcb_boxcox* norm,
+                       void* d_act, size_t act_bytes, float* d_pred, float* d_zx, float* d_zv,
+                       float* d_z, double* d_latency, int32_t* d_status, void* stream);
+/* Large-path training (costmodel.backward, costmodel.py:280-336, 343-423,
+ * 529-570, for configs the fused trainer cannot hold): one batch's forward
+ * (activations kept), loss and full backward on the tensor cores.  Inputs are
+ * dataset-resident: K1-packed rows d_x + d_ast_row, device features
+ * [n, 6], model-space targets d_y; the batch is h_idx (dataset indices in
+ * bucket order, HOST) with token offsets h_tok_off.  Writes the whole flat
+ * gradient d_grad (normalised by n_norm, the global batch) and the batch-mean
+ * loss d_loss[0].  Transformed-space losses without CMD (else UNSUPPORTED). */
+int tpcb_large_train_ws(const tpcb_model* m, int64_t n_ast, int64_t n_tok, size_t* ws_bytes);
+int tpcb_large_loss_backward(const tpcb_model* m, const float* d_params, const void* d_image,
+                             const float* d_x, const int32_t* d_ast_row, const float* d_devfeat,
+                             const double* d_y, const int32_t* h_idx, const int32_t* h_tok_off,
+                             const int32_t* d_idx /* device copies or NULL */,
+                             const int32_t* d_tok_off, int64_t n_batch, const tpcb_loss* loss, double n_norm, void* d_ws,
+                             size_t ws_bytes, float* d_grad, double* d_loss, int32_t* d_status,
+                             void* stream);
+/* the GEMM alone: C[M,N] = A[M,K] B[N,K]^T, fp32 row-major in/out (3xTF32) */
+size_t tpcb_gemm3_ws(int64_t M, int32_t N, int32_t K);
+int tpcb_gemm3(const float* d_a, const float* d_b, int64_t M, int32_t N, int32_t K, float* d_c,
+               int32_t ldc, void* d_ws, size_t ws_bytes, void* stream);
+int tpcb_gemm3_presplit(const float* a_hi, const float* a_lo, const float* b_hi,
+                        const float* b_lo, int64_t M, int32_t N, int32_t Kp, float* d_c,
+                        int32_t ldc, void* stream);
 
 /* one dataset on the device: packed rows from tpcb_featurize_pack + per-sample data */
 typedef struct {

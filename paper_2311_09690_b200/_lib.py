@@ -83,9 +83,12 @@ SIGNATURES = {
     "tpcb_positional_encoding": (i32, [vp, i64, vp, vp, vp]),
     "tpcb_forward_fits": (i32, [vp, i32]),
     "tpcb_large_sizes": (i32, [vp, i64, i64, C.POINTER(sz), C.POINTER(sz)]),
-    "tpcb_large_prepare": (i32, [vp, vp, vp, vp]),
+    "tpcb_large_prepare": (i32, [vp, vp, vp, i32, vp]),
     "tpcb_large_forward": (i32, [vp, vp, vp, C.POINTER(Packed), vp, vp, vp, i64,
                                  C.POINTER(BoxCox), vp, sz, vp, vp, vp, vp, vp, vp, vp]),
+    "tpcb_large_train_ws": (i32, [vp, i64, i64, C.POINTER(sz)]),
+    "tpcb_large_loss_backward": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64,
+                                       C.POINTER(LossCfg), f64, vp, sz, vp, vp, vp, vp]),
     "tpcb_gemm3_ws": (sz, [i64, i32, i32]),
     "tpcb_gemm3": (i32, [vp, vp, i64, i32, i32, vp, i32, vp, sz, vp]),
     "tpcb_gemm3_presplit": (i32, [vp, vp, vp, vp, i64, i32, i32, vp, i32, vp]),

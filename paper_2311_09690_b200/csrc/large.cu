@@ -22,6 +22,7 @@
 // L's rows as a [n_L, L·dp] matrix (a 2-D tensor map with row stride L·dp).
 #include <cuda.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -97,6 +98,9 @@ struct Epi {
   float* c;                 // plain fp32 output, or (c == null) the split pair:
   float* c_hi;
   float* c_lo;
+  const float* mask = nullptr;  // ReLU backward: keep x where mask[row, col] > 0
+  int ldm = 0;
+  int64_t split_stride = 0;     // split-K: split z writes c + z * split_stride
 };
 
 constexpr int kTileM = 128;
@@ -114,7 +118,7 @@ template <int NT>
 __global__ void __launch_bounds__(192, 1)
     gemm3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                  const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-                 int k_iters, Epi e) {
+                 int kc, int k_total, Epi e) {
   using Cfg = GemmCfg<NT>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -124,6 +128,8 @@ __global__ void __launch_bounds__(192, 1)
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * NT, m0 = blockIdx.y * kTileM;
+  const int k0 = blockIdx.z * kc;
+  const int k_iters = min(kc, k_total - k0);  // >= 1 (host picks the splits)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -154,10 +160,11 @@ __global__ void __launch_bounds__(192, 1)
       if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
       uint8_t* st = smem + s * Cfg::kStage;
       mbar_arrive_expect_tx(&full[s], Cfg::kStage);
-      tma_load_2d(st, &ta_hi, it * 32, m0, &full[s]);
-      tma_load_2d(st + kSlabA, &ta_lo, it * 32, m0, &full[s]);
-      tma_load_2d(st + 2 * kSlabA, &tb_hi, it * 32, n0, &full[s]);
-      tma_load_2d(st + 2 * kSlabA + Cfg::kSlabB, &tb_lo, it * 32, n0, &full[s]);
+      const int kx = (k0 + it) * 32;
+      tma_load_2d(st, &ta_hi, kx, m0, &full[s]);
+      tma_load_2d(st + kSlabA, &ta_lo, kx, m0, &full[s]);
+      tma_load_2d(st + 2 * kSlabA, &tb_hi, kx, n0, &full[s]);
+      tma_load_2d(st + 2 * kSlabA + Cfg::kSlabB, &tb_lo, kx, n0, &full[s]);
     }
   } else if (warp == 5 && lane == 0) {  // MMA issuer
     constexpr uint32_t id = idesc_tf32(kTileM, NT);
@@ -203,16 +210,18 @@ __global__ void __launch_bounds__(192, 1)
           if (e.bias) x += __ldg(e.bias + col);
           if (e.r_hi) {
             const size_t ri = (size_t)row * e.ldr + col;
-            x += e.r_hi[ri] + e.r_lo[ri];
+            x += e.r_hi[ri] + (e.r_lo ? e.r_lo[ri] : 0.f);
           }
           if (e.relu) x = fmaxf(x, 0.f);
+          if (e.mask && !(e.mask[(size_t)row * e.ldm + col] > 0.f)) x = 0.f;
         } else {
           x = 0.f;
         }
         v[j] = x;
       }
       if (e.c) {
-        float4* dst = reinterpret_cast<float4*>(e.c + (size_t)row * e.ldc + c0);
+        float4* dst = reinterpret_cast<float4*>(e.c + blockIdx.z * e.split_stride +
+                                                (size_t)row * e.ldc + c0);
 #pragma unroll
         for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
       } else {
@@ -246,11 +255,14 @@ __global__ void __launch_bounds__(192, 1)
 struct ImgEntry {
   int64_t src;   // float offset of W in the flat parameter vector
   int64_t dst;   // float offset in the image
-  int n, kp;     // image rows (= output features), padded k
-  int seg, segp; // real / padded k per segment (seg == 0: one segment of k_real = segp)
+  int n, kp;     // image rows, row length written
+  int seg, segp; // real / padded k per segment (seg == 0: one segment of k_real)
   int k_real;
   int n_src;     // row stride of W (its column count)
   int col0;      // first W column used (QKV: Wq | Wk | Wv concatenated by entries)
+  // plain (backward) entries: dst[r * dst_ld + c] = W[k(r)][col0 + c] for
+  // c < ncols_real (the dX = dY W operand: rows = W rows, k = W columns)
+  int plain, dst_ld, ncols_real;
 };
 
 __global__ void build_image_kernel(const float* __restrict__ P, const ImgEntry* __restrict__ ents,
@@ -261,17 +273,27 @@ __global__ void build_image_kernel(const float* __restrict__ P, const ImgEntry* 
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int n = (int)(i / E.kp), kq = (int)(i - (int64_t)n * E.kp);
+    // transposed: segment mapping on the k (column) index; plain: on the row
+    const int q = E.plain ? n : kq;
     int k = -1;
     if (E.seg) {
-      const int sgi = kq / E.segp, j = kq - sgi * E.segp;
+      const int sgi = q / E.segp, j = q - sgi * E.segp;
       if (j < E.seg) k = sgi * E.seg + j;
-    } else if (kq < E.k_real) {
-      k = kq;
+    } else if (q < E.k_real) {
+      k = q;
     }
-    const float v = k >= 0 ? P[E.src + (int64_t)k * E.n_src + E.col0 + n] : 0.f;
+    float v;
+    int64_t o;
+    if (E.plain) {
+      v = (k >= 0 && kq < E.ncols_real) ? P[E.src + (int64_t)k * E.n_src + E.col0 + kq] : 0.f;
+      o = E.dst + (int64_t)n * E.dst_ld + kq;
+    } else {
+      v = k >= 0 ? P[E.src + (int64_t)k * E.n_src + E.col0 + n] : 0.f;
+      o = E.dst + i;
+    }
     const float h = tf32_hi(v);
-    img_hi[E.dst + i] = h;
-    img_lo[E.dst + i] = v - h;
+    img_hi[o] = h;
+    img_lo[o] = v - h;
   }
 }
 
@@ -434,7 +456,7 @@ __global__ void output_kernel(Model M, const float* __restrict__ P, const float*
                               const float* __restrict__ h_lo, int ldh, int width,
                               const int32_t* __restrict__ perm, int n_ast, tpcb_boxcox bc,
                               float* __restrict__ pred, double* __restrict__ lat,
-                              int32_t* __restrict__ status) {
+                              int32_t* __restrict__ status, int sorted_out) {
   const int s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (s >= n_ast) return;
   const int lane = threadIdx.x & 31;
@@ -445,7 +467,7 @@ __global__ void output_kernel(Model M, const float* __restrict__ P, const float*
   }
   acc = warp_sum(acc) + P[M.outb];
   if (lane == 0) {
-    const int i = perm[s];
+    const int i = sorted_out ? s : perm[s];
     pred[i] = acc;
     if (lat) {
       bool bad = false;
@@ -507,7 +529,8 @@ struct Operand {
 };
 
 template <int NT>
-int launch_gemm_nt(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st) {
+int launch_gemm_nt(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st,
+                   int splits = 1) {
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
   int rc = tmap_2d(&ta_hi, A.hi, A.k_ext, A.rows, A.ld, kTileM);
   if (!rc) rc = tmap_2d(&ta_lo, A.lo, A.k_ext, A.rows, A.ld, kTileM);
@@ -521,9 +544,13 @@ int launch_gemm_nt(const Operand& A, const Operand& B, const Epi& e, cudaStream_
                                          GemmCfg<NT>::kSmem));
     attr = true;
   }
-  const dim3 grid((unsigned)ceil_div(e.ldc, NT), (unsigned)ceil_div(e.M, kTileM));
-  gemm3_kernel<NT><<<grid, 192, GemmCfg<NT>::kSmem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo,
-                                                          (int)(A.k_ext / 32), e);
+  const int k_total = (int)(A.k_ext / 32);
+  const int kc = ceil_div(k_total, splits);
+  splits = ceil_div(k_total, kc);  // every split gets >= 1 slab
+  const dim3 grid((unsigned)ceil_div(e.ldc, NT), (unsigned)ceil_div(e.M, kTileM),
+                  (unsigned)splits);
+  gemm3_kernel<NT><<<grid, 192, GemmCfg<NT>::kSmem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, kc,
+                                                          k_total, e);
   TPCB_LAUNCH_CHECK("gemm3");
   return TPCB_OK;
 }
@@ -540,9 +567,13 @@ int launch_gemm(const Operand& A, const Operand& B, const Epi& e, cudaStream_t s
 struct LargePlan {
   int d, dp, ff, ffp, qkv, qkvp, de, dep;
   int64_t in, layer[TPCB_MAX_LAYERS][4], leaf[TPCB_MAX_LEAF + 1], dec[TPCB_MAX_DEC];
+  // backward operands (plain layout): [0] Wq|Wk|Wv [d][qkvp], [1] Wo [d][dp],
+  // [2] fhW [d][ffp], [3] foW [ff][dp]; leaf [L·dp][dep]; dec [in][pad(out)]
+  int64_t layer_b[TPCB_MAX_LAYERS][4], leaf_b[TPCB_MAX_LEAF + 1], dec_b[TPCB_MAX_DEC];
   int dec_kp[TPCB_MAX_DEC];
   int64_t bias_qkv[TPCB_MAX_LAYERS];  // concatenated QKV bias (in the bias image)
-  int64_t img_floats, bias_floats;
+  int64_t img_floats, img_floats_fwd, bias_floats;
+  int n_ents_fwd;
   std::vector<ImgEntry> ents;
 };
 
@@ -559,11 +590,17 @@ LargePlan make_plan(const Model& M) {
   int64_t o = 0;
   auto add = [&](int64_t src, int n, int kp, int k_real, int n_src, int col0, int seg,
                  int segp) {
-    ImgEntry E{src, o, n, kp, seg, segp, k_real, n_src, col0};
+    ImgEntry E{src, o, n, kp, seg, segp, k_real, n_src, col0, 0, kp, 0};
     p.ents.push_back(E);
     const int64_t at = o;
     o += (int64_t)n * kp;
     return at;
+  };
+  // plain entry writing rows × ncols_pad at `at` (row stride ld, column c0)
+  auto add_plain = [&](int64_t at, int64_t src, int rows, int k_real, int seg, int segp,
+                       int n_src, int col0, int ncols_real, int ncols_pad, int ld) {
+    ImgEntry E{src, at, rows, ncols_pad, seg, segp, k_real, n_src, col0, 1, ld, ncols_real};
+    p.ents.push_back(E);
   };
   p.in = add(M.inW, M.d, 32, TPCB_FEAT, M.d, 0, 0, 0);
   for (int li = 0; li < M.n_layers; ++li) {
@@ -582,6 +619,38 @@ LargePlan make_plan(const Model& M) {
   for (int i = 0; i < M.n_dec; ++i) {
     p.dec_kp[i] = pad32(kin);
     p.dec[i] = add(M.decW[i], M.dec[i], pad32(kin), kin, M.dec[i], 0, 0, 0);
+    kin = M.dec[i];
+  }
+  p.img_floats_fwd = o;
+  p.n_ents_fwd = (int)p.ents.size();
+  for (int li = 0; li < M.n_layers; ++li) {
+    const LayerOff& L = M.layer[li];
+    p.layer_b[li][0] = o;
+    add_plain(o, L.Wq, M.d, M.d, 0, 0, M.d, 0, M.d, M.d, p.qkvp);
+    add_plain(o + M.d, L.Wk, M.d, M.d, 0, 0, M.d, 0, M.d, M.d, p.qkvp);
+    add_plain(o + 2 * M.d, L.Wv, M.d, M.d, 0, 0, M.d, 0, M.d, M.d, p.qkvp);
+    o += (int64_t)M.d * p.qkvp;
+    p.layer_b[li][1] = o;
+    add_plain(o, L.Wo, M.d, M.d, 0, 0, M.d, 0, M.d, p.dp, p.dp);
+    o += (int64_t)M.d * p.dp;
+    p.layer_b[li][2] = o;
+    add_plain(o, L.fhW, M.d, M.d, 0, 0, M.d_ff, 0, M.d_ff, p.ffp, p.ffp);
+    o += (int64_t)M.d * p.ffp;
+    p.layer_b[li][3] = o;
+    add_plain(o, L.foW, M.d_ff, M.d_ff, 0, 0, M.d, 0, M.d, p.dp, p.dp);
+    o += (int64_t)M.d_ff * p.dp;
+  }
+  for (int l = 1; l <= M.n_leaf_max; ++l) {
+    p.leaf_b[l] = o;
+    add_plain(o, M.leafW[l], l * p.dp, l * M.d, M.d, p.dp, M.d_e, 0, M.d_e, p.dep, p.dep);
+    o += (int64_t)l * p.dp * p.dep;
+  }
+  kin = M.d_e;
+  for (int i = 0; i < M.n_dec; ++i) {
+    const int op = pad32(M.dec[i]);
+    p.dec_b[i] = o;
+    add_plain(o, M.decW[i], kin, kin, 0, 0, M.dec[i], 0, M.dec[i], op, op);
+    o += (int64_t)kin * op;
     kin = M.dec[i];
   }
   p.img_floats = o;
@@ -607,49 +676,93 @@ __global__ void qkv_bias_kernel(const float* __restrict__ P, Model M, const int6
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
-// activation workspace (floats) for n_tok tokens / n_ast ASTs
-struct Act {
-  float *x_hi, *x_lo, *h_hi, *h_lo, *h1_hi, *h1_lo, *c_hi, *c_lo, *f_hi, *f_lo, *qkv, *sum;
-  float *zx, *z_hi, *z_lo, *d_hi[2], *d_lo[2];
-  int32_t *perm, *tok_off;
-  size_t bytes;
+// ---------------------------------------------------------------- workspace
+// Forward activations.  Training keeps one copy per layer (for the backward);
+// inference aliases every layer onto one set (layer stride 0).
+struct Pair {
+  float* hi;
+  float* lo;
 };
 
-Act carve_act(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, uint8_t* base) {
-  Act a{};
+struct Fwd {
+  int64_t T, A;            // padded token / AST rows
+  size_t sd, sq, sf;       // per-layer strides (0 = every layer aliased: inference)
+  float *x_hi, *x_lo;
+  float *h_hi, *h_lo;      // [nl + 1] layer inputs / final output  [T, dp]
+  float *qkv;              // [nl] [T, qkvp] fp32
+  float *c_hi, *c_lo;      // [nl] attention context [T, dp]
+  float *s1, *s2;          // [nl] pre-LayerNorm sums [T, dp] fp32
+  float *h1_hi, *h1_lo;    // [nl] [T, dp]
+  float *f_hi, *f_lo;      // [nl] [T, ffp]
+  float *zx, *z_hi, *z_lo; // [A, dep]
+  float *dec_hi[TPCB_MAX_DEC], *dec_lo[TPCB_MAX_DEC];
+  float *pred;             // [A] sorted order (training)
+  int32_t *idx, *tok_off;
+  Pair H(int l) const { return {h_hi + l * sd, h_lo + l * sd}; }
+  float* QKV(int l) const { return qkv + l * sq; }
+  Pair C(int l) const { return {c_hi + l * sd, c_lo + l * sd}; }
+  float* S1(int l) const { return s1 + l * sd; }
+  float* S2(int l) const { return s2 + l * sd; }
+  Pair H1(int l) const { return {h1_hi + l * sd, h1_lo + l * sd}; }
+  Pair F(int l) const { return {f_hi + l * sf, f_lo + l * sf}; }
+};
+
+struct Carver {
+  uint8_t* base;
   size_t o = 0;
-  const int64_t T = ((n_tok + kTileM - 1) / kTileM) * kTileM;
-  const int64_t A = ((n_ast + kTileM - 1) / kTileM) * kTileM;
-  int dmax = 32;
-  for (int i = 0; i < M.n_dec; ++i) dmax = max(dmax, pad32(M.dec[i]));
-  auto take = [&](size_t floats) {
+  float* take(size_t floats) {
     float* r = reinterpret_cast<float*>(base ? base + o : nullptr);
     o = align256(o + floats * 4);
     return r;
-  };
-  a.x_hi = take(T * 32);
-  a.x_lo = take(T * 32);
-  a.h_hi = take(T * p.dp);
-  a.h_lo = take(T * p.dp);
-  a.h1_hi = take(T * p.dp);
-  a.h1_lo = take(T * p.dp);
-  a.c_hi = take(T * p.dp);
-  a.c_lo = take(T * p.dp);
-  a.f_hi = take(T * p.ffp);
-  a.f_lo = take(T * p.ffp);
-  a.qkv = take(T * p.qkvp);
-  a.sum = take(T * p.dp);
-  a.zx = take(A * p.dep);
-  a.z_hi = take(A * p.dep);
-  a.z_lo = take(A * p.dep);
-  for (int k = 0; k < 2; ++k) {
-    a.d_hi[k] = take(A * dmax);
-    a.d_lo[k] = take(A * dmax);
   }
-  a.perm = reinterpret_cast<int32_t*>(take(n_ast + 1));
-  a.tok_off = reinterpret_cast<int32_t*>(take(n_ast + 1));
-  a.bytes = o;
-  return a;
+};
+
+int dec_max(const Model& M) {
+  int dmax = 32;
+  for (int i = 0; i < M.n_dec; ++i) dmax = max(dmax, pad32(M.dec[i]));
+  return dmax;
+}
+
+Fwd carve_fwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, bool train,
+              Carver* cv) {
+  Fwd f{};
+  f.T = ((n_tok + kTileM - 1) / kTileM) * kTileM;
+  f.A = ((n_ast + kTileM - 1) / kTileM) * kTileM;
+  const size_t td = (size_t)f.T * p.dp, tq = (size_t)f.T * p.qkvp, tf = (size_t)f.T * p.ffp;
+  const size_t nl = train ? M.n_layers : 1;
+  f.sd = train ? td : 0;
+  f.sq = train ? tq : 0;
+  f.sf = train ? tf : 0;
+  f.x_hi = cv->take(f.T * 32);
+  f.x_lo = cv->take(f.T * 32);
+  f.h_hi = cv->take((train ? nl + 1 : 1) * td);
+  f.h_lo = cv->take((train ? nl + 1 : 1) * td);
+  f.qkv = cv->take(nl * tq);
+  f.c_hi = cv->take(nl * td);
+  f.c_lo = cv->take(nl * td);
+  f.s1 = cv->take(nl * td);
+  f.s2 = train ? cv->take(nl * td) : f.s1;
+  f.h1_hi = cv->take(nl * td);
+  f.h1_lo = cv->take(nl * td);
+  f.f_hi = cv->take(nl * tf);
+  f.f_lo = cv->take(nl * tf);
+  f.zx = cv->take(f.A * p.dep);
+  f.z_hi = cv->take(f.A * p.dep);
+  f.z_lo = cv->take(f.A * p.dep);
+  const int dmax = dec_max(M);
+  for (int i = 0; i < M.n_dec; ++i) {
+    if (train || i < 2) {
+      f.dec_hi[i] = cv->take(f.A * (train ? pad32(M.dec[i]) : dmax));
+      f.dec_lo[i] = cv->take(f.A * (train ? pad32(M.dec[i]) : dmax));
+    } else {  // inference ping-pong
+      f.dec_hi[i] = f.dec_hi[i - 2];
+      f.dec_lo[i] = f.dec_lo[i - 2];
+    }
+  }
+  f.pred = cv->take(f.A);
+  f.idx = reinterpret_cast<int32_t*>(cv->take(n_ast + 1));
+  f.tok_off = reinterpret_cast<int32_t*>(cv->take(n_ast + 1));
+  return f;
 }
 
 }  // namespace
@@ -659,23 +772,8 @@ bool large_supported(const Model& M) {
          (size_t)3 * TPCB_MAX_LEAF * (M.dh + 1) * 4 + 17 * 16 * 4 <= 200 * 1024;
 }
 
-}  // namespace tpcb
-
-using namespace tpcb;
-
-extern "C" int tpcb_large_sizes(const tpcb_model* m, int64_t n_ast, int64_t n_tok,
-                                size_t* image_bytes, size_t* act_bytes) {
-  if (!m || !image_bytes || !act_bytes) return TPCB_ERR_VALIDATION;
-  if (!large_supported(m->dev)) return TPCB_ERR_UNSUPPORTED;
-  const LargePlan p = make_plan(m->dev);
-  *image_bytes = align256((size_t)p.img_floats * 4) * 2 + align256((size_t)p.bias_floats * 4) +
-                 align256(p.ents.size() * sizeof(ImgEntry)) + 256 * 2;
-  *act_bytes = carve_act(p, m->dev, n_tok, n_ast, nullptr).bytes;
-  return TPCB_OK;
-}
-
-namespace tpcb {
 namespace {
+
 struct ImagePtrs {
   float *hi, *lo, *bias;
   ImgEntry* ents;
@@ -692,29 +790,162 @@ ImagePtrs carve_image(const LargePlan& p, uint8_t* base) {
   r.ents = reinterpret_cast<ImgEntry*>(base + o);
   return r;
 }
+
+struct Ctx {
+  const Model& M;
+  const LargePlan& p;
+  const float* P;
+  ImagePtrs im;
+  cudaStream_t st;
+  Operand W(int64_t off, int n, int kp) const { return Operand{im.hi + off, im.lo + off, n, kp, kp}; }
+};
+
+Operand act_op(const float* hi, const float* lo, int64_t rows, int ld) {
+  return Operand{hi, lo, rows, ld, ld};
+}
+
+// the forward over the sorted tokens already gathered into f.x (host-side
+// bucket structure h_tok_off); latents / pred scattered by f.idx unless
+// `train` (then pred stays in sorted order in f.pred)
+int run_forward(const Ctx& c, const Fwd& f, int64_t n_ast, const int32_t* h_tok_off,
+                const float* d_devfeat, bool train, const tpcb_boxcox& bc, float* d_pred,
+                float* d_zx, float* d_zv, float* d_z, double* d_lat, int32_t* d_status) {
+  const Model& M = c.M;
+  const LargePlan& p = c.p;
+  const float* P = c.P;
+  cudaStream_t st = c.st;
+  const int64_t n_tok = h_tok_off[n_ast];
+  int rc;
+  {
+    Pair h = f.H(0);
+    Epi e{(int)n_tok, M.d, p.dp, P + M.inb, 0, nullptr, nullptr, 0, nullptr, h.hi, h.lo};
+    if ((rc = launch_gemm(act_op(f.x_hi, f.x_lo, n_tok, 32), c.W(p.in, M.d, 32), e, st)))
+      return rc;
+  }
+  const float scale = 1.0f / sqrtf((float)M.dh);
+  const size_t att_smem = (size_t)(3 * TPCB_MAX_LEAF * (M.dh + 1) + 16 * 17) * 4;
+  if (att_smem > 48 * 1024)
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)att_smem));
+  for (int li = 0; li < M.n_layers; ++li) {
+    const LayerOff& L = M.layer[li];
+    const Pair h = f.H(li), hn = f.H(li + 1), ctx = f.C(li), h1 = f.H1(li), ff = f.F(li);
+    float* qkv = f.QKV(li);
+    {
+      Epi e{(int)n_tok, p.qkv, p.qkvp, c.im.bias + p.bias_qkv[li], 0, nullptr, nullptr, 0, qkv,
+            nullptr, nullptr};
+      if ((rc = launch_gemm(act_op(h.hi, h.lo, n_tok, p.dp), c.W(p.layer[li][0], p.qkv, p.dp), e,
+                            st)))
+        return rc;
+    }
+    attention_kernel<<<dim3((unsigned)n_ast, M.n_heads), 128, att_smem, st>>>(
+        qkv, p.qkvp, f.tok_off, M.d, M.n_heads, M.dh, scale, p.dp, ctx.hi, ctx.lo);
+    TPCB_LAUNCH_CHECK("large_attention");
+    {
+      Epi e{(int)n_tok, M.d, p.dp, P + L.bo, 0, h.hi, h.lo, p.dp, f.S1(li), nullptr, nullptr};
+      if ((rc = launch_gemm(act_op(ctx.hi, ctx.lo, n_tok, p.dp), c.W(p.layer[li][1], M.d, p.dp),
+                            e, st)))
+        return rc;
+    }
+    layernorm_kernel<<<ceil_div(n_tok, 8), 256, 0, st>>>(f.S1(li), p.dp, (int)n_tok, M.d,
+                                                         P + L.ln1g, P + L.ln1b, h1.hi, h1.lo);
+    {
+      Epi e{(int)n_tok, M.d_ff, p.ffp, P + L.fhb, 1, nullptr, nullptr, 0, nullptr, ff.hi, ff.lo};
+      if ((rc = launch_gemm(act_op(h1.hi, h1.lo, n_tok, p.dp),
+                            c.W(p.layer[li][2], M.d_ff, p.dp), e, st)))
+        return rc;
+    }
+    {
+      Epi e{(int)n_tok, M.d, p.dp, P + L.fob, 0, h1.hi, h1.lo, p.dp, f.S2(li), nullptr, nullptr};
+      if ((rc = launch_gemm(act_op(ff.hi, ff.lo, n_tok, p.ffp), c.W(p.layer[li][3], M.d, p.ffp),
+                            e, st)))
+        return rc;
+    }
+    layernorm_kernel<<<ceil_div(n_tok, 8), 256, 0, st>>>(f.S2(li), p.dp, (int)n_tok, M.d,
+                                                         P + L.ln2g, P + L.ln2b, hn.hi, hn.lo);
+    TPCB_LAUNCH_CHECK("large_layernorm");
+  }
+  const Pair hf = f.H(M.n_layers);
+  for (int64_t s0 = 0; s0 < n_ast;) {  // leaf_embed.{L}: bucket L as [n_L, L·dp]
+    const int Lb = h_tok_off[s0 + 1] - h_tok_off[s0];
+    int64_t s1 = s0 + 1;
+    while (s1 < n_ast && h_tok_off[s1 + 1] - h_tok_off[s1] == Lb) ++s1;
+    const int64_t nb = s1 - s0, t0 = h_tok_off[s0];
+    Operand A{hf.hi + t0 * p.dp, hf.lo + t0 * p.dp, nb, (int64_t)Lb * p.dp, (int64_t)Lb * p.dp};
+    Epi e{(int)nb, M.d_e, p.dep, P + M.leafb[Lb], 0, nullptr, nullptr, 0, f.zx + s0 * p.dep,
+          nullptr, nullptr};
+    if ((rc = launch_gemm(A, c.W(p.leaf[Lb], M.d_e, Lb * p.dp), e, st))) return rc;
+    s0 = s1;
+  }
+  device_gate_kernel<<<(unsigned)n_ast, 128, M.d_dev * 4, st>>>(M, P, d_devfeat, f.idx, f.zx,
+                                                                 p.dep, f.z_hi, f.z_lo, d_zx,
+                                                                 d_zv, d_z);
+  TPCB_LAUNCH_CHECK("large_device_gate");
+  const float* in_hi = f.z_hi;
+  const float* in_lo = f.z_lo;
+  int ldin = p.dep;
+  for (int i = 0; i < M.n_dec; ++i) {
+    const int ldo = pad32(M.dec[i]);
+    Epi e{(int)n_ast, M.dec[i], ldo, P + M.decb[i], 1, nullptr, nullptr, 0, nullptr,
+          f.dec_hi[i], f.dec_lo[i]};
+    if ((rc = launch_gemm(act_op(in_hi, in_lo, n_ast, ldin), c.W(p.dec[i], M.dec[i], p.dec_kp[i]),
+                          e, st)))
+      return rc;
+    in_hi = f.dec_hi[i];
+    in_lo = f.dec_lo[i];
+    ldin = ldo;
+  }
+  output_kernel<<<ceil_div(n_ast, 8), 256, 0, st>>>(
+      M, P, in_hi, in_lo, ldin, M.n_dec ? M.dec[M.n_dec - 1] : M.d_e, f.idx, (int)n_ast, bc,
+      train ? f.pred : d_pred, train ? nullptr : d_lat, d_status, train ? 1 : 0);
+  TPCB_LAUNCH_CHECK("large_output");
+  return TPCB_OK;
+}
+
 }  // namespace
 }  // namespace tpcb
 
-// weight image: the transposed (hi, lo) B operands of every GEMM + the
-// concatenated QKV biases; rebuild after every parameter update
+using namespace tpcb;
+
+extern "C" int tpcb_large_sizes(const tpcb_model* m, int64_t n_ast, int64_t n_tok,
+                                size_t* image_bytes, size_t* act_bytes) {
+  if (!m || !image_bytes || !act_bytes) return TPCB_ERR_VALIDATION;
+  if (!large_supported(m->dev)) return TPCB_ERR_UNSUPPORTED;
+  const LargePlan p = make_plan(m->dev);
+  *image_bytes = align256((size_t)p.img_floats * 4) * 2 + align256((size_t)p.bias_floats * 4) +
+                 align256(p.ents.size() * sizeof(ImgEntry)) + 256 * 2;
+  Carver cv{nullptr};
+  carve_fwd(p, m->dev, n_tok, n_ast, false, &cv);
+  *act_bytes = cv.o;
+  return TPCB_OK;
+}
+
+// weight image: the transposed (hi, lo) B operands of every forward GEMM
+// (+ the plain operands of the backward's dX GEMMs when with_backward) and
+// the concatenated QKV biases; rebuild after every parameter update.  The
+// image must be zero-filled once at allocation (pad columns stay zero).
 extern "C" int tpcb_large_prepare(const tpcb_model* m, const float* d_params, void* d_image,
-                                  void* stream_) {
+                                  int32_t with_backward, void* stream_) {
   if (!m || !d_params || !d_image) return TPCB_ERR_VALIDATION;
   if (!large_supported(m->dev)) return TPCB_ERR_UNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream_;
   const LargePlan p = make_plan(m->dev);
   ImagePtrs im = carve_image(p, (uint8_t*)d_image);
-  TPCB_CUDA_CHECK(cudaMemcpyAsync(im.ents, p.ents.data(), p.ents.size() * sizeof(ImgEntry),
-                                  cudaMemcpyHostToDevice, st));
-  build_image_kernel<<<dim3(128, (unsigned)p.ents.size()), 256, 0, st>>>(
-      d_params, im.ents, (int)p.ents.size(), im.hi, im.lo);
   int64_t* d_off = reinterpret_cast<int64_t*>(im.ents + p.ents.size());
   d_off = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(d_off) + 255) & ~uintptr_t(255));
-  TPCB_CUDA_CHECK(cudaMemcpyAsync(d_off, p.bias_qkv, sizeof(int64_t) * m->dev.n_layers,
-                                  cudaMemcpyHostToDevice, st));
+  // entry table + offsets (a few KB; a pageable copy synchronises the stream,
+  // so callers that rebuild every step pass bit 1 after the first call)
+  if (!(with_backward & 2)) {
+    TPCB_CUDA_CHECK(cudaMemcpyAsync(im.ents, p.ents.data(), p.ents.size() * sizeof(ImgEntry),
+                                    cudaMemcpyHostToDevice, st));
+    TPCB_CUDA_CHECK(cudaMemcpyAsync(d_off, p.bias_qkv, sizeof(int64_t) * m->dev.n_layers,
+                                    cudaMemcpyHostToDevice, st));
+  }
+  const int n_ents = (with_backward & 1) ? (int)p.ents.size() : p.n_ents_fwd;
+  build_image_kernel<<<dim3(64, (unsigned)n_ents), 256, 0, st>>>(d_params, im.ents, n_ents, im.hi,
+                                                                 im.lo);
   qkv_bias_kernel<<<dim3(8, m->dev.n_layers), 256, 0, st>>>(d_params, m->dev, d_off, im.bias);
-  // the host arrays above are stack / plan locals: finish the copies first
-  TPCB_CUDA_CHECK(cudaStreamSynchronize(st));
   TPCB_LAUNCH_CHECK("large_prepare");
   return TPCB_OK;
 }
@@ -736,111 +967,20 @@ extern "C" int tpcb_large_forward(const tpcb_model* m, const float* d_params, co
   cudaStream_t st = (cudaStream_t)stream_;
   const LargePlan p = make_plan(M);
   const int64_t n_tok = h_tok_off[n_ast];
-  Act a = carve_act(p, M, n_tok, n_ast, (uint8_t*)d_act);
-  if (a.bytes > act_bytes) return TPCB_ERR_VALIDATION;
-  ImagePtrs im = carve_image(p, (uint8_t*)const_cast<void*>(d_image));
-  TPCB_CUDA_CHECK(cudaMemcpyAsync(a.perm, h_perm, n_ast * 4, cudaMemcpyHostToDevice, st));
+  Carver cv{(uint8_t*)d_act};
+  Fwd f = carve_fwd(p, M, n_tok, n_ast, false, &cv);
+  if (cv.o > act_bytes) return TPCB_ERR_VALIDATION;
+  TPCB_CUDA_CHECK(cudaMemcpyAsync(f.idx, h_perm, n_ast * 4, cudaMemcpyHostToDevice, st));
   TPCB_CUDA_CHECK(
-      cudaMemcpyAsync(a.tok_off, h_tok_off, (n_ast + 1) * 4, cudaMemcpyHostToDevice, st));
-  gather_tokens_kernel<<<ceil_div(n_ast, 8), 256, 0, st>>>(pk->x, a.perm, pk->ast_row, a.tok_off,
-                                                           (int)n_ast, a.x_hi, a.x_lo);
+      cudaMemcpyAsync(f.tok_off, h_tok_off, (n_ast + 1) * 4, cudaMemcpyHostToDevice, st));
+  gather_tokens_kernel<<<ceil_div(n_ast, 8), 256, 0, st>>>(pk->x, f.idx, pk->ast_row, f.tok_off,
+                                                           (int)n_ast, f.x_hi, f.x_lo);
   TPCB_LAUNCH_CHECK("large_gather");
-  const float* P = d_params;
-  auto W = [&](int64_t off, int n, int kp) {
-    return Operand{im.hi + off, im.lo + off, n, kp, kp};
-  };
-  auto act = [&](const float* hi, const float* lo, int64_t rows, int ld) {
-    return Operand{hi, lo, rows, ld, ld};
-  };
-  int rc;
-  // input projection
-  {
-    Epi e{(int)n_tok, M.d, p.dp, P + M.inb, 0, nullptr, nullptr, 0, nullptr, a.h_hi, a.h_lo};
-    if ((rc = launch_gemm(act(a.x_hi, a.x_lo, n_tok, 32), W(p.in, M.d, 32), e, st))) return rc;
-  }
-  const float scale = 1.0f / sqrtf((float)M.dh);
-  const size_t att_smem = (size_t)(3 * TPCB_MAX_LEAF * (M.dh + 1) + 16 * 17) * 4;
-  if (att_smem > 48 * 1024)
-    TPCB_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)att_smem));
-  for (int li = 0; li < M.n_layers; ++li) {
-    const LayerOff& L = M.layer[li];
-    {  // Q | K | V
-      Epi e{(int)n_tok, p.qkv, p.qkvp, im.bias + p.bias_qkv[li], 0, nullptr, nullptr, 0, a.qkv,
-            nullptr, nullptr};
-      if ((rc = launch_gemm(act(a.h_hi, a.h_lo, n_tok, p.dp), W(p.layer[li][0], p.qkv, p.dp), e,
-                            st)))
-        return rc;
-    }
-    attention_kernel<<<dim3((unsigned)n_ast, M.n_heads), 128, att_smem, st>>>(
-        a.qkv, p.qkvp, a.tok_off, M.d, M.n_heads, M.dh, scale, p.dp, a.c_hi, a.c_lo);
-    TPCB_LAUNCH_CHECK("large_attention");
-    {  // h + ctx Wo + bo → LN1
-      Epi e{(int)n_tok, M.d, p.dp, P + L.bo, 0, a.h_hi, a.h_lo, p.dp, a.sum, nullptr, nullptr};
-      if ((rc = launch_gemm(act(a.c_hi, a.c_lo, n_tok, p.dp), W(p.layer[li][1], M.d, p.dp), e,
-                            st)))
-        return rc;
-    }
-    layernorm_kernel<<<ceil_div(n_tok, 8), 256, 0, st>>>(a.sum, p.dp, (int)n_tok, M.d,
-                                                         P + L.ln1g, P + L.ln1b, a.h1_hi,
-                                                         a.h1_lo);
-    {  // relu(h1 W1 + b1)
-      Epi e{(int)n_tok, M.d_ff, p.ffp, P + L.fhb, 1, nullptr, nullptr, 0, nullptr, a.f_hi,
-            a.f_lo};
-      if ((rc = launch_gemm(act(a.h1_hi, a.h1_lo, n_tok, p.dp), W(p.layer[li][2], M.d_ff, p.dp),
-                            e, st)))
-        return rc;
-    }
-    {  // h1 + f W2 + b2 → LN2
-      Epi e{(int)n_tok, M.d, p.dp, P + L.fob, 0, a.h1_hi, a.h1_lo, p.dp, a.sum, nullptr, nullptr};
-      if ((rc = launch_gemm(act(a.f_hi, a.f_lo, n_tok, p.ffp), W(p.layer[li][3], M.d, p.ffp), e,
-                            st)))
-        return rc;
-    }
-    layernorm_kernel<<<ceil_div(n_tok, 8), 256, 0, st>>>(a.sum, p.dp, (int)n_tok, M.d,
-                                                         P + L.ln2g, P + L.ln2b, a.h_hi, a.h_lo);
-    TPCB_LAUNCH_CHECK("large_layernorm");
-  }
-  // leaf_embed.{L}: bucket L's rows as [n_L, L·dp]
-  for (int64_t s0 = 0; s0 < n_ast;) {
-    const int Lb = h_tok_off[s0 + 1] - h_tok_off[s0];
-    int64_t s1 = s0 + 1;
-    while (s1 < n_ast && h_tok_off[s1 + 1] - h_tok_off[s1] == Lb) ++s1;
-    const int64_t nb = s1 - s0;
-    const int64_t t0 = h_tok_off[s0];
-    Operand A{a.h_hi + t0 * p.dp, a.h_lo + t0 * p.dp, nb, (int64_t)Lb * p.dp,
-              (int64_t)Lb * p.dp};
-    Epi e{(int)nb, M.d_e, p.dep, P + M.leafb[Lb], 0, nullptr, nullptr, 0, a.zx + s0 * p.dep,
-          nullptr, nullptr};
-    if ((rc = launch_gemm(A, W(p.leaf[Lb], M.d_e, Lb * p.dp), e, st))) return rc;
-    s0 = s1;
-  }
-  device_gate_kernel<<<(unsigned)n_ast, 128, M.d_dev * 4, st>>>(M, P, d_devfeat, a.perm, a.zx,
-                                                                 p.dep, a.z_hi, a.z_lo, d_zx,
-                                                                 d_zv, d_z);
-  TPCB_LAUNCH_CHECK("large_device_gate");
-  const float* in_hi = a.z_hi;
-  const float* in_lo = a.z_lo;
-  int ldin = p.dep;
-  for (int i = 0; i < M.n_dec; ++i) {
-    const int ldo = pad32(M.dec[i]);
-    Epi e{(int)n_ast, M.dec[i], ldo, P + M.decb[i], 1, nullptr, nullptr, 0, nullptr,
-          a.d_hi[i & 1], a.d_lo[i & 1]};
-    if ((rc = launch_gemm(act(in_hi, in_lo, n_ast, ldin), W(p.dec[i], M.dec[i], p.dec_kp[i]), e,
-                          st)))
-      return rc;
-    in_hi = a.d_hi[i & 1];
-    in_lo = a.d_lo[i & 1];
-    ldin = ldo;
-  }
+  Ctx c{M, p, d_params, carve_image(p, (uint8_t*)const_cast<void*>(d_image)), st};
   tpcb_boxcox bc{};
   if (norm) bc = *norm;
-  output_kernel<<<ceil_div(n_ast, 8), 256, 0, st>>>(
-      M, P, in_hi, in_lo, ldin, M.n_dec ? M.dec[M.n_dec - 1] : M.d_e, a.perm, (int)n_ast, bc,
-      d_pred, d_latency, d_status);
-  TPCB_LAUNCH_CHECK("large_output");
-  return TPCB_OK;
+  return run_forward(c, f, n_ast, h_tok_off, d_devfeat, false, bc, d_pred, d_zx, d_zv, d_z,
+                     d_latency, d_status);
 }
 
 namespace tpcb {
@@ -900,4 +1040,638 @@ extern "C" int tpcb_gemm3_presplit(const float* a_hi, const float* a_lo, const f
   Operand A{a_hi, a_lo, M, Kp, Kp}, B{b_hi, b_lo, N, Kp, Kp};
   Epi e{(int)M, N, ldc, nullptr, 0, nullptr, nullptr, 0, d_c, nullptr, nullptr};
   return launch_gemm(A, B, e, (cudaStream_t)stream_);
+}
+
+// =================================================================== training
+// (costmodel.backward + nn.*_bwd for the large path: costmodel.py:280-336,
+// 343-423, nn.py:30-120).  Every weight gradient is a split-K tcgen05 GEMM
+// dW = Xᵀ·dY over the tokens (operands transposed + split by
+// transpose_pair_kernel), reduced in fixed split order; every input gradient
+// dX = dY·W is a GEMM on the plain weight image with the ReLU mask / residual
+// fused into its epilogue; bias / LayerNorm-parameter gradients are
+// deterministic column sums.  The flat gradient is fully rewritten per step.
+namespace tpcb {
+namespace {
+
+// [rows, cols] (row stride ld; pair or fp32 when a_lo == null) → pair
+// [cols][ldo], zero for rows <= r < ldo
+__global__ void transpose_pair_kernel(const float* __restrict__ a_hi, const float* __restrict__ a_lo,
+                                      int rows, int cols, int ld, float* __restrict__ o_hi,
+                                      float* __restrict__ o_lo, int ldo) {
+  __shared__ float t[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    float v = 0.f;
+    if (r < rows && c < cols) {
+      v = a_hi[(size_t)r * ld + c];
+      if (a_lo) v += a_lo[(size_t)r * ld + c];
+    }
+    t[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < ldo) {
+      const float v = t[threadIdx.x][i];
+      const float h = tf32_hi(v);
+      o_hi[(size_t)c * ldo + r] = h;
+      o_lo[(size_t)c * ldo + r] = v - h;
+    }
+  }
+}
+
+// out[c] = Σ_r x[r][c] (+ x_lo) in fixed order; column c goes to tensor c / colw
+struct ColDst {
+  int colw;
+  int64_t d[3];
+};
+
+__global__ void colsum_kernel(const float* __restrict__ x, const float* __restrict__ x_lo, int rows,
+                              int cols, int ld, ColDst dst, float* __restrict__ grad) {
+  __shared__ float red[8][33];
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  float acc = 0.f;
+  if (c < cols)
+    for (int r = threadIdx.y; r < rows; r += 8) {
+      acc += x[(size_t)r * ld + c];
+      if (x_lo) acc += x_lo[(size_t)r * ld + c];
+    }
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < cols) {
+    float s = red[0][threadIdx.x];
+    for (int k = 1; k < 8; ++k) s += red[k][threadIdx.x];
+    const int t = c / dst.colw;
+    grad[dst.d[t] + (c - t * dst.colw)] = s;
+  }
+}
+
+// split-K partials [splits][rows][ldc] → grad, rows through the leaf segment
+// map (seg > 0), columns split into ≤ 3 tensors of width colw
+__global__ void reduce_grad_kernel(const float* __restrict__ part, int splits, int64_t sstride,
+                                   int rows, int cols, int ldc, int seg, int segp, ColDst dst,
+                                   float* __restrict__ grad) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / cols), c = (int)(e - (int64_t)r * cols);
+    int rr = r;
+    if (seg) {
+      const int j = r % segp;
+      if (j >= seg) continue;
+      rr = (r / segp) * seg + j;
+    }
+    float v = part[(size_t)r * ldc + c];
+    for (int z = 1; z < splits; ++z) v += part[z * sstride + (size_t)r * ldc + c];
+    const int t = c / dst.colw;
+    const int cc = c - t * dst.colw;
+    grad[dst.d[t] + (int64_t)rr * dst.colw + cc] = v;
+  }
+}
+
+// LayerNorm backward (nn.py:57-66), one warp per row: dx = rstd·(dŷ − mean(dŷ)
+// − x̂·mean(dŷ·x̂)), dŷ = dy·g; prod = dy·x̂ (→ dg by column sums)
+__global__ void ln_back_kernel(const float* __restrict__ dy, const float* __restrict__ x, int ld,
+                               int rows, int d, const float* __restrict__ g,
+                               float* __restrict__ dx_hi, float* __restrict__ dx_lo,
+                               float* __restrict__ prod) {
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const float* xr = x + (size_t)r * ld;
+  const float* dr = dy + (size_t)r * ld;
+  float s = 0.f;
+  for (int j = lane; j < d; j += 32) s += xr[j];
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+  for (int j = lane; j < d; j += 32) {
+    const float t = xr[j] - mean;
+    q = fmaf(t, t, q);
+  }
+  const float rstd = rsqrtf(warp_sum(q) / d + 1e-5f);
+  float s1 = 0.f, s2 = 0.f;
+  for (int j = lane; j < d; j += 32) {
+    const float xh = (xr[j] - mean) * rstd, dxh = dr[j] * g[j];
+    s1 += dxh;
+    s2 = fmaf(dxh, xh, s2);
+  }
+  const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) / d;
+  for (int j = lane; j < ld; j += 32) {
+    float o = 0.f, pr = 0.f;
+    if (j < d) {
+      const float xh = (xr[j] - mean) * rstd, dxh = dr[j] * g[j];
+      o = rstd * (dxh - m1 - xh * m2);
+      pr = dr[j] * xh;
+    }
+    const float h = tf32_hi(o);
+    dx_hi[(size_t)r * ld + j] = h;
+    dx_lo[(size_t)r * ld + j] = o - h;
+    prod[(size_t)r * ld + j] = pr;
+  }
+}
+
+// attention backward per (AST, head) (nn.py:99-120), P recomputed
+__global__ void attention_back_kernel(const float* __restrict__ qkv, int ldq,
+                                      const float* __restrict__ dctx, int ldc,
+                                      const int32_t* __restrict__ tok_off, int d, int nh, int dh,
+                                      float scale, float* __restrict__ g_hi,
+                                      float* __restrict__ g_lo) {
+  extern __shared__ float sm[];
+  const int s = blockIdx.x, h = blockIdx.y;
+  const int t0 = tok_off[s], L = tok_off[s + 1] - t0;
+  const int dhp = dh + 1;
+  float* q = sm;
+  float* k = q + TPCB_MAX_LEAF * dhp;
+  float* v = k + TPCB_MAX_LEAF * dhp;
+  float* dc = v + TPCB_MAX_LEAF * dhp;
+  float* p = dc + TPCB_MAX_LEAF * dhp;  // [16][17]
+  float* dp = p + 16 * 17;              // [16][17]
+  for (int e = threadIdx.x; e < L * dh; e += blockDim.x) {
+    const int l = e / dh, j = e - l * dh;
+    const float* row = qkv + (size_t)(t0 + l) * ldq + h * dh + j;
+    q[l * dhp + j] = row[0];
+    k[l * dhp + j] = row[d];
+    v[l * dhp + j] = row[2 * d];
+    dc[l * dhp + j] = dctx[(size_t)(t0 + l) * ldc + h * dh + j];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
+    const int i = e / L, j = e - i * L;
+    float acc = 0.f, acc2 = 0.f;
+    for (int c = 0; c < dh; ++c) {
+      acc = fmaf(q[i * dhp + c], k[j * dhp + c], acc);
+      acc2 = fmaf(dc[i * dhp + c], v[j * dhp + c], acc2);
+    }
+    p[i * 17 + j] = acc * scale;
+    dp[i * 17 + j] = acc2;
+  }
+  __syncthreads();
+  if (threadIdx.x < L) {
+    const int i = threadIdx.x;
+    float m = -INFINITY;
+    for (int j = 0; j < L; ++j) m = fmaxf(m, p[i * 17 + j]);
+    float sum = 0.f;
+    for (int j = 0; j < L; ++j) {
+      const float ex = expf(p[i * 17 + j] - m);
+      p[i * 17 + j] = ex;
+      sum += ex;
+    }
+    float rd = 0.f;
+    for (int j = 0; j < L; ++j) {
+      p[i * 17 + j] /= sum;
+      rd = fmaf(p[i * 17 + j], dp[i * 17 + j], rd);
+    }
+    for (int j = 0; j < L; ++j) dp[i * 17 + j] = p[i * 17 + j] * (dp[i * 17 + j] - rd) * scale;
+  }
+  __syncthreads();
+  auto put = [&](int row, int col, float val) {
+    const size_t o = (size_t)row * ldq + col;
+    const float hi = tf32_hi(val);
+    g_hi[o] = hi;
+    g_lo[o] = val - hi;
+  };
+  for (int e = threadIdx.x; e < L * dh; e += blockDim.x) {
+    const int i = e / dh, c = e - i * dh;
+    float gq = 0.f, gk = 0.f, gv = 0.f;
+    for (int j = 0; j < L; ++j) {
+      gq = fmaf(dp[i * 17 + j], k[j * dhp + c], gq);  // dQ_i = Σ_j dS_ij k_j
+      gk = fmaf(dp[j * 17 + i], q[j * dhp + c], gk);  // dK_i = Σ_j dS_ji q_j
+      gv = fmaf(p[j * 17 + i], dc[j * dhp + c], gv);  // dV_i = Σ_j P_ji dc_j
+    }
+    put(t0 + i, h * dh + c, gq);
+    put(t0 + i, d + h * dh + c, gk);
+    put(t0 + i, 2 * d + h * dh + c, gv);
+  }
+  if (h == nh - 1) {
+    const int padw = ldq - 3 * d;
+    for (int e = threadIdx.x; e < L * padw; e += blockDim.x) {
+      const int i = e / padw, j = e - i * padw;
+      put(t0 + i, 3 * d + j, 0.f);
+    }
+  }
+}
+
+// loss + dL/dpred (costmodel.py:343-423, transformed space; oracle
+// predictor.loss_and_grad), one block, fixed-order reduction; pred / dpred in
+// the batch's sorted order, y gathered through idx
+__global__ void loss_kernel(const float* __restrict__ pred, const double* __restrict__ y,
+                            const int32_t* __restrict__ idx, int n, int mode, double lam,
+                            double offset, double n_norm, float* __restrict__ dpred,
+                            double* __restrict__ loss_out) {
+  __shared__ double red[32];
+  double acc_sq = 0.0, acc_rel = 0.0;
+  for (int s = threadIdx.x; s < n; s += blockDim.x) {
+    const double yy = y[idx[s]], d = (double)pred[s] - yy;
+    const double den = yy + offset;
+    const double sg = d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0);
+    double g;
+    if (mode == 1) g = 2.0 * d / n_norm;                        // mse
+    else if (mode == 2) g = sg / (den * n_norm);                // mape
+    else g = 2.0 * d / n_norm + lam * sg / (den * n_norm);      // hybrid
+    dpred[s] = (float)g;
+    acc_sq += d * d;
+    acc_rel += fabs(d) / den;
+  }
+  double v = mode == 1 ? acc_sq : mode == 2 ? acc_rel : acc_sq + lam * acc_rel;
+  v = warp_sum_d(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double w = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    w = warp_sum_d(w);
+    if (threadIdx.x == 0) loss_out[0] = w / n;  // batch mean (the step's loss)
+  }
+}
+
+// dec.out backward: dD = dpred ⊗ outW ⊙ [D > 0] (pair), prod = D·dpred (→ doutW)
+__global__ void out_back_kernel(Model M, const float* __restrict__ P, const float* __restrict__ d_hi,
+                                const float* __restrict__ d_lo, int ld, int width,
+                                const float* __restrict__ dpred, int n, float* __restrict__ g_hi,
+                                float* __restrict__ g_lo, float* __restrict__ prod) {
+  const int s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (s >= n) return;
+  const int lane = threadIdx.x & 31;
+  const float dp = dpred[s];
+  for (int j = lane; j < ld; j += 32) {
+    const size_t o = (size_t)s * ld + j;
+    float g = 0.f, pr = 0.f;
+    if (j < width) {
+      const float h = d_hi[o];
+      pr = (h + d_lo[o]) * dp;
+      g = h > 0.f ? dp * P[M.outW + j] : 0.f;
+    }
+    const float hi = tf32_hi(g);
+    g_hi[o] = hi;
+    g_lo[o] = g - hi;
+    prod[o] = pr;
+  }
+}
+
+// gate + device MLP backward per sorted AST: dzx = dz⊙zp (pair), per-sample
+// parameter-gradient rows (column-summed afterwards, fixed order)
+__global__ void gate_back_kernel(Model M, const float* __restrict__ P,
+                                 const float* __restrict__ devfeat,
+                                 const int32_t* __restrict__ idx, const float* __restrict__ dz,
+                                 const float* __restrict__ zx, int ldz, float* __restrict__ gx_hi,
+                                 float* __restrict__ gx_lo, float* __restrict__ tWp,
+                                 float* __restrict__ tbp, float* __restrict__ tWh,
+                                 float* __restrict__ tbh) {
+  extern __shared__ float sv[];  // zv [ddev] | dzp [de] | dzv [ddev]
+  float* zv = sv;
+  float* dzp = zv + M.d_dev;
+  float* dzv = dzp + M.d_e;
+  const int s = blockIdx.x;
+  const float* dv = devfeat + (size_t)idx[s] * TPCB_DEV_FEAT;
+  for (int j = threadIdx.x; j < M.d_dev; j += blockDim.x) {
+    float a = P[M.devhb + j];
+    for (int k = 0; k < TPCB_DEV_FEAT; ++k) a = fmaf(dv[k], P[M.devhW + k * M.d_dev + j], a);
+    zv[j] = fmaxf(a, 0.f);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < ldz; e += blockDim.x) {
+    float gx = 0.f;
+    if (e < M.d_e) {
+      float zp = P[M.devpb + e];
+      for (int j = 0; j < M.d_dev; ++j) zp = fmaf(zv[j], P[M.devpW + j * M.d_e + e], zp);
+      const float g = dz[(size_t)s * ldz + e];
+      gx = g * zp;
+      const float gp = g * zx[(size_t)s * ldz + e];
+      dzp[e] = gp;
+      tbp[(size_t)s * M.d_e + e] = gp;
+    }
+    const float hi = tf32_hi(gx);
+    gx_hi[(size_t)s * ldz + e] = hi;
+    gx_lo[(size_t)s * ldz + e] = gx - hi;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < M.d_dev; j += blockDim.x) {
+    float a = 0.f;
+    for (int e = 0; e < M.d_e; ++e) a = fmaf(dzp[e], P[M.devpW + j * M.d_e + e], a);
+    a = zv[j] > 0.f ? a : 0.f;
+    dzv[j] = a;
+    tbh[(size_t)s * M.d_dev + j] = a;
+  }
+  __syncthreads();
+  const int nwp = M.d_dev * M.d_e;
+  for (int e = threadIdx.x; e < nwp; e += blockDim.x)
+    tWp[(size_t)s * nwp + e] = zv[e / M.d_e] * dzp[e % M.d_e];
+  const int nwh = TPCB_DEV_FEAT * M.d_dev;
+  for (int e = threadIdx.x; e < nwh; e += blockDim.x)
+    tWh[(size_t)s * nwh + e] = dv[e / M.d_dev] * dzv[e % M.d_dev];
+}
+
+struct Bwd {
+  int64_t Tp, Ap;
+  float* dh;                 // [T, dp] fp32
+  float *ds_hi, *ds_lo;      // [T, dp]
+  float *df_hi, *df_lo;      // [T, ffp]
+  float* dctx;               // [T, dp]
+  float *dq_hi, *dq_lo;      // [T, qkvp]
+  float* prod;               // [T, max(dp, dmax)]
+  float *xt_hi, *xt_lo, *yt_hi, *yt_lo;
+  float* part;
+  float *dd_hi[2], *dd_lo[2];  // decoder grads [A, dmax]
+  float* dz;                 // [A, dep]
+  float *dzx_hi, *dzx_lo;    // [A, dep]
+  float *tWp, *tbp, *tWh, *tbh;
+  float* dpred;
+  size_t part_floats;
+};
+
+Bwd carve_bwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, Carver* cv) {
+  Bwd b{};
+  const int64_t T = ((n_tok + kTileM - 1) / kTileM) * kTileM;
+  const int64_t A = ((n_ast + kTileM - 1) / kTileM) * kTileM;
+  b.Tp = T;
+  b.Ap = A;
+  const int dmax = dec_max(M);
+  b.dh = cv->take(T * p.dp);
+  b.ds_hi = cv->take(T * p.dp);
+  b.ds_lo = cv->take(T * p.dp);
+  b.df_hi = cv->take(T * p.ffp);
+  b.df_lo = cv->take(T * p.ffp);
+  b.dctx = cv->take(T * p.dp);
+  b.dq_hi = cv->take(T * p.qkvp);
+  b.dq_lo = cv->take(T * p.qkvp);
+  b.prod = cv->take(max(T * p.dp, A * (int64_t)dmax));
+  const int64_t wmax = max(max(p.qkvp, p.ffp), max(p.dp, dmax));
+  const int64_t xt = max(wmax * (T + 32), (int64_t)p.dp * (T + 32 * TPCB_MAX_LEAF + 32));
+  b.xt_hi = cv->take(xt);
+  b.xt_lo = cv->take(xt);
+  b.yt_hi = cv->take(xt);
+  b.yt_lo = cv->take(xt);
+  const int64_t pm = max(max((int64_t)M.d * p.qkvp, (int64_t)M.d_ff * p.dp),
+                         max((int64_t)M.d * p.ffp, (int64_t)TPCB_MAX_LEAF * p.dp * p.dep));
+  b.part_floats = 8 * max(pm, (int64_t)dmax * dmax);
+  b.part = cv->take(b.part_floats);
+  for (int k = 0; k < 2; ++k) {
+    b.dd_hi[k] = cv->take(A * dmax);
+    b.dd_lo[k] = cv->take(A * dmax);
+  }
+  b.dz = cv->take(A * p.dep);
+  b.dzx_hi = cv->take(A * p.dep);
+  b.dzx_lo = cv->take(A * p.dep);
+  b.tWp = cv->take(A * M.d_dev * M.d_e);
+  b.tbp = cv->take(A * M.d_e);
+  b.tWh = cv->take(A * TPCB_DEV_FEAT * M.d_dev);
+  b.tbh = cv->take(A * M.d_dev);
+  b.dpred = cv->take(A);
+  return b;
+}
+
+int transpose_into(const float* hi, const float* lo, int rows, int cols, int ld, float* o_hi,
+                   float* o_lo, int ldo, cudaStream_t st) {
+  const dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(ldo, 32));
+  transpose_pair_kernel<<<grid, dim3(32, 8), 0, st>>>(hi, lo, rows, cols, ld, o_hi, o_lo, ldo);
+  TPCB_LAUNCH_CHECK("large_transpose");
+  return TPCB_OK;
+}
+
+int colsum(const float* x, const float* x_lo, int rows, int cols, int ld, ColDst dst, float* grad,
+           cudaStream_t st) {
+  colsum_kernel<<<ceil_div(cols, 32), dim3(32, 8), 0, st>>>(x, x_lo, rows, cols, ld, dst, grad);
+  TPCB_LAUNCH_CHECK("large_colsum");
+  return TPCB_OK;
+}
+
+ColDst one(int64_t off, int colw) { return ColDst{colw, {off, off, off}}; }
+
+// dW[M_in, N_out] = Xᵀ·dY over K = kp rows: X given as [rows, M_in] (ld_x),
+// dY as [rows, N_out] (ld_y) — both transposed + split here
+int wgrad(const Ctx& c, Bwd& b, const float* x_hi, const float* x_lo, int ld_x, int m_in,
+          const float* y_hi, const float* y_lo, int ld_y, int n_out, int rows, int seg, int segp,
+          ColDst dst, float* grad) {
+  cudaStream_t st = c.st;
+  const int kp = pad32(rows);
+  int rc;
+  if ((rc = transpose_into(x_hi, x_lo, rows, m_in, ld_x, b.xt_hi, b.xt_lo, kp, st))) return rc;
+  if ((rc = transpose_into(y_hi, y_lo, rows, n_out, ld_y, b.yt_hi, b.yt_lo, kp, st))) return rc;
+  const int ldc = pad32(n_out);
+  const int tiles = ceil_div(m_in, kTileM) * ceil_div(ldc, 128);
+  const int k_total = kp / 32;
+  int splits = max(1, min(min(2 * kNumSMs / max(tiles, 1), k_total / 4), 8));
+  const int kc = ceil_div(k_total, splits);
+  splits = ceil_div(k_total, kc);
+  if ((size_t)splits * m_in * ldc > b.part_floats) return TPCB_ERR_VALIDATION;
+  Epi e{m_in, n_out, ldc, nullptr, 0, nullptr, nullptr, 0, b.part, nullptr, nullptr};
+  e.split_stride = (int64_t)m_in * ldc;
+  Operand A{b.xt_hi, b.xt_lo, m_in, kp, kp}, B{b.yt_hi, b.yt_lo, n_out, kp, kp};
+  if ((rc = launch_gemm_nt<128>(A, B, e, st, splits))) return rc;
+  const int64_t total = (int64_t)m_in * n_out;
+  reduce_grad_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, kNumSMs * 8), 256, 0, st>>>(
+      b.part, splits, e.split_stride, m_in, n_out, ldc, seg, segp, dst, grad);
+  TPCB_LAUNCH_CHECK("large_reduce_grad");
+  return TPCB_OK;
+}
+
+}  // namespace
+}  // namespace tpcb
+
+extern "C" int tpcb_large_train_ws(const tpcb_model* m, int64_t n_ast, int64_t n_tok,
+                                   size_t* ws_bytes) {
+  if (!m || !ws_bytes) return TPCB_ERR_VALIDATION;
+  if (!large_supported(m->dev)) return TPCB_ERR_UNSUPPORTED;
+  const LargePlan p = make_plan(m->dev);
+  Carver cv{nullptr};
+  carve_fwd(p, m->dev, n_tok, n_ast, true, &cv);
+  carve_bwd(p, m->dev, n_tok, n_ast, &cv);
+  *ws_bytes = cv.o;
+  return TPCB_OK;
+}
+
+// one training batch through the large path: forward (activations kept),
+// loss, backward → the full flat gradient d_grad (rewritten) and the batch
+// loss d_loss[0] (device).  Dataset-resident inputs: packed rows d_x (K1
+// layout) with d_ast_row, device features, model-space targets d_y; the
+// batch is h_idx (dataset indices in bucket order) with token offsets
+// h_tok_off; gradients are normalised by n_norm (the global batch size).
+extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_params,
+                                        const void* d_image, const float* d_x,
+                                        const int32_t* d_ast_row, const float* d_devfeat,
+                                        const double* d_y, const int32_t* h_idx,
+                                        const int32_t* h_tok_off, const int32_t* d_idx,
+                                        const int32_t* d_tok_off, int64_t n_batch,
+                                        const tpcb_loss* loss, double n_norm, void* d_ws,
+                                        size_t ws_bytes, float* d_grad, double* d_loss,
+                                        int32_t* d_status, void* stream_) {
+  if (!m || !d_params || !d_image || !d_x || !d_ast_row || !d_devfeat || !d_y || !h_idx ||
+      !h_tok_off || !loss || !d_ws || !d_grad || !d_loss)
+    return TPCB_ERR_VALIDATION;
+  if (n_batch <= 0) return TPCB_ERR_EMPTY_BATCH;
+  const Model& M = m->dev;
+  if (!large_supported(M)) return TPCB_ERR_UNSUPPORTED;
+  if (loss->original_space || loss->alpha_cmd != 0.0 || M.n_dec < 1) return TPCB_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream_;
+  const LargePlan p = make_plan(M);
+  const int64_t n_tok = h_tok_off[n_batch];
+  Carver cv{(uint8_t*)d_ws};
+  Fwd f = carve_fwd(p, M, n_tok, n_batch, true, &cv);
+  Bwd b = carve_bwd(p, M, n_tok, n_batch, &cv);
+  if (cv.o > ws_bytes) return TPCB_ERR_VALIDATION;
+  if (d_idx && d_tok_off) {  // device copies of the plan (uploaded once per epoch)
+    f.idx = const_cast<int32_t*>(d_idx);
+    f.tok_off = const_cast<int32_t*>(d_tok_off);
+  } else {
+    TPCB_CUDA_CHECK(cudaMemcpyAsync(f.idx, h_idx, n_batch * 4, cudaMemcpyHostToDevice, st));
+    TPCB_CUDA_CHECK(
+        cudaMemcpyAsync(f.tok_off, h_tok_off, (n_batch + 1) * 4, cudaMemcpyHostToDevice, st));
+  }
+  gather_tokens_kernel<<<ceil_div(n_batch, 8), 256, 0, st>>>(d_x, f.idx, d_ast_row, f.tok_off,
+                                                             (int)n_batch, f.x_hi, f.x_lo);
+  TPCB_LAUNCH_CHECK("large_gather");
+  const Ctx c{M, p, d_params, carve_image(p, (uint8_t*)const_cast<void*>(d_image)), st};
+  tpcb_boxcox bc{};
+  int rc = run_forward(c, f, n_batch, h_tok_off, d_devfeat, true, bc, nullptr, nullptr, nullptr,
+                       nullptr, nullptr, d_status);
+  if (rc) return rc;
+  const float* P = d_params;
+  float* G = d_grad;
+  const int nt = (int)n_tok, nb = (int)n_batch;
+  TPCB_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(float) * (size_t)M.total, st));
+  loss_kernel<<<1, 1024, 0, st>>>(f.pred, d_y, f.idx, nb, loss->mode, loss->lambda_hybrid,
+                                  loss->offset, n_norm, b.dpred, d_loss);
+  TPCB_LAUNCH_CHECK("large_loss");
+  // ---- head: dec.out, decoder, gate + device MLP, leaf_embed ----
+  const int nd = M.n_dec;
+  const int wl = nd ? M.dec[nd - 1] : M.d_e, ldl = pad32(wl);
+  out_back_kernel<<<ceil_div(nb, 8), 256, 0, st>>>(M, P, f.dec_hi[nd - 1], f.dec_lo[nd - 1], ldl,
+                                                   wl, b.dpred, nb, b.dd_hi[0], b.dd_lo[0], b.prod);
+  TPCB_LAUNCH_CHECK("large_out_back");
+  if ((rc = colsum(b.prod, nullptr, nb, wl, ldl, one(M.outW, wl), G, st))) return rc;
+  if ((rc = colsum(b.dpred, nullptr, nb, 1, 1, one(M.outb, 1), G, st))) return rc;
+  int cur = 0;
+  for (int i = nd - 1; i >= 0; --i) {
+    const int wo = M.dec[i], ldo = pad32(wo);
+    const int wi = i ? M.dec[i - 1] : M.d_e, ldi = pad32(wi);
+    const float* in_hi = i ? f.dec_hi[i - 1] : f.z_hi;
+    const float* in_lo = i ? f.dec_lo[i - 1] : f.z_lo;
+    if ((rc = wgrad(c, b, in_hi, in_lo, ldi, wi, b.dd_hi[cur], b.dd_lo[cur], ldo, wo, nb, 0, 0,
+                    one(M.decW[i], wo), G)))
+      return rc;
+    if ((rc = colsum(b.dd_hi[cur], b.dd_lo[cur], nb, wo, ldo, one(M.decb[i], wo), G, st)))
+      return rc;
+    Operand A = act_op(b.dd_hi[cur], b.dd_lo[cur], nb, ldo);
+    Operand B{c.im.hi + p.dec_b[i], c.im.lo + p.dec_b[i], wi, ldo, ldo};
+    if (i) {
+      Epi e{nb, wi, ldi, nullptr, 0, nullptr, nullptr, 0, nullptr, b.dd_hi[cur ^ 1],
+            b.dd_lo[cur ^ 1]};
+      e.mask = f.dec_hi[i - 1];
+      e.ldm = ldi;
+      if ((rc = launch_gemm(A, B, e, st))) return rc;
+      cur ^= 1;
+    } else {
+      Epi e{nb, wi, ldi, nullptr, 0, nullptr, nullptr, 0, b.dz, nullptr, nullptr};
+      if ((rc = launch_gemm(A, B, e, st))) return rc;
+    }
+  }
+  gate_back_kernel<<<nb, 128, (2 * M.d_dev + M.d_e) * 4, st>>>(
+      M, P, d_devfeat, f.idx, b.dz, f.zx, p.dep, b.dzx_hi, b.dzx_lo, b.tWp, b.tbp, b.tWh, b.tbh);
+  TPCB_LAUNCH_CHECK("large_gate_back");
+  if ((rc = colsum(b.tWp, nullptr, nb, M.d_dev * M.d_e, M.d_dev * M.d_e,
+                   one(M.devpW, M.d_dev * M.d_e), G, st)))
+    return rc;
+  if ((rc = colsum(b.tbp, nullptr, nb, M.d_e, M.d_e, one(M.devpb, M.d_e), G, st))) return rc;
+  if ((rc = colsum(b.tWh, nullptr, nb, TPCB_DEV_FEAT * M.d_dev, TPCB_DEV_FEAT * M.d_dev,
+                   one(M.devhW, TPCB_DEV_FEAT * M.d_dev), G, st)))
+    return rc;
+  if ((rc = colsum(b.tbh, nullptr, nb, M.d_dev, M.d_dev, one(M.devhb, M.d_dev), G, st))) return rc;
+  const Pair hf = f.H(M.n_layers);
+  for (int64_t s0 = 0; s0 < n_batch;) {
+    const int Lb = h_tok_off[s0 + 1] - h_tok_off[s0];
+    int64_t s1 = s0 + 1;
+    while (s1 < n_batch && h_tok_off[s1 + 1] - h_tok_off[s1] == Lb) ++s1;
+    const int nbk = (int)(s1 - s0);
+    const int64_t t0 = h_tok_off[s0];
+    const int w = Lb * p.dp;
+    Operand A = act_op(b.dzx_hi + s0 * p.dep, b.dzx_lo + s0 * p.dep, nbk, p.dep);
+    Operand B{c.im.hi + p.leaf_b[Lb], c.im.lo + p.leaf_b[Lb], w, p.dep, p.dep};
+    Epi e{nbk, w, w, nullptr, 0, nullptr, nullptr, 0, b.dh + t0 * p.dp, nullptr, nullptr};
+    if ((rc = launch_gemm(A, B, e, st))) return rc;
+    if ((rc = wgrad(c, b, hf.hi + t0 * p.dp, hf.lo + t0 * p.dp, w, w, b.dzx_hi + s0 * p.dep,
+                    b.dzx_lo + s0 * p.dep, p.dep, M.d_e, nbk, M.d, p.dp, one(M.leafW[Lb], M.d_e),
+                    G)))
+      return rc;
+    if ((rc = colsum(b.dzx_hi + s0 * p.dep, b.dzx_lo + s0 * p.dep, nbk, M.d_e, p.dep,
+                     one(M.leafb[Lb], M.d_e), G, st)))
+      return rc;
+    s0 = s1;
+  }
+  // ---- encoder, top layer first ----
+  const float scale = 1.0f / sqrtf((float)M.dh);
+  const size_t att_smem = (size_t)(4 * TPCB_MAX_LEAF * (M.dh + 1) + 2 * 16 * 17) * 4;
+  if (att_smem > 48 * 1024)
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(attention_back_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)att_smem));
+  for (int li = M.n_layers - 1; li >= 0; --li) {
+    const LayerOff& L = M.layer[li];
+    const Pair h = f.H(li), h1 = f.H1(li), ff = f.F(li), ctx = f.C(li);
+    // LN2
+    ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S2(li), p.dp, nt, M.d, P + L.ln2g,
+                                                    b.ds_hi, b.ds_lo, b.prod);
+    TPCB_LAUNCH_CHECK("large_ln_back");
+    if ((rc = colsum(b.prod, nullptr, nt, M.d, p.dp, one(L.ln2g, M.d), G, st))) return rc;
+    if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln2b, M.d), G, st))) return rc;
+    // FFN out
+    if ((rc = wgrad(c, b, ff.hi, ff.lo, p.ffp, M.d_ff, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
+                    one(L.foW, M.d), G)))
+      return rc;
+    if ((rc = colsum(b.ds_hi, b.ds_lo, nt, M.d, p.dp, one(L.fob, M.d), G, st))) return rc;
+    {
+      Epi e{nt, M.d_ff, p.ffp, nullptr, 0, nullptr, nullptr, 0, nullptr, b.df_hi, b.df_lo};
+      e.mask = ff.hi;
+      e.ldm = p.ffp;
+      Operand B{c.im.hi + p.layer_b[li][3], c.im.lo + p.layer_b[li][3], M.d_ff, p.dp, p.dp};
+      if ((rc = launch_gemm(act_op(b.ds_hi, b.ds_lo, nt, p.dp), B, e, st))) return rc;
+    }
+    // FFN hidden
+    if ((rc = wgrad(c, b, h1.hi, h1.lo, p.dp, M.d, b.df_hi, b.df_lo, p.ffp, M.d_ff, nt, 0, 0,
+                    one(L.fhW, M.d_ff), G)))
+      return rc;
+    if ((rc = colsum(b.df_hi, b.df_lo, nt, M.d_ff, p.ffp, one(L.fhb, M.d_ff), G, st))) return rc;
+    {
+      Epi e{nt, M.d, p.dp, nullptr, 0, b.ds_hi, b.ds_lo, p.dp, b.dh, nullptr, nullptr};
+      Operand B{c.im.hi + p.layer_b[li][2], c.im.lo + p.layer_b[li][2], M.d, p.ffp, p.ffp};
+      if ((rc = launch_gemm(act_op(b.df_hi, b.df_lo, nt, p.ffp), B, e, st))) return rc;
+    }
+    // LN1
+    ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S1(li), p.dp, nt, M.d, P + L.ln1g,
+                                                    b.ds_hi, b.ds_lo, b.prod);
+    TPCB_LAUNCH_CHECK("large_ln_back");
+    if ((rc = colsum(b.prod, nullptr, nt, M.d, p.dp, one(L.ln1g, M.d), G, st))) return rc;
+    if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln1b, M.d), G, st))) return rc;
+    // attention output projection
+    if ((rc = wgrad(c, b, ctx.hi, ctx.lo, p.dp, M.d, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
+                    one(L.Wo, M.d), G)))
+      return rc;
+    if ((rc = colsum(b.ds_hi, b.ds_lo, nt, M.d, p.dp, one(L.bo, M.d), G, st))) return rc;
+    {
+      Epi e{nt, M.d, p.dp, nullptr, 0, nullptr, nullptr, 0, b.dctx, nullptr, nullptr};
+      Operand B{c.im.hi + p.layer_b[li][1], c.im.lo + p.layer_b[li][1], M.d, p.dp, p.dp};
+      if ((rc = launch_gemm(act_op(b.ds_hi, b.ds_lo, nt, p.dp), B, e, st))) return rc;
+    }
+    attention_back_kernel<<<dim3((unsigned)n_batch, M.n_heads), 128, att_smem, st>>>(
+        f.QKV(li), p.qkvp, b.dctx, p.dp, f.tok_off, M.d, M.n_heads, M.dh, scale, b.dq_hi,
+        b.dq_lo);
+    TPCB_LAUNCH_CHECK("large_attention_back");
+    // Q | K | V projections
+    const ColDst qkv_dst{M.d, {(int64_t)L.Wq, (int64_t)L.Wk, (int64_t)L.Wv}};
+    const ColDst qkvb_dst{M.d, {(int64_t)L.bq, (int64_t)L.bk, (int64_t)L.bv}};
+    if ((rc = wgrad(c, b, h.hi, h.lo, p.dp, M.d, b.dq_hi, b.dq_lo, p.qkvp, p.qkv, nt, 0, 0,
+                    qkv_dst, G)))
+      return rc;
+    if ((rc = colsum(b.dq_hi, b.dq_lo, nt, p.qkv, p.qkvp, qkvb_dst, G, st))) return rc;
+    {
+      Epi e{nt, M.d, p.dp, nullptr, 0, b.ds_hi, b.ds_lo, p.dp, b.dh, nullptr, nullptr};
+      Operand B{c.im.hi + p.layer_b[li][0], c.im.lo + p.layer_b[li][0], M.d, p.qkvp, p.qkvp};
+      if ((rc = launch_gemm(act_op(b.dq_hi, b.dq_lo, nt, p.qkvp), B, e, st))) return rc;
+    }
+  }
+  // input projection
+  if ((rc = wgrad(c, b, f.x_hi, f.x_lo, 32, TPCB_FEAT, b.dh, nullptr, p.dp, M.d, nt, 0, 0,
+                  one(M.inW, M.d), G)))
+    return rc;
+  if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(M.inb, M.d), G, st))) return rc;
+  return TPCB_OK;
 }

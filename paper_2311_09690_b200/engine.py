@@ -256,20 +256,23 @@ class LargePath:
     (hi, lo) weight image is built once per parameter version; the activation
     workspace grows on demand."""
 
-    def __init__(self, dm: DeviceModel, params: torch.Tensor):
+    def __init__(self, dm: DeviceModel, params: torch.Tensor, with_backward: bool = False):
         self.lib = _lib.load()
         self.dm, self.params = dm, params
+        self.with_backward = with_backward
         img, act = C.c_size_t(), C.c_size_t()
         _lib.check(self.lib.tpcb_large_sizes(dm.handle, 1, 1, C.byref(img), C.byref(act)),
                    "large_sizes")
-        self.image = torch.empty(img.value, dtype=torch.uint8, device=params.device)
+        self.image = torch.zeros(img.value, dtype=torch.uint8, device=params.device)
         self.act = torch.empty(0, dtype=torch.uint8, device=params.device)
         self.prepare()
 
     def prepare(self) -> None:
+        flags = int(self.with_backward) | (2 if getattr(self, "_table", False) else 0)
         _lib.check(self.lib.tpcb_large_prepare(self.dm.handle, self.params.data_ptr(),
-                                               self.image.data_ptr(), stream_ptr()),
+                                               self.image.data_ptr(), flags, stream_ptr()),
                    "large_prepare")
+        self._table = True
 
     @staticmethod
     def order(n_leaf: np.ndarray):

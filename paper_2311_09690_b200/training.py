@@ -315,9 +315,23 @@ def train(config, ds, devices: dict, normalizer=None) -> TrainResult:
     if config.loss_mode != "mse" and config.mape_space == "transformed" and \
             np.any(targets + normalizer.loss_offset <= 0):
         raise ValidationError("shifted labels must be positive")
-    tr = Trainer(config, params.tensors, train_rag, targets, _loss_from_config(config, normalizer),
-                 valid_rag, valid_lat, normalizer)
+    loss = _loss_from_config(config, normalizer)
+    if needs_large_path(config):
+        from .large_training import LargeTrainer
+        tr = LargeTrainer(config, params.tensors, train_rag, targets, loss, valid_rag, valid_lat,
+                          normalizer)
+    else:
+        tr = Trainer(config, params.tensors, train_rag, targets, loss, valid_rag, valid_lat,
+                     normalizer)
     return run_loop(tr, config, params, normalizer, select_best=True)
+
+
+def needs_large_path(config) -> bool:
+    """True when the fused kernels cannot hold the model (e.g.
+    full_reference_config): training and inference then run layer by layer
+    on the tensor cores (csrc/large.cu)."""
+    from .costmodel import device_model
+    return not _lib.load().tpcb_forward_fits(device_model(config).handle, 64)
 
 
 def run_loop(tr: Trainer, config, params, normalizer, select_best: bool) -> TrainResult:

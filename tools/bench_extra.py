@@ -7,7 +7,11 @@
       tensor-core (3xTF32 + exact re-rank) assignment modes
   C5  inference sweep n = 64 … 1M ASTs, fp32 parity mode and bf16 tensor-core mode
 
-python tools/bench_extra.py [c3] [c4] [c4tc] [c5] [c5bf16]     (default: all)
+  full  full_reference_config (d 716, 11 layers, 46.7 M params) inference
+        through the layer-by-layer tensor-core path, and the 3xTF32 GEMM alone
+  c4dp  point-sharded KMeans (kmeans_sharded) at the launched world size
+
+python tools/bench_extra.py [c3] [c4] [c4tc] [c5] [c5bf16] [full] [c4dp]  (default: all)
 """
 import json
 import sys
@@ -134,10 +138,87 @@ def c5(precision="fp32"):
             "unit": "ASTs/s", "by_n": res, "dtype": precision}
 
 
+def full():
+    out = []
+    lib = pb._lib.load()
+    cfg = pb.full_reference_config()
+    p = pb.Predictor(pb.init_params(cfg))
+    assert p.large is not None
+    big = synth.generate(16384, seed=0)
+    flops_ast = None
+    for n in (600, 4096, 16384):
+        sub = big.take(np.arange(n))
+        r = rag(sub)
+        rows, ordering, leaf_off, devfeat = engine.upload_ragged(r, torch.device("cuda"))
+        f = lambda: p.forward_device(rows, ordering, leaf_off, devfeat, n, False, None,  # noqa
+                                     latents=False, n_leaf=r.n_leaf)
+        for _ in range(3):
+            f()
+        t = dev_time(f, 5)
+        L = sub.n_leaf.astype(np.float64)
+        d, ff, de = cfg.d_model, cfg.d_ff, cfg.d_embed
+        fl = (2 * L * 24 * d + cfg.n_layers * (8 * L * d * d + 4 * L * L * d + 4 * L * d * ff)
+              + 2 * L * d * de + 2 * 6 * cfg.d_device + 2 * cfg.d_device * de + de)
+        dims = [de] + list(cfg.decoder_dims) + [1]
+        fl = fl + sum(2 * a * b for a, b in zip(dims[:-1], dims[1:]))
+        flops_ast = fl.mean()
+        out.append({"metric": f"full_reference_config inference ASTs/s (n={n}, 1 GPU)",
+                    "value": n / t, "unit": "ASTs/s", "ms": t * 1e3,
+                    "model_tflops": n * flops_ast / t / 1e12,
+                    "mflop_per_ast": flops_ast / 1e6,
+                    "dtype": "3xTF32 tcgen05 GEMMs, fp32 accumulate"})
+    # the GEMM alone (pre-split operands): QKV-shaped, M = 16384 tokens
+    for M, N, K in ((16384, 2148, 736), (16384, 716, 992), (65536, 716, 736)):
+        kp = (K + 31) // 32 * 32
+        a = [torch.randn(M, kp, device="cuda") for _ in range(2)]
+        b = [torch.randn(N, kp, device="cuda") for _ in range(2)]
+        ldc = (N + 31) // 32 * 32
+        c = torch.empty(M, ldc, device="cuda")
+        s = torch.cuda.current_stream().cuda_stream
+        g = lambda: lib.tpcb_gemm3_presplit(a[0].data_ptr(), a[1].data_ptr(), b[0].data_ptr(),  # noqa
+                                            b[1].data_ptr(), M, N, kp, c.data_ptr(), ldc, s)
+        for _ in range(3):
+            g()
+        t = dev_time(g, 20)
+        useful = 2.0 * M * N * K
+        out.append({"metric": f"gemm3 {M}x{N}x{K} (3xTF32, pre-split)", "ms": t * 1e3,
+                    "useful_tflops": useful / t / 1e12,
+                    "tensor_pipe_tf32_tflops": 3 * 2.0 * M * N * kp / t / 1e12})
+    return out
+
+
+def c4dp():
+    import os
+    import torch.distributed as dist
+    from paper_2311_09690_b200.sampling import kmeans_sharded
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    world, rank = dist.get_world_size(), dist.get_rank()
+    n, k = 1 << 20, 1024
+    data = synth.generate(n, seed=0)
+    off = data.offsets()
+    pooled = np.add.reduceat(data.vectors.astype(np.float64), off[:-1], axis=0) / data.n_leaf[:, None]
+    part = np.array_split(np.arange(n), world)[rank]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    m = kmeans_sharded(pooled[part], k, seed=0, assign="tc")
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+    tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return {"metric": f"C4 point-sharded KMeans {n}x{k} d24 (k-means++ + Lloyd, tc assign)",
+            "n_gpus": world, "seconds": float(tt.item()), "sizes_sum": int(m.sizes.sum())}
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c3", "c4", "c4tc", "c5", "c5bf16"]
+    which = sys.argv[1:] or ["c3", "c4", "c4tc", "c5", "c5bf16", "full", "c4dp"]
     for w in which:
         r = {"c3": c3, "c4": c4, "c4tc": lambda: c4("tc"), "c5": c5,
-             "c5bf16": lambda: c5("bf16")}[w]()
+             "c5bf16": lambda: c5("bf16"), "full": full, "c4dp": c4dp}[w]()
         for line in (r if isinstance(r, list) else [r]):
             print(json.dumps(line), flush=True)
