@@ -1087,13 +1087,18 @@ struct ColDst {
   int64_t d[3];
 };
 
-__global__ void colsum_kernel(const float* __restrict__ x, const float* __restrict__ x_lo, int rows,
-                              int cols, int ld, ColDst dst, float* __restrict__ grad) {
+// two-stage deterministic column sums: chunks of 64 rows → partial[chunk][c],
+// then the chunks in order
+constexpr int kColChunk = 64;
+
+__global__ void colsum_partial_kernel(const float* __restrict__ x, const float* __restrict__ x_lo,
+                                      int rows, int cols, int ld, float* __restrict__ part) {
   __shared__ float red[8][33];
   const int c = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = blockIdx.y * kColChunk, r1 = min(r0 + kColChunk, rows);
   float acc = 0.f;
   if (c < cols)
-    for (int r = threadIdx.y; r < rows; r += 8) {
+    for (int r = r0 + threadIdx.y; r < r1; r += 8) {
       acc += x[(size_t)r * ld + c];
       if (x_lo) acc += x_lo[(size_t)r * ld + c];
     }
@@ -1102,9 +1107,18 @@ __global__ void colsum_kernel(const float* __restrict__ x, const float* __restri
   if (threadIdx.y == 0 && c < cols) {
     float s = red[0][threadIdx.x];
     for (int k = 1; k < 8; ++k) s += red[k][threadIdx.x];
-    const int t = c / dst.colw;
-    grad[dst.d[t] + (c - t * dst.colw)] = s;
+    part[(size_t)blockIdx.y * cols + c] = s;
   }
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, int cols,
+                                    ColDst dst, float* __restrict__ grad) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = part[c];
+  for (int k = 1; k < chunks; ++k) s += part[(size_t)k * cols + c];
+  const int t = c / dst.colw;
+  grad[dst.d[t] + (c - t * dst.colw)] = s;
 }
 
 // split-K partials [splits][rows][ldc] → grad, rows through the leaf segment
@@ -1376,6 +1390,7 @@ struct Bwd {
   float *dzx_hi, *dzx_lo;    // [A, dep]
   float *tWp, *tbp, *tWh, *tbh;
   float* dpred;
+  float* colpart;            // column-sum partials [chunks][cols]
   size_t part_floats;
 };
 
@@ -1417,6 +1432,8 @@ Bwd carve_bwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, 
   b.tWh = cv->take(A * TPCB_DEV_FEAT * M.d_dev);
   b.tbh = cv->take(A * M.d_dev);
   b.dpred = cv->take(A);
+  b.colpart = cv->take((size_t)ceil_div(max(T, A), kColChunk) *
+                       max(max(M.d_dev * M.d_e, p.qkvp), max(p.ffp, dmax)));
   return b;
 }
 
@@ -1428,9 +1445,40 @@ int transpose_into(const float* hi, const float* lo, int rows, int cols, int ld,
   return TPCB_OK;
 }
 
+thread_local float* g_colsum_part = nullptr;  // column-sum scratch (set per call)
+
+// the weight-gradient branch runs on a side stream: dW = Xᵀ·dY only needs
+// dY, so it overlaps the main stream's dX chain; the main stream waits only
+// for the transposes (after which dY may be overwritten)
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[4] = {};
+  int k = 0;
+  cudaEvent_t next() { return ev[k++ & 3]; }
+};
+thread_local SideStream g_side;
+
+int side_init() {
+  if (g_side.s) return TPCB_OK;
+  TPCB_CUDA_CHECK(cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking));
+  for (auto& e : g_side.ev) TPCB_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return TPCB_OK;
+}
+
+int stream_wait(cudaStream_t waiter, cudaStream_t on) {
+  cudaEvent_t e = g_side.next();
+  TPCB_CUDA_CHECK(cudaEventRecord(e, on));
+  TPCB_CUDA_CHECK(cudaStreamWaitEvent(waiter, e, 0));
+  return TPCB_OK;
+}
+
 int colsum(const float* x, const float* x_lo, int rows, int cols, int ld, ColDst dst, float* grad,
            cudaStream_t st) {
-  colsum_kernel<<<ceil_div(cols, 32), dim3(32, 8), 0, st>>>(x, x_lo, rows, cols, ld, dst, grad);
+  const int chunks = max(1, ceil_div(rows, kColChunk));
+  colsum_partial_kernel<<<dim3(ceil_div(cols, 32), chunks), dim3(32, 8), 0, st>>>(
+      x, x_lo, rows, cols, ld, g_colsum_part);
+  colsum_final_kernel<<<ceil_div(cols, 128), 128, 0, st>>>(g_colsum_part, chunks, cols, dst,
+                                                            grad);
   TPCB_LAUNCH_CHECK("large_colsum");
   return TPCB_OK;
 }
@@ -1442,11 +1490,13 @@ ColDst one(int64_t off, int colw) { return ColDst{colw, {off, off, off}}; }
 int wgrad(const Ctx& c, Bwd& b, const float* x_hi, const float* x_lo, int ld_x, int m_in,
           const float* y_hi, const float* y_lo, int ld_y, int n_out, int rows, int seg, int segp,
           ColDst dst, float* grad) {
-  cudaStream_t st = c.st;
+  const cudaStream_t st = g_side.s;
   const int kp = pad32(rows);
   int rc;
+  if ((rc = stream_wait(st, c.st))) return rc;  // fork: dY is ready on the main stream
   if ((rc = transpose_into(x_hi, x_lo, rows, m_in, ld_x, b.xt_hi, b.xt_lo, kp, st))) return rc;
   if ((rc = transpose_into(y_hi, y_lo, rows, n_out, ld_y, b.yt_hi, b.yt_lo, kp, st))) return rc;
+  if ((rc = stream_wait(c.st, st))) return rc;  // main may overwrite dY after the copies
   const int ldc = pad32(n_out);
   const int tiles = ceil_div(m_in, kTileM) * ceil_div(ldc, 128);
   const int k_total = kp / 32;
@@ -1528,6 +1578,8 @@ extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_para
   const float* P = d_params;
   float* G = d_grad;
   const int nt = (int)n_tok, nb = (int)n_batch;
+  g_colsum_part = b.colpart;
+  if ((rc = side_init())) return rc;
   TPCB_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(float) * (size_t)M.total, st));
   loss_kernel<<<1, 1024, 0, st>>>(f.pred, d_y, f.idx, nb, loss->mode, loss->lambda_hybrid,
                                   loss->offset, n_norm, b.dpred, d_loss);
@@ -1673,5 +1725,5 @@ extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_para
                   one(M.inW, M.d), G)))
     return rc;
   if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(M.inb, M.d), G, st))) return rc;
-  return TPCB_OK;
+  return stream_wait(st, g_side.s);  // join: every weight gradient is in d_grad
 }

@@ -40,8 +40,8 @@ class LargeTrainer:
                  valid_latency: np.ndarray | None = None, normalizer=None, device="cuda",
                  comm: "engine.Comm | None" = None):
         from .costmodel import device_model
-        if config.alpha_cmd > 0:
-            raise UnsupportedConfig("CMD fine-tuning runs on the fused trainer only")
+        # pre-training only: no target set, so no CMD term (alpha_cmd applies
+        # to finetune, which runs on the fused trainer)
         if loss_struct.original_space:
             raise UnsupportedConfig("the large path trains with transformed-space losses")
         self.lib = _lib.load()

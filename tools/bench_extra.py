@@ -187,6 +187,44 @@ def full():
     return out
 
 
+def fulltrain(n_steps=40):
+    """full_reference_config training samples/s (bs 600, the reference's
+    batch; C2 data) through the large path: forward + loss + backward +
+    Adam + weight-image rebuild per step (the paper's V100 figure for this
+    config is 14,241 samples/s)."""
+    from paper_2311_09690_b200.large_training import LargeTrainer
+    from paper_2311_09690_b200.training import plan_epoch
+    cfg = pb.full_reference_config()
+    data = synth.generate(65536, seed=0)
+    norm = fit_boxcox(data.latency)
+    loss = engine.loss_struct("hybrid", cfg.lambda_hybrid, norm.loss_offset)
+    tr = LargeTrainer(cfg, pb.init_params(cfg).tensors, rag(data), norm.encode(data.latency), loss)
+    flat, steps = plan_epoch(np.random.default_rng(0), tr.n_leaf, cfg.batch_size)
+    warm = steps[:3]
+    tr.run_epoch(cfg.lr, flat, warm)
+    torch.cuda.synchronize()
+    sel = steps[3:3 + n_steps]
+    n_samples = int(sel[:, 1].sum())
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    a.record()
+    tr.run_epoch(cfg.lr, flat, sel)
+    b.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    t = a.elapsed_time(b) / 1e3
+    losses = tr.losses[:len(sel)].cpu().numpy()
+    fl = 3 * 281.0e6  # ≈ 3 × forward MFLOP/sample at the synthetic histogram
+    return {"metric": "full_reference_config training samples/s (bs 600, 1 GPU)",
+            "value": n_samples / t, "unit": "samples/s", "steps": len(sel),
+            "ms_per_step": t / len(sel) * 1e3, "wall_samples_per_s": n_samples / wall,
+            "model_tflops": n_samples * fl / t / 1e12, "loss_first_last": [float(losses[0]),
+                                                                          float(losses[-1])],
+            "paper_v100_samples_per_s": 14241,
+            "dtype": "3xTF32 tcgen05 GEMMs, fp32 params/Adam"}
+
+
 def c4dp():
     import os
     import torch.distributed as dist
@@ -216,9 +254,10 @@ def c4dp():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["c3", "c4", "c4tc", "c5", "c5bf16", "full", "c4dp"]
+    which = sys.argv[1:] or ["c3", "c4", "c4tc", "c5", "c5bf16", "full", "fulltrain", "c4dp"]
     for w in which:
         r = {"c3": c3, "c4": c4, "c4tc": lambda: c4("tc"), "c5": c5,
-             "c5bf16": lambda: c5("bf16"), "full": full, "c4dp": c4dp}[w]()
+             "c5bf16": lambda: c5("bf16"), "full": full, "fulltrain": fulltrain,
+             "c4dp": c4dp}[w]()
         for line in (r if isinstance(r, list) else [r]):
             print(json.dumps(line), flush=True)
