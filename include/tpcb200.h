@@ -201,6 +201,14 @@ int tpcb_large_loss_backward(const tpcb_model* m, const float* d_params, const v
                              const int32_t* d_tok_off, int64_t n_batch, const tpcb_loss* loss, double n_norm, void* d_ws,
                              size_t ws_bytes, float* d_grad, double* d_loss, int32_t* d_status,
                              void* stream);
+/* debug: k-slab width of the large-path GEMM (16: 64-B swizzle, deeper
+ * pipeline — default; 32: 128-B swizzle) */
+void tpcb_debug_gemm_bk(int32_t bk);
+/* debug: 1 enables 2x2 / 2x1 / 1x2 TMA-multicast clusters for that GEMM
+ * (default off: measured no gain, the per-SM shared-memory fill rate binds) */
+void tpcb_debug_gemm_cluster(int32_t on);
+/* debug: 1 = the GEMM streams its operands but skips the MMAs (probe) */
+void tpcb_debug_gemm_mode(int32_t mode);
 /* the GEMM alone: C[M,N] = A[M,K] B[N,K]^T, fp32 row-major in/out (3xTF32) */
 size_t tpcb_gemm3_ws(int64_t M, int32_t N, int32_t K);
 int tpcb_gemm3(const float* d_a, const float* d_b, int64_t M, int32_t N, int32_t K, float* d_c,

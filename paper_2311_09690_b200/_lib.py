@@ -89,6 +89,9 @@ SIGNATURES = {
     "tpcb_large_train_ws": (i32, [vp, i64, i64, C.POINTER(sz)]),
     "tpcb_large_loss_backward": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64,
                                        C.POINTER(LossCfg), f64, vp, sz, vp, vp, vp, vp]),
+    "tpcb_debug_gemm_bk": (None, [i32]),
+    "tpcb_debug_gemm_cluster": (None, [i32]),
+    "tpcb_debug_gemm_mode": (None, [i32]),
     "tpcb_gemm3_ws": (sz, [i64, i32, i32]),
     "tpcb_gemm3": (i32, [vp, vp, i64, i32, i32, vp, i32, vp, sz, vp]),
     "tpcb_gemm3_presplit": (i32, [vp, vp, vp, vp, i64, i32, i32, vp, i32, vp]),

@@ -43,13 +43,16 @@ __device__ __forceinline__ float tf32_hi(float v) {
   return __uint_as_float(r);
 }
 
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {  // K-major, SW128
+// K-major operand descriptor: BK = 32 fp32 per row → 128-byte swizzle (8-row
+// atoms of 1 KB), BK = 16 → 64-byte swizzle (8-row atoms of 512 B)
+template <int BK = 32>
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
   d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)((8 * BK * 4) >> 4) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)(BK == 32 ? 2 : 4) << 61;
   return d;
 }
 
@@ -101,25 +104,53 @@ struct Epi {
   const float* mask = nullptr;  // ReLU backward: keep x where mask[row, col] > 0
   int ldm = 0;
   int64_t split_stride = 0;     // split-K: split z writes c + z * split_stride
+  int dbg = 0;                  // probe: 1 = skip the MMAs (TMA stream only)
 };
 
 constexpr int kTileM = 128;
-constexpr int kSlabA = kTileM * 128;  // one 128-row × 32-float slab (16 KB)
-
-template <int NT>
+// BK fp32 columns per k-slab (32: 128-B swizzle, 16: 64-B swizzle and twice
+// the stages in the same shared memory — deeper TMA prefetch)
+template <int NT, int BK = 32>
 struct GemmCfg {
-  static constexpr int kStages = NT == 256 ? 2 : 3;
-  static constexpr int kSlabB = NT * 128;
+  static constexpr int kSlabA = kTileM * BK * 4;
+  static constexpr int kSlabB = NT * BK * 4;
   static constexpr int kStage = 2 * kSlabA + 2 * kSlabB;
+  static constexpr int kStages = (192 * 1024) / kStage < 8 ? (192 * 1024) / kStage : 8;
   static constexpr int kSmem = kStages * kStage + 1024;
 };
 
-template <int NT>
+// cluster helpers (CN × CM CTAs: A tiles shared along N, B tiles along M)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const void* tmap, int c0, int c1,
+                                               uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask));
+}
+
+template <int NT, int BK, int CN, int CM>
 __global__ void __launch_bounds__(192, 1)
     gemm3_kernel(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
                  const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
                  int kc, int k_total, Epi e) {
-  using Cfg = GemmCfg<NT>;
+  using Cfg = GemmCfg<NT, BK>;
+  constexpr int kSlabA = Cfg::kSlabA;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -131,10 +162,11 @@ __global__ void __launch_bounds__(192, 1)
   const int k0 = blockIdx.z * kc;
   const int k_iters = min(kc, k_total - k0);  // >= 1 (host picks the splits)
 
+  constexpr int CS = CN * CM;  // cluster size
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CS);  // every cluster CTA's MMAs must release the slot
     }
     mbar_init(&done, 1);
     mbar_fence_init();
@@ -147,8 +179,15 @@ __global__ void __launch_bounds__(192, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (CS > 1) cluster_sync_all();  // peers' barriers initialised
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
+  // cluster coordinates: x along N (shares the A tile), y along M (shares B)
+  const uint32_t crank = CS > 1 ? cluster_rank() : 0;
+  const int cx = (int)(crank % CN), cy = (int)(crank / CN);
+  uint16_t mask_a = 0, mask_b = 0;  // CTAs with my M tile / my N tile
+  for (int x = 0; x < CN; ++x) mask_a |= (uint16_t)(1u << (x + cy * CN));
+  for (int y = 0; y < CM; ++y) mask_b |= (uint16_t)(1u << (cx + y * CN));
 
   if (warp == 4 && lane == 0) {  // TMA producer
     tma_prefetch_desc(&ta_hi);
@@ -160,11 +199,25 @@ __global__ void __launch_bounds__(192, 1)
       if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
       uint8_t* st = smem + s * Cfg::kStage;
       mbar_arrive_expect_tx(&full[s], Cfg::kStage);
-      const int kx = (k0 + it) * 32;
-      tma_load_2d(st, &ta_hi, kx, m0, &full[s]);
-      tma_load_2d(st + kSlabA, &ta_lo, kx, m0, &full[s]);
-      tma_load_2d(st + 2 * kSlabA, &tb_hi, kx, n0, &full[s]);
-      tma_load_2d(st + 2 * kSlabA + Cfg::kSlabB, &tb_lo, kx, n0, &full[s]);
+      const int kx = (k0 + it) * BK;
+      if constexpr (CN == 1) {
+        tma_load_2d(st, &ta_hi, kx, m0, &full[s]);
+        tma_load_2d(st + kSlabA, &ta_lo, kx, m0, &full[s]);
+      } else {  // my 1/CN share of the A rows, to every CTA of my M tile
+        constexpr int rows = kTileM / CN, bytes = rows * BK * 4;
+        tma_load_2d_mc(st + cx * bytes, &ta_hi, kx, m0 + cx * rows, &full[s], mask_a);
+        tma_load_2d_mc(st + kSlabA + cx * bytes, &ta_lo, kx, m0 + cx * rows, &full[s], mask_a);
+      }
+      if constexpr (CM == 1) {
+        tma_load_2d(st + 2 * kSlabA, &tb_hi, kx, n0, &full[s]);
+        tma_load_2d(st + 2 * kSlabA + Cfg::kSlabB, &tb_lo, kx, n0, &full[s]);
+      } else {  // my 1/CM share of the B rows, to every CTA of my N tile
+        constexpr int rows = NT / CM, bytes = rows * BK * 4;
+        tma_load_2d_mc(st + 2 * kSlabA + cy * bytes, &tb_hi, kx, n0 + cy * rows, &full[s],
+                       mask_b);
+        tma_load_2d_mc(st + 2 * kSlabA + Cfg::kSlabB + cy * bytes, &tb_lo, kx, n0 + cy * rows,
+                       &full[s], mask_b);
+      }
     }
   } else if (warp == 5 && lane == 0) {  // MMA issuer
     constexpr uint32_t id = idesc_tf32(kTileM, NT);
@@ -175,17 +228,21 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t a_hi = smem_u32(smem + s * Cfg::kStage);
       const uint32_t a_lo = a_hi + kSlabA, b_hi = a_hi + 2 * kSlabA, b_lo = b_hi + Cfg::kSlabB;
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < BK / 8; ++kk) {
+        if (e.dbg == 1) break;
         const uint32_t o = kk * 32;
         // the two correction products accumulate in their own TMEM tile
         // (columns NT..2NT): the main accumulator then takes K/8 rounding
         // steps instead of 3K/8 (the tensor core's fp32 accumulation
         // truncates, so its error grows with the step count)
-        mma_tf32(tmem, sdesc(a_hi + o), sdesc(b_hi + o), id, (it | kk) != 0);
-        mma_tf32(tmem + NT, sdesc(a_lo + o), sdesc(b_hi + o), id, (it | kk) != 0);
-        mma_tf32(tmem + NT, sdesc(a_hi + o), sdesc(b_lo + o), id, 1);
+        mma_tf32(tmem, sdesc<BK>(a_hi + o), sdesc<BK>(b_hi + o), id, (it | kk) != 0);
+        mma_tf32(tmem + NT, sdesc<BK>(a_lo + o), sdesc<BK>(b_hi + o), id, (it | kk) != 0);
+        mma_tf32(tmem + NT, sdesc<BK>(a_hi + o), sdesc<BK>(b_lo + o), id, 1);
       }
-      mma_commit(&empty[s]);
+      if constexpr (CS > 1)
+        mma_commit_mc(&empty[s], (uint16_t)((1u << CS) - 1));
+      else
+        mma_commit(&empty[s]);
     }
     mma_commit(&done);
   } else if (warp < 4) {  // epilogue: thread = TMEM lane = output row
@@ -243,6 +300,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if constexpr (CS > 1) cluster_sync_all();  // no peer still writes into this CTA
   if (warp == 4)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(2 * NT));
@@ -503,16 +561,16 @@ int get_encoder(EncodeFn* out) {
 // fp32 [outer rows][inner cols] with row stride `stride` floats; boxes of
 // 32 columns × box_rows rows, 128-byte swizzle; out-of-range reads are zero
 int tmap_2d(CUtensorMap* m, const float* base, int64_t inner, int64_t outer, int64_t stride,
-            int box_rows) {
+            int box_rows, int box_cols = 32) {
   EncodeFn enc;
   if (int st = get_encoder(&enc)) return st;
   const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
   const cuuint64_t strides[1] = {(cuuint64_t)stride * 4};
-  const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_last_error("cuTensorMapEncodeTiled (large)", cudaErrorInvalidValue);
@@ -528,31 +586,76 @@ struct Operand {
   int64_t rows, k_ext, ld;
 };
 
-template <int NT>
-int launch_gemm_nt(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st,
-                   int splits = 1) {
+int g_gemm_bk = 16;  // k-slab width (tpcb_debug_gemm_bk)
+
+int g_gemm_cluster = 0;  // allow 2x2 / 2x1 / 1x2 clusters (tpcb_debug_gemm_cluster)
+int g_gemm_dbg = 0;      // probe mode (tpcb_debug_gemm_mode)
+
+template <int NT, int BK, int CN, int CM>
+int launch_gemm_cl(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st,
+                   int splits, int* splits_used) {
+  using Cfg = GemmCfg<NT, BK>;
   CUtensorMap ta_hi, ta_lo, tb_hi, tb_lo;
-  int rc = tmap_2d(&ta_hi, A.hi, A.k_ext, A.rows, A.ld, kTileM);
-  if (!rc) rc = tmap_2d(&ta_lo, A.lo, A.k_ext, A.rows, A.ld, kTileM);
-  if (!rc) rc = tmap_2d(&tb_hi, B.hi, B.k_ext, B.rows, B.ld, NT);
-  if (!rc) rc = tmap_2d(&tb_lo, B.lo, B.k_ext, B.rows, B.ld, NT);
+  int rc = tmap_2d(&ta_hi, A.hi, A.k_ext, A.rows, A.ld, kTileM / CN, BK);
+  if (!rc) rc = tmap_2d(&ta_lo, A.lo, A.k_ext, A.rows, A.ld, kTileM / CN, BK);
+  if (!rc) rc = tmap_2d(&tb_hi, B.hi, B.k_ext, B.rows, B.ld, NT / CM, BK);
+  if (!rc) rc = tmap_2d(&tb_lo, B.lo, B.k_ext, B.rows, B.ld, NT / CM, BK);
   if (rc) return rc;
   static bool attr = false;
   if (!attr) {
-    TPCB_CUDA_CHECK(cudaFuncSetAttribute(gemm3_kernel<NT>,
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(gemm3_kernel<NT, BK, CN, CM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         GemmCfg<NT>::kSmem));
+                                         Cfg::kSmem));
+    if (CN * CM > 1)
+      TPCB_CUDA_CHECK(cudaFuncSetAttribute(gemm3_kernel<NT, BK, CN, CM>,
+                                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
-  const int k_total = (int)(A.k_ext / 32);
+  const int k_total = (int)(A.k_ext / BK);
   const int kc = ceil_div(k_total, splits);
   splits = ceil_div(k_total, kc);  // every split gets >= 1 slab
-  const dim3 grid((unsigned)ceil_div(e.ldc, NT), (unsigned)ceil_div(e.M, kTileM),
-                  (unsigned)splits);
-  gemm3_kernel<NT><<<grid, 192, GemmCfg<NT>::kSmem, st>>>(ta_hi, ta_lo, tb_hi, tb_lo, kc,
-                                                          k_total, e);
+  if (splits_used) *splits_used = splits;
+  const int gx = ceil_div(ceil_div(e.ldc, NT), CN) * CN;
+  const int gy = ceil_div(ceil_div(e.M, kTileM), CM) * CM;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)gx, (unsigned)gy, (unsigned)splits);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CN;
+  at[0].val.clusterDim.y = CM;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  Epi ee = e;
+  ee.dbg = g_gemm_dbg;
+  TPCB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm3_kernel<NT, BK, CN, CM>, ta_hi, ta_lo, tb_hi,
+                                     tb_lo, kc, k_total, ee));
   TPCB_LAUNCH_CHECK("gemm3");
   return TPCB_OK;
+}
+
+// cluster shape: share a tile only along a dimension with an even tile count
+// (no padded CTAs)
+template <int NT, int BK>
+int launch_gemm_bk(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st,
+                   int splits, int* splits_used) {
+  const int tn = ceil_div(e.ldc, NT), tm = ceil_div(e.M, kTileM);
+  const bool cn = g_gemm_cluster && tn % 2 == 0, cm = g_gemm_cluster && tm % 2 == 0;
+  if (cn && cm) return launch_gemm_cl<NT, BK, 2, 2>(A, B, e, st, splits, splits_used);
+  if (cm) return launch_gemm_cl<NT, BK, 1, 2>(A, B, e, st, splits, splits_used);
+  if (cn) return launch_gemm_cl<NT, BK, 2, 1>(A, B, e, st, splits, splits_used);
+  return launch_gemm_cl<NT, BK, 1, 1>(A, B, e, st, splits, splits_used);
+}
+
+// splits count k-slabs of 32 columns (callers' unit), whatever the slab width
+template <int NT>
+int launch_gemm_nt(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st,
+                   int splits = 1, int* splits_used = nullptr) {
+  if (g_gemm_bk == 16) return launch_gemm_bk<NT, 16>(A, B, e, st, splits, splits_used);
+  return launch_gemm_bk<NT, 32>(A, B, e, st, splits, splits_used);
 }
 
 int launch_gemm(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st) {
@@ -1501,13 +1604,11 @@ int wgrad(const Ctx& c, Bwd& b, const float* x_hi, const float* x_lo, int ld_x, 
   const int tiles = ceil_div(m_in, kTileM) * ceil_div(ldc, 128);
   const int k_total = kp / 32;
   int splits = max(1, min(min(2 * kNumSMs / max(tiles, 1), k_total / 4), 8));
-  const int kc = ceil_div(k_total, splits);
-  splits = ceil_div(k_total, kc);
   if ((size_t)splits * m_in * ldc > b.part_floats) return TPCB_ERR_VALIDATION;
   Epi e{m_in, n_out, ldc, nullptr, 0, nullptr, nullptr, 0, b.part, nullptr, nullptr};
   e.split_stride = (int64_t)m_in * ldc;
   Operand A{b.xt_hi, b.xt_lo, m_in, kp, kp}, B{b.yt_hi, b.yt_lo, n_out, kp, kp};
-  if ((rc = launch_gemm_nt<128>(A, B, e, st, splits))) return rc;
+  if ((rc = launch_gemm_nt<128>(A, B, e, st, splits, &splits))) return rc;
   const int64_t total = (int64_t)m_in * n_out;
   reduce_grad_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, kNumSMs * 8), 256, 0, st>>>(
       b.part, splits, e.split_stride, m_in, n_out, ldc, seg, segp, dst, grad);
@@ -1727,3 +1828,8 @@ extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_para
   if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(M.inb, M.d), G, st))) return rc;
   return stream_wait(st, g_side.s);  // join: every weight gradient is in d_grad
 }
+
+extern "C" void tpcb_debug_gemm_bk(int32_t bk) { tpcb::g_gemm_bk = bk == 32 ? 32 : 16; }
+
+extern "C" void tpcb_debug_gemm_cluster(int32_t on) { tpcb::g_gemm_cluster = on ? 1 : 0; }
+extern "C" void tpcb_debug_gemm_mode(int32_t mode) { tpcb::g_gemm_dbg = mode; }
