@@ -116,6 +116,26 @@ int tpcb_featurize_pack(const void* d_vectors, int32_t vec_is_f64, const int32_t
 int tpcb_positional_encoding(const int32_t* d_ordering, int64_t n, const double* pe_denom,
                              double* d_out, void* stream);
 
+/* ---- K0: compact-AST builder (features.build_compact_ast + compute_vector,
+ * features.py:155-245) ----------------------------------
+ * Input: a forest of n_prog programs as pre-order node arrays —
+ *   d_node_off [n_prog+1] i64, d_parent [N] i32 (program-local, -1 = root),
+ *   d_extent [N] i64 (loop extent >= 1, 0 = compute leaf), d_annot [N] u8
+ *   (bit 0 vectorize, 1 unroll, 2 parallel), d_leaf_off [n_prog+1] i64,
+ *   d_stats [NL, 9] i64 (ComputeStats fields in ir.py:53-64 order, leaves in
+ *   pre-order; host-validated: counts < 2^56, extents < 2^63).
+ * Output: d_vectors [NL, 24] f64 (compute_vector), d_ordering [NL] i32,
+ *   d_serialized [N + NL] i32 (program p at node_off[p] + leaf_off[p]).
+ * *d_first_overflow = smallest program index whose enclosing extent product
+ * exceeds 2^62 (the reference's OverflowError, features.py:165-168), or
+ * UINT64_MAX.  Integer math exact, int->float and entry 22 correctly rounded;
+ * log2 within 1 ulp. */
+int tpcb_build_compact(const int64_t* d_node_off, const int32_t* d_parent,
+                       const int64_t* d_extent, const uint8_t* d_annot, const int64_t* d_leaf_off,
+                       const int64_t* d_stats, int64_t n_prog, double* d_vectors,
+                       int32_t* d_ordering, int32_t* d_serialized,
+                       unsigned long long* d_first_overflow, void* stream);
+
 /* Box-Cox label normaliser (dataset.py:69-115) */
 typedef struct {
   double lambda_bc, shift, t_mean, t_std;

@@ -7,9 +7,13 @@ or a CUDA device the compute entry points raise.
 """
 
 from .errors import TpcostError
-from .features import (CompactAst, CompactBatch, DeviceSpec, EncodedInput, device_vector,
-                       encode_input, positional_encoding)
-from .dataset import BoxCoxNormalizer, Dataset, Sample, fit_boxcox, split_dataset
+from .features import (CompactAst, CompactBatch, DeviceSpec, EncodedInput, build_compact_ast,
+                       device_vector, encode_input, positional_encoding)
+from .ir import AstNode, ComputeStats, LoopInfo, ProgramAst, count_leaves, make_program
+from .forest import FlatForest, build_compact, predict_forest
+from .dataset import (BoxCoxNormalizer, Dataset, Sample, fit_boxcox, load_batch_bin, load_dataset,
+                      load_dataset_bin, save_dataset, save_dataset_bin, split_dataset)
+from .replayer import dedup_predict
 from .costmodel import (CostModelConfig, CostModelParams, LatentBatch, LossSpec, Predictor,
                         TrainResult, backward, cmd, cmd_between, desk_config, encode_dataset,
                         finetune, forward, full_reference_config, init_params, load_checkpoint,

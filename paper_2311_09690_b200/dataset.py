@@ -152,3 +152,126 @@ def split_dataset(ds: Dataset, ratios=(8, 1, 1), seed: int = 0,
         splits[rest[idx].id] = ("train" if pos < n_train else
                                 "valid" if pos < n_train + n_valid else "test")
     return Dataset(samples=ds.samples, splits=splits)
+
+
+# ---------------------------------------------------------------------------
+# persistence: the reference's JSONL (dataset.py:421-485) and a binary ragged
+# SoA that loads straight into a CompactBatch
+# ---------------------------------------------------------------------------
+
+def _fmt(x: float) -> str:
+    if not math.isfinite(x):
+        raise ValidationError("cannot serialize non-finite float")
+    return format(float(x), ".17g")
+
+
+def sample_to_line(s: Sample) -> str:
+    """One JSONL record, byte-identical to the reference's (dataset.py:427-448)."""
+    import json
+    c = s.compact
+    vectors = "[" + ",".join("[" + ",".join(_fmt(v) for v in row) + "]"
+                             for row in np.asarray(c.leaf_vectors)) + "]"
+    return ("{" f"\"id\":{json.dumps(s.id)},\"task_id\":{json.dumps(s.task_id)},"
+            f"\"model_id\":{json.dumps(s.model_id)},\"device_id\":{json.dumps(s.device_id)},"
+            f"\"n_leaf\":{c.n_leaf},\"vectors\":{vectors},"
+            f"\"ordering\":[{','.join(str(int(i)) for i in c.ordering)}],"
+            f"\"serialized\":[{','.join(str(int(i)) for i in c.serialized)}],"
+            f"\"latency_s\":{_fmt(s.latency_s)}" "}")
+
+
+def save_dataset(ds: Dataset, path) -> None:
+    with open(path, "w", encoding="utf-8") as f:
+        for s in ds.samples:
+            f.write(sample_to_line(s))
+            f.write("\n")
+
+
+def load_dataset(path) -> Dataset:
+    """Reference JSONL reader (dataset.py:451-485), same validation."""
+    import json
+    from .features import CompactAst
+    samples = []
+    with open(path, "r", encoding="utf-8") as f:
+        for lineno, line in enumerate(f, start=1):
+            line = line.strip()
+            if not line:
+                continue
+            try:
+                d = json.loads(line)
+            except json.JSONDecodeError as e:
+                raise ValidationError(f"{path}:{lineno}: bad JSON: {e}") from e
+            vec = np.asarray(d["vectors"], dtype=np.float64)
+            if vec.ndim != 2:
+                raise ValidationError("vectors must be a 2-D array")
+            c = CompactAst(leaf_vectors=vec, ordering=tuple(int(i) for i in d["ordering"]),
+                           serialized=tuple(int(i) for i in d["serialized"]),
+                           n_leaf=int(d["n_leaf"]))
+            if c.n_leaf != vec.shape[0]:
+                raise ValidationError("n_leaf does not match vector count")
+            samples.append(Sample(id=str(d["id"]), task_id=str(d["task_id"]),
+                                  model_id=str(d["model_id"]), device_id=str(d["device_id"]),
+                                  compact=c, latency_s=float(d["latency_s"])))
+    return Dataset(samples=samples)
+
+
+_SPLIT_CODE = {None: 0, "train": 1, "valid": 2, "test": 3, "holdout": 4}
+_SPLIT_NAME = {v: k for k, v in _SPLIT_CODE.items()}
+
+
+def save_dataset_bin(ds: Dataset, path) -> None:
+    """Ragged SoA .npz: vectors (T,24) f64, ordering (T,) i32, serialized
+    (S,) i32, n_leaf / n_ser (B,), latency_s (B,) f64, string ids, split codes.
+    Bit-exact round trip of everything the JSONL holds (and the splits)."""
+    cs = [s.compact for s in ds.samples]
+    np.savez(path,
+             vectors=(np.concatenate([np.asarray(c.leaf_vectors, np.float64) for c in cs])
+                      if cs else np.zeros((0, 24))),
+             ordering=np.array([i for c in cs for i in c.ordering], dtype=np.int32),
+             serialized=np.array([i for c in cs for i in c.serialized], dtype=np.int32),
+             n_leaf=np.array([c.n_leaf for c in cs], dtype=np.int64),
+             n_ser=np.array([len(c.serialized) for c in cs], dtype=np.int64),
+             latency_s=np.array([s.latency_s for s in ds.samples], dtype=np.float64),
+             id=np.array([s.id for s in ds.samples], dtype=np.str_),
+             task_id=np.array([s.task_id for s in ds.samples], dtype=np.str_),
+             model_id=np.array([s.model_id for s in ds.samples], dtype=np.str_),
+             device_id=np.array([s.device_id for s in ds.samples], dtype=np.str_),
+             split=np.array([_SPLIT_CODE[ds.splits.get(s.id)] for s in ds.samples],
+                            dtype=np.int8))
+
+
+def load_batch_bin(path, devices: dict):
+    """The binary file straight into the GPU path's input: (CompactBatch,
+    latency_s, split codes, ids) with no per-sample Python objects."""
+    from .features import CompactBatch
+    with np.load(path, allow_pickle=False) as z:
+        names = sorted(devices)
+        dev_ix = {n: i for i, n in enumerate(names)}
+        try:
+            di = np.array([dev_ix[d] for d in z["device_id"]], dtype=np.int32)
+        except KeyError as e:
+            raise ValidationError(f"unknown device {e.args[0]!r}") from None
+        batch = CompactBatch(z["vectors"], z["ordering"], z["n_leaf"], di,
+                             [devices[n] for n in names])
+        return batch, z["latency_s"], z["split"], z["id"]
+
+
+def load_dataset_bin(path) -> Dataset:
+    from .features import CompactAst
+    with np.load(path, allow_pickle=False) as z:
+        vec, order, ser = z["vectors"], z["ordering"], z["serialized"]
+        lo = np.concatenate([[0], np.cumsum(z["n_leaf"])])
+        so = np.concatenate([[0], np.cumsum(z["n_ser"])])
+        samples, splits = [], {}
+        for i in range(z["n_leaf"].shape[0]):
+            c = CompactAst(leaf_vectors=vec[lo[i]:lo[i + 1]].copy(),
+                           ordering=tuple(int(v) for v in order[lo[i]:lo[i + 1]]),
+                           serialized=tuple(int(v) for v in ser[so[i]:so[i + 1]]),
+                           n_leaf=int(z["n_leaf"][i]))
+            s = Sample(id=str(z["id"][i]), task_id=str(z["task_id"][i]),
+                       model_id=str(z["model_id"][i]), device_id=str(z["device_id"][i]),
+                       compact=c, latency_s=float(z["latency_s"][i]))
+            samples.append(s)
+            code = int(z["split"][i])
+            if code:
+                splits[s.id] = _SPLIT_NAME[code]
+    return Dataset(samples=samples, splits=splits)

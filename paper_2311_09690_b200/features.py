@@ -4,8 +4,8 @@ API of the reference module `tpcost.features` (features.py:60-279) on the
 hot path: `CompactAst`, `DeviceSpec`, `EncodedInput`, `positional_encoding`,
 `device_vector`, `encode_input` — plus `CompactBatch`, the bulk SoA batch the
 GPU path is fed with (one host→device copy per batch instead of per-object
-Python lists).  The tree walk that *builds* compact ASTs (build_compact_ast,
-compute_vector) is outside the hot path and not provided here.
+Python lists) — and `build_compact_ast`, the tree → compact-AST step, run on
+the GPU by K0 over a flattened forest (forest.py, csrc/compact.cu).
 """
 
 from __future__ import annotations
@@ -108,6 +108,22 @@ def encode_input(compact: CompactAst, device: DeviceSpec,
     """leaf vectors + PE, with the device features attached (features.py:274-279)."""
     matrix = np.asarray(compact.leaf_vectors, dtype=np.float64) + positional_encoding(compact, theta)
     return EncodedInput(matrix=matrix, device_vector=device_vector(device))
+
+
+def build_compact_ast(ast, max_leaves: int | None = None) -> CompactAst:
+    """Serialize a program tree pre-order (marker after each leaf) and build
+    its leaf computation vectors (features.py:209-245) — one program through
+    the device builder K0; `forest.build_compact` does many per launch.
+    Raises LeafCountExceeded above `max_leaves`, OverflowError when an
+    enclosing extent product exceeds 2^62, like the reference."""
+    from .forest import FlatForest, build_compact
+    if max_leaves is not None and ast.n_leaf > max_leaves:
+        raise LeafCountExceeded(f"{ast.n_leaf} leaves exceeds maximum {max_leaves}")
+    forest = FlatForest.from_programs([ast])
+    if int(forest.n_leaf[0]) != ast.n_leaf:
+        raise ValidationError(
+            f"leaf count mismatch: tree has {int(forest.n_leaf[0])}, header says {ast.n_leaf}")
+    return build_compact(forest).to_host()[0]
 
 
 # ---------------------------------------------------------------------------

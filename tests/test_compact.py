@@ -1,0 +1,218 @@
+"""K0 compact-AST builder (features.build_compact_ast, features.py:155-245):
+oracle vs the reference's golden output (CPU), flat-forest validation and the
+binary format (CPU), and the CUDA builder vs golden + oracle (GPU)."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import compact as oc
+
+INT_COLS = [0, 4, 5, 6, 20, 21]  # integer-valued entries: exact on every path
+
+
+def golden_forest():
+    from paper_2311_09690_b200.forest import FlatForest
+    z = load_golden("compact")
+    f = FlatForest(node_off=z["node_off"], parent=z["parent"], extent=z["extent"],
+                   annot=z["annot"], leaf_off=z["leaf_off"], stats=z["stats"])
+    return f, z
+
+
+def split_golden(z):
+    f_lo, n_lo = z["leaf_off"], z["node_off"]
+    ser_lo = n_lo + f_lo
+    out = []
+    for p in range(len(n_lo) - 1):
+        out.append((z["vectors"][f_lo[p]:f_lo[p + 1]],
+                    tuple(z["ordering"][f_lo[p]:f_lo[p + 1]]),
+                    tuple(z["serialized"][ser_lo[p]:ser_lo[p + 1]])))
+    return out
+
+
+def test_oracle_matches_reference_golden_bit_exact():
+    f, z = golden_forest()
+    got = oc.build_forest(f.node_off, f.parent, f.extent, f.annot, f.leaf_off, f.stats)
+    want = split_golden(z)
+    assert len(got) == len(want) == 605
+    for (gv, go, gs), (wv, wo, ws) in zip(got, want):
+        assert go == wo and gs == ws
+        assert np.array_equal(gv, wv)
+
+
+def test_reference_known_answers():
+    """test_features.py:28-44: serialized (0,1,2,-1,3,-1), ordering (2,4);
+    single leaf (0,-1) / (0,)."""
+    _, z = golden_forest()
+    g = split_golden(z)
+    assert g[0][2] == (0, 1, 2, -1, 3, -1) and g[0][1] == (2, 4)
+    assert g[1][2] == (0, -1) and g[1][1] == (0,)
+
+
+def test_oracle_overflow_and_compute_vector_examples():
+    """test_features.py:100-132 restated on the oracle."""
+    import math
+    v = oc.leaf_vector([2, 0, 0, 0, 0, 16, 8, 0, 0], [(4, 0)], 0, 1)
+    assert v[0] == 1 and v[1] == math.log2(5) and v[15] == math.log2(1 + 16)
+    v0 = oc.leaf_vector([0] * 9, [], 1, 2)
+    want = np.zeros(24)
+    want[23] = 0.5
+    assert np.array_equal(v0, want)
+    with pytest.raises(OverflowError):
+        oc.leaf_vector([1] + [0] * 8, [(2 ** 32, 0), (2 ** 31, 0)], 0, 1)
+
+
+def test_forest_roundtrip_and_flatten_of_package_trees(tmp_path):
+    from paper_2311_09690_b200 import ir
+    from paper_2311_09690_b200.forest import FlatForest
+    st = ir.ComputeStats(fma_count=1)
+    prog = ir.make_program("q", ir.loop(ir.LoopInfo("i", 2), [
+        ir.loop(ir.LoopInfo("j", 3, frozenset({"vectorize"})), [ir.leaf("a", st)]),
+        ir.leaf("b", ir.ComputeStats(add_count=1))]))
+    f = FlatForest.from_programs([prog, prog])
+    f.validate()
+    assert f.parent.tolist() == [-1, 0, 1, 0] * 2
+    assert f.extent.tolist() == [2, 3, 0, 0] * 2 and f.annot.tolist() == [0, 1, 0, 0] * 2
+    got = oc.build_forest(f.node_off, f.parent, f.extent, f.annot, f.leaf_off, f.stats)
+    assert got[0][2] == (0, 1, 2, -1, 3, -1) and got[0][1] == (2, 4)
+    f.save(tmp_path / "forest.npz")
+    g = FlatForest.load(tmp_path / "forest.npz")
+    for k in ("node_off", "parent", "extent", "annot", "leaf_off", "stats"):
+        assert np.array_equal(getattr(f, k), getattr(g, k))
+    assert g.names == ["q", "q"]
+
+
+@pytest.mark.parametrize("mutate,msg", [
+    (lambda f: f.parent.__setitem__(2, 2), "precede"),
+    (lambda f: f.parent.__setitem__(3, 2), "no children"),
+    (lambda f: f.extent.__setitem__(3, -1), "negative"),
+    (lambda f: f.annot.__setitem__(0, 9), "annotation"),
+    (lambda f: f.stats.__setitem__((0, 0), 0), "no ops"),
+    (lambda f: f.stats.__setitem__((0, 0), 2 ** 57), r"0\.\.2\^56"),
+])
+def test_forest_validation_rejects(mutate, msg):
+    from paper_2311_09690_b200 import ir
+    from paper_2311_09690_b200.errors import ValidationError
+    from paper_2311_09690_b200.forest import FlatForest
+    prog = ir.make_program("q", ir.loop(ir.LoopInfo("i", 2), [
+        ir.loop(ir.LoopInfo("j", 3), [ir.leaf("a", ir.ComputeStats(fma_count=1))]),
+        ir.leaf("b", ir.ComputeStats(add_count=1))]))
+    f = FlatForest.from_programs([prog])
+    mutate(f)
+    with pytest.raises(ValidationError, match=msg):
+        f.validate()
+
+
+def test_forest_validation_rejects_non_preorder():
+    """root(0) -> A(1) -> leaf(3); root -> leaf(2): node 3's parent (1) is not
+    on node 2's ancestor chain, so the arrays are not a pre-order."""
+    from paper_2311_09690_b200.errors import ValidationError
+    from paper_2311_09690_b200.forest import FlatForest
+    f = FlatForest(node_off=np.array([0, 4]), parent=np.array([-1, 0, 0, 1], np.int32),
+                   extent=np.array([2, 3, 0, 0]), annot=np.zeros(4, np.uint8),
+                   leaf_off=np.array([0, 2]), stats=np.ones((2, 9), np.int64))
+    with pytest.raises(ValidationError, match="pre-order"):
+        f.validate()
+
+
+# ---------------------------------------------------------------------------
+# GPU
+# ---------------------------------------------------------------------------
+
+def _ulps(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.abs(a - b) / np.maximum(np.spacing(np.abs(b)), np.finfo(np.float64).tiny)
+
+
+@pytest.mark.gpu
+def test_gpu_builder_matches_reference_golden():
+    from paper_2311_09690_b200.forest import build_compact
+    f, z = golden_forest()
+    dc = build_compact(f)
+    assert np.array_equal(dc.ordering.cpu().numpy(), z["ordering"])
+    assert np.array_equal(dc.serialized.cpu().numpy(), z["serialized"])
+    got = dc.vectors.cpu().numpy()
+    want = z["vectors"]
+    assert np.array_equal(got[:, INT_COLS], want[:, INT_COLS])
+    assert np.array_equal(got[:, 22:24], want[:, 22:24])  # correctly rounded quotients
+    # log2 entries: CUDA log2 is within 1 ulp of glibc's
+    assert _ulps(got, want).max() <= 2, _ulps(got, want).max()
+    assert np.mean(got == want) > 0.95
+
+
+@pytest.mark.gpu
+def test_gpu_builder_large_random_forest_vs_oracle(rng):
+    """The synthetic workload's tree shapes at scale (a root loop over per-leaf
+    chains) with random extents up to 2^16 (products up to 2^57, below the
+    2^62 guard) and counts up to 2^40 (flop totals up to 2^98: the 128-bit
+    products and the exact-quotient path of entry 22)."""
+    from paper_2311_09690_b200 import ir
+    from paper_2311_09690_b200.forest import FlatForest, build_compact
+    progs = []
+    for p in range(3000):
+        kids = []
+        for c in range(int(rng.integers(1, 7))):
+            node = ir.leaf(f"c{c}", ir.ComputeStats(*(int(x) for x in rng.integers(0, 2 ** 40, 9))))
+            for _ in range(int(rng.integers(0, 4))):
+                node = ir.loop(ir.LoopInfo("v", int(rng.integers(1, 2 ** 16)),
+                                           frozenset(a for a in ir.ANNOTATIONS if rng.random() < .3)),
+                               [node])
+            kids.append(node)
+        progs.append(ir.make_program(f"p{p}", ir.loop(ir.LoopInfo("r", int(rng.integers(1, 512))),
+                                                      kids)))
+    f = FlatForest.from_programs(progs)
+    want = oc.build_forest(f.node_off, f.parent, f.extent, f.annot, f.leaf_off, f.stats)
+    dc = build_compact(f)
+    hosts = dc.to_host()
+    wv = np.concatenate([w[0] for w in want])
+    gv = np.concatenate([h.leaf_vectors for h in hosts])
+    assert [h.ordering for h in hosts] == [w[1] for w in want]
+    assert [h.serialized for h in hosts] == [w[2] for w in want]
+    assert np.array_equal(gv[:, INT_COLS + [22, 23]], wv[:, INT_COLS + [22, 23]])
+    assert _ulps(gv, wv).max() <= 2
+
+
+@pytest.mark.gpu
+def test_gpu_builder_errors_follow_reference_order():
+    from paper_2311_09690_b200 import ir
+    from paper_2311_09690_b200.errors import LeafCountExceeded
+    from paper_2311_09690_b200.features import build_compact_ast
+    from paper_2311_09690_b200.forest import FlatForest, build_compact
+    st = ir.ComputeStats(fma_count=1)
+    big = ir.make_program("big", ir.loop(ir.LoopInfo("a", 2 ** 32),
+                                         [ir.loop(ir.LoopInfo("b", 2 ** 31), [ir.leaf("x", st)])]))
+    many = ir.make_program("many", ir.loop(ir.LoopInfo("i", 2), [ir.leaf(f"c{i}", st)
+                                                                 for i in range(9)]))
+    ok = ir.make_program("ok", ir.loop(ir.LoopInfo("i", 2 ** 31), [ir.loop(
+        ir.LoopInfo("j", 2 ** 31), [ir.leaf("x", st)])]))  # exactly 2^62: allowed
+    with pytest.raises(OverflowError):
+        build_compact_ast(big)
+    with pytest.raises(LeafCountExceeded):
+        build_compact_ast(many, max_leaves=8)
+    c = build_compact_ast(ok)
+    assert c.leaf_vectors[0, 1] == 62.0
+    with pytest.raises(LeafCountExceeded):  # program 0 fails first
+        build_compact(FlatForest.from_programs([many, big]), max_leaves=8)
+    with pytest.raises(OverflowError):
+        build_compact(FlatForest.from_programs([ok, big, many]), max_leaves=8)
+
+
+@pytest.mark.gpu
+def test_predict_forest_equals_forward_batch_on_reference_compacts(golden_model):
+    """Trees → K0 → K1 → forward equals the bulk predictor fed the
+    reference-built compact ASTs of the same programs (bit-identical: the
+    compact vectors agree to 2 ulp in fp64, the network runs in fp32)."""
+    import paper_2311_09690_b200 as pb
+    from paper_2311_09690_b200.features import CompactAst, CompactBatch
+    from paper_2311_09690_b200.forest import predict_forest
+    f, z = golden_forest()
+    params = pb.init_params(pb.desk_config(seed=0))
+    pred_forest = pb.Predictor(params)
+    dev = pb.DeviceSpec("b200", 1965, 180, 7700, 148, 80000, 126)
+    pf, _ = predict_forest(pred_forest, f, dev)
+    compacts = [CompactAst(leaf_vectors=v, ordering=o, serialized=s, n_leaf=len(o))
+                for v, o, s in split_golden(z)]
+    batch = CompactBatch.from_compacts(compacts, dev, dtype=np.float64)
+    pb_, _, _, _, _ = pred_forest.forward_batch(batch)
+    np.testing.assert_allclose(pf, pb_, rtol=1e-6, atol=1e-6)
