@@ -26,10 +26,13 @@
 // < 2^56 and extents to < 2^63 by the host validation), so the 2^62 overflow
 // guard of _log_extent_product (features.py:158-169) is exact, and every
 // int -> float conversion and the intensity quotient (entry 22, a Python
-// int/int true division) are correctly rounded like CPython's.  log2 is the
-// CUDA libdevice log2 (<= 1 ulp), the only non-bit-exact step.
+// int/int true division) are correctly rounded like CPython's.  log2 of
+// arguments below 4096 is the host libm's own value (a table); above, the
+// CUDA libdevice log2 (<= 1 ulp) is the only non-bit-exact step.
 
 #include <algorithm>
+#include <cmath>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -70,7 +73,17 @@ __device__ double div_u128(u128 a, u128 b) {
   return ldexp(__ull2double_rn(q), e - 55);
 }
 
-__device__ __forceinline__ double log2_1p_int(u128 v) { return log2(u128_to_double(v + 1)); }
+// log2(1 + v): small arguments (counts, extents, per-iteration bytes — 7 of
+// the 13 log2 entries on typical programs) come from a table the host fills
+// with its own libm log2, i.e. the very values CPython's math.log2 returns to
+// the reference; larger ones use the device log2 (<= 1 ulp).
+constexpr int kLog2Table = 4096;
+__device__ double g_log2_table[kLog2Table];
+
+__device__ __forceinline__ double log2_1p_int(u128 v) {
+  if (v < (u128)kLog2Table) return __ldg(&g_log2_table[(int)v]);
+  return log2(u128_to_double(v + 1));
+}
 
 constexpr u128 kProductLimit = ((u128)1) << 62;  // features.py:26
 
@@ -81,83 +94,241 @@ struct CompactOut {
   unsigned long long* first_bad;  // min program index that overflowed
 };
 
-__global__ void __launch_bounds__(256) build_compact_kernel(
+// Enclosing-loop aggregates of one leaf from its parent chain (innermost
+// first); Tree gives parent(i) / extent(i) / annot(i) in program-local ids.
+struct Chain {
+  int depth;
+  u128 prod, tprod[3];
+  int tcount[3];
+  int64_t inner, outer;
+  bool overflow;
+};
+
+template <class Tree>
+__device__ __forceinline__ Chain walk_chain(const Tree& t, int32_t leaf) {
+  Chain c;
+  c.depth = 0;
+  c.prod = 1;
+  c.inner = c.outer = 0;
+  c.overflow = false;
+  for (int q = 0; q < 3; ++q) { c.tprod[q] = 1; c.tcount[q] = 0; }
+  for (int32_t a = t.parent(leaf); a >= 0; a = t.parent(a)) {
+    const int64_t e = t.extent(a);
+    const unsigned bits = t.annot(a);
+    if (c.depth == 0) c.inner = e;
+    c.outer = e;
+    ++c.depth;
+    c.prod *= (u128)e;
+    if (c.prod > kProductLimit) { c.overflow = true; c.prod = kProductLimit; }
+    for (int q = 0; q < 3; ++q)
+      if (bits >> q & 1u) {
+        ++c.tcount[q];
+        c.tprod[q] *= (u128)e;
+        if (c.tprod[q] > kProductLimit) c.tprod[q] = kProductLimit;
+      }
+  }
+  return c;
+}
+
+// compute_vector (features.py:172-206) into v[0..23] (any address space)
+__device__ __forceinline__ void leaf_vector(const Chain& c, const int64_t* __restrict__ st,
+                                            int k, int n_leaf, double* v) {
+  const u128 iters = c.depth ? c.prod : (u128)1;
+  v[0] = (double)c.depth;
+  v[1] = c.depth ? log2_1p_int(c.prod) : 0.0;
+  v[2] = c.depth ? log2_1p_int((u128)c.inner) : 0.0;
+  v[3] = c.depth ? log2_1p_int((u128)c.outer) : 0.0;
+  for (int q = 0; q < 3; ++q) {
+    v[4 + q] = (double)c.tcount[q];
+    v[7 + q] = c.tcount[q] ? log2_1p_int(c.tprod[q]) : 0.0;
+  }
+  int64_t s[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) s[q] = st[q];
+  u128 per_iter = 2 * (u128)s[0];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    v[10 + q] = log2_1p_int((u128)s[q]);
+    if (q) per_iter += (u128)s[q];
+  }
+  const u128 tot_flops = per_iter * iters;
+  const u128 tot_read = (u128)s[5] * iters, tot_written = (u128)s[6] * iters;
+  v[15] = log2_1p_int(tot_flops);
+  v[16] = log2_1p_int((u128)s[5]);
+  v[17] = log2_1p_int((u128)s[6]);
+  v[18] = log2_1p_int(tot_read);
+  v[19] = log2_1p_int(tot_written);
+  v[20] = u128_to_double((u128)s[7]);
+  v[21] = u128_to_double((u128)s[8]);
+  v[22] = div_u128(tot_flops, tot_read + tot_written + 1);
+  v[23] = (double)k / (double)n_leaf;
+}
+
+struct GlobalTree {  // one program's arrays in global memory
+  const int32_t* par;
+  const int64_t* ext;
+  const uint8_t* ann;
+  __device__ int32_t parent(int32_t i) const { return par[i]; }
+  __device__ int64_t extent(int32_t i) const { return ext[i]; }
+  __device__ unsigned annot(int32_t i) const { return ann[i]; }
+};
+
+// Tile path (the default): a block owns kProgsPerBlock consecutive programs whose node
+// arrays (one contiguous range) are staged in shared memory with coalesced
+// loads; a block-wide scan of "is leaf" gives every node its serialized
+// position, then one thread per leaf walks its chain in shared memory and
+// writes its vector into a padded staging tile that the block streams out
+// with coalesced 8-byte stores (the vectors of a block are contiguous).
+constexpr int kProgsPerBlock = 64;
+constexpr int kThreads = 256;
+constexpr int kNodeCap = 2048;   // nodes staged per block
+constexpr int kVecPitch = 25;    // doubles per staged vector (bank spread)
+
+struct SmemTree {  // block-local ids; base = first node of the program
+  const int16_t* par;
+  const int64_t* ext;
+  const uint8_t* ann;
+  int base;
+  __device__ int32_t parent(int32_t i) const {
+    return par[base + i];
+  }
+  __device__ int64_t extent(int32_t i) const { return ext[base + i]; }
+  __device__ unsigned annot(int32_t i) const { return ann[base + i]; }
+};
+
+struct TileSmem {
+  int64_t ext[kNodeCap];
+  double vec[kThreads * kVecPitch];
+  int16_t par[kNodeCap];
+  int16_t leaf_node[kNodeCap];  // block-local node of block-local leaf g
+  int64_t node_off[kProgsPerBlock + 1], leaf_off[kProgsPerBlock + 1];
+  int warp_sum[kThreads / 32];
+  uint8_t ann[kNodeCap];
+};
+
+__device__ __forceinline__ int find_prog(const int64_t* off, int n, int64_t x) {
+  int lo = 0, hi = n;  // largest p with off[p] <= x
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (off[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// warp-per-program path for blocks whose programs exceed the node cap
+__device__ void program_warp(const int64_t* __restrict__ node_off,
+                             const int32_t* __restrict__ parent,
+                             const int64_t* __restrict__ extent,
+                             const uint8_t* __restrict__ annot,
+                             const int64_t* __restrict__ leaf_off,
+                             const int64_t* __restrict__ stats, int64_t p, const CompactOut& out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n0 = node_off[p], nn = node_off[p + 1] - n0;
+  const int64_t l0 = leaf_off[p];
+  const int n_leaf = (int)(leaf_off[p + 1] - l0);
+  const int64_t s0 = n0 + l0;
+  const GlobalTree tree{parent + n0, extent + n0, annot + n0};
+  int before = 0;
+  for (int64_t c = 0; c < nn; c += 32) {
+    const int64_t i = c + lane;
+    const bool valid = i < nn;
+    const bool is_leaf = valid && extent[n0 + i] == 0;
+    const unsigned ball = __ballot_sync(0xffffffffu, is_leaf);
+    const int k = before + __popc(ball & ((1u << lane) - 1u));
+    if (valid) {
+      out.serialized[s0 + i + k] = (int32_t)i;
+      if (is_leaf) out.serialized[s0 + i + k + 1] = -1;
+    }
+    if (is_leaf) {
+      out.ordering[l0 + k] = (int32_t)(i + k);
+      const Chain ch = walk_chain(tree, (int32_t)i);
+      if (ch.overflow) atomicMin(out.first_bad, (unsigned long long)p);
+      leaf_vector(ch, stats + (l0 + k) * 9, k, n_leaf, out.vectors + (l0 + k) * TPCB_FEAT);
+    }
+    before += __popc(ball);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) build_compact_kernel(
     const int64_t* __restrict__ node_off, const int32_t* __restrict__ parent,
     const int64_t* __restrict__ extent, const uint8_t* __restrict__ annot,
     const int64_t* __restrict__ leaf_off, const int64_t* __restrict__ stats, int64_t n_prog,
     CompactOut out) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < n_prog;
-       p += warps) {
-    const int64_t n0 = node_off[p], nn = node_off[p + 1] - n0;
-    const int64_t l0 = leaf_off[p];
-    const int n_leaf = (int)(leaf_off[p + 1] - l0);
-    const int64_t s0 = n0 + l0;
-    int before = 0;  // leaves in earlier chunks
-    for (int64_t c = 0; c < nn; c += 32) {
-      const int64_t i = c + lane;
-      const bool valid = i < nn;
-      const int64_t ext = valid ? extent[n0 + i] : 1;
-      const bool is_leaf = valid && ext == 0;
-      const unsigned ball = __ballot_sync(0xffffffffu, is_leaf);
-      const int k = before + __popc(ball & ((1u << lane) - 1u));  // leaf index
-      if (valid) {
-        const int64_t pos = i + k;  // node id + markers emitted before it
-        out.serialized[s0 + pos] = (int32_t)i;
-        if (is_leaf) out.serialized[s0 + pos + 1] = -1;  // MARKER
-      }
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t p0 = (int64_t)blockIdx.x * kProgsPerBlock;
+  const int np = (int)(n_prog - p0 < kProgsPerBlock ? n_prog - p0 : kProgsPerBlock);
+  if (t <= np) {
+    sm.node_off[t] = node_off[p0 + t];
+    sm.leaf_off[t] = leaf_off[p0 + t];
+  }
+  __syncthreads();
+  const int64_t gn0 = sm.node_off[0], gl0 = sm.leaf_off[0];
+  const int nodes = (int)(sm.node_off[np] - gn0);
+  const int leaves = (int)(sm.leaf_off[np] - gl0);
+  if (nodes > kNodeCap) {  // oversized programs: warp per program from global memory
+    for (int q = warp; q < np; q += kThreads / 32)
+      program_warp(node_off, parent, extent, annot, leaf_off, stats, p0 + q, out);
+    return;
+  }
+  // stage the node arrays (coalesced), parents as block-local indices
+  for (int j = t; j < nodes; j += kThreads) {
+    sm.ext[j] = extent[gn0 + j];
+    sm.ann[j] = annot[gn0 + j];
+  }
+  for (int j = t; j < nodes; j += kThreads) sm.par[j] = (int16_t)parent[gn0 + j];  // local ids
+  // block-wide exclusive scan of is_leaf, 256 nodes per round
+  int carry = 0;
+  for (int c = 0; c < nodes; c += kThreads) {
+    const int j = c + t;
+    const bool is_leaf = j < nodes && sm.ext[j] == 0;
+    const unsigned ball = __ballot_sync(0xffffffffu, is_leaf);
+    if (lane == 0) sm.warp_sum[warp] = __popc(ball);
+    __syncthreads();
+    int before = carry;
+    for (int w = 0; w < warp; ++w) before += sm.warp_sum[w];
+    int total = 0;
+    for (int w = 0; w < kThreads / 32; ++w) total += sm.warp_sum[w];
+    const int g = before + __popc(ball & ((1u << lane) - 1u));  // block-local leaf rank
+    if (j < nodes) {
+      const int p = find_prog(sm.node_off, np, gn0 + j);
+      const int64_t pn0 = sm.node_off[p], pl0 = sm.leaf_off[p];
+      const int i = (int)(gn0 + j - pn0);              // program-local node id
+      const int k = (int)(gl0 + g - pl0);              // leaves before it in the program
+      const int64_t pos = pn0 + pl0 + i + k;
+      out.serialized[pos] = i;
       if (is_leaf) {
-        out.ordering[l0 + k] = (int32_t)(i + k);
-        // enclosing loops: parent chain, innermost first
-        int depth = 0;
-        u128 prod = 1, tprod[3] = {1, 1, 1};
-        int tcount[3] = {0, 0, 0};
-        int64_t inner = 0, outer = 0;
-        bool overflow = false;
-        for (int32_t a = parent[n0 + i]; a >= 0; a = parent[n0 + a]) {
-          const int64_t e = extent[n0 + a];
-          const unsigned bits = annot[n0 + a];
-          if (depth == 0) inner = e;
-          outer = e;
-          ++depth;
-          prod *= (u128)e;
-          if (prod > kProductLimit) overflow = true;
-          if (overflow) prod = kProductLimit;  // keep the walk well-defined
-          for (int t = 0; t < 3; ++t)
-            if (bits >> t & 1u) { ++tcount[t]; tprod[t] *= (u128)e; if (tprod[t] > kProductLimit) tprod[t] = kProductLimit; }
-        }
-        if (overflow) atomicMin(out.first_bad, (unsigned long long)p);
-        const int64_t* st = stats + (l0 + k) * 9;
-        double* v = out.vectors + (l0 + k) * TPCB_FEAT;
-        const u128 iters = depth ? prod : (u128)1;
-        v[0] = (double)depth;
-        v[1] = depth ? log2_1p_int(prod) : 0.0;
-        v[2] = depth ? log2_1p_int((u128)inner) : 0.0;
-        v[3] = depth ? log2_1p_int((u128)outer) : 0.0;
-        for (int t = 0; t < 3; ++t) {
-          v[4 + t] = (double)tcount[t];
-          v[7 + t] = tcount[t] ? log2_1p_int(tprod[t]) : 0.0;
-        }
-        u128 per_iter = 2 * (u128)st[0];
-        for (int t = 0; t < 5; ++t) {
-          v[10 + t] = log2_1p_int((u128)st[t]);
-          if (t) per_iter += (u128)st[t];
-        }
-        const u128 tot_flops = per_iter * iters;
-        const u128 tot_read = (u128)st[5] * iters, tot_written = (u128)st[6] * iters;
-        v[15] = log2_1p_int(tot_flops);
-        v[16] = log2_1p_int((u128)st[5]);
-        v[17] = log2_1p_int((u128)st[6]);
-        v[18] = log2_1p_int(tot_read);
-        v[19] = log2_1p_int(tot_written);
-        v[20] = u128_to_double((u128)st[7]);
-        v[21] = u128_to_double((u128)st[8]);
-        v[22] = div_u128(tot_flops, tot_read + tot_written + 1);
-        v[23] = (double)k / (double)n_leaf;
+        out.serialized[pos + 1] = -1;
+        out.ordering[gl0 + g] = i + k;
+        sm.leaf_node[g] = (int16_t)j;
       }
-      before += __popc(ball);
     }
+    carry += total;
+    __syncthreads();  // warp_sum reuse
+  }
+  // one thread per leaf, staged vectors, coalesced stores
+  for (int c = 0; c < leaves; c += kThreads) {
+    const int g = c + t;
+    if (g < leaves) {
+      const int j = sm.leaf_node[g];
+      const int p = find_prog(sm.node_off, np, gn0 + j);
+      const int base = (int)(sm.node_off[p] - gn0);
+      const SmemTree tree{sm.par, sm.ext, sm.ann, base};
+      const Chain ch = walk_chain(tree, j - base);
+      if (ch.overflow) atomicMin(out.first_bad, (unsigned long long)(p0 + p));
+      const int k = (int)(gl0 + g - sm.leaf_off[p]);
+      const int n_leaf = (int)(sm.leaf_off[p + 1] - sm.leaf_off[p]);
+      leaf_vector(ch, stats + (gl0 + g) * 9, k, n_leaf, sm.vec + t * kVecPitch);
+    }
+    __syncthreads();
+    const int n = min(kThreads, leaves - c);
+    double* dst = out.vectors + (gl0 + c) * TPCB_FEAT;
+    for (int e = t; e < n * TPCB_FEAT; e += kThreads) {
+      const int r = e / TPCB_FEAT, col = e - r * TPCB_FEAT;
+      dst[e] = sm.vec[r * kVecPitch + col];
+    }
+    __syncthreads();
   }
 }
 
@@ -174,13 +345,31 @@ extern "C" int tpcb_build_compact(const int64_t* d_node_off, const int32_t* d_pa
   cudaStream_t s = (cudaStream_t)stream;
   TPCB_CUDA_CHECK(cudaMemsetAsync(d_first_overflow, 0xff, sizeof(unsigned long long), s));
   if (n_prog == 0) return TPCB_OK;
-  int dev = 0, sms = 148;
-  TPCB_CUDA_CHECK(cudaGetDevice(&dev));
-  TPCB_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int64_t blocks_needed = (n_prog + 7) / 8;  // 8 warps per block
-  const int blocks = (int)std::min<int64_t>(blocks_needed, (int64_t)sms * 8);
+  {  // per-device one-time upload of the host-libm log2 table
+    static double host_table[tpcb::kLog2Table];
+    static bool table_built = false;
+    static bool uploaded[64] = {};
+    static std::mutex mu;
+    int dev = 0;
+    TPCB_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (!table_built) {
+      for (int i = 0; i < tpcb::kLog2Table; ++i) host_table[i] = std::log2(1.0 + (double)i);
+      table_built = true;
+    }
+    if (dev >= 64) return TPCB_ERR_UNSUPPORTED;
+    if (!uploaded[dev]) {
+      TPCB_CUDA_CHECK(cudaMemcpyToSymbol(tpcb::g_log2_table, host_table, sizeof(host_table)));
+      uploaded[dev] = true;
+    }
+  }
+  const int64_t blocks = (n_prog + tpcb::kProgsPerBlock - 1) / tpcb::kProgsPerBlock;
+  if (blocks > 0x7fffffff) return TPCB_ERR_UNSUPPORTED;
+  const size_t smem = sizeof(tpcb::TileSmem);
+  TPCB_CUDA_CHECK(cudaFuncSetAttribute(tpcb::build_compact_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   tpcb::CompactOut out{d_vectors, d_ordering, d_serialized, d_first_overflow};
-  tpcb::build_compact_kernel<<<blocks, 256, 0, s>>>(d_node_off, d_parent, d_extent, d_annot,
+  tpcb::build_compact_kernel<<<(unsigned)blocks, tpcb::kThreads, smem, s>>>(d_node_off, d_parent, d_extent, d_annot,
                                                      d_leaf_off, d_stats, n_prog, out);
   TPCB_LAUNCH_CHECK("build_compact_kernel");
   return TPCB_OK;
