@@ -335,6 +335,17 @@ int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_params_t, fl
 int tpcb_cmd(const void* d_z, int32_t z_is_f64, int64_t ns, int64_t nt, int32_t de, int32_t k,
              double* d_value, double* d_grad, void* stream);
 
+/* Grid version for large sets (cmd_between over whole datasets; SURVEY 8(d)
+ * "full-set CMD is HBM-bound"): same value / gradient contract as tpcb_cmd,
+ * de <= 128.  Three streaming passes over Z (extrema + sums, central power
+ * sums, gradient) with fixed-order chunk combines (chunks of 2,048 rows of
+ * one set, bitwise reproducible; cmd(S, S) == 0 exactly).  d_ws:
+ * tpcb_cmd_grid_ws(ns, nt, de, k) bytes. */
+size_t tpcb_cmd_grid_ws(int64_t ns, int64_t nt, int32_t de, int32_t k);
+int tpcb_cmd_grid(const void* d_z, int32_t z_is_f64, int64_t ns, int64_t nt, int32_t de,
+                  int32_t k, double* d_value, double* d_grad, void* d_ws, size_t ws_bytes,
+                  void* stream);
+
 /* ---- K8–K11: KMeans task sampler (sampling.py:40-144), float64 ----------
  * x: [n, d] row-major fp64 on the device (d ≤ 128).  Distances follow the
  * reference's exact recipe (numpy pairwise summation order), so assignments

@@ -103,6 +103,8 @@ SIGNATURES = {
                                 vp, vp, vp, vp, vp]),
     "tpcb_metrics": (i32, [vp, vp, i64, vp, vp]),
     "tpcb_cmd": (i32, [vp, i32, i64, i64, i32, i32, vp, vp, vp]),
+    "tpcb_cmd_grid_ws": (sz, [i64, i64, i32, i32]),
+    "tpcb_cmd_grid": (i32, [vp, i32, i64, i64, i32, i32, vp, vp, vp, sz, vp]),
     "tpcb_train_ws_sizes": (i32, [vp, i32, i32, C.POINTER(i32), C.POINTER(i64),
                                   C.POINTER(i64), C.POINTER(i64)]),
     "tpcb_transpose_params": (i32, [vp, vp, vp, vp]),

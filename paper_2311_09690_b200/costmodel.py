@@ -328,14 +328,34 @@ def _cmd_device(zs, zt, k: int, want_grad: bool):
     z = torch.from_numpy(np.ascontiguousarray(np.vstack([zs, zt]))).cuda()
     val = torch.zeros(1, dtype=torch.float64, device=z.device)
     grad = torch.empty_like(z) if want_grad else None
-    lib = engine._lib.load()
-    engine._lib.check(lib.tpcb_cmd(z.data_ptr(), 1, zs.shape[0], zt.shape[0], zs.shape[1], int(k),
-                                   val.data_ptr(), engine.dptr(grad), engine.stream_ptr()), "cmd")
+    cmd_device_z(z, zs.shape[0], zt.shape[0], int(k), val, grad)
     value = float(val.item())
     if not want_grad:
         return value
     g = grad.cpu().numpy()
     return value, g[:zs.shape[0]], g[zs.shape[0]:]
+
+
+CMD_GRID_ROWS = 16384  # at or above: the multi-block HBM-streaming kernels
+
+
+def cmd_device_z(z: torch.Tensor, ns: int, nt: int, k: int, val: torch.Tensor,
+                 grad: torch.Tensor | None = None) -> None:
+    """CMD of device rows z = [zs; zt] (f32/f64) into val[0] (+ grad):
+    one CTA for small sets (the in-step size), the grid kernels for large
+    ones (cmd_between over whole datasets)."""
+    lib = engine._lib.load()
+    is64 = 1 if z.dtype == torch.float64 else 0
+    de = int(z.shape[1])
+    if ns + nt >= CMD_GRID_ROWS and de <= 128:
+        ws = torch.empty(int(lib.tpcb_cmd_grid_ws(ns, nt, de, k)), dtype=torch.uint8,
+                         device=z.device)
+        engine._lib.check(lib.tpcb_cmd_grid(z.data_ptr(), is64, ns, nt, de, k, val.data_ptr(),
+                                            engine.dptr(grad), ws.data_ptr(), ws.numel(),
+                                            engine.stream_ptr()), "cmd")
+    else:
+        engine._lib.check(lib.tpcb_cmd(z.data_ptr(), is64, ns, nt, de, k, val.data_ptr(),
+                                       engine.dptr(grad), engine.stream_ptr()), "cmd")
 
 
 def cmd(zs, zt, k: int = 5) -> float:

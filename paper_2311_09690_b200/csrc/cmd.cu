@@ -4,6 +4,8 @@
 // first index, means, central power sums up to order K) and, optionally, the
 // gradient w.r.t. every row (costmodel.py:426-486).  The in-training CMD term
 // uses the same device functions (train.cu).
+#include <algorithm>
+
 #include "cmd.cuh"
 #include "common.cuh"
 
@@ -25,10 +27,315 @@ __global__ void __launch_bounds__(1024) cmd_kernel(const T* __restrict__ Z, int 
   }
 }
 
+// ---- grid version for large sets (cmd_between over whole datasets) --------
+// HBM-bound: pass A (extrema + per-set sums), pass C (central power sums),
+// pass E (gradient) each stream Z once with coalesced row reads (lane =
+// column); the two combine kernels run on one block.  Each block owns a
+// chunk of kChunk rows of ONE set, chunked from that set's own first row, and
+// partials are combined in block order — so the reduction order is fixed
+// (bitwise reproducible) and identical for identical sets: cmd(S, S) is
+// exactly 0 as in the reference (costmodel.py:446-475 guards).
+constexpr int kChunk = 512;
+constexpr int kGridThreads = 256;
+constexpr int kMaxGridDe = 128;  // columns per lane <= 4
+
+struct GridPlan {
+  int ns, nt, de, K, bs, bt;  // bs / bt: chunks of the source / target set
+  __device__ void chunk(int b, int& r0, int& r1, bool& is_s) const {
+    is_s = b < bs;
+    const int lb = is_s ? b : b - bs;
+    const int base = is_s ? 0 : ns, cnt = is_s ? ns : nt;
+    r0 = base + lb * kChunk;
+    r1 = base + min(cnt, (lb + 1) * kChunk);
+  }
+};
+
+// pass A: per block and column: min/argmin, max/argmax, sum
+template <typename T>
+__global__ void __launch_bounds__(kGridThreads) cmd_pass_a(const T* __restrict__ Z, GridPlan g,
+                                                           double* __restrict__ part) {
+  __shared__ double s_mn[8][kMaxGridDe], s_mx[8][kMaxGridDe], s_sum[8][kMaxGridDe];
+  __shared__ int s_imn[8][kMaxGridDe], s_imx[8][kMaxGridDe];
+  int r0, r1;
+  bool is_s;
+  g.chunk(blockIdx.x, r0, r1, is_s);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c = lane; c < g.de; c += 32) {
+    double mn = INFINITY, mx = -INFINITY, sum = 0.0;
+    int imn = 0x7fffffff, imx = 0x7fffffff;
+#pragma unroll 4
+    for (int r = r0 + w; r < r1; r += 8) {
+      const double v = (double)Z[(size_t)r * g.de + c];
+      argmin_merge(mn, imn, v, r);
+      argmax_merge(mx, imx, v, r);
+      sum += v;
+    }
+    s_mn[w][c] = mn; s_imn[w][c] = imn;
+    s_mx[w][c] = mx; s_imx[w][c] = imx;
+    s_sum[w][c] = sum;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < g.de; c += kGridThreads) {
+    double mn = s_mn[0][c], mx = s_mx[0][c], sum = s_sum[0][c];
+    int imn = s_imn[0][c], imx = s_imx[0][c];
+    for (int q = 1; q < 8; ++q) {
+      argmin_merge(mn, imn, s_mn[q][c], s_imn[q][c]);
+      argmax_merge(mx, imx, s_mx[q][c], s_imx[q][c]);
+      sum += s_sum[q][c];
+    }
+    double* o = part + (size_t)blockIdx.x * 5 * g.de;
+    o[c] = mn; o[g.de + c] = (double)imn;
+    o[2 * g.de + c] = mx; o[3 * g.de + c] = (double)imx;
+    o[4 * g.de + c] = sum;
+  }
+}
+
+// Fixed-shape block reduction of one set's chunk partials: thread q takes
+// the chunks q, q+256, ... of THAT set in order, then warp xor-trees and the
+// 8 warp totals in warp order — deterministic, and the same shape for two
+// identical sets (cmd(S, S) == 0 exactly).  Result valid in thread 0.
+__device__ __forceinline__ double block_set_sum(const double* part, int first, int count,
+                                                size_t stride, double* red) {
+  double a = 0.0;
+  for (int q = threadIdx.x; q < count; q += kGridThreads) a += part[(size_t)(first + q) * stride];
+  a = warp_sum_d(a);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kGridThreads / 32; ++w) t += red[w];
+  return t;
+}
+
+// combine A: one block per column — extrema over all chunks, per-set means
+__global__ void __launch_bounds__(kGridThreads) cmd_combine_a(GridPlan g,
+                                                              const double* __restrict__ part,
+                                                              double* __restrict__ cs) {
+  __shared__ double red[kGridThreads / 32], rmn[kGridThreads / 32], rmx[kGridThreads / 32];
+  __shared__ int rimn[kGridThreads / 32], rimx[kGridThreads / 32];
+  const int de = g.de, c = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nb = g.bs + g.bt;
+  double mn = INFINITY, mx = -INFINITY;
+  int imn = 0x7fffffff, imx = 0x7fffffff;
+  for (int b = threadIdx.x; b < nb; b += kGridThreads) {
+    const double* o = part + (size_t)b * 5 * de;
+    argmin_merge(mn, imn, o[c], (int)o[de + c]);
+    argmax_merge(mx, imx, o[2 * de + c], (int)o[3 * de + c]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, mn, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, imn, o);
+    argmin_merge(mn, imn, v2, i2);
+    const double v3 = __shfl_xor_sync(0xffffffffu, mx, o);
+    const int i3 = __shfl_xor_sync(0xffffffffu, imx, o);
+    argmax_merge(mx, imx, v3, i3);
+  }
+  if (lane == 0) { rmn[w] = mn; rimn[w] = imn; rmx[w] = mx; rimx[w] = imx; }
+  const double ss = block_set_sum(part + 4 * de + c, 0, g.bs, (size_t)5 * de, red);
+  const double st = block_set_sum(part + 4 * de + c, g.bs, g.bt, (size_t)5 * de, red);
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < kGridThreads / 32; ++q) {
+      argmin_merge(mn, imn, rmn[q], rimn[q]);
+      argmax_merge(mx, imx, rmx[q], rimx[q]);
+    }
+    cs[c] = mn;
+    cs[de + c] = mx;
+    cs[2 * de + c] = ss / g.ns;
+    cs[3 * de + c] = st / g.nt;
+    const double raw = mx - mn;
+    cs[4 * de + c] = raw < kCmdSupportFloor ? -kCmdSupportFloor : raw;
+    cs[7 * de + c] = (double)imn;
+    cs[8 * de + c] = (double)imx;
+  }
+}
+
+// pass C: central power sums sum (z - mu)^j, j = 1..K, per block and column
+template <typename T>
+__global__ void __launch_bounds__(kGridThreads) cmd_pass_c(const T* __restrict__ Z, GridPlan g,
+                                                           const double* __restrict__ cs,
+                                                           double* __restrict__ part) {
+  __shared__ double s_p[8][kMaxCmdOrder][32];
+  int r0, r1;
+  bool is_s;
+  g.chunk(blockIdx.x, r0, r1, is_s);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double* mu = cs + (is_s ? 2 : 3) * g.de;
+  for (int c0 = 0; c0 < g.de; c0 += 32) {
+    const int c = c0 + lane;
+    double ps[kMaxCmdOrder];
+#pragma unroll
+    for (int j = 0; j < kMaxCmdOrder; ++j) ps[j] = 0.0;
+    if (c < g.de) {
+      const double m = mu[c];
+#pragma unroll 4
+      for (int r = r0 + w; r < r1; r += 8) {
+        const double cen = (double)Z[(size_t)r * g.de + c] - m;
+        double pw = cen;
+#pragma unroll
+        for (int j = 0; j < kMaxCmdOrder; ++j) {
+          if (j < g.K) { ps[j] += pw; pw *= cen; }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxCmdOrder; ++j) s_p[w][j][lane] = ps[j];
+    __syncthreads();
+    for (int e = threadIdx.x; e < g.K * 32; e += kGridThreads) {
+      const int j = e >> 5, l = e & 31;
+      if (c0 + l < g.de) {
+        double a = s_p[0][j][l];
+        for (int q = 1; q < 8; ++q) a += s_p[q][j][l];
+        part[((size_t)blockIdx.x * g.K + j) * g.de + c0 + l] = a;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// combine C: one block per (order j, column c) — per-set central moments
+__global__ void __launch_bounds__(kGridThreads) cmd_combine_c(GridPlan g,
+                                                              const double* __restrict__ part,
+                                                              double* __restrict__ cs) {
+  __shared__ double red[kGridThreads / 32];
+  const int de = g.de, KM = kMaxCmdOrder + 1;
+  const int j = blockIdx.x / de, c = blockIdx.x - j * de;
+  const size_t stride = (size_t)g.K * de;
+  const double a = block_set_sum(part + (size_t)j * de + c, 0, g.bs, stride, red);
+  const double b = block_set_sum(part + (size_t)j * de + c, g.bs, g.bt, stride, red);
+  if (threadIdx.x == 0) {
+    cs[9 * de + (j + 1) * de + c] = a / g.ns;
+    cs[9 * de + KM * de + (j + 1) * de + c] = b / g.nt;
+  }
+}
+
+// finish (one block): norms, support gradient, value (costmodel.py:440-476)
+__global__ void __launch_bounds__(256) cmd_finish_kernel(GridPlan g, double* __restrict__ cs_g,
+                                                         double* __restrict__ value) {
+  extern __shared__ double cs[];
+  const int n_cs = cmd_scratch_doubles(g.de);
+  for (int e = threadIdx.x; e < n_cs; e += blockDim.x) cs[e] = cs_g[e];
+  __syncthreads();
+  const double v = cmd_finish(cs, g.de, g.K, 0, blockDim.x);
+  if (threadIdx.x == 0) *value = v;
+  for (int e = threadIdx.x; e < n_cs; e += blockDim.x) cs_g[e] = cs[e];
+}
+
+// pass E: gradient of every element (coalesced).  The per-column factors of
+// cmd_grad_elem (costmodel.py:446-475) are formed once per block in the same
+// operation order, so each element costs K-1 FMAs instead of K pow() calls.
+template <typename T>
+__global__ void __launch_bounds__(kGridThreads) cmd_pass_e(const T* __restrict__ Z, GridPlan g,
+                                                           const double* __restrict__ cs,
+                                                           double* __restrict__ grad) {
+  // per set: mu, c0, then per order j = 2..K: w_j, mean(cen^(j-1))
+  extern __shared__ double coef[];
+  const int de = g.de, K = g.K, KM = kMaxCmdOrder + 1;
+  const int per_set = (2 + 2 * (K - 1)) * de;
+  const double* mus = cs + 2 * de;
+  const double* mut = cs + 3 * de;
+  const double* s = cs + 4 * de;
+  const double* u = cs + 5 * de;
+  const double* ds = cs + 6 * de;
+  const double* amin = cs + 7 * de;
+  const double* amax = cs + 8 * de;
+  const double* ms = cs + 9 * de;
+  const double* mt = ms + KM * de;
+  const double* norms = mt + KM * de;
+  for (int e = threadIdx.x; e < 2 * de; e += blockDim.x) {
+    const int set = e / de, c = e - set * de;
+    const bool is_s = set == 0;
+    const double cnt = is_s ? (double)g.ns : (double)g.nt;
+    const double sign = is_s ? 1.0 : -1.0;
+    const double sc = fabs(s[c]);
+    const double* mm = is_s ? ms : mt;
+    double* o = coef + set * per_set;
+    o[c] = is_s ? mus[c] : mut[c];
+    o[de + c] = norms[1] > 0.0 ? sign * (u[c] / norms[1]) / (sc * cnt) : 0.0;
+    for (int j = 2; j <= K; ++j) {
+      double w = 0.0;
+      if (norms[j] > 0.0) {
+        const double sj = pow(sc, (double)j);
+        const double v = (ms[j * de + c] - mt[j * de + c]) / sj;
+        w = sign * ((double)j / cnt) * (v / norms[j]) / sj;
+      }
+      o[(2 * (j - 1)) * de + c] = w;
+      o[(2 * (j - 1) + 1) * de + c] = mm[(j - 1) * de + c];
+    }
+  }
+  __syncthreads();
+  const int total = (g.ns + g.nt) * de;  // < 2^31 (checked at launch)
+  const bool de32 = de == 32;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int row = de32 ? e >> 5 : e / de, c = de32 ? e & 31 : e - row * de;
+    const double* o = coef + (row < g.ns ? 0 : per_set);
+    const double cen = (double)Z[e] - o[c];
+    double gv = o[de + c];
+    double pw = 1.0;
+    for (int j = 2; j <= K; ++j) {
+      pw *= cen;
+      gv += o[(2 * (j - 1)) * de + c] * (pw - o[(2 * (j - 1) + 1) * de + c]);
+    }
+    if ((double)row == amax[c]) gv += ds[c];
+    if ((double)row == amin[c]) gv -= ds[c];
+    grad[e] = gv;
+  }
+}
+
+template <typename T>
+int launch_cmd_grid(const T* Z, const GridPlan& g, double* value, double* grad, double* ws,
+                    cudaStream_t st) {
+  const int blocks = g.bs + g.bt;
+  const size_t n_cs = cmd_scratch_doubles(g.de);
+  double* cs = ws;
+  double* part = ws + n_cs;
+  const size_t smem = n_cs * sizeof(double);
+  cmd_pass_a<T><<<blocks, kGridThreads, 0, st>>>(Z, g, part);
+  cmd_combine_a<<<g.de, kGridThreads, 0, st>>>(g, part, cs);
+  cmd_pass_c<T><<<blocks, kGridThreads, 0, st>>>(Z, g, cs, part);
+  cmd_combine_c<<<g.K * g.de, kGridThreads, 0, st>>>(g, part, cs);
+  TPCB_CUDA_CHECK(cudaFuncSetAttribute(cmd_finish_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cmd_finish_kernel<<<1, 256, smem, st>>>(g, cs, value);
+  if (grad) {
+    const size_t esmem = (size_t)2 * (2 + 2 * (g.K - 1)) * g.de * sizeof(double);
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(cmd_pass_e<T>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
+    cmd_pass_e<T><<<kNumSMs * 8, kGridThreads, esmem, st>>>(Z, g, cs, grad);
+  }
+  TPCB_LAUNCH_CHECK("cmd_grid");
+  return TPCB_OK;
+}
+
 }  // namespace
 }  // namespace tpcb
 
 using namespace tpcb;
+
+extern "C" size_t tpcb_cmd_grid_ws(int64_t ns, int64_t nt, int32_t de, int32_t k) {
+  if (ns < 1 || nt < 1 || de < 1 || k < 1) return 0;
+  const int64_t blocks = (ns + kChunk - 1) / kChunk + (nt + kChunk - 1) / kChunk;
+  const int64_t per = std::max<int64_t>(5, k);
+  return (size_t)(cmd_scratch_doubles(de) + blocks * per * de) * sizeof(double);
+}
+
+extern "C" int tpcb_cmd_grid(const void* d_z, int32_t z_is_f64, int64_t ns, int64_t nt,
+                             int32_t de, int32_t k, double* d_value, double* d_grad, void* d_ws,
+                             size_t ws_bytes, void* stream) {
+  if (!d_z || !d_value || !d_ws) return TPCB_ERR_VALIDATION;
+  if (ns < 1 || nt < 1) return TPCB_ERR_EMPTY_SET;
+  if (de < 1 || k < 1) return TPCB_ERR_VALIDATION;
+  if (k > kMaxCmdOrder || de > kMaxGridDe) return TPCB_ERR_UNSUPPORTED;
+  if ((ns + nt) * de > 0x7fffffff) return TPCB_ERR_UNSUPPORTED;
+  if (ws_bytes < tpcb_cmd_grid_ws(ns, nt, de, k)) return TPCB_ERR_VALIDATION;
+  GridPlan g{(int)ns, (int)nt, de, k, (int)((ns + kChunk - 1) / kChunk),
+             (int)((nt + kChunk - 1) / kChunk)};
+  cudaStream_t st = (cudaStream_t)stream;
+  double* ws = static_cast<double*>(d_ws);
+  return z_is_f64 ? launch_cmd_grid(static_cast<const double*>(d_z), g, d_value, d_grad, ws, st)
+                  : launch_cmd_grid(static_cast<const float*>(d_z), g, d_value, d_grad, ws, st);
+}
 
 extern "C" int tpcb_cmd(const void* d_z, int32_t z_is_f64, int64_t ns, int64_t nt, int32_t de,
                         int32_t k, double* d_value, double* d_grad, void* stream) {

@@ -43,6 +43,64 @@ __device__ __forceinline__ void cmd_bar(int bar_id, int nthr) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nthr) : "memory");
 }
 
+// Second half of the CMD statistics once lo/hi/amin/amax/mus/mut/s and the
+// central moments ms/mt are in `cs`: the per-order norms, the support
+// gradient and the value (costmodel.py:440-476).  Whole group participates.
+static __device__ __noinline__ double cmd_finish(double* cs, int de, int K, int bar_id,
+                                                 int nthr) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int KM = kMaxCmdOrder + 1;
+  double* mus = cs + 2 * de;
+  double* mut = mus + de;
+  double* s = mut + de;
+  double* u = s + de;
+  double* ds = u + de;
+  double* ms = cs + 9 * de;
+  double* mt = ms + KM * de;
+  double* norms = mt + KM * de;
+  // norms over columns (warp 0)
+  if (w == 0) {
+    double acc = 0.0;
+    for (int c = lane; c < de; c += 32) {
+      const double sc = fabs(s[c]);
+      const double uc = (mus[c] - mut[c]) / sc;
+      u[c] = uc;
+      acc += uc * uc;
+    }
+    acc = warp_sum_d(acc);
+    if (lane == 0) norms[1] = sqrt(acc);
+    for (int j = 2; j <= K; ++j) {
+      double a2 = 0.0;
+      for (int c = lane; c < de; c += 32) {
+        const double sc = fabs(s[c]);
+        const double v = (ms[j * de + c] - mt[j * de + c]) / pow(sc, (double)j);
+        a2 += v * v;
+      }
+      a2 = warp_sum_d(a2);
+      if (lane == 0) norms[j] = sqrt(a2);
+    }
+  }
+  cmd_bar(bar_id, nthr);
+  // support gradient per column
+  for (int c = threadIdx.x; c < de; c += nthr) {
+    const double sc = fabs(s[c]);
+    double d = 0.0;
+    if (norms[1] > 0.0) d -= (u[c] / norms[1]) * u[c] / sc;
+    for (int j = 2; j <= K; ++j) {
+      if (norms[j] > 0.0) {
+        const double v = (ms[j * de + c] - mt[j * de + c]) / pow(sc, (double)j);
+        d -= j * (v / norms[j]) * v / sc;
+      }
+    }
+    ds[c] = (s[c] < 0.0) ? 0.0 : d;
+  }
+  cmd_bar(bar_id, nthr);
+  double value = norms[1];
+  for (int j = 2; j <= K; ++j) value += norms[j];
+  cmd_bar(bar_id, nthr);
+  return value;
+}
+
 template <typename T>
 static __device__ __noinline__ double cmd_stats(const T* __restrict__ Z, int ns, int nt, int de,
                                                 int K, double* cs, int bar_id = 0,
@@ -128,47 +186,7 @@ static __device__ __noinline__ double cmd_stats(const T* __restrict__ Z, int ns,
     }
   }
   cmd_bar(bar_id, nthr);
-  // norms over columns (warp 0)
-  if (w == 0) {
-    double acc = 0.0;
-    for (int c = lane; c < de; c += 32) {
-      const double sc = fabs(s[c]);
-      const double uc = (mus[c] - mut[c]) / sc;
-      u[c] = uc;
-      acc += uc * uc;
-    }
-    acc = warp_sum_d(acc);
-    if (lane == 0) norms[1] = sqrt(acc);
-    for (int j = 2; j <= K; ++j) {
-      double a2 = 0.0;
-      for (int c = lane; c < de; c += 32) {
-        const double sc = fabs(s[c]);
-        const double v = (ms[j * de + c] - mt[j * de + c]) / pow(sc, (double)j);
-        a2 += v * v;
-      }
-      a2 = warp_sum_d(a2);
-      if (lane == 0) norms[j] = sqrt(a2);
-    }
-  }
-  cmd_bar(bar_id, nthr);
-  // support gradient per column
-  for (int c = threadIdx.x; c < de; c += nthr) {
-    const double sc = fabs(s[c]);
-    double d = 0.0;
-    if (norms[1] > 0.0) d -= (u[c] / norms[1]) * u[c] / sc;
-    for (int j = 2; j <= K; ++j) {
-      if (norms[j] > 0.0) {
-        const double v = (ms[j * de + c] - mt[j * de + c]) / pow(sc, (double)j);
-        d -= j * (v / norms[j]) * v / sc;
-      }
-    }
-    ds[c] = (s[c] < 0.0) ? 0.0 : d;
-  }
-  cmd_bar(bar_id, nthr);
-  double value = norms[1];
-  for (int j = 2; j <= K; ++j) value += norms[j];
-  cmd_bar(bar_id, nthr);
-  return value;
+  return cmd_finish(cs, de, K, bar_id, nthr);
 }
 
 // d CMD / d z[row, c] from the statistics in `cs` (costmodel.py:446-485),

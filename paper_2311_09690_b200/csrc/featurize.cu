@@ -10,9 +10,12 @@
 //
 // Four kernels (HBM-bound; pack_rows is the only one that moves bulk data):
 //   bucket_count   per-block n_leaf histogram + range check
-//   bucket_scan    bucket offsets, per-block bases, tile plan (1 CTA)
-//   bucket_scatter stable rank → perm, ast_row (warp match/ballot, no atomics)
+//   bucket_scan    per-bucket scan of the block histograms (one CTA per bucket)
+//   bucket_scatter stable rank → perm, ast_row (warp match/ballot, no atomics),
+//                  plus the per-tile plan (grid-strided)
+//   pe_table       fp64 PE rows of positions 0..1023 (same sincos, looked up)
 //   pack_rows      gather leaf vectors, add fp64 PE, write padded 128-B rows
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -76,71 +79,103 @@ __device__ int block_excl_scan(int v, int* total) {
   return res;
 }
 
-// One CTA of 1024 threads.  ws layout: blk_hist[nblk][17], blk_base[nblk][17],
-// tile_off[18].
-__global__ void __launch_bounds__(1024) bucket_scan_kernel(
-    const int32_t* __restrict__ blk_hist, int nblk, int n_leaf_max, int R,
-    int32_t* __restrict__ blk_base, int32_t* __restrict__ bucket_off,
-    int32_t* __restrict__ tile_off, int32_t* __restrict__ tile_L,
-    int32_t* __restrict__ tile_first, int32_t* __restrict__ tile_count,
-    int32_t* __restrict__ n_tiles_out, int n_tiles_max) {
-  __shared__ int s_boff[kMaxL + 2];
-  __shared__ int s_toff[kMaxL + 2];
+// One CTA per bucket L (grid n_leaf_max, 1024 threads): exclusive scan of
+// column L of the per-block histograms → blk_base[b][L] (relative to the
+// bucket start) and the bucket's size cnt[L].  ws layout: blk_hist[nblk][17],
+// blk_base[nblk][17], cnt[18], PE table.
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(const int32_t* __restrict__ blk_hist,
+                                                           int nblk,
+                                                           int32_t* __restrict__ blk_base,
+                                                           int32_t* __restrict__ cnt) {
+  const int L = blockIdx.x + 1;
   const int per = (nblk + blockDim.x - 1) / blockDim.x;
-  int running = 0;  // start of bucket L
-  if (threadIdx.x == 0) s_boff[0] = 0;
-  for (int L = 1; L <= n_leaf_max; ++L) {
-    int b0 = threadIdx.x * per;
-    int sum = 0;
-    for (int b = b0; b < b0 + per && b < nblk; ++b) sum += blk_hist[(int64_t)b * (kMaxL + 1) + L];
-    int total;
-    int ex = block_excl_scan(sum, &total);
-    int acc = running + ex;
-    for (int b = b0; b < b0 + per && b < nblk; ++b) {
+  const int b0 = threadIdx.x * per, b1 = min(nblk, b0 + per);
+  int v[8];
+  int sum = 0;
+  if (per <= 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      v[q] = (b0 + q < b1) ? blk_hist[(int64_t)(b0 + q) * (kMaxL + 1) + L] : 0;
+      sum += v[q];
+    }
+  } else {
+    for (int b = b0; b < b1; ++b) sum += blk_hist[(int64_t)b * (kMaxL + 1) + L];
+  }
+  int total;
+  int acc = block_excl_scan(sum, &total);
+  if (per <= 8) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (b0 + q < b1) {
+        blk_base[(int64_t)(b0 + q) * (kMaxL + 1) + L] = acc;
+        acc += v[q];
+      }
+  } else {
+    for (int b = b0; b < b1; ++b) {
       blk_base[(int64_t)b * (kMaxL + 1) + L] = acc;
       acc += blk_hist[(int64_t)b * (kMaxL + 1) + L];
     }
-    if (threadIdx.x == 0) s_boff[L] = running;
-    running += total;
   }
-  if (threadIdx.x == 0) {
-    s_boff[n_leaf_max + 1] = running;
-    int t = 0;
-    for (int L = 1; L <= n_leaf_max; ++L) {
-      s_toff[L] = t;
-      int cnt = s_boff[L + 1] - s_boff[L];
-      int A = R / L;
-      t += (cnt + A - 1) / A;
-    }
-    s_toff[n_leaf_max + 1] = t;
-    *n_tiles_out = t < n_tiles_max ? t : n_tiles_max;
-  }
-  __syncthreads();
-  if (threadIdx.x <= n_leaf_max + 1) {
-    bucket_off[threadIdx.x] = s_boff[threadIdx.x];
-    tile_off[threadIdx.x] = s_toff[threadIdx.x];
-  }
-  const int nt = s_toff[n_leaf_max + 1];
-  for (int t = threadIdx.x; t < nt && t < n_tiles_max; t += blockDim.x) {
-    int L = 1;
-    while (L < n_leaf_max && s_toff[L + 1] <= t) ++L;
-    int A = R / L;
-    int first = s_boff[L] + (t - s_toff[L]) * A;
-    int end = s_boff[L + 1];
-    tile_L[t] = L;
-    tile_first[t] = first;
-    tile_count[t] = min(A, end - first);
-  }
+  if (threadIdx.x == 0) cnt[L] = total;
+}
+
+// PE rows for serialized positions 0..kPeRows-1, fp64, the same sincos the
+// pack kernel would evaluate (bit-identical table lookups)
+constexpr int kPeRows = 1024;
+__global__ void pe_table_kernel(PeDenom den, double* __restrict__ table) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= kPeRows * (TPCB_FEAT / 2)) return;
+  const int pos = idx / (TPCB_FEAT / 2), dl = idx - pos * (TPCB_FEAT / 2);
+  double sn, cs;
+  sincos((double)pos / den.v[dl], &sn, &cs);
+  table[pos * TPCB_FEAT + 2 * dl] = sn;
+  table[pos * TPCB_FEAT + 2 * dl + 1] = cs;
 }
 
 __global__ void bucket_scatter_kernel(const int64_t* __restrict__ leaf_off, int64_t n_ast,
                                       int n_leaf_max, int R,
                                       const int32_t* __restrict__ blk_base,
-                                      const int32_t* __restrict__ bucket_off,
-                                      const int32_t* __restrict__ tile_off,
-                                      int32_t* __restrict__ perm, int32_t* __restrict__ ast_row) {
+                                      const int32_t* __restrict__ cnt,
+                                      int32_t* __restrict__ bucket_off_out,
+                                      int32_t* __restrict__ perm, int32_t* __restrict__ ast_row,
+                                      int32_t* __restrict__ n_tiles_out, int n_tiles_max,
+                                      int32_t* __restrict__ tile_L,
+                                      int32_t* __restrict__ tile_first,
+                                      int32_t* __restrict__ tile_count,
+                                      int32_t* __restrict__ row_tok,
+                                      int32_t* __restrict__ row_ast) {
   __shared__ int warp_cnt[kScatterBlock / 32][kMaxL + 1];
+  __shared__ int bucket_off[kMaxL + 2], tile_off[kMaxL + 2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {  // bucket and tile offsets from the bucket sizes
+    int b = 0, t = 0;
+    for (int L = 1; L <= n_leaf_max; ++L) {
+      bucket_off[L] = b;
+      tile_off[L] = t;
+      const int c = cnt[L], A = R / L;
+      b += c;
+      t += (c + A - 1) / A;
+    }
+    bucket_off[0] = tile_off[0] = 0;
+    bucket_off[n_leaf_max + 1] = b;
+    tile_off[n_leaf_max + 1] = t;
+    if (blockIdx.x == 0) *n_tiles_out = t < n_tiles_max ? t : n_tiles_max;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x <= n_leaf_max + 1)
+    bucket_off_out[threadIdx.x] = bucket_off[threadIdx.x];
+  {  // tile plan, grid-strided over the tiles (bucket L cut into tiles of R/L ASTs)
+    const int nt = min(tile_off[n_leaf_max + 1], n_tiles_max);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+      int L = 1;
+      while (L < n_leaf_max && tile_off[L + 1] <= t) ++L;
+      const int A = R / L;
+      const int first = bucket_off[L] + (t - tile_off[L]) * A;
+      tile_L[t] = L;
+      tile_first[t] = first;
+      tile_count[t] = min(A, bucket_off[L + 1] - first);
+    }
+  }
   for (int k = threadIdx.x; k < (kScatterBlock / 32) * (kMaxL + 1); k += blockDim.x)
     (&warp_cnt[0][0])[k] = 0;
   __syncthreads();
@@ -158,66 +193,121 @@ __global__ void bucket_scatter_kernel(const int64_t* __restrict__ leaf_off, int6
   if (i < n_ast && L > 0) {
     int pre = 0;
     for (int ww = 0; ww < w; ++ww) pre += warp_cnt[ww][L];
-    int pos = blk_base[(int64_t)blockIdx.x * (kMaxL + 1) + L] + pre + rank;
+    int pos = bucket_off[L] + blk_base[(int64_t)blockIdx.x * (kMaxL + 1) + L] + pre + rank;
     perm[pos] = (int32_t)i;
     int r = pos - bucket_off[L];
     int A = R / L;
     int tile = tile_off[L] + r / A;
-    ast_row[i] = tile * R + (r % A) * L;
+    const int row0 = tile * R + (r % A) * L;
+    ast_row[i] = row0;
+    const int tok0 = (int)leaf_off[i];  // n_tok < 2^31 (tpcb_pack_sizes)
+    for (int l = 0; l < L; ++l) {  // the packed rows of AST i: source token + owner
+      row_tok[row0 + l] = tok0 + l;
+      row_ast[row0 + l] = (int32_t)i;
+    }
   }
 }
 
+// One thread per packed row: the perm → leaf_off → ordering chain once per
+// row, all 6 leaf-vector loads (and PE table reads) in flight together, the
+// row staged in shared memory so the block writes its 256 consecutive rows
+// (32 KB) with coalesced 16-byte stores.
+constexpr int kPackThreads = 256;
+
+// PE term for positions outside the table (rare): out of line, scalar in /
+// scalar out, so the pack kernel keeps its row in registers
+__device__ __noinline__ double pe_term(double pos, double den, int is_cos) {
+  double sn, cs;
+  sincos(pos / den, &sn, &cs);
+  return is_cos ? cs : sn;
+}
+constexpr int kStagePitch = 36;  // floats per staged row (144 B: spreads banks)
+
 template <bool F64, bool PE>
-__global__ void pack_rows_kernel(const void* __restrict__ vectors_,
-                                 const int32_t* __restrict__ ordering,
-                                 const int64_t* __restrict__ leaf_off,
-                                 const int32_t* __restrict__ perm,
-                                 const int32_t* __restrict__ tile_L,
-                                 const int32_t* __restrict__ tile_first,
-                                 const int32_t* __restrict__ tile_count,
-                                 const int32_t* __restrict__ n_tiles, int R, PeDenom den,
-                                 float* __restrict__ x, int32_t* __restrict__ row_ast) {
-  const int nt = *n_tiles;
+__global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
+    const void* __restrict__ vectors_, const int32_t* __restrict__ ordering,
+    const int64_t* __restrict__ leaf_off, const int32_t* __restrict__ perm,
+    const int32_t* __restrict__ tile_L, const int32_t* __restrict__ tile_first,
+    const int32_t* __restrict__ tile_count, const int32_t* __restrict__ n_tiles, int R,
+    PeDenom den, const double* __restrict__ pe_table, const int32_t* __restrict__ row_tok,
+    float* __restrict__ x, int32_t* __restrict__ row_ast) {
+  __shared__ __align__(16) float stage[kPackThreads * kStagePitch];
   constexpr int kChunks = TPCB_FEAT_PAD / 4;  // 8 float4 per packed row
-  for (int t = blockIdx.x; t < nt; t += gridDim.x) {
-    const int L = tile_L[t], first = tile_first[t], cnt = tile_count[t];
-    for (int item = threadIdx.x; item < R * kChunks; item += blockDim.x) {
-      const int r = item / kChunks, ch = item % kChunks;
-      const int a = r / L, l = r - a * L;
-      float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-      int ast = -1;
-      if (a < cnt) {
-        ast = perm[first + a];
-        if (ch * 4 < TPCB_FEAT) {
-          const int64_t tok = leaf_off[ast] + l;
-          const double pos = (double)ordering[tok];
-          double v[4];
+  const int rshift = R == 32 ? 5 : (R == 64 ? 6 : 7);
+  const int64_t rows = (int64_t)(*n_tiles) << rshift;
+  for (int64_t base = (int64_t)blockIdx.x * kPackThreads; base < rows;
+       base += (int64_t)gridDim.x * kPackThreads) {
+    const int64_t gr = base + threadIdx.x;
+    float4 out[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (gr < rows) {
+      const int t = (int)(gr >> rshift), r = (int)(gr & (R - 1));
+      const int L = tile_L[t], cnt = tile_count[t];
+      const int tok_r = row_tok[gr];  // in flight with the tile record
+      if (r / L < cnt) {
+        const int64_t tok = tok_r;
+        const int ipos = PE ? ordering[tok] : 0;
+        const bool table = ipos >= 0 && ipos < kPeRows;
+        // two halves of 12 columns: half the live registers, 3-6 loads in flight each
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double v[12];
           if (F64) {
             const double2* src = reinterpret_cast<const double2*>(
-                static_cast<const double*>(vectors_) + tok * TPCB_FEAT + ch * 4);
-            double2 p0 = __ldg(src), p1 = __ldg(src + 1);
-            v[0] = p0.x; v[1] = p0.y; v[2] = p1.x; v[3] = p1.y;
+                static_cast<const double*>(vectors_) + tok * TPCB_FEAT + h * 12);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+              const double2 p = __ldg(src + q);
+              v[2 * q] = p.x;
+              v[2 * q + 1] = p.y;
+            }
           } else {
-            float4 p = __ldg(reinterpret_cast<const float4*>(
-                static_cast<const float*>(vectors_) + tok * TPCB_FEAT + ch * 4));
-            v[0] = p.x; v[1] = p.y; v[2] = p.z; v[3] = p.w;
+            const float4* src = reinterpret_cast<const float4*>(
+                static_cast<const float*>(vectors_) + tok * TPCB_FEAT + h * 12);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              const float4 p = __ldg(src + q);
+              v[4 * q] = p.x; v[4 * q + 1] = p.y; v[4 * q + 2] = p.z; v[4 * q + 3] = p.w;
+            }
           }
-          // column 2δ: sin(pos/θ^(2δ/24)); 2δ+1: cos (features.py:255-262)
-          double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
-          if (PE) {
-            const int d0 = ch * 2;
-            sincos(pos / den.v[d0], &s0, &c0);
-            sincos(pos / den.v[d0 + 1], &s1, &c1);
+          if (PE) {  // column 2δ: sin(pos/θ^(2δ/24)); 2δ+1: cos (features.py:255-262)
+            if (table) {  // table row (L1/L2 resident)
+              const double2* tp =
+                  reinterpret_cast<const double2*>(pe_table + ipos * TPCB_FEAT + h * 12);
+#pragma unroll
+              for (int q = 0; q < 6; ++q) {
+                const double2 p = __ldg(tp + q);
+                v[2 * q] += p.x;
+                v[2 * q + 1] += p.y;
+              }
+            } else {
+#pragma unroll
+              for (int q = 0; q < 12; ++q) v[q] += pe_term((double)ipos, den.v[h * 6 + q / 2], q & 1);
+            }
           }
-          out.x = (float)(v[0] + s0);
-          out.y = (float)(v[1] + c0);
-          out.z = (float)(v[2] + s1);
-          out.w = (float)(v[3] + c1);
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            out[3 * h + q] = make_float4((float)v[4 * q], (float)v[4 * q + 1],
+                                         (float)v[4 * q + 2], (float)v[4 * q + 3]);
         }
       }
-      reinterpret_cast<float4*>(x)[((int64_t)t * R + r) * kChunks + ch] = out;
-      if (ch == 0) row_ast[(int64_t)t * R + r] = ast;
+      else
+        row_ast[gr] = -1;  // pad row (real rows were written by bucket_scatter)
     }
+    float4* my = reinterpret_cast<float4*>(stage + threadIdx.x * kStagePitch);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) my[q] = out[q];
+    my[6] = make_float4(0.f, 0.f, 0.f, 0.f);
+    my[7] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+    const int n_rows = rows - base < kPackThreads ? (int)(rows - base) : kPackThreads;
+    float4* dst = reinterpret_cast<float4*>(x) + base * kChunks;
+    for (int e = threadIdx.x; e < n_rows * kChunks; e += kPackThreads) {
+      const int rr = e >> 3, ch = e & 7;
+      dst[e] = reinterpret_cast<const float4*>(stage + rr * kStagePitch)[ch];
+    }
+    __syncthreads();
   }
 }
 
@@ -231,6 +321,12 @@ __global__ void positional_kernel(const int32_t* __restrict__ ordering, int64_t 
   sincos((double)ordering[r] / den.v[dl], &s, &c);
   out[r * TPCB_FEAT + 2 * dl] = s;
   out[r * TPCB_FEAT + 2 * dl + 1] = c;
+}
+
+// byte offset of the PE table in the K1 workspace (16-byte aligned)
+size_t pe_table_offset(int64_t nblk) {
+  const size_t ints = (size_t)(2 * nblk * (TPCB_MAX_LEAF + 1) + TPCB_MAX_LEAF + 2) * 4;
+  return (ints + 15) & ~(size_t)15;
 }
 
 int min_rows_per_tile(int R, int n_leaf_max) {
@@ -257,7 +353,9 @@ extern "C" int tpcb_pack_sizes(int64_t n_ast, int64_t n_tok, int32_t n_leaf_max,
   if (n_tiles_max) *n_tiles_max = (int32_t)tiles;
   int64_t nblk = (n_ast + kScatterBlock - 1) / kScatterBlock;
   if (nblk < 1) nblk = 1;
-  if (ws_bytes) *ws_bytes = (size_t)(2 * nblk * (TPCB_MAX_LEAF + 1) + TPCB_MAX_LEAF + 2) * 4;
+  if (ws_bytes)
+    *ws_bytes = pe_table_offset(nblk) + (size_t)kPeRows * TPCB_FEAT * sizeof(double) +
+                (size_t)tiles * R * sizeof(int32_t);  // row_tok
   return TPCB_OK;
 }
 
@@ -278,29 +376,34 @@ extern "C" int tpcb_featurize_pack(const void* d_vectors, int32_t vec_is_f64,
   const int nblk = (int)((n_ast + kScatterBlock - 1) / kScatterBlock);
   int32_t* blk_hist = static_cast<int32_t*>(d_ws);
   int32_t* blk_base = blk_hist + (int64_t)nblk * (TPCB_MAX_LEAF + 1);
-  int32_t* tile_off = blk_base + (int64_t)nblk * (TPCB_MAX_LEAF + 1);
+  int32_t* cnt = blk_base + (int64_t)nblk * (TPCB_MAX_LEAF + 1);
 
   bucket_count_kernel<<<nblk, kScatterBlock, 0, stream>>>(d_leaf_off, n_ast, n_leaf_max,
                                                           blk_hist, d_status);
   TPCB_LAUNCH_CHECK("bucket_count");
-  bucket_scan_kernel<<<1, 1024, 0, stream>>>(blk_hist, nblk, n_leaf_max, R, blk_base,
-                                             out->bucket_off, tile_off, out->tile_L,
-                                             out->tile_first, out->tile_count, out->n_tiles,
-                                             out->n_tiles_max);
+  bucket_scan_kernel<<<n_leaf_max, 1024, 0, stream>>>(blk_hist, nblk, blk_base, cnt);
   TPCB_LAUNCH_CHECK("bucket_scan");
   bucket_scatter_kernel<<<nblk, kScatterBlock, 0, stream>>>(
-      d_leaf_off, n_ast, n_leaf_max, R, blk_base, out->bucket_off, tile_off, out->perm,
-      out->ast_row);
+      d_leaf_off, n_ast, n_leaf_max, R, blk_base, cnt, out->bucket_off, out->perm, out->ast_row,
+      out->n_tiles, out->n_tiles_max, out->tile_L, out->tile_first, out->tile_count, row_tok,
+      out->row_ast);
   TPCB_LAUNCH_CHECK("bucket_scatter");
   PeDenom den;
   for (int i = 0; i < TPCB_FEAT / 2; ++i) den.v[i] = pe_denom ? pe_denom[i] : 1.0;
-  const int grid = min(out->n_tiles_max, kNumSMs * 8);
+  double* pe_table = reinterpret_cast<double*>(static_cast<char*>(d_ws) + pe_table_offset(nblk));
+  int32_t* row_tok = reinterpret_cast<int32_t*>(pe_table + kPeRows * TPCB_FEAT);
+  if (pe_denom) {
+    pe_table_kernel<<<(kPeRows * (TPCB_FEAT / 2) + 255) / 256, 256, 0, stream>>>(den, pe_table);
+    TPCB_LAUNCH_CHECK("pe_table");
+  }
+  const int grid = (int)std::min<int64_t>(((int64_t)out->n_tiles_max * R + kPackThreads - 1) /
+                                              kPackThreads, (int64_t)kNumSMs * 8);
   cudaStream_t st_ = stream;
 #define TPCB_PACK(F64, PEF)                                                                  \
-  pack_rows_kernel<F64, PEF><<<grid, 256, 0, st_>>>(d_vectors, d_ordering, d_leaf_off,      \
+  pack_rows_kernel<F64, PEF><<<grid, kPackThreads, 0, st_>>>(d_vectors, d_ordering, d_leaf_off,      \
                                                     out->perm, out->tile_L, out->tile_first, \
                                                     out->tile_count, out->n_tiles, R, den,   \
-                                                    out->x, out->row_ast)
+                                                    pe_table, row_tok, out->x, out->row_ast)
   if (vec_is_f64) {
     if (pe_denom) TPCB_PACK(true, true); else TPCB_PACK(true, false);
   } else {

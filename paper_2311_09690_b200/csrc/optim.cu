@@ -216,57 +216,101 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(
   }
 }
 
+// one parameter of Adam / SGD (nn.py:136-167), fp32, oracle operation order
+struct OptScalars {
+  float lr, bc1, bc2, b1, b2, eps, wd, omb1, omb2;
+};
+__device__ __forceinline__ void opt1(const OptDev& opt, const OptScalars& k, float g, float& w,
+                                     float& m, float& v) {
+  if (k.wd != 0.f) g = g + k.wd * w;
+  if (opt.kind == kOptSgd) {
+    w = w - k.lr * g;
+    return;
+  }
+  m = __fadd_rn(__fmul_rn(m, k.b1), __fmul_rn(k.omb1, g));
+  v = __fadd_rn(__fmul_rn(v, k.b2), __fmul_rn(__fmul_rn(k.omb2, g), g));
+  w = w - __fdiv_rn(__fmul_rn(k.lr, __fdiv_rn(m, k.bc1)),
+                    __fadd_rn(sqrtf(__fdiv_rn(v, k.bc2)), k.eps));
+}
+
+__device__ __forceinline__ OptScalars opt_scalars(const OptDev& opt, double lr, double t) {
+  OptScalars k;
+  k.lr = (float)lr;
+  k.bc1 = (float)(1.0 - pow(opt.beta1, t));
+  k.bc2 = (float)(1.0 - pow(opt.beta2, t));
+  k.b1 = (float)opt.beta1;
+  k.b2 = (float)opt.beta2;
+  k.eps = (float)opt.eps;
+  k.wd = (float)opt.weight_decay;
+  k.omb1 = (float)(1.0 - opt.beta1);
+  k.omb2 = (float)(1.0 - opt.beta2);
+  return k;
+}
+
+// Optimizer over a gradient vector, HBM-bound (7 x 4 B per parameter):
+// float4 loads/stores for the 16-byte-aligned body (VEC), scalar tail.
+template <bool VEC>
+__device__ __forceinline__ void opt_body(int n, const float* __restrict__ grad,
+                                         float* __restrict__ P, float* __restrict__ mbuf,
+                                         float* __restrict__ vbuf, const OptDev& opt,
+                                         const OptScalars& k) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
+  const bool adam = opt.kind == kOptAdam;
+  int done = 0;
+  if (VEC) {
+    const int n4 = n >> 2;
+    for (int q = tid; q < n4; q += nthr) {
+      const float4 g4 = __ldcs(reinterpret_cast<const float4*>(grad) + q);
+      float4 w4 = reinterpret_cast<float4*>(P)[q];
+      float4 m4 = make_float4(0.f, 0.f, 0.f, 0.f), v4 = m4;
+      if (adam) {
+        m4 = reinterpret_cast<float4*>(mbuf)[q];
+        v4 = reinterpret_cast<float4*>(vbuf)[q];
+      }
+      opt1(opt, k, g4.x, w4.x, m4.x, v4.x);
+      opt1(opt, k, g4.y, w4.y, m4.y, v4.y);
+      opt1(opt, k, g4.z, w4.z, m4.z, v4.z);
+      opt1(opt, k, g4.w, w4.w, m4.w, v4.w);
+      reinterpret_cast<float4*>(P)[q] = w4;
+      if (adam) {
+        reinterpret_cast<float4*>(mbuf)[q] = m4;
+        reinterpret_cast<float4*>(vbuf)[q] = v4;
+      }
+    }
+    done = n4 << 2;
+  }
+  for (int p = done + tid; p < n; p += nthr) {
+    float w = P[p], m = 0.f, v = 0.f;
+    if (adam) {
+      m = mbuf[p];
+      v = vbuf[p];
+    }
+    opt1(opt, k, grad[p], w, m, v);
+    P[p] = w;
+    if (adam) {
+      mbuf[p] = m;
+      vbuf[p] = v;
+    }
+  }
+}
+
 // standalone optimizer over a given gradient vector (nn.Adam.step drop-in)
+template <bool VEC>
 __global__ void optimizer_kernel(int n, const float* __restrict__ grad, float* __restrict__ P,
                                  float* __restrict__ mbuf, float* __restrict__ vbuf, OptDev opt,
                                  double lr_d, double t_d) {
-  const float lr = (float)lr_d;
-  const float bc1 = (float)(1.0 - pow(opt.beta1, t_d)), bc2 = (float)(1.0 - pow(opt.beta2, t_d));
-  const float b1 = (float)opt.beta1, b2 = (float)opt.beta2, eps = (float)opt.eps,
-              wd = (float)opt.weight_decay;
-  const float omb1 = (float)(1.0 - opt.beta1), omb2 = (float)(1.0 - opt.beta2);
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    float g = grad[p], w = P[p];
-    if (wd != 0.f) g = g + wd * w;
-    if (opt.kind == kOptSgd) {
-      P[p] = w - lr * g;
-      continue;
-    }
-    float m = mbuf[p], v = vbuf[p];
-    m = __fadd_rn(__fmul_rn(m, b1), __fmul_rn(omb1, g));
-    v = __fadd_rn(__fmul_rn(v, b2), __fmul_rn(__fmul_rn(omb2, g), g));
-    mbuf[p] = m;
-    vbuf[p] = v;
-    P[p] = w - __fdiv_rn(__fmul_rn(lr, __fdiv_rn(m, bc1)), __fadd_rn(sqrtf(__fdiv_rn(v, bc2)), eps));
-  }
+  opt_body<VEC>(n, grad, P, mbuf, vbuf, opt, opt_scalars(opt, lr_d, t_d));
 }
 
 // Adam / SGD from a (data-parallel all-reduced) gradient vector; lr and the
 // step count before the epoch in device memory (graph replay across epochs)
+template <bool VEC>
 __global__ void opt_from_grad_kernel(int n, const float* __restrict__ grad, float* __restrict__ P,
                                      float* __restrict__ mbuf, float* __restrict__ vbuf,
                                      OptDev opt, const double* __restrict__ lr_p,
                                      const int64_t* __restrict__ t_p, int step) {
-  const float lr = (float)lr_p[0];
-  const double t = (double)(t_p[0] + step + 1);
-  const float bc1 = (float)(1.0 - pow(opt.beta1, t)), bc2 = (float)(1.0 - pow(opt.beta2, t));
-  const float b1 = (float)opt.beta1, b2 = (float)opt.beta2, eps = (float)opt.eps,
-              wd = (float)opt.weight_decay;
-  const float omb1 = (float)(1.0 - opt.beta1), omb2 = (float)(1.0 - opt.beta2);
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    float g = grad[p], w = P[p];
-    if (wd != 0.f) g = g + wd * w;
-    if (opt.kind == kOptSgd) {
-      P[p] = w - lr * g;
-      continue;
-    }
-    float m = mbuf[p], v = vbuf[p];
-    m = __fadd_rn(__fmul_rn(m, b1), __fmul_rn(omb1, g));
-    v = __fadd_rn(__fmul_rn(v, b2), __fmul_rn(__fmul_rn(omb2, g), g));
-    mbuf[p] = m;
-    vbuf[p] = v;
-    P[p] = w - __fdiv_rn(__fmul_rn(lr, __fdiv_rn(m, bc1)), __fadd_rn(sqrtf(__fdiv_rn(v, bc2)), eps));
-  }
+  opt_body<VEC>(n, grad, P, mbuf, vbuf, opt,
+                opt_scalars(opt, lr_p[0], (double)(t_p[0] + step + 1)));
 }
 
 __global__ void transpose_kernel(const float* __restrict__ P, float* __restrict__ PT, T2Table tt) {
@@ -306,8 +350,13 @@ int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps
 int launch_opt_from_grad(const Model& M, const float* grad, float* P, float* m, float* v,
                          const OptDev& opt, const double* lr, const int64_t* t, int step,
                          cudaStream_t stream) {
-  const int grid = min(ceil_div(M.total, 256), kNumSMs * 8);
-  opt_from_grad_kernel<<<grid, 256, 0, stream>>>(M.total, grad, P, m, v, opt, lr, t, step);
+  const bool vec = ((reinterpret_cast<uintptr_t>(grad) | reinterpret_cast<uintptr_t>(P) |
+                     reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+  const int grid = min(ceil_div(M.total, vec ? 1024 : 256), kNumSMs * 8);
+  if (vec)
+    opt_from_grad_kernel<true><<<grid, 256, 0, stream>>>(M.total, grad, P, m, v, opt, lr, t, step);
+  else
+    opt_from_grad_kernel<false><<<grid, 256, 0, stream>>>(M.total, grad, P, m, v, opt, lr, t, step);
   TPCB_LAUNCH_CHECK("opt_from_grad");
   return TPCB_OK;
 }
@@ -324,8 +373,13 @@ int launch_transpose(const tpcb_model* m, const float* P, float* PT, cudaStream_
 
 int launch_optimizer(int n, const float* grad, float* P, float* m, float* v, const OptDev& opt,
                      double lr, double t, cudaStream_t stream) {
-  const int grid = min(ceil_div(n, 256), kNumSMs * 4);
-  optimizer_kernel<<<grid, 256, 0, stream>>>(n, grad, P, m, v, opt, lr, t);
+  const bool vec = ((reinterpret_cast<uintptr_t>(grad) | reinterpret_cast<uintptr_t>(P) |
+                     reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+  const int grid = min(ceil_div(n, vec ? 1024 : 256), kNumSMs * 8);
+  if (vec)
+    optimizer_kernel<true><<<grid, 256, 0, stream>>>(n, grad, P, m, v, opt, lr, t);
+  else
+    optimizer_kernel<false><<<grid, 256, 0, stream>>>(n, grad, P, m, v, opt, lr, t);
   TPCB_LAUNCH_CHECK("optimizer");
   return TPCB_OK;
 }

@@ -147,3 +147,31 @@ def test_adam_sgd_vs_reference():
     sgd.step(params, {n: g["g2." + n] for n in names}, 0.5)
     for n in names:
         np.testing.assert_allclose(params[n], g["sgd." + n], rtol=1e-5, atol=1e-6)
+
+
+def test_cmd_grid_kernels_vs_oracle_large_sets():
+    """cmd_between-sized sets take the multi-block kernels (tpcb_cmd_grid):
+    value and gradient vs the float64 oracle (itself pinned to the reference,
+    tests/test_oracle_golden.py), cmd(S, S) exactly 0, f32 input, ties in
+    the extrema routed to the first row."""
+    from oracle import moments as om
+    from paper_2311_09690_b200.costmodel import CMD_GRID_ROWS, cmd, cmd_grad
+    rng = np.random.default_rng(7)
+    ns, nt = 20000, 13001
+    assert ns + nt >= CMD_GRID_ROWS
+    zs = rng.normal(size=(ns, 32))
+    zt = rng.normal(0.2, 1.3, size=(nt, 32))
+    zs[5, 3] = zs[17, 3] = 9.0   # tie on the max: first row (5) carries the support grad
+    zt[100, 7] = -9.0
+    for k in (5, 3):
+        v, gs, gt = cmd_grad(zs, zt, k)
+        wv, wgs, wgt = om.cmd_grad(zs, zt, k)
+        assert v == pytest.approx(wv, rel=1e-11)
+        np.testing.assert_allclose(gs, wgs, rtol=1e-7, atol=1e-13)
+        np.testing.assert_allclose(gt, wgt, rtol=1e-7, atol=1e-13)
+    big = rng.normal(size=(CMD_GRID_ROWS, 32))
+    assert cmd(big, big.copy()) == 0.0
+    v32 = cmd(zs.astype(np.float32), zt.astype(np.float32))
+    w32 = om.cmd_grad(zs.astype(np.float32).astype(np.float64),
+                      zt.astype(np.float32).astype(np.float64), 5)[0]
+    assert v32 == pytest.approx(w32, rel=1e-11)
