@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kGridThreads) cmd_pass_a(const T* __restrict__
   for (int c = lane; c < g.de; c += 32) {
     double mn = INFINITY, mx = -INFINITY, sum = 0.0;
     int imn = 0x7fffffff, imx = 0x7fffffff;
-#pragma unroll 4
+#pragma unroll 8
     for (int r = r0 + w; r < r1; r += 8) {
       const double v = (double)Z[(size_t)r * g.de + c];
       argmin_merge(mn, imn, v, r);
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(kGridThreads) cmd_pass_c(const T* __restrict__
     for (int j = 0; j < kMaxCmdOrder; ++j) ps[j] = 0.0;
     if (c < g.de) {
       const double m = mu[c];
-#pragma unroll 4
+#pragma unroll 8
       for (int r = r0 + w; r < r1; r += 8) {
         const double cen = (double)Z[(size_t)r * g.de + c] - m;
         double pw = cen;
@@ -267,19 +267,32 @@ __global__ void __launch_bounds__(kGridThreads) cmd_pass_e(const T* __restrict__
   __syncthreads();
   const int total = (g.ns + g.nt) * de;  // < 2^31 (checked at launch)
   const bool de32 = de == 32;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const int row = de32 ? e >> 5 : e / de, c = de32 ? e & 31 : e - row * de;
-    const double* o = coef + (row < g.ns ? 0 : per_set);
-    const double cen = (double)Z[e] - o[c];
-    double gv = o[de + c];
-    double pw = 1.0;
-    for (int j = 2; j <= K; ++j) {
-      pw *= cen;
-      gv += o[(2 * (j - 1)) * de + c] * (pw - o[(2 * (j - 1) + 1) * de + c]);
+  const int stride = gridDim.x * blockDim.x;
+  constexpr int U = 4;  // elements in flight per thread
+  for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += U * stride) {
+    double z[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * stride;
+      z[u] = e < total ? (double)Z[e] : 0.0;
     }
-    if ((double)row == amax[c]) gv += ds[c];
-    if ((double)row == amin[c]) gv -= ds[c];
-    grad[e] = gv;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * stride;
+      if (e >= total) break;
+      const int row = de32 ? e >> 5 : e / de, c = de32 ? e & 31 : e - row * de;
+      const double* o = coef + (row < g.ns ? 0 : per_set);
+      const double cen = z[u] - o[c];
+      double gv = o[de + c];
+      double pw = 1.0;
+      for (int j = 2; j <= K; ++j) {
+        pw *= cen;
+        gv += o[(2 * (j - 1)) * de + c] * (pw - o[(2 * (j - 1) + 1) * de + c]);
+      }
+      if ((double)row == amax[c]) gv += ds[c];
+      if ((double)row == amin[c]) gv -= ds[c];
+      grad[e] = gv;
+    }
   }
 }
 

@@ -378,6 +378,8 @@ extern "C" int tpcb_featurize_pack(const void* d_vectors, int32_t vec_is_f64,
   int32_t* blk_base = blk_hist + (int64_t)nblk * (TPCB_MAX_LEAF + 1);
   int32_t* cnt = blk_base + (int64_t)nblk * (TPCB_MAX_LEAF + 1);
 
+  double* pe_table = reinterpret_cast<double*>(static_cast<char*>(d_ws) + pe_table_offset(nblk));
+  int32_t* row_tok = reinterpret_cast<int32_t*>(pe_table + kPeRows * TPCB_FEAT);
   bucket_count_kernel<<<nblk, kScatterBlock, 0, stream>>>(d_leaf_off, n_ast, n_leaf_max,
                                                           blk_hist, d_status);
   TPCB_LAUNCH_CHECK("bucket_count");
@@ -390,8 +392,6 @@ extern "C" int tpcb_featurize_pack(const void* d_vectors, int32_t vec_is_f64,
   TPCB_LAUNCH_CHECK("bucket_scatter");
   PeDenom den;
   for (int i = 0; i < TPCB_FEAT / 2; ++i) den.v[i] = pe_denom ? pe_denom[i] : 1.0;
-  double* pe_table = reinterpret_cast<double*>(static_cast<char*>(d_ws) + pe_table_offset(nblk));
-  int32_t* row_tok = reinterpret_cast<int32_t*>(pe_table + kPeRows * TPCB_FEAT);
   if (pe_denom) {
     pe_table_kernel<<<(kPeRows * (TPCB_FEAT / 2) + 255) / 256, 256, 0, stream>>>(den, pe_table);
     TPCB_LAUNCH_CHECK("pe_table");
