@@ -414,6 +414,9 @@ int tpcb_debug_train_trace(long long* d_trace);
 /* debug: training-kernel selection — 0 automatic (the desk fast path v4 where
  * the config matches, else the generic v2), 2 generic, 3 warp-group, 4 fast path */
 int tpcb_debug_train_impl(int32_t impl);
+/* debug: overlapped reduce + optimizer (the step's gradient reduction and Adam
+ * on the SMs the training kernel leaves idle, stage by stage): 1 on (default), 0 off */
+int tpcb_debug_overlap(int32_t on);
 /* debug: cap the training grid so CTAs loop over several samples (0 = no cap) */
 int tpcb_debug_grid_cap(int32_t cap);
 

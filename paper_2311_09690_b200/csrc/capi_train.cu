@@ -1,6 +1,7 @@
 // C ABI of the training path: single backward (costmodel.backward), the
 // optimizer (nn.Adam / nn.Sgd), and the native epoch loop (train/finetune
 // inner loops, costmodel.py:697-707 and :755-773).
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -94,6 +95,78 @@ struct StepProfiler {
 };
 thread_local StepProfiler* g_prof = nullptr;
 
+// overlapped reduce + optimizer (optim.cu): on by default, tpcb_debug_overlap
+int g_overlap = 1;
+
+struct SideStream {  // per device: the reduce branch of an overlapped step
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int sms = 0;
+};
+int side_stream(SideStream** out) {
+  thread_local SideStream per_dev[16];
+  int dev = 0;
+  TPCB_CUDA_CHECK(cudaGetDevice(&dev));
+  if (dev >= 16) return TPCB_ERR_UNSUPPORTED;
+  SideStream& s = per_dev[dev];
+  if (!s.side) {
+    TPCB_CUDA_CHECK(cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking));
+    TPCB_CUDA_CHECK(cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming));
+    TPCB_CUDA_CHECK(cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming));
+    TPCB_CUDA_CHECK(cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  *out = &s;
+  return TPCB_OK;
+}
+
+// Single GPU, no CMD, an optimizer, the desk fast-path kernel with one sample
+// per CTA: the reduce + optimizer of step k runs on the SMs the training
+// kernel leaves idle, each backward stage as soon as every CTA published it
+// (train4.cu stage_flags, optim.cu reduce_overlap_kernel).  Returns 1 when
+// the step was enqueued this way, 0 to use the sequential path.
+int try_overlapped_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
+                        const SampleSetDev& src, const SampleSetDev& tgt, const int32_t* batch,
+                        const StepDesc* steps, int step, int grid, const LossDev& loss,
+                        const OptDev& opt, const double* lr, const int64_t* t0,
+                        const TrainWs& ws, float* grad_out, double* step_loss, double* step_cmd,
+                        float* pred_out, int32_t* status, cudaStream_t stream, int* st_out) {
+  *st_out = TPCB_OK;
+  if (!g_overlap || loss.use_cmd || opt.kind == kOptNone || !t0 || g_grid_cap > 0) return 0;
+  if (!(g_train_impl == 0 || g_train_impl == 4) || !v4_fits(m->dev, ws.l_cap)) return 0;
+  SideStream* ss = nullptr;
+  if (side_stream(&ss)) return 0;
+  const int tgrid = std::max(1, std::min(grid, ws.n_slots));
+  const int rgrid = ss->sms - tgrid;  // the reduce never blocks the training CTAs' SMs
+  if (rgrid < 16) return 0;
+  OvlDev ov{};
+  if (overlap_sched(m, &ov) || ws.n_slots > ov.flag_stride) return 0;
+  TrainWs w2 = ws;
+  w2.stage_flags = ov.flags;
+  w2.t_tag = t0;
+  w2.flag_stride = ov.flag_stride;
+  int st = TPCB_OK;
+  auto fail = [&](int e) { *st_out = e; return 1; };
+  if (step == 0)  // tags are unique within a run; clear the previous run's
+    if (cudaMemsetAsync(ov.flags, 0, (size_t)ov.n_stages * ov.flag_stride * 8, stream))
+      return fail(TPCB_ERR_CUDA);
+  if (g_prof) g_prof->mark(stream);
+  if (cudaEventRecord(ss->fork, stream) || cudaStreamWaitEvent(ss->side, ss->fork, 0))
+    return fail(TPCB_ERR_CUDA);
+  st = launch_reduce_overlap(m->dev, w2, ov, steps, step, batch, src, grad_out, P, mb, vb, opt,
+                             lr, t0, loss, step_loss, step_cmd, status,
+                             std::min(rgrid, ov.n_items), ss->side);
+  if (st) return fail(st);
+  if (cudaEventRecord(ss->join, ss->side)) return fail(TPCB_ERR_CUDA);
+  st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 1, w2, pred_out,
+                    status, stream);
+  if (st) return fail(st);
+  if (g_prof) g_prof->mark(stream);
+  if (cudaStreamWaitEvent(stream, ss->join, 0)) return fail(TPCB_ERR_CUDA);
+  if (g_prof) g_prof->mark(stream);
+  if (g_prof) g_prof->mark(stream);
+  return 1;
+}
+
 // one training step on an already uploaded step table.  With a
 // communicator (data parallel): local fwd/bwd → local gradient sum into
 // `gbuf` → all-reduce(gradient, step loss) → optimizer from the gradient.
@@ -106,6 +179,13 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
   (void)PT;
   int st;
   const bool dp = comm != nullptr;  // (a 1-rank communicator exercises the same path)
+  if (!dp) {
+    int ost = TPCB_OK;
+    if (try_overlapped_step(m, P, PT, mb, vb, src, tgt, batch, steps, step, grid, loss, opt, lr,
+                            t0, ws, grad_out, step_loss, step_cmd, pred_out, status, stream,
+                            &ost))
+      return ost;
+  }
   if (g_prof) g_prof->mark(stream);
   if (loss.use_cmd) {
     if (dp) {  // every rank fills its own rows; the all-reduce assembles [zs; zt]
@@ -216,6 +296,12 @@ extern "C" int tpcb_optimizer_step(const tpcb_model* m, int64_t n, float* d_para
 
 namespace tpcb {
 int set_train_trace(long long* d_trace);
+}
+
+/* debug: overlapped reduce + optimizer on (1, default) / off (0) */
+extern "C" int tpcb_debug_overlap(int32_t on) {
+  g_overlap = on ? 1 : 0;
+  return TPCB_OK;
 }
 
 /* debug: training-kernel selection (0 automatic, 2 generic, 3 warp-group, 4 desk fast path) */

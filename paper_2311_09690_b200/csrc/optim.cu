@@ -10,7 +10,11 @@
 // HBM/L2-bound: per parameter it reads the gradient slots of the CTAs that
 // touched its region (bit mask per slot) in slot order, then reads/writes
 // p, m, v.  No float atomics anywhere, so a step is bitwise reproducible.
+#include <algorithm>
 #include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "train.cuh"
@@ -216,6 +220,208 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(
   }
 }
 
+// ---- overlapped reduce + optimizer ----------------------------------------
+// Runs concurrently with the training kernel on the SMs it leaves idle.  The
+// training CTAs publish, per backward stage, that their gradient slot holds
+// the stage's parameters (train4.cu, stage_flags); this kernel walks the
+// 256-parameter items in stage order, waits for a stage only when it reaches
+// its first item, and reduces + applies the optimizer exactly as
+// reduce_apply_kernel does (same slot order, same arithmetic: bitwise equal
+// results).  Untouched leaf_embed tensors (stage -1: gradient 0, Adam still
+// decays m / v and moves p) run while the forward is still in flight.
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// block-wide wait until every CTA c < n_cta published `tag` for stage q
+__device__ bool wait_stage(const OvlDev& ov, int q, int n_cta, unsigned long long tag,
+                           int32_t* status) {
+  __shared__ int s_ok;
+  if (threadIdx.x < 32) {
+    bool ok = false;
+    for (long it = 0; it < (1l << 22); ++it) {  // bounded (~1 s): a bug must not hang the GPU
+      bool mine = true;
+      for (int c = threadIdx.x; c < n_cta; c += 32)
+        mine &= ld_acquire_gpu(ov.flags + (size_t)q * ov.flag_stride + c) == tag;
+      if (__all_sync(0xffffffffu, mine)) { ok = true; break; }
+      __nanosleep(128);
+    }
+    if (threadIdx.x == 0) {
+      s_ok = ok;
+      if (!ok) raise_status(status, TPCB_ERR_CUDA);
+    }
+  }
+  __syncthreads();
+  return s_ok;
+}
+
+__global__ void __launch_bounds__(256) reduce_overlap_kernel(
+    const __grid_constant__ Model M, const float* __restrict__ partial, size_t stride,
+    const uint32_t* __restrict__ touched, const StepDesc* __restrict__ steps, int step,
+    const int32_t* __restrict__ batch_all, const int32_t* __restrict__ n_leaf, OvlDev ov,
+    const int64_t* __restrict__ t_p, float* __restrict__ grad_out, float* __restrict__ P,
+    float* __restrict__ mbuf, float* __restrict__ vbuf, OptDev opt,
+    const double* __restrict__ lr_p, const double* __restrict__ terms, LossDev loss,
+    double* __restrict__ step_loss, double* __restrict__ step_cmd, int32_t* status) {
+  __shared__ float4 s_part[4][64];
+  __shared__ float s_opt[3];
+  __shared__ uint32_t s_touch[1024];
+  __shared__ uint32_t s_and, s_or;
+  __shared__ int s_L;
+  const StepDesc sd = steps[step];
+  const int n_src = sd.n_src;
+  const int G = n_src;  // one CTA (gradient slot) per sample
+  const int col = threadIdx.x & 63, quarter = threadIdx.x >> 6;
+  const int n4 = M.total >> 2;
+  const size_t st4 = stride >> 2;
+  const unsigned long long tag = (unsigned long long)(__ldg(t_p) + step + 1);
+  const int final_stage = ov.n_stages - 1;
+  if (threadIdx.x == 0) {
+    const int32_t* batch = batch_all + sd.off;
+    int L = n_leaf[batch[0]];
+    for (int i = 1; i < n_src; ++i)
+      if (n_leaf[batch[i]] != L) L = 0;  // mixed leaf counts: everything at the final stage
+    s_L = (L >= 1 && L <= ov.n_leaf_max) ? L : 0;
+    float lr = 0.f, bc1 = 1.f, bc2 = 1.f;
+    if (opt.kind != kOptNone) {
+      lr = (float)__ldg(lr_p);
+      if (opt.kind == kOptAdam) {
+        const double t = (double)(__ldg(t_p) + step + 1);
+        bc1 = (float)(1.0 - pow(opt.beta1, t));
+        bc2 = (float)(1.0 - pow(opt.beta2, t));
+      }
+    }
+    s_opt[0] = lr;
+    s_opt[1] = bc1;
+    s_opt[2] = bc2;
+  }
+  __syncthreads();
+  const int L = s_L;
+  const bool mixed = L == 0;
+  const int32_t* order = ov.order + (size_t)L * ov.n_items;
+  const int8_t* stage_of = ov.stage + (size_t)L * ov.n_items;
+  const float lr = s_opt[0], bc1 = s_opt[1], bc2 = s_opt[2];
+  int ready = -1;  // highest stage known complete on every CTA
+  for (int k = blockIdx.x; k < ov.n_items; k += gridDim.x) {
+    const int item = order[k];
+    const int stg = stage_of[item];
+    if (stg > ready) {
+      wait_stage(ov, stg, G, tag, status);
+      ready = stg;
+      if (mixed && threadIdx.x < 32) {  // slot masks (written before the final stage)
+        uint32_t a = ~0u, o = 0u;
+        for (int c = threadIdx.x; c < G; c += 32) {
+          const uint32_t t = __ldcg(touched + c);
+          s_touch[c] = t;
+          a &= t;
+          o |= t;
+        }
+#pragma unroll
+        for (int d = 16; d; d >>= 1) {
+          a &= __shfl_xor_sync(0xffffffffu, a, d);
+          o |= __shfl_xor_sync(0xffffffffu, o, d);
+        }
+        if (threadIdx.x == 0) {
+          s_and = G > 0 ? a : 0u;
+          s_or = o;
+        }
+      }
+      __syncthreads();
+    }
+    const int base = item * 64;
+    const int pp = base * 4 + threadIdx.x;
+    const bool pv = pp < M.total && opt.kind != kOptNone;
+    float w = 0.f, m = 0.f, v = 0.f;
+    if (pv) {
+      w = P[pp];
+      if (opt.kind == kOptAdam) {
+        m = mbuf[pp];
+        v = vbuf[pp];
+      }
+    }
+    const int q = base + col;
+    const bool qv = q < n4;
+    const int p = q << 2;
+    const int per_q = (G + 3) >> 2;
+    const int c_lo = min(G, quarter * per_q), c_hi = min(G, c_lo + per_q);
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool all_slots = false, some = false;
+    uint32_t want = 0;
+    if (!mixed) {
+      all_slots = stg >= 0;  // single bucket: every slot touched exactly these regions
+      some = all_slots;
+    } else if (qv) {
+      want = 1u << region_bit(M, p, s_leaf_of(M));
+      all_slots = (s_and & want) != 0;
+      some = (s_or & want) != 0;
+    }
+    if (qv && some) {
+      const float4* src = reinterpret_cast<const float4*>(partial + p) + (size_t)c_lo * st4;
+      const int n = c_hi - c_lo;
+      if (all_slots) {
+        int c = 0;
+        for (; c + 8 <= n; c += 8) {
+          float4 x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) x[u] = __ldcg(src + (size_t)(c + u) * st4);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            g.x += x[u].x; g.y += x[u].y; g.z += x[u].z; g.w += x[u].w;
+          }
+        }
+        for (; c < n; ++c) {
+          const float4 x = __ldcg(src + (size_t)c * st4);
+          g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
+        }
+      } else {
+        for (int c = 0; c < n; ++c) {
+          if (s_touch[c_lo + c] & want) {
+            const float4 x = __ldcg(src + (size_t)c * st4);
+            g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
+          }
+        }
+      }
+    }
+    s_part[quarter][col] = g;
+    __syncthreads();
+    if (pp < M.total) {
+      const int cc = threadIdx.x >> 2, comp = threadIdx.x & 3;
+      const float* part = reinterpret_cast<const float*>(s_part);
+      float gs = part[(0 * 64 + cc) * 4 + comp];
+      gs += part[(1 * 64 + cc) * 4 + comp];
+      gs += part[(2 * 64 + cc) * 4 + comp];
+      gs += part[(3 * 64 + cc) * 4 + comp];
+      apply1(pp, gs, w, m, v, grad_out, P, mbuf, vbuf, opt, lr, bc1, bc2);
+    }
+    __syncthreads();
+  }
+  // loss value of the step (fixed order), costmodel.py:539-550; terms are
+  // written before stage 0
+  if (blockIdx.x == 0) {
+    if (ready < 0) wait_stage(ov, 0, G, tag, status);
+    if (threadIdx.x < 32) {
+      double sq = 0.0, rel = 0.0;
+      for (int i = threadIdx.x; i < n_src; i += 32) {
+        sq += __ldcg(terms + 2 * i);
+        rel += __ldcg(terms + 2 * i + 1);
+      }
+      sq = warp_sum_d(sq);
+      rel = warp_sum_d(rel);
+      if (threadIdx.x == 0 && step_loss) {
+        const double n = (double)sd.n_norm;
+        const double val = loss.mode == kLossMse ? sq / n
+                           : loss.mode == kLossMape ? rel / n
+                                                    : sq / n + loss.lambda * (rel / n);
+        step_loss[step] = val;
+        if (step_cmd) step_cmd[step] = 0.0;
+      }
+    }
+  }
+  (void)final_stage;
+}
+
 // one parameter of Adam / SGD (nn.py:136-167), fp32, oracle operation order
 struct OptScalars {
   float lr, bc1, bc2, b1, b2, eps, wd, omb1, omb2;
@@ -381,6 +587,115 @@ int launch_optimizer(int n, const float* grad, float* P, float* m, float* v, con
   else
     optimizer_kernel<false><<<grid, 256, 0, stream>>>(n, grad, P, m, v, opt, lr, t);
   TPCB_LAUNCH_CHECK("optimizer");
+  return TPCB_OK;
+}
+
+
+// ---- overlapped reduce: host schedule + launch -----------------------------
+namespace {
+struct OvlCache {
+  int device;
+  Model key;
+  OvlDev dev;
+};
+std::vector<OvlCache>& ovl_cache() {
+  static std::vector<OvlCache> c;
+  return c;
+}
+std::mutex& ovl_mu() {
+  static std::mutex mu;
+  return mu;
+}
+}  // namespace
+
+int overlap_sched(const tpcb_model* m, OvlDev* out) {
+  const Model& M = m->dev;
+  int dev = 0;
+  TPCB_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(ovl_mu());
+  for (auto& e : ovl_cache())
+    if (e.device == dev && memcmp(&e.key, &M, sizeof(Model)) == 0) {
+      *out = e.dev;
+      return TPCB_OK;
+    }
+  const int n4 = M.total >> 2;
+  const int n_items = (n4 + 63) / 64;
+  const int nl = M.n_leaf_max;
+  const int n_stages = 2 + 2 * M.n_layers;
+  const int final_stage = n_stages - 1;
+  // stage of every parameter for batch leaf count L (tensor names, costmodel.py:116-150)
+  std::vector<int8_t> pstage_base(M.total, 0);
+  std::vector<int> leaf_of(M.total, 0);
+  for (const TensorInfo& t : m->tensors) {
+    const int64_t size = (int64_t)t.rows * (t.cols ? t.cols : 1);
+    int st = 0, leaf = 0;
+    if (t.name.rfind("input.", 0) == 0) {
+      st = final_stage;
+    } else if (t.name.rfind("enc", 0) == 0) {
+      const int li = atoi(t.name.c_str() + 3);
+      const bool attn = t.name.find(".attn.") != std::string::npos ||
+                        t.name.find(".ln1.") != std::string::npos;
+      st = (attn ? 2 : 1) + 2 * (M.n_layers - 1 - li);
+    } else if (t.name.rfind("leaf_embed.", 0) == 0) {
+      leaf = atoi(t.name.c_str() + 11);
+    }
+    for (int64_t i = 0; i < size; ++i) {
+      pstage_base[t.offset + i] = (int8_t)st;
+      leaf_of[t.offset + i] = leaf;
+    }
+  }
+  std::vector<int32_t> order((size_t)(nl + 1) * n_items);
+  std::vector<int8_t> stage((size_t)(nl + 1) * n_items);
+  for (int L = 0; L <= nl; ++L) {
+    for (int it = 0; it < n_items; ++it) {
+      int st = -1;
+      const int p0 = it * 256, p1 = std::min<int>(M.total, p0 + 256);
+      for (int p = p0; p < p1; ++p) {
+        int sp = pstage_base[p];
+        if (leaf_of[p]) sp = (L == 0) ? final_stage : (leaf_of[p] == L ? 0 : -1);
+        if (L == 0) sp = final_stage;
+        st = std::max(st, sp);
+      }
+      stage[(size_t)L * n_items + it] = (int8_t)st;
+    }
+    int32_t* o = order.data() + (size_t)L * n_items;
+    for (int it = 0; it < n_items; ++it) o[it] = it;
+    const int8_t* sg = stage.data() + (size_t)L * n_items;
+    std::stable_sort(o, o + n_items, [&](int a, int b) { return sg[a] < sg[b]; });
+  }
+  OvlDev d{};
+  d.n_items = n_items;
+  d.n_stages = n_stages;
+  d.flag_stride = 1024;  // >= n_slots (tpcb_train_ws_sizes caps slots at 1024)
+  d.n_leaf_max = nl;
+  int32_t* d_order = nullptr;
+  int8_t* d_stage = nullptr;
+  unsigned long long* d_flags = nullptr;
+  TPCB_CUDA_CHECK(cudaMalloc(&d_order, order.size() * sizeof(int32_t)));
+  TPCB_CUDA_CHECK(cudaMalloc(&d_stage, stage.size()));
+  TPCB_CUDA_CHECK(cudaMalloc(&d_flags, (size_t)n_stages * d.flag_stride * 8));
+  TPCB_CUDA_CHECK(cudaMemcpy(d_order, order.data(), order.size() * 4, cudaMemcpyHostToDevice));
+  TPCB_CUDA_CHECK(cudaMemcpy(d_stage, stage.data(), stage.size(), cudaMemcpyHostToDevice));
+  TPCB_CUDA_CHECK(cudaMemset(d_flags, 0, (size_t)n_stages * d.flag_stride * 8));
+  d.order = d_order;
+  d.stage = d_stage;
+  d.flags = d_flags;
+  ovl_cache().push_back(OvlCache{dev, M, d});
+  *out = d;
+  return TPCB_OK;
+}
+
+int launch_reduce_overlap(const Model& M, const TrainWs& ws, const OvlDev& ov,
+                          const StepDesc* steps, int step, const int32_t* batch,
+                          const SampleSetDev& src, float* grad_out, float* P, float* m, float* v,
+                          const OptDev& opt, const double* lr, const int64_t* t,
+                          const LossDev& loss, double* step_loss, double* step_cmd,
+                          int32_t* status, int grid, cudaStream_t stream) {
+  reduce_overlap_kernel<<<grid, 256, 0, stream>>>(M, ws.partial, ws.slot_stride, ws.touched,
+                                                  steps, step, batch, src.n_leaf, ov, t,
+                                                  grad_out, P, m, v, opt, lr, ws.terms, loss,
+                                                  step_loss, step_cmd, status);
+  TPCB_LAUNCH_CHECK("reduce_overlap");
   return TPCB_OK;
 }
 

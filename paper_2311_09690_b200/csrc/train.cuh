@@ -121,7 +121,32 @@ struct TrainWs {
   double* scalars;     // [8] cmd value, loss value, ...
   size_t zall_bytes;   // size of zall (zeroed before phase 0 under data parallelism)
   int l_cap;           // largest leaf count of any sample (sizes the smem plan)
+  // overlapped reduce (optim.cu): per-CTA stage completion tags written by the
+  // training kernel's producer warp; nullptr = off
+  unsigned long long* stage_flags = nullptr;
+  const int64_t* t_tag = nullptr;  // tag of step s = t_tag[0] + s + 1
+  int flag_stride = 0;
 };
+
+// Overlapped gradient reduction + optimizer (single GPU, no CMD): the items
+// of 256 parameters sorted, per batch leaf count L, by the backward stage
+// after which every CTA has written their gradients (stage -1: leaf_embed of
+// other leaf counts, never touched; row L = 0: mixed batches, every item at
+// the final stage).
+struct OvlDev {
+  const int32_t* order;       // [(n_leaf_max + 1) * n_items]
+  const int8_t* stage;        // [(n_leaf_max + 1) * n_items]
+  unsigned long long* flags;  // [n_stages * flag_stride]
+  int n_items, n_stages, flag_stride, n_leaf_max;
+};
+// schedule of a model (built once per parameter layout, cached per device)
+int overlap_sched(const tpcb_model* m, OvlDev* out);
+int launch_reduce_overlap(const Model& M, const TrainWs& ws, const OvlDev& ov,
+                          const StepDesc* steps, int step, const int32_t* batch,
+                          const SampleSetDev& src, float* grad_out, float* P, float* m, float* v,
+                          const OptDev& opt, const double* lr, const int64_t* t,
+                          const LossDev& loss, double* step_loss, double* step_cmd,
+                          int32_t* status, int grid, cudaStream_t stream);
 
 // steps[s] = {offset of step s in batch, n_src, n_tgt, 0}; batch holds the
 // source sample indices of the step followed by its target sample indices.

@@ -55,6 +55,7 @@ constexpr int NW = 8;              // compute warps
 constexpr int NT = NW * 32;        // compute threads
 constexpr int kThreads4 = NT + 32; // + producer warp
 constexpr int kBar = 1;            // named barrier of the compute warps
+constexpr int kStages4 = 2 + 2 * NLAY;  // backward stages published to the overlapped reduce
 
 constexpr int LDH = 68;   // 64-wide activation rows
 constexpr int LDQ = 196;  // Q|K|V rows
@@ -84,6 +85,9 @@ constexpr int SV_OUTB = SV_OUTW + DEC;
 constexpr int SV_TOTAL = SV_OUTB + 4;
 
 __device__ __forceinline__ void cbar() { group_bar(kBar, NT); }
+__device__ __forceinline__ void st_relaxed_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
@@ -817,14 +821,16 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
     const __grid_constant__ TmaMaps maps,
     float* __restrict__ zall, float* __restrict__ partial, size_t slot_stride,
     uint32_t* __restrict__ touched, double* __restrict__ terms, double* __restrict__ scalars,
-    float* __restrict__ pred_out, int32_t* status) {
+    float* __restrict__ pred_out, int32_t* status, unsigned long long* __restrict__ stage_flags,
+    const int64_t* __restrict__ t_tag, int flag_stride) {
   extern __shared__ __align__(1024) float sm[];
-  __shared__ __align__(8) uint64_t bars[20];
+  __shared__ __align__(8) uint64_t bars[20 + kStages4];
   const int NS = tp.NS;
   uint64_t* full = bars;
   uint64_t* empty = bars + 8;
   uint64_t* svbar = bars + 16;  // small vectors landed
   uint64_t* xfull = bars + 17;  // [2] input rows of the current sample landed
+  uint64_t* stage_bar = bars + 20;  // [kStages4] backward stage written (overlapped reduce)
   const StepDesc sd = steps[step];
   const int32_t* batch = batch_all + sd.off;
   const int n_src = sd.n_src, n_tgt = sd.n_tgt;
@@ -839,6 +845,7 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
     mbar_init(svbar, 1);
     mbar_init(&xfull[0], 1);
     mbar_init(&xfull[1], 1);
+    for (int q = 0; q < kStages4; ++q) mbar_init(&stage_bar[q], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -858,12 +865,26 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
       const int d = sv_item(M, lane, &off, &n);
       bulk_g2s(SV + d, Pw + off, (uint32_t)(n * 4), svbar);
     }
+    // Overlapped reduce: once the compute warps have written a backward
+    // stage's gradients (stage_bar[q]), publish this CTA's tag for it —
+    // gpu-scope release by the producer lane, off the compute critical path.
+    int next_stage = 0, had_sample = 0;
+    const unsigned long long tag = stage_flags ? (unsigned long long)(t_tag[0] + step + 1) : 0ull;
+    auto publish = [&](bool block) {
+      while (next_stage < kStages4 && (block ? (mbar_wait(&stage_bar[next_stage], 0), true)
+                                             : mbar_try_wait(&stage_bar[next_stage], 0))) {
+        __threadfence();
+        st_relaxed_gpu(stage_flags + (size_t)next_stage * flag_stride + blockIdx.x, tag);
+        ++next_stage;
+      }
+    };
     int s = 0, ph = 0, J = 0, xs = 0;
     for (int w = blockIdx.x; w < n_all; w += gridDim.x) {
       const SampleSetDev set = w >= n_src ? tgt : src;
       const int idx = batch[w];
       const int L = set.n_leaf[idx];
       if (L < 1 || L > tp.R) continue;  // the compute warps skip it too
+      had_sample = 1;
       if (lane == 0) {  // the sample's packed input rows (contiguous, 128 B each)
         const int b = xs & 1;
         mbar_arrive_expect_tx(&xfull[b], (uint32_t)(L * LDX * 4));
@@ -873,6 +894,7 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
       ++xs;
       const int n_slots = phase == 0 ? n_fwd_slots(L, false) : n_all_slots(L);
       for (int j = 0; j < n_slots; ++j, ++J) {
+        if (stage_flags && lane == 0) publish(false);
         if (J >= NS) mbar_wait(&empty[s], ph ^ 1);
         const SlotLoad x = stream_slot(M, L, j);
         float* dst = ring + s * kSlot;
@@ -890,6 +912,7 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
         if (++s == NS) { s = 0; ph ^= 1; }
       }
     }
+    if (stage_flags && lane == 0 && had_sample) publish(true);
     return;
   }
 
@@ -925,6 +948,9 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
   float* red = sm + tp.red;
   float* misc = sm + tp.misc;
   double* cmds = reinterpret_cast<double*>(sm + tp.cmd);
+  auto stage_done = [&](int q) {  // all compute warps passed cbar() after the stage's writes
+    if (stage_flags && threadIdx.x == 0) mbar_arrive(&stage_bar[q]);
+  };
   long long* trace = g_trace4;
   Stream4 ws{ring, full, empty, NS, 0, 0,
              (trace != nullptr && blockIdx.x == 0 && threadIdx.x == 0) ? trace : nullptr, 0};
@@ -1213,6 +1239,7 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
       colsum(dzv, 0, nullptr, 0, 1, DDEV, G + M.devhb, fs, NT - DDEV);
     }
     cbar();
+    stage_done(0);  // head, decoder, leaf_embed.L, device MLP (+ loss terms)
     PT(59);
     for (int li = NLAY - 1; li >= 0; --li) {
       const LayerOff& lo = M.layer[li];
@@ -1255,6 +1282,7 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
         PT(60 + (NLAY - 1 - li) * 30 + 8);
       }
       cbar();
+      stage_done(1 + 2 * (NLAY - 1 - li));  // layer li: ffn + LayerNorm-2
       PT(60 + (NLAY - 1 - li) * 30 + 9);
       {  // B3: dC = dA·Woᵀ; dW_o, bo, ln1 g/b
         const float* W = ws.acquire();
@@ -1304,6 +1332,7 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
         PT(60 + (NLAY - 1 - li) * 30 + 22);
       }
       cbar();
+      stage_done(2 + 2 * (NLAY - 1 - li));  // layer li: attention + LayerNorm-1
       PT(60 + (NLAY - 1 - li) * 30 + 23);
     }
     wgrad(X0, LDX, nullptr, nullptr, dH, LDH, L, FEAT, D, G + M.inW, fs);
@@ -1314,6 +1343,7 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
     if (ws.trace) ws.trace[511] = clock64();
   }
   if (threadIdx.x == 0) touched[blockIdx.x] = mask;
+  stage_done(kStages4 - 1);  // input projection, touched mask
 }
 
 }  // namespace
@@ -1420,7 +1450,8 @@ int launch_train4(const Model& M, const float* P, const SampleSetDev& src, const
   train4_kernel<<<grid, kThreads4, smem, stream>>>(M, P, src, tgt, batch, steps, step, loss, phase,
                                                    tp, maps, ws.zall, ws.partial, ws.slot_stride,
                                                    ws.touched, ws.terms, ws.scalars, pred_out,
-                                                   status);
+                                                   status, ws.stage_flags, ws.t_tag,
+                                                   ws.flag_stride);
   TPCB_LAUNCH_CHECK("train4_kernel");
   return TPCB_OK;
 }
