@@ -296,6 +296,10 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     lib = _lib.load()
     cfg = pb.desk_config(seed=0, batch_size=args.batch_size)
+    from paper_2311_09690_b200 import _lib as _l
+    _l.load().tpcb_debug_overlap(int(args.overlap))
+    if args.poll_ns:
+        _l.load().tpcb_debug_poll_ns(int(args.poll_ns))
     data, train, valid = make_data()
     norm = fit_boxcox(train.latency)
     targets = norm.encode(train.latency)
@@ -482,6 +486,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true",
                     help="skip the full_reference_config training/inference block")
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="1: reduce + Adam of each step overlapped with its backward (default); "
+                         "0: sequential reduce kernel (A/B)")
+    ap.add_argument("--poll-ns", type=int, default=0, help="debug: stage-wait poll interval")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -415,8 +415,12 @@ int tpcb_debug_train_trace(long long* d_trace);
  * the config matches, else the generic v2), 2 generic, 3 warp-group, 4 fast path */
 int tpcb_debug_train_impl(int32_t impl);
 /* debug: overlapped reduce + optimizer (the step's gradient reduction and Adam
- * on the SMs the training kernel leaves idle, stage by stage): 1 on (default), 0 off */
+ * on the SMs the training kernel leaves idle, stage by stage): 1 on (default),
+ * 0 off (sequential reduce kernel), 2 stage publishing on but the reduce
+ * sequential (overhead A/B), >= 16 on with at most that many reduce blocks */
 int tpcb_debug_overlap(int32_t on);
+/* debug: poll interval (ns) of the overlapped reduce's stage waits (default 512) */
+int tpcb_debug_poll_ns(int32_t ns);
 /* debug: cap the training grid so CTAs loop over several samples (0 = no cap) */
 int tpcb_debug_grid_cap(int32_t cap);
 

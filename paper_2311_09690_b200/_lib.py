@@ -126,6 +126,7 @@ SIGNATURES = {
     "tpcb_debug_train_impl": (i32, [i32]),
     "tpcb_debug_grid_cap": (i32, [i32]),
     "tpcb_debug_overlap": (i32, [i32]),
+    "tpcb_debug_poll_ns": (i32, [i32]),
     "tpcb_kmeans_ws_size": (i32, [i64, i32, i32, C.POINTER(sz)]),
     "tpcb_kmeanspp_init": (i32, [vp, i64, i32, i64, vp, vp, vp, vp, sz, vp]),
     "tpcb_kmeanspp_step": (i32, [vp, i64, i32, i32, f64, i64, vp, vp, vp, vp, vp, sz, vp]),

@@ -149,12 +149,26 @@ int try_overlapped_step(const tpcb_model* m, float* P, float* PT, float* mb, flo
   if (step == 0)  // tags are unique within a run; clear the previous run's
     if (cudaMemsetAsync(ov.flags, 0, (size_t)ov.n_stages * ov.flag_stride * 8, stream))
       return fail(TPCB_ERR_CUDA);
+  if (g_overlap == 2) {  // debug A/B: stage publishing on, reduce sequential afterwards
+    if (g_prof) g_prof->mark(stream);
+    st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 1, w2, pred_out,
+                      status, stream);
+    if (st) return fail(st);
+    if (g_prof) g_prof->mark(stream);
+    st = launch_reduce_apply(m->dev, ws, steps, step, 0, 1, grad_out, P, mb, vb, opt, lr, t0,
+                             loss, step_loss, step_cmd, stream);
+    if (st) return fail(st);
+    if (g_prof) g_prof->mark(stream);
+    if (g_prof) g_prof->mark(stream);
+    return 1;
+  }
   if (g_prof) g_prof->mark(stream);
   if (cudaEventRecord(ss->fork, stream) || cudaStreamWaitEvent(ss->side, ss->fork, 0))
     return fail(TPCB_ERR_CUDA);
   st = launch_reduce_overlap(m->dev, w2, ov, steps, step, batch, src, grad_out, P, mb, vb, opt,
                              lr, t0, loss, step_loss, step_cmd, status,
-                             std::min(rgrid, ov.n_items), ss->side);
+                             std::min(g_overlap >= 16 ? std::min(g_overlap, rgrid) : rgrid,
+                                      ov.n_items), ss->side);
   if (st) return fail(st);
   if (cudaEventRecord(ss->join, ss->side)) return fail(TPCB_ERR_CUDA);
   st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 1, w2, pred_out,
@@ -300,8 +314,14 @@ int set_train_trace(long long* d_trace);
 
 /* debug: overlapped reduce + optimizer on (1, default) / off (0) */
 extern "C" int tpcb_debug_overlap(int32_t on) {
-  g_overlap = on ? 1 : 0;
+  g_overlap = on;
   return TPCB_OK;
+}
+
+/* debug: poll interval (ns) of the overlapped reduce's stage waits */
+extern "C" int tpcb_debug_poll_ns(int32_t ns) {
+  if (ns < 0) return TPCB_ERR_VALIDATION;
+  return set_poll_ns((unsigned)ns);
 }
 
 /* debug: training-kernel selection (0 automatic, 2 generic, 3 warp-group, 4 desk fast path) */
@@ -426,6 +446,15 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
     }
     st = prepare_train_kernels(m->dev, ws->l_cap);  // attributes are set outside capture
     if (st) return st;
+    {  // the overlapped reduce's schedule / side stream are allocated outside capture too
+      OvlDev ov{};
+      SideStream* ss = nullptr;
+      if (g_overlap && !comm) {
+        st = overlap_sched(m, &ov);
+        if (!st) st = side_stream(&ss);
+        if (st) return st;
+      }
+    }
     TPCB_CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     st = enqueue();
     cudaGraph_t g = nullptr;

@@ -235,23 +235,26 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
   return v;
 }
 
-// block-wide wait until every CTA c < n_cta published `tag` for stage q
-__device__ bool wait_stage(const OvlDev& ov, int q, int n_cta, unsigned long long tag,
-                           int32_t* status) {
+__constant__ unsigned kPollNsC = 256;
+#define kPollNs kPollNsC
+// block-wide wait until the training CTAs of this step (and of every earlier
+// step of the epoch) counted themselves into stage q's word (train4.cu): the
+// word must reach `target` = samples of steps first..this.  A poll is one L2
+// request by one lane.
+__device__ bool wait_stage(const OvlDev& ov, int q, unsigned long long target, int32_t* status) {
   __shared__ int s_ok;
-  if (threadIdx.x < 32) {
+  if (threadIdx.x == 0) {
+    const unsigned long long* f = ov.flags + (size_t)q * ov.flag_stride;
     bool ok = false;
-    for (long it = 0; it < (1l << 22); ++it) {  // bounded (~1 s): a bug must not hang the GPU
-      bool mine = true;
-      for (int c = threadIdx.x; c < n_cta; c += 32)
-        mine &= ld_acquire_gpu(ov.flags + (size_t)q * ov.flag_stride + c) == tag;
-      if (__all_sync(0xffffffffu, mine)) { ok = true; break; }
-      __nanosleep(128);
+    for (long it = 0; it < (1l << 21); ++it) {  // bounded (~1 s): a bug must not hang the GPU
+      if (ld_acquire_gpu(f) >= target) {
+        ok = true;
+        break;
+      }
+      __nanosleep(kPollNs);
     }
-    if (threadIdx.x == 0) {
-      s_ok = ok;
-      if (!ok) raise_status(status, TPCB_ERR_CUDA);
-    }
+    s_ok = ok;
+    if (!ok) raise_status(status, TPCB_ERR_CUDA);
   }
   __syncthreads();
   return s_ok;
@@ -276,7 +279,8 @@ __global__ void __launch_bounds__(256) reduce_overlap_kernel(
   const int col = threadIdx.x & 63, quarter = threadIdx.x >> 6;
   const int n4 = M.total >> 2;
   const size_t st4 = stride >> 2;
-  const unsigned long long tag = (unsigned long long)(__ldg(t_p) + step + 1);
+  // cumulative CTA count the stage words reach at the end of this step
+  const unsigned long long target = (unsigned long long)(sd.off - steps[0].off + n_src);
   const int final_stage = ov.n_stages - 1;
   if (threadIdx.x == 0) {
     const int32_t* batch = batch_all + sd.off;
@@ -308,7 +312,7 @@ __global__ void __launch_bounds__(256) reduce_overlap_kernel(
     const int item = order[k];
     const int stg = stage_of[item];
     if (stg > ready) {
-      wait_stage(ov, stg, G, tag, status);
+      wait_stage(ov, stg, target, status);
       ready = stg;
       if (mixed && threadIdx.x < 32) {  // slot masks (written before the final stage)
         uint32_t a = ~0u, o = 0u;
@@ -349,9 +353,11 @@ __global__ void __launch_bounds__(256) reduce_overlap_kernel(
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
     bool all_slots = false, some = false;
     uint32_t want = 0;
-    if (!mixed) {
-      all_slots = stg >= 0;  // single bucket: every slot touched exactly these regions
-      some = all_slots;
+    if (!mixed) {  // single bucket: every slot touched the shared region and leaf_embed.L only
+      if (qv) {
+        const int rb = region_bit(M, p, s_leaf_of(M));
+        all_slots = some = (rb == 0 || rb == L);
+      }
     } else if (qv) {
       want = 1u << region_bit(M, p, s_leaf_of(M));
       all_slots = (s_and & want) != 0;
@@ -400,7 +406,7 @@ __global__ void __launch_bounds__(256) reduce_overlap_kernel(
   // loss value of the step (fixed order), costmodel.py:539-550; terms are
   // written before stage 0
   if (blockIdx.x == 0) {
-    if (ready < 0) wait_stage(ov, 0, G, tag, status);
+    if (ready < 0) wait_stage(ov, 0, target, status);
     if (threadIdx.x < 32) {
       double sq = 0.0, rel = 0.0;
       for (int i = threadIdx.x; i < n_src; i += 32) {
@@ -607,6 +613,11 @@ std::mutex& ovl_mu() {
   return mu;
 }
 }  // namespace
+
+int set_poll_ns(unsigned ns) {
+  TPCB_CUDA_CHECK(cudaMemcpyToSymbol(kPollNsC, &ns, sizeof(ns)));
+  return TPCB_OK;
+}
 
 int overlap_sched(const tpcb_model* m, OvlDev* out) {
   const Model& M = m->dev;

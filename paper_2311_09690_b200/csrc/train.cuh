@@ -141,6 +141,7 @@ struct OvlDev {
 };
 // schedule of a model (built once per parameter layout, cached per device)
 int overlap_sched(const tpcb_model* m, OvlDev* out);
+int set_poll_ns(unsigned ns);  // stage-wait poll interval of the overlapped reduce
 int launch_reduce_overlap(const Model& M, const TrainWs& ws, const OvlDev& ov,
                           const StepDesc* steps, int step, const int32_t* batch,
                           const SampleSetDev& src, float* grad_out, float* P, float* m, float* v,

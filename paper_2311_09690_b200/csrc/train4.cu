@@ -53,7 +53,7 @@ constexpr int RMAX = 16;
 
 constexpr int NW = 8;              // compute warps
 constexpr int NT = NW * 32;        // compute threads
-constexpr int kThreads4 = NT + 32; // + producer warp
+constexpr int kThreads4 = NT + 64; // + producer warp + stage publisher warp
 constexpr int kBar = 1;            // named barrier of the compute warps
 constexpr int kStages4 = 2 + 2 * NLAY;  // backward stages published to the overlapped reduce
 
@@ -865,26 +865,12 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
       const int d = sv_item(M, lane, &off, &n);
       bulk_g2s(SV + d, Pw + off, (uint32_t)(n * 4), svbar);
     }
-    // Overlapped reduce: once the compute warps have written a backward
-    // stage's gradients (stage_bar[q]), publish this CTA's tag for it —
-    // gpu-scope release by the producer lane, off the compute critical path.
-    int next_stage = 0, had_sample = 0;
-    const unsigned long long tag = stage_flags ? (unsigned long long)(t_tag[0] + step + 1) : 0ull;
-    auto publish = [&](bool block) {
-      while (next_stage < kStages4 && (block ? (mbar_wait(&stage_bar[next_stage], 0), true)
-                                             : mbar_try_wait(&stage_bar[next_stage], 0))) {
-        __threadfence();
-        st_relaxed_gpu(stage_flags + (size_t)next_stage * flag_stride + blockIdx.x, tag);
-        ++next_stage;
-      }
-    };
     int s = 0, ph = 0, J = 0, xs = 0;
     for (int w = blockIdx.x; w < n_all; w += gridDim.x) {
       const SampleSetDev set = w >= n_src ? tgt : src;
       const int idx = batch[w];
       const int L = set.n_leaf[idx];
       if (L < 1 || L > tp.R) continue;  // the compute warps skip it too
-      had_sample = 1;
       if (lane == 0) {  // the sample's packed input rows (contiguous, 128 B each)
         const int b = xs & 1;
         mbar_arrive_expect_tx(&xfull[b], (uint32_t)(L * LDX * 4));
@@ -894,7 +880,6 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
       ++xs;
       const int n_slots = phase == 0 ? n_fwd_slots(L, false) : n_all_slots(L);
       for (int j = 0; j < n_slots; ++j, ++J) {
-        if (stage_flags && lane == 0) publish(false);
         if (J >= NS) mbar_wait(&empty[s], ph ^ 1);
         const SlotLoad x = stream_slot(M, L, j);
         float* dst = ring + s * kSlot;
@@ -912,7 +897,26 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
         if (++s == NS) { s = 0; ph ^= 1; }
       }
     }
-    if (stage_flags && lane == 0 && had_sample) publish(true);
+    return;
+  }
+  // ============================================ stage publisher (one lane)
+  // Overlapped reduce: once the compute warps have written a backward stage's
+  // gradients (stage_bar[q]), count this CTA into the stage's word after a
+  // gpu-scope fence — a warp of its own, so neither the weight stream nor the
+  // compute warps wait on the fence.  The words count CTAs cumulatively over
+  // the steps of an epoch (zeroed at its first step).
+  if (warp == NW + 1) {
+    if (!stage_flags || lane != 0 || (int)blockIdx.x >= n_all) return;
+    const int w = blockIdx.x;  // one sample per CTA on this path
+    const SampleSetDev set = w >= n_src ? tgt : src;
+    const int L = set.n_leaf[batch[w]];
+    if (L < 1 || L > tp.R) return;
+    (void)t_tag;
+    for (int q = 0; q < kStages4; ++q) {
+      mbar_wait(&stage_bar[q], 0);
+      __threadfence();
+      atomicAdd(stage_flags + (size_t)q * flag_stride, 1ull);  // one L2 atomic, never retried
+    }
     return;
   }
 
