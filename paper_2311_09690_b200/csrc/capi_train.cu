@@ -15,8 +15,17 @@ using namespace tpcb;
 // per-epoch inputs (plan contents, lr, step count) are read from device
 // memory, so the same graph serves every epoch of a training run.
 struct tpcb_graph {
-  cudaGraphExec_t exec = nullptr;
-  std::vector<uint8_t> key;
+  // a few instantiated epochs keyed by everything they captured (pointers,
+  // step count, loss / optimizer settings): epochs whose plans have different
+  // step counts alternate without re-capturing
+  struct Entry {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<uint8_t> key;
+    uint64_t used = 0;
+  };
+  std::vector<Entry> entries;
+  uint64_t clock = 0;
+  static constexpr size_t kMax = 8;
 };
 
 namespace {
@@ -359,7 +368,8 @@ extern "C" int tpcb_graph_create(tpcb_graph** out) {
 
 extern "C" void tpcb_graph_destroy(tpcb_graph* g) {
   if (!g) return;
-  if (g->exec) cudaGraphExecDestroy(g->exec);
+  for (auto& e : g->entries)
+    if (e.exec) cudaGraphExecDestroy(e.exec);
   delete g;
 }
 
@@ -439,10 +449,17 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
   key_add(key, d_status);
   key_add(key, comm);
   key_add(key, d_grad);
-  if (!graph->exec || graph->key != key) {
-    if (graph->exec) {
-      cudaGraphExecDestroy(graph->exec);
-      graph->exec = nullptr;
+  tpcb_graph::Entry* hit = nullptr;
+  for (auto& e : graph->entries)
+    if (e.key == key) hit = &e;
+  if (!hit) {
+    if (graph->entries.size() >= tpcb_graph::kMax) {  // evict the least recently used
+      auto lru = std::min_element(graph->entries.begin(), graph->entries.end(),
+                                  [](const tpcb_graph::Entry& a, const tpcb_graph::Entry& b) {
+                                    return a.used < b.used;
+                                  });
+      cudaGraphExecDestroy(lru->exec);
+      graph->entries.erase(lru);
     }
     st = prepare_train_kernels(m->dev, ws->l_cap);  // attributes are set outside capture
     if (st) return st;
@@ -455,27 +472,32 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
         if (st) return st;
       }
     }
+    graph->entries.emplace_back();
+    hit = &graph->entries.back();
     TPCB_CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
     st = enqueue();
     cudaGraph_t g = nullptr;
     cudaError_t e = cudaStreamEndCapture(stream, &g);
     if (st) {
       if (g) cudaGraphDestroy(g);
+      graph->entries.pop_back();
       return st;
     }
     if (e != cudaSuccess) {
       set_last_error("cudaStreamEndCapture", e);
+      graph->entries.pop_back();
       return TPCB_ERR_CUDA;
     }
-    e = cudaGraphInstantiate(&graph->exec, g, 0);
+    e = cudaGraphInstantiate(&hit->exec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) {
       set_last_error("cudaGraphInstantiate", e);
-      graph->exec = nullptr;
+      graph->entries.pop_back();
       return TPCB_ERR_CUDA;
     }
-    graph->key = key;
+    hit->key = key;
   }
-  TPCB_CUDA_CHECK(cudaGraphLaunch(graph->exec, stream));
+  hit->used = ++graph->clock;
+  TPCB_CUDA_CHECK(cudaGraphLaunch(hit->exec, stream));
   return TPCB_OK;
 }
