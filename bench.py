@@ -284,6 +284,16 @@ def run_full_config(args, data, norm, dv, dev, world, comm, n_steps: int = 12):
     return out
 
 
+def _ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/r01/ncu_traffic.json)."""
+    p = ROOT / "profiles" / "r01" / "ncu_traffic.json"
+    try:
+        return int(json.loads(p.read_text())[kernel]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
     import paper_2311_09690_b200 as pb
@@ -406,7 +416,7 @@ def run_ours(args):
     bf16 = peaks.get("bf16_tflops", 1590.0)
     roofline = {"bound": "tensor", "kernel": "train4_kernel (fused fwd+bwd per sample, desk fast path)",
                 "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                "frac": achieved / bf16, "traffic": None,
+                "frac": achieved / bf16, "traffic": _ncu_traffic("train4_kernel"),
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst)" if peaks else
                                "fallback 1.59 PFLOP/s",
                 "fp32_ffma_peak_measured": ffma, "frac_of_fp32_ffma": achieved / ffma,
