@@ -172,18 +172,21 @@ int try_overlapped_step(const tpcb_model* m, float* P, float* PT, float* mb, flo
     return 1;
   }
   if (g_prof) g_prof->mark(stream);
-  if (cudaEventRecord(ss->fork, stream) || cudaStreamWaitEvent(ss->side, ss->fork, 0))
-    return fail(TPCB_ERR_CUDA);
+  if (cudaEventRecord(ss->fork, stream)) return fail(TPCB_ERR_CUDA);
+  // the training kernel is enqueued first: where launches are serialised
+  // (profilers, CUDA_LAUNCH_BLOCKING) it completes every stage before the
+  // reduce starts, which then never waits
+  st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 1, w2, pred_out,
+                    status, stream);
+  if (st) return fail(st);
+  if (g_prof) g_prof->mark(stream);
+  if (cudaStreamWaitEvent(ss->side, ss->fork, 0)) return fail(TPCB_ERR_CUDA);
   st = launch_reduce_overlap(m->dev, w2, ov, steps, step, batch, src, grad_out, P, mb, vb, opt,
                              lr, t0, loss, step_loss, step_cmd, status,
                              std::min(g_overlap >= 16 ? std::min(g_overlap, rgrid) : rgrid,
                                       ov.n_items), ss->side);
   if (st) return fail(st);
   if (cudaEventRecord(ss->join, ss->side)) return fail(TPCB_ERR_CUDA);
-  st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 1, w2, pred_out,
-                    status, stream);
-  if (st) return fail(st);
-  if (g_prof) g_prof->mark(stream);
   if (cudaStreamWaitEvent(stream, ss->join, 0)) return fail(TPCB_ERR_CUDA);
   if (g_prof) g_prof->mark(stream);
   if (g_prof) g_prof->mark(stream);
