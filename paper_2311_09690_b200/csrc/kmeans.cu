@@ -65,29 +65,78 @@ __device__ __forceinline__ double pw_sq(const double* a, const double* b, int d)
 }
 
 // closest[i] = dist²(x_i, c) (init) or min(closest[i], dist²(x_i, c)); block
-// partial sums of the updated closest into part[blockIdx.x]
-__global__ void closest_update_kernel(const double* __restrict__ x, int64_t n, int d,
-                                      const double* __restrict__ c, double* __restrict__ closest,
-                                      int init, double* __restrict__ part) {
-  __shared__ double sc[kMaxDim * 2];
-  __shared__ double red[32];
+// partial sums of the updated closest into part[blockIdx.x].  HBM-bound: a
+// block stages 128 consecutive rows (one contiguous span of x) into shared
+// memory with coalesced 16-byte loads, rows padded to an odd number of
+// doubles so each thread then walks its own row conflict-free, in numpy's
+// pairwise summation order (pw_sq_range).
+constexpr int kCuRows = 128;
+__host__ __device__ inline int cu_stride(int d) { return d | 1; }
+
+__global__ void __launch_bounds__(kCuRows) closest_update_kernel(
+    const double* __restrict__ x, int64_t n, int d, const double* __restrict__ c,
+    double* __restrict__ closest, int init, double* __restrict__ part) {
+  extern __shared__ double sx[];  // [kCuRows][stride] rows, then the centre
+  __shared__ double red[kCuRows / 32];
+  const int st = cu_stride(d);
+  double* sc = sx + kCuRows * st;
   for (int k = threadIdx.x; k < d; k += blockDim.x) sc[k] = c[k];
-  __syncthreads();
+  const int d2 = d >> 1;                       // 16-byte columns per row
+  const bool d2_ok = d2 >= 1 && d2 <= kCuRows;
+  const int rpp = d2_ok ? kCuRows / d2 : 1;    // rows per pass
+  const int r_off = d2_ok ? threadIdx.x / d2 : 0, k2 = d2_ok ? threadIdx.x % d2 : 0;
+  const bool active = r_off < rpp;
   double acc = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = pw_sq(x + i * d, sc, d);
-    const double nv = init ? v : fmin(closest[i], v);
-    closest[i] = nv;
-    acc += nv;
+  const int64_t n_tiles = (n + kCuRows - 1) / kCuRows;
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int64_t i0 = t * kCuRows;
+    const int rows = (int)(n - i0 < kCuRows ? n - i0 : kCuRows);
+    const int total = rows * d;
+    const double* src = x + i0 * d;
+    __syncthreads();  // previous tile consumed (and the centre staged)
+    if (((reinterpret_cast<uintptr_t>(src) & 15) == 0) && ((d & 1) == 0) && d2_ok) {
+      // thread -> (row offset, 16-byte column): no division in the loop, 8
+      // loads in flight per thread
+      const double2* s2 = reinterpret_cast<const double2*>(src);
+      constexpr int U = 8;
+      for (int r0 = r_off; r0 < rows; r0 += U * rpp) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r = r0 + u * rpp;
+          if (r < rows && active) v[u] = __ldcs(s2 + (size_t)r * d2 + k2);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r = r0 + u * rpp;
+          if (r < rows && active) {
+            sx[r * st + 2 * k2] = v[u].x;
+            sx[r * st + 2 * k2 + 1] = v[u].y;
+          }
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < total; e += kCuRows) {
+        const int r = e / d, k = e - r * d;
+        sx[r * st + k] = __ldcs(src + e);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < rows) {
+      const int64_t i = i0 + threadIdx.x;
+      const double v = pw_sq(sx + threadIdx.x * st, sc, d);
+      const double nv = init ? v : fmin(closest[i], v);
+      closest[i] = nv;
+      acc += nv;
+    }
   }
   acc = warp_sum_d(acc);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    v = warp_sum_d(v);
-    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < kCuRows / 32; ++w) v += red[w];
+    part[blockIdx.x] = v;
   }
 }
 
@@ -105,26 +154,42 @@ __global__ void sum_parts_kernel(const double* __restrict__ part, int np, double
   }
 }
 
-__global__ void div_kernel(const double* __restrict__ a, const double* __restrict__ total,
-                           double* __restrict__ p, int64_t n) {
-  const double t = *total;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = a[i] / t;
+
+// First j in [0, n) whose monotone predicate holds (n if none): one warp,
+// 32-ary narrowing — 4 rounds of one load per lane for n = 1 M (the old
+// grid-wide scan hammered one atomicMin from every thread past the answer).
+template <class Pred>
+__device__ void warp_first_true(int64_t n, Pred pred, unsigned long long* found) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = n;  // answer in [lo, hi]
+  while (lo < hi) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t j = lo + lane * step;
+    const bool p = j >= hi || pred(j);
+    const unsigned b = __ballot_sync(0xffffffffu, p);
+    if (b == 0u) {  // all 32 probes false: answer after the last probe
+      lo = lo + 31 * step + 1;
+      continue;
+    }
+    const int f = __ffs(b) - 1;
+    if (f == 0) {
+      hi = lo;
+    } else {
+      const int64_t nlo = lo + (f - 1) * step + 1, nhi = lo + f * step;
+      lo = nlo;
+      hi = nhi < hi ? nhi : hi;
+    }
+  }
+  if (lane == 0) *found = (unsigned long long)lo;
 }
 
 // first j with cdf[j] / cdf[n-1] > u  (Generator.choice: cdf /= cdf[-1];
-// cdf.searchsorted(u, side="right"))
+// cdf.searchsorted(u, side="right")); the CDF is non-decreasing, so the
+// predicate is monotone
 __global__ void search_kernel(const double* __restrict__ cdf, int64_t n, double u,
                               unsigned long long* __restrict__ found) {
   const double last = cdf[n - 1];
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    if (cdf[j] / last > u) {
-      atomicMin(found, (unsigned long long)j);
-      return;  // later j of this thread are larger
-    }
-  }
+  warp_first_true(n, [&](int64_t j) { return cdf[j] / last > u; }, found);
 }
 
 __global__ void set_center_kernel(const double* __restrict__ x, int d,
@@ -252,13 +317,7 @@ __global__ void member_mean_kernel(const double* __restrict__ x, int d, int kapp
 __global__ void search_offset_kernel(const double* __restrict__ cdf, int64_t n, double offset,
                                      double total, double u,
                                      unsigned long long* __restrict__ found) {
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    if ((offset + cdf[j]) / total > u) {
-      atomicMin(found, (unsigned long long)j);
-      return;
-    }
-  }
+  warp_first_true(n, [&](int64_t j) { return (offset + cdf[j]) / total > u; }, found);
 }
 
 __global__ void found_to_i64_kernel(const unsigned long long* __restrict__ found, int64_t n,
@@ -318,6 +377,28 @@ __global__ void psi_kernel(const double* __restrict__ f, const int64_t* __restri
   psi[(size_t)c * nt + t] = acc / (double)(r1 - r0);
 }
 
+// p[i] = closest[i] / total, read on the fly by the CDF scan (div_kernel's
+// arithmetic, no p array round trip through HBM)
+struct DivByTotal {
+  const double* total;
+  __host__ __device__ double operator()(double a) const { return a / *total; }
+};
+inline cub::TransformInputIterator<double, DivByTotal, const double*> p_iter(const double* c,
+                                                                              const double* t) {
+  return cub::TransformInputIterator<double, DivByTotal, const double*>(c, DivByTotal{t});
+}
+
+// closest_update: 4 tiles of 128 rows per block at least, up to 8 blocks per SM
+int closest_grid(int64_t n) {
+  const int64_t tiles = (n + kCuRows - 1) / kCuRows;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kNumSMs * 8));
+}
+size_t closest_smem(int d) { return (size_t)(kCuRows * cu_stride(d) + d) * sizeof(double); }
+cudaError_t prep_closest(int d) {
+  return cudaFuncSetAttribute(closest_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)closest_smem(d));
+}
+
 int grid_for(int64_t n, int block = 256) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + block - 1) / block, kNumSMs * 16));
 }
@@ -334,6 +415,10 @@ extern "C" int tpcb_kmeans_ws_size(int64_t n, int32_t d, int32_t kappa, size_t* 
   if (n > 0x7fffffff) return TPCB_ERR_UNSUPPORTED;
   size_t scan_tmp = 0, sort_tmp = 0;
   cub::DeviceScan::InclusiveSum(nullptr, scan_tmp, (double*)nullptr, (double*)nullptr, (int)n);
+  size_t scan_tmp2 = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, scan_tmp2, p_iter(nullptr, nullptr), (double*)nullptr,
+                                (int)n);
+  scan_tmp = std::max(scan_tmp, scan_tmp2);
   cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (int32_t*)nullptr, (int32_t*)nullptr,
                                   (int32_t*)nullptr, (int32_t*)nullptr, (int)n);
   size_t b = 0;
@@ -392,8 +477,9 @@ extern "C" int tpcb_kmeanspp_init(const double* d_x, int64_t n, int32_t d, int64
   cudaStream_t stream = (cudaStream_t)stream_;
   KWs w = carve(ws, ws_bytes, n, 1);
   set_center_direct_kernel<<<1, 128, 0, stream>>>(d_x, d, first, d_centers);
-  const int g = std::min(grid_for(n), 4096);
-  closest_update_kernel<<<g, 256, 0, stream>>>(d_x, n, d, d_centers, d_closest, 1, w.part);
+  const int g = closest_grid(n);
+  TPCB_CUDA_CHECK(prep_closest(d));
+  closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(d_x, n, d, d_centers, d_closest, 1, w.part);
   sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
   TPCB_LAUNCH_CHECK("kmeanspp_init");
   return TPCB_OK;
@@ -409,18 +495,18 @@ extern "C" int tpcb_kmeanspp_step(const double* d_x, int64_t n, int32_t d, int32
   KWs w = carve(ws, ws_bytes, n, 1);
   double* center = d_centers + (size_t)i * d;
   if (u >= 0.0) {
-    div_kernel<<<grid_for(n), 256, 0, stream>>>(d_closest, d_total, w.p, n);
-    size_t tb = w.tmp_bytes;
-    TPCB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(w.tmp, tb, w.p, w.cdf, (int)n, stream));
-    TPCB_CUDA_CHECK(cudaMemsetAsync(w.found, 0xff, sizeof(unsigned long long), stream));
-    search_kernel<<<grid_for(n), 256, 0, stream>>>(w.cdf, n, u, w.found);
+    size_t tb = w.tmp_bytes;  // cdf of p = closest / total, the division fused into the scan
+    TPCB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(w.tmp, tb, p_iter(d_closest, d_total), w.cdf,
+                                                  (int)n, stream));
+    search_kernel<<<1, 32, 0, stream>>>(w.cdf, n, u, w.found);
     set_center_kernel<<<1, 128, 0, stream>>>(d_x, d, w.found, n, center, d_chosen);
   } else {
     if (direct < 0 || direct >= n) return TPCB_ERR_VALIDATION;
     set_center_direct_kernel<<<1, 128, 0, stream>>>(d_x, d, direct, center);
   }
-  const int g = std::min(grid_for(n), 4096);
-  closest_update_kernel<<<g, 256, 0, stream>>>(d_x, n, d, center, d_closest, 0, w.part);
+  const int g = closest_grid(n);
+  TPCB_CUDA_CHECK(prep_closest(d));
+  closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(d_x, n, d, center, d_closest, 0, w.part);
   sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
   TPCB_LAUNCH_CHECK("kmeanspp_step");
   return TPCB_OK;
@@ -497,8 +583,9 @@ extern "C" int tpcb_kmeanspp_closest(const double* d_x, int64_t n, int32_t d,
   if (d > kMaxDim) return TPCB_ERR_UNSUPPORTED;
   cudaStream_t stream = (cudaStream_t)stream_;
   KWs w = carve(ws, ws_bytes, n, 1);
-  const int g = std::min(grid_for(n), 4096);
-  closest_update_kernel<<<g, 256, 0, stream>>>(d_x, n, d, d_center, d_closest, init ? 1 : 0,
+  const int g = closest_grid(n);
+  TPCB_CUDA_CHECK(prep_closest(d));
+  closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(d_x, n, d, d_center, d_closest, init ? 1 : 0,
                                                w.part);
   sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
   TPCB_LAUNCH_CHECK("kmeanspp_closest");
@@ -510,9 +597,9 @@ extern "C" int tpcb_kmeanspp_cdf(const double* d_closest, int64_t n, const doubl
   if (!d_closest || !d_total || !d_local_sum || !ws) return TPCB_ERR_VALIDATION;
   cudaStream_t stream = (cudaStream_t)stream_;
   KWs w = carve(ws, ws_bytes, n, 1);
-  div_kernel<<<grid_for(n), 256, 0, stream>>>(d_closest, d_total, w.p, n);
-  size_t tb = w.tmp_bytes;
-  TPCB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(w.tmp, tb, w.p, w.cdf, (int)n, stream));
+  size_t tb = w.tmp_bytes;  // cdf of p = closest / total, the division fused into the scan
+  TPCB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(w.tmp, tb, p_iter(d_closest, d_total), w.cdf,
+                                                (int)n, stream));
   TPCB_CUDA_CHECK(cudaMemcpyAsync(d_local_sum, w.cdf + (n - 1), sizeof(double),
                                   cudaMemcpyDeviceToDevice, stream));
   TPCB_LAUNCH_CHECK("kmeanspp_cdf");
@@ -524,8 +611,7 @@ extern "C" int tpcb_kmeanspp_search(int64_t n, double offset, double total, doub
   if (!d_found || !ws) return TPCB_ERR_VALIDATION;
   cudaStream_t stream = (cudaStream_t)stream_;
   KWs w = carve(ws, ws_bytes, n, 1);
-  TPCB_CUDA_CHECK(cudaMemsetAsync(w.found, 0xff, sizeof(unsigned long long), stream));
-  search_offset_kernel<<<grid_for(n), 256, 0, stream>>>(w.cdf, n, offset, total, u, w.found);
+  search_offset_kernel<<<1, 32, 0, stream>>>(w.cdf, n, offset, total, u, w.found);
   found_to_i64_kernel<<<1, 1, 0, stream>>>(w.found, n, d_found);
   TPCB_LAUNCH_CHECK("kmeanspp_search");
   return TPCB_OK;
