@@ -48,7 +48,16 @@ constexpr int kFO1 = 7 * kTileB;                // N=64, k = 64..127
 constexpr int kImgLStride = 8 * kTileB;
 constexpr int kImgDec0 = kImgLayer + NLAY * kImgLStride;  // decoder 0: N=64, K=32 (zero-padded)
 constexpr int kImgDec1 = kImgDec0 + kTileB;              // decoder 1: N=64, K=64
-constexpr int kImgBytes = kImgDec1 + kTileB;              // 155,648
+constexpr int kImgBytes = kImgDec1 + kTileB;              // 155,648 (resident in smem)
+// leaf_embed.L images (global only, staged per tile): for each L, a B operand of
+// N = L·32 rows (row l·32 + n = column n of W_L's l-th 64-row block) × K = 64,
+// SW128, 4 KB per leaf position; image L starts at kImgBytes + 4 KB · L(L−1)/2.
+constexpr int kLeafChunkB = 32 * 128;
+constexpr int kMaxLeafTC = 16;
+__host__ __device__ constexpr int leaf_img_off(int L) {
+  return kImgBytes + kLeafChunkB * (L * (L - 1) / 2);
+}
+constexpr int kImgTotal = leaf_img_off(kMaxLeafTC + 1);   // 712,704
 
 // ---- shared memory (bytes, dynamic) ----
 constexpr int kSmA = kImgBytes;                 // A operand [128][64] bf16, SW128 (16 KB)
@@ -58,7 +67,23 @@ constexpr int kSmVec = kSmKV + TR * kKVLd * 2;  // biases / LN vectors fp32
 constexpr int kVecIn = 0, kVecLayer = 64, kVecLStride = 704;  // (same order as train4)
 constexpr int kVBQKV = 0, kVBO = 192, kVLN1G = 256, kVLN1B = 320, kVFHB = 384, kVFOB = 512,
               kVLN2G = 576, kVLN2B = 640;
-constexpr int kVecFloats = kVecLayer + NLAY * kVecLStride;
+constexpr int kVecHead = kVecLayer + NLAY * kVecLStride;  // head vectors (fp32)
+constexpr int kVHLeafB = 0;                            // leaf_embed.L.b, [17][32]
+constexpr int kVHDevHW = kVHLeafB + (kMaxLeafTC + 1) * DE;  // [6][16]
+constexpr int kVHDevHB = kVHDevHW + TPCB_DEV_FEAT * DDEV;
+constexpr int kVHDevPW = kVHDevHB + DDEV;               // [16][32]
+constexpr int kVHDevPB = kVHDevPW + DDEV * DE;
+constexpr int kVHDecB0 = kVHDevPB + DE;
+constexpr int kVHDecB1 = kVHDecB0 + DEC;
+constexpr int kVHOutW = kVHDecB1 + DEC;
+constexpr int kVHOutB = kVHOutW + DEC;
+constexpr int kVecFloats = kVecHead + kVHOutB + 4;
+// leaf_embed GEMM staging inside [kSmA, kSmVec): A chunk l (row a = token a·L + l)
+// at l · leaf_chunk_a(L), B chunks after them (see the head)
+constexpr int kLeafRegion = kSmVec - kSmA;             // 51,200
+__device__ __forceinline__ int leaf_chunk_a(int L) {   // bytes per A chunk: ⌈⌊128/L⌋/8⌉ atoms
+  return L == 1 ? TR * 128 : (((TR / L) + 7) >> 3) * 1024;
+}
 constexpr int kSmTotal = kSmVec + kVecFloats * 4;
 
 __host__ __device__ inline uint32_t sw128(int r, int k) {  // bf16 element (row r, col k < 64)
@@ -179,9 +204,20 @@ __device__ __forceinline__ double boxcox_decode_tc(double e, const tpcb_boxcox& 
 // fp32 parameters → the bf16 weight image (see kImg*)
 __global__ void prep_weights_kernel(const Model M, const float* __restrict__ P,
                                     uint8_t* __restrict__ img) {
-  const int total = kImgBytes / 2;
+  const int total = kImgTotal / 2;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int byte = e * 2;
+    if (byte >= kImgBytes) {  // leaf_embed.L: find L, then (l, n, k) inside its image
+      int L = 1;
+      while (leaf_img_off(L + 1) <= byte) ++L;
+      const int in = byte - leaf_img_off(L);
+      const int atom = in >> 10, rr = (in >> 7) & 7, chunk = ((in >> 4) & 7) ^ rr;
+      const int nrow = atom * 8 + rr, k = chunk * 8 + ((in & 15) >> 1);
+      const int l = nrow >> 5, n = nrow & 31;
+      const float v = L <= M.n_leaf_max ? P[M.leafW[L] + (l * D + k) * DE + n] : 0.f;
+      reinterpret_cast<__nv_bfloat16*>(img)[e] = __float2bfloat16_rn(v);
+      continue;
+    }
     // locate (tile base, n, k) from the byte offset: invert sw128 within 8-KB tiles
     const int tile = byte / kTileB, in = byte - tile * kTileB;
     const int atom = in >> 10, rr = (in >> 7) & 7, chunk = ((in >> 4) & 7) ^ rr;
@@ -213,11 +249,11 @@ __global__ void prep_weights_kernel(const Model M, const float* __restrict__ P,
 }
 
 __device__ long long* g_trace_tc = nullptr;
-// debug: per-phase timestamps of CTA 0 / thread 0 for its first 8 tiles
+// debug: per-phase timestamps of CTA 0 / thread 0 for its last 8 tiles (ring)
 #define TT(id)                                                                   \
   do {                                                                           \
-    if (g_trace_tc && blockIdx.x == 0 && t == 0 && tcount < 8)                   \
-      g_trace_tc[tcount * 32 + (id)] = clock64();                                \
+    if (g_trace_tc && blockIdx.x == 0 && t == 0)                                 \
+      g_trace_tc[(tcount & 7) * 32 + (id)] = clock64();                          \
   } while (0)
 
 __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
@@ -229,7 +265,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     float* __restrict__ pred_out, float* __restrict__ zx_out, float* __restrict__ zv_out,
     float* __restrict__ z_out, double* __restrict__ lat_out, int32_t* status) {
   extern __shared__ __align__(1024) uint8_t smb[];
-  __shared__ __align__(8) uint64_t bars[2];  // [0] weights landed, [1] MMA done
+  __shared__ __align__(8) uint64_t bars[4];  // [0] weights, [1] MMA done, [2] leaf B landed, [3] leaf group done
   __shared__ uint32_t s_tmem;
   const int t = threadIdx.x, warp = t >> 5;
   const int n_tiles = *n_tiles_p;
@@ -239,6 +275,8 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
   if (t == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    mbar_init(&bars[3], 1);
     mbar_fence_init();
   }
   if (warp == 0) {
@@ -274,10 +312,28 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     }
     for (int i = t; i < FF; i += NTH) b[kVFHB + i] = __ldg(P + lo.fhb + i);
   }
+  {
+    float* hv = sv + kVecHead;
+    for (int i = t; i < (kMaxLeafTC + 1) * DE; i += NTH) {
+      const int L = i / DE;
+      hv[kVHLeafB + i] = (L >= 1 && L <= M.n_leaf_max) ? __ldg(P + M.leafb[L] + (i - L * DE)) : 0.f;
+    }
+    for (int i = t; i < TPCB_DEV_FEAT * DDEV; i += NTH) hv[kVHDevHW + i] = __ldg(P + M.devhW + i);
+    for (int i = t; i < DDEV * DE; i += NTH) hv[kVHDevPW + i] = __ldg(P + M.devpW + i);
+    for (int i = t; i < DDEV; i += NTH) hv[kVHDevHB + i] = __ldg(P + M.devhb + i);
+    for (int i = t; i < DE; i += NTH) hv[kVHDevPB + i] = __ldg(P + M.devpb + i);
+    for (int i = t; i < DEC; i += NTH) {
+      hv[kVHDecB0 + i] = __ldg(P + M.decb[0] + i);
+      hv[kVHDecB1 + i] = __ldg(P + M.decb[1] + i);
+      hv[kVHOutW + i] = __ldg(P + M.outW + i);
+    }
+    if (t == 0) hv[kVHOutB] = __ldg(P + M.outb);
+  }
+  const float* hv = sv + kVecHead;
   mbar_wait(&bars[0], 0);
   const uint32_t a_addr = smem_u32(sA), kv_addr = smem_u32(sKV), w_addr = smem_u32(smb);
   const float scale = 1.f / sqrtf((float)DH);
-  uint32_t phase = 0;
+  uint32_t phase = 0, phase_b = 0, phase_g = 0;
 
   int tcount = -1;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -444,6 +500,12 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       }
       wait_mma(&bars[1], phase);
       TT(10 + li * 12);
+      if (li + 1 == NLAY && t == 0) {  // K|V / F are dead: stage leaf_embed B chunks now
+        const int boff = L * leaf_chunk_a(L);
+        const int g = min(L, (kLeafRegion - boff) / kLeafChunkB);
+        mbar_arrive_expect_tx(&bars[2], (uint32_t)(g * kLeafChunkB));
+        bulk_g2s(sA + boff, img + leaf_img_off(L), (uint32_t)(g * kLeafChunkB), &bars[2]);
+      }
       tmem_ld32(tlane, h);
       tmem_ld32(tlane + 32, h + 32);
 #pragma unroll
@@ -453,75 +515,89 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
         store_row_bf16(sA, t, h);
         sync_for_mma();
         TT(11 + li * 12);
+      } else if (live) {  // leaf_embed A operand: chunk l = t mod L, row a = t / L
+        store_row_bf16(sA + (t % L) * leaf_chunk_a(L), t / L, h);
       }
     }
     TT(30);
     // ---------------------------------------------------------------- head
-    // leaf_embed: each row's partial H_l · W_L[l] (fp32, CUDA cores), summed
-    // in row order by the AST's first thread with the device MLP and the gate;
-    // the decoder then runs on the tensor cores with one AST per TMEM lane.
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();  // (the last encoder epilogue may still read K|V / A)
-    float* s_part = reinterpret_cast<float*>(sKV);  // [128][33] leaf_embed partials
-    const int a = t / L, l = t - a * L;
-    if (live) {
-      const float* W = P + M.leafW[L] + (size_t)l * D * DE;
-      float part[DE];
-#pragma unroll
-      for (int n = 0; n < DE; ++n) part[n] = 0.f;
-#pragma unroll 4
-      for (int k = 0; k < D; ++k) {
-        const float hv = h[k];
-        const float4* wr = reinterpret_cast<const float4*>(W + (size_t)k * DE);
-#pragma unroll
-        for (int n4 = 0; n4 < DE / 4; ++n4) {
-          const float4 w4 = __ldg(wr + n4);
-          part[4 * n4] = fmaf(hv, w4.x, part[4 * n4]);
-          part[4 * n4 + 1] = fmaf(hv, w4.y, part[4 * n4 + 1]);
-          part[4 * n4 + 2] = fmaf(hv, w4.z, part[4 * n4 + 2]);
-          part[4 * n4 + 3] = fmaf(hv, w4.w, part[4 * n4 + 3]);
+    // leaf_embed on the tensor cores (costmodel.py:213-216): A chunk l holds row
+    // a = token a·L + l (written by the last LayerNorm epilogue), B chunk l is
+    // W_L's l-th 64-row block, so D[a] = Σ_l h[a·L+l] · W_L[l] = z_x[a] − b_L
+    // accumulates over the L chunks in TMEM (columns 0..31, one AST per lane).
+    sync_for_mma();
+    if (t == 0) {
+      const int cb = leaf_chunk_a(L), boff = L * cb;
+      const int G = min(L, (kLeafRegion - boff) / kLeafChunkB);
+      const uint32_t id = idesc_bf16(TR, DE);
+      for (int l0 = 0; l0 < L; l0 += G) {
+        const int g = min(G, L - l0);
+        if (l0 > 0) {  // L > G: the previous group's MMAs must finish before B is restaged
+          mma_commit(&bars[3]);
+          mbar_wait(&bars[3], phase_g);
+          phase_g ^= 1;
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          mbar_arrive_expect_tx(&bars[2], (uint32_t)(g * kLeafChunkB));
+          bulk_g2s(sA + boff, img + leaf_img_off(L) + l0 * kLeafChunkB,
+                   (uint32_t)(g * kLeafChunkB), &bars[2]);
+        }
+        mbar_wait(&bars[2], phase_b);
+        phase_b ^= 1;
+        for (int j = 0; j < g; ++j) {
+          const uint32_t ab = a_addr + (uint32_t)((l0 + j) * cb),
+                         bb = a_addr + (uint32_t)(boff + j * kLeafChunkB);
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = sdesc(ab + k * 32), bd = sdesc(bb + k * 32);
+            const uint32_t acc = ((l0 + j) | k) != 0;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+                "l"(ad), "l"(bd), "r"(id), "r"(acc));
+          }
         }
       }
-#pragma unroll
-      for (int n = 0; n < DE; ++n) s_part[t * 33 + n] = part[n];
+      mma_commit(&bars[1]);
     }
-    __syncthreads();
-    if (live && l == 0) {  // z_x (rows of the AST in order), device MLP, gate → decoder operand row a
-      const int idx = perm[first + a];
-      float zx[DE], zv[DDEV], z[D];
+    wait_mma(&bars[1], phase);
+    TT(25);
+    {  // z_x, device MLP and gate for AST t (t < A) → decoder operand row t
+      float zx[DE];
+      tmem_ld32(tlane, zx);  // warp-collective: every lane loads, rows ≥ A are ignored
+      if (t < A) {
+        const int idx = perm[first + t];
+        float zv[DDEV], z[D];
 #pragma unroll
-      for (int n = 0; n < DE; ++n) zx[n] = __ldg(P + M.leafb[L] + n);
-      for (int j = 0; j < L; ++j)
+        for (int n = 0; n < DE; ++n) zx[n] += hv[kVHLeafB + L * DE + n];
+        float dv[TPCB_DEV_FEAT];
 #pragma unroll
-        for (int n = 0; n < DE; ++n) zx[n] += s_part[(t + j) * 33 + n];
-      float dv[TPCB_DEV_FEAT];
+        for (int f = 0; f < TPCB_DEV_FEAT; ++f) dv[f] = __ldg(devfeat + (size_t)idx * TPCB_DEV_FEAT + f);
 #pragma unroll
-      for (int f = 0; f < TPCB_DEV_FEAT; ++f) dv[f] = __ldg(devfeat + (size_t)idx * TPCB_DEV_FEAT + f);
+        for (int n = 0; n < DDEV; ++n) {
+          float sacc = hv[kVHDevHB + n];
 #pragma unroll
-      for (int n = 0; n < DDEV; ++n) {
-        float sacc = __ldg(P + M.devhb + n);
+          for (int f = 0; f < TPCB_DEV_FEAT; ++f) sacc = fmaf(dv[f], hv[kVHDevHW + f * DDEV + n], sacc);
+          zv[n] = fmaxf(sacc, 0.f);
+        }
 #pragma unroll
-        for (int f = 0; f < TPCB_DEV_FEAT; ++f) sacc = fmaf(dv[f], __ldg(P + M.devhW + f * DDEV + n), sacc);
-        zv[n] = fmaxf(sacc, 0.f);
+        for (int n = 0; n < DE; ++n) {
+          float sacc = hv[kVHDevPB + n];
+#pragma unroll
+          for (int k = 0; k < DDEV; ++k) sacc = fmaf(zv[k], hv[kVHDevPW + k * DE + n], sacc);
+          z[n] = zx[n] * sacc;
+        }
+#pragma unroll
+        for (int n = DE; n < D; ++n) z[n] = 0.f;
+        store_row_bf16(sA, t, z);
+        if (zx_out)
+          for (int n = 0; n < DE; ++n) zx_out[(size_t)idx * DE + n] = zx[n];
+        if (z_out)
+          for (int n = 0; n < DE; ++n) z_out[(size_t)idx * DE + n] = z[n];
+        if (zv_out)
+          for (int n = 0; n < DDEV; ++n) zv_out[(size_t)idx * DDEV + n] = zv[n];
       }
-#pragma unroll
-      for (int n = 0; n < DE; ++n) {
-        float sacc = __ldg(P + M.devpb + n);
-#pragma unroll
-        for (int k = 0; k < DDEV; ++k) sacc = fmaf(zv[k], __ldg(P + M.devpW + k * DE + n), sacc);
-        z[n] = zx[n] * sacc;
-      }
-#pragma unroll
-      for (int n = DE; n < D; ++n) z[n] = 0.f;
-      store_row_bf16(sA, a, z);
-      if (zx_out)
-        for (int n = 0; n < DE; ++n) zx_out[(size_t)idx * DE + n] = zx[n];
-      if (z_out)
-        for (int n = 0; n < DE; ++n) z_out[(size_t)idx * DE + n] = z[n];
-      if (zv_out)
-        for (int n = 0; n < DDEV; ++n) zv_out[(size_t)idx * DDEV + n] = zv[n];
     }
     sync_for_mma();
+    TT(26);
     // decoder on the tensor cores, one AST per row / TMEM lane / thread
     if (t == 0) {
       const uint32_t at[1] = {a_addr}, bt[1] = {w_addr + kImgDec0};
@@ -529,12 +605,13 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       mma_commit(&bars[1]);
     }
     wait_mma(&bars[1], phase);
+    TT(27);
     {
       float u[DEC];
       tmem_ld32(tlane, u);
       tmem_ld32(tlane + 32, u + 32);
 #pragma unroll
-      for (int j = 0; j < DEC; ++j) u[j] = fmaxf(u[j] + __ldg(P + M.decb[0] + j), 0.f);
+      for (int j = 0; j < DEC; ++j) u[j] = fmaxf(u[j] + hv[kVHDecB0 + j], 0.f);
       store_row_bf16(sA, t, u);
     }
     sync_for_mma();
@@ -544,15 +621,16 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       mma_commit(&bars[1]);
     }
     wait_mma(&bars[1], phase);
+    TT(28);
     {
       float u[DEC];
       tmem_ld32(tlane, u);
       tmem_ld32(tlane + 32, u + 32);
       if (t < A) {
-        float pred = __ldg(P + M.outb);
+        float pred = hv[kVHOutB];
 #pragma unroll
         for (int j = 0; j < DEC; ++j)
-          pred = fmaf(fmaxf(u[j] + __ldg(P + M.decb[1] + j), 0.f), __ldg(P + M.outW + j), pred);
+          pred = fmaf(fmaxf(u[j] + hv[kVHDecB1 + j], 0.f), hv[kVHOutW + j], pred);
         const int idx = perm[first + t];
         pred_out[idx] = pred;
         if (lat_out) {
@@ -574,7 +652,7 @@ bool tc_supported(const Model& M) {
   if (M.d != D || M.n_layers != NLAY || M.n_heads != 2 || M.dh != DH || M.d_ff != FF) return false;
   if (M.d_e != DE || M.d_dev != DDEV || M.n_dec != 2 || M.dec[0] != DEC || M.dec[1] != DEC)
     return false;
-  return M.n_leaf_max <= 16;
+  return M.n_leaf_max <= kMaxLeafTC;
 }
 
 }  // namespace
@@ -586,7 +664,7 @@ using namespace tpcb;
 /* bf16 tensor-core forward (C5 mode): same contract as tpcb_forward, desk-shaped
  * models, rows_per_tile must be 128; d_img: caller workspace of
  * tpcb_forward_bf16_workspace() bytes (the bf16 weight image, rebuilt per call). */
-extern "C" size_t tpcb_forward_bf16_workspace(void) { return (size_t)kImgBytes; }
+extern "C" size_t tpcb_forward_bf16_workspace(void) { return (size_t)kImgTotal; }
 
 namespace tpcb {
 int set_forward_tc_trace(long long* d) {

@@ -31,11 +31,15 @@ for li in range(2):
     for k, nm in enumerate(["qkv mma", "qkv epi+attn", "attn->A", "wo mma", "ln1 epi", "ffn1 mma",
                             "ffn1 epi", "ffn2 mma", "ln2 epi"]):
         names[base + k] = f"L{li} {nm}"
+names[25] = "leaf mma"
+names[26] = "zx+dev mlp+gate->A"
+names[27] = "dec0 mma"
+names[28] = "dec0 epi+dec1 mma"
 names[30] = "enc done"
-names[31] = "head"
-for tile in range(3):
+names[31] = "dec1 epi+store"
+for tile in range(8):
     row = b[tile]
-    ids = [i for i in range(32) if row[i]]
+    ids = sorted([i for i in range(32) if row[i]], key=lambda i: row[i])
     prev = row[0]
     parts = []
     for i in ids[1:]:
