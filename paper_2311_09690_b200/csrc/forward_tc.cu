@@ -34,7 +34,7 @@ namespace {
 
 constexpr int D = 64, FF = 128, DE = 32, DDEV = 16, DEC = 64, NLAY = 2, DH = 32;
 constexpr int TR = 128;   // rows per tile = TMEM lanes = threads
-constexpr int NTH = 128;
+constexpr int NTH = 256;  // two warpgroups over the same 128 TMEM lanes
 
 // ---- weight image (bytes): bf16 B operands [N rows][64 k] K-major, SW128 ----
 constexpr int kTileB = 64 * 128;  // bytes per 64-row B tile (8 KB)
@@ -159,6 +159,23 @@ __device__ __forceinline__ void store_row_bf16(uint8_t* tile, int r, const float
   }
 }
 
+// 32 bf16 values → columns 32·half .. 32·half+31 of row r of a SW128 A tile
+__device__ __forceinline__ void store_half_row_bf16(uint8_t* tile, int r, int half, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * c + 0], v[8 * c + 1]);
+    __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * c + 2], v[8 * c + 3]);
+    __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * c + 4], v[8 * c + 5]);
+    __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * c + 6], v[8 * c + 7]);
+    uint4 u;
+    u.x = *reinterpret_cast<uint32_t*>(&p0);
+    u.y = *reinterpret_cast<uint32_t*>(&p1);
+    u.z = *reinterpret_cast<uint32_t*>(&p2);
+    u.w = *reinterpret_cast<uint32_t*>(&p3);
+    *reinterpret_cast<uint4*>(tile + sw128(r, 32 * half + 8 * c)) = u;
+  }
+}
+
 // operand writes (generic proxy) → visible to the tensor cores; CTA barrier
 __device__ __forceinline__ void sync_for_mma() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -173,21 +190,28 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// LayerNorm of a row held by this thread (nn.py:48-54)
-__device__ __forceinline__ void ln_row(float* v, const float* g, const float* b) {
+// LayerNorm of a row split over two threads (warpgroup wg holds columns
+// 32·wg .. 32·wg+31): two-pass mean / biased variance, eps 1e-5 (nn.py:48-54);
+// both halves combine the partial sums in the same order.  red: [4][TR].
+__device__ __forceinline__ void ln_half(float* v, const float* g, const float* b, int wg, int r,
+                                        float* red) {
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < D; ++i) s += v[i];
-  const float mu = s * (1.f / D);
+  for (int i = 0; i < DH; ++i) s += v[i];
+  red[wg * TR + r] = s;
+  __syncthreads();
+  const float mu = (red[r] + red[TR + r]) * (1.f / D);
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < D; ++i) {
+  for (int i = 0; i < DH; ++i) {
     const float t = v[i] - mu;
     q = fmaf(t, t, q);
   }
-  const float inv = 1.f / sqrtf(q * (1.f / D) + 1e-5f);
+  red[(2 + wg) * TR + r] = q;
+  __syncthreads();
+  const float inv = 1.f / sqrtf((red[2 * TR + r] + red[3 * TR + r]) * (1.f / D) + 1e-5f);
 #pragma unroll
-  for (int i = 0; i < D; ++i) v[i] = fmaf(g[i], (v[i] - mu) * inv, b[i]);
+  for (int i = 0; i < DH; ++i) v[i] = fmaf(g[DH * wg + i], (v[i] - mu) * inv, b[DH * wg + i]);
 }
 
 __device__ __forceinline__ double boxcox_decode_tc(double e, const tpcb_boxcox& bc, bool* bad) {
@@ -267,7 +291,9 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
   extern __shared__ __align__(1024) uint8_t smb[];
   __shared__ __align__(8) uint64_t bars[4];  // [0] weights, [1] MMA done, [2] leaf B landed, [3] leaf group done
   __shared__ uint32_t s_tmem;
+  __shared__ float s_red[4 * TR];  // split-row LayerNorm partial sums
   const int t = threadIdx.x, warp = t >> 5;
+  const int wg = warp >> 2, r = t & (TR - 1);  // warpgroup, row = TMEM lane
   const int n_tiles = *n_tiles_p;
   uint8_t* sA = smb + kSmA;
   uint8_t* sKV = smb + kSmKV;
@@ -288,7 +314,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  const uint32_t tlane = tmem + ((uint32_t)(32 * warp) << 16);  // this warp's lanes
+  const uint32_t tlane = tmem + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lanes
   if (t == 0 && (smem_u32(smb) & 1023u)) raise_status(status, TPCB_ERR_CUDA);  // swizzle atoms
   if (t == 0) {  // the weight image: one bulk copy for the CTA's lifetime
     mbar_arrive_expect_tx(&bars[0], (uint32_t)kImgBytes);
@@ -335,26 +361,33 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
   const float scale = 1.f / sqrtf((float)DH);
   uint32_t phase = 0, phase_b = 0, phase_g = 0;
 
+  // warpgroup 1 prefetches the next tile's input rows into registers while
+  // warpgroup 0 runs the previous tile's last LayerNorm, leaf_embed and head
+  float xn[TPCB_FEAT];
+  auto load_x = [&](int tl) {
+    if (wg == 1 && tl < n_tiles) {
+      const float* xr = x + ((size_t)tl * TR + r) * TPCB_FEAT_PAD;
+#pragma unroll
+      for (int i = 0; i < TPCB_FEAT; i += 4) {
+        const float4 q4 = __ldg(reinterpret_cast<const float4*>(xr + i));
+        xn[i] = q4.x; xn[i + 1] = q4.y; xn[i + 2] = q4.z; xn[i + 3] = q4.w;
+      }
+    }
+  };
+  load_x(blockIdx.x);
   int tcount = -1;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     ++tcount;
     TT(0);
     const int L = tile_L[tile], first = tile_first[tile], A = tile_count[tile];
     const int rows = A * L;
-    const bool live = t < rows;
-    float h[D];  // this row's residual stream (fp32)
-    {  // input rows → A operand (24 features, zero-padded to 64)
-      const float* xr = x + ((size_t)tile * TR + t) * TPCB_FEAT_PAD;
+    const bool live = r < rows;
+    float h[DH];  // this row's residual stream, columns 32·wg .. 32·wg+31 (fp32)
+    if (wg == 1) {  // prefetched input rows → A operand (24 features, zero-padded to 64)
       float v[D];
 #pragma unroll
-      for (int i = 0; i < D; ++i) v[i] = 0.f;
-      if (live)
-#pragma unroll
-        for (int i = 0; i < TPCB_FEAT; i += 4) {
-          const float4 q = __ldg(reinterpret_cast<const float4*>(xr + i));
-          v[i] = q.x; v[i + 1] = q.y; v[i + 2] = q.z; v[i + 3] = q.w;
-        }
-      store_row_bf16(sA, t, v);
+      for (int i = 0; i < D; ++i) v[i] = (live && i < TPCB_FEAT) ? xn[i < TPCB_FEAT ? i : 0] : 0.f;
+      store_row_bf16(sA, r, v);
     }
     sync_for_mma();
     TT(1);
@@ -365,11 +398,12 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     }
     wait_mma(&bars[1], phase);
     TT(2);
-    tmem_ld32(tlane, h);
-    tmem_ld32(tlane + 32, h + 32);
+    {
+      tmem_ld32(tlane + DH * wg, h);
 #pragma unroll
-    for (int i = 0; i < D; ++i) h[i] += sv[kVecIn + i];
-    store_row_bf16(sA, t, h);
+      for (int i = 0; i < DH; ++i) h[i] += sv[kVecIn + DH * wg + i];
+      store_half_row_bf16(sA, r, wg, h);
+    }
     sync_for_mma();
     TT(3);
 
@@ -383,20 +417,22 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       }
       wait_mma(&bars[1], phase);
       TT(4 + li * 12);
-      float q[D];
-      tmem_ld32(tlane, q);
-      tmem_ld32(tlane + 32, q + 32);
+      // warpgroup wg owns head wg (nn.py:79-96): its 32 Q columns stay in
+      // registers, its K and V columns go to bf16 rows [K 0..63 | V 64..127]
+      const int hc = wg * DH;
+      float q[DH];
+      tmem_ld32(tlane + hc, q);
 #pragma unroll
-      for (int i = 0; i < D; ++i) q[i] += b[kVBQKV + i];
-      {  // K, V rows → bf16 [row][K 0..63 | V 64..127] (16-byte stores)
-        float kv[D];
-        uint8_t* dst = sKV + t * kKVLd * 2;
+      for (int i = 0; i < DH; ++i) q[i] += b[kVBQKV + hc + i];
+      {
+        float kv[DH];
+        uint8_t* dst = sKV + r * kKVLd * 2;
+#pragma unroll
         for (int part = 0; part < 2; ++part) {
-          tmem_ld32(tlane + 64 + 64 * part, kv);
-          tmem_ld32(tlane + 96 + 64 * part, kv + 32);
+          tmem_ld32(tlane + 64 + 64 * part + hc, kv);
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float* bb = b + kVBQKV + (1 + part) * D + 8 * c;
+          for (int c = 0; c < 4; ++c) {
+            const float* bb = b + kVBQKV + (1 + part) * D + hc + 8 * c;
             __nv_bfloat162 p0 = __floats2bfloat162_rn(kv[8 * c] + bb[0], kv[8 * c + 1] + bb[1]);
             __nv_bfloat162 p1 = __floats2bfloat162_rn(kv[8 * c + 2] + bb[2], kv[8 * c + 3] + bb[3]);
             __nv_bfloat162 p2 = __floats2bfloat162_rn(kv[8 * c + 4] + bb[4], kv[8 * c + 5] + bb[5]);
@@ -406,55 +442,61 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
             u.y = *reinterpret_cast<uint32_t*>(&p1);
             u.z = *reinterpret_cast<uint32_t*>(&p2);
             u.w = *reinterpret_cast<uint32_t*>(&p3);
-            *reinterpret_cast<uint4*>(dst + (64 * part + 8 * c) * 2) = u;
+            *reinterpret_cast<uint4*>(dst + (64 * part + hc + 8 * c) * 2) = u;
           }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncthreads();
-      // attention of this query row over its AST's L keys (nn.py:79-96)
-      float c[D];
+      // attention of this query row over its AST's L keys, head wg
+      float c[DH];
 #pragma unroll
-      for (int i = 0; i < D; ++i) c[i] = 0.f;
+      for (int i = 0; i < DH; ++i) c[i] = 0.f;
       if (live) {
-        const int a = t / L, r0 = a * L;
-        const __nv_bfloat16* kvb = reinterpret_cast<const __nv_bfloat16*>(sKV);
+        const int r0 = (r / L) * L;
+        float s[kMaxLeafTC];
+        float m = -INFINITY;
+        for (int j = 0; j < L; ++j) {
+          {
+            const uint4* kr = reinterpret_cast<const uint4*>(sKV + ((r0 + j) * kKVLd + hc) * 2);
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float s[16];
-          float m = -INFINITY;
-          for (int j = 0; j < L; ++j) {
-            const __nv_bfloat162* kr =
-                reinterpret_cast<const __nv_bfloat162*>(kvb + (r0 + j) * kKVLd + hh * DH);
-            float acc = 0.f;
+            for (int i = 0; i < DH / 8; ++i) {
+              const uint4 u = kr[i];
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-            for (int i = 0; i < DH / 2; ++i) {
-              const float2 kf = __bfloat1622float2(kr[i]);
-              acc = fmaf(q[hh * DH + 2 * i], kf.x, fmaf(q[hh * DH + 2 * i + 1], kf.y, acc));
+              for (int e = 0; e < 4; ++e) {
+                const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+                acc[e] = fmaf(q[8 * i + 2 * e], kf.x, fmaf(q[8 * i + 2 * e + 1], kf.y, acc[e]));
+              }
             }
-            s[j] = acc * scale;
+            s[j] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * scale;
             m = fmaxf(m, s[j]);
           }
-          float sum = 0.f;
-          for (int j = 0; j < L; ++j) {
-            s[j] = expf(s[j] - m);
-            sum += s[j];
-          }
-          const float inv = 1.f / sum;
-          for (int j = 0; j < L; ++j) {
-            const float p = s[j] * inv;
-            const __nv_bfloat162* vr =
-                reinterpret_cast<const __nv_bfloat162*>(kvb + (r0 + j) * kKVLd + D + hh * DH);
+        }
+        float sum = 0.f;
+        for (int j = 0; j < L; ++j) {
+          s[j] = expf(s[j] - m);
+          sum += s[j];
+        }
+        const float inv = 1.f / sum;
+        for (int j = 0; j < L; ++j) {
+          const float pj = s[j] * inv;
+          const uint4* vr = reinterpret_cast<const uint4*>(sKV + ((r0 + j) * kKVLd + D + hc) * 2);
 #pragma unroll
-            for (int i = 0; i < DH / 2; ++i) {
-              const float2 vf = __bfloat1622float2(vr[i]);
-              c[hh * DH + 2 * i] = fmaf(p, vf.x, c[hh * DH + 2 * i]);
-              c[hh * DH + 2 * i + 1] = fmaf(p, vf.y, c[hh * DH + 2 * i + 1]);
+          for (int i = 0; i < DH / 8; ++i) {
+            const uint4 u = vr[i];
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+              c[8 * i + 2 * e] = fmaf(pj, vf.x, c[8 * i + 2 * e]);
+              c[8 * i + 2 * e + 1] = fmaf(pj, vf.y, c[8 * i + 2 * e + 1]);
             }
           }
         }
       }
-      store_row_bf16(sA, t, c);
+      store_half_row_bf16(sA, r, wg, c);
       sync_for_mma();
       TT(5 + li * 12);
       if (t == 0) {  // output projection
@@ -464,13 +506,14 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       }
       wait_mma(&bars[1], phase);
       TT(6 + li * 12);
-      float h1[D];
-      tmem_ld32(tlane, h1);
-      tmem_ld32(tlane + 32, h1 + 32);
+      float h1[DH];
+      {
+        tmem_ld32(tlane + DH * wg, h1);
 #pragma unroll
-      for (int i = 0; i < D; ++i) h1[i] += b[kVBO + i] + h[i];
-      ln_row(h1, b + kVLN1G, b + kVLN1B);
-      store_row_bf16(sA, t, h1);
+        for (int i = 0; i < DH; ++i) h1[i] += b[kVBO + DH * wg + i] + h[i];
+        ln_half(h1, b + kVLN1G, b + kVLN1B, wg, r, s_red);
+        store_half_row_bf16(sA, r, wg, h1);
+      }
       sync_for_mma();
       TT(7 + li * 12);
       if (t == 0) {  // FFN hidden (N = 128)
@@ -480,16 +523,15 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       }
       wait_mma(&bars[1], phase);
       TT(8 + li * 12);
-      {  // ReLU → F (two SW128 A tiles in the K|V region: the keys are dead)
+      {  // ReLU → F half wg (two SW128 A tiles in the K|V region: the keys are dead)
         float f[D];
-        for (int half = 0; half < 2; ++half) {
-          tmem_ld32(tlane + 64 * half, f);
-          tmem_ld32(tlane + 64 * half + 32, f + 32);
+        tmem_ld32(tlane + 64 * wg, f);
+        tmem_ld32(tlane + 64 * wg + 32, f + 32);
 #pragma unroll
-          for (int i = 0; i < D; ++i) f[i] = fmaxf(f[i] + b[kVFHB + 64 * half + i], 0.f);
-          store_row_bf16(sKV + half * TR * 128, t, f);
-        }
+        for (int i = 0; i < D; ++i) f[i] = fmaxf(f[i] + b[kVFHB + 64 * wg + i], 0.f);
+        store_row_bf16(sKV + wg * TR * 128, r, f);
       }
+      if (li + 1 == NLAY) load_x(tile + gridDim.x);
       sync_for_mma();
       TT(9 + li * 12);
       if (t == 0) {  // FFN out (K = 128)
@@ -506,17 +548,18 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
         mbar_arrive_expect_tx(&bars[2], (uint32_t)(g * kLeafChunkB));
         bulk_g2s(sA + boff, img + leaf_img_off(L), (uint32_t)(g * kLeafChunkB), &bars[2]);
       }
-      tmem_ld32(tlane, h);
-      tmem_ld32(tlane + 32, h + 32);
+      {
+        tmem_ld32(tlane + DH * wg, h);
 #pragma unroll
-      for (int i = 0; i < D; ++i) h[i] += b[kVFOB + i] + h1[i];
-      ln_row(h, b + kVLN2G, b + kVLN2B);
+        for (int i = 0; i < DH; ++i) h[i] += b[kVFOB + DH * wg + i] + h1[i];
+        ln_half(h, b + kVLN2G, b + kVLN2B, wg, r, s_red);
+        if (li + 1 < NLAY) store_half_row_bf16(sA, r, wg, h);
+        else if (live)  // leaf_embed A operand: chunk l = r mod L, row a = r / L
+          store_half_row_bf16(sA + (r % L) * leaf_chunk_a(L), r / L, wg, h);
+      }
       if (li + 1 < NLAY) {
-        store_row_bf16(sA, t, h);
         sync_for_mma();
         TT(11 + li * 12);
-      } else if (live) {  // leaf_embed A operand: chunk l = t mod L, row a = t / L
-        store_row_bf16(sA + (t % L) * leaf_chunk_a(L), t / L, h);
       }
     }
     TT(30);
@@ -560,7 +603,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     }
     wait_mma(&bars[1], phase);
     TT(25);
-    {  // z_x, device MLP and gate for AST t (t < A) → decoder operand row t
+    if (wg == 0) {  // z_x, device MLP and gate for AST t (t < A) → decoder operand row t
       float zx[DE];
       tmem_ld32(tlane, zx);  // warp-collective: every lane loads, rows ≥ A are ignored
       if (t < A) {
@@ -606,7 +649,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     }
     wait_mma(&bars[1], phase);
     TT(27);
-    {
+    if (wg == 0) {
       float u[DEC];
       tmem_ld32(tlane, u);
       tmem_ld32(tlane + 32, u + 32);
@@ -622,7 +665,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     }
     wait_mma(&bars[1], phase);
     TT(28);
-    {
+    if (wg == 0) {
       float u[DEC];
       tmem_ld32(tlane, u);
       tmem_ld32(tlane + 32, u + 32);

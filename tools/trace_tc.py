@@ -28,8 +28,8 @@ b = buf.cpu().numpy().reshape(8, 32)
 names = {0: "start", 1: "x->A", 2: "inproj mma", 3: "inproj epi"}
 for li in range(2):
     base = 4 + 12 * li
-    for k, nm in enumerate(["qkv mma", "qkv epi+attn", "attn->A", "wo mma", "ln1 epi", "ffn1 mma",
-                            "ffn1 epi", "ffn2 mma", "ln2 epi"]):
+    for k, nm in enumerate(["qkv mma", "qkv epi+attn", "wo mma", "ln1 epi", "ffn1 mma", "ffn1 epi",
+                            "ffn2 mma", "ln2 epi"]):
         names[base + k] = f"L{li} {nm}"
 names[25] = "leaf mma"
 names[26] = "zx+dev mlp+gate->A"
