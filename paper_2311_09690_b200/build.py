@@ -56,7 +56,8 @@ def _compile(src: Path, force: bool) -> tuple[Path, str]:
         newest = max(p.stat().st_mtime for p in _deps(src))
         if obj.stat().st_mtime >= newest:
             return obj, ""
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    extra = os.environ.get("TPCB_NVCC_EXTRA", "").split()  # debug builds, e.g. -DTPCB_TRACE_PHASES
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stderr}")

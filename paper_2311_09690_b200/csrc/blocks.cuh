@@ -114,11 +114,15 @@ __device__ __forceinline__ void layernorm_rows(const float* X, int ldx, float* Y
 __device__ __forceinline__ void attention_rows(const float* Q, const float* K, const float* V,
                                                int ld, float* C, int ldc, int A, int L, int H,
                                                int dh, float scale, float* P = nullptr) {
-  const int jobs = A * H * L;
+  // CP threads per (AST, head, query row) when the block has room: each
+  // recomputes the L scores and owns dh/CP context columns
+  const int CP = 1;  // (2-4 measured slower: the duplicated score chains dominate)
+  const int jobs = A * H * L * CP;
   for (int job = threadIdx.x; job < jobs; job += blockDim.x) {
-    const int i = job % L;
-    const int h = (job / L) % H;
-    const int a = job / (L * H);
+    const int cp = job % CP, q_job = job / CP;
+    const int i = q_job % L;
+    const int h = (q_job / L) % H;
+    const int a = q_job / (L * H);
     const float* q = Q + (a * L + i) * ld + h * dh;
     float p[TPCB_MAX_LEAF];
     float m = -INFINITY;
@@ -126,9 +130,14 @@ __device__ __forceinline__ void attention_rows(const float* Q, const float* K, c
     for (int j = 0; j < TPCB_MAX_LEAF; ++j) {
       if (j < L) {
         const float* k = K + (a * L + j) * ld + h * dh;
-        float s = 0.f;
-        for (int c = 0; c < dh; ++c) s = fmaf(q[c], k[c], s);
-        s *= scale;
+        float s0 = 0.f, s1 = 0.f;
+        int c = 0;
+        for (; c + 1 < dh; c += 2) {
+          s0 = fmaf(q[c], k[c], s0);
+          s1 = fmaf(q[c + 1], k[c + 1], s1);
+        }
+        if (c < dh) s0 = fmaf(q[c], k[c], s0);
+        float s = (s0 + s1) * scale;
         p[j] = s;
         m = fmaxf(m, s);
       }
@@ -146,14 +155,15 @@ __device__ __forceinline__ void attention_rows(const float* Q, const float* K, c
     for (int j = 0; j < TPCB_MAX_LEAF; ++j)
       if (j < L) p[j] = p[j] / sum;
     (void)inv;
-    if (P) {
+    if (P && cp == 0) {
       float* pp = P + ((a * H + h) * L + i) * L;
 #pragma unroll
       for (int j = 0; j < TPCB_MAX_LEAF; ++j)
         if (j < L) pp[j] = p[j];
     }
     float* c_out = C + (a * L + i) * ldc + h * dh;
-    for (int c = 0; c < dh; ++c) {
+    const int cw = dh / CP;
+    for (int c = cp * cw; c < (cp + 1) * cw; ++c) {
       float acc = 0.f;
 #pragma unroll
       for (int j = 0; j < TPCB_MAX_LEAF; ++j)
@@ -165,10 +175,46 @@ __device__ __forceinline__ void attention_rows(const float* Q, const float* K, c
 
 // z_x[a, e] = b[e] + Σ_{l<L, j<d} H[a*L + l, j] · W[l*d + j, e]
 // (flatten row-major then leaf_embed.{L}, costmodel.py:213-216).
+// Jobs = (AST, 4-column group, leaf position l); the L per-position partials
+// are summed in l order through `scratch` (A·L·de floats).  The summation
+// order depends only on L, never on the batch (the reference's exact batch
+// equivariance, test_costmodel.py:73-80).  Needs de % 4 == 0 and a 16-byte
+// aligned W, else the one-thread-per-output form below.
 __device__ __forceinline__ void leaf_embed_rows(const float* Hs, int ld, int A, int L, int d,
                                                 const float* __restrict__ W,
                                                 const float* __restrict__ b, int de, float* Z,
-                                                int ldz) {
+                                                int ldz, float* scratch) {
+  if ((de & 3) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0) {
+    const int ncg = de >> 2;
+    const int S = L;
+    for (int job = threadIdx.x; job < S * A * ncg; job += blockDim.x) {
+      const int cg = job % ncg, a = (job / ncg) % A, sl = job / (ncg * A);
+      const int l0 = sl * L / S, l1 = (sl + 1) * L / S;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int l = l0; l < l1; ++l) {
+        const float* h = Hs + (a * L + l) * ld;
+        const float4* w = reinterpret_cast<const float4*>(W + (size_t)l * d * de) + cg;
+#pragma unroll 4
+        for (int j = 0; j < d; ++j) {
+          const float x = h[j];
+          const float4 w4 = __ldg(w + (size_t)j * ncg);
+          acc.x = fmaf(x, w4.x, acc.x);
+          acc.y = fmaf(x, w4.y, acc.y);
+          acc.z = fmaf(x, w4.z, acc.z);
+          acc.w = fmaf(x, w4.w, acc.w);
+        }
+      }
+      *reinterpret_cast<float4*>(scratch + (sl * A + a) * de + 4 * cg) = acc;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < A * de; idx += blockDim.x) {
+      const int a = idx / de, e = idx - a * de;
+      float v = __ldg(b + e);
+      for (int sl = 0; sl < S; ++sl) v += scratch[(sl * A + a) * de + e];
+      Z[a * ldz + e] = v;
+    }
+    return;
+  }
   for (int job = threadIdx.x; job < A * de; job += blockDim.x) {
     const int e = job % de, a = job / de;
     float acc = __ldg(b + e);

@@ -22,6 +22,7 @@ struct FwdPlan {
   int R, ld, ldf;
   int H, C, V, Q, K, F, X0;             // encoder buffers
   int zx, zv, zp, z, u0, u1, dv, uw;    // head buffers (uw = max decoder width)
+  int ls;                               // leaf_embed slice partials (16-B aligned)
   int total;                            // floats
 };
 
@@ -56,6 +57,8 @@ FwdPlan make_fwd_plan(const Model& M, int R) {
   p.u0 = o; o += R * uw;
   p.u1 = o; o += R * uw;
   p.dv = o; o += R * TPCB_DEV_FEAT;
+  o = (o + 3) & ~3;
+  p.ls = o; o += max(4 * 256, R * M.d_e);
   p.total = max(end, o);
   return p;
 }
@@ -70,6 +73,18 @@ __device__ __forceinline__ double boxcox_decode(double e, const tpcb_boxcox& bc,
   }
   return pow(base, 1.0 / bc.lambda_bc) - bc.shift;
 }
+
+__device__ long long* g_trace_fwd = nullptr;
+int set_forward_trace(long long* d) {
+  TPCB_CUDA_CHECK(cudaMemcpyToSymbol(g_trace_fwd, &d, sizeof(d)));
+  return TPCB_OK;
+}
+// debug: per-phase timestamps of CTA 0 / thread 0, last 8 tiles (ring)
+#define FT(id)                                                                      \
+  do {                                                                              \
+    if (g_trace_fwd && blockIdx.x == 0 && threadIdx.x == 0)                         \
+      g_trace_fwd[(tcount & 7) * 32 + (id)] = clock64();                            \
+  } while (0)
 
 __global__ void __launch_bounds__(256) forward_kernel(
     Model M, const float* __restrict__ P, const float* __restrict__ x,
@@ -91,7 +106,11 @@ __global__ void __launch_bounds__(256) forward_kernel(
   float* X0 = sm + sp.X0;
   const float scale = 1.f / sqrtf((float)M.dh);
 
+  int tcount = -1;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    ++tcount;
+    FT(0);
+    if (g_trace_fwd && blockIdx.x == 0 && threadIdx.x == 0) g_trace_fwd[(tcount & 7) * 32 + 31] = tile_L[t];
     const int L = tile_L[t], first = tile_first[t], A = tile_count[t];
     const int rows = A * L;
     const float* xt = x + (size_t)t * R * TPCB_FEAT_PAD;
@@ -100,28 +119,36 @@ __global__ void __launch_bounds__(256) forward_kernel(
       X0[r * (TPCB_FEAT + 1) + c] = __ldg(xt + r * TPCB_FEAT_PAD + c);
     }
     __syncthreads();
+    FT(1);
     gemm_rows<4, 4>(X0, TPCB_FEAT + 1, P + M.inW, P + M.inb, H, ld, rows, TPCB_FEAT, d, false);
     __syncthreads();
+    FT(2);
     for (int li = 0; li < M.n_layers; ++li) {
       const LayerOff& lo = M.layer[li];
       gemm_rows<4, 4>(H, ld, P + lo.Wq, P + lo.bq, Q, ld, rows, d, d, false);
       gemm_rows<4, 4>(H, ld, P + lo.Wk, P + lo.bk, K, ld, rows, d, d, false);
       gemm_rows<4, 4>(H, ld, P + lo.Wv, P + lo.bv, V, ld, rows, d, d, false);
       __syncthreads();
+      FT(3 + 6 * li);
       attention_rows(Q, K, V, ld, C, ld, A, L, M.n_heads, M.dh, scale);
       __syncthreads();
+      FT(4 + 6 * li);
       // r1 = H + ctx Wo + bo  → V (dead after attention)
       gemm_rows<4, 4>(C, ld, P + lo.Wo, P + lo.bo, V, ld, rows, d, d, false, H, ld);
       __syncthreads();
+      FT(5 + 6 * li);
       layernorm_rows(V, ld, C, ld, rows, d, P + lo.ln1g, P + lo.ln1b);  // h1 → C
       __syncthreads();
+      FT(6 + 6 * li);
       gemm_rows<4, 4>(C, ld, P + lo.fhW, P + lo.fhb, F, ldf, rows, d, M.d_ff, true);
       __syncthreads();
       // r2 = h1 + relu(..) Wo2 + b → V
+      FT(7 + 6 * li);
       gemm_rows<4, 4>(F, ldf, P + lo.foW, P + lo.fob, V, ld, rows, M.d_ff, d, false, C, ld);
       __syncthreads();
       layernorm_rows(V, ld, H, ld, rows, d, P + lo.ln2g, P + lo.ln2b);
       __syncthreads();
+      FT(8 + 6 * li);
     }
     // ---------------------------------------------------------------- head
     float* zx = sm + sp.zx;
@@ -133,8 +160,11 @@ __global__ void __launch_bounds__(256) forward_kernel(
       const int a = idx / TPCB_DEV_FEAT, f = idx - a * TPCB_DEV_FEAT;
       dv[idx] = __ldg(devfeat + (size_t)perm[first + a] * TPCB_DEV_FEAT + f);
     }
-    leaf_embed_rows(H, ld, A, L, d, P + M.leafW[L], P + M.leafb[L], M.d_e, zx, M.d_e);
+    FT(20);
+    leaf_embed_rows(H, ld, A, L, d, P + M.leafW[L], P + M.leafb[L], M.d_e, zx, M.d_e,
+                    sm + sp.ls);
     __syncthreads();
+    FT(21);
     gemm_rows<1, 4>(dv, TPCB_DEV_FEAT, P + M.devhW, P + M.devhb, zv, M.d_dev, A, TPCB_DEV_FEAT,
                     M.d_dev, true);
     __syncthreads();
@@ -142,6 +172,7 @@ __global__ void __launch_bounds__(256) forward_kernel(
     __syncthreads();
     for (int idx = threadIdx.x; idx < A * M.d_e; idx += blockDim.x) z[idx] = zx[idx] * zp[idx];
     __syncthreads();
+    FT(22);
     const float* u = z;
     int w = M.d_e;
     float* ubuf[2] = {sm + sp.u0, sm + sp.u1};
@@ -152,6 +183,7 @@ __global__ void __launch_bounds__(256) forward_kernel(
       u = o;
       w = M.dec[j];
     }
+    FT(23);
     // final scalar: one warp per AST
     {
       const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -170,6 +202,7 @@ __global__ void __launch_bounds__(256) forward_kernel(
         }
       }
     }
+    FT(24);
     if (zx_out || z_out) {
       for (int idx = threadIdx.x; idx < A * M.d_e; idx += blockDim.x) {
         const int a = idx / M.d_e, e = idx - a * M.d_e;
