@@ -194,6 +194,10 @@ typedef struct {
  * change; zero-fill it once at allocation.  h_perm / h_tok_off: the
  * HOST bucket order (stable argsort of n_leaf) and the token offsets in it. */
 int32_t tpcb_forward_fits(const tpcb_model* m, int32_t rows_per_tile);
+/* preferred rows_per_tile for tpcb_forward: 128 when the desk-shaped fp32
+ * kernel applies (row-per-thread FFMA products over smem-staged weight
+ * tiles, csrc/forward_f32.cu), else 64 (the generic kernel). */
+int32_t tpcb_forward_rows(const tpcb_model* m);
 int tpcb_large_sizes(const tpcb_model* m, int64_t n_ast, int64_t n_tok, size_t* image_bytes,
                      size_t* act_bytes);
 /* flags: bit 0 = also the backward operands, bit 1 = entry table already

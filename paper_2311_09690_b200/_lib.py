@@ -83,6 +83,7 @@ SIGNATURES = {
     "tpcb_positional_encoding": (i32, [vp, i64, vp, vp, vp]),
     "tpcb_build_compact": (i32, [vp, vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp]),
     "tpcb_forward_fits": (i32, [vp, i32]),
+    "tpcb_forward_rows": (i32, [vp]),
     "tpcb_large_sizes": (i32, [vp, i64, i64, C.POINTER(sz), C.POINTER(sz)]),
     "tpcb_large_prepare": (i32, [vp, vp, vp, i32, vp]),
     "tpcb_large_forward": (i32, [vp, vp, vp, C.POINTER(Packed), vp, vp, vp, i64,

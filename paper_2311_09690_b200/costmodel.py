@@ -179,7 +179,8 @@ class Predictor:
     """Device-resident model: flat fp32 parameters + the model handle.
     The bulk inference entry point (`forward_batch`) of the GPU path."""
 
-    def __init__(self, params: CostModelParams, rows_per_tile: int = 64, precision: str = "fp32",
+    def __init__(self, params: CostModelParams, rows_per_tile: int | None = None,
+                 precision: str = "fp32",
                  path: str = "auto"):
         """precision "fp32": the parity mode (FP32 FFMA, decoded latency within
         1e-3 of the float64 reference); "bf16": encoder GEMMs on the tcgen05
@@ -196,7 +197,12 @@ class Predictor:
         self.dm = device_model(params.config)
         self.params = self.dm.upload(params.tensors)
         self.precision = precision
-        self.R = 128 if precision == "bf16" else rows_per_tile
+        if precision == "bf16":
+            self.R = 128
+        elif rows_per_tile is None:  # 128 for desk shapes (forward_f32.cu), else 64
+            self.R = int(_lib.load().tpcb_forward_rows(self.dm.handle))
+        else:
+            self.R = rows_per_tile
         self.status = engine.Status(self.params.device)
         # configs the fused one-CTA-per-tile kernels cannot hold (e.g.
         # full_reference_config) run layer by layer on the tensor cores

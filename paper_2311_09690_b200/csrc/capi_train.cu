@@ -356,12 +356,14 @@ int set_train3_trace(long long* d_trace);
 int set_train4_trace(long long* d_trace);
 int set_forward_tc_trace(long long* d_trace);
 int set_forward_trace(long long* d_trace);
+int set_forward_f32_trace(long long* d_trace);
 }
 extern "C" int tpcb_debug_train_trace(long long* d_trace) {
   int st = tpcb::set_train_trace(d_trace);
   if (!st) st = tpcb::set_train3_trace(d_trace);
   if (!st) st = tpcb::set_forward_tc_trace(d_trace);
   if (!st) st = tpcb::set_forward_trace(d_trace);
+  if (!st) st = tpcb::set_forward_f32_trace(d_trace);
   return st ? st : tpcb::set_train4_trace(d_trace);
 }
 

@@ -274,8 +274,24 @@ extern "C" int tpcb_metrics(const double* d_pred, const double* d_y, int64_t n, 
   return TPCB_OK;
 }
 
+namespace tpcb {
+bool f32_fast_supported(const Model& M);
+int launch_forward_f32(const Model& M, const float* d_params, const tpcb_packed* pk,
+                       const float* d_devfeat, const tpcb_boxcox* norm, float* d_pred,
+                       float* d_zx, float* d_zv, float* d_z, double* d_latency, int32_t* d_status,
+                       cudaStream_t stream);
+}  // namespace tpcb
+
+/* preferred rows per packed tile for tpcb_forward: 128 when the desk-shaped
+ * fp32 kernel (forward_f32.cu) applies, else 64 (the generic kernel) */
+extern "C" int32_t tpcb_forward_rows(const tpcb_model* m) {
+  if (!m) return 64;
+  return f32_fast_supported(m->dev) ? 128 : 64;
+}
+
 extern "C" int32_t tpcb_forward_fits(const tpcb_model* m, int32_t R) {
   if (!m || R < m->dev.n_leaf_max) return 0;
+  if (R == 128 && f32_fast_supported(m->dev)) return 1;
   return (size_t)make_fwd_plan(m->dev, R).total * sizeof(float) <= 227 * 1024 ? 1 : 0;
 }
 
@@ -287,6 +303,9 @@ extern "C" int tpcb_forward(const tpcb_model* m, const float* d_params, const tp
   if (n_ast < 1) return TPCB_ERR_EMPTY_BATCH;
   const int R = pk->rows_per_tile;
   if (R < m->dev.n_leaf_max) return TPCB_ERR_UNSUPPORTED;
+  if (R == 128 && f32_fast_supported(m->dev))  // desk shapes: forward_f32.cu
+    return launch_forward_f32(m->dev, d_params, pk, d_devfeat, norm, d_pred, d_zx, d_zv, d_z,
+                              d_latency, d_status, (cudaStream_t)stream_);
   FwdPlan sp = make_fwd_plan(m->dev, R);
   const size_t smem = (size_t)sp.total * sizeof(float);
   if (smem > 227 * 1024) return TPCB_ERR_UNSUPPORTED;

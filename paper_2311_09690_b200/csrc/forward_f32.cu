@@ -1,0 +1,545 @@
+// K2+K3, fp32 parity mode, desk-shaped models: the fused encoder + head
+// forward with one thread per packed row and warpgroup, FP32 FFMA products
+// against weight tiles staged in shared memory.
+//
+// Same network and arithmetic class as forward.cu (reference:
+// costmodel.py:193-269, nn.py:26-96, dataset.py:97-115): every product
+// accumulates in fp32, LayerNorm is two-pass, the Box-Cox decode is fp64.
+// The generic kernel (forward.cu) reads weights through L1 and tiles 64 rows
+// over 256 (row group × column group) threads; this one is built for the
+// desk shape:
+//
+//  * one CTA per 128-row packed tile (persistent over tiles), 256 threads:
+//    thread (r, wg) owns row r and the column half wg (= attention head wg);
+//    the residual stream lives in registers, split over the two threads of
+//    the row (LayerNorm combines the halves' partial sums through smem);
+//  * products are row × tile: the row's activations come from a padded smem
+//    row (LDS.128, conflict-free), the weights from a 16 KB smem slot read
+//    as warp-uniform LDS.128 broadcasts (one wavefront serves 32 lanes ×
+//    4 FFMA), 32 or 64 independent accumulators per thread;
+//  * weights stream from L2 (they are fp32 parameters, 16-B aligned, copied
+//    straight from the flat parameter vector) through a 4-slot ring by bulk
+//    async copies one phase ahead: per layer Wq Wk Wv Wo → slots 0 1 2 3,
+//    fhW → slots 0-1, foW → slots 2-3; the input projection and decoder
+//    weights stay resident; leaf_embed.L is staged into the K|V / FFN region
+//    once the encoder is done with it.
+#include <cmath>
+
+#include "async.cuh"
+#include "common.cuh"
+
+namespace tpcb {
+
+namespace {
+
+constexpr int D = 64, FF = 128, DE = 32, DDEV = 16, DEC = 64, NLAY = 2, DH = 32;
+constexpr int TR = 128;   // rows per tile
+constexpr int NTH = 256;  // two warpgroups
+constexpr int kMaxLeaf = 16;
+
+// ---- shared memory (bytes) ----
+constexpr int kSlotB = 64 * 64 * 4;            // ring slot: one 64 × 64 fp32 tile
+constexpr int kRing = 0;                       // 4 slots
+constexpr int LDA = 68;                        // activation row stride (floats)
+constexpr int kSmA = kRing + 4 * kSlotB;       // [128][68] activation rows
+constexpr int LDK = 132;                       // K|V and FFN-hidden row stride (floats)
+constexpr int kSmKV = kSmA + TR * LDA * 4;     // [128][132]: K|V, then F, then leaf_embed.L
+constexpr int kSmRes = kSmKV + TR * LDK * 4;   // resident: inW [24][64], dec0W [32][64], dec1W [64][64]
+constexpr int kResIn = 0, kResDec0 = TPCB_FEAT * D, kResDec1 = kResDec0 + DE * DEC;
+constexpr int kResFloats = kResDec1 + DEC * DEC;
+constexpr int kSmZx = kSmRes + kResFloats * 4;  // z_x rows [128][36]
+constexpr int LDZ = 36;
+constexpr int kSmVec = kSmZx + TR * LDZ * 4;    // biases / LN / head vectors
+constexpr int kVIn = 0, kVLayer = 64, kVLStride = 704;  // (same order as forward_tc / train4)
+constexpr int kVBQKV = 0, kVBO = 192, kVLN1G = 256, kVLN1B = 320, kVFHB = 384, kVFOB = 512,
+              kVLN2G = 576, kVLN2B = 640;
+constexpr int kVHead = kVLayer + NLAY * kVLStride;
+constexpr int kVHLeafB = 0;
+constexpr int kVHDevHW = kVHLeafB + (kMaxLeaf + 1) * DE;
+constexpr int kVHDevHB = kVHDevHW + TPCB_DEV_FEAT * DDEV;
+constexpr int kVHDevPW = kVHDevHB + DDEV;
+constexpr int kVHDevPB = kVHDevPW + DDEV * DE;
+constexpr int kVHDecB0 = kVHDevPB + DE;
+constexpr int kVHDecB1 = kVHDecB0 + DEC;
+constexpr int kVHOutW = kVHDecB1 + DEC;
+constexpr int kVHOutB = kVHOutW + DEC;
+constexpr int kVecFloats = kVHead + kVHOutB + 4;
+constexpr int kSmTotal = kSmVec + kVecFloats * 4;
+static_assert(kSmTotal <= 227 * 1024 - 2560, "forward_f32 shared memory (+ 2.1 KB static)");
+static_assert(kMaxLeaf * D * DE * 4 / 2 <= TR * LDK * 4, "leaf_embed group must fit");
+
+__device__ __forceinline__ void fence_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// acc[j] += Σ_{k<K} x[k] · W[k·ldw + j], j < NJ — x: this row (smem, 16-B
+// aligned), W: a warp-uniform smem tile (every lane reads the same float4)
+template <int NJ, int K>
+__device__ __forceinline__ void row_mm(float* acc, const float* x, const float* W, int ldw) {
+#pragma unroll 2
+  for (int k = 0; k < K; k += 4) {
+    const float4 x4 = *reinterpret_cast<const float4*>(x + k);
+    const float xs[4] = {x4.x, x4.y, x4.z, x4.w};
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const float* wr = W + (k + kk) * ldw;
+#pragma unroll
+      for (int j = 0; j < NJ; j += 4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(wr + j);
+        acc[j] = fmaf(xs[kk], w4.x, acc[j]);
+        acc[j + 1] = fmaf(xs[kk], w4.y, acc[j + 1]);
+        acc[j + 2] = fmaf(xs[kk], w4.z, acc[j + 2]);
+        acc[j + 3] = fmaf(xs[kk], w4.w, acc[j + 3]);
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void st_row(float* dst, const float* v, int n) {
+  for (int j = 0; j < n; j += 4)
+    *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+}
+
+// two-pass LayerNorm of a row split over (r, wg = 0/1), 32 columns each
+// (nn.py:48-54, eps 1e-5, biased variance); red: [4][TR]
+__device__ __forceinline__ void ln_half(float* v, const float* g, const float* b, int wg, int r,
+                                        float* red) {
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < DH; ++i) s += v[i];
+  red[wg * TR + r] = s;
+  __syncthreads();
+  const float mu = (red[r] + red[TR + r]) * (1.f / D);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < DH; ++i) {
+    const float t = v[i] - mu;
+    q = fmaf(t, t, q);
+  }
+  red[(2 + wg) * TR + r] = q;
+  __syncthreads();
+  const float inv = 1.f / sqrtf((red[2 * TR + r] + red[3 * TR + r]) * (1.f / D) + 1e-5f);
+#pragma unroll
+  for (int i = 0; i < DH; ++i) v[i] = fmaf(g[DH * wg + i], (v[i] - mu) * inv, b[DH * wg + i]);
+}
+
+__device__ __forceinline__ double boxcox_decode_f32(double e, const tpcb_boxcox& bc, bool* bad) {
+  const double t = e * bc.t_std + bc.t_mean;
+  if (fabs(bc.lambda_bc) < 1e-9) return exp(t) - bc.shift;
+  const double base = bc.lambda_bc * t + 1.0;
+  if (!(base > 0.0)) {
+    *bad = true;
+    return nan("");
+  }
+  return pow(base, 1.0 / bc.lambda_bc) - bc.shift;
+}
+
+__device__ long long* g_trace_f32 = nullptr;
+#define FT32(id)                                                                 \
+  do {                                                                           \
+    if (g_trace_f32 && blockIdx.x == 0 && t == 0)                                \
+      g_trace_f32[(tcount & 7) * 32 + (id)] = clock64();                         \
+  } while (0)
+
+__global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
+    const __grid_constant__ Model M, const float* __restrict__ P, const float* __restrict__ x,
+    const int32_t* __restrict__ tile_L, const int32_t* __restrict__ tile_first,
+    const int32_t* __restrict__ tile_count, const int32_t* __restrict__ n_tiles_p,
+    const int32_t* __restrict__ perm, const float* __restrict__ devfeat, tpcb_boxcox bc,
+    float* __restrict__ pred_out, float* __restrict__ zx_out, float* __restrict__ zv_out,
+    float* __restrict__ z_out, double* __restrict__ lat_out, int32_t* status) {
+  extern __shared__ __align__(1024) uint8_t smb[];
+  __shared__ __align__(8) uint64_t bars[6];  // [0..3] ring slots, [4] resident, [5] leaf stage
+  __shared__ float s_red[4 * TR];
+  const int t = threadIdx.x, wg = t >> 7, r = t & (TR - 1);
+  const int n_tiles = *n_tiles_p;
+  float* ring = reinterpret_cast<float*>(smb + kRing);
+  float* sA = reinterpret_cast<float*>(smb + kSmA);
+  float* sKV = reinterpret_cast<float*>(smb + kSmKV);
+  float* sRes = reinterpret_cast<float*>(smb + kSmRes);
+  float* sZx = reinterpret_cast<float*>(smb + kSmZx);
+  float* sv = reinterpret_cast<float*>(smb + kSmVec);
+  const float* hv = sv + kVHead;
+  if (t == 0) {
+    for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  // ring: slot s's k-th fill is waited with parity k & 1 (every thread waits
+  // every fill once, in the same order)
+  uint32_t par = 0, leaf_par = 0;
+  auto slot = [&](int s) { return ring + s * (kSlotB / 4); };
+  auto fill = [&](int s, const float* src, uint32_t bytes) {  // thread 0 only
+    mbar_arrive_expect_tx(&bars[s], bytes);
+    bulk_g2s(slot(s), src, bytes, &bars[s]);
+  };
+  auto wait_slot = [&](int s) {
+    mbar_wait(&bars[s], (par >> s) & 1u);
+    par ^= 1u << s;
+  };
+  // layer li's first four tiles (Wq Wk Wv Wo → slots 0..3)
+  auto fill_qkvo = [&](int li, int from_slot) {
+    const LayerOff& lo = M.layer[li];
+    const int off[4] = {lo.Wq, lo.Wk, lo.Wv, lo.Wo};
+    for (int s = from_slot; s < from_slot + 2; ++s) fill(s, P + off[s], kSlotB);
+  };
+
+  if (t == 0 && blockIdx.x < n_tiles) {
+    fill_qkvo(0, 0);
+    fill_qkvo(0, 2);
+    mbar_arrive_expect_tx(&bars[4], kResFloats * 4);
+    bulk_g2s(sRes + kResIn, P + M.inW, TPCB_FEAT * D * 4, &bars[4]);
+    bulk_g2s(sRes + kResDec0, P + M.decW[0], DE * DEC * 4, &bars[4]);
+    bulk_g2s(sRes + kResDec1, P + M.decW[1], DEC * DEC * 4, &bars[4]);
+  }
+  // biases / LayerNorm / head vectors
+  for (int i = t; i < D; i += NTH) sv[kVIn + i] = __ldg(P + M.inb + i);
+  for (int li = 0; li < NLAY; ++li) {
+    const LayerOff& lo = M.layer[li];
+    float* b = sv + kVLayer + li * kVLStride;
+    for (int i = t; i < D; i += NTH) {
+      b[kVBQKV + i] = __ldg(P + lo.bq + i);
+      b[kVBQKV + D + i] = __ldg(P + lo.bk + i);
+      b[kVBQKV + 2 * D + i] = __ldg(P + lo.bv + i);
+      b[kVBO + i] = __ldg(P + lo.bo + i);
+      b[kVLN1G + i] = __ldg(P + lo.ln1g + i);
+      b[kVLN1B + i] = __ldg(P + lo.ln1b + i);
+      b[kVFOB + i] = __ldg(P + lo.fob + i);
+      b[kVLN2G + i] = __ldg(P + lo.ln2g + i);
+      b[kVLN2B + i] = __ldg(P + lo.ln2b + i);
+    }
+    for (int i = t; i < FF; i += NTH) b[kVFHB + i] = __ldg(P + lo.fhb + i);
+  }
+  {
+    float* h = sv + kVHead;
+    for (int i = t; i < (kMaxLeaf + 1) * DE; i += NTH) {
+      const int L = i / DE;
+      h[kVHLeafB + i] = (L >= 1 && L <= M.n_leaf_max) ? __ldg(P + M.leafb[L] + (i - L * DE)) : 0.f;
+    }
+    for (int i = t; i < TPCB_DEV_FEAT * DDEV; i += NTH) h[kVHDevHW + i] = __ldg(P + M.devhW + i);
+    for (int i = t; i < DDEV * DE; i += NTH) h[kVHDevPW + i] = __ldg(P + M.devpW + i);
+    for (int i = t; i < DDEV; i += NTH) h[kVHDevHB + i] = __ldg(P + M.devhb + i);
+    for (int i = t; i < DE; i += NTH) h[kVHDevPB + i] = __ldg(P + M.devpb + i);
+    for (int i = t; i < DEC; i += NTH) {
+      h[kVHDecB0 + i] = __ldg(P + M.decb[0] + i);
+      h[kVHDecB1 + i] = __ldg(P + M.decb[1] + i);
+      h[kVHOutW + i] = __ldg(P + M.outW + i);
+    }
+    if (t == 0) h[kVHOutB] = __ldg(P + M.outb);
+  }
+  __syncthreads();
+  if (blockIdx.x < n_tiles) mbar_wait(&bars[4], 0);
+  const float scale = 1.f / sqrtf((float)DH);
+
+  // warpgroup 1 prefetches the next tile's input rows into registers
+  float xn[TPCB_FEAT];
+  auto load_x = [&](int tl) {
+    if (wg == 1 && tl < n_tiles) {
+      const float* xr = x + ((size_t)tl * TR + r) * TPCB_FEAT_PAD;
+#pragma unroll
+      for (int i = 0; i < TPCB_FEAT; i += 4) {
+        const float4 q4 = __ldg(reinterpret_cast<const float4*>(xr + i));
+        xn[i] = q4.x; xn[i + 1] = q4.y; xn[i + 2] = q4.z; xn[i + 3] = q4.w;
+      }
+    }
+  };
+  load_x(blockIdx.x);
+
+  int tcount = -1;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    ++tcount;
+    FT32(0);
+    const int L = tile_L[tile], first = tile_first[tile], A = tile_count[tile];
+    const bool live = r < A * L;
+    const bool has_next = tile + (int)gridDim.x < n_tiles;
+    float* xrow = sA + r * LDA;
+    if (wg == 1) {
+#pragma unroll
+      for (int i = 0; i < TPCB_FEAT; i += 4)
+        *reinterpret_cast<float4*>(xrow + i) =
+            live ? make_float4(xn[i], xn[i + 1], xn[i + 2], xn[i + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncthreads();
+    float h[DH];  // residual stream, columns 32·wg .. 32·wg+31
+#pragma unroll
+    for (int j = 0; j < DH; ++j) h[j] = sv[kVIn + DH * wg + j];
+    row_mm<DH, TPCB_FEAT>(h, xrow, sRes + kResIn + DH * wg, D);
+    __syncthreads();
+    st_row(xrow + DH * wg, h, DH);
+    __syncthreads();
+    FT32(1);
+
+    for (int li = 0; li < NLAY; ++li) {
+      const float* b = sv + kVLayer + li * kVLStride;
+      const LayerOff& lo = M.layer[li];
+      // ---- Q (registers), K and V (smem rows) of head wg
+      wait_slot(0);
+      wait_slot(1);
+      wait_slot(2);
+      float q[DH];
+#pragma unroll
+      for (int j = 0; j < DH; ++j) q[j] = b[kVBQKV + DH * wg + j];
+      row_mm<DH, D>(q, xrow, slot(0) + DH * wg, D);
+      {
+        float kv[DH];
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+#pragma unroll
+          for (int j = 0; j < DH; ++j) kv[j] = b[kVBQKV + (1 + part) * D + DH * wg + j];
+          row_mm<DH, D>(kv, xrow, slot(1 + part) + DH * wg, D);
+          st_row(sKV + r * LDK + part * D + DH * wg, kv, DH);
+        }
+      }
+      fence_async();
+      __syncthreads();
+      if (t == 0) {  // fhW → slots 0-1, foW rows 0..63 → slot 2
+        fill(0, P + lo.fhW, kSlotB);
+        fill(1, P + lo.fhW + 64 * 64, kSlotB);
+        fill(2, P + lo.foW, kSlotB);
+      }
+      FT32(2 + 6 * li);
+      // ---- attention of row r over its AST's L keys, head wg (nn.py:79-96)
+      float c[DH];
+#pragma unroll
+      for (int j = 0; j < DH; ++j) c[j] = 0.f;
+      if (live) {
+        const int r0 = (r / L) * L;
+        float s[kMaxLeaf];
+        float m = -INFINITY;
+        for (int jj = 0; jj < L; ++jj) {
+          const float* kr = sKV + (r0 + jj) * LDK + DH * wg;
+          float a4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int i = 0; i < DH; i += 4) {
+            const float4 k4 = *reinterpret_cast<const float4*>(kr + i);
+            a4[0] = fmaf(q[i], k4.x, a4[0]);
+            a4[1] = fmaf(q[i + 1], k4.y, a4[1]);
+            a4[2] = fmaf(q[i + 2], k4.z, a4[2]);
+            a4[3] = fmaf(q[i + 3], k4.w, a4[3]);
+          }
+          s[jj] = ((a4[0] + a4[1]) + (a4[2] + a4[3])) * scale;
+          m = fmaxf(m, s[jj]);
+        }
+        float sum = 0.f;
+        for (int jj = 0; jj < L; ++jj) {
+          s[jj] = expf(s[jj] - m);
+          sum += s[jj];
+        }
+        const float inv = 1.f / sum;
+        for (int jj = 0; jj < L; ++jj) {
+          const float pj = s[jj] * inv;
+          const float* vr = sKV + (r0 + jj) * LDK + D + DH * wg;
+#pragma unroll
+          for (int i = 0; i < DH; i += 4) {
+            const float4 v4 = *reinterpret_cast<const float4*>(vr + i);
+            c[i] = fmaf(pj, v4.x, c[i]);
+            c[i + 1] = fmaf(pj, v4.y, c[i + 1]);
+            c[i + 2] = fmaf(pj, v4.z, c[i + 2]);
+            c[i + 3] = fmaf(pj, v4.w, c[i + 3]);
+          }
+        }
+      }
+      st_row(xrow + DH * wg, c, DH);  // the QKV products are done with the h rows
+      __syncthreads();
+      FT32(3 + 6 * li);
+      // ---- output projection + residual + LayerNorm 1
+      wait_slot(3);
+      float h1[DH];
+#pragma unroll
+      for (int j = 0; j < DH; ++j) h1[j] = b[kVBO + DH * wg + j];
+      row_mm<DH, D>(h1, xrow, slot(3) + DH * wg, D);
+#pragma unroll
+      for (int j = 0; j < DH; ++j) h1[j] += h[j];
+      fence_async();
+      ln_half(h1, b + kVLN1G, b + kVLN1B, wg, r, s_red);  // (its barriers end the Wo reads)
+      if (t == 0) fill(3, P + lo.foW + 64 * 64, kSlotB);  // foW rows 64..127
+      st_row(xrow + DH * wg, h1, DH);
+      __syncthreads();
+      FT32(4 + 6 * li);
+      // ---- FFN hidden: columns 64·wg .. 64·wg+63 of relu(h1·fhW + b)
+      wait_slot(0);
+      wait_slot(1);
+      {
+        float f[2 * DH];
+#pragma unroll
+        for (int j = 0; j < 2 * DH; ++j) f[j] = b[kVFHB + 2 * DH * wg + j];
+        row_mm<2 * DH, D>(f, xrow, slot(0) + 2 * DH * wg, FF);
+#pragma unroll
+        for (int j = 0; j < 2 * DH; ++j) f[j] = fmaxf(f[j], 0.f);
+        st_row(sKV + r * LDK + 2 * DH * wg, f, 2 * DH);
+      }
+      if (wg == 1 && li + 1 == NLAY) load_x(tile + gridDim.x);
+      fence_async();
+      __syncthreads();
+      if (t == 0) {  // next layer's (or next tile's layer 0) Wq, Wk → slots 0, 1
+        if (li + 1 < NLAY) fill_qkvo(li + 1, 0);
+        else if (has_next) fill_qkvo(0, 0);
+      }
+      FT32(5 + 6 * li);
+      // ---- FFN out + residual + LayerNorm 2
+      wait_slot(2);
+      wait_slot(3);
+#pragma unroll
+      for (int j = 0; j < DH; ++j) h[j] = b[kVFOB + DH * wg + j];
+      row_mm<DH, FF>(h, sKV + r * LDK, slot(2) + DH * wg, D);
+#pragma unroll
+      for (int j = 0; j < DH; ++j) h[j] += h1[j];
+      fence_async();
+      ln_half(h, b + kVLN2G, b + kVLN2B, wg, r, s_red);  // (its barriers end the foW / F reads)
+      if (t == 0) {  // Wv, Wo → slots 2, 3
+        if (li + 1 < NLAY) fill_qkvo(li + 1, 2);
+        else if (has_next) fill_qkvo(0, 2);
+      }
+      st_row(xrow + DH * wg, h, DH);
+      __syncthreads();
+      FT32(6 + 6 * li);
+    }
+
+    // ---------------------------------------------------------------- head
+    // z_x[a] = b_L + Σ_l h[a·L + l] · W_L[l] (costmodel.py:213-216): jobs
+    // (AST a, 4-column group), leaf_embed.L staged in the dead K|V region in
+    // groups of ≤ 8 leaf positions (l-ordered single-chain sums)
+    const float* WL = P + M.leafW[L];
+    for (int g0 = 0; g0 < L; g0 += 8) {
+      const int gl = min(8, L - g0);
+      if (t == 0) {
+        mbar_arrive_expect_tx(&bars[5], (uint32_t)(gl * D * DE * 4));
+        bulk_g2s(sKV, WL + (size_t)g0 * D * DE, (uint32_t)(gl * D * DE * 4), &bars[5]);
+      }
+      mbar_wait(&bars[5], leaf_par);
+      leaf_par ^= 1u;
+      for (int job = t; job < A * (DE / 4); job += NTH) {
+        const int a = job >> 3, cg = job & 7;
+        float4 acc = g0 == 0 ? *reinterpret_cast<const float4*>(hv + kVHLeafB + L * DE + 4 * cg)
+                             : *reinterpret_cast<const float4*>(sZx + a * LDZ + 4 * cg);
+        for (int l = 0; l < gl; ++l) {
+          const float* hr = sA + (a * L + g0 + l) * LDA;
+          const float* w = sKV + l * D * DE + 4 * cg;
+#pragma unroll 4
+          for (int k = 0; k < D; k += 4) {
+            const float4 h4 = *reinterpret_cast<const float4*>(hr + k);
+            const float hs[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const float4 w4 = *reinterpret_cast<const float4*>(w + (k + kk) * DE);
+              acc.x = fmaf(hs[kk], w4.x, acc.x);
+              acc.y = fmaf(hs[kk], w4.y, acc.y);
+              acc.z = fmaf(hs[kk], w4.z, acc.z);
+              acc.w = fmaf(hs[kk], w4.w, acc.w);
+            }
+          }
+        }
+        *reinterpret_cast<float4*>(sZx + a * LDZ + 4 * cg) = acc;
+      }
+      fence_async();
+      __syncthreads();
+    }
+    FT32(20);
+    // device MLP, gate, decoder: thread (AST a = r, column half wg)
+    float* sU = sKV;  // decoder hidden rows [128][LDK]
+    const bool ast = r < A;
+    float z[DE];
+    if (ast) {
+      const int idx = perm[first + r];
+      float dv[TPCB_DEV_FEAT], zv[DDEV];
+#pragma unroll
+      for (int f = 0; f < TPCB_DEV_FEAT; ++f) dv[f] = __ldg(devfeat + (size_t)idx * TPCB_DEV_FEAT + f);
+#pragma unroll
+      for (int n = 0; n < DDEV; ++n) {
+        float sacc = hv[kVHDevHB + n];
+#pragma unroll
+        for (int f = 0; f < TPCB_DEV_FEAT; ++f) sacc = fmaf(dv[f], hv[kVHDevHW + f * DDEV + n], sacc);
+        zv[n] = fmaxf(sacc, 0.f);
+      }
+#pragma unroll
+      for (int n = 0; n < DE; ++n) {
+        float sacc = hv[kVHDevPB + n];
+#pragma unroll
+        for (int k = 0; k < DDEV; ++k) sacc = fmaf(zv[k], hv[kVHDevPW + k * DE + n], sacc);
+        z[n] = sZx[r * LDZ + n] * sacc;
+      }
+      if (wg == 0) {
+        if (zx_out)
+          for (int n = 0; n < DE; ++n) zx_out[(size_t)idx * DE + n] = sZx[r * LDZ + n];
+        if (z_out)
+          for (int n = 0; n < DE; ++n) z_out[(size_t)idx * DE + n] = z[n];
+        if (zv_out)
+          for (int n = 0; n < DDEV; ++n) zv_out[(size_t)idx * DDEV + n] = zv[n];
+      }
+    }
+    __syncthreads();  // both halves have read z_x row r
+    if (ast && wg == 0) st_row(sZx + r * LDZ, z, DE);  // z row: the first decoder product's input
+    __syncthreads();
+    {
+      float u[DH];
+#pragma unroll
+      for (int j = 0; j < DH; ++j) u[j] = hv[kVHDecB0 + DH * wg + j];
+      row_mm<DH, DE>(u, sZx + r * LDZ, sRes + kResDec0 + DH * wg, DEC);
+#pragma unroll
+      for (int j = 0; j < DH; ++j) u[j] = fmaxf(u[j], 0.f);
+      st_row(sU + r * LDK + DH * wg, u, DH);
+    }
+    __syncthreads();
+    {
+      float u[DH];
+#pragma unroll
+      for (int j = 0; j < DH; ++j) u[j] = hv[kVHDecB1 + DH * wg + j];
+      row_mm<DH, DEC>(u, sU + r * LDK, sRes + kResDec1 + DH * wg, DEC);
+      float part = 0.f;
+#pragma unroll
+      for (int j = 0; j < DH; ++j) part = fmaf(fmaxf(u[j], 0.f), hv[kVHOutW + DH * wg + j], part);
+      s_red[wg * TR + r] = part;
+    }
+    __syncthreads();
+    if (wg == 0 && ast) {
+      const float pred = hv[kVHOutB] + (s_red[r] + s_red[TR + r]);
+      const int idx = perm[first + r];
+      pred_out[idx] = pred;
+      if (lat_out) {
+        bool bad = false;
+        lat_out[idx] = bc.enabled ? boxcox_decode_f32((double)pred, bc, &bad) : (double)pred;
+        if (bad) raise_status(status, TPCB_ERR_DOMAIN);
+      }
+    }
+    FT32(21);
+    fence_async();
+    __syncthreads();  // K|V region (decoder rows) and z_x rows are rewritten by the next tile
+  }
+}
+
+}  // namespace
+
+bool f32_fast_supported(const Model& M) {
+  if (M.d != D || M.n_layers != NLAY || M.n_heads != 2 || M.dh != DH || M.d_ff != FF) return false;
+  if (M.d_e != DE || M.d_dev != DDEV || M.n_dec != 2 || M.dec[0] != DEC || M.dec[1] != DEC)
+    return false;
+  return M.n_leaf_max <= kMaxLeaf;
+}
+
+int set_forward_f32_trace(long long* d) {
+  TPCB_CUDA_CHECK(cudaMemcpyToSymbol(g_trace_f32, &d, sizeof(d)));
+  return TPCB_OK;
+}
+
+int launch_forward_f32(const Model& M, const float* d_params, const tpcb_packed* pk,
+                       const float* d_devfeat, const tpcb_boxcox* norm, float* d_pred,
+                       float* d_zx, float* d_zv, float* d_z, double* d_latency, int32_t* d_status,
+                       cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(forward_f32_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTotal));
+    attr = true;
+  }
+  tpcb_boxcox bc{};
+  if (norm) bc = *norm;
+  const int grid = (int)std::min<int64_t>(pk->n_tiles_max, (int64_t)kNumSMs);
+  forward_f32_kernel<<<grid, NTH, kSmTotal, stream>>>(
+      M, d_params, pk->x, pk->tile_L, pk->tile_first, pk->tile_count, pk->n_tiles, pk->perm,
+      d_devfeat, bc, d_pred, d_zx, d_zv, d_z, d_latency, d_status);
+  TPCB_LAUNCH_CHECK("forward_f32_kernel");
+  return TPCB_OK;
+}
+
+}  // namespace tpcb

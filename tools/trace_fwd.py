@@ -13,7 +13,8 @@ data = synth.generate(n, seed=0)
 dv = pb.device_vector(pb.DeviceSpec("synth0", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0)).astype(np.float32)
 rag = engine.RaggedHost(rows=data.vectors.astype(np.float32), ordering=data.ordering,
                         n_leaf=data.n_leaf, devfeat=np.tile(dv, (n, 1)), encoded=False)
-p = pb.Predictor(pb.init_params(pb.desk_config(seed=0)), precision="fp32")
+R = int(sys.argv[2]) if len(sys.argv) > 2 else None
+p = pb.Predictor(pb.init_params(pb.desk_config(seed=0)), precision="fp32", rows_per_tile=R)
 rows, ordering, leaf_off, devfeat = engine.upload_ragged(rag, torch.device("cuda"))
 f = lambda: p.forward_device(rows, ordering, leaf_off, devfeat, n, False, None, latents=False)  # noqa
 f()
@@ -25,11 +26,19 @@ f()
 torch.cuda.synchronize()
 lib.tpcb_debug_train_trace(None)
 b = buf.cpu().numpy().reshape(8, 32)
-names = {1: "x->smem", 2: "inproj", 20: "encoder", 21: "leaf_embed", 22: "dev mlp+gate",
-         23: "decoder", 24: "out+decode"}
-for li in range(2):
-    for k, nm in enumerate(["qkv", "attn", "wo", "ln1", "ffn1", "ffn2+ln2"]):
-        names[3 + 6 * li + k] = f"L{li} {nm}"
+if p.R == 128:  # forward_f32.cu (desk fast path)
+    names = {1: "x+inproj", 20: "leaf_embed", 21: "head+decoder"}
+    for li in range(2):
+        for k, nm in enumerate(["qkv", "attn", "wo+ln1", "ffn1", "ffn2+ln2"]):
+            names[2 + 6 * li + k] = f"L{li} {nm}"
+    end = 21
+else:
+    names = {1: "x->smem", 2: "inproj", 20: "encoder", 21: "leaf_embed", 22: "dev mlp+gate",
+             23: "decoder", 24: "out+decode"}
+    for li in range(2):
+        for k, nm in enumerate(["qkv", "attn", "wo", "ln1", "ffn1", "ffn2+ln2"]):
+            names[3 + 6 * li + k] = f"L{li} {nm}"
+    end = 24
 for tile in range(8):
     row = b[tile]
     ids = sorted([i for i in range(31) if row[i]], key=lambda i: row[i])
@@ -38,4 +47,4 @@ for tile in range(8):
     for i in ids[1:]:
         parts.append(f"{names.get(i, i)}:{row[i] - prev}")
         prev = row[i]
-    print(f"tile L={row[31]}: total {row[24] - row[0]} cycles | " + ", ".join(parts))
+    print(f"tile: total {row[end] - row[0]} cycles | " + ", ".join(parts))
