@@ -95,6 +95,35 @@ __device__ __forceinline__ void row_mm(float* acc, const float* x, const float* 
   }
 }
 
+// two-row register blocking: acc0/acc1 (rows x0/x1) share every weight
+// float4, halving the shared-memory loads per FFMA of row_mm
+template <int NJ, int K>
+__device__ __forceinline__ void row_mm2(float* acc0, float* acc1, const float* x0, const float* x1,
+                                        const float* W, int ldw) {
+#pragma unroll 2
+  for (int k = 0; k < K; k += 4) {
+    const float4 a4 = *reinterpret_cast<const float4*>(x0 + k);
+    const float4 b4 = *reinterpret_cast<const float4*>(x1 + k);
+    const float as[4] = {a4.x, a4.y, a4.z, a4.w}, bs[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const float* wr = W + (k + kk) * ldw;
+#pragma unroll
+      for (int j = 0; j < NJ; j += 4) {
+        const float4 w4 = *reinterpret_cast<const float4*>(wr + j);
+        acc0[j] = fmaf(as[kk], w4.x, acc0[j]);
+        acc0[j + 1] = fmaf(as[kk], w4.y, acc0[j + 1]);
+        acc0[j + 2] = fmaf(as[kk], w4.z, acc0[j + 2]);
+        acc0[j + 3] = fmaf(as[kk], w4.w, acc0[j + 3]);
+        acc1[j] = fmaf(bs[kk], w4.x, acc1[j]);
+        acc1[j + 1] = fmaf(bs[kk], w4.y, acc1[j + 1]);
+        acc1[j + 2] = fmaf(bs[kk], w4.z, acc1[j + 2]);
+        acc1[j + 3] = fmaf(bs[kk], w4.w, acc1[j + 3]);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void st_row(float* dst, const float* v, int n) {
   for (int j = 0; j < n; j += 4)
     *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -273,30 +302,48 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
     for (int li = 0; li < NLAY; ++li) {
       const float* b = sv + kVLayer + li * kVLStride;
       const LayerOff& lo = M.layer[li];
-      // ---- Q (registers), K and V (smem rows) of head wg
+      // ---- Q, K, V: thread (row pair p, p + 64; column quarter cq) — K, V
+      // rows to the K|V region, Q rows (after every thread has read the h
+      // rows) over the h rows; the attention threads (r, head) read them back
       wait_slot(0);
       wait_slot(1);
       wait_slot(2);
-      float q[DH];
-#pragma unroll
-      for (int j = 0; j < DH; ++j) q[j] = b[kVBQKV + DH * wg + j];
-      row_mm<DH, D>(q, xrow, slot(0) + DH * wg, D);
+      const int p = t & 63, cq = t >> 6;
+      const float* x0 = sA + p * LDA;
+      const float* x1 = sA + (p + 64) * LDA;
+      constexpr int QC = D / 4;  // 16 columns per quarter
       {
-        float kv[DH];
+        float k0[QC], k1[QC];
 #pragma unroll
         for (int part = 0; part < 2; ++part) {
 #pragma unroll
-          for (int j = 0; j < DH; ++j) kv[j] = b[kVBQKV + (1 + part) * D + DH * wg + j];
-          row_mm<DH, D>(kv, xrow, slot(1 + part) + DH * wg, D);
-          st_row(sKV + r * LDK + part * D + DH * wg, kv, DH);
+          for (int j = 0; j < QC; ++j) k0[j] = k1[j] = b[kVBQKV + (1 + part) * D + QC * cq + j];
+          row_mm2<QC, D>(k0, k1, x0, x1, slot(1 + part) + QC * cq, D);
+          st_row(sKV + p * LDK + part * D + QC * cq, k0, QC);
+          st_row(sKV + (p + 64) * LDK + part * D + QC * cq, k1, QC);
         }
       }
-      fence_async();
-      __syncthreads();
+      {
+        float q0[QC], q1[QC];
+#pragma unroll
+        for (int j = 0; j < QC; ++j) q0[j] = q1[j] = b[kVBQKV + QC * cq + j];
+        row_mm2<QC, D>(q0, q1, x0, x1, slot(0) + QC * cq, D);
+        fence_async();
+        __syncthreads();  // every h row read: Q overwrites them; slots 0..2 free
+        st_row(sA + p * LDA + QC * cq, q0, QC);
+        st_row(sA + (p + 64) * LDA + QC * cq, q1, QC);
+      }
       if (t == 0) {  // fhW → slots 0-1, foW rows 0..63 → slot 2
         fill(0, P + lo.fhW, kSlotB);
         fill(1, P + lo.fhW + 64 * 64, kSlotB);
         fill(2, P + lo.foW, kSlotB);
+      }
+      __syncthreads();
+      float q[DH];
+#pragma unroll
+      for (int j = 0; j < DH; j += 4) {
+        const float4 v4 = *reinterpret_cast<const float4*>(xrow + DH * wg + j);
+        q[j] = v4.x; q[j + 1] = v4.y; q[j + 2] = v4.z; q[j + 3] = v4.w;
       }
       FT32(2 + 6 * li);
       // ---- attention of row r over its AST's L keys, head wg (nn.py:79-96)
@@ -344,30 +391,47 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
       __syncthreads();
       FT32(3 + 6 * li);
       // ---- output projection + residual + LayerNorm 1
+      // (product by row pairs into the dead K|V rows, epilogue by (r, wg))
       wait_slot(3);
+      {
+        float o0[QC], o1[QC];
+#pragma unroll
+        for (int j = 0; j < QC; ++j) o0[j] = o1[j] = b[kVBO + QC * cq + j];
+        row_mm2<QC, D>(o0, o1, x0, x1, slot(3) + QC * cq, D);
+        st_row(sKV + p * LDK + QC * cq, o0, QC);
+        st_row(sKV + (p + 64) * LDK + QC * cq, o1, QC);
+      }
+      fence_async();
+      __syncthreads();  // Wo reads done, output rows complete
+      if (t == 0) fill(3, P + lo.foW + 64 * 64, kSlotB);  // foW rows 64..127
       float h1[DH];
 #pragma unroll
-      for (int j = 0; j < DH; ++j) h1[j] = b[kVBO + DH * wg + j];
-      row_mm<DH, D>(h1, xrow, slot(3) + DH * wg, D);
-#pragma unroll
-      for (int j = 0; j < DH; ++j) h1[j] += h[j];
-      fence_async();
-      ln_half(h1, b + kVLN1G, b + kVLN1B, wg, r, s_red);  // (its barriers end the Wo reads)
-      if (t == 0) fill(3, P + lo.foW + 64 * 64, kSlotB);  // foW rows 64..127
+      for (int j = 0; j < DH; j += 4) {
+        const float4 v4 = *reinterpret_cast<const float4*>(sKV + r * LDK + DH * wg + j);
+        h1[j] = v4.x + h[j]; h1[j + 1] = v4.y + h[j + 1];
+        h1[j + 2] = v4.z + h[j + 2]; h1[j + 3] = v4.w + h[j + 3];
+      }
+      ln_half(h1, b + kVLN1G, b + kVLN1B, wg, r, s_red);
       st_row(xrow + DH * wg, h1, DH);
       __syncthreads();
       FT32(4 + 6 * li);
-      // ---- FFN hidden: columns 64·wg .. 64·wg+63 of relu(h1·fhW + b)
+      // ---- FFN hidden relu(h1·fhW + b): thread (rows p, p + 64; columns
+      // 32·cq .. 32·cq+31)
       wait_slot(0);
       wait_slot(1);
       {
-        float f[2 * DH];
+        constexpr int FC = FF / 4;
+        float f0[FC], f1[FC];
 #pragma unroll
-        for (int j = 0; j < 2 * DH; ++j) f[j] = b[kVFHB + 2 * DH * wg + j];
-        row_mm<2 * DH, D>(f, xrow, slot(0) + 2 * DH * wg, FF);
+        for (int j = 0; j < FC; ++j) f0[j] = f1[j] = b[kVFHB + FC * cq + j];
+        row_mm2<FC, D>(f0, f1, x0, x1, slot(0) + FC * cq, FF);
 #pragma unroll
-        for (int j = 0; j < 2 * DH; ++j) f[j] = fmaxf(f[j], 0.f);
-        st_row(sKV + r * LDK + 2 * DH * wg, f, 2 * DH);
+        for (int j = 0; j < FC; ++j) {
+          f0[j] = fmaxf(f0[j], 0.f);
+          f1[j] = fmaxf(f1[j], 0.f);
+        }
+        st_row(sKV + p * LDK + FC * cq, f0, FC);
+        st_row(sKV + (p + 64) * LDK + FC * cq, f1, FC);
       }
       if (wg == 1 && li + 1 == NLAY) load_x(tile + gridDim.x);
       fence_async();
@@ -378,19 +442,30 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
       }
       FT32(5 + 6 * li);
       // ---- FFN out + residual + LayerNorm 2
+      // (product by row pairs into the dead h1 rows, epilogue by (r, wg))
       wait_slot(2);
       wait_slot(3);
+      {
+        float o0[QC], o1[QC];
 #pragma unroll
-      for (int j = 0; j < DH; ++j) h[j] = b[kVFOB + DH * wg + j];
-      row_mm<DH, FF>(h, sKV + r * LDK, slot(2) + DH * wg, D);
-#pragma unroll
-      for (int j = 0; j < DH; ++j) h[j] += h1[j];
+        for (int j = 0; j < QC; ++j) o0[j] = o1[j] = b[kVFOB + QC * cq + j];
+        row_mm2<QC, FF>(o0, o1, sKV + p * LDK, sKV + (p + 64) * LDK, slot(2) + QC * cq, D);
+        st_row(sA + p * LDA + QC * cq, o0, QC);
+        st_row(sA + (p + 64) * LDA + QC * cq, o1, QC);
+      }
       fence_async();
-      ln_half(h, b + kVLN2G, b + kVLN2B, wg, r, s_red);  // (its barriers end the foW / F reads)
+      __syncthreads();  // F / foW reads done, output rows complete
       if (t == 0) {  // Wv, Wo → slots 2, 3
         if (li + 1 < NLAY) fill_qkvo(li + 1, 2);
         else if (has_next) fill_qkvo(0, 2);
       }
+#pragma unroll
+      for (int j = 0; j < DH; j += 4) {
+        const float4 v4 = *reinterpret_cast<const float4*>(xrow + DH * wg + j);
+        h[j] = v4.x + h1[j]; h[j + 1] = v4.y + h1[j + 1];
+        h[j + 2] = v4.z + h1[j + 2]; h[j + 3] = v4.w + h1[j + 3];
+      }
+      ln_half(h, b + kVLN2G, b + kVLN2B, wg, r, s_red);
       st_row(xrow + DH * wg, h, DH);
       __syncthreads();
       FT32(6 + 6 * li);
@@ -401,6 +476,8 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
     // (AST a, 4-column group), leaf_embed.L staged in the dead K|V region in
     // groups of ≤ 8 leaf positions (l-ordered single-chain sums)
     const float* WL = P + M.leafW[L];
+    // jobs (AST a, 4-column group, leaf position l) write partial rows l·A + a
+    // of sZx; the partials are then summed in l order (batch-invariant)
     for (int g0 = 0; g0 < L; g0 += 8) {
       const int gl = min(8, L - g0);
       if (t == 0) {
@@ -409,92 +486,132 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
       }
       mbar_wait(&bars[5], leaf_par);
       leaf_par ^= 1u;
-      for (int job = t; job < A * (DE / 4); job += NTH) {
-        const int a = job >> 3, cg = job & 7;
-        float4 acc = g0 == 0 ? *reinterpret_cast<const float4*>(hv + kVHLeafB + L * DE + 4 * cg)
-                             : *reinterpret_cast<const float4*>(sZx + a * LDZ + 4 * cg);
-        for (int l = 0; l < gl; ++l) {
-          const float* hr = sA + (a * L + g0 + l) * LDA;
-          const float* w = sKV + l * D * DE + 4 * cg;
+      for (int job = t; job < A * gl * (DE / 4); job += NTH) {
+        const int cg = job & 7, rest = job >> 3, a = rest % A, l = rest / A;
+        const float* hr = sA + (a * L + g0 + l) * LDA;
+        const float* w = sKV + l * D * DE + 4 * cg;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 4
-          for (int k = 0; k < D; k += 4) {
-            const float4 h4 = *reinterpret_cast<const float4*>(hr + k);
-            const float hs[4] = {h4.x, h4.y, h4.z, h4.w};
+        for (int k = 0; k < D; k += 4) {
+          const float4 h4 = *reinterpret_cast<const float4*>(hr + k);
+          const float hs[4] = {h4.x, h4.y, h4.z, h4.w};
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const float4 w4 = *reinterpret_cast<const float4*>(w + (k + kk) * DE);
-              acc.x = fmaf(hs[kk], w4.x, acc.x);
-              acc.y = fmaf(hs[kk], w4.y, acc.y);
-              acc.z = fmaf(hs[kk], w4.z, acc.z);
-              acc.w = fmaf(hs[kk], w4.w, acc.w);
-            }
+          for (int kk = 0; kk < 4; ++kk) {
+            const float4 w4 = *reinterpret_cast<const float4*>(w + (k + kk) * DE);
+            acc.x = fmaf(hs[kk], w4.x, acc.x);
+            acc.y = fmaf(hs[kk], w4.y, acc.y);
+            acc.z = fmaf(hs[kk], w4.z, acc.z);
+            acc.w = fmaf(hs[kk], w4.w, acc.w);
           }
         }
-        *reinterpret_cast<float4*>(sZx + a * LDZ + 4 * cg) = acc;
+        *reinterpret_cast<float4*>(sZx + ((g0 + l) * A + a) * LDZ + 4 * cg) = acc;
       }
       fence_async();
       __syncthreads();
     }
+    for (int idx = t; idx < A * DE; idx += NTH) {  // row a = b_L + Σ_l partial(l, a), in place
+      const int a = idx / DE, n = idx - a * DE;
+      float v = hv[kVHLeafB + L * DE + n];
+      for (int l = 0; l < L; ++l) v += sZx[(l * A + a) * LDZ + n];
+      sZx[a * LDZ + n] = v;
+    }
+    __syncthreads();
     FT32(20);
     // device MLP, gate, decoder: thread (AST a = r, column half wg)
     float* sU = sKV;  // decoder hidden rows [128][LDK]
     const bool ast = r < A;
-    float z[DE];
-    if (ast) {
+    if (ast) {  // gate half: columns 16·wg .. 16·wg+15 of z = z_x ⊙ proj(relu(hidden(v)))
+      constexpr int HZ = DE / 2;
       const int idx = perm[first + r];
-      float dv[TPCB_DEV_FEAT], zv[DDEV];
+      float dv[TPCB_DEV_FEAT], zv[DDEV], zp[HZ];
 #pragma unroll
       for (int f = 0; f < TPCB_DEV_FEAT; ++f) dv[f] = __ldg(devfeat + (size_t)idx * TPCB_DEV_FEAT + f);
 #pragma unroll
-      for (int n = 0; n < DDEV; ++n) {
-        float sacc = hv[kVHDevHB + n];
+      for (int n = 0; n < DDEV; ++n) zv[n] = hv[kVHDevHB + n];
 #pragma unroll
-        for (int f = 0; f < TPCB_DEV_FEAT; ++f) sacc = fmaf(dv[f], hv[kVHDevHW + f * DDEV + n], sacc);
-        zv[n] = fmaxf(sacc, 0.f);
+      for (int f = 0; f < TPCB_DEV_FEAT; ++f)
+#pragma unroll
+        for (int n = 0; n < DDEV; n += 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(hv + kVHDevHW + f * DDEV + n);
+          zv[n] = fmaf(dv[f], w4.x, zv[n]);
+          zv[n + 1] = fmaf(dv[f], w4.y, zv[n + 1]);
+          zv[n + 2] = fmaf(dv[f], w4.z, zv[n + 2]);
+          zv[n + 3] = fmaf(dv[f], w4.w, zv[n + 3]);
+        }
+#pragma unroll
+      for (int n = 0; n < DDEV; ++n) zv[n] = fmaxf(zv[n], 0.f);
+#pragma unroll
+      for (int n = 0; n < HZ; ++n) zp[n] = hv[kVHDevPB + HZ * wg + n];
+#pragma unroll
+      for (int k = 0; k < DDEV; ++k)
+#pragma unroll
+        for (int n = 0; n < HZ; n += 4) {
+          const float4 w4 = *reinterpret_cast<const float4*>(hv + kVHDevPW + k * DE + HZ * wg + n);
+          zp[n] = fmaf(zv[k], w4.x, zp[n]);
+          zp[n + 1] = fmaf(zv[k], w4.y, zp[n + 1]);
+          zp[n + 2] = fmaf(zv[k], w4.z, zp[n + 2]);
+          zp[n + 3] = fmaf(zv[k], w4.w, zp[n + 3]);
+        }
+      float* zr = sZx + r * LDZ + HZ * wg;  // this half's z_x → z in place
+      float zx[HZ];
+#pragma unroll
+      for (int n = 0; n < HZ; ++n) {
+        zx[n] = zr[n];
+        zp[n] *= zx[n];
       }
-#pragma unroll
-      for (int n = 0; n < DE; ++n) {
-        float sacc = hv[kVHDevPB + n];
-#pragma unroll
-        for (int k = 0; k < DDEV; ++k) sacc = fmaf(zv[k], hv[kVHDevPW + k * DE + n], sacc);
-        z[n] = sZx[r * LDZ + n] * sacc;
+      if (zx_out)
+        for (int n = 0; n < HZ; ++n) zx_out[(size_t)idx * DE + HZ * wg + n] = zx[n];
+      if (z_out)
+        for (int n = 0; n < HZ; ++n) z_out[(size_t)idx * DE + HZ * wg + n] = zp[n];
+      if (zv_out && wg == 0)
+        for (int n = 0; n < DDEV; ++n) zv_out[(size_t)idx * DDEV + n] = zv[n];
+      st_row(zr, zp, HZ);
+    }
+    __syncthreads();  // z rows complete: the first decoder product's input
+    // decoder (costmodel.py:221-229): jobs (AST a, 4-column group) over all
+    // 256 threads; hidden rows in the K|V region
+    for (int job = t; job < A * (DEC / 4); job += NTH) {
+      const int a = job >> 4, cg = job & 15;
+      const float* zr = sZx + a * LDZ;
+      const float* w = sRes + kResDec0 + 4 * cg;
+      float4 acc = *reinterpret_cast<const float4*>(hv + kVHDecB0 + 4 * cg);
+#pragma unroll 8
+      for (int k = 0; k < DE; ++k) {
+        const float zk = zr[k];
+        const float4 w4 = *reinterpret_cast<const float4*>(w + k * DEC);
+        acc.x = fmaf(zk, w4.x, acc.x);
+        acc.y = fmaf(zk, w4.y, acc.y);
+        acc.z = fmaf(zk, w4.z, acc.z);
+        acc.w = fmaf(zk, w4.w, acc.w);
       }
-      if (wg == 0) {
-        if (zx_out)
-          for (int n = 0; n < DE; ++n) zx_out[(size_t)idx * DE + n] = sZx[r * LDZ + n];
-        if (z_out)
-          for (int n = 0; n < DE; ++n) z_out[(size_t)idx * DE + n] = z[n];
-        if (zv_out)
-          for (int n = 0; n < DDEV; ++n) zv_out[(size_t)idx * DDEV + n] = zv[n];
+      *reinterpret_cast<float4*>(sU + a * LDK + 4 * cg) =
+          make_float4(fmaxf(acc.x, 0.f), fmaxf(acc.y, 0.f), fmaxf(acc.z, 0.f), fmaxf(acc.w, 0.f));
+    }
+    __syncthreads();
+    for (int job = t; job < A * (DEC / 4); job += NTH) {
+      const int a = job >> 4, cg = job & 15;
+      const float* ur = sU + a * LDK;
+      const float* w = sRes + kResDec1 + 4 * cg;
+      float4 acc = *reinterpret_cast<const float4*>(hv + kVHDecB1 + 4 * cg);
+#pragma unroll 8
+      for (int k = 0; k < DEC; ++k) {
+        const float uk = ur[k];
+        const float4 w4 = *reinterpret_cast<const float4*>(w + k * DEC);
+        acc.x = fmaf(uk, w4.x, acc.x);
+        acc.y = fmaf(uk, w4.y, acc.y);
+        acc.z = fmaf(uk, w4.z, acc.z);
+        acc.w = fmaf(uk, w4.w, acc.w);
       }
-    }
-    __syncthreads();  // both halves have read z_x row r
-    if (ast && wg == 0) st_row(sZx + r * LDZ, z, DE);  // z row: the first decoder product's input
-    __syncthreads();
-    {
-      float u[DH];
-#pragma unroll
-      for (int j = 0; j < DH; ++j) u[j] = hv[kVHDecB0 + DH * wg + j];
-      row_mm<DH, DE>(u, sZx + r * LDZ, sRes + kResDec0 + DH * wg, DEC);
-#pragma unroll
-      for (int j = 0; j < DH; ++j) u[j] = fmaxf(u[j], 0.f);
-      st_row(sU + r * LDK + DH * wg, u, DH);
+      *reinterpret_cast<float4*>(sU + a * LDK + DEC + 4 * cg) =
+          make_float4(fmaxf(acc.x, 0.f), fmaxf(acc.y, 0.f), fmaxf(acc.z, 0.f), fmaxf(acc.w, 0.f));
     }
     __syncthreads();
-    {
-      float u[DH];
-#pragma unroll
-      for (int j = 0; j < DH; ++j) u[j] = hv[kVHDecB1 + DH * wg + j];
-      row_mm<DH, DEC>(u, sU + r * LDK, sRes + kResDec1 + DH * wg, DEC);
-      float part = 0.f;
-#pragma unroll
-      for (int j = 0; j < DH; ++j) part = fmaf(fmaxf(u[j], 0.f), hv[kVHOutW + DH * wg + j], part);
-      s_red[wg * TR + r] = part;
-    }
-    __syncthreads();
-    if (wg == 0 && ast) {
-      const float pred = hv[kVHOutB] + (s_red[r] + s_red[TR + r]);
-      const int idx = perm[first + r];
+    if (t < A) {
+      float pred = hv[kVHOutB];
+      const float* ur = sU + t * LDK + DEC;
+#pragma unroll 8
+      for (int j = 0; j < DEC; ++j) pred = fmaf(ur[j], hv[kVHOutW + j], pred);
+      const int idx = perm[first + t];
       pred_out[idx] = pred;
       if (lat_out) {
         bool bad = false;
