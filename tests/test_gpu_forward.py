@@ -196,3 +196,40 @@ def test_forward_large_random_vs_oracle():
                                      np.stack([e.device_vector for e in inputs]))
     assert np.all(np.abs(pred - want) <= 2e-5 * (1 + np.abs(want)))
     assert np.all(np.abs(lat.z - wz) <= 2e-5 * (1 + np.abs(wz)))
+
+
+@pytest.mark.parametrize("R", [128, 64])
+def test_forward_desk_every_leaf_count_both_kernels(R):
+    """The desk fp32 kernel (forward_f32.cu, 128-row tiles; leaf_embed staged in
+    groups of 8 leaf positions, so L = 9..16 takes the multi-group path) and
+    the generic kernel (64-row tiles) against the float64 oracle on every leaf
+    count 1..16; same 2e-5·(1+|ref|) bar as the reference-config tests."""
+    pb = _pb()
+    cfg = pb.desk_config(seed=0)
+    params = pb.init_params(cfg)
+    rng = np.random.default_rng(11)
+    n_leaf = np.concatenate([np.full(int(rng.integers(30, 200)), L) for L in range(1, 17)])
+    rng.shuffle(n_leaf)
+    n = len(n_leaf)
+    vec = rng.uniform(0.0, 8.0, size=(int(n_leaf.sum()), 24))
+    ordering = np.concatenate([rng.permutation(28)[:L] for L in n_leaf]).astype(np.int32)
+    synth = pb.DeviceSpec("synth0", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0)
+    batch = pb.CompactBatch(vec, ordering, n_leaf.astype(np.int64), np.zeros(n, np.int32), [synth])
+    p = pb.Predictor(params, rows_per_tile=R)
+    assert p.R == R
+    pred, zx, zv, z, _ = p.forward_batch(batch, latents=True)
+    off = np.concatenate([[0], np.cumsum(n_leaf)])
+    x = [of.encode_rows(vec[off[i]:off[i + 1]], ordering[off[i]:off[i + 1]]) for i in range(n)]
+    dv = of.device_features(1000.0, 16.0, 1024.0, 16, 2048.0, 4.0)
+    ref = op.forward(params.tensors, _dims(cfg), x, np.tile(dv, (n, 1)))
+    tol = lambda w: 2e-5 * (1.0 + np.abs(w))  # noqa: E731
+    assert np.all(np.abs(pred - ref[0]) <= tol(ref[0])), np.abs(pred - ref[0]).max()
+    for got, want, k in ((zx, ref[1], "z_x"), (zv, ref[2], "z_v"), (z, ref[3], "z")):
+        assert np.all(np.abs(got - want) <= tol(want)), k
+
+
+def test_forward_desk_default_tiles_use_the_desk_kernel():
+    pb = _pb()
+    assert pb.Predictor(pb.init_params(pb.desk_config(seed=0))).R == 128
+    small = pb.desk_config(seed=0, d_model=32, d_ff=64, d_embed=16)
+    assert pb.Predictor(pb.init_params(small)).R == 64
