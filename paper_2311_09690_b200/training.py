@@ -165,7 +165,8 @@ class Trainer:
         if valid_rag is not None:
             rows_, ordering, leaf_off, devfeat = engine.upload_ragged(valid_rag, device)
             self.valid_pk = engine.pack(rows_, ordering, leaf_off, valid_rag.n_ast, n_max,
-                                        valid_rag.encoded, self.status)
+                                        valid_rag.encoded, self.status,
+                                        int(_lib.load().tpcb_forward_rows(self.dm.handle)))
             self.valid_devfeat = devfeat
             self.valid_y = torch.from_numpy(np.asarray(valid_latency, dtype=np.float64)).to(device)
             self.valid = valid_rag
