@@ -458,6 +458,11 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
       if (t == 0) {  // Wv, Wo → slots 2, 3
         if (li + 1 < NLAY) fill_qkvo(li + 1, 2);
         else if (has_next) fill_qkvo(0, 2);
+        if (li + 1 == NLAY) {  // K|V region now dead: stage leaf_embed.L group 0
+          const uint32_t b0 = (uint32_t)(min(8, L) * D * DE * 4);  // under LN2
+          mbar_arrive_expect_tx(&bars[5], b0);
+          bulk_g2s(sKV, P + M.leafW[L], b0, &bars[5]);
+        }
       }
 #pragma unroll
       for (int j = 0; j < DH; j += 4) {
@@ -480,7 +485,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
     // of sZx; the partials are then summed in l order (batch-invariant)
     for (int g0 = 0; g0 < L; g0 += 8) {
       const int gl = min(8, L - g0);
-      if (t == 0) {
+      if (t == 0 && g0 > 0) {  // group 0 was issued after the last FFN out
         mbar_arrive_expect_tx(&bars[5], (uint32_t)(gl * D * DE * 4));
         bulk_g2s(sKV, WL + (size_t)g0 * D * DE, (uint32_t)(gl * D * DE * 4), &bars[5]);
       }
