@@ -351,11 +351,13 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
 #pragma unroll
       for (int j = 0; j < DH; ++j) c[j] = 0.f;
       if (live) {
+        // one pass over the keys with a running max (no score array, so no
+        // stack frame): the context is rescaled only when the max grows
         const int r0 = (r / L) * L;
-        float s[kMaxLeaf];
-        float m = -INFINITY;
+        float m = -INFINITY, sum = 0.f;
         for (int jj = 0; jj < L; ++jj) {
           const float* kr = sKV + (r0 + jj) * LDK + DH * wg;
+          const float* vr = sKV + (r0 + jj) * LDK + D + DH * wg;
           float a4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int i = 0; i < DH; i += 4) {
@@ -365,18 +367,16 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
             a4[2] = fmaf(q[i + 2], k4.z, a4[2]);
             a4[3] = fmaf(q[i + 3], k4.w, a4[3]);
           }
-          s[jj] = ((a4[0] + a4[1]) + (a4[2] + a4[3])) * scale;
-          m = fmaxf(m, s[jj]);
-        }
-        float sum = 0.f;
-        for (int jj = 0; jj < L; ++jj) {
-          s[jj] = expf(s[jj] - m);
-          sum += s[jj];
-        }
-        const float inv = 1.f / sum;
-        for (int jj = 0; jj < L; ++jj) {
-          const float pj = s[jj] * inv;
-          const float* vr = sKV + (r0 + jj) * LDK + D + DH * wg;
+          const float sj = ((a4[0] + a4[1]) + (a4[2] + a4[3])) * scale;
+          if (sj > m) {
+            const float alpha = expf(m - sj);  // 0 on the first key
+            sum *= alpha;
+#pragma unroll
+            for (int i = 0; i < DH; ++i) c[i] *= alpha;
+            m = sj;
+          }
+          const float pj = expf(sj - m);
+          sum += pj;
 #pragma unroll
           for (int i = 0; i < DH; i += 4) {
             const float4 v4 = *reinterpret_cast<const float4*>(vr + i);
@@ -386,6 +386,9 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
             c[i + 3] = fmaf(pj, v4.w, c[i + 3]);
           }
         }
+        const float inv = 1.f / sum;
+#pragma unroll
+        for (int i = 0; i < DH; ++i) c[i] *= inv;
       }
       st_row(xrow + DH * wg, c, DH);  // the QKV products are done with the h rows
       __syncthreads();

@@ -453,36 +453,34 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
 #pragma unroll
       for (int i = 0; i < DH; ++i) c[i] = 0.f;
       if (live) {
+        // one pass over the keys with a running max (no score array, so no
+        // stack frame): the context is rescaled only when the max grows
         const int r0 = (r / L) * L;
-        float s[kMaxLeafTC];
-        float m = -INFINITY;
+        float m = -INFINITY, sum = 0.f;
         for (int j = 0; j < L; ++j) {
-          {
-            const uint4* kr = reinterpret_cast<const uint4*>(sKV + ((r0 + j) * kKVLd + hc) * 2);
-            float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int i = 0; i < DH / 8; ++i) {
-              const uint4 u = kr[i];
-              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
-                acc[e] = fmaf(q[8 * i + 2 * e], kf.x, fmaf(q[8 * i + 2 * e + 1], kf.y, acc[e]));
-              }
-            }
-            s[j] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * scale;
-            m = fmaxf(m, s[j]);
-          }
-        }
-        float sum = 0.f;
-        for (int j = 0; j < L; ++j) {
-          s[j] = expf(s[j] - m);
-          sum += s[j];
-        }
-        const float inv = 1.f / sum;
-        for (int j = 0; j < L; ++j) {
-          const float pj = s[j] * inv;
+          const uint4* kr = reinterpret_cast<const uint4*>(sKV + ((r0 + j) * kKVLd + hc) * 2);
           const uint4* vr = reinterpret_cast<const uint4*>(sKV + ((r0 + j) * kKVLd + D + hc) * 2);
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int i = 0; i < DH / 8; ++i) {
+            const uint4 u = kr[i];
+            const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+              acc[e] = fmaf(q[8 * i + 2 * e], kf.x, fmaf(q[8 * i + 2 * e + 1], kf.y, acc[e]));
+            }
+          }
+          const float sj = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * scale;
+          if (sj > m) {
+            const float alpha = expf(m - sj);  // 0 on the first key
+            sum *= alpha;
+#pragma unroll
+            for (int i = 0; i < DH; ++i) c[i] *= alpha;
+            m = sj;
+          }
+          const float pj = expf(sj - m);
+          sum += pj;
 #pragma unroll
           for (int i = 0; i < DH / 8; ++i) {
             const uint4 u = vr[i];
@@ -495,6 +493,9 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
             }
           }
         }
+        const float inv = 1.f / sum;
+#pragma unroll
+        for (int i = 0; i < DH; ++i) c[i] *= inv;
       }
       store_half_row_bf16(sA, r, wg, c);
       sync_for_mma();
