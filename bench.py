@@ -322,10 +322,6 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     lib = _lib.load()
     cfg = pb.desk_config(seed=0, batch_size=args.batch_size)
-    from paper_2311_09690_b200 import _lib as _l
-    _l.load().tpcb_debug_overlap(int(args.overlap))
-    if args.poll_ns:
-        _l.load().tpcb_debug_poll_ns(int(args.poll_ns))
     data, train, valid = make_data()
     norm = fit_boxcox(train.latency)
     targets = norm.encode(train.latency)
@@ -340,7 +336,7 @@ def run_ours(args):
     loss = engine.loss_struct("hybrid", cfg.lambda_hybrid, norm.loss_offset, 0.0, 5,
                               "transformed", norm)
     tr = Trainer(cfg, params.tensors, rag_of(train, dv), targets, loss, rag_of(valid, dv),
-                 valid.latency, norm, device=dev, comm=comm)
+                 valid.latency, norm, device=dev, comm=comm, overlap=bool(args.overlap))
     rng = np.random.default_rng(cfg.seed)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -515,7 +511,6 @@ def main():
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: reduce + Adam of each step overlapped with its backward (default); "
                          "0: sequential reduce kernel (A/B)")
-    ap.add_argument("--poll-ns", type=int, default=0, help="debug: stage-wait poll interval")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -225,14 +225,6 @@ int tpcb_large_loss_backward(const tpcb_model* m, const float* d_params, const v
                              const int32_t* d_tok_off, int64_t n_batch, const tpcb_loss* loss, double n_norm, void* d_ws,
                              size_t ws_bytes, float* d_grad, double* d_loss, int32_t* d_status,
                              void* stream);
-/* debug: k-slab width of the large-path GEMM (16: 64-B swizzle, deeper
- * pipeline — default; 32: 128-B swizzle) */
-void tpcb_debug_gemm_bk(int32_t bk);
-/* debug: 1 enables 2x2 / 2x1 / 1x2 TMA-multicast clusters for that GEMM
- * (default off: measured no gain, the per-SM shared-memory fill rate binds) */
-void tpcb_debug_gemm_cluster(int32_t on);
-/* debug: 1 = the GEMM streams its operands but skips the MMAs (probe) */
-void tpcb_debug_gemm_mode(int32_t mode);
 /* the GEMM alone: C[M,N] = A[M,K] B[N,K]^T, fp32 row-major in/out (3xTF32) */
 size_t tpcb_gemm3_ws(int64_t M, int32_t N, int32_t K);
 int tpcb_gemm3(const float* d_a, const float* d_b, int64_t M, int32_t N, int32_t K, float* d_c,
@@ -267,6 +259,13 @@ typedef struct {
   double* scalars;      /* [8]: [0] CMD value, [1] loss value */
   int64_t zall_floats;  /* size of zall (global rows × d_embed) */
   int32_t l_cap;        /* largest leaf count among the samples (≤ n_leaf_max) */
+  /* overlapped reduce + optimizer (single GPU, no CMD): per-backward-stage
+   * completion counters owned by this workspace, stage_flag_words long
+   * (tpcb_train_ws_sizes); NULL runs the step's reduction sequentially after
+   * the training kernel.  The overlap is taken only when every training CTA
+   * of a step is co-resident with the reduce blocks (occupancy check). */
+  uint64_t* stage_flags;
+  int64_t stage_flag_words;
 } tpcb_train_ws;
 
 /* epoch plan: steps[s] = 8 × int32 {offset into d_batch, n_src, n_tgt,
@@ -281,7 +280,8 @@ typedef struct {
 } tpcb_plan;
 
 int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t l_cap, int32_t* n_slots,
-                        int64_t* slot_stride, int64_t* zall_floats, int64_t* terms_doubles);
+                        int64_t* slot_stride, int64_t* zall_floats, int64_t* terms_doubles,
+                        int64_t* stage_flag_words);
 /* refresh the transposed copy of every 2-D weight (read by the backward) */
 int tpcb_transpose_params(const tpcb_model* m, const float* d_params, float* d_params_t,
                           void* stream);
@@ -299,6 +299,13 @@ int tpcb_loss_backward(const tpcb_model* m, const float* d_params, const float* 
 int tpcb_optimizer_step(const tpcb_model* m, int64_t n, float* d_params, float* d_params_t,
                         const float* d_grad, float* d_m, float* d_v, const tpcb_optim* opt,
                         double lr, int64_t t, void* stream);
+/* float64 optimizer step for the drop-in nn.Adam / nn.Sgd (nn.py:136-167):
+ * d_params / d_grad / d_m / d_v float64 [n] (m, v Adam only, zero before the
+ * first step); bc1 = 1 - beta1**t, bc2 = 1 - beta2**t computed by the caller.
+ * Same IEEE operation sequence as the reference's numpy update (bit-exact). */
+int tpcb_optimizer_step_f64(int64_t n, double* d_params, const double* d_grad, double* d_m,
+                            double* d_v, const tpcb_optim* opt, double lr, double bc1,
+                            double bc2, void* stream);
 /* ---- data parallel: NCCL communicator (one process per GPU) --------------
  * rank 0 creates the id, the host broadcasts it (torch.distributed), every
  * rank creates its communicator; tpcb_train_epoch all-reduces each step's
@@ -411,22 +418,6 @@ int tpcb_kmeans_changed(const int64_t* d_a, const int64_t* d_b, int64_t n, int32
 int tpcb_distance_table(const double* d_feats, const int64_t* d_task_off, int32_t n_tasks,
                         int32_t d, const double* d_centers, int32_t kappa, double* d_psi,
                         void* stream);
-
-/* debug: per-weight-op timestamps (clock64 pairs) of CTA 0 of the training
- * kernel into d_trace[512] (NULL disables) — tools/trace_train.py */
-int tpcb_debug_train_trace(long long* d_trace);
-/* debug: training-kernel selection — 0 automatic (the desk fast path v4 where
- * the config matches, else the generic v2), 2 generic, 3 warp-group, 4 fast path */
-int tpcb_debug_train_impl(int32_t impl);
-/* debug: overlapped reduce + optimizer (the step's gradient reduction and Adam
- * on the SMs the training kernel leaves idle, stage by stage): 1 on (default),
- * 0 off (sequential reduce kernel), 2 stage publishing on but the reduce
- * sequential (overhead A/B), >= 16 on with at most that many reduce blocks */
-int tpcb_debug_overlap(int32_t on);
-/* debug: poll interval (ns) of the overlapped reduce's stage waits (default 512) */
-int tpcb_debug_poll_ns(int32_t ns);
-/* debug: cap the training grid so CTAs loop over several samples (0 = no cap) */
-int tpcb_debug_grid_cap(int32_t cap);
 
 /* ---- measurement helpers (bench.py) -------------------------------------
  * FP32 FFMA throughput of this GPU in TFLOP/s (d_scratch: >= 1184 floats);

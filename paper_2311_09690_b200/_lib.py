@@ -60,7 +60,7 @@ class Samples(C.Structure):
 class TrainWs(C.Structure):
     _fields_ = [("partial", vp), ("slot_stride", i64), ("n_slots", i32), ("touched", vp),
                 ("zall", vp), ("terms", vp), ("scalars", vp), ("zall_floats", i64),
-                ("l_cap", i32)]
+                ("l_cap", i32), ("stage_flags", vp), ("stage_flag_words", i64)]
 
 
 class Plan(C.Structure):
@@ -91,9 +91,6 @@ SIGNATURES = {
     "tpcb_large_train_ws": (i32, [vp, i64, i64, C.POINTER(sz)]),
     "tpcb_large_loss_backward": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64,
                                        C.POINTER(LossCfg), f64, vp, sz, vp, vp, vp, vp]),
-    "tpcb_debug_gemm_bk": (None, [i32]),
-    "tpcb_debug_gemm_cluster": (None, [i32]),
-    "tpcb_debug_gemm_mode": (None, [i32]),
     "tpcb_gemm3_ws": (sz, [i64, i32, i32]),
     "tpcb_gemm3": (i32, [vp, vp, i64, i32, i32, vp, i32, vp, sz, vp]),
     "tpcb_gemm3_presplit": (i32, [vp, vp, vp, vp, i64, i32, i32, vp, i32, vp]),
@@ -107,13 +104,15 @@ SIGNATURES = {
     "tpcb_cmd_grid_ws": (sz, [i64, i64, i32, i32]),
     "tpcb_cmd_grid": (i32, [vp, i32, i64, i64, i32, i32, vp, vp, vp, sz, vp]),
     "tpcb_train_ws_sizes": (i32, [vp, i32, i32, C.POINTER(i32), C.POINTER(i64),
-                                  C.POINTER(i64), C.POINTER(i64)]),
+                                  C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
     "tpcb_transpose_params": (i32, [vp, vp, vp, vp]),
     "tpcb_loss_backward": (i32, [vp, vp, vp, C.POINTER(Samples), C.POINTER(Samples), vp, i32,
                                  i32, C.POINTER(LossCfg), C.POINTER(TrainWs), vp, vp, vp, vp,
                                  vp]),
     "tpcb_optimizer_step": (i32, [vp, i64, vp, vp, vp, vp, vp, C.POINTER(OptimCfg), f64, i64,
                                   vp]),
+    "tpcb_optimizer_step_f64": (i32, [i64, vp, vp, vp, vp, C.POINTER(OptimCfg), f64, f64, f64,
+                                      vp]),
     "tpcb_train_epoch": (i32, [vp, vp, vp, vp, vp, C.POINTER(Samples), C.POINTER(Samples),
                                C.POINTER(Plan), C.POINTER(LossCfg), C.POINTER(OptimCfg), vp, vp,
                                C.POINTER(TrainWs), vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -124,10 +123,6 @@ SIGNATURES = {
     "tpcb_graph_create": (i32, [C.POINTER(vp)]),
     "tpcb_probe_ffma": (i32, [vp, C.POINTER(f64), vp]),
     "tpcb_debug_train_trace": (i32, [vp]),
-    "tpcb_debug_train_impl": (i32, [i32]),
-    "tpcb_debug_grid_cap": (i32, [i32]),
-    "tpcb_debug_overlap": (i32, [i32]),
-    "tpcb_debug_poll_ns": (i32, [i32]),
     "tpcb_kmeans_ws_size": (i32, [i64, i32, i32, C.POINTER(sz)]),
     "tpcb_kmeanspp_init": (i32, [vp, i64, i32, i64, vp, vp, vp, vp, sz, vp]),
     "tpcb_kmeanspp_step": (i32, [vp, i64, i32, i32, f64, i64, vp, vp, vp, vp, vp, sz, vp]),

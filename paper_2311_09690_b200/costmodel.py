@@ -450,7 +450,7 @@ def backward(params: CostModelParams, batch: list, targets, loss: LossSpec,
     src = engine.DeviceSamples(rag, cfg.n_leaf_max, st, y=targets)
     tgt = engine.DeviceSamples(trag, cfg.n_leaf_max, st) if use_cmd else None
     l_cap = max(int(rag.n_leaf.max()), int(trag.n_leaf.max()) if trag is not None else 1)
-    ws = engine.TrainWorkspace(dm, src.n + (tgt.n if tgt else 0), l_cap=l_cap)
+    ws = engine.TrainWorkspace(dm, src.n + (tgt.n if tgt else 0), l_cap=l_cap, overlap=False)
     grad, pred = engine.run_backward(dm, P, PT, src, tgt, _loss_struct(loss), ws, st)
     st.check("backward")
     sc = ws.scalars.cpu().numpy()

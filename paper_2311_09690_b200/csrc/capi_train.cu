@@ -5,6 +5,7 @@
 #include <cstring>
 #include <vector>
 
+#include "../../include/tpcb200_debug.h"
 #include "common.cuh"
 #include "dist.cuh"
 #include "train.cuh"
@@ -64,8 +65,11 @@ TrainWs to_dev(const tpcb_train_ws* w) {
   d.zall = w->zall;
   d.terms = w->terms;
   d.scalars = w->scalars;
-  d.zall_bytes = 0;
+  d.zall_bytes = (size_t)std::max<int64_t>(w->zall_floats, 0) * sizeof(float);
   d.l_cap = w->l_cap;
+  // overlapped reduce: the caller's counters, when large enough for this model
+  d.stage_flags = reinterpret_cast<unsigned long long*>(w->stage_flags);
+  d.n_stage_words = (int)std::min<int64_t>(w->stage_flag_words, 1 << 30);
   return d;
 }
 
@@ -104,9 +108,6 @@ struct StepProfiler {
 };
 thread_local StepProfiler* g_prof = nullptr;
 
-// overlapped reduce + optimizer (optim.cu): on by default, tpcb_debug_overlap
-int g_overlap = 1;
-
 struct SideStream {  // per device: the reduce branch of an overlapped step
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -129,10 +130,15 @@ int side_stream(SideStream** out) {
 }
 
 // Single GPU, no CMD, an optimizer, the desk fast-path kernel with one sample
-// per CTA: the reduce + optimizer of step k runs on the SMs the training
-// kernel leaves idle, each backward stage as soon as every CTA published it
-// (train4.cu stage_flags, optim.cu reduce_overlap_kernel).  Returns 1 when
-// the step was enqueued this way, 0 to use the sequential path.
+// per CTA, and a workspace that owns stage counters: the reduce + optimizer
+// of step k runs on the SMs the training kernel leaves idle, each backward
+// stage as soon as every CTA published it (train4.cu stage_flags, optim.cu
+// reduce_overlap_kernel).  The reduce blocks spin on counters the training
+// CTAs advance, so the overlap is only taken when every training CTA is
+// co-resident (occupancy check against this device's SM count, which also
+// reflects a MIG slice) and the waits are bounded: a wait that times out
+// raises TPCB_ERR_CUDA and the reduce applies nothing from that stage on.
+// Returns 1 when the step was enqueued this way, 0 to use the sequential path.
 int try_overlapped_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
                         const SampleSetDev& src, const SampleSetDev& tgt, const int32_t* batch,
                         const StepDesc* steps, int step, int grid, const LossDev& loss,
@@ -140,37 +146,28 @@ int try_overlapped_step(const tpcb_model* m, float* P, float* PT, float* mb, flo
                         const TrainWs& ws, float* grad_out, double* step_loss, double* step_cmd,
                         float* pred_out, int32_t* status, cudaStream_t stream, int* st_out) {
   *st_out = TPCB_OK;
-  if (!g_overlap || loss.use_cmd || opt.kind == kOptNone || !t0 || g_grid_cap > 0) return 0;
-  if (!(g_train_impl == 0 || g_train_impl == 4) || !v4_fits(m->dev, ws.l_cap)) return 0;
+  const Knobs& kn = knobs();
+  if (!ws.stage_flags || loss.use_cmd || opt.kind == kOptNone || !t0 || kn.grid_cap > 0) return 0;
+  if (ws.n_stage_words < ovl_stage_words(m->dev.n_layers)) return 0;
+  if (!(kn.train_impl == 0 || kn.train_impl == 4) || !v4_fits(m->dev, ws.l_cap)) return 0;
   SideStream* ss = nullptr;
   if (side_stream(&ss)) return 0;
   const int tgrid = std::max(1, std::min(grid, ws.n_slots));
   const int rgrid = ss->sms - tgrid;  // the reduce never blocks the training CTAs' SMs
   if (rgrid < 16) return 0;
+  if (train4_blocks_per_sm(m->dev, ws.l_cap) < 1) return 0;
   OvlDev ov{};
   if (overlap_sched(m, &ov) || ws.n_slots > ov.flag_stride) return 0;
+  ov.flags = ws.stage_flags;
+  ov.poll_ns = kn.poll_ns;
   TrainWs w2 = ws;
-  w2.stage_flags = ov.flags;
   w2.t_tag = t0;
   w2.flag_stride = ov.flag_stride;
   int st = TPCB_OK;
   auto fail = [&](int e) { *st_out = e; return 1; };
-  if (step == 0)  // tags are unique within a run; clear the previous run's
+  if (step == 0)  // the counters are cumulative within an epoch
     if (cudaMemsetAsync(ov.flags, 0, (size_t)ov.n_stages * ov.flag_stride * 8, stream))
       return fail(TPCB_ERR_CUDA);
-  if (g_overlap == 2) {  // debug A/B: stage publishing on, reduce sequential afterwards
-    if (g_prof) g_prof->mark(stream);
-    st = launch_train(m->dev, P, PT, src, tgt, batch, steps, step, grid, loss, 1, w2, pred_out,
-                      status, stream);
-    if (st) return fail(st);
-    if (g_prof) g_prof->mark(stream);
-    st = launch_reduce_apply(m->dev, ws, steps, step, 0, 1, grad_out, P, mb, vb, opt, lr, t0,
-                             loss, step_loss, step_cmd, stream);
-    if (st) return fail(st);
-    if (g_prof) g_prof->mark(stream);
-    if (g_prof) g_prof->mark(stream);
-    return 1;
-  }
   if (g_prof) g_prof->mark(stream);
   if (cudaEventRecord(ss->fork, stream)) return fail(TPCB_ERR_CUDA);
   // the training kernel is enqueued first: where launches are serialised
@@ -182,9 +179,8 @@ int try_overlapped_step(const tpcb_model* m, float* P, float* PT, float* mb, flo
   if (g_prof) g_prof->mark(stream);
   if (cudaStreamWaitEvent(ss->side, ss->fork, 0)) return fail(TPCB_ERR_CUDA);
   st = launch_reduce_overlap(m->dev, w2, ov, steps, step, batch, src, grad_out, P, mb, vb, opt,
-                             lr, t0, loss, step_loss, step_cmd, status,
-                             std::min(g_overlap >= 16 ? std::min(g_overlap, rgrid) : rgrid,
-                                      ov.n_items), ss->side);
+                             lr, t0, loss, step_loss, step_cmd, status, std::min(rgrid, ov.n_items),
+                             ss->side);
   if (st) return fail(st);
   if (cudaEventRecord(ss->join, ss->side)) return fail(TPCB_ERR_CUDA);
   if (cudaStreamWaitEvent(stream, ss->join, 0)) return fail(TPCB_ERR_CUDA);
@@ -199,7 +195,7 @@ int try_overlapped_step(const tpcb_model* m, float* P, float* PT, float* mb, flo
 int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
              const SampleSetDev& src, const SampleSetDev& tgt, const int32_t* batch,
              const StepDesc* steps, int step, int grid, const LossDev& loss, const OptDev& opt,
-             const double* lr, const int64_t* t0, const TrainWs& ws, float* grad_out,
+             const double* lr, const int64_t* t0, const TrainWs& ws_in, float* grad_out,
              double* step_loss, double* step_cmd, float* pred_out, int32_t* status,
              cudaStream_t stream, tpcb_comm* comm = nullptr, float* gbuf = nullptr) {
   (void)PT;
@@ -208,10 +204,12 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
   if (!dp) {
     int ost = TPCB_OK;
     if (try_overlapped_step(m, P, PT, mb, vb, src, tgt, batch, steps, step, grid, loss, opt, lr,
-                            t0, ws, grad_out, step_loss, step_cmd, pred_out, status, stream,
+                            t0, ws_in, grad_out, step_loss, step_cmd, pred_out, status, stream,
                             &ost))
       return ost;
   }
+  TrainWs ws = ws_in;  // sequential step: the training CTAs publish no stage counters
+  ws.stage_flags = nullptr;
   if (g_prof) g_prof->mark(stream);
   if (loss.use_cmd) {
     if (dp) {  // every rank fills its own rows; the all-reduce assembles [zs; zt]
@@ -258,8 +256,9 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
 
 extern "C" int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t l_cap,
                                    int32_t* n_slots, int64_t* slot_stride, int64_t* zall_floats,
-                                   int64_t* terms_doubles) {
+                                   int64_t* terms_doubles, int64_t* stage_flag_words) {
   if (!m || max_rows < 1) return TPCB_ERR_VALIDATION;
+  if (stage_flag_words) *stage_flag_words = ovl_stage_words(m->dev.n_layers);
   const int slots = std::min<int32_t>(max_rows, 1024);
   if (n_slots) *n_slots = slots;
   // 64-float (256 B) aligned slots
@@ -324,35 +323,8 @@ namespace tpcb {
 int set_train_trace(long long* d_trace);
 }
 
-/* debug: overlapped reduce + optimizer on (1, default) / off (0) */
-extern "C" int tpcb_debug_overlap(int32_t on) {
-  g_overlap = on;
-  return TPCB_OK;
-}
-
-/* debug: poll interval (ns) of the overlapped reduce's stage waits */
-extern "C" int tpcb_debug_poll_ns(int32_t ns) {
-  if (ns < 0) return TPCB_ERR_VALIDATION;
-  return set_poll_ns((unsigned)ns);
-}
-
-/* debug: training-kernel selection (0 automatic, 2 generic, 3 warp-group, 4 desk fast path) */
-extern "C" int tpcb_debug_train_impl(int32_t impl) {
-  if (impl != 0 && impl != 2 && impl != 3 && impl != 4) return TPCB_ERR_VALIDATION;
-  tpcb::g_train_impl = impl;
-  return TPCB_OK;
-}
-
-/* debug: cap the training grid (CTAs then loop over several samples); 0 = no cap */
-extern "C" int tpcb_debug_grid_cap(int32_t cap) {
-  if (cap < 0) return TPCB_ERR_VALIDATION;
-  tpcb::g_grid_cap = cap;
-  return TPCB_OK;
-}
-
 /* debug: per-op timestamps of CTA 0 of the training kernel (NULL disables) */
 namespace tpcb {
-int set_train3_trace(long long* d_trace);
 int set_train4_trace(long long* d_trace);
 int set_forward_tc_trace(long long* d_trace);
 int set_forward_trace(long long* d_trace);
@@ -360,7 +332,6 @@ int set_forward_f32_trace(long long* d_trace);
 }
 extern "C" int tpcb_debug_train_trace(long long* d_trace) {
   int st = tpcb::set_train_trace(d_trace);
-  if (!st) st = tpcb::set_train3_trace(d_trace);
   if (!st) st = tpcb::set_forward_tc_trace(d_trace);
   if (!st) st = tpcb::set_forward_trace(d_trace);
   if (!st) st = tpcb::set_forward_f32_trace(d_trace);
@@ -473,7 +444,7 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
     {  // the overlapped reduce's schedule / side stream are allocated outside capture too
       OvlDev ov{};
       SideStream* ss = nullptr;
-      if (g_overlap && !comm) {
+      if (ws->stage_flags && !comm) {
         st = overlap_sched(m, &ov);
         if (!st) st = side_stream(&ss);
         if (st) return st;

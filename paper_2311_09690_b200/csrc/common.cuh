@@ -62,6 +62,18 @@ namespace tpcb {
 
 void set_last_error(const char* what, cudaError_t e);
 
+// Developer A/B switches, read once from the environment on first use and
+// immutable afterwards (no process-global state a caller can flip while
+// another thread trains): TPCB_TRAIN_IMPL (0 automatic, 2 generic kernel,
+// 4 desk fast path), TPCB_GRID_CAP (cap on the training grid), TPCB_POLL_NS
+// (stage-wait poll interval of the overlapped reduce), TPCB_GEMM_BK (16 / 32
+// k-slab of the large-path GEMM), TPCB_GEMM_CLUSTER, TPCB_GEMM_MODE (probe).
+struct Knobs {
+  int train_impl, grid_cap, gemm_bk, gemm_cluster, gemm_mode;
+  unsigned poll_ns;
+};
+const Knobs& knobs();
+
 #define TPCB_CUDA_CHECK(call)                              \
   do {                                                     \
     cudaError_t _e = (call);                               \

@@ -586,10 +586,6 @@ struct Operand {
   int64_t rows, k_ext, ld;
 };
 
-int g_gemm_bk = 16;  // k-slab width (tpcb_debug_gemm_bk)
-
-int g_gemm_cluster = 0;  // allow 2x2 / 2x1 / 1x2 clusters (tpcb_debug_gemm_cluster)
-int g_gemm_dbg = 0;      // probe mode (tpcb_debug_gemm_mode)
 
 template <int NT, int BK, int CN, int CM>
 int launch_gemm_cl(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st,
@@ -630,7 +626,7 @@ int launch_gemm_cl(const Operand& A, const Operand& B, const Epi& e, cudaStream_
   cfg.attrs = at;
   cfg.numAttrs = 1;
   Epi ee = e;
-  ee.dbg = g_gemm_dbg;
+  ee.dbg = knobs().gemm_mode;
   TPCB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, gemm3_kernel<NT, BK, CN, CM>, ta_hi, ta_lo, tb_hi,
                                      tb_lo, kc, k_total, ee));
   TPCB_LAUNCH_CHECK("gemm3");
@@ -643,7 +639,7 @@ template <int NT, int BK>
 int launch_gemm_bk(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st,
                    int splits, int* splits_used) {
   const int tn = ceil_div(e.ldc, NT), tm = ceil_div(e.M, kTileM);
-  const bool cn = g_gemm_cluster && tn % 2 == 0, cm = g_gemm_cluster && tm % 2 == 0;
+  const bool cn = knobs().gemm_cluster && tn % 2 == 0, cm = knobs().gemm_cluster && tm % 2 == 0;
   if (cn && cm) return launch_gemm_cl<NT, BK, 2, 2>(A, B, e, st, splits, splits_used);
   if (cm) return launch_gemm_cl<NT, BK, 1, 2>(A, B, e, st, splits, splits_used);
   if (cn) return launch_gemm_cl<NT, BK, 2, 1>(A, B, e, st, splits, splits_used);
@@ -654,7 +650,7 @@ int launch_gemm_bk(const Operand& A, const Operand& B, const Epi& e, cudaStream_
 template <int NT>
 int launch_gemm_nt(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st,
                    int splits = 1, int* splits_used = nullptr) {
-  if (g_gemm_bk == 16) return launch_gemm_bk<NT, 16>(A, B, e, st, splits, splits_used);
+  if (knobs().gemm_bk == 16) return launch_gemm_bk<NT, 16>(A, B, e, st, splits, splits_used);
   return launch_gemm_bk<NT, 32>(A, B, e, st, splits, splits_used);
 }
 
@@ -1829,7 +1825,3 @@ extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_para
   return stream_wait(st, g_side.s);  // join: every weight gradient is in d_grad
 }
 
-extern "C" void tpcb_debug_gemm_bk(int32_t bk) { tpcb::g_gemm_bk = bk == 32 ? 32 : 16; }
-
-extern "C" void tpcb_debug_gemm_cluster(int32_t on) { tpcb::g_gemm_cluster = on ? 1 : 0; }
-extern "C" void tpcb_debug_gemm_mode(int32_t mode) { tpcb::g_gemm_dbg = mode; }

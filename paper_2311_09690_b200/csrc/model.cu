@@ -1,6 +1,8 @@
 // Host side of the model handle: canonical tensor layout of the flat fp32
 // parameter vector (creation order of costmodel.py:127-149), status strings
 // and the thread-local CUDA error record.
+#include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 
@@ -9,6 +11,24 @@
 namespace tpcb {
 
 static thread_local char g_last_error[512] = "";
+
+const Knobs& knobs() {
+  static const Knobs k = [] {
+    auto env = [](const char* name, int dflt) {
+      const char* v = getenv(name);
+      return v && *v ? atoi(v) : dflt;
+    };
+    Knobs r{};
+    r.train_impl = env("TPCB_TRAIN_IMPL", 0);
+    r.grid_cap = env("TPCB_GRID_CAP", 0);
+    r.gemm_bk = env("TPCB_GEMM_BK", 16) == 32 ? 32 : 16;
+    r.gemm_cluster = env("TPCB_GEMM_CLUSTER", 0) ? 1 : 0;
+    r.gemm_mode = env("TPCB_GEMM_MODE", 0);
+    r.poll_ns = (unsigned)std::max(0, env("TPCB_POLL_NS", 256));
+    return r;
+  }();
+  return k;
+}
 
 void set_last_error(const char* what, cudaError_t e) {
   snprintf(g_last_error, sizeof(g_last_error), "%s: %s (%d)", what, cudaGetErrorString(e), (int)e);

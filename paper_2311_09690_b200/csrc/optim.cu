@@ -235,8 +235,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
   return v;
 }
 
-__constant__ unsigned kPollNsC = 256;
-#define kPollNs kPollNsC
 // block-wide wait until the training CTAs of this step (and of every earlier
 // step of the epoch) counted themselves into stage q's word (train4.cu): the
 // word must reach `target` = samples of steps first..this.  A poll is one L2
@@ -251,7 +249,7 @@ __device__ bool wait_stage(const OvlDev& ov, int q, unsigned long long target, i
         ok = true;
         break;
       }
-      __nanosleep(kPollNs);
+      __nanosleep(ov.poll_ns);
     }
     s_ok = ok;
     if (!ok) raise_status(status, TPCB_ERR_CUDA);
@@ -312,7 +310,9 @@ __global__ void __launch_bounds__(256) reduce_overlap_kernel(
     const int item = order[k];
     const int stg = stage_of[item];
     if (stg > ready) {
-      wait_stage(ov, stg, target, status);
+      // a timed-out wait (status raised) must not apply partially written
+      // gradients: this block stops applying here
+      if (!wait_stage(ov, stg, target, status)) return;
       ready = stg;
       if (mixed && threadIdx.x < 32) {  // slot masks (written before the final stage)
         uint32_t a = ~0u, o = 0u;
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(256) reduce_overlap_kernel(
   // loss value of the step (fixed order), costmodel.py:539-550; terms are
   // written before stage 0
   if (blockIdx.x == 0) {
-    if (ready < 0) wait_stage(ov, 0, target, status);
+    if (ready < 0 && !wait_stage(ov, 0, target, status)) return;
     if (threadIdx.x < 32) {
       double sq = 0.0, rel = 0.0;
       for (int i = threadIdx.x; i < n_src; i += 32) {
@@ -614,11 +614,6 @@ std::mutex& ovl_mu() {
 }
 }  // namespace
 
-int set_poll_ns(unsigned ns) {
-  TPCB_CUDA_CHECK(cudaMemcpyToSymbol(kPollNsC, &ns, sizeof(ns)));
-  return TPCB_OK;
-}
-
 int overlap_sched(const tpcb_model* m, OvlDev* out) {
   const Model& M = m->dev;
   int dev = 0;
@@ -677,20 +672,17 @@ int overlap_sched(const tpcb_model* m, OvlDev* out) {
   OvlDev d{};
   d.n_items = n_items;
   d.n_stages = n_stages;
-  d.flag_stride = 1024;  // >= n_slots (tpcb_train_ws_sizes caps slots at 1024)
+  d.flag_stride = kOvlFlagStride;
   d.n_leaf_max = nl;
   int32_t* d_order = nullptr;
   int8_t* d_stage = nullptr;
-  unsigned long long* d_flags = nullptr;
   TPCB_CUDA_CHECK(cudaMalloc(&d_order, order.size() * sizeof(int32_t)));
   TPCB_CUDA_CHECK(cudaMalloc(&d_stage, stage.size()));
-  TPCB_CUDA_CHECK(cudaMalloc(&d_flags, (size_t)n_stages * d.flag_stride * 8));
   TPCB_CUDA_CHECK(cudaMemcpy(d_order, order.data(), order.size() * 4, cudaMemcpyHostToDevice));
   TPCB_CUDA_CHECK(cudaMemcpy(d_stage, stage.data(), stage.size(), cudaMemcpyHostToDevice));
-  TPCB_CUDA_CHECK(cudaMemset(d_flags, 0, (size_t)n_stages * d.flag_stride * 8));
   d.order = d_order;
   d.stage = d_stage;
-  d.flags = d_flags;
+  d.flags = nullptr;  // the stage counters belong to each training workspace
   ovl_cache().push_back(OvlCache{dev, M, d});
   *out = d;
   return TPCB_OK;
@@ -711,3 +703,52 @@ int launch_reduce_overlap(const Model& M, const TrainWs& ws, const OvlDev& ov,
 }
 
 }  // namespace tpcb
+
+// ---- float64 optimizer step (the drop-in nn.Adam / nn.Sgd, nn.py:136-167) ----
+// The reference updates float64 numpy arrays in place; this kernel applies
+// the same sequence of IEEE float64 operations (no contraction into FMAs:
+// every product and sum rounded separately, exactly as numpy evaluates
+// m *= b1; m += (1-b1)*g; v *= b2; v += (1-b2)*g*g;
+// p -= lr*(m/bc1)/(sqrt(v/bc2)+eps)), so a step is bit-identical to the
+// reference's.  bc1 / bc2 come from the host (Python's 1 - beta**t).
+namespace tpcb {
+namespace {
+__global__ void optimizer_f64_kernel(int64_t n, double* __restrict__ P, const double* __restrict__ G,
+                                     double* __restrict__ M, double* __restrict__ V, int kind,
+                                     double b1, double one_b1, double b2, double one_b2,
+                                     double eps, double wd, double lr, double bc1, double bc2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double p = P[i], g = G[i];
+    if (wd != 0.0) g = __dadd_rn(g, __dmul_rn(wd, p));
+    if (kind == kOptSgd) {
+      P[i] = __dsub_rn(p, __dmul_rn(lr, g));
+      continue;
+    }
+    double m = __dadd_rn(__dmul_rn(M[i], b1), __dmul_rn(one_b1, g));
+    double v = __dadd_rn(__dmul_rn(V[i], b2), __dmul_rn(__dmul_rn(one_b2, g), g));
+    M[i] = m;
+    V[i] = v;
+    const double num = __dmul_rn(lr, __ddiv_rn(m, bc1));
+    const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(v, bc2)), eps);
+    P[i] = __dsub_rn(p, __ddiv_rn(num, den));
+  }
+}
+}  // namespace
+}  // namespace tpcb
+
+extern "C" int tpcb_optimizer_step_f64(int64_t n, double* d_params, const double* d_grad,
+                                       double* d_m, double* d_v, const tpcb_optim* opt,
+                                       double lr, double bc1, double bc2, void* stream) {
+  using namespace tpcb;
+  if (n < 0 || !opt || (n > 0 && (!d_params || !d_grad))) return TPCB_ERR_VALIDATION;
+  if (opt->kind != kOptAdam && opt->kind != kOptSgd) return TPCB_ERR_VALIDATION;
+  if (opt->kind == kOptAdam && n > 0 && (!d_m || !d_v)) return TPCB_ERR_VALIDATION;
+  if (n == 0) return TPCB_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)kNumSMs * 8);
+  optimizer_f64_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      n, d_params, d_grad, d_m, d_v, opt->kind, opt->beta1, 1.0 - opt->beta1, opt->beta2,
+      1.0 - opt->beta2, opt->eps, opt->weight_decay, lr, bc1, bc2);
+  TPCB_LAUNCH_CHECK("optimizer_f64");
+  return TPCB_OK;
+}

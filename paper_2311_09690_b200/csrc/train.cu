@@ -612,9 +612,6 @@ __global__ void __launch_bounds__(kTrainThreads) train_kernel(
 
 }  // namespace
 
-int g_train_impl = 0;
-int g_grid_cap = 0;
-
 int set_train_trace(long long* d_trace) {
   TPCB_CUDA_CHECK(cudaMemcpyToSymbol(g_trace, &d_trace, sizeof(d_trace)));
   return TPCB_OK;
@@ -650,12 +647,10 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                  int32_t* status, cudaStream_t stream) {
   (void)PT;
-  if (g_grid_cap > 0) grid = std::min(grid, g_grid_cap);
-  if ((g_train_impl == 0 || g_train_impl == 4) && v4_fits(M, ws.l_cap))
+  const Knobs& kn = knobs();
+  if (kn.grid_cap > 0) grid = std::min(grid, kn.grid_cap);
+  if ((kn.train_impl == 0 || kn.train_impl == 4) && v4_fits(M, ws.l_cap))
     return launch_train4(M, P, src, tgt, batch, steps, step, grid, loss, phase, ws, pred_out,
-                         status, stream);
-  if (g_train_impl == 3 && v3_supported(M))
-    return launch_train3(M, P, src, tgt, batch, steps, step, grid, loss, phase, ws, pred_out,
                          status, stream);
   TrainPlan tp = make_train_plan(M, ws.l_cap);
   const size_t smem = (size_t)tp.total * sizeof(float);

@@ -40,7 +40,7 @@ TrainPlan make_train_plan(const Model& M, int l_cap);
 __host__ __device__ inline int round4(int v) { return (v + 3) & ~3; }
 
 // weight stream: the fixed order in which the fwd+bwd of one sample consumes
-// weight matrices (shared by the v2 and v3 training kernels)
+// weight matrices (the generic training kernel, train.cu)
 
 __host__ __device__ inline int n_fwd_entries(const Model& M, int L) {
   return 1 + 6 * M.n_layers + L + 2 + M.n_dec + 1;
@@ -126,6 +126,7 @@ struct TrainWs {
   unsigned long long* stage_flags = nullptr;
   const int64_t* t_tag = nullptr;  // tag of step s = t_tag[0] + s + 1
   int flag_stride = 0;
+  int n_stage_words = 0;  // words of the caller's stage_flags (0: overlap off)
 };
 
 // Overlapped gradient reduction + optimizer (single GPU, no CMD): the items
@@ -136,12 +137,16 @@ struct TrainWs {
 struct OvlDev {
   const int32_t* order;       // [(n_leaf_max + 1) * n_items]
   const int8_t* stage;        // [(n_leaf_max + 1) * n_items]
-  unsigned long long* flags;  // [n_stages * flag_stride]
+  unsigned long long* flags;  // [n_stages * flag_stride], owned by the training workspace
   int n_items, n_stages, flag_stride, n_leaf_max;
+  unsigned poll_ns;           // stage-wait poll interval
 };
+constexpr int kOvlFlagStride = 1024;  // >= n_slots (tpcb_train_ws_sizes caps slots at 1024)
+__host__ __device__ constexpr int ovl_stage_words(int n_layers) {
+  return (2 + 2 * n_layers) * kOvlFlagStride;
+}
 // schedule of a model (built once per parameter layout, cached per device)
 int overlap_sched(const tpcb_model* m, OvlDev* out);
-int set_poll_ns(unsigned ns);  // stage-wait poll interval of the overlapped reduce
 int launch_reduce_overlap(const Model& M, const TrainWs& ws, const OvlDev& ov,
                           const StepDesc* steps, int step, const int32_t* batch,
                           const SampleSetDev& src, float* grad_out, float* P, float* m, float* v,
@@ -156,23 +161,14 @@ int launch_train(const Model& M, const float* P, const float* PT, const SampleSe
                  int grid, const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                  int32_t* status, cudaStream_t stream);
 int prepare_train_kernels(const Model& M, int l_cap);
-// v3 (warp-group per sample, producer warp + mbarrier weight stream)
-bool v3_supported(const Model& M);
-size_t train3_smem(const Model& M, int l_cap);
-int launch_train3(const Model& M, const float* P, const SampleSetDev& src, const SampleSetDev& tgt,
-                  const int32_t* batch, const StepDesc* steps, int step, int grid,
-                  const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
-                  int32_t* status, cudaStream_t stream);
 // v4 (desk-shaped fast path)
 bool v4_supported(const Model& M);
 bool v4_fits(const Model& M, int l_cap);
+int train4_blocks_per_sm(const Model& M, int l_cap);
 int launch_train4(const Model& M, const float* P, const SampleSetDev& src, const SampleSetDev& tgt,
                   const int32_t* batch, const StepDesc* steps, int step, int grid,
                   const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,
                   int32_t* status, cudaStream_t stream);
-// training-kernel selection: 0 automatic (v4 where it applies, else v2), 2/3/4 forced
-extern int g_train_impl;
-extern int g_grid_cap;  // debug: cap on the training grid (0 = none)
 int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps, int step,
                         int use_cmd, int add_cmd, float* grad_out, float* P, float* m, float* v,
                         const OptDev& opt, const double* lr, const int64_t* t,

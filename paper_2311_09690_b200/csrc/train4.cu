@@ -1430,6 +1430,25 @@ static int build_maps(const Model& M, const float* P, TmaMaps* t) {
   return st;
 }
 
+// resident train4 CTAs per SM for this model / leaf cap (0: does not fit);
+// the overlapped reduce is only used when every training CTA of a step is
+// co-resident next to the reduce blocks (capi_train.cu)
+int train4_blocks_per_sm(const Model& M, int l_cap) {
+  const size_t lim = train4_dyn_limit();
+  if (!lim) return 0;
+  const int ns = ring_slots_for(M, l_cap, lim);
+  if (!ns) return 0;
+  const Plan4 tp = make_plan4(M, l_cap, ns);
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, train4_kernel, kThreads4,
+                                                    (size_t)tp.total * sizeof(float)) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return blocks;
+}
+
 int launch_train4(const Model& M, const float* P, const SampleSetDev& src, const SampleSetDev& tgt,
                   const int32_t* batch, const StepDesc* steps, int step, int grid,
                   const LossDev& loss, int phase, const TrainWs& ws, float* pred_out,

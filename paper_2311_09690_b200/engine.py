@@ -373,12 +373,13 @@ class TrainWorkspace:
     z_rows: rows of the global [zs; zt] CMD matrix (≥ max_rows)."""
 
     def __init__(self, dm: DeviceModel, max_rows: int, device="cuda", z_rows: int = 0,
-                 l_cap: int = 0):
+                 l_cap: int = 0, overlap: bool = True):
         lib = _lib.load()
-        ns, stride, zf, tf = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64()
+        ns, stride, zf, tf, sw = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
         self.l_cap = int(l_cap) if l_cap else dm.cfg.n_leaf_max
         _lib.check(lib.tpcb_train_ws_sizes(dm.handle, max_rows, self.l_cap, C.byref(ns),
-                                           C.byref(stride), C.byref(zf), C.byref(tf)),
+                                           C.byref(stride), C.byref(zf), C.byref(tf),
+                                           C.byref(sw)),
                    "train_ws_sizes")
         zf = C.c_int64(max(zf.value, z_rows * dm.cfg.d_embed))
         self.max_rows = max_rows
@@ -395,6 +396,12 @@ class TrainWorkspace:
         w.terms, w.scalars = self.terms.data_ptr(), self.scalars.data_ptr()
         w.zall_floats = self.zall.numel()
         w.l_cap = self.l_cap
+        # stage counters of the overlapped reduce (owned by this workspace;
+        # None = the step's reduction runs after the training kernel)
+        self.stage_flags = (torch.zeros(sw.value, dtype=torch.int64, device=device)
+                            if overlap else None)
+        w.stage_flags = self.stage_flags.data_ptr() if overlap else None
+        w.stage_flag_words = sw.value if overlap else 0
         self.struct = w
 
 

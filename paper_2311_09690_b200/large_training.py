@@ -38,12 +38,13 @@ class LargeTrainer:
     def __init__(self, config, tensors: dict, train_rag: engine.RaggedHost, targets: np.ndarray,
                  loss_struct, valid_rag: engine.RaggedHost | None = None,
                  valid_latency: np.ndarray | None = None, normalizer=None, device="cuda",
-                 comm: "engine.Comm | None" = None):
+                 comm: "engine.Comm | None" = None,
+                 target_rag: engine.RaggedHost | None = None):
         from .costmodel import device_model
-        # pre-training only: no target set, so no CMD term (alpha_cmd applies
-        # to finetune, which runs on the fused trainer)
         if loss_struct.original_space:
             raise UnsupportedConfig("the large path trains with transformed-space losses")
+        if target_rag is not None and loss_struct.alpha_cmd > 0:
+            raise UnsupportedConfig("CMD fine-tuning is not available on the large path")
         self.lib = _lib.load()
         self.config = config
         self.dm = device_model(config)

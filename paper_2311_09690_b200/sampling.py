@@ -233,12 +233,14 @@ def build_distance_table(clusters: ClusterModel, tasks: list) -> DistanceTable:
     return DistanceTable(psi=psi.cpu().numpy(), task_ids=[t.task_id for t in tasks])
 
 
-def select_tasks(x, kappa: int, tasks: list, seed: int = 0, init_centers=None) -> list:
+def select_tasks(x, kappa: int, tasks: list, seed: int = 0, init_centers=None,
+                 assign: str = "exact") -> list:
     """κ task ids: clusters by size desc (stable), each takes the closest
-    remaining task, ties to the earlier task (sampling.py:126-144)."""
+    remaining task, ties to the earlier task (sampling.py:126-144).
+    assign: the clustering's assignment mode (see DeviceKMeans)."""
     if len(tasks) < kappa:
         raise TooFewTasks(f"{len(tasks)} tasks < kappa={kappa}")
-    clusters = kmeans(x, kappa, seed=seed, init_centers=init_centers)
+    clusters = kmeans(x, kappa, seed=seed, init_centers=init_centers, assign=assign)
     table = build_distance_table(clusters, tasks)
     order = np.argsort(-clusters.sizes, kind="stable")
     taken = np.zeros(len(tasks), dtype=bool)

@@ -112,7 +112,8 @@ class Trainer:
                  targets: np.ndarray, loss_struct, valid_rag: engine.RaggedHost | None = None,
                  valid_latency: np.ndarray | None = None, normalizer=None,
                  target_rag: engine.RaggedHost | None = None, device="cuda",
-                 use_graph: bool = True, comm: "engine.Comm | None" = None):
+                 use_graph: bool = True, comm: "engine.Comm | None" = None,
+                 overlap: bool = True):
         from .costmodel import device_model
         self.config = config
         self.dm = device_model(config)
@@ -147,7 +148,7 @@ class Trainer:
         if target_rag is not None:
             l_cap = max(l_cap, int(np.max(target_rag.n_leaf)))
         self.ws = engine.TrainWorkspace(self.dm, rows, device, z_rows=rows * self.world,
-                                        l_cap=l_cap)
+                                        l_cap=l_cap, overlap=overlap and comm is None)
         self.grad = torch.zeros_like(self.P) if comm is not None else None
         self.n_train = train_rag.n_ast
         self.n_leaf = np.asarray(train_rag.n_leaf)
@@ -313,9 +314,7 @@ def train(config, ds, devices: dict, normalizer=None) -> TrainResult:
     if config.epochs == 0:
         return TrainResult(params=params, normalizer=normalizer, log=[], best_epoch=-1,
                            best_val_mape=math.inf)
-    if config.loss_mode != "mse" and config.mape_space == "transformed" and \
-            np.any(targets + normalizer.loss_offset <= 0):
-        raise ValidationError("shifted labels must be positive")
+    _check_targets(config, normalizer, targets)
     loss = _loss_from_config(config, normalizer)
     if needs_large_path(config):
         from .large_training import LargeTrainer
@@ -325,6 +324,16 @@ def train(config, ds, devices: dict, normalizer=None) -> TrainResult:
         tr = Trainer(config, params.tensors, train_rag, targets, loss, valid_rag, valid_lat,
                      normalizer)
     return run_loop(tr, config, params, normalizer, select_best=True)
+
+
+def _check_targets(config, normalizer, targets) -> None:
+    """The reference's relative term rejects non-positive shifted labels
+    (costmodel.py:394-396) when a batch holding one is processed; every
+    training sample is visited in the first epoch, so the check runs once
+    up front (the device kernels would otherwise divide by them)."""
+    if config.epochs > 0 and config.loss_mode != "mse" and config.mape_space == "transformed" \
+            and np.any(targets + normalizer.loss_offset <= 0):
+        raise ValidationError("shifted labels must be positive")
 
 
 def needs_large_path(config) -> bool:
@@ -387,7 +396,13 @@ def finetune(params, source, target_inputs: list, config, devices: dict,
     tgt_rag = ragged_from_encoded(target_inputs, config.n_leaf_max) if (
         config.alpha_cmd > 0 and target_inputs) else None
     alpha = config.alpha_cmd if tgt_rag is not None else 0.0
-    tr = Trainer(config, params.tensors, train_rag, targets,
-                 _loss_from_config(config, normalizer, alpha), valid_rag, valid_lat, normalizer,
-                 target_rag=tgt_rag)
+    _check_targets(config, normalizer, targets)
+    loss = _loss_from_config(config, normalizer, alpha)
+    if needs_large_path(config):  # e.g. full_reference_config (alpha_cmd = 1 by default)
+        from .large_training import LargeTrainer
+        tr = LargeTrainer(config, params.tensors, train_rag, targets, loss, valid_rag, valid_lat,
+                          normalizer, target_rag=tgt_rag)
+    else:
+        tr = Trainer(config, params.tensors, train_rag, targets, loss, valid_rag, valid_lat,
+                     normalizer, target_rag=tgt_rag)
     return run_loop(tr, config, params, normalizer, select_best=False)

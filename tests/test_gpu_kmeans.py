@@ -125,3 +125,39 @@ def test_tensor_core_assign_agreement():
     m_tc = s.kmeans(x32, 256, init_centers=init, assign="tc")
     assert np.mean(m_ex.assignment == m_tc.assignment) >= 0.999
     assert len(m_tc.sizes) == len(m_ex.sizes) == 256
+
+
+def test_tensor_core_kmeans_at_scale():
+    """C4 at scale (262,144 points x k = 1024, d = 24 and 32): one assignment
+    pass from identical centres agrees >= 99.9 % with the exact float64
+    assignment; a full Lloyd run from the same k-means++ init agrees >= 99.9 %
+    with the same cluster count, and select_tasks picks the same number of
+    tasks (kappa) in both modes."""
+    s = _s()
+    rng = np.random.default_rng(11)
+    n_blob, per = 256, 1024
+    for d in (24, 32):
+        centres = rng.normal(scale=6.0, size=(n_blob, d))
+        x = np.concatenate([c + rng.normal(scale=rng.uniform(0.5, 2.0), size=(per, d))
+                            for c in centres])
+        x = x[rng.permutation(len(x))]
+        assert x.shape == (262144, d)
+        k = 1024
+        init = x[rng.choice(len(x), k, replace=False)]
+        ex = s.DeviceKMeans(x, k)
+        tc = s.DeviceKMeans(x, k, assign="tc")
+        for km in (ex, tc):
+            km.centers.copy_(torch.from_numpy(init))
+            km.assign_step()
+        agree = np.mean(ex.assign.cpu().numpy() == tc.assign.cpu().numpy())
+        assert agree >= 0.999, (d, agree)
+        if d == 32:
+            m_ex = s.kmeans(x, k, seed=5)
+            m_tc = s.kmeans(x, k, seed=5, assign="tc")
+            assert np.mean(m_ex.assignment == m_tc.assignment) >= 0.999
+            assert len(m_ex.sizes) == len(m_tc.sizes) == k
+            tasks = [s.TaskFeatureSet(f"t{i}", x[32 * i:32 * (i + 1)]) for i in range(len(x) // 32)]
+            sel_ex = s.select_tasks(x, k, tasks, seed=5)
+            sel_tc = s.select_tasks(x, k, tasks, seed=5, assign="tc")
+            assert len(sel_ex) == len(sel_tc) == k
+            assert len(set(sel_ex)) == len(set(sel_tc)) == k

@@ -5,7 +5,7 @@ Tolerances (fp32 accumulate; CMD statistics in fp64):
   gradients   per tensor  max|Δ| ≤ 2e-4 · max|ref| + 1e-6
   loss value  relative    ≤ 1e-5
   CMD (fp64 standalone)   value rel ≤ 1e-12, gradients ≤ 1e-10 abs
-  Adam / SGD  (fp32 state) relative ≤ 1e-5 per parameter
+  Adam / SGD  (drop-in nn, float64 state) bit-exact vs the reference
 """
 
 import numpy as np
@@ -140,13 +140,18 @@ def test_adam_sgd_vs_reference():
     for step in range(3):
         grads = {n: g[f"g{step}." + n] for n in names}
         opt.step(params, grads, 1e-2)
-        for n in names:
-            np.testing.assert_allclose(params[n], g[f"p{step + 1}." + n], rtol=1e-5, atol=1e-6)
+        for n in names:  # float64 state, the reference's operation order: bit-exact
+            assert params[n].dtype == np.float64
+            np.testing.assert_array_equal(params[n], g[f"p{step + 1}." + n], err_msg=n)
     sgd = nn.Sgd(names, weight_decay=0.1)
     params = {n: g["p3." + n].copy() for n in names}
     sgd.step(params, {n: g["g2." + n] for n in names}, 0.5)
     for n in names:
-        np.testing.assert_allclose(params[n], g["sgd." + n], rtol=1e-5, atol=1e-6)
+        np.testing.assert_array_equal(params[n], g["sgd." + n], err_msg=n)
+    with pytest.raises(ValueError):  # a changed parameter set is rejected, not mis-scattered
+        bad = dict(params)
+        bad[names[0]] = np.zeros((3, 3))
+        sgd.step(bad, {n: g["g2." + n] for n in names}, 0.5)
 
 
 def test_cmd_grid_kernels_vs_oracle_large_sets():

@@ -249,28 +249,23 @@ def test_overlapped_reduce_bitwise_equals_sequential(use_graph):
     parameters, Adam moments and step losses to the sequential reduce kernel
     over two epochs of the desk model (graph-captured and eager)."""
     pb = _pb()
-    from paper_2311_09690_b200 import _lib
     from paper_2311_09690_b200.training import Trainer
     data, norm, y, dv, rag, loss = _oracle_setup(n=2048)
     cfg = pb.desk_config(seed=0)
     params = pb.init_params(cfg)
-    lib = _lib.load()
     runs = []
-    try:
-        for on in (0, 1):
-            assert lib.tpcb_debug_overlap(on) == 0
-            tr = Trainer(cfg, params.tensors, rag, y, loss, use_graph=use_graph)
-            rng = np.random.default_rng(3)
-            for _ in range(2):
-                flat, steps = tr.plan(rng)
-                n = tr.run_epoch(1e-3, flat, steps)
-                losses, _, _ = tr.collect(n, 0)
-            st = int(tr.status.t.item()) if hasattr(tr, "status") else 0
-            assert st == 0
-            runs.append((losses, tr.tensors(), tr.m.cpu().numpy().copy(),
-                         tr.v.cpu().numpy().copy()))
-    finally:
-        lib.tpcb_debug_overlap(1)
+    for on in (False, True):
+        tr = Trainer(cfg, params.tensors, rag, y, loss, use_graph=use_graph, overlap=on)
+        assert (tr.ws.stage_flags is not None) == on
+        rng = np.random.default_rng(3)
+        for _ in range(2):
+            flat, steps = tr.plan(rng)
+            n = tr.run_epoch(1e-3, flat, steps)
+            losses, _, _ = tr.collect(n, 0)
+        st = int(tr.status.t.item()) if hasattr(tr, "status") else 0
+        assert st == 0
+        runs.append((losses, tr.tensors(), tr.m.cpu().numpy().copy(),
+                     tr.v.cpu().numpy().copy()))
     assert np.array_equal(runs[0][0], runs[1][0])
     for k in runs[0][1]:
         assert np.array_equal(runs[0][1][k], runs[1][1][k]), k

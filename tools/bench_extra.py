@@ -169,9 +169,6 @@ def full():
                     "dtype": "3xTF32 tcgen05 GEMMs, fp32 accumulate"})
     # the GEMM alone (pre-split operands): QKV-shaped, M = 16384 tokens
     import os
-    lib.tpcb_debug_gemm_bk(int(os.environ.get("TPCB_GEMM_BK", "16")))
-    lib.tpcb_debug_gemm_cluster(int(os.environ.get("TPCB_GEMM_CLUSTER", "0")))
-    lib.tpcb_debug_gemm_mode(int(os.environ.get("TPCB_GEMM_MODE", "0")))
     for M, N, K in ((16384, 2148, 736), (16384, 716, 992), (65536, 716, 736)):
         kp = (K + 31) // 32 * 32
         a = [torch.randn(M, kp, device="cuda") for _ in range(2)]

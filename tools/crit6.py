@@ -1,4 +1,5 @@
-"""Reference acceptance criterion 6 on the GPU trainer: prints test MAPE / p90 for
+"""(kernel selection / grid cap: TPCB_TRAIN_IMPL / TPCB_GRID_CAP env vars)
+Reference acceptance criterion 6 on the GPU trainer: prints test MAPE / p90 for
 training-kernel implementations and seeds.  python tools/crit6.py [impl ...]"""
 import sys
 from pathlib import Path
@@ -26,7 +27,6 @@ inputs = pb.encode_dataset(test, devs)
 actual = np.array([s.latency_s for s in test])
 impls = [int(a) for a in sys.argv[1:]] or [4]
 for impl in impls:
-    _lib.load().tpcb_debug_train_impl(impl)
     for seed in (0, 1, 2):
         res = pb.train(pb.desk_config(epochs=300, seed=seed), ds, devs)
         pred = pb.predict_batch(res.params, inputs, res.normalizer)

@@ -1,4 +1,5 @@
-"""Quick per-step timing of the training epoch (profiled + graph), desk config.
+"""(kernel selection / grid cap: TPCB_TRAIN_IMPL / TPCB_GRID_CAP env vars)
+Quick per-step timing of the training epoch (profiled + graph), desk config.
 python tools/time_train.py [n_samples]"""
 import sys
 import time
@@ -16,7 +17,6 @@ from paper_2311_09690_b200.training import Trainer  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 impl = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # 0 auto, 2 generic, 3, 4 fast path
 from paper_2311_09690_b200 import _lib  # noqa: E402
-assert _lib.load().tpcb_debug_train_impl(impl) == 0
 data = synth.generate(n, seed=0)
 norm = fit_boxcox(data.latency)
 y = norm.encode(data.latency)

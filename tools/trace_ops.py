@@ -1,4 +1,5 @@
-"""Per-op cycle trace of CTA 0 (v3/v4 kernels): wait for weights vs work.
+"""(kernel selection / grid cap: TPCB_TRAIN_IMPL / TPCB_GRID_CAP env vars)
+Per-op cycle trace of CTA 0 (v3/v4 kernels): wait for weights vs work.
 python tools/trace3.py [impl=4]"""
 import sys
 from pathlib import Path
@@ -20,7 +21,6 @@ rag = engine.RaggedHost(rows=data.vectors.astype(np.float32), ordering=data.orde
                         encoded=False)
 loss = engine.loss_struct("hybrid", 1e-3, norm.loss_offset, 0.0, 5, "transformed", norm)
 impl = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-assert _lib.load().tpcb_debug_train_impl(impl) == 0
 tr = Trainer(cfg, pb.init_params(cfg).tensors, rag, y, loss, use_graph=False)
 flat, steps = tr.plan(np.random.default_rng(0))
 tr.run_epoch(1e-3, flat, steps[:3].copy())
@@ -29,7 +29,6 @@ buf = torch.zeros(512, dtype=torch.int64, device="cuda")
 lib = _lib.load()
 Ls = [int(a) for a in sys.argv[2:]] or [5]
 cap = int(__import__('os').environ.get('GRID_CAP', '0'))
-lib.tpcb_debug_grid_cap(cap)
 step_L = data.n_leaf[flat[steps[:, 0]]]
 for want in Ls:
     cand = np.nonzero(step_L == want)[0]
