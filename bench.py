@@ -139,11 +139,70 @@ def barrier(world):
     torch.cuda.synchronize()
 
 
+REF_PATH = ROOT / "baseline" / "_ref"        # the unmodified reference (install_ref.sh)
+CACHE = ROOT / "bench_cache" / f"ref_synth_{N_GEN}_seed0.npz"
+
+
+def _import_reference():
+    """tpcost from baseline/_ref (falls back to /root/reference in the build
+    container); None when neither exists."""
+    for p in (REF_PATH, Path("/root/reference/pkg/src")):
+        if (p / "tpcost" / "__init__.py").exists():
+            if str(p) not in sys.path:
+                sys.path.insert(0, str(p))
+            import tpcost  # noqa: F401
+            return p
+    return None
+
+
+def generate_bench_data(path: Path = CACHE) -> None:
+    """The reference's own generator — generate_synthetic(327,680,
+    [DEFAULT_SYNTH_DEVICE], SynthOracleConfig(noise_sigma=0.0), seed=0)
+     — run once (~60 s) and cached as arrays; the 8:1:1
+    split_dataset(seed=0) labels are stored with it."""
+    if _import_reference() is None:
+        raise RuntimeError("reference package not installed (baseline/install_ref.sh)")
+    from tpcost.dataset import (DEFAULT_SYNTH_DEVICE, SynthOracleConfig, generate_synthetic,
+                                split_dataset)
+    ds = generate_synthetic(N_GEN, [DEFAULT_SYNTH_DEVICE], SynthOracleConfig(noise_sigma=0.0),
+                            seed=0)
+    sp = split_dataset(ds, seed=0)
+    code = {"train": 0, "valid": 1, "test": 2}
+    path.parent.mkdir(parents=True, exist_ok=True)
+    tmp = path.with_suffix(".tmp.npz")
+    np.savez_compressed(
+        tmp, vectors=np.concatenate([s.compact.leaf_vectors for s in ds.samples]),
+        ordering=np.concatenate([np.asarray(s.compact.ordering, np.int32) for s in ds.samples]),
+        n_leaf=np.array([s.compact.n_leaf for s in ds.samples], np.int64),
+        latency=np.array([s.latency_s for s in ds.samples]),
+        task=np.array([int(s.task_id[1:]) for s in ds.samples], np.int64),
+        split=np.array([code[sp.splits[s.id]] for s in ds.samples], np.int8))
+    tmp.replace(path)
+
+
 def make_data():
-    from paper_2311_09690_b200 import synth
-    data = synth.generate(N_GEN, seed=0)
-    tr, va, _ = synth.split(N_GEN, seed=0)
-    return data, data.take(np.sort(tr)), data.take(np.sort(va))
+    """(all, train, valid) as SynthSet arrays of the reference-generated set;
+    train / valid in the reference's subset order (ascending sample index)."""
+    from paper_2311_09690_b200.synth import SynthSet
+    if not CACHE.exists():
+        generate_bench_data()
+    z = np.load(CACHE)
+    data = SynthSet(z["vectors"], z["ordering"], z["n_leaf"], z["latency"], z["task"])
+    split = z["split"]
+    return data, data.take(np.flatnonzero(split == 0)), data.take(np.flatnonzero(split == 1))
+
+
+def bench_config(world: int, dp_mode: str, batch: int, n_steps: int) -> dict:
+    """The `config` both arms print (same workload, same keys)."""
+    gb = batch * world if dp_mode == "weak" else batch
+    return {"workload": "train epoch, 262,144 synthetic ASTs (configs[1]): "
+                        "generate_synthetic(327680, seed=0) + split_dataset(seed=0) train split",
+            "model": "desk_config (354,577 params), init_params seed 0",
+            "global_batch": gb, "seq_len": "1..6 leaves",
+            "parallelism": (f"dp{world} ({dp_mode} scaling)" if world > 1 else "single GPU"),
+            "optimizer_steps_per_epoch": int(n_steps),
+            "loss": "hybrid (lambda 1e-3, transformed space), Adam lr 1e-3",
+            "l2": "flushed (256 MiB write) between timed epochs"}
 
 
 def rag_of(s, device_feat):
@@ -155,89 +214,175 @@ def rag_of(s, device_feat):
 
 # --------------------------------------------------------------- CPU baseline
 
-def cpu_baseline(train, device_feat, offset, norm, budget_s: float = 12.0, batch: int = 64,
-                 threads: int = 1):
-    """Oracle restatement of the reference train step (float64 numpy), bounded
-    sample: as many bs-64 steps of the planned epoch as fit in `budget_s`, with
-    numpy's BLAS pool limited to `threads` (the steps themselves are serial:
-    each depends on the previous Adam update)."""
-    from threadpoolctl import threadpool_limits
-    from oracle import featurize as of
-    from oracle import predictor as op
-    from oracle import trainer as ot
-    import paper_2311_09690_b200 as pb
-    from paper_2311_09690_b200.training import epoch_batches
-    cfg = pb.desk_config(seed=0)
-    T = {k: v.copy() for k, v in pb.init_params(cfg).tensors.items()}
-    dm = op.Dims(cfg.d_model, cfg.n_layers, cfg.n_heads, cfg.d_ff, cfg.d_embed, cfg.d_device,
-                 tuple(cfg.decoder_dims), cfg.n_leaf_max)
-    off = train.offsets()
-    y = norm.encode(train.latency)
-    batches = epoch_batches(np.random.default_rng(0), train.n_leaf, batch)
-    opt = ot.AdamState(T)
-    n_done, t_used, steps = 0, 0.0, 0
-    with threadpool_limits(limits=threads):
+class RefTrainer:
+    """The reference's own training loop body on this host: tpcost from
+    baseline/_ref, costmodel.train's setup (encode_dataset once, fit_boxcox,
+    init_params(desk_config(seed=0)), nn.Adam, the seeded _epoch_batches
+    plan) and per step exactly `backward` + `opt.step` (costmodel.py:697-706).
+    `run(budget_s)` advances through the epoch plan for a bounded sample."""
+
+    def __init__(self, train, batch: int = 64):
+        if _import_reference() is None:
+            raise RuntimeError("reference package not installed (baseline/install_ref.sh)")
+        from tpcost import costmodel as cm
+        from tpcost.dataset import DEFAULT_SYNTH_DEVICE, Sample, fit_boxcox
+        from tpcost.features import CompactAst
+        self.cm = cm
+        self.config = cm.desk_config(seed=0, batch_size=batch)
+        off = train.offsets()
+        samples = [Sample(id=f"s{i}", task_id="t0", model_id="m0",
+                          device_id=DEFAULT_SYNTH_DEVICE.name,
+                          compact=CompactAst(leaf_vectors=train.vectors[off[i]:off[i + 1]],
+                                             ordering=tuple(train.ordering[off[i]:off[i + 1]].tolist()),
+                                             serialized=(), n_leaf=int(train.n_leaf[i])),
+                          latency_s=float(train.latency[i])) for i in range(train.n)]
         t0 = time.perf_counter()
-        for b in batches:
-            L = int(train.n_leaf[b[0]])
-            x = np.stack([of.encode_rows(train.vectors[off[i]:off[i] + L],
-                                         train.ordering[off[i]:off[i] + L]) for i in b])
-            dev = np.tile(device_feat, (len(b), 1))
-            ot.train_step(T, dm, x, dev, y[b], opt, 1e-3, offset)
-            n_done += len(b)
-            steps += 1
-            t_used = time.perf_counter() - t0
-            if t_used >= budget_s and steps >= 8:
-                break
-    return {"value": n_done / t_used, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"{steps} reference train steps (bs {batch}, encode+backward+Adam, "
-                      f"{n_done} samples, {t_used:.1f} s) of the same epoch plan, float64 "
-                      f"numpy oracle, {threads} BLAS thread(s)"}
+        self.inputs = cm.encode_dataset(samples, {DEFAULT_SYNTH_DEVICE.name: DEFAULT_SYNTH_DEVICE})
+        self.encode_s = time.perf_counter() - t0
+        self.norm = fit_boxcox([s.latency_s for s in samples])
+        self.targets = self.norm.encode(np.array([s.latency_s for s in samples]))
+        self.params = cm.init_params(self.config)
+        self.opt = cm._make_optimizer(self.config, self.params.tensors.keys())
+        self.spec = cm.LossSpec(mode=self.config.loss_mode,
+                                lambda_hybrid=self.config.lambda_hybrid,
+                                offset=self.norm.loss_offset, mape_space=self.config.mape_space,
+                                normalizer=self.norm)
+        self.rng = np.random.default_rng(self.config.seed)
+        self.n_leaves = [e.n_leaf for e in self.inputs]
+        self.batches = cm._epoch_batches(self.rng, self.n_leaves, self.config.batch_size)
+        self.pos = 0
+        self.lr = cm._lr_at(self.config, 0)
+
+    def run(self, budget_s: float, threads: int, min_steps: int = 4):
+        from threadpoolctl import threadpool_limits
+        cm = self.cm
+        done = steps = 0
+        with threadpool_limits(limits=threads):
+            t0 = time.perf_counter()
+            while True:
+                if self.pos == len(self.batches):  # next epoch of the same run
+                    self.batches = cm._epoch_batches(self.rng, self.n_leaves,
+                                                     self.config.batch_size)
+                    self.pos = 0
+                idx = self.batches[self.pos]
+                self.pos += 1
+                batch = [self.inputs[i] for i in idx]
+                value, grads, _ = cm.backward(self.params, batch, self.targets[idx], self.spec)
+                self.opt.step(self.params.tensors, grads, self.lr)
+                done += len(idx)
+                steps += 1
+                el = time.perf_counter() - t0
+                if el >= budget_s and steps >= min_steps:
+                    return done, steps, el
+
+
+def _host_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def cpu_baseline(train, budget_s: float = 12.0, threads: int = 1, ref: RefTrainer | None = None):
+    """Bounded sample of the reference's training loop (tpcost itself) on
+    this host's cores."""
+    ref = ref or RefTrainer(train)
+    done, steps, el = ref.run(budget_s, threads)
+    return {"value": done / el, "unit": "samples/s", "cores": threads, "kind": "reference",
+            "sample": f"{steps} steps of tpcost.costmodel.train's loop body (backward + "
+                      f"nn.Adam.step, bs {ref.config.batch_size}, {done} samples, {el:.1f} s) "
+                      f"over the same epoch plan; encode_dataset done once "
+                      f"({ref.encode_s:.1f} s, outside the sample); {threads} BLAS thread(s)"}
+
+
+def _ref_infer_worker(args):
+    """one reference process: predict_batch over its contiguous shard"""
+    vec, ordering, n_leaf, reps = args
+    _import_reference()
+    from tpcost import costmodel as cm
+    from tpcost.dataset import DEFAULT_SYNTH_DEVICE
+    from tpcost.features import CompactAst, encode_input
+    off = np.concatenate([[0], np.cumsum(n_leaf)])
+    inputs = [encode_input(CompactAst(vec[off[i]:off[i + 1]],
+                                      tuple(ordering[off[i]:off[i + 1]].tolist()), (),
+                                      int(n_leaf[i])), DEFAULT_SYNTH_DEVICE)
+              for i in range(len(n_leaf))]
+    params = cm.init_params(cm.desk_config(seed=0))
+    cm.forward(params, inputs[:8])
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        cm.forward(params, inputs)
+    return time.perf_counter() - t0
+
+
+def cpu_inference_baseline(data, n: int = 4096):
+    """C1 on the reference: costmodel.forward over the
+    first 4,096 ASTs of the set (= generate_synthetic(4096, seed=0)), single
+    process, and one process per host core on contiguous shards (summed)."""
+    from multiprocessing import get_context
+    sub = data.take(np.arange(n))
+    off = sub.offsets()
+    one = _ref_infer_worker((sub.vectors, sub.ordering, sub.n_leaf, 2))
+    cores = max(1, _host_threads())
+    shards = np.array_split(np.arange(n), cores)
+    jobs = [(sub.vectors[off[c[0]]:off[c[-1] + 1]], sub.ordering[off[c[0]]:off[c[-1] + 1]],
+             sub.n_leaf[c], 2) for c in shards if len(c)]
+    with get_context("spawn").Pool(len(jobs)) as pool:
+        t0 = time.perf_counter()
+        times = pool.map(_ref_infer_worker, jobs)
+        wall = time.perf_counter() - t0
+    return {"single_process_asts_per_s": 2 * n / one,
+            "all_cores_asts_per_s": 2 * n / max(times), "cores": cores,
+            "all_cores_wall_s_incl_import": wall, "kind": "reference",
+            "sample": f"tpcost.costmodel.forward over {n} ASTs x 2 (init_params(desk seed 0)); "
+                      f"all cores: {len(jobs)} processes on contiguous shards, slowest shard's "
+                      f"forward time"}
 
 
 def run_reference_arm(args):
-    """--impl reference: the reference algorithm (oracle port, float64) on the
-    host cores; each step = a bounded sample of the epoch."""
+    """--impl reference: the unmodified reference (tpcost from baseline/_ref)
+    on the host cores, on the repo arm's workload / metric / config; each
+    step a bounded sample of the epoch (its loop body is serial: every step
+    depends on the previous Adam update).  Falls back to the oracle port when
+    baseline/_ref is absent."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_2311_09690_b200 as pb
     data, train, valid = make_data()
-    from paper_2311_09690_b200.dataset import fit_boxcox
-    norm = fit_boxcox(train.latency)
-    dv = pb.device_vector(pb.DeviceSpec("synth0", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0))
-    # All the host threads it can use: the train steps are serial, so the only
-    # parallelism is numpy's BLAS pool; probe 1 thread vs every core during
-    # the warm-up and keep whichever is faster (small bs-64 GEMMs usually
-    # lose to the pool's fork/join overhead).
-    n_cpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    ref = RefTrainer(train, args.batch_size)
+    # all the host threads it can use: the steps are serial, so the only
+    # parallelism is numpy's BLAS pool — probe 1 thread vs every core in the
+    # warm-up and keep the faster
+    n_cpu = _host_threads()
     cand = {1: 0.0}
     if n_cpu and n_cpu > 1:
         cand[int(n_cpu)] = 0.0
-    for w in range(max(args.warmup, 1)):
+    for _ in range(max(args.warmup, 1)):
         for th in cand:
-            r = cpu_baseline(train, dv, norm.loss_offset, norm, budget_s=1.0, threads=th)
-            cand[th] = max(cand[th], r["value"])
+            d, _, el = ref.run(1.0, th)
+            cand[th] = max(cand[th], d / el)
     threads = max(cand, key=cand.get)
-    vals = []
+    done = steps = 0
+    el_sum = 0.0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_baseline(train, dv, norm.loss_offset, norm, budget_s=6.0,
-                                 threads=threads))
+        d, st, el = ref.run(5.0, threads)
+        done, steps, el_sum = done + d, steps + st, el_sum + el
     elapsed = time.perf_counter() - t0
-    v = float(np.mean([r["value"] for r in vals]))
+    v = done / el_sum
+    n_plan = len(ref.batches)
+    cfg = bench_config(world, args.dp_mode, args.batch_size, n_plan)
+    cfg["threads_probe_samples_per_s"] = {str(k): val for k, val in cand.items()}
     line = {"metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed * 1e3 / max(args.steps, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": "train epoch, 262,144 synthetic ASTs, desk model, bs 64",
-                       "model": "desk (354,577 params)", "global_batch": 64, "seq_len": "1..6 leaves",
-                       "parallelism": f"host, {threads} BLAS thread(s) (best of "
-                                      f"{sorted(cand)} probed in warm-up)",
-                       "thread_probe_samples_per_s": {str(k): v for k, v in cand.items()}},
-            "cpu_baseline": {**vals[-1], "value": v},
+            "impl": "reference", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads,
+                             "kind": "reference",
+                             "sample": f"{steps} steps of tpcost's train loop body (backward + "
+                                       f"nn.Adam.step, bs {args.batch_size}, {done} samples in "
+                                       f"{args.steps} samples of 5 s) over the epoch plan; "
+                                       f"encode_dataset once ({ref.encode_s:.1f} s, untimed); "
+                                       f"{threads} BLAS thread(s)"},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -300,6 +445,49 @@ def run_full_config(args, data, norm, dv, dev, world, comm, n_steps: int = 12):
     return out
 
 
+def run_large_batch(cfg, train, targets, norm, dv, dev, flush_l2, batch: int = 600):
+    """Desk config at global batch 600, one epoch (device time, L2 flushed
+    before it): fused FFMA trainer vs the layer-by-layer tcgen05 path."""
+    import torch
+    import paper_2311_09690_b200 as pb
+    from paper_2311_09690_b200 import engine
+    from paper_2311_09690_b200.large_training import LargeTrainer
+    from paper_2311_09690_b200.training import Trainer
+    cfg6 = pb.desk_config(seed=0, batch_size=batch)
+    params = pb.init_params(cfg6)
+    loss = engine.loss_struct("hybrid", cfg6.lambda_hybrid, norm.loss_offset, 0.0, 5,
+                              "transformed", norm)
+    out = {"global_batch": batch,
+           "semantics": "the reference's train loop at batch_size 600 (per-bucket batches of "
+                        "<= 600, ~437 optimizer steps per epoch): a different optimisation "
+                        "trajectory from bs 64, same per-sample work"}
+    for name, mk in (("fused_ffma", lambda: Trainer(cfg6, params.tensors, rag_of(train, dv),
+                                                    targets, loss, device=dev)),
+                     ("tcgen05_3xtf32_layerwise",
+                      lambda: LargeTrainer(cfg6, params.tensors, rag_of(train, dv), targets,
+                                           loss, device=dev))):
+        tr = mk()
+        rng = np.random.default_rng(0)
+        flat, steps = tr.plan(rng)
+        with torch.cuda.stream(tr.stream):
+            tr.run_epoch(cfg6.lr, flat, steps[:8])   # warm-up (+ graph capture)
+        torch.cuda.synchronize()
+        flat, steps = tr.plan(rng)
+        flush_l2()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(tr.stream):
+            a.record()
+            tr.run_epoch(cfg6.lr, flat, steps)
+            b.record()
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) / 1e3
+        out[name] = {"samples_per_s": train.n / t, "ms_per_step": t * 1e3 / len(steps),
+                     "optimizer_steps": int(len(steps))}
+        del tr
+    return out
+
+
 def _ncu_traffic(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
     the committed ncu --set full capture (profiles/r01/ncu_traffic.json)."""
@@ -327,16 +515,18 @@ def run_ours(args):
     targets = norm.encode(train.latency)
     dspec = pb.DeviceSpec("synth0", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0)
     dv = pb.device_vector(dspec)
-    # data parallel (N > 1): weak scaling — every rank keeps bs 64 per step,
-    # global batch 64·N, gradients all-reduced over NCCL inside the captured
-    # epoch; each rank holds the whole (synthetic) training set and takes its
-    # share of every global batch from the common plan
+    # data parallel (N > 1): --dp-mode weak (default: bs 64 per rank, global
+    # batch 64·N) or strong (each reference batch of 64 split across the
+    # ranks, the reference's step count); gradients reduced in rank order
+    # over NCCL inside the captured epoch; each rank holds the whole training
+    # set and takes its share of every global batch from the common plan
     comm = engine.Comm(rank, world) if world > 1 else None
     params = pb.init_params(cfg)
     loss = engine.loss_struct("hybrid", cfg.lambda_hybrid, norm.loss_offset, 0.0, 5,
                               "transformed", norm)
     tr = Trainer(cfg, params.tensors, rag_of(train, dv), targets, loss, rag_of(valid, dv),
-                 valid.latency, norm, device=dev, comm=comm, overlap=bool(args.overlap))
+                 valid.latency, norm, device=dev, comm=comm, overlap=bool(args.overlap),
+                 dp_mode=args.dp_mode)
     rng = np.random.default_rng(cfg.seed)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -439,7 +629,9 @@ def run_ours(args):
     # ----------------------------------------------- inference (extra keys)
     # batch inference sharded with no communication: every rank runs the
     # forward over its own contiguous shard of n ASTs of the global batch
-    # (n · world); throughput = global batch / max-over-ranks device time
+    # (n · world); throughput = global batch / max-over-ranks device time.
+    # e2e: the public bulk API (Predictor.forward_batch: host CompactBatch in
+    # — arrays in pinned host memory — decoded latencies out), wall clock.
     infer = {}
     for prec in ("fp32", "bf16"):
         p = pb.Predictor(params, precision=prec)
@@ -459,6 +651,32 @@ def run_ours(args):
             torch.cuda.synchronize()
             t_inf = max_over_ranks(a.elapsed_time(b) / 1e3, world)
             infer[f"infer_{tag}asts_per_s_{n * world}"] = n * world * reps / t_inf
+            # e2e through the public API from pinned host arrays
+            pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa
+            batch = pb.CompactBatch(pin(sub.vectors.astype(np.float32)),
+                                    pin(sub.ordering.astype(np.int32)), pin(sub.n_leaf),
+                                    np.zeros(n, np.int32), [dspec])
+            p.forward_batch(batch, norm)
+            barrier(world)
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                _, _, _, _, lat_h = p.forward_batch(batch, norm)
+            t_e2e = max_over_ranks(time.perf_counter() - t0, world)
+            infer[f"infer_{tag}e2e_asts_per_s_{n * world}"] = n * world * reps / t_e2e
+            infer[f"infer_e2e_h2d_bytes_{n}"] = int(batch.vectors.nbytes + batch.ordering.nbytes
+                                                    + 8 * (n + 1) + 4 * 6 * n)
+            infer[f"infer_e2e_d2h_bytes_{n}"] = int(8 * n + 4 * n)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        infer["cpu_reference_c1"] = cpu_inference_baseline(data)
+
+    # ------------------------------------------ large-batch desk variant
+    # the same epoch at global batch 600 (the paper's batch;
+    # the reference's semantics at that batch size, ~437 optimizer steps):
+    # the fused FFMA trainer (one CTA per sample) and the layer-by-layer
+    # tcgen05 3xTF32 path (large.cu), device time of one epoch each
+    large_batch = None
+    if world == 1 and not args.no_large_batch:
+        large_batch = run_large_batch(cfg, train, targets, norm, dv, dev, flush_l2)
 
     # ------------------------- full_reference_config (extra keys)
     # d 716 × 11 layers, 46.7 M params: the layer-by-layer tcgen05 path
@@ -472,22 +690,19 @@ def run_ours(args):
         full = run_full_config(args, data, norm, dv, dev, world, comm)
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(train, dv, norm.loss_offset, norm)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(train)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic",
-                "config": {"workload": "train epoch, 262,144 synthetic ASTs (configs[1])",
-                           "model": "desk_config (354,577 params), init seed 0",
-                           "global_batch": args.batch_size * world, "seq_len": "1..6 leaves",
-                           "parallelism": f"dp{world}" if world > 1 else "single GPU",
-                           "optimizer_steps_per_epoch": int(n_steps),
-                           "l2": "flushed (256 MiB write) between timed epochs"},
+                "higher_is_better": True,
+                "scaling": "weak" if (world == 1 or args.dp_mode == "weak") else "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": bench_config(world, args.dp_mode, args.batch_size, n_steps),
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
                 "gpu_launches": int(args.steps * n_steps * (2 if world == 1 else 4)),
-                "clocks": clk.summary(), "extra": infer, "full_reference_config": full,
+                "clocks": clk.summary(), "extra": infer, "large_batch": large_batch,
+                "full_reference_config": full,
                 "final_val_mape": float(met[0]), "final_train_loss": float(np.mean(losses))}
         print(json.dumps(line))
     if comm is not None:
@@ -508,6 +723,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full", action="store_true",
                     help="skip the full_reference_config training/inference block")
+    ap.add_argument("--dp-mode", choices=["weak", "strong"], default="weak",
+                    help="data parallel (N > 1): weak = bs per rank, strong = the reference "
+                         "batch split across ranks")
+    ap.add_argument("--no-large-batch", action="store_true",
+                    help="skip the desk large-batch (600) variant")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: reduce + Adam of each step overlapped with its backward (default); "
                          "0: sequential reduce kernel (A/B)")

@@ -237,11 +237,11 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
                              nullptr, nullptr, nullptr, none, nullptr, nullptr, loss, step_loss,
                              step_cmd, stream);
     if (st) return st;
-    if ((st = group_start())) return st;
-    st = allreduce_sum(comm, gbuf, m->dev.total, 0, stream);
-    if (!st && step_loss) st = allreduce_sum(comm, step_loss + step, 1, 1, stream);
-    int st2 = group_end();
-    if (st || st2) return st ? st : st2;
+    // gradient: rank-ordered sum (deterministic for a given world size,
+    // independent of NCCL's algorithm choice); the step loss is a logged
+    // scalar
+    if ((st = ordered_allreduce_sum(comm, gbuf, m->dev.total, stream))) return st;
+    if (step_loss && (st = allreduce_sum(comm, step_loss + step, 1, 1, stream))) return st;
     if (opt.kind != kOptNone) {
       st = launch_opt_from_grad(m->dev, gbuf, P, mb, vb, opt, lr, t0, step, stream);
       if (st) return st;
@@ -374,6 +374,7 @@ extern "C" int tpcb_train_epoch(const tpcb_model* m, float* d_params, float* d_p
   int st = check_loss(loss);
   if (st) return st;
   if (plan->n_steps < 0) return TPCB_ERR_VALIDATION;
+  if (comm && (st = ensure_gather(comm, m->dev.total))) return st;  // (outside capture)
   cudaStream_t stream = (cudaStream_t)stream_;
   const LossDev ld = to_dev(loss, tgt != nullptr);
   const OptDev od = to_dev(opt);

@@ -72,16 +72,26 @@ def epoch_batches(rng: np.random.Generator, n_leaves: np.ndarray, batch_size: in
 
 
 def plan_epoch(rng: np.random.Generator, n_leaf: np.ndarray, batch_size: int, world: int = 1,
-               rank: int = 0, tgt_buckets: dict | None = None, n_tgt: int = 0):
+               rank: int = 0, tgt_buckets: dict | None = None, n_tgt: int = 0,
+               dp_mode: str = "weak"):
     """One epoch's batch plan for `rank` of `world` data-parallel ranks.
 
-    Every rank draws the same global plan — `epoch_batches` with
-    batch_size × world (costmodel.py:632-645) and, for fine-tuning, the
-    same-leaf-count target draw per batch (costmodel.py:762-766) — and keeps
-    its contiguous share (np.array_split) of each batch.  Returns (flat int32
-    sample indices, int32 [n_steps, 8] step table: offset, n_src, n_tgt,
-    n_norm = global batch, src_pos, ns_glob, tgt_pos, nt_glob)."""
-    gbs = batch_size * world
+    Every rank draws the same global plan — `epoch_batches`
+    (costmodel.py:632-645) and, for fine-tuning, the same-leaf-count target
+    draw per batch (costmodel.py:762-766) — and keeps its contiguous share
+    (np.array_split) of each global batch.  dp_mode:
+      "strong"  the global batch is the reference's batch_size: each
+                reference batch is split across the ranks, so the epoch has
+                the reference's optimizer steps and batch composition at any
+                world size (SURVEY §8(e));
+      "weak"    the global batch is batch_size × world (batch_size per rank;
+                the reference's semantics at that larger batch size).
+    Returns (flat int32 sample indices, int32 [n_steps, 8] step table:
+    offset, n_src, n_tgt, n_norm = global batch, src_pos, ns_glob, tgt_pos,
+    nt_glob)."""
+    if dp_mode not in ("weak", "strong"):
+        raise ValidationError(f"unknown data-parallel mode '{dp_mode}'")
+    gbs = batch_size * world if dp_mode == "weak" else batch_size
     batches = epoch_batches(rng, n_leaf, gbs)
     parts, steps, off = [], [], 0
     for b in batches:
@@ -113,7 +123,7 @@ class Trainer:
                  valid_latency: np.ndarray | None = None, normalizer=None,
                  target_rag: engine.RaggedHost | None = None, device="cuda",
                  use_graph: bool = True, comm: "engine.Comm | None" = None,
-                 overlap: bool = True):
+                 overlap: bool = True, dp_mode: str = "weak"):
         from .costmodel import device_model
         self.config = config
         self.dm = device_model(config)
@@ -137,10 +147,12 @@ class Trainer:
             self.tgt_buckets = {k: np.asarray(v) for k, v in self.tgt_buckets.items()}
         self.loss = loss_struct
         self.opt = engine.optim_struct(config.optimizer, weight_decay=config.weight_decay)
-        # data parallel (weak scaling): every rank takes a contiguous share of
-        # each global batch of batch_size × world samples (the reference's
-        # semantics at that batch size); gradients all-reduced every step
+        # data parallel: every rank takes a contiguous share of each global
+        # batch (plan_epoch dp_mode: "weak" = batch_size per rank, "strong" =
+        # the reference's batch split across ranks); gradients reduced every
+        # step in rank order (capi_train.cu)
         self.comm = comm
+        self.dp_mode = dp_mode
         self.world = comm.world if comm is not None else 1
         self.rank = comm.rank if comm is not None else 0
         rows = config.batch_size * (2 if self.use_cmd else 1)
@@ -196,7 +208,7 @@ class Trainer:
         """Host batch plan of this rank for one epoch (see plan_epoch)."""
         return plan_epoch(rng, self.n_leaf, self.config.batch_size, self.world, self.rank,
                           self.tgt_buckets if self.use_cmd else None,
-                          len(self.tgt_leaf) if self.use_cmd else 0)
+                          len(self.tgt_leaf) if self.use_cmd else 0, self.dp_mode)
 
     # ------------------------------------------------------------ one epoch
     def run_epoch(self, lr: float, flat: np.ndarray, steps: np.ndarray, profile=None):

@@ -16,7 +16,7 @@ import torch.multiprocessing as mp
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, mode):
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -31,8 +31,9 @@ def _worker(rank, world, port, q):
         for i, L in enumerate(tgt_leaf.tolist()):
             tb.setdefault(L, []).append(i)
         tb = {k: np.asarray(v) for k, v in tb.items()}
-        flat, steps = plan_epoch(np.random.default_rng(9), n_leaf, 8, world, rank, tb,
-                                 len(tgt_leaf))
+        # weak: 8 per rank (global 16); strong: the global batch of 16 split
+        flat, steps = plan_epoch(np.random.default_rng(9), n_leaf, 8 if mode == "weak" else 16,
+                                 world, rank, tb, len(tgt_leaf), dp_mode=mode)
         # gather every rank's plan
         gathered = [None] * world
         dist.all_gather_object(gathered, (flat.tolist(), steps.tolist()))
@@ -62,12 +63,17 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(240)
-def test_dp_plan_partition_and_gradient_allreduce():
+@pytest.mark.parametrize("mode", ["weak", "strong"])
+def test_dp_plan_partition_and_gradient_allreduce(mode):
+    """Both data-parallel modes: "weak" (8 per rank, global batch 16) and
+    "strong" (the global batch of 16 split across the ranks) partition the
+    same world-1 plan of batch 16 — strong keeps the reference's step count
+    for its batch size at any world size."""
     world = 2
-    port = 29500 + (os.getpid() % 2000)
+    port = 29500 + (os.getpid() % 2000) + (0 if mode == "weak" else 7)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, mode)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=200) for _ in range(world)]
@@ -88,6 +94,9 @@ def test_dp_plan_partition_and_gradient_allreduce():
     tb = {k: np.asarray(v) for k, v in tb.items()}
     full_flat, full_steps = plan_epoch(np.random.default_rng(9), n_leaf, 8 * world, 1, 0, tb,
                                        len(tgt_leaf))
+    if mode == "strong":  # the reference's own batching at batch size 16
+        from paper_2311_09690_b200.training import epoch_batches
+        assert len(full_steps) == len(epoch_batches(np.random.default_rng(9), n_leaf, 16))
     plans = [(np.array(f, dtype=np.int64), np.array(s)) for f, s in gathered]
     assert all(len(p[1]) == len(full_steps) for p in plans)
     for k, (o, ns, nt, n_norm, sp, nsg, tp, ntg) in enumerate(full_steps):
