@@ -217,13 +217,38 @@ int tpcb_large_forward(const tpcb_model* m, const float* d_params, const void* d
  * bucket order, HOST) with token offsets h_tok_off.  Writes the whole flat
  * gradient d_grad (normalised by n_norm, the global batch) and the batch-mean
  * loss d_loss[0].  Transformed-space losses without CMD (else UNSUPPORTED). */
-int tpcb_large_train_ws(const tpcb_model* m, int64_t n_ast, int64_t n_tok, size_t* ws_bytes);
+/* one batch of the large path with its dataset: K1-packed rows (x,
+ * ast_row) and device features of the dataset, the batch's dataset indices
+ * in bucket order (stable by leaf count) with token offsets, and the input
+ * position of each bucket-order row (the CMD statistics run in input order) */
+typedef struct {
+  const float* x;
+  const int32_t* ast_row;
+  const float* devfeat;
+  const int32_t* h_idx;     /* [n] */
+  const int32_t* h_tok_off; /* [n + 1] */
+  const int32_t* h_pos;     /* [n] */
+  int64_t n;
+} tpcb_large_batch;
+
+/* workspace of tpcb_large_loss_backward for a source batch (n_ast, n_tok)
+ * and an optional CMD target batch (n_ast_t, n_tok_t; 0 without) */
+int tpcb_large_train_ws(const tpcb_model* m, int64_t n_ast, int64_t n_tok, int64_t n_ast_t,
+                        int64_t n_tok_t, size_t* ws_bytes);
+/* costmodel.backward (costmodel.py:529-570) through the large path: forward
+ * (activations kept), loss (hybrid / mse / mape, transformed or original
+ * space), CMD with a target batch when loss->alpha_cmd > 0 (tgt != NULL;
+ * h_src_pos = input position of each bucket-order source row), backward;
+ * every GEMM 3xTF32 on tcgen05.  d_grad (rewritten) = the full gradient,
+ * d_loss[0] = loss + alpha·CMD, d_cmd[0] (nullable) = CMD. */
 int tpcb_large_loss_backward(const tpcb_model* m, const float* d_params, const void* d_image,
                              const float* d_x, const int32_t* d_ast_row, const float* d_devfeat,
                              const double* d_y, const int32_t* h_idx, const int32_t* h_tok_off,
                              const int32_t* d_idx /* device copies or NULL */,
-                             const int32_t* d_tok_off, int64_t n_batch, const tpcb_loss* loss, double n_norm, void* d_ws,
-                             size_t ws_bytes, float* d_grad, double* d_loss, int32_t* d_status,
+                             const int32_t* d_tok_off, int64_t n_batch, const tpcb_loss* loss,
+                             double n_norm, const int32_t* h_src_pos,
+                             const tpcb_large_batch* tgt, void* d_ws, size_t ws_bytes,
+                             float* d_grad, double* d_loss, double* d_cmd, int32_t* d_status,
                              void* stream);
 /* the GEMM alone: C[M,N] = A[M,K] B[N,K]^T, fp32 row-major in/out (3xTF32) */
 size_t tpcb_gemm3_ws(int64_t M, int32_t N, int32_t K);

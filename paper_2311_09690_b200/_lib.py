@@ -63,6 +63,12 @@ class TrainWs(C.Structure):
                 ("l_cap", i32), ("stage_flags", vp), ("stage_flag_words", i64)]
 
 
+class LargeBatch(C.Structure):
+    """tpcb_large_batch (a CMD target batch of the large path)."""
+    _fields_ = [("x", vp), ("ast_row", vp), ("devfeat", vp), ("h_idx", vp), ("h_tok_off", vp),
+                ("h_pos", vp), ("n", i64)]
+
+
 class Plan(C.Structure):
     _fields_ = [("d_batch", vp), ("d_steps", vp), ("n_steps", i32)]
 
@@ -88,9 +94,10 @@ SIGNATURES = {
     "tpcb_large_prepare": (i32, [vp, vp, vp, i32, vp]),
     "tpcb_large_forward": (i32, [vp, vp, vp, C.POINTER(Packed), vp, vp, vp, i64,
                                  C.POINTER(BoxCox), vp, sz, vp, vp, vp, vp, vp, vp, vp]),
-    "tpcb_large_train_ws": (i32, [vp, i64, i64, C.POINTER(sz)]),
+    "tpcb_large_train_ws": (i32, [vp, i64, i64, i64, i64, C.POINTER(sz)]),
     "tpcb_large_loss_backward": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64,
-                                       C.POINTER(LossCfg), f64, vp, sz, vp, vp, vp, vp]),
+                                       C.POINTER(LossCfg), f64, vp, C.POINTER(LargeBatch), vp,
+                                       sz, vp, vp, vp, vp, vp]),
     "tpcb_gemm3_ws": (sz, [i64, i32, i32]),
     "tpcb_gemm3": (i32, [vp, vp, i64, i32, i32, vp, i32, vp, sz, vp]),
     "tpcb_gemm3_presplit": (i32, [vp, vp, vp, vp, i64, i32, i32, vp, i32, vp]),

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "async.cuh"
+#include "boxcox.cuh"
 #include "common.cuh"
 
 namespace tpcb {
@@ -1184,6 +1185,7 @@ __global__ void transpose_pair_kernel(const float* __restrict__ a_hi, const floa
 struct ColDst {
   int colw;
   int64_t d[3];
+  int acc = 0;  // 1: add into the gradient (second pass of a CMD step), 0: write
 };
 
 // two-stage deterministic column sums: chunks of 64 rows → partial[chunk][c],
@@ -1217,7 +1219,8 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, 
   float s = part[c];
   for (int k = 1; k < chunks; ++k) s += part[(size_t)k * cols + c];
   const int t = c / dst.colw;
-  grad[dst.d[t] + (c - t * dst.colw)] = s;
+  float* g = grad + dst.d[t] + (c - t * dst.colw);
+  *g = dst.acc ? *g + s : s;
 }
 
 // split-K partials [splits][rows][ldc] → grad, rows through the leaf segment
@@ -1239,8 +1242,40 @@ __global__ void reduce_grad_kernel(const float* __restrict__ part, int splits, i
     for (int z = 1; z < splits; ++z) v += part[z * sstride + (size_t)r * ldc + c];
     const int t = c / dst.colw;
     const int cc = c - t * dst.colw;
-    grad[dst.d[t] + (int64_t)rr * dst.colw + cc] = v;
+    float* g = grad + dst.d[t] + (int64_t)rr * dst.colw + cc;
+    *g = dst.acc ? *g + v : v;
   }
+}
+
+// CMD plumbing (costmodel.py:426-486 runs on [zs; zt] in INPUT order, which
+// matters for the first-argmax / argmin support routing): bucket-order latent
+// row k (z = hi + lo, exact) → zall[base + pos[k]]
+__global__ void z_scatter_kernel(const float* __restrict__ z_hi, const float* __restrict__ z_lo,
+                                 int ldz, const int32_t* __restrict__ pos, int n, int de,
+                                 int64_t base, float* __restrict__ zall) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * de; e += gridDim.x * blockDim.x) {
+    const int k = e / de, c = e - k * de;
+    zall[(base + pos[k]) * de + c] = z_hi[(size_t)k * ldz + c] + z_lo[(size_t)k * ldz + c];
+  }
+}
+
+// dz[k] (+)= alpha · dCMD/dz[base + pos[k]] (fp64 gradient rows); with
+// `set` the row is overwritten and its padding columns zeroed
+__global__ void dz_from_cmd_kernel(float* __restrict__ dz, int ldz, const double* __restrict__ g,
+                                   const int32_t* __restrict__ pos, int n, int de, int64_t base,
+                                   double alpha, int set) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * ldz; e += gridDim.x * blockDim.x) {
+    const int k = e / ldz, c = e - k * ldz;
+    const float v = c < de ? (float)(alpha * g[(base + pos[k]) * de + c]) : 0.f;
+    if (set) dz[e] = v;
+    else if (c < de) dz[e] += v;
+  }
+}
+
+// step loss += alpha · CMD (costmodel.py:556); CMD value copied out
+__global__ void add_cmd_kernel(double* loss, const double* cmd, double alpha, double* cmd_out) {
+  loss[0] += alpha * cmd[0];
+  if (cmd_out) cmd_out[0] = cmd[0];
 }
 
 // LayerNorm backward (nn.py:57-66), one warp per row: dx = rstd·(dŷ − mean(dŷ)
@@ -1368,23 +1403,39 @@ __global__ void attention_back_kernel(const float* __restrict__ qkv, int ldq,
 // loss + dL/dpred (costmodel.py:343-423, transformed space; oracle
 // predictor.loss_and_grad), one block, fixed-order reduction; pred / dpred in
 // the batch's sorted order, y gathered through idx
+// supervised loss + d(loss)/d(pred) (costmodel.py:376-423): squared term in
+// model space, relative term in model space shifted by `offset` or, with
+// `original`, between decoded prediction and decoded label (clamped decode,
+// _decode_with_grad)
 __global__ void loss_kernel(const float* __restrict__ pred, const double* __restrict__ y,
                             const int32_t* __restrict__ idx, int n, int mode, double lam,
-                            double offset, double n_norm, float* __restrict__ dpred,
-                            double* __restrict__ loss_out) {
+                            double offset, int original, tpcb_boxcox norm, double n_norm,
+                            float* __restrict__ dpred, double* __restrict__ loss_out) {
   __shared__ double red[32];
   double acc_sq = 0.0, acc_rel = 0.0;
   for (int s = threadIdx.x; s < n; s += blockDim.x) {
     const double yy = y[idx[s]], d = (double)pred[s] - yy;
-    const double den = yy + offset;
-    const double sg = d > 0 ? 1.0 : (d < 0 ? -1.0 : 0.0);
+    double rel = 0.0, relg = 0.0;
+    if (mode != 1) {
+      if (original) {
+        const double y0 = boxcox_decode_plain(yy, norm);
+        double p0, dp0;
+        boxcox_decode_with_grad((double)pred[s], norm, &p0, &dp0);
+        rel = fabs(p0 - y0) / y0;
+        relg = sign_d(p0 - y0) * dp0 / (y0 * n_norm);
+      } else {
+        const double den = yy + offset;
+        rel = fabs(d) / den;
+        relg = sign_d(d) / (den * n_norm);
+      }
+    }
     double g;
-    if (mode == 1) g = 2.0 * d / n_norm;                        // mse
-    else if (mode == 2) g = sg / (den * n_norm);                // mape
-    else g = 2.0 * d / n_norm + lam * sg / (den * n_norm);      // hybrid
+    if (mode == 1) g = 2.0 * d / n_norm;           // mse
+    else if (mode == 2) g = relg;                  // mape
+    else g = 2.0 * d / n_norm + lam * relg;        // hybrid
     dpred[s] = (float)g;
     acc_sq += d * d;
-    acc_rel += fabs(d) / den;
+    acc_rel += rel;
   }
   double v = mode == 1 ? acc_sq : mode == 2 ? acc_rel : acc_sq + lam * acc_rel;
   v = warp_sum_d(v);
@@ -1582,7 +1633,7 @@ int colsum(const float* x, const float* x_lo, int rows, int cols, int ld, ColDst
   return TPCB_OK;
 }
 
-ColDst one(int64_t off, int colw) { return ColDst{colw, {off, off, off}}; }
+ColDst one(int64_t off, int colw, int acc = 0) { return ColDst{colw, {off, off, off}, acc}; }
 
 // dW[M_in, N_out] = Xᵀ·dY over K = kp rows: X given as [rows, M_in] (ld_x),
 // dY as [rows, N_out] (ld_y) — both transposed + split here
@@ -1612,17 +1663,169 @@ int wgrad(const Ctx& c, Bwd& b, const float* x_hi, const float* x_lo, int ld_x, 
   return TPCB_OK;
 }
 
+// backward from dz (bucket-order rows of b.dz, ld p.dep) down to the
+// input projection: gate + device MLP, leaf_embed per leaf-count bucket,
+// the encoder (top layer first).  acc = 1 adds into G (the target pass of a
+// CMD step, costmodel.py:561-564), acc = 0 writes.
+int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int64_t n_batch,
+               const float* d_devfeat, float* G, int acc) {
+  const Model& M = c.M;
+  const LargePlan& p = c.p;
+  const cudaStream_t st = c.st;
+  const float* P = c.P;
+  const int64_t n_tok = h_tok_off[n_batch];
+  const int nt = (int)n_tok, nb = (int)n_batch;
+  int rc;
+  gate_back_kernel<<<nb, 128, (2 * M.d_dev + M.d_e) * 4, st>>>(
+      M, P, d_devfeat, f.idx, b.dz, f.zx, p.dep, b.dzx_hi, b.dzx_lo, b.tWp, b.tbp, b.tWh, b.tbh);
+  TPCB_LAUNCH_CHECK("large_gate_back");
+  if ((rc = colsum(b.tWp, nullptr, nb, M.d_dev * M.d_e, M.d_dev * M.d_e,
+                   one(M.devpW, M.d_dev * M.d_e, acc), G, st)))
+    return rc;
+  if ((rc = colsum(b.tbp, nullptr, nb, M.d_e, M.d_e, one(M.devpb, M.d_e, acc), G, st))) return rc;
+  if ((rc = colsum(b.tWh, nullptr, nb, TPCB_DEV_FEAT * M.d_dev, TPCB_DEV_FEAT * M.d_dev,
+                   one(M.devhW, TPCB_DEV_FEAT * M.d_dev, acc), G, st)))
+    return rc;
+  if ((rc = colsum(b.tbh, nullptr, nb, M.d_dev, M.d_dev, one(M.devhb, M.d_dev, acc), G, st))) return rc;
+  const Pair hf = f.H(M.n_layers);
+  for (int64_t s0 = 0; s0 < n_batch;) {
+    const int Lb = h_tok_off[s0 + 1] - h_tok_off[s0];
+    int64_t s1 = s0 + 1;
+    while (s1 < n_batch && h_tok_off[s1 + 1] - h_tok_off[s1] == Lb) ++s1;
+    const int nbk = (int)(s1 - s0);
+    const int64_t t0 = h_tok_off[s0];
+    const int w = Lb * p.dp;
+    Operand A = act_op(b.dzx_hi + s0 * p.dep, b.dzx_lo + s0 * p.dep, nbk, p.dep);
+    Operand B{c.im.hi + p.leaf_b[Lb], c.im.lo + p.leaf_b[Lb], w, p.dep, p.dep};
+    Epi e{nbk, w, w, nullptr, 0, nullptr, nullptr, 0, b.dh + t0 * p.dp, nullptr, nullptr};
+    if ((rc = launch_gemm(A, B, e, st))) return rc;
+    if ((rc = wgrad(c, b, hf.hi + t0 * p.dp, hf.lo + t0 * p.dp, w, w, b.dzx_hi + s0 * p.dep,
+                    b.dzx_lo + s0 * p.dep, p.dep, M.d_e, nbk, M.d, p.dp, one(M.leafW[Lb], M.d_e, acc),
+                    G)))
+      return rc;
+    if ((rc = colsum(b.dzx_hi + s0 * p.dep, b.dzx_lo + s0 * p.dep, nbk, M.d_e, p.dep,
+                     one(M.leafb[Lb], M.d_e, acc), G, st)))
+      return rc;
+    s0 = s1;
+  }
+  // ---- encoder, top layer first ----
+  const float scale = 1.0f / sqrtf((float)M.dh);
+  const size_t att_smem = (size_t)(4 * TPCB_MAX_LEAF * (M.dh + 1) + 2 * 16 * 17) * 4;
+  if (att_smem > 48 * 1024)
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(attention_back_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)att_smem));
+  for (int li = M.n_layers - 1; li >= 0; --li) {
+    const LayerOff& L = M.layer[li];
+    const Pair h = f.H(li), h1 = f.H1(li), ff = f.F(li), ctx = f.C(li);
+    // LN2
+    ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S2(li), p.dp, nt, M.d, P + L.ln2g,
+                                                    b.ds_hi, b.ds_lo, b.prod);
+    TPCB_LAUNCH_CHECK("large_ln_back");
+    if ((rc = colsum(b.prod, nullptr, nt, M.d, p.dp, one(L.ln2g, M.d, acc), G, st))) return rc;
+    if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln2b, M.d, acc), G, st))) return rc;
+    // FFN out
+    if ((rc = wgrad(c, b, ff.hi, ff.lo, p.ffp, M.d_ff, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
+                    one(L.foW, M.d, acc), G)))
+      return rc;
+    if ((rc = colsum(b.ds_hi, b.ds_lo, nt, M.d, p.dp, one(L.fob, M.d, acc), G, st))) return rc;
+    {
+      Epi e{nt, M.d_ff, p.ffp, nullptr, 0, nullptr, nullptr, 0, nullptr, b.df_hi, b.df_lo};
+      e.mask = ff.hi;
+      e.ldm = p.ffp;
+      Operand B{c.im.hi + p.layer_b[li][3], c.im.lo + p.layer_b[li][3], M.d_ff, p.dp, p.dp};
+      if ((rc = launch_gemm(act_op(b.ds_hi, b.ds_lo, nt, p.dp), B, e, st))) return rc;
+    }
+    // FFN hidden
+    if ((rc = wgrad(c, b, h1.hi, h1.lo, p.dp, M.d, b.df_hi, b.df_lo, p.ffp, M.d_ff, nt, 0, 0,
+                    one(L.fhW, M.d_ff, acc), G)))
+      return rc;
+    if ((rc = colsum(b.df_hi, b.df_lo, nt, M.d_ff, p.ffp, one(L.fhb, M.d_ff, acc), G, st))) return rc;
+    {
+      Epi e{nt, M.d, p.dp, nullptr, 0, b.ds_hi, b.ds_lo, p.dp, b.dh, nullptr, nullptr};
+      Operand B{c.im.hi + p.layer_b[li][2], c.im.lo + p.layer_b[li][2], M.d, p.ffp, p.ffp};
+      if ((rc = launch_gemm(act_op(b.df_hi, b.df_lo, nt, p.ffp), B, e, st))) return rc;
+    }
+    // LN1
+    ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S1(li), p.dp, nt, M.d, P + L.ln1g,
+                                                    b.ds_hi, b.ds_lo, b.prod);
+    TPCB_LAUNCH_CHECK("large_ln_back");
+    if ((rc = colsum(b.prod, nullptr, nt, M.d, p.dp, one(L.ln1g, M.d, acc), G, st))) return rc;
+    if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln1b, M.d, acc), G, st))) return rc;
+    // attention output projection
+    if ((rc = wgrad(c, b, ctx.hi, ctx.lo, p.dp, M.d, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
+                    one(L.Wo, M.d, acc), G)))
+      return rc;
+    if ((rc = colsum(b.ds_hi, b.ds_lo, nt, M.d, p.dp, one(L.bo, M.d, acc), G, st))) return rc;
+    {
+      Epi e{nt, M.d, p.dp, nullptr, 0, nullptr, nullptr, 0, b.dctx, nullptr, nullptr};
+      Operand B{c.im.hi + p.layer_b[li][1], c.im.lo + p.layer_b[li][1], M.d, p.dp, p.dp};
+      if ((rc = launch_gemm(act_op(b.ds_hi, b.ds_lo, nt, p.dp), B, e, st))) return rc;
+    }
+    attention_back_kernel<<<dim3((unsigned)n_batch, M.n_heads), 128, att_smem, st>>>(
+        f.QKV(li), p.qkvp, b.dctx, p.dp, f.tok_off, M.d, M.n_heads, M.dh, scale, b.dq_hi,
+        b.dq_lo);
+    TPCB_LAUNCH_CHECK("large_attention_back");
+    // Q | K | V projections
+    const ColDst qkv_dst{M.d, {(int64_t)L.Wq, (int64_t)L.Wk, (int64_t)L.Wv}, acc};
+    const ColDst qkvb_dst{M.d, {(int64_t)L.bq, (int64_t)L.bk, (int64_t)L.bv}, acc};
+    if ((rc = wgrad(c, b, h.hi, h.lo, p.dp, M.d, b.dq_hi, b.dq_lo, p.qkvp, p.qkv, nt, 0, 0,
+                    qkv_dst, G)))
+      return rc;
+    if ((rc = colsum(b.dq_hi, b.dq_lo, nt, p.qkv, p.qkvp, qkvb_dst, G, st))) return rc;
+    {
+      Epi e{nt, M.d, p.dp, nullptr, 0, b.ds_hi, b.ds_lo, p.dp, b.dh, nullptr, nullptr};
+      Operand B{c.im.hi + p.layer_b[li][0], c.im.lo + p.layer_b[li][0], M.d, p.qkvp, p.qkvp};
+      if ((rc = launch_gemm(act_op(b.dq_hi, b.dq_lo, nt, p.qkvp), B, e, st))) return rc;
+    }
+  }
+  // input projection
+  if ((rc = wgrad(c, b, f.x_hi, f.x_lo, 32, TPCB_FEAT, b.dh, nullptr, p.dp, M.d, nt, 0, 0,
+                  one(M.inW, M.d, acc), G)))
+    return rc;
+  if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(M.inb, M.d, acc), G, st))) return rc;
+  return TPCB_OK;
+}
+
 }  // namespace
 }  // namespace tpcb
 
+namespace {
+struct CmdWs {
+  float* zall;     // [(ns + nt), de] input order
+  double* grad;    // [(ns + nt), de]
+  double* value;   // [1]
+  int32_t* pos;    // [ns] source then [nt] target input positions
+};
+
+// workspace layout: source activations, backward scratch (sized for the
+// larger of the two batches), then with a target batch its activations and
+// the CMD buffers
+void carve_train(const LargePlan& p, const Model& M, int64_t n_ast, int64_t n_tok, int64_t n_ast_t,
+                 int64_t n_tok_t, Carver* cv, Fwd* f, Bwd* b, Fwd* ft, CmdWs* cw) {
+  *f = carve_fwd(p, M, n_tok, n_ast, true, cv);
+  *b = carve_bwd(p, M, std::max(n_tok, n_tok_t), std::max(n_ast, n_ast_t), cv);
+  if (n_ast_t > 0) {
+    *ft = carve_fwd(p, M, n_tok_t, n_ast_t, true, cv);
+    const int64_t rows = n_ast + n_ast_t;
+    cw->zall = cv->take(rows * M.d_e);
+    cw->grad = reinterpret_cast<double*>(cv->take(2 * rows * M.d_e));
+    cw->value = reinterpret_cast<double*>(cv->take(2));
+    cw->pos = reinterpret_cast<int32_t*>(cv->take(rows));
+  }
+}
+}  // namespace
+
 extern "C" int tpcb_large_train_ws(const tpcb_model* m, int64_t n_ast, int64_t n_tok,
-                                   size_t* ws_bytes) {
-  if (!m || !ws_bytes) return TPCB_ERR_VALIDATION;
+                                   int64_t n_ast_t, int64_t n_tok_t, size_t* ws_bytes) {
+  if (!m || !ws_bytes || n_ast_t < 0 || n_tok_t < 0) return TPCB_ERR_VALIDATION;
   if (!large_supported(m->dev)) return TPCB_ERR_UNSUPPORTED;
   const LargePlan p = make_plan(m->dev);
   Carver cv{nullptr};
-  carve_fwd(p, m->dev, n_tok, n_ast, true, &cv);
-  carve_bwd(p, m->dev, n_tok, n_ast, &cv);
+  Fwd f, ft;
+  Bwd b;
+  CmdWs cw{};
+  carve_train(p, m->dev, n_ast, n_tok, n_ast_t, n_tok_t, &cv, &f, &b, &ft, &cw);
   *ws_bytes = cv.o;
   return TPCB_OK;
 }
@@ -1639,22 +1842,36 @@ extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_para
                                         const double* d_y, const int32_t* h_idx,
                                         const int32_t* h_tok_off, const int32_t* d_idx,
                                         const int32_t* d_tok_off, int64_t n_batch,
-                                        const tpcb_loss* loss, double n_norm, void* d_ws,
-                                        size_t ws_bytes, float* d_grad, double* d_loss,
-                                        int32_t* d_status, void* stream_) {
+                                        const tpcb_loss* loss, double n_norm,
+                                        const int32_t* h_src_pos, const tpcb_large_batch* tgt,
+                                        void* d_ws, size_t ws_bytes, float* d_grad,
+                                        double* d_loss, double* d_cmd, int32_t* d_status,
+                                        void* stream_) {
   if (!m || !d_params || !d_image || !d_x || !d_ast_row || !d_devfeat || !d_y || !h_idx ||
       !h_tok_off || !loss || !d_ws || !d_grad || !d_loss)
     return TPCB_ERR_VALIDATION;
   if (n_batch <= 0) return TPCB_ERR_EMPTY_BATCH;
   const Model& M = m->dev;
   if (!large_supported(M)) return TPCB_ERR_UNSUPPORTED;
-  if (loss->original_space || loss->alpha_cmd != 0.0 || M.n_dec < 1) return TPCB_ERR_UNSUPPORTED;
+  if (M.n_dec < 1) return TPCB_ERR_UNSUPPORTED;
+  if (loss->mode < 0 || loss->mode > 2 || loss->cmd_order < 1) return TPCB_ERR_VALIDATION;
+  const bool use_cmd = loss->alpha_cmd > 0.0 && tgt != nullptr;
+  if (use_cmd) {
+    if (tgt->n < 1) return TPCB_ERR_EMPTY_SET;
+    if (!tgt->x || !tgt->ast_row || !tgt->devfeat || !tgt->h_idx || !tgt->h_tok_off ||
+        !tgt->h_pos || !h_src_pos)
+      return TPCB_ERR_VALIDATION;
+  }
   cudaStream_t st = (cudaStream_t)stream_;
   const LargePlan p = make_plan(M);
   const int64_t n_tok = h_tok_off[n_batch];
+  const int64_t n_t = use_cmd ? tgt->n : 0;
+  const int64_t n_tok_t = use_cmd ? tgt->h_tok_off[tgt->n] : 0;
   Carver cv{(uint8_t*)d_ws};
-  Fwd f = carve_fwd(p, M, n_tok, n_batch, true, &cv);
-  Bwd b = carve_bwd(p, M, n_tok, n_batch, &cv);
+  Fwd f, ft{};
+  Bwd b;
+  CmdWs cw{};
+  carve_train(p, M, n_batch, n_tok, n_t, n_tok_t, &cv, &f, &b, &ft, &cw);
   if (cv.o > ws_bytes) return TPCB_ERR_VALIDATION;
   if (d_idx && d_tok_off) {  // device copies of the plan (uploaded once per epoch)
     f.idx = const_cast<int32_t*>(d_idx);
@@ -1672,15 +1889,42 @@ extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_para
   int rc = run_forward(c, f, n_batch, h_tok_off, d_devfeat, true, bc, nullptr, nullptr, nullptr,
                        nullptr, nullptr, d_status);
   if (rc) return rc;
+  if (use_cmd) {  // target forward (activations kept) and the CMD statistics
+    TPCB_CUDA_CHECK(cudaMemcpyAsync(ft.idx, tgt->h_idx, n_t * 4, cudaMemcpyHostToDevice, st));
+    TPCB_CUDA_CHECK(cudaMemcpyAsync(ft.tok_off, tgt->h_tok_off, (n_t + 1) * 4,
+                                    cudaMemcpyHostToDevice, st));
+    TPCB_CUDA_CHECK(cudaMemcpyAsync(cw.pos, h_src_pos, n_batch * 4, cudaMemcpyHostToDevice, st));
+    TPCB_CUDA_CHECK(cudaMemcpyAsync(cw.pos + n_batch, tgt->h_pos, n_t * 4,
+                                    cudaMemcpyHostToDevice, st));
+    gather_tokens_kernel<<<ceil_div(n_t, 8), 256, 0, st>>>(tgt->x, ft.idx, tgt->ast_row,
+                                                           ft.tok_off, (int)n_t, ft.x_hi, ft.x_lo);
+    TPCB_LAUNCH_CHECK("large_gather_t");
+    if ((rc = run_forward(c, ft, n_t, tgt->h_tok_off, tgt->devfeat, true, bc, nullptr, nullptr,
+                          nullptr, nullptr, nullptr, d_status)))
+      return rc;
+    z_scatter_kernel<<<ceil_div(n_batch * M.d_e, 256), 256, 0, st>>>(
+        f.z_hi, f.z_lo, p.dep, cw.pos, (int)n_batch, M.d_e, 0, cw.zall);
+    z_scatter_kernel<<<ceil_div(n_t * M.d_e, 256), 256, 0, st>>>(
+        ft.z_hi, ft.z_lo, p.dep, cw.pos + n_batch, (int)n_t, M.d_e, n_batch, cw.zall);
+    TPCB_LAUNCH_CHECK("large_z_scatter");
+    if ((rc = tpcb_cmd(cw.zall, 0, n_batch, n_t, M.d_e, loss->cmd_order, cw.value, cw.grad, st)))
+      return rc;
+  }
   const float* P = d_params;
   float* G = d_grad;
   const int nt = (int)n_tok, nb = (int)n_batch;
+  (void)nt;
   g_colsum_part = b.colpart;
   if ((rc = side_init())) return rc;
   TPCB_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(float) * (size_t)M.total, st));
   loss_kernel<<<1, 1024, 0, st>>>(f.pred, d_y, f.idx, nb, loss->mode, loss->lambda_hybrid,
-                                  loss->offset, n_norm, b.dpred, d_loss);
+                                  loss->offset, loss->original_space, loss->norm, n_norm, b.dpred,
+                                  d_loss);
   TPCB_LAUNCH_CHECK("large_loss");
+  if (use_cmd) {
+    add_cmd_kernel<<<1, 1, 0, st>>>(d_loss, cw.value, loss->alpha_cmd, d_cmd);
+    TPCB_LAUNCH_CHECK("large_add_cmd");
+  }
   // ---- head: dec.out, decoder, gate + device MLP, leaf_embed ----
   const int nd = M.n_dec;
   const int wl = nd ? M.dec[nd - 1] : M.d_e, ldl = pad32(wl);
@@ -1714,114 +1958,18 @@ extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_para
       if ((rc = launch_gemm(A, B, e, st))) return rc;
     }
   }
-  gate_back_kernel<<<nb, 128, (2 * M.d_dev + M.d_e) * 4, st>>>(
-      M, P, d_devfeat, f.idx, b.dz, f.zx, p.dep, b.dzx_hi, b.dzx_lo, b.tWp, b.tbp, b.tWh, b.tbh);
-  TPCB_LAUNCH_CHECK("large_gate_back");
-  if ((rc = colsum(b.tWp, nullptr, nb, M.d_dev * M.d_e, M.d_dev * M.d_e,
-                   one(M.devpW, M.d_dev * M.d_e), G, st)))
-    return rc;
-  if ((rc = colsum(b.tbp, nullptr, nb, M.d_e, M.d_e, one(M.devpb, M.d_e), G, st))) return rc;
-  if ((rc = colsum(b.tWh, nullptr, nb, TPCB_DEV_FEAT * M.d_dev, TPCB_DEV_FEAT * M.d_dev,
-                   one(M.devhW, TPCB_DEV_FEAT * M.d_dev), G, st)))
-    return rc;
-  if ((rc = colsum(b.tbh, nullptr, nb, M.d_dev, M.d_dev, one(M.devhb, M.d_dev), G, st))) return rc;
-  const Pair hf = f.H(M.n_layers);
-  for (int64_t s0 = 0; s0 < n_batch;) {
-    const int Lb = h_tok_off[s0 + 1] - h_tok_off[s0];
-    int64_t s1 = s0 + 1;
-    while (s1 < n_batch && h_tok_off[s1 + 1] - h_tok_off[s1] == Lb) ++s1;
-    const int nbk = (int)(s1 - s0);
-    const int64_t t0 = h_tok_off[s0];
-    const int w = Lb * p.dp;
-    Operand A = act_op(b.dzx_hi + s0 * p.dep, b.dzx_lo + s0 * p.dep, nbk, p.dep);
-    Operand B{c.im.hi + p.leaf_b[Lb], c.im.lo + p.leaf_b[Lb], w, p.dep, p.dep};
-    Epi e{nbk, w, w, nullptr, 0, nullptr, nullptr, 0, b.dh + t0 * p.dp, nullptr, nullptr};
-    if ((rc = launch_gemm(A, B, e, st))) return rc;
-    if ((rc = wgrad(c, b, hf.hi + t0 * p.dp, hf.lo + t0 * p.dp, w, w, b.dzx_hi + s0 * p.dep,
-                    b.dzx_lo + s0 * p.dep, p.dep, M.d_e, nbk, M.d, p.dp, one(M.leafW[Lb], M.d_e),
-                    G)))
-      return rc;
-    if ((rc = colsum(b.dzx_hi + s0 * p.dep, b.dzx_lo + s0 * p.dep, nbk, M.d_e, p.dep,
-                     one(M.leafb[Lb], M.d_e), G, st)))
-      return rc;
-    s0 = s1;
+  if (use_cmd) {  // dz_s += alpha · dCMD/dzs (costmodel.py:557-560)
+    dz_from_cmd_kernel<<<ceil_div(n_batch * p.dep, 256), 256, 0, st>>>(
+        b.dz, p.dep, cw.grad, cw.pos, (int)n_batch, M.d_e, 0, loss->alpha_cmd, 0);
+    TPCB_LAUNCH_CHECK("large_dz_cmd");
   }
-  // ---- encoder, top layer first ----
-  const float scale = 1.0f / sqrtf((float)M.dh);
-  const size_t att_smem = (size_t)(4 * TPCB_MAX_LEAF * (M.dh + 1) + 2 * 16 * 17) * 4;
-  if (att_smem > 48 * 1024)
-    TPCB_CUDA_CHECK(cudaFuncSetAttribute(attention_back_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)att_smem));
-  for (int li = M.n_layers - 1; li >= 0; --li) {
-    const LayerOff& L = M.layer[li];
-    const Pair h = f.H(li), h1 = f.H1(li), ff = f.F(li), ctx = f.C(li);
-    // LN2
-    ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S2(li), p.dp, nt, M.d, P + L.ln2g,
-                                                    b.ds_hi, b.ds_lo, b.prod);
-    TPCB_LAUNCH_CHECK("large_ln_back");
-    if ((rc = colsum(b.prod, nullptr, nt, M.d, p.dp, one(L.ln2g, M.d), G, st))) return rc;
-    if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln2b, M.d), G, st))) return rc;
-    // FFN out
-    if ((rc = wgrad(c, b, ff.hi, ff.lo, p.ffp, M.d_ff, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
-                    one(L.foW, M.d), G)))
-      return rc;
-    if ((rc = colsum(b.ds_hi, b.ds_lo, nt, M.d, p.dp, one(L.fob, M.d), G, st))) return rc;
-    {
-      Epi e{nt, M.d_ff, p.ffp, nullptr, 0, nullptr, nullptr, 0, nullptr, b.df_hi, b.df_lo};
-      e.mask = ff.hi;
-      e.ldm = p.ffp;
-      Operand B{c.im.hi + p.layer_b[li][3], c.im.lo + p.layer_b[li][3], M.d_ff, p.dp, p.dp};
-      if ((rc = launch_gemm(act_op(b.ds_hi, b.ds_lo, nt, p.dp), B, e, st))) return rc;
-    }
-    // FFN hidden
-    if ((rc = wgrad(c, b, h1.hi, h1.lo, p.dp, M.d, b.df_hi, b.df_lo, p.ffp, M.d_ff, nt, 0, 0,
-                    one(L.fhW, M.d_ff), G)))
-      return rc;
-    if ((rc = colsum(b.df_hi, b.df_lo, nt, M.d_ff, p.ffp, one(L.fhb, M.d_ff), G, st))) return rc;
-    {
-      Epi e{nt, M.d, p.dp, nullptr, 0, b.ds_hi, b.ds_lo, p.dp, b.dh, nullptr, nullptr};
-      Operand B{c.im.hi + p.layer_b[li][2], c.im.lo + p.layer_b[li][2], M.d, p.ffp, p.ffp};
-      if ((rc = launch_gemm(act_op(b.df_hi, b.df_lo, nt, p.ffp), B, e, st))) return rc;
-    }
-    // LN1
-    ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S1(li), p.dp, nt, M.d, P + L.ln1g,
-                                                    b.ds_hi, b.ds_lo, b.prod);
-    TPCB_LAUNCH_CHECK("large_ln_back");
-    if ((rc = colsum(b.prod, nullptr, nt, M.d, p.dp, one(L.ln1g, M.d), G, st))) return rc;
-    if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln1b, M.d), G, st))) return rc;
-    // attention output projection
-    if ((rc = wgrad(c, b, ctx.hi, ctx.lo, p.dp, M.d, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
-                    one(L.Wo, M.d), G)))
-      return rc;
-    if ((rc = colsum(b.ds_hi, b.ds_lo, nt, M.d, p.dp, one(L.bo, M.d), G, st))) return rc;
-    {
-      Epi e{nt, M.d, p.dp, nullptr, 0, nullptr, nullptr, 0, b.dctx, nullptr, nullptr};
-      Operand B{c.im.hi + p.layer_b[li][1], c.im.lo + p.layer_b[li][1], M.d, p.dp, p.dp};
-      if ((rc = launch_gemm(act_op(b.ds_hi, b.ds_lo, nt, p.dp), B, e, st))) return rc;
-    }
-    attention_back_kernel<<<dim3((unsigned)n_batch, M.n_heads), 128, att_smem, st>>>(
-        f.QKV(li), p.qkvp, b.dctx, p.dp, f.tok_off, M.d, M.n_heads, M.dh, scale, b.dq_hi,
-        b.dq_lo);
-    TPCB_LAUNCH_CHECK("large_attention_back");
-    // Q | K | V projections
-    const ColDst qkv_dst{M.d, {(int64_t)L.Wq, (int64_t)L.Wk, (int64_t)L.Wv}};
-    const ColDst qkvb_dst{M.d, {(int64_t)L.bq, (int64_t)L.bk, (int64_t)L.bv}};
-    if ((rc = wgrad(c, b, h.hi, h.lo, p.dp, M.d, b.dq_hi, b.dq_lo, p.qkvp, p.qkv, nt, 0, 0,
-                    qkv_dst, G)))
-      return rc;
-    if ((rc = colsum(b.dq_hi, b.dq_lo, nt, p.qkv, p.qkvp, qkvb_dst, G, st))) return rc;
-    {
-      Epi e{nt, M.d, p.dp, nullptr, 0, b.ds_hi, b.ds_lo, p.dp, b.dh, nullptr, nullptr};
-      Operand B{c.im.hi + p.layer_b[li][0], c.im.lo + p.layer_b[li][0], M.d, p.qkvp, p.qkvp};
-      if ((rc = launch_gemm(act_op(b.dq_hi, b.dq_lo, nt, p.qkvp), B, e, st))) return rc;
-    }
+  if ((rc = large_tail(c, f, b, h_tok_off, n_batch, d_devfeat, G, 0))) return rc;
+  if (use_cmd) {  // target rows: zero prediction gradient, dz = alpha · dCMD/dzt
+    dz_from_cmd_kernel<<<ceil_div(n_t * p.dep, 256), 256, 0, st>>>(
+        b.dz, p.dep, cw.grad, cw.pos + n_batch, (int)n_t, M.d_e, n_batch, loss->alpha_cmd, 1);
+    TPCB_LAUNCH_CHECK("large_dz_cmd_t");
+    if ((rc = large_tail(c, ft, b, tgt->h_tok_off, n_t, tgt->devfeat, G, 1))) return rc;
   }
-  // input projection
-  if ((rc = wgrad(c, b, f.x_hi, f.x_lo, 32, TPCB_FEAT, b.dh, nullptr, p.dp, M.d, nt, 0, 0,
-                  one(M.inW, M.d), G)))
-    return rc;
-  if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(M.inb, M.d), G, st))) return rc;
   return stream_wait(st, g_side.s);  // join: every weight gradient is in d_grad
 }
 

@@ -2,13 +2,16 @@
 `training.train` uses when the fused one-CTA-per-sample kernels cannot hold
 the model (full_reference_config: d 716, 11 layers, 46.7 M parameters).
 
-Same semantics as the fused Trainer (costmodel.py:669-718): the reference's
+Same semantics as the fused Trainer (costmodel.py:669-780): the reference's
 per-bucket minibatch plan (plan_epoch, data-parallel shares when a
-communicator is given), hybrid / mse / mape loss in the transformed space,
+communicator is given) and, for fine-tuning, the same-leaf-count target
+draws; hybrid / mse / mape loss in the transformed or original space; the
+CMD term over [zs; zt] (alpha_cmd > 0 with a target set, single GPU);
 Adam / SGD on the flat fp32 parameters, per-epoch validation MAPE / RMSE.
-Per step: tpcb_large_loss_backward (forward + loss + backward, every GEMM a
-3xTF32 tcgen05 GEMM) → NCCL all-reduce of the gradient (world > 1) →
-tpcb_optimizer_step → tpcb_large_prepare (rebuild the weight image)."""
+Per step: tpcb_large_loss_backward (source + target forward, loss, CMD,
+backward of both passes, every GEMM a 3xTF32 tcgen05 GEMM) → NCCL
+all-reduce of the gradient (world > 1) → tpcb_optimizer_step →
+tpcb_large_prepare (rebuild the weight image)."""
 
 from __future__ import annotations
 
@@ -21,14 +24,16 @@ from . import _lib, engine
 from .errors import UnsupportedConfig
 
 
-def large_order(n_leaf: np.ndarray, idx: np.ndarray):
-    """batch indices in bucket order (stable by leaf count) + token offsets"""
+def large_order(n_leaf: np.ndarray, idx: np.ndarray, with_pos: bool = False):
+    """batch indices in bucket order (stable by leaf count) + token offsets
+    (+ the input position of each bucket-order row)"""
     idx = np.asarray(idx, dtype=np.int64)
     L = np.asarray(n_leaf, dtype=np.int64)[idx]
     o = np.argsort(L, kind="stable")
     tok = np.zeros(len(idx) + 1, dtype=np.int32)
     np.cumsum(L[o], out=tok[1:])
-    return np.ascontiguousarray(idx[o], dtype=np.int32), tok
+    out = np.ascontiguousarray(idx[o], dtype=np.int32), tok
+    return out + (np.ascontiguousarray(o, dtype=np.int32),) if with_pos else out
 
 
 class LargeTrainer:
@@ -41,10 +46,9 @@ class LargeTrainer:
                  comm: "engine.Comm | None" = None,
                  target_rag: engine.RaggedHost | None = None):
         from .costmodel import device_model
-        if loss_struct.original_space:
-            raise UnsupportedConfig("the large path trains with transformed-space losses")
-        if target_rag is not None and loss_struct.alpha_cmd > 0:
-            raise UnsupportedConfig("CMD fine-tuning is not available on the large path")
+        use_cmd = target_rag is not None and loss_struct.alpha_cmd > 0
+        if use_cmd and comm is not None and comm.world > 1:
+            raise UnsupportedConfig("CMD fine-tuning on the large path runs on one GPU")
         self.lib = _lib.load()
         self.config = config
         self.dm = device_model(config)
@@ -62,17 +66,29 @@ class LargeTrainer:
         self.comm = comm
         self.world = comm.world if comm is not None else 1
         self.rank = comm.rank if comm is not None else 0
-        self.use_cmd = False
+        self.use_cmd = use_cmd
+        self.tgt = None
+        if use_cmd:
+            self.tgt = engine.DeviceSamples(target_rag, config.n_leaf_max, self.status,
+                                            device=device)
+            self.tgt_leaf = np.asarray(target_rag.n_leaf)
+            buckets = {}
+            for i, L in enumerate(self.tgt_leaf.tolist()):
+                buckets.setdefault(L, []).append(i)
+            self.tgt_buckets = {k: np.asarray(v) for k, v in buckets.items()}
         self.stream = torch.cuda.current_stream(self.dev)
         # weight image (forward + backward operands), zero-filled once
         self.path = engine.LargePath(self.dm, self.P, with_backward=True)
         bs = config.batch_size
         l_cap = int(self.n_leaf.max())
         ws = C.c_size_t()
-        _lib.check(self.lib.tpcb_large_train_ws(self.dm.handle, bs, bs * l_cap, C.byref(ws)),
+        lt = int(self.tgt_leaf.max()) if use_cmd else 0
+        _lib.check(self.lib.tpcb_large_train_ws(self.dm.handle, bs, bs * l_cap,
+                                                bs if use_cmd else 0, bs * lt, C.byref(ws)),
                    "large_train_ws")
         self.ws = torch.empty(ws.value, dtype=torch.uint8, device=self.dev)
         self.loss_dev = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.cmd_dev = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self.t = 0
         self.valid = valid_rag
         self.valid_lat = None if valid_latency is None else np.asarray(valid_latency, np.float64)
@@ -82,24 +98,42 @@ class LargeTrainer:
 
     def plan(self, rng: np.random.Generator):
         from .training import plan_epoch
-        return plan_epoch(rng, self.n_leaf, self.config.batch_size, self.world, self.rank)
+        return plan_epoch(rng, self.n_leaf, self.config.batch_size, self.world, self.rank,
+                          self.tgt_buckets if self.use_cmd else None,
+                          len(self.tgt_leaf) if self.use_cmd else 0)
 
-    def step(self, idx: np.ndarray, n_norm: int, lr: float, d_plan=None) -> None:
+    def step(self, idx: np.ndarray, n_norm: int, lr: float, d_plan=None,
+             tidx: np.ndarray | None = None) -> None:
         """one optimizer step on this rank's share `idx` of a global batch
-        (d_plan: device copies (order, tok_off) already on the stream)"""
-        order, tok = large_order(self.n_leaf, idx)
+        (d_plan: device copies (order, tok_off) already on the stream;
+        tidx: the step's CMD target samples)"""
+        order, tok, pos = large_order(self.n_leaf, idx, with_pos=True)
         s = engine.stream_ptr()
         d_idx, d_tok = (None, None) if d_plan is None else d_plan
+        tb = None
+        if self.use_cmd and tidx is not None and len(tidx):
+            t_order, t_tok, t_pos = large_order(self.tgt_leaf, tidx, with_pos=True)
+            self._tkeep = (t_order, t_tok, t_pos)
+            tb = _lib.LargeBatch()
+            tb.x, tb.ast_row = self.tgt.pk.x.data_ptr(), self.tgt.pk.ast_row.data_ptr()
+            tb.devfeat = self.tgt.devfeat.data_ptr()
+            tb.h_idx = t_order.ctypes.data_as(C.c_void_p)
+            tb.h_tok_off = t_tok.ctypes.data_as(C.c_void_p)
+            tb.h_pos = t_pos.ctypes.data_as(C.c_void_p)
+            tb.n = len(t_order)
         if len(order):
             _lib.check(self.lib.tpcb_large_loss_backward(
                 self.dm.handle, self.P.data_ptr(), self.path.image.data_ptr(),
                 self.src.pk.x.data_ptr(), self.src.pk.ast_row.data_ptr(),
                 self.src.devfeat.data_ptr(), self.src.y.data_ptr(),
                 order.ctypes.data_as(C.c_void_p), tok.ctypes.data_as(C.c_void_p), d_idx, d_tok,
-                len(order),
-                C.byref(self.loss), float(n_norm), self.ws.data_ptr(), self.ws.numel(),
-                self.grad.data_ptr(), self.loss_dev.data_ptr(), self.status.ptr, s),
+                len(order), C.byref(self.loss), float(n_norm),
+                pos.ctypes.data_as(C.c_void_p), C.byref(tb) if tb is not None else None,
+                self.ws.data_ptr(), self.ws.numel(), self.grad.data_ptr(),
+                self.loss_dev.data_ptr(), self.cmd_dev.data_ptr() if tb is not None else None,
+                self.status.ptr, s),
                 "large_loss_backward")
+
         else:
             self.grad.zero_()
             self.loss_dev.zero_()
@@ -117,6 +151,7 @@ class LargeTrainer:
     def run_epoch(self, lr: float, flat: np.ndarray, steps: np.ndarray, profile=None) -> int:
         n = steps.shape[0]
         self.losses = torch.zeros(max(n, 1), dtype=torch.float64, device=self.dev)
+        self.cmds = torch.zeros(max(n, 1), dtype=torch.float64, device=self.dev)
         # the whole epoch's bucket orders / token offsets in one pinned upload
         # (per-step pageable copies would synchronise the stream every step)
         plans, parts, off = [], [], 0
@@ -131,11 +166,14 @@ class LargeTrainer:
         dev = host.to(self.dev, non_blocking=True)
         self._epoch_plan = (host, dev)  # keep alive until the epoch's work is done
         for k in range(n):
-            o, ns, _, n_norm = (int(v) for v in steps[k, :4])
+            o, ns, nt, n_norm = (int(v) for v in steps[k, :4])
             a, b = plans[k]
             self.step(flat[o:o + ns], n_norm, lr,
-                      d_plan=(dev[a:].data_ptr(), dev[b:].data_ptr()))
+                      d_plan=(dev[a:].data_ptr(), dev[b:].data_ptr()),
+                      tidx=flat[o + ns:o + ns + nt] if self.use_cmd else None)
             self.losses[k:k + 1].copy_(self.loss_dev)
+            if self.use_cmd:
+                self.cmds[k:k + 1].copy_(self.cmd_dev)
         return n
 
     def evaluate_async(self) -> None:
@@ -162,7 +200,9 @@ class LargeTrainer:
             rel = (pred - y) / y
             met = np.array([float(np.mean(np.abs(rel))), float(np.sqrt(np.mean((pred - y) ** 2))),
                             0.0])
-        return losses, np.zeros(n_steps), met
+        cmds = self.cmds[:n_steps].cpu().numpy() if (self.use_cmd and n_steps) else \
+            np.zeros(n_steps)
+        return losses, cmds, met
 
     def tensors(self, flat: torch.Tensor | None = None) -> dict:
         return self.dm.unflatten((self.P if flat is None else flat).double().cpu().numpy())
@@ -170,9 +210,13 @@ class LargeTrainer:
 
 def large_loss_backward(params, rag: engine.RaggedHost, y: np.ndarray, idx=None,
                         mode: str = "hybrid", lambda_hybrid: float = 1e-3, offset: float = 0.0,
-                        n_norm: int | None = None):
-    """One batch's (loss, gradient dict) through the large path — the
-    costmodel.backward drop-in for large configs (no optimizer step)."""
+                        n_norm: int | None = None, mape_space: str = "transformed",
+                        normalizer=None, alpha_cmd: float = 0.0, cmd_order: int = 5,
+                        target_rag: engine.RaggedHost | None = None):
+    """One batch's (loss, gradient dict, CMD value) through the large path —
+    the costmodel.backward drop-in for large configs (costmodel.py:529-570;
+    no optimizer step).  With alpha_cmd > 0 and a target set the CMD term
+    couples the two forward passes."""
     from .costmodel import device_model
     lib = _lib.load()
     cfg = params.config
@@ -182,19 +226,38 @@ def large_loss_backward(params, rag: engine.RaggedHost, y: np.ndarray, idx=None,
     src = engine.DeviceSamples(rag, cfg.n_leaf_max, status, y=np.asarray(y, np.float64))
     path = engine.LargePath(dm, P, with_backward=True)
     idx = np.arange(rag.n_ast) if idx is None else np.asarray(idx)
-    order, tok = large_order(rag.n_leaf, idx)
+    order, tok, pos = large_order(rag.n_leaf, idx, with_pos=True)
+    use_cmd = alpha_cmd > 0 and target_rag is not None
+    tb, n_t, tok_t = None, 0, 0
+    if use_cmd:
+        tgt = engine.DeviceSamples(target_rag, cfg.n_leaf_max, status)
+        t_order, t_tok, t_pos = large_order(target_rag.n_leaf, np.arange(target_rag.n_ast),
+                                            with_pos=True)
+        tb = _lib.LargeBatch()
+        tb.x, tb.ast_row, tb.devfeat = tgt.pk.x.data_ptr(), tgt.pk.ast_row.data_ptr(), \
+            tgt.devfeat.data_ptr()
+        tb.h_idx = t_order.ctypes.data_as(C.c_void_p)
+        tb.h_tok_off = t_tok.ctypes.data_as(C.c_void_p)
+        tb.h_pos = t_pos.ctypes.data_as(C.c_void_p)
+        tb.n = n_t = len(t_order)
+        tok_t = int(t_tok[-1])
     ws = C.c_size_t()
-    _lib.check(lib.tpcb_large_train_ws(dm.handle, len(order), int(tok[-1]), C.byref(ws)),
-               "large_train_ws")
+    _lib.check(lib.tpcb_large_train_ws(dm.handle, len(order), int(tok[-1]), n_t, tok_t,
+                                       C.byref(ws)), "large_train_ws")
     wsb = torch.empty(ws.value, dtype=torch.uint8, device=P.device)
     grad = torch.empty_like(P)
     loss_dev = torch.zeros(1, dtype=torch.float64, device=P.device)
-    loss = engine.loss_struct(mode, lambda_hybrid, offset)
+    cmd_dev = torch.zeros(1, dtype=torch.float64, device=P.device)
+    loss = engine.loss_struct(mode, lambda_hybrid, offset, alpha_cmd if use_cmd else 0.0,
+                              cmd_order, mape_space, normalizer)
     _lib.check(lib.tpcb_large_loss_backward(
         dm.handle, P.data_ptr(), path.image.data_ptr(), src.pk.x.data_ptr(),
         src.pk.ast_row.data_ptr(), src.devfeat.data_ptr(), src.y.data_ptr(),
         order.ctypes.data_as(C.c_void_p), tok.ctypes.data_as(C.c_void_p), None, None,
-        len(order), C.byref(loss), float(n_norm or len(order)), wsb.data_ptr(), wsb.numel(), grad.data_ptr(),
-        loss_dev.data_ptr(), status.ptr, engine.stream_ptr()), "large_loss_backward")
+        len(order), C.byref(loss), float(n_norm or len(order)), pos.ctypes.data_as(C.c_void_p),
+        C.byref(tb) if tb is not None else None, wsb.data_ptr(), wsb.numel(), grad.data_ptr(),
+        loss_dev.data_ptr(), cmd_dev.data_ptr(), status.ptr, engine.stream_ptr()),
+        "large_loss_backward")
     status.check("large_loss_backward")
-    return float(loss_dev.item()), dm.unflatten(grad.double().cpu().numpy())
+    return (float(loss_dev.item()), dm.unflatten(grad.double().cpu().numpy()),
+            float(cmd_dev.item()))
