@@ -4,8 +4,8 @@ float64 oracle and the fp32 parity path.
 Stated tolerance of the bf16 mode (north_star: "bf16 path tolerance stated
 separately"), on the reference-trained desk checkpoint and the reference's
 4,096-AST C1 set: decoded latency within 0.10 relative of the float64
-oracle for every AST and 0.02 relative on average (measured: max 3.4e-2,
-mean 5.7e-3); model-space predictions within 0.05·(1+|p|).  The fp32 mode
+oracle for every AST and 0.02 relative on average (measured with the
+current two-warpgroup kernel: max 5.1e-2, mean 1.1e-2); model-space predictions within 0.05·(1+|p|).  The fp32 mode
 keeps the 1e-3 bar (test_gpu_forward.py)."""
 
 import numpy as np
@@ -52,6 +52,7 @@ def test_bf16_forward_vs_oracle_and_fp32():
     pred_b, lat_b, zv_b = out["bf16"]
     assert np.all(np.abs(pred_b - ref_pred) <= 0.05 * (1 + np.abs(ref_pred)))
     rel = np.abs(lat_b - ref_lat) / np.abs(ref_lat)
+    print(f"bf16 decoded-latency rel err vs fp64: max {rel.max():.3e} mean {rel.mean():.3e}")
     assert rel.max() <= 0.10, rel.max()
     assert rel.mean() <= 0.02, rel.mean()
     # the device MLP never touches the tensor cores: identical to the fp32 mode
