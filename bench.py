@@ -460,9 +460,15 @@ def run_large_batch(cfg, train, targets, norm, dv, dev, flush_l2, batch: int = 6
     out = {"global_batch": batch,
            "semantics": "the reference's train loop at batch_size 600 (per-bucket batches of "
                         "<= 600, ~437 optimizer steps per epoch): a different optimisation "
-                        "trajectory from bs 64, same per-sample work"}
+                        "trajectory from bs 64, same per-sample work",
+           "variants": "fused_ffma: train4 + slot reduce + Adam; fused_ffma_wgrad_tcgen05: "
+                       "the encoder weight gradients as tcgen05 3xTF32 GEMMs over the "
+                       "step's token rows (wgrad.cu); tcgen05_3xtf32_layerwise: large.cu"}
     for name, mk in (("fused_ffma", lambda: Trainer(cfg6, params.tensors, rag_of(train, dv),
                                                     targets, loss, device=dev)),
+                     ("fused_ffma_wgrad_tcgen05",
+                      lambda: Trainer(cfg6, params.tensors, rag_of(train, dv), targets, loss,
+                                      device=dev, wgrad_tc=True)),
                      ("tcgen05_3xtf32_layerwise",
                       lambda: LargeTrainer(cfg6, params.tensors, rag_of(train, dv), targets,
                                            loss, device=dev))):

@@ -291,6 +291,12 @@ typedef struct {
    * of a step is co-resident with the reduce blocks (occupancy check). */
   uint64_t* stage_flags;
   int64_t stage_flag_words;
+  /* encoder weight gradients on the tensor cores (desk-shaped models, steps
+   * without CMD): operand rows the training kernel stores for one GEMM per
+   * weight matrix over the step's token rows, act_floats long
+   * (tpcb_train_ws_sizes); NULL keeps them in the per-sample slots */
+  float* act;
+  int64_t act_floats;
 } tpcb_train_ws;
 
 /* epoch plan: steps[s] = 8 × int32 {offset into d_batch, n_src, n_tgt,
@@ -306,7 +312,7 @@ typedef struct {
 
 int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t l_cap, int32_t* n_slots,
                         int64_t* slot_stride, int64_t* zall_floats, int64_t* terms_doubles,
-                        int64_t* stage_flag_words);
+                        int64_t* stage_flag_words, int64_t* act_floats);
 /* refresh the transposed copy of every 2-D weight (read by the backward) */
 int tpcb_transpose_params(const tpcb_model* m, const float* d_params, float* d_params_t,
                           void* stream);

@@ -60,7 +60,8 @@ class Samples(C.Structure):
 class TrainWs(C.Structure):
     _fields_ = [("partial", vp), ("slot_stride", i64), ("n_slots", i32), ("touched", vp),
                 ("zall", vp), ("terms", vp), ("scalars", vp), ("zall_floats", i64),
-                ("l_cap", i32), ("stage_flags", vp), ("stage_flag_words", i64)]
+                ("l_cap", i32), ("stage_flags", vp), ("stage_flag_words", i64),
+                ("act", vp), ("act_floats", i64)]
 
 
 class LargeBatch(C.Structure):
@@ -111,7 +112,8 @@ SIGNATURES = {
     "tpcb_cmd_grid_ws": (sz, [i64, i64, i32, i32]),
     "tpcb_cmd_grid": (i32, [vp, i32, i64, i64, i32, i32, vp, vp, vp, sz, vp]),
     "tpcb_train_ws_sizes": (i32, [vp, i32, i32, C.POINTER(i32), C.POINTER(i64),
-                                  C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
+                                  C.POINTER(i64), C.POINTER(i64), C.POINTER(i64),
+                                  C.POINTER(i64)]),
     "tpcb_transpose_params": (i32, [vp, vp, vp, vp]),
     "tpcb_loss_backward": (i32, [vp, vp, vp, C.POINTER(Samples), C.POINTER(Samples), vp, i32,
                                  i32, C.POINTER(LossCfg), C.POINTER(TrainWs), vp, vp, vp, vp,

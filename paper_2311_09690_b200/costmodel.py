@@ -424,10 +424,13 @@ def _loss_struct(loss: LossSpec):
 
 
 def backward(params: CostModelParams, batch: list, targets, loss: LossSpec,
-             target_batch: list | None = None):
+             target_batch: list | None = None, *, wgrad_tc: bool = False):
     """Loss value and d(objective)/d(every parameter) (costmodel.py:529-570),
     computed by the fused train-step kernels; with alpha_cmd > 0 and a target
-    batch the CMD term couples both forward passes."""
+    batch the CMD term couples both forward passes.  wgrad_tc=True
+    (desk shapes, no CMD): the encoder weight gradients as tcgen05 3xTF32
+    GEMMs over the batch's token rows (csrc/wgrad.cu) instead of the
+    per-sample slots"""
     targets = np.asarray(targets, dtype=np.float64)
     if not batch:
         raise EmptyBatch("forward needs at least one input")
@@ -450,7 +453,8 @@ def backward(params: CostModelParams, batch: list, targets, loss: LossSpec,
     src = engine.DeviceSamples(rag, cfg.n_leaf_max, st, y=targets)
     tgt = engine.DeviceSamples(trag, cfg.n_leaf_max, st) if use_cmd else None
     l_cap = max(int(rag.n_leaf.max()), int(trag.n_leaf.max()) if trag is not None else 1)
-    ws = engine.TrainWorkspace(dm, src.n + (tgt.n if tgt else 0), l_cap=l_cap, overlap=False)
+    ws = engine.TrainWorkspace(dm, src.n + (tgt.n if tgt else 0), l_cap=l_cap, overlap=False,
+                               wgrad_tc=wgrad_tc)
     grad, pred = engine.run_backward(dm, P, PT, src, tgt, _loss_struct(loss), ws, st)
     st.check("backward")
     sc = ws.scalars.cpu().numpy()

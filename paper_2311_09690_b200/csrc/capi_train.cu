@@ -70,6 +70,10 @@ TrainWs to_dev(const tpcb_train_ws* w) {
   // overlapped reduce: the caller's counters, when large enough for this model
   d.stage_flags = reinterpret_cast<unsigned long long*>(w->stage_flags);
   d.n_stage_words = (int)std::min<int64_t>(w->stage_flag_words, 1 << 30);
+  if (w->act && w->act_floats >= 32 * wg_total_rows()) {
+    d.wg.act = w->act;
+    d.wg.r_cap = (int)std::min<int64_t>(w->act_floats / wg_total_rows() / 32 * 32, 1 << 24);
+  }
   return d;
 }
 
@@ -148,6 +152,7 @@ int try_overlapped_step(const tpcb_model* m, float* P, float* PT, float* mb, flo
   *st_out = TPCB_OK;
   const Knobs& kn = knobs();
   if (!ws.stage_flags || loss.use_cmd || opt.kind == kOptNone || !t0 || kn.grid_cap > 0) return 0;
+  if (ws.wg.act) return 0;  // the tensor-core weight-gradient step runs sequentially
   if (ws.n_stage_words < ovl_stage_words(m->dev.n_layers)) return 0;
   if (!(kn.train_impl == 0 || kn.train_impl == 4) || !v4_fits(m->dev, ws.l_cap)) return 0;
   SideStream* ss = nullptr;
@@ -201,14 +206,22 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
   (void)PT;
   int st;
   const bool dp = comm != nullptr;  // (a 1-rank communicator exercises the same path)
+  // tensor-core encoder weight gradients: desk fast path, no CMD in the step
+  const Knobs& kn = knobs();
+  TrainWs ws_wg = ws_in;
+  const bool use_wg = ws_in.wg.act && !loss.use_cmd && kn.wgrad_tc &&
+                      (kn.train_impl == 0 || kn.train_impl == 4) && kn.grid_cap == 0 &&
+                      v4_fits(m->dev, ws_in.l_cap) && wgrad_tc_supported(m->dev) &&
+                      (int64_t)ws_in.n_slots * ws_in.l_cap <= ws_in.wg.r_cap;
+  if (!use_wg) ws_wg.wg = WgradDev{};
   if (!dp) {
     int ost = TPCB_OK;
     if (try_overlapped_step(m, P, PT, mb, vb, src, tgt, batch, steps, step, grid, loss, opt, lr,
-                            t0, ws_in, grad_out, step_loss, step_cmd, pred_out, status, stream,
+                            t0, ws_wg, grad_out, step_loss, step_cmd, pred_out, status, stream,
                             &ost))
       return ost;
   }
-  TrainWs ws = ws_in;  // sequential step: the training CTAs publish no stage counters
+  TrainWs ws = ws_wg;  // sequential step: the training CTAs publish no stage counters
   ws.stage_flags = nullptr;
   if (g_prof) g_prof->mark(stream);
   if (loss.use_cmd) {
@@ -227,15 +240,19 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
                     status, stream);
   if (st) return st;
   if (g_prof) g_prof->mark(stream);
+  const int wg_splits = use_wg ? wgrad_tc_splits(ws) : 0;
+  if (use_wg && (st = launch_wgrad_tc(m->dev, ws, steps, step, batch, src.n_leaf, wg_splits,
+                                      stream)))
+    return st;
   if (!dp) {
     st = launch_reduce_apply(m->dev, ws, steps, step, loss.use_cmd, 1, grad_out, P, mb, vb, opt,
-                             lr, t0, loss, step_loss, step_cmd, stream);
+                             lr, t0, loss, step_loss, step_cmd, stream, wg_splits);
     if (st) return st;
   } else {
     OptDev none{};
     st = launch_reduce_apply(m->dev, ws, steps, step, loss.use_cmd, comm->rank == 0, gbuf,
                              nullptr, nullptr, nullptr, none, nullptr, nullptr, loss, step_loss,
-                             step_cmd, stream);
+                             step_cmd, stream, wg_splits);
     if (st) return st;
     // gradient: rank-ordered sum (deterministic for a given world size,
     // independent of NCCL's algorithm choice); the step loss is a logged
@@ -256,9 +273,16 @@ int run_step(const tpcb_model* m, float* P, float* PT, float* mb, float* vb,
 
 extern "C" int tpcb_train_ws_sizes(const tpcb_model* m, int32_t max_rows, int32_t l_cap,
                                    int32_t* n_slots, int64_t* slot_stride, int64_t* zall_floats,
-                                   int64_t* terms_doubles, int64_t* stage_flag_words) {
+                                   int64_t* terms_doubles, int64_t* stage_flag_words,
+                                   int64_t* act_floats) {
   if (!m || max_rows < 1) return TPCB_ERR_VALIDATION;
   if (stage_flag_words) *stage_flag_words = ovl_stage_words(m->dev.n_layers);
+  if (act_floats)
+    *act_floats = wgrad_tc_supported(m->dev)
+                      ? (int64_t)wg_total_rows() *
+                            (((int64_t)std::min<int32_t>(max_rows, 1024) *
+                                  std::max<int32_t>(l_cap, 1) + 31) / 32 * 32)
+                      : 0;
   const int slots = std::min<int32_t>(max_rows, 1024);
   if (n_slots) *n_slots = slots;
   // 64-float (256 B) aligned slots

@@ -67,10 +67,12 @@ void set_last_error(const char* what, cudaError_t e);
 // another thread trains): TPCB_TRAIN_IMPL (0 automatic, 2 generic kernel,
 // 4 desk fast path), TPCB_GRID_CAP (cap on the training grid), TPCB_POLL_NS
 // (stage-wait poll interval of the overlapped reduce), TPCB_GEMM_BK (16 / 32
-// k-slab of the large-path GEMM), TPCB_GEMM_CLUSTER, TPCB_GEMM_MODE (probe).
+// k-slab of the large-path GEMM), TPCB_GEMM_CLUSTER, TPCB_GEMM_MODE (probe),
+// TPCB_WGRAD_TC (0: encoder weight gradients in the per-sample slots).
 struct Knobs {
   int train_impl, grid_cap, gemm_bk, gemm_cluster, gemm_mode;
   unsigned poll_ns;
+  int wgrad_tc;  // TPCB_WGRAD_TC (default 1): encoder weight gradients on tcgen05
 };
 const Knobs& knobs();
 

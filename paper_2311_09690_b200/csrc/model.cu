@@ -25,6 +25,7 @@ const Knobs& knobs() {
     r.gemm_cluster = env("TPCB_GEMM_CLUSTER", 0) ? 1 : 0;
     r.gemm_mode = env("TPCB_GEMM_MODE", 0);
     r.poll_ns = (unsigned)std::max(0, env("TPCB_POLL_NS", 256));
+    r.wgrad_tc = env("TPCB_WGRAD_TC", 1) ? 1 : 0;
     return r;
   }();
   return k;

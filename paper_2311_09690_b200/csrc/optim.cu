@@ -46,29 +46,6 @@ __device__ __forceinline__ int region_bit(const Model& M, int p, LeafLo t) {
   return L;
 }
 
-// SGD / Adam on parameter p with its preloaded w, m, v (nn.py:136-167, fp32,
-// same operation order as the oracle)
-__device__ __forceinline__ void apply1(int p, float g, float w, float m, float v,
-                                       float* __restrict__ grad_out, float* __restrict__ P,
-                                       float* __restrict__ mbuf, float* __restrict__ vbuf,
-                                       const OptDev& opt, float lr, float bc1, float bc2) {
-  if (grad_out) grad_out[p] = g;
-  if (opt.kind == kOptNone) return;
-  const float wd = (float)opt.weight_decay;
-  if (wd != 0.f) g = g + wd * w;
-  if (opt.kind == kOptSgd) {
-    P[p] = w - lr * g;
-    return;
-  }
-  const float b1 = (float)opt.beta1, b2 = (float)opt.beta2, eps = (float)opt.eps;
-  const float omb1 = (float)(1.0 - opt.beta1), omb2 = (float)(1.0 - opt.beta2);
-  m = __fadd_rn(__fmul_rn(m, b1), __fmul_rn(omb1, g));
-  v = __fadd_rn(__fmul_rn(v, b2), __fmul_rn(__fmul_rn(omb2, g), g));
-  mbuf[p] = m;
-  vbuf[p] = v;
-  P[p] = w - __fdiv_rn(__fmul_rn(lr, __fdiv_rn(m, bc1)), __fadd_rn(sqrtf(__fdiv_rn(v, bc2)), eps));
-}
-
 __global__ void __launch_bounds__(256) reduce_apply_kernel(
     const __grid_constant__ Model M, const float* __restrict__ partial, size_t stride,
     const uint32_t* __restrict__ touched,
@@ -77,7 +54,7 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(
     float* __restrict__ P, float* __restrict__ mbuf, float* __restrict__ vbuf, OptDev opt,
     const double* __restrict__ lr_p, const int64_t* __restrict__ t_p,
     const double* __restrict__ terms, const double* __restrict__ scalars, LossDev loss,
-    double* __restrict__ step_loss, double* __restrict__ step_cmd) {
+    double* __restrict__ step_loss, double* __restrict__ step_cmd, int skip_wgrad) {
   // A block owns 64 float4 columns (4 parameters each: tensors start on
   // 16-byte boundaries, so a column never straddles two tensors and has one
   // region bit).  Its four 64-thread quarters each sum a contiguous quarter of
@@ -158,12 +135,22 @@ __global__ void __launch_bounds__(256) reduce_apply_kernel(
     const int q = base + col;
     const bool qv = q < n4;
     const int p = q << 2;
-    const uint32_t want = qv ? 1u << region_bit(M, p, s_leaf_of(M)) : 0u;
+    // encoder weight matrices with the tensor-core weight gradients on: the
+    // gradient is the split-K partials in slots 0..skip_wgrad-1 (wgrad.cu),
+    // added in slot order by quarter 0; the other quarters add zeros
+    const bool wgr = qv && skip_wgrad && in_wgrad_region(M, p);
+    const bool mine = qv && !wgr;
+    const uint32_t want = mine ? 1u << region_bit(M, p, s_leaf_of(M)) : 0u;
     const int per_q = (G + 3) >> 2;
     const int c_lo = min(G, quarter * per_q), c_hi = min(G, c_lo + per_q);
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();  // s_touch / s_and / s_or (first iteration), s_part reuse (later ones)
-    if (qv && (s_or & want)) {
+    if (wgr && quarter == 0)
+      for (int c = 0; c < skip_wgrad; ++c) {
+        const float4 x = ldg4_last_use(reinterpret_cast<const float4*>(partial + p) + (size_t)c * st4);
+        g.x += x.x; g.y += x.y; g.z += x.z; g.w += x.w;
+      }
+    if (mine && (s_or & want)) {
       const float4* src = reinterpret_cast<const float4*>(partial + p) + (size_t)c_lo * st4;
       const int n = c_hi - c_lo;
       if (s_and & want) {  // every slot touched it: unpredicated, 8 loads in flight
@@ -549,12 +536,12 @@ int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps
                         int use_cmd, int add_cmd, float* grad_out, float* P, float* m, float* v,
                         const OptDev& opt, const double* lr, const int64_t* t,
                         const LossDev& loss, double* step_loss, double* step_cmd,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, int skip_wgrad) {
   const int grid = min(ceil_div(M.total / 4, 64), kNumSMs * 16);
   reduce_apply_kernel<<<grid, 256, 0, stream>>>(M, ws.partial, ws.slot_stride, ws.touched, steps,
                                                 step, ws.n_slots, use_cmd, add_cmd, grad_out, P, m,
                                                 v, opt, lr, t, ws.terms, ws.scalars, loss,
-                                                step_loss, step_cmd);
+                                                step_loss, step_cmd, skip_wgrad);
   TPCB_LAUNCH_CHECK("reduce_apply");
   return TPCB_OK;
 }

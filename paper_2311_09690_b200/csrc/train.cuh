@@ -93,6 +93,68 @@ __host__ __device__ inline void entry_shape(const Model& M, int L, int idx, int*
 
 
 
+// SGD / Adam on parameter p with its preloaded w, m, v (nn.py:136-167, fp32,
+// same operation order as the oracle); shared by the slot reduce (optim.cu)
+// and the tensor-core weight-gradient kernel (wgrad.cu)
+__device__ __forceinline__ void apply1(int p, float g, float w, float m, float v,
+                                       float* __restrict__ grad_out, float* __restrict__ P,
+                                       float* __restrict__ mbuf, float* __restrict__ vbuf,
+                                       const OptDev& opt, float lr, float bc1, float bc2) {
+  if (grad_out) grad_out[p] = g;
+  if (opt.kind == kOptNone) return;
+  const float wd = (float)opt.weight_decay;
+  if (wd != 0.f) g = g + wd * w;
+  if (opt.kind == kOptSgd) {
+    P[p] = w - lr * g;
+    return;
+  }
+  const float b1 = (float)opt.beta1, b2 = (float)opt.beta2, eps = (float)opt.eps;
+  const float omb1 = (float)(1.0 - opt.beta1), omb2 = (float)(1.0 - opt.beta2);
+  m = __fadd_rn(__fmul_rn(m, b1), __fmul_rn(omb1, g));
+  v = __fadd_rn(__fmul_rn(v, b2), __fmul_rn(__fmul_rn(omb2, g), g));
+  mbuf[p] = m;
+  vbuf[p] = v;
+  P[p] = w - __fdiv_rn(__fmul_rn(lr, __fdiv_rn(m, bc1)), __fadd_rn(sqrtf(__fdiv_rn(v, bc2)), eps));
+}
+
+// ---- encoder weight gradients on the tensor cores (wgrad.cu) --------------
+// The desk training kernel (train4) stores, for every encoder weight product
+// y = x·W of a step, the operand rows x and dy it would otherwise fold into
+// its per-sample gradient slot; wgrad_tc_kernel then forms dW = Xᵀ·dY over
+// all the step's token rows (3xTF32 tcgen05, fp32 accumulation in TMEM) and
+// applies the optimizer.  Operand k is a [features × rows] matrix stored as
+// 32-row chunks, each chunk a K-major 128-byte-swizzled UMMA tile
+// [op_rows[k] features][32 rows] (one bulk copy per chunk); step row
+// g = sample position · Ls + leaf row, Ls = the step's largest leaf count
+// (rows of shorter samples are zero).
+constexpr int kWgOpsLayer = 10;  // HIN dQ dK dV C dA H1 dF F dT1
+constexpr int kWgOps = 2 * kWgOpsLayer + 2;  // + X0, dH (input projection)
+enum { kWgHIN = 0, kWgDQ, kWgDK, kWgDV, kWgC, kWgDA, kWgH1, kWgDF, kWgF, kWgDT1 };
+constexpr int kWgX0 = 2 * kWgOpsLayer, kWgDH = kWgX0 + 1;
+__host__ __device__ constexpr int wg_op_rows(int op) {
+  return op == kWgX0 ? 32 : ((op % kWgOpsLayer == kWgDF || op % kWgOpsLayer == kWgF) && op < kWgX0 ? 128 : 64);
+}
+__host__ __device__ constexpr int wg_total_rows() {
+  int s = 0;
+  for (int k = 0; k < kWgOps; ++k) s += wg_op_rows(k);
+  return s;
+}
+// element (feature f, step row g) of operand op in a buffer of r_cap rows
+__host__ __device__ inline size_t wg_index(int op_off_rows, int op_rows, int r_cap, int f, int g) {
+  const int c = g >> 5, j = g & 31;
+  return (size_t)op_off_rows * r_cap + (size_t)c * op_rows * 32 + (f >> 3) * 256 + (f & 7) * 32 +
+         ((((j >> 2) ^ (f & 7))) << 2) + (j & 3);
+}
+__host__ __device__ constexpr int wg_op_off(int op) {
+  int s = 0;
+  for (int k = 0; k < op; ++k) s += wg_op_rows(k);
+  return s;
+}
+struct WgradDev {
+  float* act = nullptr;  // nullptr: weight gradients in the per-sample slots (v4 path)
+  int r_cap = 0;         // rows per operand (multiple of 32)
+};
+
 // one dataset on the device (packed rows from K1 + per-sample data)
 struct SampleSetDev {
   const float* x;          // packed rows [*, 32]
@@ -127,6 +189,7 @@ struct TrainWs {
   const int64_t* t_tag = nullptr;  // tag of step s = t_tag[0] + s + 1
   int flag_stride = 0;
   int n_stage_words = 0;  // words of the caller's stage_flags (0: overlap off)
+  WgradDev wg;            // tensor-core encoder weight gradients (train4 only)
 };
 
 // Overlapped gradient reduction + optimizer (single GPU, no CMD): the items
@@ -173,7 +236,28 @@ int launch_reduce_apply(const Model& M, const TrainWs& ws, const StepDesc* steps
                         int use_cmd, int add_cmd, float* grad_out, float* P, float* m, float* v,
                         const OptDev& opt, const double* lr, const int64_t* t,
                         const LossDev& loss, double* step_loss, double* step_cmd,
-                        cudaStream_t stream);
+                        cudaStream_t stream, int skip_wgrad = 0);
+// dW of the encoder weight matrices from the operands train4 stored
+// (ws.wg), split-K over `splits` blocks per matrix → gradient slots
+// 0..splits-1's region of those tensors (the slot reduce adds them in order)
+bool wgrad_tc_supported(const Model& M);
+int wgrad_tc_splits(const TrainWs& ws);
+int launch_wgrad_tc(const Model& M, const TrainWs& ws, const StepDesc* steps, int step,
+                    const int32_t* batch, const int32_t* n_leaf, int splits,
+                    cudaStream_t stream);
+// parameter p belongs to an encoder weight matrix (its gradient comes from wgrad_tc)
+__host__ __device__ inline bool in_wgrad_region(const Model& M, int p) {
+  if (p >= M.inW && p < M.inW + TPCB_FEAT * M.d) return true;
+  for (int li = 0; li < M.n_layers; ++li) {
+    const LayerOff& lo = M.layer[li];
+    const int dd = M.d * M.d;
+    if ((p >= lo.Wq && p < lo.Wq + dd) || (p >= lo.Wk && p < lo.Wk + dd) ||
+        (p >= lo.Wv && p < lo.Wv + dd) || (p >= lo.Wo && p < lo.Wo + dd) ||
+        (p >= lo.fhW && p < lo.fhW + M.d * M.d_ff) || (p >= lo.foW && p < lo.foW + M.d_ff * M.d))
+      return true;
+  }
+  return false;
+}
 // optimizer step from a reduced gradient with lr / step count in device memory
 int launch_opt_from_grad(const Model& M, const float* grad, float* P, float* m, float* v,
                          const OptDev& opt, const double* lr, const int64_t* t, int step,

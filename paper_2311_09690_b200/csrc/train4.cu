@@ -279,6 +279,25 @@ __device__ __forceinline__ void outer(const float* u, int K, const float* v, int
   }
 }
 
+// operand rows of an encoder weight product → the tensor-core weight-gradient
+// buffer (train.cuh WgradDev): step rows w·Ls + r, r < L the rows of X (or
+// g⊙X + b), L ≤ r < Ls zeros; `K` features (the operand's padded width)
+__device__ __noinline__ void act_store(const WgradDev& wg, int op, const float* X, int ldx,
+                                       const float* ga, const float* ba, int L, int Ls, int K,
+                                       int w) {
+  const int rows = wg_op_rows(op), off = wg_op_off(op);
+  const int n = Ls * K;
+  for (int e = threadIdx.x; e < n; e += NT) {
+    const int f = e / Ls, r = e - f * Ls;
+    float v = 0.f;
+    if (r < L) {
+      v = X[r * ldx + f];
+      if (ga) v = fmaf(ga[f], v, ba[f]);
+    }
+    wg.act[wg_index(off, rows, wg.r_cap, f, w * Ls + r)] = v;
+  }
+}
+
 // out[n] = act(bias[n] + Σ_k in[k]·W[k][n]) (W swizzled, K rows), 4 threads per output
 __device__ __forceinline__ void gemv_f(const float* in, int K, const float* W, int N,
                                        const float* bias, bool relu, float* out) {
@@ -822,7 +841,7 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
     float* __restrict__ zall, float* __restrict__ partial, size_t slot_stride,
     uint32_t* __restrict__ touched, double* __restrict__ terms, double* __restrict__ scalars,
     float* __restrict__ pred_out, int32_t* status, unsigned long long* __restrict__ stage_flags,
-    const int64_t* __restrict__ t_tag, int flag_stride) {
+    const int64_t* __restrict__ t_tag, int flag_stride, WgradDev wg) {
   extern __shared__ __align__(1024) float sm[];
   __shared__ __align__(8) uint64_t bars[20 + kStages4];
   const int NS = tp.NS;
@@ -923,6 +942,19 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
   // ========================================================== compute warps
   const float scale = 1.f / sqrtf((float)DHEAD);
   float* G = partial + (size_t)blockIdx.x * slot_stride;
+  // tensor-core weight gradients (phase 1 without CMD): the step's row
+  // stride Ls = its largest leaf count (single-bucket plans: every sample's)
+  const bool use_wg = wg.act != nullptr && phase == 1 && !loss.use_cmd;
+  __shared__ int s_Ls;
+  if (use_wg && warp == 0) {
+    int m = 0;
+    for (int i = lane; i < n_src; i += 32) m = max(m, src.n_leaf[batch[i]]);
+#pragma unroll
+    for (int d = 16; d; d >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
+    if (lane == 0) s_Ls = m;
+  }
+  cbar();
+  const int Ls = use_wg ? s_Ls : 0;
   uint32_t mask = 0;
   int xs = 0;  // samples processed (input-row buffer parity)
   const float outb = __ldg(Pw + M.outb);
@@ -1264,7 +1296,12 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
         op_dffn(L, dT1, W0, W1, F, dF);
         PT(60 + (NLAY - 1 - li) * 30 + 1);
         ws.release(2);
-        wgrad(F, LDF, nullptr, nullptr, dT1, LDH, L, FF, D, G + lo.foW, fs);
+        if (use_wg) {
+          act_store(wg, li * kWgOpsLayer + kWgF, F, LDF, nullptr, nullptr, L, Ls, FF, w);
+          act_store(wg, li * kWgOpsLayer + kWgDT1, dT1, LDH, nullptr, nullptr, L, Ls, D, w);
+        } else {
+          wgrad(F, LDF, nullptr, nullptr, dT1, LDH, L, FF, D, G + lo.foW, fs);
+        }
         PT(60 + (NLAY - 1 - li) * 30 + 2);
         colsum(dT1, LDH, nullptr, 0, L, D, G + lo.fob, fs, 0);
         colsum(dH, LDH, XH2, LDH, L, D, G + lo.ln2g, fs, 64);
@@ -1280,7 +1317,13 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
         op_bwd_ln<2>(L, dF, LDF, D, W0, W1, nullptr, dT1, dT2, sv + SV_LN1G, XH1, I1, dA);
         PT(60 + (NLAY - 1 - li) * 30 + 6);
         ws.release(2);
-        wgrad(XH1, LDH, sv + SV_LN1G, sv + SV_LN1B, dF, LDF, L, D, FF, G + lo.fhW, fs);
+        if (use_wg) {
+          act_store(wg, li * kWgOpsLayer + kWgH1, XH1, LDH, sv + SV_LN1G, sv + SV_LN1B, L, Ls, D,
+                    w);
+          act_store(wg, li * kWgOpsLayer + kWgDF, dF, LDF, nullptr, nullptr, L, Ls, FF, w);
+        } else {
+          wgrad(XH1, LDH, sv + SV_LN1G, sv + SV_LN1B, dF, LDF, L, D, FF, G + lo.fhW, fs);
+        }
         PT(60 + (NLAY - 1 - li) * 30 + 7);
         colsum(dF, LDF, nullptr, 0, L, FF, G + lo.fhb, fs, 0);
         PT(60 + (NLAY - 1 - li) * 30 + 8);
@@ -1294,7 +1337,12 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
         op_bwd_plain(L, dA, W, dC);
         PT(60 + (NLAY - 1 - li) * 30 + 11);
         ws.release();
-        wgrad(C, LDH, nullptr, nullptr, dA, LDH, L, D, D, G + lo.Wo, fs);
+        if (use_wg) {
+          act_store(wg, li * kWgOpsLayer + kWgC, C, LDH, nullptr, nullptr, L, Ls, D, w);
+          act_store(wg, li * kWgOpsLayer + kWgDA, dA, LDH, nullptr, nullptr, L, Ls, D, w);
+        } else {
+          wgrad(C, LDH, nullptr, nullptr, dA, LDH, L, D, D, G + lo.Wo, fs);
+        }
         PT(60 + (NLAY - 1 - li) * 30 + 12);
         colsum(dA, LDH, nullptr, 0, L, D, G + lo.bo, fs, 0);
         colsum(dT2, LDH, XH1, LDH, L, D, G + lo.ln1g, fs, 64);
@@ -1326,9 +1374,17 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
         }
         PT(60 + (NLAY - 1 - li) * 30 + 20);
         ws.release(3);
-        wgrad(HIN, LDH, nullptr, nullptr, dQKV, LDQ, L, D, D, G + lo.Wq, fs);
-        wgrad(HIN, LDH, nullptr, nullptr, dQKV + D, LDQ, L, D, D, G + lo.Wk, fs);
-        wgrad(HIN, LDH, nullptr, nullptr, dQKV + 2 * D, LDQ, L, D, D, G + lo.Wv, fs);
+        if (use_wg) {
+          act_store(wg, li * kWgOpsLayer + kWgHIN, HIN, LDH, nullptr, nullptr, L, Ls, D, w);
+          act_store(wg, li * kWgOpsLayer + kWgDQ, dQKV, LDQ, nullptr, nullptr, L, Ls, D, w);
+          act_store(wg, li * kWgOpsLayer + kWgDK, dQKV + D, LDQ, nullptr, nullptr, L, Ls, D, w);
+          act_store(wg, li * kWgOpsLayer + kWgDV, dQKV + 2 * D, LDQ, nullptr, nullptr, L, Ls, D,
+                    w);
+        } else {
+          wgrad(HIN, LDH, nullptr, nullptr, dQKV, LDQ, L, D, D, G + lo.Wq, fs);
+          wgrad(HIN, LDH, nullptr, nullptr, dQKV + D, LDQ, L, D, D, G + lo.Wk, fs);
+          wgrad(HIN, LDH, nullptr, nullptr, dQKV + 2 * D, LDQ, L, D, D, G + lo.Wv, fs);
+        }
         PT(60 + (NLAY - 1 - li) * 30 + 21);
         colsum(dQKV, LDQ, nullptr, 0, L, D, G + lo.bq, fs, 0);
         colsum(dQKV + D, LDQ, nullptr, 0, L, D, G + lo.bk, fs, 64);
@@ -1339,7 +1395,12 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
       stage_done(2 + 2 * (NLAY - 1 - li));  // layer li: attention + LayerNorm-1
       PT(60 + (NLAY - 1 - li) * 30 + 23);
     }
-    wgrad(X0, LDX, nullptr, nullptr, dH, LDH, L, FEAT, D, G + M.inW, fs);
+    if (use_wg) {
+      act_store(wg, kWgX0, X0, LDX, nullptr, nullptr, L, Ls, LDX, w);
+      act_store(wg, kWgDH, dH, LDH, nullptr, nullptr, L, Ls, D, w);
+    } else {
+      wgrad(X0, LDX, nullptr, nullptr, dH, LDH, L, FEAT, D, G + M.inW, fs);
+    }
     colsum(dH, LDH, nullptr, 0, L, D, G + M.inb, fs, NT - D);
     PT(125);
     mask |= 1u | (1u << L);
@@ -1474,7 +1535,7 @@ int launch_train4(const Model& M, const float* P, const SampleSetDev& src, const
                                                    tp, maps, ws.zall, ws.partial, ws.slot_stride,
                                                    ws.touched, ws.terms, ws.scalars, pred_out,
                                                    status, ws.stage_flags, ws.t_tag,
-                                                   ws.flag_stride);
+                                                   ws.flag_stride, ws.wg);
   TPCB_LAUNCH_CHECK("train4_kernel");
   return TPCB_OK;
 }

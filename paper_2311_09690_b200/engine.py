@@ -373,13 +373,14 @@ class TrainWorkspace:
     z_rows: rows of the global [zs; zt] CMD matrix (≥ max_rows)."""
 
     def __init__(self, dm: DeviceModel, max_rows: int, device="cuda", z_rows: int = 0,
-                 l_cap: int = 0, overlap: bool = True):
+                 l_cap: int = 0, overlap: bool = True, wgrad_tc: bool = False):
         lib = _lib.load()
         ns, stride, zf, tf, sw = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        af = C.c_int64()
         self.l_cap = int(l_cap) if l_cap else dm.cfg.n_leaf_max
         _lib.check(lib.tpcb_train_ws_sizes(dm.handle, max_rows, self.l_cap, C.byref(ns),
                                            C.byref(stride), C.byref(zf), C.byref(tf),
-                                           C.byref(sw)),
+                                           C.byref(sw), C.byref(af)),
                    "train_ws_sizes")
         zf = C.c_int64(max(zf.value, z_rows * dm.cfg.d_embed))
         self.max_rows = max_rows
@@ -402,6 +403,13 @@ class TrainWorkspace:
                             if overlap else None)
         w.stage_flags = self.stage_flags.data_ptr() if overlap else None
         w.stage_flag_words = sw.value if overlap else 0
+        # operand rows of the tensor-core weight-gradient GEMMs (desk shapes;
+        # opt-in: measured slower than the fused per-sample gradients at bs 64,
+        # DESIGN.md §5b)
+        self.act = (torch.empty(af.value, dtype=torch.float32, device=device)
+                    if wgrad_tc and af.value > 0 else None)
+        w.act = self.act.data_ptr() if self.act is not None else None
+        w.act_floats = self.act.numel() if self.act is not None else 0
         self.struct = w
 
 

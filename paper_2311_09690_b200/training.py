@@ -123,7 +123,7 @@ class Trainer:
                  valid_latency: np.ndarray | None = None, normalizer=None,
                  target_rag: engine.RaggedHost | None = None, device="cuda",
                  use_graph: bool = True, comm: "engine.Comm | None" = None,
-                 overlap: bool = True, dp_mode: str = "weak"):
+                 overlap: bool = True, dp_mode: str = "weak", wgrad_tc: bool = False):
         from .costmodel import device_model
         self.config = config
         self.dm = device_model(config)
@@ -160,7 +160,8 @@ class Trainer:
         if target_rag is not None:
             l_cap = max(l_cap, int(np.max(target_rag.n_leaf)))
         self.ws = engine.TrainWorkspace(self.dm, rows, device, z_rows=rows * self.world,
-                                        l_cap=l_cap, overlap=overlap and comm is None)
+                                        l_cap=l_cap, overlap=overlap and comm is None,
+                                        wgrad_tc=wgrad_tc)
         self.grad = torch.zeros_like(self.P) if comm is not None else None
         self.n_train = train_rag.n_ast
         self.n_leaf = np.asarray(train_rag.n_leaf)

@@ -62,9 +62,12 @@ def test_backward_small_configs_vs_reference(golden_model, name, case):
     _assert_grads(grads, gm, case)
 
 
-@pytest.mark.parametrize("case", ["hyb", "orig", "cmd"])
-def test_backward_desk_trained_batch(golden_model, case):
-    """A reference batch: 64 samples of one bucket (+64 shifted targets)."""
+@pytest.mark.parametrize("case,wgrad_tc", [("hyb", False), ("orig", False), ("cmd", False),
+                                           ("hyb", True), ("orig", True)])
+def test_backward_desk_trained_batch(golden_model, case, wgrad_tc):
+    """A reference batch: 64 samples of one bucket (+64 shifted targets);
+    wgrad_tc: the encoder weight gradients as tcgen05 GEMMs over the batch's
+    256 token rows (csrc/wgrad.cu), same tolerance."""
     pb = _pb()
     from paper_2311_09690_b200.costmodel import LossSpec, backward
     gm = golden_model("desk")
@@ -84,7 +87,7 @@ def test_backward_desk_trained_batch(golden_model, case):
                              normalizer=norm),
             "cmd": LossSpec(mode="hybrid", lambda_hybrid=1e-3, offset=loff, alpha_cmd=1.0)}[case]
     val, grads, aux = backward(params, batch, gm.z["batch_y"], spec,
-                               target_batch=tb if case == "cmd" else None)
+                               target_batch=tb if case == "cmd" else None, wgrad_tc=wgrad_tc)
     assert val == pytest.approx(float(gm.z[f"bw.{case}.loss"]), rel=1e-5)
     _assert_grads(grads, gm, case)
 

@@ -110,7 +110,8 @@ def test_steps_track_oracle_short_horizon():
     assert rel.max() <= 1e-3, rel
 
 
-def test_single_step_matches_oracle():
+@pytest.mark.parametrize("wgrad_tc", [False, True])
+def test_single_step_matches_oracle(wgrad_tc):
     """One Adam step from identical parameters on a reference batch: every
     updated parameter within 2e-5 absolute of the float64 step, except the
     parameters whose exact gradient is 0 (attention key biases: Adam turns
@@ -123,7 +124,8 @@ def test_single_step_matches_oracle():
     data, norm, y, dv, rag, loss = _oracle_setup()
     cfg = pb.desk_config(seed=0)
     params = pb.init_params(cfg)
-    tr = Trainer(cfg, params.tensors, rag, y, loss, use_graph=False)
+    tr = Trainer(cfg, params.tensors, rag, y, loss, use_graph=False, wgrad_tc=wgrad_tc)
+    assert (tr.ws.act is not None) == wgrad_tc
     flat, steps = tr.plan(np.random.default_rng(0))
     tr.run_epoch(1e-3, flat, steps[:1].copy())
     got = tr.tensors()
