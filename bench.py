@@ -496,8 +496,8 @@ def run_large_batch(cfg, train, targets, norm, dv, dev, flush_l2, batch: int = 6
 
 def _ncu_traffic(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
-    the committed ncu --set full capture (profiles/r01/ncu_traffic.json)."""
-    p = ROOT / "profiles" / "r01" / "ncu_traffic.json"
+    the committed ncu --set full capture (profiles/r02/ncu_traffic.json)."""
+    p = ROOT / "profiles" / "r02" / "ncu_traffic.json"
     try:
         return int(json.loads(p.read_text())[kernel]["dram_bytes_per_launch"])
     except Exception:
