@@ -28,9 +28,9 @@ __global__ void __launch_bounds__(1024) cmd_kernel(const T* __restrict__ Z, int 
 }
 
 // ---- grid version for large sets (cmd_between over whole datasets) --------
-// HBM-bound: pass A (extrema + per-set sums), pass C (central power sums),
-// pass E (gradient) each stream Z once with coalesced row reads (lane =
-// column); the two combine kernels run on one block.  Each block owns a
+// HBM-bound: pass AC (extrema + shifted power sums) and pass E (gradient)
+// each stream Z once with coalesced row reads (lane = column); the combine
+// runs one block per column.  Each block owns a
 // chunk of kChunk rows of ONE set, chunked from that set's own first row, and
 // partials are combined in block order — so the reduction order is fixed
 // (bitwise reproducible) and identical for identical sets: cmd(S, S) is
@@ -50,46 +50,6 @@ struct GridPlan {
   }
 };
 
-// pass A: per block and column: min/argmin, max/argmax, sum
-template <typename T>
-__global__ void __launch_bounds__(kGridThreads) cmd_pass_a(const T* __restrict__ Z, GridPlan g,
-                                                           double* __restrict__ part) {
-  __shared__ double s_mn[8][kMaxGridDe], s_mx[8][kMaxGridDe], s_sum[8][kMaxGridDe];
-  __shared__ int s_imn[8][kMaxGridDe], s_imx[8][kMaxGridDe];
-  int r0, r1;
-  bool is_s;
-  g.chunk(blockIdx.x, r0, r1, is_s);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int c = lane; c < g.de; c += 32) {
-    double mn = INFINITY, mx = -INFINITY, sum = 0.0;
-    int imn = 0x7fffffff, imx = 0x7fffffff;
-#pragma unroll 8
-    for (int r = r0 + w; r < r1; r += 8) {
-      const double v = (double)Z[(size_t)r * g.de + c];
-      argmin_merge(mn, imn, v, r);
-      argmax_merge(mx, imx, v, r);
-      sum += v;
-    }
-    s_mn[w][c] = mn; s_imn[w][c] = imn;
-    s_mx[w][c] = mx; s_imx[w][c] = imx;
-    s_sum[w][c] = sum;
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < g.de; c += kGridThreads) {
-    double mn = s_mn[0][c], mx = s_mx[0][c], sum = s_sum[0][c];
-    int imn = s_imn[0][c], imx = s_imx[0][c];
-    for (int q = 1; q < 8; ++q) {
-      argmin_merge(mn, imn, s_mn[q][c], s_imn[q][c]);
-      argmax_merge(mx, imx, s_mx[q][c], s_imx[q][c]);
-      sum += s_sum[q][c];
-    }
-    double* o = part + (size_t)blockIdx.x * 5 * g.de;
-    o[c] = mn; o[g.de + c] = (double)imn;
-    o[2 * g.de + c] = mx; o[3 * g.de + c] = (double)imx;
-    o[4 * g.de + c] = sum;
-  }
-}
-
 // Fixed-shape block reduction of one set's chunk partials: thread q takes
 // the chunks q, q+256, ... of THAT set in order, then warp xor-trees and the
 // 8 warp totals in warp order — deterministic, and the same shape for two
@@ -108,20 +68,108 @@ __device__ __forceinline__ double block_set_sum(const double* part, int first, i
   return t;
 }
 
-// combine A: one block per column — extrema over all chunks, per-set means
-__global__ void __launch_bounds__(kGridThreads) cmd_combine_a(GridPlan g,
-                                                              const double* __restrict__ part,
-                                                              double* __restrict__ cs) {
+// pass AC (one streaming read of Z): per block and column, min/argmin,
+// max/argmax and the power sums S_j = Σ (z − c0)^j, j = 1..K, around the
+// shift c0 = the column's value in the set's first row (the central sums
+// follow in the combine by the binomial expansion around the mean; with c0
+// one sample of the set, |c0 − μ| is a few standard deviations and the
+// expansion loses < 1e-13 relative on these moments).  Partial layout per
+// block: [mn | imn | mx | imx | S_1 .. S_K] × de.
+template <typename T>
+__global__ void __launch_bounds__(kGridThreads) cmd_pass_ac(const T* __restrict__ Z, GridPlan g,
+                                                            double* __restrict__ part) {
+  __shared__ double s_mn[8][32], s_mx[8][32];
+  __shared__ int s_imn[8][32], s_imx[8][32];
+  __shared__ double s_p[8][kMaxCmdOrder][32];
+  int r0, r1;
+  bool is_s;
+  g.chunk(blockIdx.x, r0, r1, is_s);
+  const int row_first = is_s ? 0 : g.ns;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < g.de; c0 += 32) {
+    const int c = c0 + lane;
+    double mn = INFINITY, mx = -INFINITY;
+    int imn = 0x7fffffff, imx = 0x7fffffff;
+    double ps[kMaxCmdOrder];
+#pragma unroll
+    for (int j = 0; j < kMaxCmdOrder; ++j) ps[j] = 0.0;
+    if (c < g.de) {
+      const double sh = (double)Z[(size_t)row_first * g.de + c];
+      int r = r0 + w;
+      for (; r + 56 < r1; r += 64) {  // 8 rows in flight per thread
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = (double)Z[(size_t)(r + 8 * u) * g.de + c];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          argmin_merge(mn, imn, v[u], r + 8 * u);
+          argmax_merge(mx, imx, v[u], r + 8 * u);
+          const double cen = v[u] - sh;
+          double pw = cen;
+#pragma unroll
+          for (int j = 0; j < kMaxCmdOrder; ++j)
+            if (j < g.K) { ps[j] += pw; pw *= cen; }
+        }
+      }
+      for (; r < r1; r += 8) {
+        const double v = (double)Z[(size_t)r * g.de + c];
+        argmin_merge(mn, imn, v, r);
+        argmax_merge(mx, imx, v, r);
+        const double cen = v - sh;
+        double pw = cen;
+#pragma unroll
+        for (int j = 0; j < kMaxCmdOrder; ++j)
+          if (j < g.K) { ps[j] += pw; pw *= cen; }
+      }
+    }
+    s_mn[w][lane] = mn; s_imn[w][lane] = imn;
+    s_mx[w][lane] = mx; s_imx[w][lane] = imx;
+#pragma unroll
+    for (int j = 0; j < kMaxCmdOrder; ++j) s_p[w][j][lane] = ps[j];
+    __syncthreads();
+    for (int e = threadIdx.x; e < (4 + g.K) * 32; e += kGridThreads) {
+      const int q = e >> 5, l = e & 31, cc = c0 + l;
+      if (cc >= g.de) continue;
+      double* o = part + ((size_t)blockIdx.x * (4 + g.K) + q) * g.de + cc;
+      if (q == 0 || q == 1) {
+        double m = s_mn[0][l];
+        int im = s_imn[0][l];
+        for (int k = 1; k < 8; ++k) argmin_merge(m, im, s_mn[k][l], s_imn[k][l]);
+        *o = q == 0 ? m : (double)im;
+      } else if (q == 2 || q == 3) {
+        double m = s_mx[0][l];
+        int im = s_imx[0][l];
+        for (int k = 1; k < 8; ++k) argmax_merge(m, im, s_mx[k][l], s_imx[k][l]);
+        *o = q == 2 ? m : (double)im;
+      } else {
+        const int j = q - 4;
+        double a = s_p[0][j][l];
+        for (int k = 1; k < 8; ++k) a += s_p[k][j][l];
+        *o = a;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// combine AC: one block per column — extrema over all chunks; per set the
+// power sums S_j in fixed chunk order, the mean μ = c0 + S_1/n and the
+// central moments m_j = (1/n) Σ_i C(j,i) S_i (c0 − μ)^(j−i) (S_0 = n)
+template <typename T>
+__global__ void __launch_bounds__(kGridThreads) cmd_combine_ac(const T* __restrict__ Z, GridPlan g,
+                                                               const double* __restrict__ part,
+                                                               double* __restrict__ cs) {
   __shared__ double red[kGridThreads / 32], rmn[kGridThreads / 32], rmx[kGridThreads / 32];
   __shared__ int rimn[kGridThreads / 32], rimx[kGridThreads / 32];
+  __shared__ double S[2][kMaxCmdOrder + 1];
   const int de = g.de, c = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int nb = g.bs + g.bt;
+  const int nb = g.bs + g.bt, KM = kMaxCmdOrder + 1;
   double mn = INFINITY, mx = -INFINITY;
   int imn = 0x7fffffff, imx = 0x7fffffff;
+  auto fld = [&](int f, int b) { return part[((size_t)b * (4 + g.K) + f) * de + c]; };
   for (int b = threadIdx.x; b < nb; b += kGridThreads) {
-    const double* o = part + (size_t)b * 5 * de;
-    argmin_merge(mn, imn, o[c], (int)o[de + c]);
-    argmax_merge(mx, imx, o[2 * de + c], (int)o[3 * de + c]);
+    argmin_merge(mn, imn, fld(0, b), (int)fld(1, b));
+    argmax_merge(mx, imx, fld(2, b), (int)fld(3, b));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -133,8 +181,37 @@ __global__ void __launch_bounds__(kGridThreads) cmd_combine_a(GridPlan g,
     argmax_merge(mx, imx, v3, i3);
   }
   if (lane == 0) { rmn[w] = mn; rimn[w] = imn; rmx[w] = mx; rimx[w] = imx; }
-  const double ss = block_set_sum(part + 4 * de + c, 0, g.bs, (size_t)5 * de, red);
-  const double st = block_set_sum(part + 4 * de + c, g.bs, g.bt, (size_t)5 * de, red);
+  {  // every S_j of both sets in one pass over the partials: thread q takes
+     // the chunks q, q+256, … of each set in order, then warp xor-trees and the
+     // 8 warp totals in warp order (fixed shape, identical for identical sets)
+    __shared__ double rs[kGridThreads / 32][2][kMaxCmdOrder];
+    double a[2][kMaxCmdOrder];
+#pragma unroll
+    for (int j = 0; j < kMaxCmdOrder; ++j) a[0][j] = a[1][j] = 0.0;
+    for (int set = 0; set < 2; ++set) {
+      const int first = set == 0 ? 0 : g.bs, count = set == 0 ? g.bs : g.bt;
+      for (int q = threadIdx.x; q < count; q += kGridThreads) {
+#pragma unroll
+        for (int j = 0; j < kMaxCmdOrder; ++j)
+          if (j < g.K) a[set][j] += fld(4 + j, first + q);
+      }
+    }
+#pragma unroll
+    for (int set = 0; set < 2; ++set)
+#pragma unroll
+      for (int j = 0; j < kMaxCmdOrder; ++j) {
+        const double v = warp_sum_d(a[set][j]);
+        if (lane == 0) rs[w][set][j] = v;
+      }
+    __syncthreads();
+    if (threadIdx.x < 2 * kMaxCmdOrder) {
+      const int set = threadIdx.x / kMaxCmdOrder, j = threadIdx.x % kMaxCmdOrder;
+      double t = 0.0;
+      for (int q = 0; q < kGridThreads / 32; ++q) t += rs[q][set][j];
+      if (j < g.K) S[set][j + 1] = t;
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     for (int q = 1; q < kGridThreads / 32; ++q) {
       argmin_merge(mn, imn, rmn[q], rimn[q]);
@@ -142,71 +219,29 @@ __global__ void __launch_bounds__(kGridThreads) cmd_combine_a(GridPlan g,
     }
     cs[c] = mn;
     cs[de + c] = mx;
-    cs[2 * de + c] = ss / g.ns;
-    cs[3 * de + c] = st / g.nt;
     const double raw = mx - mn;
     cs[4 * de + c] = raw < kCmdSupportFloor ? -kCmdSupportFloor : raw;
     cs[7 * de + c] = (double)imn;
     cs[8 * de + c] = (double)imx;
-  }
-}
-
-// pass C: central power sums sum (z - mu)^j, j = 1..K, per block and column
-template <typename T>
-__global__ void __launch_bounds__(kGridThreads) cmd_pass_c(const T* __restrict__ Z, GridPlan g,
-                                                           const double* __restrict__ cs,
-                                                           double* __restrict__ part) {
-  __shared__ double s_p[8][kMaxCmdOrder][32];
-  int r0, r1;
-  bool is_s;
-  g.chunk(blockIdx.x, r0, r1, is_s);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const double* mu = cs + (is_s ? 2 : 3) * g.de;
-  for (int c0 = 0; c0 < g.de; c0 += 32) {
-    const int c = c0 + lane;
-    double ps[kMaxCmdOrder];
-#pragma unroll
-    for (int j = 0; j < kMaxCmdOrder; ++j) ps[j] = 0.0;
-    if (c < g.de) {
-      const double m = mu[c];
-#pragma unroll 8
-      for (int r = r0 + w; r < r1; r += 8) {
-        const double cen = (double)Z[(size_t)r * g.de + c] - m;
-        double pw = cen;
-#pragma unroll
-        for (int j = 0; j < kMaxCmdOrder; ++j) {
-          if (j < g.K) { ps[j] += pw; pw *= cen; }
+    for (int set = 0; set < 2; ++set) {
+      const double n = set == 0 ? (double)g.ns : (double)g.nt;
+      const double sh = (double)Z[(size_t)(set == 0 ? 0 : g.ns) * de + c];
+      const double mu = sh + S[set][1] / n;
+      const double d = sh - mu;
+      cs[(2 + set) * de + c] = mu;
+      double* mom = cs + 9 * de + set * KM * de;
+      S[set][0] = n;
+      for (int j = 1; j <= g.K; ++j) {
+        // Σ_i C(j,i) S_i d^(j-i), highest power of d first
+        double acc = 0.0, binom = 1.0, dp = 1.0;
+        for (int i = j; i >= 0; --i) {
+          acc += binom * S[set][i] * dp;
+          dp *= d;
+          binom = binom * (double)i / (double)(j - i + 1);
         }
+        mom[j * de + c] = acc / n;
       }
     }
-#pragma unroll
-    for (int j = 0; j < kMaxCmdOrder; ++j) s_p[w][j][lane] = ps[j];
-    __syncthreads();
-    for (int e = threadIdx.x; e < g.K * 32; e += kGridThreads) {
-      const int j = e >> 5, l = e & 31;
-      if (c0 + l < g.de) {
-        double a = s_p[0][j][l];
-        for (int q = 1; q < 8; ++q) a += s_p[q][j][l];
-        part[((size_t)blockIdx.x * g.K + j) * g.de + c0 + l] = a;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// combine C: one block per (order j, column c) — per-set central moments
-__global__ void __launch_bounds__(kGridThreads) cmd_combine_c(GridPlan g,
-                                                              const double* __restrict__ part,
-                                                              double* __restrict__ cs) {
-  __shared__ double red[kGridThreads / 32];
-  const int de = g.de, KM = kMaxCmdOrder + 1;
-  const int j = blockIdx.x / de, c = blockIdx.x - j * de;
-  const size_t stride = (size_t)g.K * de;
-  const double a = block_set_sum(part + (size_t)j * de + c, 0, g.bs, stride, red);
-  const double b = block_set_sum(part + (size_t)j * de + c, g.bs, g.bt, stride, red);
-  if (threadIdx.x == 0) {
-    cs[9 * de + (j + 1) * de + c] = a / g.ns;
-    cs[9 * de + KM * de + (j + 1) * de + c] = b / g.nt;
   }
 }
 
@@ -268,7 +303,7 @@ __global__ void __launch_bounds__(kGridThreads) cmd_pass_e(const T* __restrict__
   const int total = (g.ns + g.nt) * de;  // < 2^31 (checked at launch)
   const bool de32 = de == 32;
   const int stride = gridDim.x * blockDim.x;
-  constexpr int U = 4;  // elements in flight per thread
+  constexpr int U = 8;  // elements in flight per thread
   for (int e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += U * stride) {
     double z[U];
 #pragma unroll
@@ -304,10 +339,8 @@ int launch_cmd_grid(const T* Z, const GridPlan& g, double* value, double* grad, 
   double* cs = ws;
   double* part = ws + n_cs;
   const size_t smem = n_cs * sizeof(double);
-  cmd_pass_a<T><<<blocks, kGridThreads, 0, st>>>(Z, g, part);
-  cmd_combine_a<<<g.de, kGridThreads, 0, st>>>(g, part, cs);
-  cmd_pass_c<T><<<blocks, kGridThreads, 0, st>>>(Z, g, cs, part);
-  cmd_combine_c<<<g.K * g.de, kGridThreads, 0, st>>>(g, part, cs);
+  cmd_pass_ac<T><<<blocks, kGridThreads, 0, st>>>(Z, g, part);
+  cmd_combine_ac<T><<<g.de, kGridThreads, 0, st>>>(Z, g, part, cs);
   TPCB_CUDA_CHECK(cudaFuncSetAttribute(cmd_finish_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cmd_finish_kernel<<<1, 256, smem, st>>>(g, cs, value);
@@ -329,7 +362,7 @@ using namespace tpcb;
 extern "C" size_t tpcb_cmd_grid_ws(int64_t ns, int64_t nt, int32_t de, int32_t k) {
   if (ns < 1 || nt < 1 || de < 1 || k < 1) return 0;
   const int64_t blocks = (ns + kChunk - 1) / kChunk + (nt + kChunk - 1) / kChunk;
-  const int64_t per = std::max<int64_t>(5, k);
+  const int64_t per = 4 + k;
   return (size_t)(cmd_scratch_doubles(de) + blocks * per * de) * sizeof(double);
 }
 
