@@ -30,7 +30,7 @@ from .dataset import BoxCoxNormalizer, fit_boxcox
 from .errors import (CheckpointError, DimensionMismatch, DomainError, EmptyBatch,
                      EmptyDataset, EmptySet, NonFiniteLoss, UnsupportedConfig, ValidationError)
 from .features import (N_ENTRY, CompactAst, CompactBatch, DeviceSpec, EncodedInput,
-                       check_leaf_counts, encode_input, ragged_from_encoded)
+                       check_leaf_counts, device_vector, encode_input, ragged_from_encoded)
 
 DEVICE_FEATURES = 6
 
@@ -240,11 +240,82 @@ class Predictor:
         self.status.check("forward")
         return out
 
+    # ASTs per pipelined chunk of forward_batch (host↔device copies of chunk
+    # i+1 overlap the featurize + forward of chunk i)
+    CHUNK = 1 << 18
+
     def forward_batch(self, batch: CompactBatch, normalizer=None, latents=False):
-        """Bulk path: raw compact ASTs in, (pred, z_x, z_v, z, latency) out."""
-        pred, zx, zv, z, lat = self.forward_ragged(batch.ragged(), normalizer, latents)
-        cpu = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
-        return cpu(pred), cpu(zx), cpu(zv), cpu(z), cpu(lat)
+        """Bulk path: raw compact ASTs in, (pred, z_x, z_v, z, latency) out.
+
+        Large batches run as a pipeline of CHUNK-AST pieces on two streams:
+        the H2D copy of a piece's rows / orderings / leaf counts / device
+        indices overlaps the previous piece's K1 + forward, leaf offsets and
+        device features are formed on the device, results come back with
+        async D2H copies into pinned buffers.  Per-AST results do not depend
+        on the batching (every kernel is per AST / per token row), so the
+        output equals the one-shot path bit for bit.  Host arrays in pinned
+        memory (e.g. views of `torch.Tensor.pin_memory()`) get the overlap;
+        pageable arrays still work, with the copies serialised."""
+        n = batch.n_ast
+        if n == 0:
+            raise EmptyBatch("forward needs at least one input")
+        if self.large is not None or n <= self.CHUNK:
+            pred, zx, zv, z, lat = self.forward_ragged(batch.ragged(), normalizer, latents)
+            cpu = lambda t: None if t is None else t.cpu().numpy()  # noqa: E731
+            return cpu(pred), cpu(zx), cpu(zv), cpu(z), cpu(lat)
+        return self._forward_pipelined(batch, normalizer, latents)
+
+    def _forward_pipelined(self, batch: CompactBatch, normalizer, latents):
+        n = batch.n_ast
+        n_leaf = np.ascontiguousarray(batch.n_leaf, dtype=np.int64)
+        check_leaf_counts(n_leaf, self.config.n_leaf_max)
+        dev = self.params.device
+        tok_off = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(n_leaf, out=tok_off[1:])
+        table = torch.from_numpy(np.stack([device_vector(d) for d in batch.devices])
+                                 .astype(np.float32)).to(dev)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
+        rows_h, ord_h = t(batch.vectors), t(np.asarray(batch.ordering, dtype=np.int32))
+        nl_h, di_h = t(n_leaf), t(np.asarray(batch.device_index, dtype=np.int32))
+        out_pred = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        out_lat = (torch.empty(n, dtype=torch.float64, pin_memory=True)
+                   if normalizer is not None else None)
+        de, ddev = self.config.d_embed, self.config.d_device
+        outs_lat = [torch.empty((n, w), dtype=torch.float32, pin_memory=True)
+                    for w in (de, ddev, de)] if latents else None
+        compute = torch.cuda.current_stream(dev)
+        copy = torch.cuda.Stream(device=dev)
+        chunks = [(a, min(n, a + self.CHUNK)) for a in range(0, n, self.CHUNK)]
+        keep = []
+        for a, b in chunks:
+            ta, tb = int(tok_off[a]), int(tok_off[b])
+            with torch.cuda.stream(copy):  # H2D of this chunk (async from pinned memory)
+                rows = rows_h[ta:tb].to(dev, non_blocking=True)
+                ordering = ord_h[ta:tb].to(dev, non_blocking=True)
+                nl = nl_h[a:b].to(dev, non_blocking=True)
+                di = di_h[a:b].to(dev, non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(copy)
+            compute.wait_event(ready)
+            for x in (rows, ordering, nl, di):
+                x.record_stream(compute)
+            leaf_off = torch.zeros(b - a + 1, dtype=torch.int64, device=dev)
+            torch.cumsum(nl, 0, out=leaf_off[1:])
+            devfeat = table.index_select(0, di.long())
+            pred, zx, zv, z, lat = self.forward_device(rows, ordering, leaf_off, devfeat, b - a,
+                                                       False, normalizer, latents)
+            out_pred[a:b].copy_(pred, non_blocking=True)
+            if out_lat is not None:
+                out_lat[a:b].copy_(lat, non_blocking=True)
+            if latents:
+                for o, v in zip(outs_lat, (zx, zv, z)):
+                    o[a:b].copy_(v, non_blocking=True)
+            keep.append((pred, zx, zv, z, lat))  # alive until the D2H copies ran
+        compute.synchronize()
+        self.status.check("forward")
+        res = (out_pred.numpy(),) + (tuple(o.numpy() for o in outs_lat) if latents
+                                     else (None, None, None))
+        return res + (out_lat.numpy() if out_lat is not None else None,)
 
 
 def forward(params: CostModelParams, inputs: list) -> tuple:

@@ -233,3 +233,30 @@ def test_forward_desk_default_tiles_use_the_desk_kernel():
     assert pb.Predictor(pb.init_params(pb.desk_config(seed=0))).R == 128
     small = pb.desk_config(seed=0, d_model=32, d_ff=64, d_embed=16)
     assert pb.Predictor(pb.init_params(small)).R == 64
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_forward_batch_pipelined_equals_one_shot(precision):
+    """The chunked two-stream bulk path (H2D of chunk i+1 overlapping the
+    forward of chunk i, device-side leaf offsets / device features) returns
+    the one-shot results bit for bit: every kernel is per AST / token row."""
+    import paper_2311_09690_b200 as pb
+    from paper_2311_09690_b200 import synth
+    from paper_2311_09690_b200.dataset import fit_boxcox
+    import torch
+    data = synth.generate(20000, seed=9)
+    norm = fit_boxcox(data.latency)
+    devs = [pb.DeviceSpec("a", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0),
+            pb.DeviceSpec("b", 1590.0, 16.0, 320.0, 40, 8100.0, 4.0)]
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
+    batch = pb.CompactBatch(pin(data.vectors.astype(np.float32)),
+                            pin(data.ordering.astype(np.int32)), pin(data.n_leaf),
+                            pin((np.arange(data.n) % 2).astype(np.int32)), devs)
+    params = pb.init_params(pb.desk_config(seed=4))
+    p = pb.Predictor(params, precision=precision)
+    one = p.forward_batch(batch, None, latents=True)  # n <= CHUNK: one shot
+    p.CHUNK = 3000  # several pipelined chunks (instance attribute shadows the class default)
+    many = p.forward_batch(batch, None, latents=True)
+    for a, b in zip(one[:4], many[:4]):
+        assert np.array_equal(a, b)
+    assert one[4] is None and many[4] is None
