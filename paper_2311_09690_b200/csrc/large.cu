@@ -246,57 +246,71 @@ __global__ void __launch_bounds__(192, 1)
         mma_commit(&empty[s]);
     }
     mma_commit(&done);
-  } else if (warp < 4) {  // epilogue: thread = TMEM lane = output row
+  } else if (warp < 4) {  // epilogue
+    // pass 1 (thread = TMEM lane = tile row): accumulators + bias → a padded
+    // [128][36] shared-memory tile per 32-column chunk (the TMA ring is dead
+    // once `done` fired); pass 2: 8 lanes per row, float4 per lane — residual,
+    // ReLU / mask and the output stores as 128-byte row segments (coalesced),
+    // instead of one 16-byte store per thread per row.  Same arithmetic.
     mbar_wait(&done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int row = m0 + 32 * warp + lane;
-    const bool live = row < e.M;
+    float* stile = reinterpret_cast<float*>(smem);
+    constexpr int kLd = 36;  // floats per staged row (16-byte aligned, spreads banks)
+    const int r_loc = 32 * warp + lane;
+    const int sub = lane & 7, rq = lane >> 3;  // pass 2: column quad, row in the group
     for (int ch = 0; ch < NT / 32; ++ch) {
       const int c0 = n0 + 32 * ch;
       if (c0 >= e.ldc) break;  // warp-uniform
       float v[32], w[32];
       tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32 * ch, v);
       tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + NT + 32 * ch, w);
-      if (!live) continue;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += w[j];
+      for (int q = 0; q < 8; ++q) {
+        float4 x;
+        float* xs = &x.x;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = c0 + j;
-        float x = v[j];
-        if (col < e.N) {
-          if (e.bias) x += __ldg(e.bias + col);
-          if (e.r_hi) {
-            const size_t ri = (size_t)row * e.ldr + col;
-            x += e.r_hi[ri] + (e.r_lo ? e.r_lo[ri] : 0.f);
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * q + u;
+          float t = v[j] + w[j];
+          if (e.bias && c0 + j < e.N) t += __ldg(e.bias + c0 + j);
+          xs[u] = t;
+        }
+        *reinterpret_cast<float4*>(stile + r_loc * kLd + 4 * q) = x;
+      }
+      group_bar(1, 128);
+      const int col = c0 + 4 * sub;
+      for (int rr = 4 * warp + rq; rr < kTileM; rr += 16) {
+        const int row = m0 + rr;
+        if (row >= e.M) break;
+        float4 x = *reinterpret_cast<const float4*>(stile + rr * kLd + 4 * sub);
+        float* xs = &x.x;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cc = col + u;
+          float t = xs[u];
+          if (cc < e.N) {
+            if (e.r_hi) {
+              const size_t ri = (size_t)row * e.ldr + cc;
+              t += e.r_hi[ri] + (e.r_lo ? e.r_lo[ri] : 0.f);
+            }
+            if (e.relu) t = fmaxf(t, 0.f);
+            if (e.mask && !(e.mask[(size_t)row * e.ldm + cc] > 0.f)) t = 0.f;
+          } else {
+            t = 0.f;
           }
-          if (e.relu) x = fmaxf(x, 0.f);
-          if (e.mask && !(e.mask[(size_t)row * e.ldm + col] > 0.f)) x = 0.f;
+          xs[u] = t;
+        }
+        if (e.c) {
+          *reinterpret_cast<float4*>(e.c + blockIdx.z * e.split_stride + (size_t)row * e.ldc + col) = x;
         } else {
-          x = 0.f;
-        }
-        v[j] = x;
-      }
-      if (e.c) {
-        float4* dst = reinterpret_cast<float4*>(e.c + blockIdx.z * e.split_stride +
-                                                (size_t)row * e.ldc + c0);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      } else {
-        float4* dh = reinterpret_cast<float4*>(e.c_hi + (size_t)row * e.ldc + c0);
-        float4* dl = reinterpret_cast<float4*>(e.c_lo + (size_t)row * e.ldc + c0);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float h[4], l[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            h[u] = tf32_hi(v[4 * q + u]);
-            l[u] = v[4 * q + u] - h[u];
-          }
-          dh[q] = make_float4(h[0], h[1], h[2], h[3]);
-          dl[q] = make_float4(l[0], l[1], l[2], l[3]);
+          float4 h, l;
+          h.x = tf32_hi(x.x); h.y = tf32_hi(x.y); h.z = tf32_hi(x.z); h.w = tf32_hi(x.w);
+          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+          *reinterpret_cast<float4*>(e.c_hi + (size_t)row * e.ldc + col) = h;
+          *reinterpret_cast<float4*>(e.c_lo + (size_t)row * e.ldc + col) = l;
         }
       }
+      group_bar(1, 128);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
