@@ -1212,11 +1212,24 @@ __global__ void colsum_partial_kernel(const float* __restrict__ x, const float* 
   const int c = blockIdx.x * 32 + threadIdx.x;
   const int r0 = blockIdx.y * kColChunk, r1 = min(r0 + kColChunk, rows);
   float acc = 0.f;
-  if (c < cols)
-    for (int r = r0 + threadIdx.y; r < r1; r += 8) {
-      acc += x[(size_t)r * ld + c];
-      if (x_lo) acc += x_lo[(size_t)r * ld + c];
+  if (c < cols) {  // the chunk's rows for this thread: loads first, adds in row order
+    constexpr int kPer = kColChunk / 8;
+    float xv[kPer], xl[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int r = r0 + threadIdx.y + 8 * u;
+      xv[u] = r < r1 ? x[(size_t)r * ld + c] : 0.f;
+      xl[u] = (r < r1 && x_lo) ? x_lo[(size_t)r * ld + c] : 0.f;
     }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int r = r0 + threadIdx.y + 8 * u;
+      if (r < r1) {
+        acc += xv[u];
+        if (x_lo) acc += xl[u];
+      }
+    }
+  }
   red[threadIdx.y][threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.y == 0 && c < cols) {
@@ -1231,7 +1244,15 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, 
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   float s = part[c];
-  for (int k = 1; k < chunks; ++k) s += part[(size_t)k * cols + c];
+  int k = 1;
+  for (; k + 8 <= chunks; k += 8) {  // 8 loads in flight, added in chunk order
+    float x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = part[(size_t)(k + u) * cols + c];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += x[u];
+  }
+  for (; k < chunks; ++k) s += part[(size_t)k * cols + c];
   const int t = c / dst.colw;
   float* g = grad + dst.d[t] + (c - t * dst.colw);
   *g = dst.acc ? *g + s : s;
