@@ -84,7 +84,10 @@ constexpr int kLeafRegion = kSmVec - kSmA;             // 51,200
 __device__ __forceinline__ int leaf_chunk_a(int L) {   // bytes per A chunk: ⌈⌊128/L⌋/8⌉ atoms
   return L == 1 ? TR * 128 : (((TR / L) + 7) >> 3) * 1024;
 }
-constexpr int kSmTotal = kSmVec + kVecFloats * 4;
+// per-AST sample index and device features of the current tile, fetched by
+// cp.async at the tile start (off the head's critical path)
+constexpr int kSmAst = kSmVec + kVecFloats * 4;
+constexpr int kSmTotal = kSmAst + TR * 4 + TR * TPCB_DEV_FEAT * 4;
 
 __host__ __device__ inline uint32_t sw128(int r, int k) {  // bf16 element (row r, col k < 64)
   return (r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) ^ (r & 7))) << 4) + (k & 7) * 2;
@@ -140,6 +143,43 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// 16 consecutive fp32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// 8 bf16 values → columns c0..c0+7 of row r of a SW128 A tile
+__device__ __forceinline__ void store8_bf16(uint8_t* tile, int r, int c0, const float* v) {
+  __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]);
+  __nv_bfloat162 p1 = __floats2bfloat162_rn(v[2], v[3]);
+  __nv_bfloat162 p2 = __floats2bfloat162_rn(v[4], v[5]);
+  __nv_bfloat162 p3 = __floats2bfloat162_rn(v[6], v[7]);
+  uint4 u;
+  u.x = *reinterpret_cast<uint32_t*>(&p0);
+  u.y = *reinterpret_cast<uint32_t*>(&p1);
+  u.z = *reinterpret_cast<uint32_t*>(&p2);
+  u.w = *reinterpret_cast<uint32_t*>(&p3);
+  *reinterpret_cast<uint4*>(tile + sw128(r, c0)) = u;
 }
 
 // this thread's 64 bf16 values → row r of a SW128 A tile
@@ -382,12 +422,16 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     const int L = tile_L[tile], first = tile_first[tile], A = tile_count[tile];
     const int rows = A * L;
     const bool live = r < rows;
+    int32_t* s_idx = reinterpret_cast<int32_t*>(smb + kSmAst);
+    float* s_dv = reinterpret_cast<float*>(smb + kSmAst + TR * 4);
+
     float h[DH];  // this row's residual stream, columns 32·wg .. 32·wg+31 (fp32)
     if (wg == 1) {  // prefetched input rows → A operand (24 features, zero-padded to 64)
       float v[D];
 #pragma unroll
       for (int i = 0; i < D; ++i) v[i] = (live && i < TPCB_FEAT) ? xn[i < TPCB_FEAT ? i : 0] : 0.f;
       store_row_bf16(sA, r, v);
+      if (r < A) cp_async4(s_idx + r, perm + first + r);  // lands under the input projection
     }
     sync_for_mma();
     TT(1);
@@ -398,6 +442,12 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     }
     wait_mma(&bars[1], phase);
     TT(2);
+    if (wg == 1 && r < A) {  // the AST's device features, by its (now landed) index
+      cp_async_wait_all();
+      const float* dvp = devfeat + (size_t)s_idx[r] * TPCB_DEV_FEAT;
+#pragma unroll
+      for (int f = 0; f < TPCB_DEV_FEAT; ++f) cp_async4(s_dv + r * TPCB_DEV_FEAT + f, dvp + f);
+    }
     {
       tmem_ld32(tlane + DH * wg, h);
 #pragma unroll
@@ -564,6 +614,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       }
     }
     TT(30);
+    if (wg == 1) cp_async_wait_all();  // device features (visible after the barrier below)
     // ---------------------------------------------------------------- head
     // leaf_embed on the tensor cores (costmodel.py:213-216): A chunk l holds row
     // a = token a·L + l (written by the last LayerNorm epilogue), B chunk l is
@@ -604,17 +655,14 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     }
     wait_mma(&bars[1], phase);
     TT(25);
-    if (wg == 0) {  // z_x, device MLP and gate for AST t (t < A) → decoder operand row t
-      float zx[DE];
-      tmem_ld32(tlane, zx);  // warp-collective: every lane loads, rows ≥ A are ignored
-      if (t < A) {
-        const int idx = perm[first + t];
-        float zv[DDEV], z[D];
-#pragma unroll
-        for (int n = 0; n < DE; ++n) zx[n] += hv[kVHLeafB + L * DE + n];
-        float dv[TPCB_DEV_FEAT];
-#pragma unroll
-        for (int f = 0; f < TPCB_DEV_FEAT; ++f) dv[f] = __ldg(devfeat + (size_t)idx * TPCB_DEV_FEAT + f);
+    {  // z_x, device MLP and gate for AST a = r (a < A), columns 16·wg .. 16·wg+15
+       // per warpgroup → decoder operand row a (costmodel.py:213-220)
+      float zx[16];
+      tmem_ld16(tlane + 16 * wg, zx);  // warp-collective: every lane loads
+      if (r < A) {
+        const int a = r, idx = s_idx[a];
+        const float* dv = s_dv + a * TPCB_DEV_FEAT;
+        float zv[DDEV];
 #pragma unroll
         for (int n = 0; n < DDEV; ++n) {
           float sacc = hv[kVHDevHB + n];
@@ -622,21 +670,26 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
           for (int f = 0; f < TPCB_DEV_FEAT; ++f) sacc = fmaf(dv[f], hv[kVHDevHW + f * DDEV + n], sacc);
           zv[n] = fmaxf(sacc, 0.f);
         }
+        float z[16];
 #pragma unroll
-        for (int n = 0; n < DE; ++n) {
+        for (int q = 0; q < 16; ++q) {
+          const int n = 16 * wg + q;
+          zx[q] += hv[kVHLeafB + L * DE + n];
           float sacc = hv[kVHDevPB + n];
 #pragma unroll
           for (int k = 0; k < DDEV; ++k) sacc = fmaf(zv[k], hv[kVHDevPW + k * DE + n], sacc);
-          z[n] = zx[n] * sacc;
+          z[q] = zx[q] * sacc;
         }
-#pragma unroll
-        for (int n = DE; n < D; ++n) z[n] = 0.f;
-        store_row_bf16(sA, t, z);
+        const float zero[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        store8_bf16(sA, a, 16 * wg, z);
+        store8_bf16(sA, a, 16 * wg + 8, z + 8);
+        store8_bf16(sA, a, 32 + 16 * wg, zero);
+        store8_bf16(sA, a, 40 + 16 * wg, zero);
         if (zx_out)
-          for (int n = 0; n < DE; ++n) zx_out[(size_t)idx * DE + n] = zx[n];
+          for (int q = 0; q < 16; ++q) zx_out[(size_t)idx * DE + 16 * wg + q] = zx[q];
         if (z_out)
-          for (int n = 0; n < DE; ++n) z_out[(size_t)idx * DE + n] = z[n];
-        if (zv_out)
+          for (int q = 0; q < 16; ++q) z_out[(size_t)idx * DE + 16 * wg + q] = z[q];
+        if (zv_out && wg == 0)
           for (int n = 0; n < DDEV; ++n) zv_out[(size_t)idx * DDEV + n] = zv[n];
       }
     }
@@ -675,7 +728,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
 #pragma unroll
         for (int j = 0; j < DEC; ++j)
           pred = fmaf(fmaxf(u[j] + hv[kVHDecB1 + j], 0.f), hv[kVHOutW + j], pred);
-        const int idx = perm[first + t];
+        const int idx = s_idx[t];
         pred_out[idx] = pred;
         if (lat_out) {
           bool bad = false;
