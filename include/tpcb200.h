@@ -403,6 +403,13 @@ int tpcb_kmeanspp_init(const double* d_x, int64_t n, int32_t d, int64_t first, d
 int tpcb_kmeanspp_step(const double* d_x, int64_t n, int32_t d, int32_t i, double u,
                        int64_t direct, double* d_centers, double* d_closest, double* d_total,
                        int64_t* d_chosen, void* ws, size_t ws_bytes, void* stream);
+/* steps i0 .. i1-1 with host pre-drawn uniforms h_u[i1-i0] (the reference's
+ * rng.random() per step while the total is > 0), no host synchronisation;
+ * *d_zero_step (caller-initialised to INT32_MAX) = the first step whose total
+ * was 0 (the reference then draws rng.integers: replay from there). */
+int tpcb_kmeanspp_steps(const double* d_x, int64_t n, int32_t d, int32_t i0, int32_t i1,
+                        const double* h_u, double* d_centers, double* d_closest, double* d_total,
+                        int32_t* d_zero_step, void* ws, size_t ws_bytes, void* stream);
 /* Lloyd assignment: first-index argmin of sqrt distance, own distance, counts */
 int tpcb_kmeans_assign(const double* d_x, int64_t n, int32_t d, const double* d_centers,
                        int32_t kappa, int64_t* d_assign, double* d_own, int32_t* d_counts,

@@ -135,6 +135,7 @@ SIGNATURES = {
     "tpcb_kmeans_ws_size": (i32, [i64, i32, i32, C.POINTER(sz)]),
     "tpcb_kmeanspp_init": (i32, [vp, i64, i32, i64, vp, vp, vp, vp, sz, vp]),
     "tpcb_kmeanspp_step": (i32, [vp, i64, i32, i32, f64, i64, vp, vp, vp, vp, vp, sz, vp]),
+    "tpcb_kmeanspp_steps": (i32, [vp, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]),
     "tpcb_kmeans_assign": (i32, [vp, i64, i32, vp, i32, vp, vp, vp, vp]),
     "tpcb_kmeans_assign_tc_ws": (C.c_size_t, [i32]),
     "tpcb_kmeans_assign_tc": (i32, [vp, i64, i32, vp, i32, vp, vp, vp, vp, C.c_size_t, vp]),

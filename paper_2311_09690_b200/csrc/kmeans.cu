@@ -187,7 +187,17 @@ __device__ void warp_first_true(int64_t n, Pred pred, unsigned long long* found)
 // cdf.searchsorted(u, side="right")); the CDF is non-decreasing, so the
 // predicate is monotone
 __global__ void search_kernel(const double* __restrict__ cdf, int64_t n, double u,
-                              unsigned long long* __restrict__ found) {
+                              unsigned long long* __restrict__ found,
+                              const double* __restrict__ total = nullptr,
+                              int32_t* __restrict__ zero_step = nullptr, int step = 0) {
+  // speculative multi-step launch (tpcb_kmeanspp_steps): a step whose total
+  // is 0 takes the reference's other RNG branch (rng.integers) — record the
+  // first such step; the host replays from it
+  if (zero_step && !(*total > 0.0)) {
+    if (threadIdx.x == 0) atomicMin(zero_step, step);
+    if (threadIdx.x == 0) *found = 0;
+    return;
+  }
   const double last = cdf[n - 1];
   warp_first_true(n, [&](int64_t j) { return cdf[j] / last > u; }, found);
 }
@@ -509,6 +519,39 @@ extern "C" int tpcb_kmeanspp_step(const double* d_x, int64_t n, int32_t d, int32
   closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(d_x, n, d, center, d_closest, 0, w.part);
   sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
   TPCB_LAUNCH_CHECK("kmeanspp_step");
+  return TPCB_OK;
+}
+
+// steps i0 .. i1-1 of k-means++ with the uniforms pre-drawn on the host
+// (h_u[i - i0]: the reference draws rng.random() once per step while the
+// running total is > 0), enqueued back to back without host synchronisation;
+// *d_zero_step (initialised by the caller to INT32_MAX) receives the first
+// step whose total was 0 — there the reference draws rng.integers instead, so
+// the caller replays from that step with tpcb_kmeanspp_step.
+extern "C" int tpcb_kmeanspp_steps(const double* d_x, int64_t n, int32_t d, int32_t i0,
+                                   int32_t i1, const double* h_u, double* d_centers,
+                                   double* d_closest, double* d_total, int32_t* d_zero_step,
+                                   void* ws, size_t ws_bytes, void* stream_) {
+  if (!d_x || !d_centers || !d_closest || !d_total || !ws || !h_u || !d_zero_step)
+    return TPCB_ERR_VALIDATION;
+  if (d > kMaxDim) return TPCB_ERR_UNSUPPORTED;
+  if (i0 < 1 || i1 < i0) return TPCB_ERR_VALIDATION;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KWs w = carve(ws, ws_bytes, n, 1);
+  const int g = closest_grid(n);
+  TPCB_CUDA_CHECK(prep_closest(d));
+  for (int i = i0; i < i1; ++i) {
+    double* center = d_centers + (size_t)i * d;
+    size_t tb = w.tmp_bytes;
+    TPCB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(w.tmp, tb, p_iter(d_closest, d_total), w.cdf,
+                                                  (int)n, stream));
+    search_kernel<<<1, 32, 0, stream>>>(w.cdf, n, h_u[i - i0], w.found, d_total, d_zero_step, i);
+    set_center_kernel<<<1, 128, 0, stream>>>(d_x, d, w.found, n, center, nullptr);
+    closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(d_x, n, d, center, d_closest,
+                                                                     0, w.part);
+    sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
+  }
+  TPCB_LAUNCH_CHECK("kmeanspp_steps");
   return TPCB_OK;
 }
 

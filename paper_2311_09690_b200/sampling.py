@@ -109,7 +109,42 @@ class DeviceKMeans:
                                                self.centers.data_ptr(), self.closest.data_ptr(),
                                                self.total.data_ptr(), self.ws.ptr, self.ws.size,
                                                self.s()), "kmeanspp_init")
-        for i in range(1, self.kappa):
+        if self.kappa < 2:
+            return
+        # the common case — the running total stays > 0, so every step draws
+        # rng.random() — runs with the uniforms pre-drawn and no per-step host
+        # synchronisation; a step that saw total == 0 (the reference then
+        # draws rng.integers) is replayed exactly from there
+        saved = rng.bit_generator.state
+        us = np.ascontiguousarray(rng.random(self.kappa - 1))
+        zero = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=self.dev)
+        _lib.check(self.lib.tpcb_kmeanspp_steps(self.x.data_ptr(), self.n, self.d, 1, self.kappa,
+                                                us.ctypes.data_as(C.c_void_p),
+                                                self.centers.data_ptr(), self.closest.data_ptr(),
+                                                self.total.data_ptr(), zero.data_ptr(),
+                                                self.ws.ptr, self.ws.size, self.s()),
+                   "kmeanspp_steps")
+        z = int(zero.item())
+        if z >= self.kappa:
+            return
+        rng.bit_generator.state = saved
+        rng.random(z - 1)  # the draws of steps 1 .. z-1, as consumed above
+        # rebuild the state after step z-1 (the speculative steps ≥ z
+        # overwrote closest / total) by re-running steps 1 .. z-1, then step
+        # by step with the reference's branch per step
+        _lib.check(self.lib.tpcb_kmeanspp_init(self.x.data_ptr(), self.n, self.d, first,
+                                               self.centers.data_ptr(), self.closest.data_ptr(),
+                                               self.total.data_ptr(), self.ws.ptr, self.ws.size,
+                                               self.s()), "kmeanspp_init")
+        if z > 1:
+            _lib.check(self.lib.tpcb_kmeanspp_steps(self.x.data_ptr(), self.n, self.d, 1, z,
+                                                    us.ctypes.data_as(C.c_void_p),
+                                                    self.centers.data_ptr(),
+                                                    self.closest.data_ptr(),
+                                                    self.total.data_ptr(), zero.data_ptr(),
+                                                    self.ws.ptr, self.ws.size, self.s()),
+                       "kmeanspp_steps")
+        for i in range(z, self.kappa):
             total = float(self.total.item())
             if total == 0.0:
                 u, direct = -1.0, int(rng.integers(0, self.n))

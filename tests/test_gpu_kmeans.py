@@ -161,3 +161,24 @@ def test_tensor_core_kmeans_at_scale():
             sel_tc = s.select_tasks(x, k, tasks, seed=5, assign="tc")
             assert len(sel_ex) == len(sel_tc) == k
             assert len(set(sel_ex)) == len(set(sel_tc)) == k
+
+
+def test_kmeanspp_zero_total_replay():
+    """k-means++ on data with fewer distinct points than kappa: once every
+    point coincides with a centre the running total is 0 and the reference
+    draws rng.integers instead of rng.random (sampling.py:53-58).  The device
+    path pre-draws the uniforms, detects the zero-total step and replays from
+    it — same centres and the same RNG state afterwards as the float64
+    restatement (itself pinned to the reference)."""
+    s = _s()
+    rng0 = np.random.default_rng(4)
+    base = rng0.normal(size=(3, 5))
+    x = base[rng0.integers(0, 3, size=200)]  # 3 distinct points
+    for kappa in (3, 5, 8):
+        want_rng = np.random.default_rng(21)
+        want = lloyd.kmeanspp(x, kappa, want_rng)
+        got_rng = np.random.default_rng(21)
+        km = s.DeviceKMeans(x, kappa)
+        km.kmeanspp(got_rng)
+        np.testing.assert_array_equal(km.centers.cpu().numpy(), want)
+        assert got_rng.random() == want_rng.random()  # identical stream position
