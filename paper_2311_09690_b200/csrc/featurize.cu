@@ -232,6 +232,15 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
     PeDenom den, const double* __restrict__ pe_table, const int32_t* __restrict__ row_tok,
     float* __restrict__ x, int32_t* __restrict__ row_ast) {
   __shared__ __align__(16) float stage[kPackThreads * kStagePitch];
+  // the first kPeSmem rows of the PE table (positions < 64: every synthetic
+  // ordering) in shared memory — the L1 path served them from L2 (ncu: L2
+  // sectors ~2x the DRAM traffic)
+  constexpr int kPeSmem = 64;
+  __shared__ __align__(16) double pe_s[PE ? kPeSmem * TPCB_FEAT : 2];
+  if (PE) {
+    for (int i = threadIdx.x; i < kPeSmem * TPCB_FEAT; i += kPackThreads) pe_s[i] = pe_table[i];
+    __syncthreads();
+  }
   constexpr int kChunks = TPCB_FEAT_PAD / 4;  // 8 float4 per packed row
   const int rshift = R == 32 ? 5 : (R == 64 ? 6 : 7);
   const int64_t rows = (int64_t)(*n_tiles) << rshift;
@@ -272,7 +281,16 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
             }
           }
           if (PE) {  // column 2δ: sin(pos/θ^(2δ/24)); 2δ+1: cos (features.py:255-262)
-            if (table) {  // table row (L1/L2 resident)
+            if (ipos >= 0 && ipos < kPeSmem) {  // shared-memory rows
+              const double2* tp =
+                  reinterpret_cast<const double2*>(pe_s + ipos * TPCB_FEAT + h * 12);
+#pragma unroll
+              for (int q = 0; q < 6; ++q) {
+                const double2 p = tp[q];
+                v[2 * q] += p.x;
+                v[2 * q + 1] += p.y;
+              }
+            } else if (table) {  // table row (L1/L2 resident)
               const double2* tp =
                   reinterpret_cast<const double2*>(pe_table + ipos * TPCB_FEAT + h * 12);
 #pragma unroll
