@@ -665,7 +665,12 @@ int launch_gemm_bk(const Operand& A, const Operand& B, const Epi& e, cudaStream_
 template <int NT>
 int launch_gemm_nt(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st,
                    int splits = 1, int* splits_used = nullptr) {
-  if (knobs().gemm_bk == 16) return launch_gemm_bk<NT, 16>(A, B, e, st, splits, splits_used);
+  // k-slab width: 16 columns (64-byte swizzle, 6-stage ring) for tall
+  // products (inference batches: +3 %), 32 (128-byte swizzle, 3 stages) for
+  // the M ~ 600·L training products (full_reference_config step −6 %);
+  // TPCB_GEMM_BK forces one
+  const int bk = knobs().gemm_bk ? knobs().gemm_bk : (A.rows >= 8192 ? 16 : 32);
+  if (bk == 16) return launch_gemm_bk<NT, 16>(A, B, e, st, splits, splits_used);
   return launch_gemm_bk<NT, 32>(A, B, e, st, splits, splits_used);
 }
 

@@ -21,7 +21,8 @@ const Knobs& knobs() {
     Knobs r{};
     r.train_impl = env("TPCB_TRAIN_IMPL", 0);
     r.grid_cap = env("TPCB_GRID_CAP", 0);
-    r.gemm_bk = env("TPCB_GEMM_BK", 16) == 32 ? 32 : 16;
+    const int bk = env("TPCB_GEMM_BK", 0);
+    r.gemm_bk = bk == 16 || bk == 32 ? bk : 0;  // 0: by shape (large.cu)
     r.gemm_cluster = env("TPCB_GEMM_CLUSTER", 0) ? 1 : 0;
     r.gemm_mode = env("TPCB_GEMM_MODE", 0);
     r.poll_ns = (unsigned)std::max(0, env("TPCB_POLL_NS", 256));
