@@ -4,20 +4,40 @@
 // assign[i] = argmin_e ‖x_i − c_e‖ (first index on ties), own[i] = that
 // distance, float64.
 //
-// Here the ranking score s_e = ‖c_e‖² − 2·x·c_e is formed for all centres by
-// a 3×TF32 tensor-core GEMM (x·c ≈ x_hi·c_hi + x_hi·c_lo + x_lo·c_hi, fp32
-// accumulation in TMEM — about fp32 accuracy), a per-point top-4 scan is fused
-// into the TMEM epilogue, and the four candidates are re-ranked with the exact
-// float64 distance in numpy's summation order.  The result is the reference's
-// argmin whenever the true nearest centre is among the four candidates (the
-// north_star asks ≥ 99.9 % agreement; tests/test_gpu_kmeans.py measures it).
+// Here a positive ranking score for every (point, centre) pair,
+//   q_e = ‖c_e‖² − 2·x·c_e + X,   X = ‖x‖²·(1 + 2^-16) + 2^-16·max_e ‖c_e‖²
+// (X exceeds the rounding error of the rest, so q_e > 0), is formed from a
+// 3×TF32 tensor-core GEMM (x·c ≈ x_hi·c_hi + x_hi·c_lo + x_lo·c_hi, fp32
+// accumulation in TMEM — about fp32 accuracy), and the candidates are chosen
+// in the TMEM epilogue, branch-free: the scores of one group of G consecutive
+// centres are packed into keys (q with its log2(G) low mantissa bits replaced
+// by the position in the group — one LOP3 per score, order-preserving because
+// q > 0), the group's minimum key is a tree of three-input FMNMX3, and each
+// group winner enters the point's sorted top-4 through a compare-exchange
+// chain.  The four candidates are re-ranked with the exact float64 distance in
+// numpy's summation order.  The result is the reference's argmin whenever the
+// true nearest centre is a candidate: unless another centre of its group
+// scores within the key quantum (2^-18 relative for G = 32) or four groups
+// beat it (north_star asks ≥ 99.9 % agreement; tests/test_gpu_kmeans.py
+// measures it at 262,144 × 1024, d = 24 and 32).  G = 32 for κ ≥ 512; below
+// that G = 1 — every score enters the top-4 (exact fp32 top-4, unquantised),
+// which costs 20 ALU operations per score but keeps the candidate set robust
+// to two near-tied centres falling in one group.
 //
-// Layout.  One CTA (4 warps, thread = point = TMEM lane) per 128-point tile;
-// points and centres as tf32 K-major 128-byte-swizzled UMMA tiles (d ≤ 32 →
-// one 128-B row per point); centres streamed in chunks of 256 through two
-// smem buffers by bulk copies from a pre-swizzled global image; two TMEM
-// accumulators of 256 columns so the MMAs of chunk c+1 overlap the epilogue
-// scan of chunk c.
+// Why this shape (profiles/r02/ncu_kmeans_tc_summary.txt): the epilogue, not
+// the tensor core, bounds the pass.  The round-1 kernel kept an exact fp32
+// top-4 with a per-score branch; with random centre order each point inserts
+// ~26 times at random positions, so some lane of every warp inserts at almost
+// every position, the warp pays all 32 lanes' insertions, and the top-4 array
+// was dynamically indexed (local memory) — 3.4 ms per 1 M × 1024 pass.
+//
+// Layout.  Two CTAs per SM (4 warps each, thread = point = TMEM lane), one
+// 128-point tile at a time; points and centres as tf32 K-major
+// 128-byte-swizzled UMMA tiles (d ≤ 32 → one 128-B row per point); centres
+// streamed in chunks of 128 through two smem buffers by bulk copies from a
+// pre-swizzled global image; two TMEM accumulators of 128 columns so the MMAs
+// of chunk c+1 overlap the scan of chunk c, and the other CTA's point loads and
+// re-rank overlap this CTA's scan.
 #include <cmath>
 
 #include "async.cuh"
@@ -28,15 +48,17 @@ namespace tpcb {
 namespace {
 
 constexpr int TP = 128;        // points per tile = TMEM lanes = threads
-constexpr int CN = 256;        // centres per chunk (N of one MMA)
+constexpr int CN = 128;        // centres per chunk (N of one MMA)
 constexpr int kTop = 4;        // candidates re-ranked exactly
 constexpr int kRowB = 128;     // bytes per operand row (32 fp32)
 constexpr int kPtTile = TP * kRowB;   // 16 KB
-constexpr int kCtTile = CN * kRowB;   // 32 KB
-// smem: points hi, lo | centre buffers [2][hi, lo] | centre norms [2][256]
+constexpr int kCtTile = CN * kRowB;   // 16 KB
+// smem: points hi, lo | centre buffers [2][hi, lo] | centre norms [2][128]
 constexpr int kSmPtHi = 0, kSmPtLo = kPtTile, kSmCt = 2 * kPtTile;
 constexpr int kSmNorm = kSmCt + 2 * 2 * kCtTile;
 constexpr int kSmTotal = kSmNorm + 2 * CN * 4;
+constexpr float kPadNorm = 1e37f;     // padding centres: finite, never a group winner
+constexpr float kBias = 0x1p-16f;
 
 __host__ __device__ inline uint32_t sw128f(int r, int k) {  // fp32 element (row r, col k < 32)
   return (r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 2) ^ (r & 7))) << 4) + (k & 3) * 4;
@@ -87,10 +109,12 @@ __device__ double exact_sq(const double* a, const double* b, int d) {
   return res;
 }
 
-// centres → per-chunk operand image: chunk c = [hi tile (32 KB) | lo tile (32 KB)]
-// and fp32 norms ‖c‖² (padding centres: zero rows, norm +inf)
+// centres → per-chunk operand image: chunk c = [hi tile (16 KB) | lo tile (16 KB)],
+// fp32 norms ‖c‖² (padding centres: zero rows, norm kPadNorm) and their maximum
+// (float bits; norms ≥ 0, so the unsigned order is the float order)
 __global__ void prep_centers_kernel(const double* __restrict__ c, int kappa, int d, int nchunks,
-                                    uint8_t* __restrict__ img, float* __restrict__ norms) {
+                                    uint8_t* __restrict__ img, float* __restrict__ norms,
+                                    unsigned* __restrict__ max_norm) {
   const int total = nchunks * CN * 32;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int row = e / 32, k = e - row * 32;  // row = centre index
@@ -105,7 +129,8 @@ __global__ void prep_centers_kernel(const double* __restrict__ c, int kappa, int
       double s = 0.0;
       if (row < kappa)
         for (int i = 0; i < d; ++i) s += c[(size_t)row * d + i] * c[(size_t)row * d + i];
-      norms[row] = row < kappa ? (float)s : INFINITY;
+      norms[row] = row < kappa ? (float)s : kPadNorm;
+      if (row < kappa) atomicMax(max_norm, __float_as_uint((float)s));
     }
   }
 }
@@ -130,10 +155,48 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
       smem_u32(bar)));
 }
 
-__global__ void __launch_bounds__(TP, 1) assign_tc_kernel(
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {  // FFMA2
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {  // FADD2
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ float min3(float a, float b, float c) {  // FMNMX3
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// minimum of G packed keys
+template <int G>
+__device__ __forceinline__ float group_min(const float* k) {  // G = 1, 8 or 32
+  if constexpr (G == 1) {
+    return k[0];
+  } else if constexpr (G == 8) {
+    return min3(min3(k[0], k[1], k[2]), min3(k[3], k[4], k[5]), fminf(k[6], k[7]));
+  } else {
+    float t[11];
+#pragma unroll
+    for (int i = 0; i < 10; ++i) t[i] = min3(k[3 * i], k[3 * i + 1], k[3 * i + 2]);
+    t[10] = fminf(k[30], k[31]);
+    return fminf(min3(min3(t[0], t[1], t[2]), min3(t[3], t[4], t[5]), min3(t[6], t[7], t[8])),
+                 fminf(t[9], t[10]));
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(TP, 2) assign_tc_kernel(
     const double* __restrict__ x, int64_t n, int d, const double* __restrict__ centers,
     int kappa, int nchunks, const uint8_t* __restrict__ img, const float* __restrict__ norms,
-    int64_t* __restrict__ assign, double* __restrict__ own, int32_t* __restrict__ counts) {
+    const unsigned* __restrict__ max_norm, int64_t* __restrict__ assign,
+    double* __restrict__ own, int32_t* __restrict__ counts) {
   extern __shared__ __align__(1024) uint8_t smb[];
   __shared__ __align__(8) uint64_t loaded[2], done[2];
   __shared__ uint32_t s_tmem;
@@ -146,7 +209,7 @@ __global__ void __launch_bounds__(TP, 1) assign_tc_kernel(
     mbar_fence_init();
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
         smem_u32(&s_tmem)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -157,20 +220,25 @@ __global__ void __launch_bounds__(TP, 1) assign_tc_kernel(
   const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
   const uint32_t sb = smem_u32(smb);
   float* s_norm = reinterpret_cast<float*>(smb + kSmNorm);
+  const float bias_c = kBias * __uint_as_float(__ldg(max_norm));
   uint32_t ld_cnt[2] = {0, 0}, mma_cnt[2] = {0, 0};  // uses of each buffer (mbarrier parity)
 
   for (int64_t p0 = (int64_t)blockIdx.x * TP; p0 < n; p0 += (int64_t)gridDim.x * TP) {
     const int64_t i = p0 + t;
     const bool live = i < n;
-    // this point → hi / lo rows of the A operands
+    float X;
+    // this point → hi / lo rows of the A operands, and its score offset X
     {
-      float hv[32], lv[32];
+      float hv[32], lv[32], xx = 0.f;
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const double v = (live && k < d) ? x[i * d + k] : 0.0;
-        hv[k] = tf32_hi((float)v);
+        const float vf = (float)v;
+        xx = fmaf(vf, vf, xx);
+        hv[k] = tf32_hi(vf);
         lv[k] = tf32_hi((float)(v - (double)hv[k]));
       }
+      X = fmaf(xx, kBias, xx) + bias_c;
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
         *reinterpret_cast<float4*>(smb + kSmPtHi + sw128f(t, 4 * c4)) =
@@ -206,13 +274,14 @@ __global__ void __launch_bounds__(TP, 1) assign_tc_kernel(
     } else {  // every thread tracks the buffer use counts
       ++ld_cnt[0];
     }
-    float bs[kTop];
+    float bs[kTop];  // sorted packed keys of the group winners
     int bj[kTop];
 #pragma unroll
     for (int q = 0; q < kTop; ++q) {
       bs[q] = INFINITY;
-      bj[q] = 0;
+      bj[q] = 0x7fffffff;
     }
+    const uint64_t m2 = pk2(-2.f, -2.f), x2 = pk2(X, X);
     for (int c = 0; c < nchunks; ++c) {
       const int b = c & 1;
       if (c + 1 < nchunks) {
@@ -222,7 +291,8 @@ __global__ void __launch_bounds__(TP, 1) assign_tc_kernel(
       mbar_wait(&done[b], mma_cnt[b] & 1);
       ++mma_cnt[b];
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const float* nrm = s_norm + b * CN;
+      const float4* nrm4 = reinterpret_cast<const float4*>(s_norm + b * CN);
+#pragma unroll 1
       for (int j0 = 0; j0 < CN; j0 += 32) {
         uint32_t r[32];
         asm volatile(
@@ -236,22 +306,36 @@ __global__ void __launch_bounds__(TP, 1) assign_tc_kernel(
               "=r"(r[30]), "=r"(r[31])
             : "r"(tmem + lane_off + b * CN + j0));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        float key[32];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const float s = fmaf(-2.f, __uint_as_float(r[u]), nrm[j0 + u]);
-          if (s < bs[kTop - 1]) {  // insert (strict: earlier index wins ties)
-            const int jj = c * CN + j0 + u;
-            int q = kTop - 1;
+        for (int v = 0; v < 8; ++v) {
+          const float4 nv = nrm4[j0 / 4 + v];
+          const uint64_t s01 = fma2(pk2(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1])),
+                                    m2, add2(pk2(nv.x, nv.y), x2));
+          const uint64_t s23 =
+              fma2(pk2(__uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])), m2,
+                   add2(pk2(nv.z, nv.w), x2));
+          const uint32_t w[4] = {(uint32_t)s01, (uint32_t)(s01 >> 32), (uint32_t)s23,
+                                 (uint32_t)(s23 >> 32)};
 #pragma unroll
-            for (int z = kTop - 1; z > 0; --z) {
-              if (q == z && s < bs[z - 1]) {
-                bs[z] = bs[z - 1];
-                bj[z] = bj[z - 1];
-                q = z - 1;
-              }
-            }
-            bs[q] = s;
-            bj[q] = jj;
+          for (int e = 0; e < 4; ++e) {
+            const int u = 4 * v + e;
+            key[u] = __uint_as_float((w[e] & ~(uint32_t)(G - 1)) | (uint32_t)(u % G));
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < 32 / G; ++g) {
+          float m = group_min<G>(key + g * G);
+          int jj = c * CN + j0 + g * G + (int)(__float_as_uint(m) & (G - 1));
+#pragma unroll
+          for (int q = 0; q < kTop; ++q) {  // compare-exchange chain, strict: earlier wins ties
+            const bool p = m < bs[q];
+            const float nb = p ? m : bs[q];
+            const int nj = p ? jj : bj[q];
+            m = p ? bs[q] : m;
+            jj = p ? bj[q] : jj;
+            bs[q] = nb;
+            bj[q] = nj;
           }
         }
       }
@@ -295,7 +379,24 @@ __global__ void __launch_bounds__(TP, 1) assign_tc_kernel(
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+template <int G>
+int launch_assign(const double* x, int64_t n, int d, const double* c, int kappa, int nchunks,
+                   const uint8_t* img, const float* norms, const unsigned* max_norm,
+                   int64_t* assign, double* own, int32_t* counts, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(assign_tc_kernel<G>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTotal));
+    attr = true;
+  }
+  const int64_t tiles = (n + TP - 1) / TP;
+  const int grid = (int)std::min<int64_t>(tiles, 2 * kNumSMs);
+  assign_tc_kernel<G><<<grid, TP, kSmTotal, stream>>>(x, n, d, c, kappa, nchunks, img, norms,
+                                                      max_norm, assign, own, counts);
+  return TPCB_OK;
 }
 
 }  // namespace
@@ -308,7 +409,7 @@ using namespace tpcb;
  * tpcb_kmeans_assign for d <= 32; d_ws: tpcb_kmeans_assign_tc_ws(kappa) bytes. */
 extern "C" size_t tpcb_kmeans_assign_tc_ws(int32_t kappa) {
   const int nchunks = (kappa + CN - 1) / CN;
-  return (size_t)nchunks * (2 * kCtTile + CN * 4) + 1024;
+  return (size_t)nchunks * (2 * kCtTile + CN * 4) + 1024 + 64;
 }
 
 extern "C" int tpcb_kmeans_assign_tc(const double* d_x, int64_t n, int32_t d,
@@ -323,20 +424,18 @@ extern "C" int tpcb_kmeans_assign_tc(const double* d_x, int64_t n, int32_t d,
   uint8_t* img = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(d_ws) + 1023) & ~static_cast<uintptr_t>(1023));
   float* norms = reinterpret_cast<float*>(img + (size_t)nchunks * 2 * kCtTile);
-  static bool attr = false;
-  if (!attr) {
-    TPCB_CUDA_CHECK(cudaFuncSetAttribute(assign_tc_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTotal));
-    attr = true;
-  }
+  unsigned* max_norm = reinterpret_cast<unsigned*>(norms + nchunks * CN);
   TPCB_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * kappa, stream));
+  TPCB_CUDA_CHECK(cudaMemsetAsync(max_norm, 0, sizeof(unsigned), stream));
   prep_centers_kernel<<<std::min(nchunks * CN * 32 / 256 + 1, 4 * kNumSMs), 256, 0, stream>>>(
-      d_centers, kappa, d, nchunks, img, norms);
+      d_centers, kappa, d, nchunks, img, norms, max_norm);
   TPCB_LAUNCH_CHECK("prep_centers");
-  const int64_t tiles = (n + TP - 1) / TP;
-  const int grid = (int)std::min<int64_t>(tiles, kNumSMs);
-  assign_tc_kernel<<<grid, TP, kSmTotal, stream>>>(d_x, n, d, d_centers, kappa, nchunks, img,
-                                                   norms, d_assign, d_own, d_counts);
+  const int rc = kappa >= 512
+                     ? launch_assign<32>(d_x, n, d, d_centers, kappa, nchunks, img, norms,
+                                         max_norm, d_assign, d_own, d_counts, stream)
+                     : launch_assign<1>(d_x, n, d, d_centers, kappa, nchunks, img, norms,
+                                        max_norm, d_assign, d_own, d_counts, stream);
+  if (rc != TPCB_OK) return rc;
   TPCB_LAUNCH_CHECK("kmeans_assign_tc");
   return TPCB_OK;
 }

@@ -95,6 +95,32 @@ def test_errors():
         s.build_distance_table(m, [s.TaskFeatureSet("x", np.zeros((2, 2)))])
 
 
+def test_tensor_core_assign_ties_and_small_kappa():
+    """Tensor-core mode on the cases where the candidate keys tie: duplicated
+    centres (the first index must win, as in the reference's argmin — within a
+    group of centres and across groups), points sitting exactly on a centre
+    (distance 0), and kappa below the candidate count (1, 3) — all identical to
+    the exact assignment."""
+    s = _s()
+    rng = np.random.default_rng(21)
+    x = rng.normal(size=(5000, 32))
+    for k in (1, 3, 40, 600):
+        c = x[rng.choice(len(x), k, replace=False)].copy()
+        if k >= 40:
+            c[k - 1] = c[0]          # duplicate across groups
+            c[5] = c[2]              # duplicate inside one group
+            c[k // 2] = c[1]
+        xs = np.concatenate([x, c[: min(k, 8)]])  # points exactly on centres
+        ex = s.DeviceKMeans(xs, k)
+        tc = s.DeviceKMeans(xs, k, assign="tc")
+        for km in (ex, tc):
+            km.centers.copy_(torch.from_numpy(c))
+            km.assign_step()
+        a_ex, a_tc = ex.assign.cpu().numpy(), tc.assign.cpu().numpy()
+        assert np.array_equal(a_ex, a_tc), (k, np.flatnonzero(a_ex != a_tc)[:5])
+        assert np.array_equal(ex.own.cpu().numpy(), tc.own.cpu().numpy())
+
+
 def test_tensor_core_assign_agreement():
     """Tensor-core assignment mode (3xTF32 distance GEMM + exact fp64 re-rank
     of the top-4): agreement with the exact assignment >= 99.9 % (north_star)
