@@ -53,10 +53,9 @@ constexpr int kTop = 4;        // candidates re-ranked exactly
 constexpr int kRowB = 128;     // bytes per operand row (32 fp32)
 constexpr int kPtTile = TP * kRowB;   // 16 KB
 constexpr int kCtTile = CN * kRowB;   // 16 KB
-// smem: points hi, lo | centre buffers [2][hi, lo] | centre norms [2][128]
+// smem: points hi, lo | centre buffers [2][hi, lo]
 constexpr int kSmPtHi = 0, kSmPtLo = kPtTile, kSmCt = 2 * kPtTile;
-constexpr int kSmNorm = kSmCt + 2 * 2 * kCtTile;
-constexpr int kSmTotal = kSmNorm + 2 * CN * 4;
+constexpr int kSmTotal = kSmCt + 2 * 2 * kCtTile;
 constexpr float kPadNorm = 1e37f;     // padding centres: finite, never a group winner
 constexpr float kBias = 0x1p-16f;
 
@@ -192,20 +191,25 @@ __device__ __forceinline__ float group_min(const float* k) {  // G = 1, 8 or 32
 }
 
 template <int G>
-__global__ void __launch_bounds__(TP, 2) assign_tc_kernel(
+__global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
     const double* __restrict__ x, int64_t n, int d, const double* __restrict__ centers,
     int kappa, int nchunks, const uint8_t* __restrict__ img, const float* __restrict__ norms,
     const unsigned* __restrict__ max_norm, int64_t* __restrict__ assign,
     double* __restrict__ own, int32_t* __restrict__ counts) {
   extern __shared__ __align__(1024) uint8_t smb[];
-  __shared__ __align__(8) uint64_t loaded[2], done[2];
+  // loaded: chunk image in smem buffer b; done: its MMAs complete (TMEM buffer b
+  // holds chunk scores); empty: the 4 scanning warps finished TMEM buffer b;
+  // pts: the 4 warps staged the next tile's points
+  __shared__ __align__(8) uint64_t loaded[2], done[2], empty[2], pts;
   __shared__ uint32_t s_tmem;
-  const int t = threadIdx.x, warp = t >> 5;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(&loaded[i], 1);
       mbar_init(&done[i], 1);
+      mbar_init(&empty[i], 4);
     }
+    mbar_init(&pts, 4);
     mbar_fence_init();
   }
   if (warp == 0) {
@@ -217,28 +221,50 @@ __global__ void __launch_bounds__(TP, 2) assign_tc_kernel(
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
   const uint32_t sb = smem_u32(smb);
-  float* s_norm = reinterpret_cast<float*>(smb + kSmNorm);
-  const float bias_c = kBias * __uint_as_float(__ldg(max_norm));
-  uint32_t ld_cnt[2] = {0, 0}, mma_cnt[2] = {0, 0};  // uses of each buffer (mbarrier parity)
+  const int64_t stride = (int64_t)gridDim.x * TP, first = (int64_t)blockIdx.x * TP;
+  const int ntiles = first < n ? (int)((n - first + stride - 1) / stride) : 0;
+  const int total = ntiles * nchunks;  // chunk steps of this CTA, buffers alternate across tiles
 
-  for (int64_t p0 = (int64_t)blockIdx.x * TP; p0 < n; p0 += (int64_t)gridDim.x * TP) {
-    const int64_t i = p0 + t;
-    const bool live = i < n;
-    float X;
-    // this point → hi / lo rows of the A operands, and its score offset X
-    {
+  if (warp == 4) {  // producer: bulk loads of the centre image + MMA issue, one lane
+    if (lane == 0 && total > 0) {
+      auto load = [&](int gc) {
+        const int b = gc & 1, c = gc % nchunks;
+        mbar_arrive_expect_tx(&loaded[b], (uint32_t)(2 * kCtTile));
+        bulk_g2s(smb + kSmCt + b * 2 * kCtTile, img + (size_t)c * 2 * kCtTile, 2 * kCtTile,
+                 &loaded[b]);
+      };
+      load(0);
+      if (total > 1) load(1);
+      for (int gc = 0; gc < total; ++gc) {
+        const int b = gc & 1;
+        if (gc % nchunks == 0) mbar_wait(&pts, (gc / nchunks) & 1);
+        mbar_wait(&loaded[b], (gc >> 1) & 1);
+        if (gc >= 2) mbar_wait(&empty[b], ((gc - 2) >> 1) & 1);  // TMEM buffer b scanned
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t cb = sb + kSmCt + b * 2 * kCtTile;
+        mma3(tmem + b * CN, sb + kSmPtHi, sb + kSmPtLo, cb, cb + kCtTile);
+        commit(&done[b]);
+        if (gc + 2 < total) {  // smem buffer b is free once these MMAs complete
+          mbar_wait(&done[b], (gc >> 1) & 1);
+          load(gc + 2);
+        }
+      }
+    }
+  } else {  // warps 0-3: thread = point = TMEM lane
+    const uint32_t lane_off = (uint32_t)(32 * warp) << 16;
+    const float bias_c = kBias * __uint_as_float(__ldg(max_norm));
+    // point i → hi / lo rows of the A operands; returns its score offset X
+    auto stage = [&](int64_t i) {
+      const bool live = i < n;
       float hv[32], lv[32], xx = 0.f;
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const double v = (live && k < d) ? x[i * d + k] : 0.0;
-        const float vf = (float)v;
+      for (int k = 0; k < 32; ++k) {  // fp32 split: the 2^-24 rounding of x is below 3xTF32's
+        const float vf = (live && k < d) ? (float)x[i * d + k] : 0.f;
         xx = fmaf(vf, vf, xx);
         hv[k] = tf32_hi(vf);
-        lv[k] = tf32_hi((float)(v - (double)hv[k]));
+        lv[k] = tf32_hi(vf - hv[k]);
       }
-      X = fmaf(xx, kBias, xx) + bias_c;
 #pragma unroll
       for (int c4 = 0; c4 < 8; ++c4) {
         *reinterpret_cast<float4*>(smb + kSmPtHi + sw128f(t, 4 * c4)) =
@@ -246,105 +272,86 @@ __global__ void __launch_bounds__(TP, 2) assign_tc_kernel(
         *reinterpret_cast<float4*>(smb + kSmPtLo + sw128f(t, 4 * c4)) =
             make_float4(lv[4 * c4], lv[4 * c4 + 1], lv[4 * c4 + 2], lv[4 * c4 + 3]);
       }
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    auto load_chunk = [&](int c) {  // thread 0: chunk c → buffer c & 1
-      const int b = c & 1;
-      mbar_arrive_expect_tx(&loaded[b], (uint32_t)(2 * kCtTile + CN * 4));
-      bulk_g2s(smb + kSmCt + b * 2 * kCtTile, img + (size_t)c * 2 * kCtTile, 2 * kCtTile,
-               &loaded[b]);
-      bulk_g2s(s_norm + b * CN, norms + (size_t)c * CN, CN * 4, &loaded[b]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pts);
+      return fmaf(xx, kBias, xx) + bias_c;
     };
-    auto issue = [&](int c) {  // thread 0: wait for chunk c, MMAs into TMEM buffer c & 1
-      const int b = c & 1;
-      mbar_wait(&loaded[b], ld_cnt[b] & 1);
-      ++ld_cnt[b];
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t cb = sb + kSmCt + b * 2 * kCtTile;
-      mma3(tmem + b * CN, sb + kSmPtHi, sb + kSmPtLo, cb, cb + kCtTile);
-      commit(&done[b]);
-    };
-    if (t == 0) {
-      load_chunk(0);
-      if (nchunks > 1) load_chunk(1);
-      issue(0);
-    } else {  // every thread tracks the buffer use counts
-      ++ld_cnt[0];
-    }
-    float bs[kTop];  // sorted packed keys of the group winners
-    int bj[kTop];
+    float X = ntiles > 0 ? stage(first + t) : 0.f;
+    int gc = 0;
+    for (int it = 0; it < ntiles; ++it) {
+      const int64_t i = first + it * stride + t;
+      const bool live = i < n;
+      float bs[kTop];  // sorted packed keys of the group winners
+      int bj[kTop];
 #pragma unroll
-    for (int q = 0; q < kTop; ++q) {
-      bs[q] = INFINITY;
-      bj[q] = 0x7fffffff;
-    }
-    const uint64_t m2 = pk2(-2.f, -2.f), x2 = pk2(X, X);
-    for (int c = 0; c < nchunks; ++c) {
-      const int b = c & 1;
-      if (c + 1 < nchunks) {
-        if (t == 0) issue(c + 1);
-        else ++ld_cnt[(c + 1) & 1];
+      for (int q = 0; q < kTop; ++q) {
+        bs[q] = INFINITY;
+        bj[q] = 0x7fffffff;
       }
-      mbar_wait(&done[b], mma_cnt[b] & 1);
-      ++mma_cnt[b];
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const float4* nrm4 = reinterpret_cast<const float4*>(s_norm + b * CN);
+      const uint64_t m2 = pk2(-2.f, -2.f), x2 = pk2(X, X);
+      for (int c = 0; c < nchunks; ++c, ++gc) {
+        const int b = gc & 1;
+        mbar_wait(&done[b], (gc >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const float4* nrm4 = reinterpret_cast<const float4*>(norms + (size_t)c * CN);
 #pragma unroll 1
-      for (int j0 = 0; j0 < CN; j0 += 32) {
-        uint32_t r[32];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-            "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
-              "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
-              "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]),
-              "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
-              "=r"(r[30]), "=r"(r[31])
-            : "r"(tmem + lane_off + b * CN + j0));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        float key[32];
+        for (int j0 = 0; j0 < CN; j0 += 32) {
+          uint32_t r[32];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+              "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]),
+                "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+                "=r"(r[30]), "=r"(r[31])
+              : "r"(tmem + lane_off + b * CN + j0));
+          float4 nv[8];
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const float4 nv = nrm4[j0 / 4 + v];
-          const uint64_t s01 = fma2(pk2(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1])),
-                                    m2, add2(pk2(nv.x, nv.y), x2));
-          const uint64_t s23 =
-              fma2(pk2(__uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])), m2,
-                   add2(pk2(nv.z, nv.w), x2));
-          const uint32_t w[4] = {(uint32_t)s01, (uint32_t)(s01 >> 32), (uint32_t)s23,
-                                 (uint32_t)(s23 >> 32)};
+          for (int v = 0; v < 8; ++v) nv[v] = __ldg(nrm4 + j0 / 4 + v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          float key[32];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int u = 4 * v + e;
-            key[u] = __uint_as_float((w[e] & ~(uint32_t)(G - 1)) | (uint32_t)(u % G));
+          for (int v = 0; v < 8; ++v) {
+            const uint64_t s01 =
+                fma2(pk2(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1])), m2,
+                     add2(pk2(nv[v].x, nv[v].y), x2));
+            const uint64_t s23 =
+                fma2(pk2(__uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3])), m2,
+                     add2(pk2(nv[v].z, nv[v].w), x2));
+            const uint32_t w[4] = {(uint32_t)s01, (uint32_t)(s01 >> 32), (uint32_t)s23,
+                                   (uint32_t)(s23 >> 32)};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int u = 4 * v + e;
+              key[u] = __uint_as_float((w[e] & ~(uint32_t)(G - 1)) | (uint32_t)(u % G));
+            }
+          }
+#pragma unroll
+          for (int g = 0; g < 32 / G; ++g) {
+            float m = group_min<G>(key + g * G);
+            int jj = c * CN + j0 + g * G + (int)(__float_as_uint(m) & (G - 1));
+#pragma unroll
+            for (int q = 0; q < kTop; ++q) {  // compare-exchange chain, strict: earlier wins ties
+              const bool p = m < bs[q];
+              const float nb = p ? m : bs[q];
+              const int nj = p ? jj : bj[q];
+              m = p ? bs[q] : m;
+              jj = p ? bj[q] : jj;
+              bs[q] = nb;
+              bj[q] = nj;
+            }
           }
         }
-#pragma unroll
-        for (int g = 0; g < 32 / G; ++g) {
-          float m = group_min<G>(key + g * G);
-          int jj = c * CN + j0 + g * G + (int)(__float_as_uint(m) & (G - 1));
-#pragma unroll
-          for (int q = 0; q < kTop; ++q) {  // compare-exchange chain, strict: earlier wins ties
-            const bool p = m < bs[q];
-            const float nb = p ? m : bs[q];
-            const int nj = p ? jj : bj[q];
-            m = p ? bs[q] : m;
-            jj = p ? bj[q] : jj;
-            bs[q] = nb;
-            bj[q] = nj;
-          }
-        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[b]);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncthreads();  // TMEM buffer b and its norms fully read before chunk c + 2 reuses them
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      // chunk c's MMAs are complete and its scan is done: refill the buffer
-      if (t == 0 && c + 2 < nchunks) load_chunk(c + 2);
-    }
+      // every MMA of this tile has completed (done waited for its last chunk):
+      // stage the next tile's points so its MMAs overlap this tile's re-rank
+      if (it + 1 < ntiles) X = stage(i + stride);
     if (live) {  // exact float64 re-rank of the candidates (numpy argmin semantics)
       const double* xi = x + i * d;
       double best = INFINITY;
@@ -362,11 +369,53 @@ __global__ void __launch_bounds__(TP, 2) assign_tc_kernel(
             cand[q1] = cand[q1 + 1];
             cand[q1 + 1] = tmp;
           }
+      double sq[kTop];
+      if (d % 8 == 0) {  // all four candidates at once: 8-wide loads, 32 independent chains
+        const double* cr[kTop];
+#pragma unroll
+        for (int q = 0; q < kTop; ++q) cr[q] = centers + (size_t)min(cand[q], kappa - 1) * d;
+        double acc[kTop][8];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (8 * b >= d) break;
+          double xv[8], cv[kTop][8];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const double2 v = *reinterpret_cast<const double2*>(xi + 8 * b + 2 * h);
+            xv[2 * h] = v.x;
+            xv[2 * h + 1] = v.y;
+          }
+#pragma unroll
+          for (int q = 0; q < kTop; ++q)
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const double2 v = __ldg(reinterpret_cast<const double2*>(cr[q] + 8 * b + 2 * h));
+              cv[q][2 * h] = v.x;
+              cv[q][2 * h + 1] = v.y;
+            }
+#pragma unroll
+          for (int q = 0; q < kTop; ++q)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // numpy order: 8 running sums, i ≡ j (mod 8)
+              const double t = __dsub_rn(xv[j], cv[q][j]);
+              acc[q][j] = b == 0 ? __dmul_rn(t, t) : __dadd_rn(acc[q][j], __dmul_rn(t, t));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kTop; ++q)
+          sq[q] = __dadd_rn(__dadd_rn(__dadd_rn(acc[q][0], acc[q][1]),
+                                      __dadd_rn(acc[q][2], acc[q][3])),
+                            __dadd_rn(__dadd_rn(acc[q][4], acc[q][5]),
+                                      __dadd_rn(acc[q][6], acc[q][7])));
+      } else {
+#pragma unroll
+        for (int q = 0; q < kTop; ++q)
+          sq[q] = exact_sq(xi, centers + (size_t)min(cand[q], kappa - 1) * d, d);
+      }
 #pragma unroll
       for (int q = 0; q < kTop; ++q) {
-        if (cand[q] >= kappa) continue;
-        const double dist = sqrt(exact_sq(xi, centers + (size_t)cand[q] * d, d));
-        if (dist < best) {
+        const double dist = sqrt(sq[q]);
+        if (cand[q] < kappa && dist < best) {
           best = dist;
           bi = cand[q];
         }
@@ -375,7 +424,7 @@ __global__ void __launch_bounds__(TP, 2) assign_tc_kernel(
       own[i] = best;
       atomicAdd(&counts[bi], 1);
     }
-    __syncthreads();
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -394,7 +443,7 @@ int launch_assign(const double* x, int64_t n, int d, const double* c, int kappa,
   }
   const int64_t tiles = (n + TP - 1) / TP;
   const int grid = (int)std::min<int64_t>(tiles, 2 * kNumSMs);
-  assign_tc_kernel<G><<<grid, TP, kSmTotal, stream>>>(x, n, d, c, kappa, nchunks, img, norms,
+  assign_tc_kernel<G><<<grid, TP + 32, kSmTotal, stream>>>(x, n, d, c, kappa, nchunks, img, norms,
                                                       max_norm, assign, own, counts);
   return TPCB_OK;
 }
