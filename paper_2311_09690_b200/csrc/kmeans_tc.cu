@@ -53,9 +53,10 @@ constexpr int kTop = 4;        // candidates re-ranked exactly
 constexpr int kRowB = 128;     // bytes per operand row (32 fp32)
 constexpr int kPtTile = TP * kRowB;   // 16 KB
 constexpr int kCtTile = CN * kRowB;   // 16 KB
-// smem: points hi, lo | centre buffers [2][hi, lo]
+// smem: points hi, lo | centre buffers [2][hi, lo] | centre norms [2][128]
 constexpr int kSmPtHi = 0, kSmPtLo = kPtTile, kSmCt = 2 * kPtTile;
-constexpr int kSmTotal = kSmCt + 2 * 2 * kCtTile;
+constexpr int kSmNorm = kSmCt + 2 * 2 * kCtTile;
+constexpr int kSmTotal = kSmNorm + 2 * CN * 4;
 constexpr float kPadNorm = 1e37f;     // padding centres: finite, never a group winner
 constexpr float kBias = 0x1p-16f;
 
@@ -199,8 +200,8 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
   extern __shared__ __align__(1024) uint8_t smb[];
   // loaded: chunk image in smem buffer b; done: its MMAs complete (TMEM buffer b
   // holds chunk scores); empty: the 4 scanning warps finished TMEM buffer b;
-  // pts: the 4 warps staged the next tile's points
-  __shared__ __align__(8) uint64_t loaded[2], done[2], empty[2], pts;
+  // pts: the 4 warps staged the next tile's points; nld: chunk norms in slot b
+  __shared__ __align__(8) uint64_t loaded[2], done[2], empty[2], nld[2], pts;
   __shared__ uint32_t s_tmem;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) {
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
       mbar_init(&loaded[i], 1);
       mbar_init(&done[i], 1);
       mbar_init(&empty[i], 4);
+      mbar_init(&nld[i], 1);
     }
     mbar_init(&pts, 4);
     mbar_fence_init();
@@ -222,6 +224,7 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
   const uint32_t sb = smem_u32(smb);
+  float* s_norm = reinterpret_cast<float*>(smb + kSmNorm);
   const int64_t stride = (int64_t)gridDim.x * TP, first = (int64_t)blockIdx.x * TP;
   const int ntiles = first < n ? (int)((n - first + stride - 1) / stride) : 0;
   const int total = ntiles * nchunks;  // chunk steps of this CTA, buffers alternate across tiles
@@ -241,6 +244,8 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
         if (gc % nchunks == 0) mbar_wait(&pts, (gc / nchunks) & 1);
         mbar_wait(&loaded[b], (gc >> 1) & 1);
         if (gc >= 2) mbar_wait(&empty[b], ((gc - 2) >> 1) & 1);  // TMEM buffer b scanned
+        mbar_arrive_expect_tx(&nld[b], (uint32_t)(CN * 4));
+        bulk_g2s(s_norm + b * CN, norms + (size_t)(gc % nchunks) * CN, CN * 4, &nld[b]);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t cb = sb + kSmCt + b * 2 * kCtTile;
         mma3(tmem + b * CN, sb + kSmPtHi, sb + kSmPtLo, cb, cb + kCtTile);
@@ -257,10 +262,22 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
     // point i → hi / lo rows of the A operands; returns its score offset X
     auto stage = [&](int64_t i) {
       const bool live = i < n;
-      float hv[32], lv[32], xx = 0.f;
+      float hv[32], lv[32], xx = 0.f, xf[32];
+      if ((d & 1) == 0) {  // 16-B loads
+#pragma unroll
+        for (int k = 0; k < 32; k += 2) {
+          const double2 v = (live && k < d) ? *reinterpret_cast<const double2*>(x + i * d + k)
+                                            : make_double2(0.0, 0.0);
+          xf[k] = (float)v.x;
+          xf[k + 1] = (float)v.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) xf[k] = (live && k < d) ? (float)x[i * d + k] : 0.f;
+      }
 #pragma unroll
       for (int k = 0; k < 32; ++k) {  // fp32 split: the 2^-24 rounding of x is below 3xTF32's
-        const float vf = (live && k < d) ? (float)x[i * d + k] : 0.f;
+        const float vf = xf[k];
         xx = fmaf(vf, vf, xx);
         hv[k] = tf32_hi(vf);
         lv[k] = tf32_hi(vf - hv[k]);
@@ -293,8 +310,9 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
       for (int c = 0; c < nchunks; ++c, ++gc) {
         const int b = gc & 1;
         mbar_wait(&done[b], (gc >> 1) & 1);
+        mbar_wait(&nld[b], (gc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const float4* nrm4 = reinterpret_cast<const float4*>(norms + (size_t)c * CN);
+        const float4* nrm4 = reinterpret_cast<const float4*>(s_norm + b * CN);
 #pragma unroll 1
         for (int j0 = 0; j0 < CN; j0 += 32) {
           uint32_t r[32];
@@ -310,7 +328,7 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
               : "r"(tmem + lane_off + b * CN + j0));
           float4 nv[8];
 #pragma unroll
-          for (int v = 0; v < 8; ++v) nv[v] = __ldg(nrm4 + j0 / 4 + v);
+          for (int v = 0; v < 8; ++v) nv[v] = nrm4[j0 / 4 + v];
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           float key[32];
 #pragma unroll
