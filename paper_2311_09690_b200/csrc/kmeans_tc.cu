@@ -174,6 +174,14 @@ __device__ __forceinline__ float min3(float a, float b, float c) {  // FMNMX3
   return r;
 }
 
+// (w & mask) | u in ONE LOP3: the mask lives in a register, u is the immediate
+// (with both as constants the compiler spends two LOP3s per score)
+__device__ __forceinline__ uint32_t pack_key(uint32_t w, uint32_t mask, uint32_t u) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(w), "r"(mask), "r"(u));  // (a & b) | c
+  return r;
+}
+
 // minimum of G packed keys
 template <int G>
 __device__ __forceinline__ float group_min(const float* k) {  // G = 1, 8 or 32
@@ -307,6 +315,8 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
         bj[q] = 0x7fffffff;
       }
       const uint64_t m2 = pk2(-2.f, -2.f), x2 = pk2(X, X);
+      // n ≥ 1, so the OR adds nothing — it only keeps the mask a runtime register
+      const uint32_t kmask = ~(uint32_t)(G - 1) | (uint32_t)((uint64_t)n >> 63);
       for (int c = 0; c < nchunks; ++c, ++gc) {
         const int b = gc & 1;
         mbar_wait(&done[b], (gc >> 1) & 1);
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int u = 4 * v + e;
-              key[u] = __uint_as_float((w[e] & ~(uint32_t)(G - 1)) | (uint32_t)(u % G));
+              key[u] = __uint_as_float(pack_key(w[e], kmask, u % G));
             }
           }
 #pragma unroll
