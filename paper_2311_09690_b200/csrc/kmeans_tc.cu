@@ -31,13 +31,17 @@
 // every position, the warp pays all 32 lanes' insertions, and the top-4 array
 // was dynamically indexed (local memory) — 3.4 ms per 1 M × 1024 pass.
 //
-// Layout.  Two CTAs per SM (4 warps each, thread = point = TMEM lane), one
-// 128-point tile at a time; points and centres as tf32 K-major
-// 128-byte-swizzled UMMA tiles (d ≤ 32 → one 128-B row per point); centres
-// streamed in chunks of 128 through two smem buffers by bulk copies from a
-// pre-swizzled global image; two TMEM accumulators of 128 columns so the MMAs
-// of chunk c+1 overlap the scan of chunk c, and the other CTA's point loads and
-// re-rank overlap this CTA's scan.
+// Layout.  Two CTAs per SM, each 4 scanning warps (thread = point = TMEM
+// lane, one 128-point tile at a time) + 1 producer warp.  Points and centres
+// are tf32 K-major 128-byte-swizzled UMMA tiles (d ≤ 32 → one 128-B row per
+// point); the producer streams the pre-swizzled centre image in chunks of 128
+// through a 2-deep smem ring (bulk copies; chunk norms through their own
+// ring) and one lane issues the MMAs into two 128-column TMEM buffers, so the
+// MMAs of chunk c+1 overlap the scan of chunk c.  Synchronisation is mbarriers
+// only (loaded / done / empty per buffer, one for the staged points): the
+// warps drift freely within a tile, and each warp stages its points of the
+// next tile as soon as its scan ends, so the next tile's MMAs overlap this
+// tile's fp64 re-rank.
 #include <cmath>
 
 #include "async.cuh"
