@@ -265,45 +265,93 @@ class Predictor:
             return cpu(pred), cpu(zx), cpu(zv), cpu(z), cpu(lat)
         return self._forward_pipelined(batch, normalizer, latents)
 
+    def _buf(self, name, numel, dtype, device=None):
+        """Cached pipeline buffer (device, or pinned host when device is None),
+        grown on demand; every call synchronises before returning, so a buffer
+        is never resized under in-flight work."""
+        cache = self.__dict__.setdefault("_pipe_bufs", {})
+        buf = cache.get(name)
+        if buf is None or buf.numel() < numel or buf.dtype != dtype:
+            buf = (torch.empty(max(numel, 1), dtype=dtype, device=device) if device is not None
+                   else torch.empty(max(numel, 1), dtype=dtype, pin_memory=True))
+            cache[name] = buf
+        return buf[:numel]
+
     def _forward_pipelined(self, batch: CompactBatch, normalizer, latents):
         n = batch.n_ast
         n_leaf = np.ascontiguousarray(batch.n_leaf, dtype=np.int64)
-        check_leaf_counts(n_leaf, self.config.n_leaf_max)
         dev = self.params.device
-        tok_off = np.zeros(n + 1, dtype=np.int64)
-        np.cumsum(n_leaf, out=tok_off[1:])
         table = torch.from_numpy(np.stack([device_vector(d) for d in batch.devices])
                                  .astype(np.float32)).to(dev)
-        t = lambda a: torch.from_numpy(np.ascontiguousarray(a))  # noqa: E731
-        rows_h, ord_h = t(batch.vectors), t(np.asarray(batch.ordering, dtype=np.int32))
-        nl_h, di_h = t(n_leaf), t(np.asarray(batch.device_index, dtype=np.int32))
-        out_pred = torch.empty(n, dtype=torch.float32, pin_memory=True)
-        out_lat = (torch.empty(n, dtype=torch.float64, pin_memory=True)
-                   if normalizer is not None else None)
+
+        def t(a, small=False):
+            # a copy from pageable memory blocks the host until the copy stream
+            # drains, which serialises the pipeline: small arrays (counts,
+            # orderings, device indices) are staged into pinned memory once;
+            # the rows are used as given (pin them to get the overlap)
+            x = torch.from_numpy(np.ascontiguousarray(a))
+            return x.pin_memory() if small and not x.is_pinned() else x
+        rows_h = t(batch.vectors)
+        ord_h = t(np.asarray(batch.ordering, dtype=np.int32), small=True)
+        nl_h = t(n_leaf, small=True)
+        one_dev = len(batch.devices) == 1  # every AST on device 0: no index upload
+        di_h = None if one_dev else t(np.asarray(batch.device_index, dtype=np.int32), small=True)
+        # a short first piece fills the pipeline sooner
+        bounds = [0] + list(range(min(n, self.CHUNK // 4), n, self.CHUNK)) + [n]
+        tok = np.add.reduceat(n_leaf, bounds[:-1])  # tokens per piece
+        cap_tok, cap_ast = int(tok.max()), int(np.diff(bounds).max())
+        F = rows_h.shape[1]
+        # two sets of device input buffers reused across pieces and calls (fresh
+        # allocations per piece, held by the side stream, made the caching
+        # allocator fall back to cudaMalloc / cudaFree — device-wide syncs)
+        ins = [(self._buf(f"rows{k}", cap_tok * F, rows_h.dtype, dev),
+                self._buf(f"ord{k}", cap_tok, torch.int32, dev),
+                self._buf(f"nl{k}", cap_ast, torch.int64, dev),
+                None if one_dev else self._buf(f"di{k}", cap_ast, torch.int32, dev))
+               for k in range(2)]
         de, ddev = self.config.d_embed, self.config.d_device
-        outs_lat = [torch.empty((n, w), dtype=torch.float32, pin_memory=True)
-                    for w in (de, ddev, de)] if latents else None
+        out_pred = self._buf("out_pred", n, torch.float32)  # pinned staging, copied out
+        out_lat = self._buf("out_lat", n, torch.float64) if normalizer is not None else None
+        outs_lat = [self._buf(f"out_{w}_{i}", n * w, torch.float32).view(n, w)
+                    for i, w in enumerate((de, ddev, de))] if latents else None
         compute = torch.cuda.current_stream(dev)
-        copy = torch.cuda.Stream(device=dev)
-        chunks = [(a, min(n, a + self.CHUNK)) for a in range(0, n, self.CHUNK)]
+        copy = self.__dict__.setdefault("_copy_stream", torch.cuda.Stream(device=dev))
+        free = [None, None]  # compute finished with input buffer set k
         keep = []
-        for a, b in chunks:
-            ta, tb = int(tok_off[a]), int(tok_off[b])
-            with torch.cuda.stream(copy):  # H2D of this chunk (async from pinned memory)
-                rows = rows_h[ta:tb].to(dev, non_blocking=True)
-                ordering = ord_h[ta:tb].to(dev, non_blocking=True)
-                nl = nl_h[a:b].to(dev, non_blocking=True)
-                di = di_h[a:b].to(dev, non_blocking=True)
+        tb = 0
+        for i, (a, b) in enumerate(zip(bounds[:-1], bounds[1:])):
+            nl_c = n_leaf[a:b]
+            if nl_c.min() < 1 or nl_c.max() > self.config.n_leaf_max:
+                compute.synchronize()  # pieces already queued finish; nothing is returned
+                check_leaf_counts(n_leaf, self.config.n_leaf_max)  # raises, global index
+            if one_dev and np.any(batch.device_index[a:b]):  # as table[device_index] would
+                compute.synchronize()
+                raise IndexError("device index out of range for a batch with one device")
+            ta, tb = tb, tb + int(tok[i])
+            k = i & 1
+            rows_d, ord_d, nl_d, di_d = ins[k]
+            rows = rows_d[:(tb - ta) * F].view(tb - ta, F)
+            ordering, nl = ord_d[:tb - ta], nl_d[:b - a]
+            di = None if one_dev else di_d[:b - a]
+            with torch.cuda.stream(copy):  # H2D of this piece (async from pinned memory)
+                if free[k] is not None:
+                    copy.wait_event(free[k])
+                rows.copy_(rows_h[ta:tb], non_blocking=True)
+                ordering.copy_(ord_h[ta:tb], non_blocking=True)
+                nl.copy_(nl_h[a:b], non_blocking=True)
+                if di is not None:
+                    di.copy_(di_h[a:b], non_blocking=True)
                 ready = torch.cuda.Event()
                 ready.record(copy)
             compute.wait_event(ready)
-            for x in (rows, ordering, nl, di):
-                x.record_stream(compute)
             leaf_off = torch.zeros(b - a + 1, dtype=torch.int64, device=dev)
             torch.cumsum(nl, 0, out=leaf_off[1:])
-            devfeat = table.index_select(0, di.long())
+            devfeat = table[:1].expand(b - a, -1).contiguous() if one_dev else \
+                table.index_select(0, di.long())
             pred, zx, zv, z, lat = self.forward_device(rows, ordering, leaf_off, devfeat, b - a,
                                                        False, normalizer, latents)
+            free[k] = torch.cuda.Event()
+            free[k].record(compute)
             out_pred[a:b].copy_(pred, non_blocking=True)
             if out_lat is not None:
                 out_lat[a:b].copy_(lat, non_blocking=True)
@@ -313,9 +361,10 @@ class Predictor:
             keep.append((pred, zx, zv, z, lat))  # alive until the D2H copies ran
         compute.synchronize()
         self.status.check("forward")
-        res = (out_pred.numpy(),) + (tuple(o.numpy() for o in outs_lat) if latents
-                                     else (None, None, None))
-        return res + (out_lat.numpy() if out_lat is not None else None,)
+        cp = lambda x: x.numpy().copy()  # noqa: E731  (the staging buffers are reused)
+        res = (cp(out_pred),) + (tuple(cp(o) for o in outs_lat) if latents
+                                 else (None, None, None))
+        return res + (cp(out_lat) if out_lat is not None else None,)
 
 
 def forward(params: CostModelParams, inputs: list) -> tuple:

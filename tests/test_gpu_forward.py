@@ -260,3 +260,13 @@ def test_forward_batch_pipelined_equals_one_shot(precision):
     for a, b in zip(one[:4], many[:4]):
         assert np.array_equal(a, b)
     assert one[4] is None and many[4] is None
+    # a bad leaf count in a later piece: the same error and global index as
+    # the one-shot path (checked per piece, after earlier pieces were queued)
+    from paper_2311_09690_b200.errors import LeafCountExceeded
+    nl = np.array(data.n_leaf)
+    bad = 17000
+    nl[bad] = 0
+    bad_batch = pb.CompactBatch(batch.vectors[: int(nl.sum())], batch.ordering[: int(nl.sum())],
+                                nl, batch.device_index, devs)
+    with pytest.raises(LeafCountExceeded, match=f"input {bad} "):
+        p.forward_batch(bad_batch, None)
