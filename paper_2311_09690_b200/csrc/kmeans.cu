@@ -20,6 +20,7 @@
 //   K11 distance_table Ψ[e, t] = mean over task t's rows of dist(row, c_e)
 #include <cub/cub.cuh>
 
+#include "async.cuh"
 #include "common.cuh"
 
 namespace tpcb {
@@ -409,6 +410,298 @@ cudaError_t prep_closest(int d) {
                               (int)closest_smem(d));
 }
 
+// closest_update for d ∈ {24, 32} (the sampler's feature widths): same values,
+// a bulk-copy pipeline instead of load-then-compute.  Thread t owns row t of a
+// 128-row tile: it issues the 16-byte-aligned bulk copy of that row for the
+// NEXT tile (cp.async.bulk → smem, padded pitch so the LDS.128 row walk is
+// conflict-free) before computing the current one, arriving on the buffer's
+// mbarrier with its byte count — no CTA barrier in the loop, ~2 tiles in flight
+// per block, 3 blocks per SM.
+template <int D>
+__global__ void __launch_bounds__(kCuRows) closest_bulk_kernel(
+    const double* __restrict__ x, int64_t n, const double* __restrict__ c,
+    double* __restrict__ closest, int init, double* __restrict__ part,
+    double* __restrict__ total, unsigned* __restrict__ done, double* __restrict__ wsum) {
+  constexpr int kPitch = D * 8 + 16;  // bytes per staged row
+  extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ double sc[D];
+  __shared__ double red[kCuRows / 32];
+  const int t = threadIdx.x;
+  if (t < D) sc[t] = c[t];
+  if (t == 0) {
+    mbar_init(&bar[0], kCuRows);
+    mbar_init(&bar[1], kCuRows);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t n_tiles = (n + kCuRows - 1) / kCuRows;
+  auto issue = [&](int64_t tile, int b) {  // this thread's row of `tile` → buffer b
+    const int64_t i = tile * kCuRows + t;
+    if (i < n) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // WAR vs the last reads
+      mbar_arrive_expect_tx(&bar[b], (uint32_t)(D * 8));
+      bulk_g2s(sm + (size_t)(b * kCuRows + t) * kPitch, x + i * D, (uint32_t)(D * 8), &bar[b]);
+    } else {
+      mbar_arrive(&bar[b]);
+    }
+  };
+  double acc = 0.0;
+  uint32_t ph[2] = {0, 0};
+  int b = 0;
+  if ((int64_t)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, b ^= 1) {
+    const int64_t next = tile + gridDim.x;
+    if (next < n_tiles) issue(next, b ^ 1);
+    const int64_t i = tile * kCuRows + t;
+    const double old = (i < n && !init) ? closest[i] : 0.0;
+    mbar_wait(&bar[b], ph[b]);
+    ph[b] ^= 1;
+    double nv = 0.0;
+    if (i < n) {
+      double v[D];
+      const double2* row = reinterpret_cast<const double2*>(sm + (size_t)(b * kCuRows + t) * kPitch);
+#pragma unroll
+      for (int k = 0; k < D / 2; ++k) {
+        const double2 q = row[k];
+        v[2 * k] = q.x;
+        v[2 * k + 1] = q.y;
+      }
+      const double dist = pw_sq_fixed<D>(v, sc);
+      nv = init ? dist : fmin(old, dist);
+      closest[i] = nv;
+      acc += nv;
+    }
+    // per-warp partial of this tile (32 consecutive points) for pick_kernel
+    const double ws = warp_sum_d(nv);
+    if ((t & 31) == 0) wsum[tile * (kCuRows / 32) + (t >> 5)] = ws;
+  }
+  acc = warp_sum_d(acc);
+  if ((t & 31) == 0) red[t >> 5] = acc;
+  __syncthreads();
+  __shared__ bool last;
+  if (t == 0) {
+    double v = 0.0;
+    for (int w = 0; w < kCuRows / 32; ++w) v += red[w];
+    part[blockIdx.x] = v;
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {  // the total over the partials in a fixed order (sum_parts_kernel's fold)
+    __threadfence();
+    double v = 0.0;
+    for (int i = t; i < (int)gridDim.x; i += kCuRows) v += __ldcg(part + i);
+    v = warp_sum_d(v);
+    if ((t & 31) == 0) red[t >> 5] = v;
+    __syncthreads();
+    if (t == 0) {
+      double r = 0.0;
+      for (int w = 0; w < kCuRows / 32; ++w) r += red[w];
+      *total = r;
+      *done = 0;  // ready for the next launch on this workspace
+    }
+  }
+}
+
+bool closest_is_bulk(const double* x, int d) {
+  return (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (d == 24 || d == 32);
+}
+
+// the next k-means++ centre from the last bulk closest update's per-warp
+// partials (wsum, W = 4 per 128-point tile): first j with C_j > u·C_last,
+// C the prefix sums of closest (cdf[j] / cdf[n-1] > u, the reference's
+// searchsorted on the normalised CDF; like the scan path, the prefix order is
+// parallel — warp partials, a fixed-order block scan, then the 32 points of
+// the crossing warp in sequence); writes the centre row.  A zero total is the
+// reference's other RNG branch: record the step, leave the centre.
+__global__ void __launch_bounds__(1024) pick_kernel(
+    const double* __restrict__ wsum, int64_t W, const double* __restrict__ closest, int64_t n,
+    double u, const double* __restrict__ total, int32_t* __restrict__ zero_step, int step,
+    const double* __restrict__ x, int d, double* __restrict__ center) {
+  // three levels, every load coalesced: super-chunks of 1024 warp partials
+  // (one warp each), their 32 sub-chunks of 32 (one warp each), then 32
+  // partials and 32 points in sequence; a level whose partial sums round
+  // short of the threshold falls back to its last element
+  __shared__ double s_sum[32];
+  __shared__ int64_t s_c, s_k;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (!(*total > 0.0)) {
+    if (t == 0 && zero_step) atomicMin(zero_step, step);
+    return;
+  }
+  const int64_t n_super = (W + 1023) / 1024;
+  // level 1: super-chunk sums, then the crossing super-chunk (thread 0, in order)
+  double thr = 0.0, base = 0.0;
+  {
+    constexpr int kKeep = 128;  // super-chunk sums kept from the first pass (n ≤ 4 M points)
+    __shared__ double s_super[32], s_keep[kKeep];
+    __shared__ double s_thr, s_base;
+    double run_all = 0.0;
+    for (int64_t c0 = 0; c0 < n_super; c0 += 32) {  // ≤ 32 super-chunks per pass
+      const int64_t c = c0 + warp;
+      double v = 0.0;
+      if (c < n_super)
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int64_t i = c * 1024 + k * 32 + lane;
+          v += i < W ? wsum[i] : 0.0;
+        }
+      v = warp_sum_d(v);
+      if (lane == 0) {
+        s_super[warp] = v;
+        if (c < kKeep) s_keep[c] = v;
+      }
+      __syncthreads();
+      if (t == 0) {
+        for (int w = 0; w < 32 && c0 + w < n_super; ++w) run_all += s_super[w];
+        s_sum[0] = run_all;
+      }
+      __syncthreads();
+    }
+    if (t == 0) {
+      s_thr = u * s_sum[0];
+      s_c = n_super - 1;
+    }
+    __syncthreads();
+    thr = s_thr;
+    double run = 0.0;
+    bool found = false;
+    if (n_super <= kKeep) {  // the crossing from the kept sums (same values, same order)
+      if (t == 0) {
+        for (int64_t c1 = 0; c1 < n_super; ++c1) {
+          if (run + s_keep[c1] > thr) {
+            s_c = c1;
+            found = true;
+            break;
+          }
+          run += s_keep[c1];
+        }
+        s_base = run;
+      }
+      found = true;  // s_base set (the last super-chunk on a rounding miss)
+    }
+    // otherwise a second pass over the super-chunk sums (recomputed
+    // identically: same loads, same order)
+    for (int64_t c0 = 0; c0 < n_super && !found; c0 += 32) {
+      const int64_t c = c0 + warp;
+      double v = 0.0;
+      if (c < n_super)
+        for (int k = 0; k < 32; ++k) {
+          const int64_t i = c * 1024 + k * 32 + lane;
+          v += i < W ? wsum[i] : 0.0;
+        }
+      v = warp_sum_d(v);
+      if (lane == 0) s_super[warp] = v;
+      __syncthreads();
+      if (t == 0) {
+        for (int w = 0; w < 32 && c0 + w < n_super; ++w) {
+          if (run + s_super[w] > thr) {
+            s_c = c0 + w;
+            found = true;
+            break;
+          }
+          run += s_super[w];
+        }
+        s_base = run;
+        s_sum[1] = found ? 1.0 : 0.0;
+      }
+      __syncthreads();
+      found = s_sum[1] != 0.0;
+      __syncthreads();
+    }
+    if (t == 0 && !found) s_base = run;  // rounding: the last super-chunk
+    __syncthreads();
+    base = s_base;
+  }
+  // level 2: the 32 sub-chunks of the crossing super-chunk (warp k sums sub-chunk k)
+  const int64_t c = s_c;
+  {
+    const int64_t i = c * 1024 + warp * 32 + lane;
+    double v = i < W ? wsum[i] : 0.0;
+    v = warp_sum_d(v);
+    if (lane == 0) s_sum[warp] = v;
+    __syncthreads();
+    if (t == 0) {
+      double run = base;
+      int64_t k = 31;
+      for (int w = 0; w < 32; ++w) {
+        if (run + s_sum[w] > thr) {
+          k = w;
+          break;
+        }
+        run += s_sum[w];
+      }
+      s_k = c * 1024 + k * 32;  // first warp partial of the sub-chunk
+      s_sum[0] = run;           // prefix before it (level-3 base)
+    }
+    __syncthreads();
+  }
+  // level 3 (warp 0): 32 partials in sequence, then 32 points in sequence
+  if (warp == 0) {
+    const int64_t i0 = s_k;
+    const double pv = i0 + lane < W ? wsum[i0 + lane] : 0.0;
+    double run = s_sum[0];
+    int64_t wi = -1;
+    for (int k = 0; k < 32; ++k) {
+      const double v = __shfl_sync(0xffffffffu, pv, k);
+      if (wi < 0 && i0 + k < W) {
+        if (run + v > thr) wi = i0 + k;
+        else run += v;
+      }
+    }
+    if (wi < 0) wi = (i0 + 31 < W ? i0 + 31 : W - 1);  // rounding: the last partial
+    const int64_t r0 = wi * 32;
+    const double cv = r0 + lane < n ? closest[r0 + lane] : 0.0;
+    int64_t j = -1;
+    for (int k = 0; k < 32; ++k) {
+      const double v = __shfl_sync(0xffffffffu, cv, k);
+      if (j < 0 && r0 + k < n) {
+        run += v;
+        if (run > thr) j = r0 + k;
+      }
+    }
+    if (j < 0) j = (r0 + 31 < n ? r0 + 31 : n - 1);
+    if (lane == 0) s_k = j;
+  }
+  __syncthreads();
+  const int64_t j = s_k;
+  for (int k = t; k < d; k += 1024) center[k] = x[j * d + k];
+}
+
+// closest update + the total Σ closest → *total (done: a zeroed counter the
+// bulk kernel leaves zeroed; wsum: per-warp partials for pick_kernel)
+cudaError_t launch_closest(const double* x, int64_t n, int d, const double* c, double* closest,
+                           int init, double* part, double* total, unsigned* done,
+                           double* wsum, cudaStream_t stream) {
+  const int64_t tiles = (n + kCuRows - 1) / kCuRows;
+  if (closest_is_bulk(x, d)) {
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 3 * kNumSMs));
+    const int smem = 2 * kCuRows * (d * 8 + 16);
+    cudaError_t e;
+    if (d == 32) {
+      e = cudaFuncSetAttribute(closest_bulk_kernel<32>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      closest_bulk_kernel<32><<<g, kCuRows, smem, stream>>>(x, n, c, closest, init, part, total,
+                                                             done, wsum);
+    } else {
+      e = cudaFuncSetAttribute(closest_bulk_kernel<24>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      closest_bulk_kernel<24><<<g, kCuRows, smem, stream>>>(x, n, c, closest, init, part, total,
+                                                             done, wsum);
+    }
+    return cudaGetLastError();
+  }
+  const int g = closest_grid(n);
+  cudaError_t e = prep_closest(d);
+  if (e != cudaSuccess) return e;
+  closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(x, n, d, c, closest, init, part);
+  sum_parts_kernel<<<1, 1024, 0, stream>>>(part, g, total);
+  return cudaGetLastError();
+}
+
 int grid_for(int64_t n, int block = 256) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((n + block - 1) / block, kNumSMs * 16));
 }
@@ -486,11 +779,10 @@ extern "C" int tpcb_kmeanspp_init(const double* d_x, int64_t n, int32_t d, int64
   if (first < 0 || first >= n || d > kMaxDim) return TPCB_ERR_VALIDATION;
   cudaStream_t stream = (cudaStream_t)stream_;
   KWs w = carve(ws, ws_bytes, n, 1);
+  TPCB_CUDA_CHECK(cudaMemsetAsync(w.flag, 0, 4, stream));  // launch_closest's counter
   set_center_direct_kernel<<<1, 128, 0, stream>>>(d_x, d, first, d_centers);
-  const int g = closest_grid(n);
-  TPCB_CUDA_CHECK(prep_closest(d));
-  closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(d_x, n, d, d_centers, d_closest, 1, w.part);
-  sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
+  TPCB_CUDA_CHECK(launch_closest(d_x, n, d, d_centers, d_closest, 1, w.part, d_total,
+                                 reinterpret_cast<unsigned*>(w.flag), w.p, stream));
   TPCB_LAUNCH_CHECK("kmeanspp_init");
   return TPCB_OK;
 }
@@ -503,6 +795,7 @@ extern "C" int tpcb_kmeanspp_step(const double* d_x, int64_t n, int32_t d, int32
   if (d > kMaxDim) return TPCB_ERR_UNSUPPORTED;
   cudaStream_t stream = (cudaStream_t)stream_;
   KWs w = carve(ws, ws_bytes, n, 1);
+  TPCB_CUDA_CHECK(cudaMemsetAsync(w.flag, 0, 4, stream));  // launch_closest's counter
   double* center = d_centers + (size_t)i * d;
   if (u >= 0.0) {
     size_t tb = w.tmp_bytes;  // cdf of p = closest / total, the division fused into the scan
@@ -514,10 +807,8 @@ extern "C" int tpcb_kmeanspp_step(const double* d_x, int64_t n, int32_t d, int32
     if (direct < 0 || direct >= n) return TPCB_ERR_VALIDATION;
     set_center_direct_kernel<<<1, 128, 0, stream>>>(d_x, d, direct, center);
   }
-  const int g = closest_grid(n);
-  TPCB_CUDA_CHECK(prep_closest(d));
-  closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(d_x, n, d, center, d_closest, 0, w.part);
-  sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
+  TPCB_CUDA_CHECK(launch_closest(d_x, n, d, center, d_closest, 0, w.part, d_total,
+                                 reinterpret_cast<unsigned*>(w.flag), w.p, stream));
   TPCB_LAUNCH_CHECK("kmeanspp_step");
   return TPCB_OK;
 }
@@ -538,18 +829,23 @@ extern "C" int tpcb_kmeanspp_steps(const double* d_x, int64_t n, int32_t d, int3
   if (i0 < 1 || i1 < i0) return TPCB_ERR_VALIDATION;
   cudaStream_t stream = (cudaStream_t)stream_;
   KWs w = carve(ws, ws_bytes, n, 1);
-  const int g = closest_grid(n);
-  TPCB_CUDA_CHECK(prep_closest(d));
+  TPCB_CUDA_CHECK(cudaMemsetAsync(w.flag, 0, 4, stream));  // launch_closest's counter
   for (int i = i0; i < i1; ++i) {
     double* center = d_centers + (size_t)i * d;
-    size_t tb = w.tmp_bytes;
-    TPCB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(w.tmp, tb, p_iter(d_closest, d_total), w.cdf,
-                                                  (int)n, stream));
-    search_kernel<<<1, 32, 0, stream>>>(w.cdf, n, h_u[i - i0], w.found, d_total, d_zero_step, i);
-    set_center_kernel<<<1, 128, 0, stream>>>(d_x, d, w.found, n, center, nullptr);
-    closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(d_x, n, d, center, d_closest,
-                                                                     0, w.part);
-    sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
+    if (closest_is_bulk(d_x, d)) {  // one launch: search + centre (w.p: the warp partials)
+      const int64_t W = (n + kCuRows - 1) / kCuRows * (kCuRows / 32);
+      pick_kernel<<<1, 1024, 0, stream>>>(w.p, W, d_closest, n, h_u[i - i0], d_total,
+                                          d_zero_step, i, d_x, d, center);
+    } else {
+      size_t tb = w.tmp_bytes;
+      TPCB_CUDA_CHECK(cub::DeviceScan::InclusiveSum(w.tmp, tb, p_iter(d_closest, d_total),
+                                                    w.cdf, (int)n, stream));
+      search_kernel<<<1, 32, 0, stream>>>(w.cdf, n, h_u[i - i0], w.found, d_total, d_zero_step,
+                                          i);
+      set_center_kernel<<<1, 128, 0, stream>>>(d_x, d, w.found, n, center, nullptr);
+    }
+    TPCB_CUDA_CHECK(launch_closest(d_x, n, d, center, d_closest, 0, w.part, d_total,
+                                   reinterpret_cast<unsigned*>(w.flag), w.p, stream));
   }
   TPCB_LAUNCH_CHECK("kmeanspp_steps");
   return TPCB_OK;
@@ -626,11 +922,9 @@ extern "C" int tpcb_kmeanspp_closest(const double* d_x, int64_t n, int32_t d,
   if (d > kMaxDim) return TPCB_ERR_UNSUPPORTED;
   cudaStream_t stream = (cudaStream_t)stream_;
   KWs w = carve(ws, ws_bytes, n, 1);
-  const int g = closest_grid(n);
-  TPCB_CUDA_CHECK(prep_closest(d));
-  closest_update_kernel<<<g, kCuRows, closest_smem(d), stream>>>(d_x, n, d, d_center, d_closest, init ? 1 : 0,
-                                               w.part);
-  sum_parts_kernel<<<1, 1024, 0, stream>>>(w.part, g, d_total);
+  TPCB_CUDA_CHECK(cudaMemsetAsync(w.flag, 0, 4, stream));  // launch_closest's counter
+  TPCB_CUDA_CHECK(launch_closest(d_x, n, d, d_center, d_closest, init ? 1 : 0, w.part, d_total,
+                                 reinterpret_cast<unsigned*>(w.flag), w.p, stream));
   TPCB_LAUNCH_CHECK("kmeanspp_closest");
   return TPCB_OK;
 }
