@@ -46,8 +46,10 @@ __device__ __forceinline__ void cmd_bar(int bar_id, int nthr) {
 // Second half of the CMD statistics once lo/hi/amin/amax/mus/mut/s and the
 // central moments ms/mt are in `cs`: the per-order norms, the support
 // gradient and the value (costmodel.py:440-476).  Whole group participates.
+// spow (optional): spow[j * de + c] = pow(|s_c|, j) for j = 2..K, precomputed
+// in parallel (the same pow calls, so the same values)
 static __device__ __noinline__ double cmd_finish(double* cs, int de, int K, int bar_id,
-                                                 int nthr) {
+                                                 int nthr, const double* spow = nullptr) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int KM = kMaxCmdOrder + 1;
   double* mus = cs + 2 * de;
@@ -73,7 +75,8 @@ static __device__ __noinline__ double cmd_finish(double* cs, int de, int K, int 
       double a2 = 0.0;
       for (int c = lane; c < de; c += 32) {
         const double sc = fabs(s[c]);
-        const double v = (ms[j * de + c] - mt[j * de + c]) / pow(sc, (double)j);
+        const double v = (ms[j * de + c] - mt[j * de + c]) /
+                         (spow ? spow[j * de + c] : pow(sc, (double)j));
         a2 += v * v;
       }
       a2 = warp_sum_d(a2);
@@ -88,7 +91,8 @@ static __device__ __noinline__ double cmd_finish(double* cs, int de, int K, int 
     if (norms[1] > 0.0) d -= (u[c] / norms[1]) * u[c] / sc;
     for (int j = 2; j <= K; ++j) {
       if (norms[j] > 0.0) {
-        const double v = (ms[j * de + c] - mt[j * de + c]) / pow(sc, (double)j);
+        const double v = (ms[j * de + c] - mt[j * de + c]) /
+                         (spow ? spow[j * de + c] : pow(sc, (double)j));
         d -= j * (v / norms[j]) * v / sc;
       }
     }
