@@ -208,3 +208,36 @@ def test_kmeanspp_zero_total_replay():
         km.kmeanspp(got_rng)
         np.testing.assert_array_equal(km.centers.cpu().numpy(), want)
         assert got_rng.random() == want_rng.random()  # identical stream position
+
+
+@pytest.mark.parametrize("d,n", [(32, 100_003), (24, 65_537), (16, 40_000)])
+def test_kmeanspp_fused_pick_matches_scan_path(d, n):
+    """k-means++ through tpcb_kmeanspp_steps (for d 24 / 32: the bulk-copy
+    closest update + the one-launch CDF pick) against the same seeding step by
+    step through tpcb_kmeanspp_step (CUB scan + search): identical centres.
+    The two prefix orders differ, so a draw could differ only for a uniform
+    within rounding of a CDF step; n not a multiple of 32 / 128 exercises the
+    ragged last warp and tile."""
+    import ctypes as C
+    s = _s()
+    from paper_2311_09690_b200 import _lib
+    rng = np.random.default_rng(5)
+    x = rng.normal(loc=rng.normal(scale=3, size=(8, d))[rng.integers(0, 8, n)], size=(n, d))
+    k = 48
+    a = s.DeviceKMeans(x, k)
+    a.kmeanspp(np.random.default_rng(9))
+    b = s.DeviceKMeans(x, k)
+    r = np.random.default_rng(9)
+    first = int(r.integers(0, n))
+    lib = b.lib
+    _lib.check(lib.tpcb_kmeanspp_init(b.x.data_ptr(), n, d, first, b.centers.data_ptr(),
+                                      b.closest.data_ptr(), b.total.data_ptr(), b.ws.ptr,
+                                      b.ws.size, b.s()), "init")
+    for i in range(1, k):
+        assert float(b.total.item()) > 0.0
+        _lib.check(lib.tpcb_kmeanspp_step(b.x.data_ptr(), n, d, i, float(r.random()), -1,
+                                          b.centers.data_ptr(), b.closest.data_ptr(),
+                                          b.total.data_ptr(), None, b.ws.ptr, b.ws.size,
+                                          b.s()), "step")
+    assert np.array_equal(a.centers.cpu().numpy(), b.centers.cpu().numpy())
+    assert np.array_equal(a.closest.cpu().numpy(), b.closest.cpu().numpy())

@@ -171,10 +171,12 @@ def test_cmd_grid_kernels_vs_oracle_large_sets():
     zt = rng.normal(0.2, 1.3, size=(nt, 32))
     zs[5, 3] = zs[17, 3] = 9.0   # tie on the max: first row (5) carries the support grad
     zt[100, 7] = -9.0
-    for k in (5, 3):
-        v, gs, gt = cmd_grad(zs, zt, k)
-        wv, wgs, wgt = om.cmd_grad(zs, zt, k)
-        assert v == pytest.approx(wv, rel=1e-11)
+    # k 3 / 4 / 5: compile-time orders of pass AC; 2 and 7: the runtime-order
+    # pass AC; de 24: the generic (shared-memory coefficient) pass E
+    for k, de in ((5, 32), (3, 32), (2, 32), (7, 32), (5, 24), (4, 24)):
+        v, gs, gt = cmd_grad(zs[:, :de], zt[:, :de], k)
+        wv, wgs, wgt = om.cmd_grad(zs[:, :de], zt[:, :de], k)
+        assert v == pytest.approx(wv, rel=1e-11), (k, de)
         np.testing.assert_allclose(gs, wgs, rtol=1e-7, atol=1e-13)
         np.testing.assert_allclose(gt, wgt, rtol=1e-7, atol=1e-13)
     big = rng.normal(size=(CMD_GRID_ROWS, 32))
