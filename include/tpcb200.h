@@ -45,7 +45,7 @@ typedef enum {
 #define TPCB_MAX_LEAF 16
 #define TPCB_MAX_DEC 8
 #define TPCB_FEAT 24      /* computation-vector width, features.py:18 */
-#define TPCB_FEAT_PAD 32  /* packed row stride (128-byte rows) */
+#define TPCB_FEAT_PAD 24  /* packed row stride (96-byte rows, 16-byte aligned) */
 #define TPCB_DEV_FEAT 6   /* device-vector width, costmodel.py:28 */
 
 /* CostModelConfig (costmodel.py:36-57), architecture fields only */

@@ -17,7 +17,7 @@ LIB_PATH = Path(os.environ.get("TPCB_LIB_PATH") or
                 Path(__file__).resolve().parent / "libtpcb200.so")  # (env: A/B experiments)
 
 MAX_LAYERS, MAX_LEAF, MAX_DEC = 16, 16, 8
-FEAT, FEAT_PAD, DEV_FEAT = 24, 32, 6
+FEAT, FEAT_PAD, DEV_FEAT = 24, 24, 6
 
 vp = C.c_void_p
 i32, i64, f64 = C.c_int32, C.c_int64, C.c_double

@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
     for (int i = threadIdx.x; i < kPeSmem * TPCB_FEAT; i += kPackThreads) pe_s[i] = pe_table[i];
     __syncthreads();
   }
-  constexpr int kChunks = TPCB_FEAT_PAD / 4;  // 8 float4 per packed row
+  constexpr int kChunks = TPCB_FEAT_PAD / 4;  // 6 float4 per packed row
   const int rshift = R == 32 ? 5 : (R == 64 ? 6 : 7);
   const int64_t rows = (int64_t)(*n_tiles) << rshift;
   for (int64_t base = (int64_t)blockIdx.x * kPackThreads; base < rows;
@@ -315,14 +315,12 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
     }
     float4* my = reinterpret_cast<float4*>(stage + threadIdx.x * kStagePitch);
 #pragma unroll
-    for (int q = 0; q < 6; ++q) my[q] = out[q];
-    my[6] = make_float4(0.f, 0.f, 0.f, 0.f);
-    my[7] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < kChunks; ++q) my[q] = out[q];
     __syncthreads();
     const int n_rows = rows - base < kPackThreads ? (int)(rows - base) : kPackThreads;
     float4* dst = reinterpret_cast<float4*>(x) + base * kChunks;
     for (int e = threadIdx.x; e < n_rows * kChunks; e += kPackThreads) {
-      const int rr = e >> 3, ch = e & 7;
+      const int rr = e / kChunks, ch = e - rr * kChunks;
       dst[e] = reinterpret_cast<const float4*>(stage + rr * kStagePitch)[ch];
     }
     __syncthreads();

@@ -382,7 +382,7 @@ __global__ void gather_tokens_kernel(const float* __restrict__ px, const int32_t
   const int t0 = tok_off[s], L = tok_off[s + 1] - t0;
   const int r0 = ast_row[perm[s]];
   for (int l = 0; l < L; ++l) {
-    const float v = px[(size_t)(r0 + l) * 32 + lane];
+    const float v = lane < TPCB_FEAT ? px[(size_t)(r0 + l) * TPCB_FEAT_PAD + lane] : 0.f;
     const float h = tf32_hi(v);
     x_hi[(size_t)(t0 + l) * 32 + lane] = h;
     x_lo[(size_t)(t0 + l) * 32 + lane] = v - h;

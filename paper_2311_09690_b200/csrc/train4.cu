@@ -290,7 +290,7 @@ __device__ __noinline__ void act_store(const WgradDev& wg, int op, const float* 
   for (int e = threadIdx.x; e < n; e += NT) {
     const int f = e / Ls, r = e - f * Ls;
     float v = 0.f;
-    if (r < L) {
+    if (r < L && f < ldx) {  // f ≥ ldx: the K padding of a narrower operand (X0)
       v = X[r * ldx + f];
       if (ga) v = fmaf(ga[f], v, ba[f]);
     }
@@ -1396,7 +1396,7 @@ __global__ void __launch_bounds__(kThreads4, 1) train4_kernel(
       PT(60 + (NLAY - 1 - li) * 30 + 23);
     }
     if (use_wg) {
-      act_store(wg, kWgX0, X0, LDX, nullptr, nullptr, L, Ls, LDX, w);
+      act_store(wg, kWgX0, X0, LDX, nullptr, nullptr, L, Ls, 32, w);  // K padded to 32
       act_store(wg, kWgDH, dH, LDH, nullptr, nullptr, L, Ls, D, w);
     } else {
       wgrad(X0, LDX, nullptr, nullptr, dH, LDH, L, FEAT, D, G + M.inW, fs);

@@ -62,11 +62,11 @@ def test_featurize_pack_contract(R, dtype):
     assert np.array_equal(pk.ast_row.cpu().numpy(), want["ast_row"])
     row_ast = pk.row_ast[:nt * R].cpu().numpy().reshape(nt, R)
     assert np.array_equal(row_ast, want["row_ast"])
-    x = pk.x[:nt * R * 32].cpu().numpy().reshape(nt, R, 32).astype(np.float64)
-    err = np.abs(x - want["tiles"])
+    x = pk.x[:nt * R * 24].cpu().numpy().reshape(nt, R, 24).astype(np.float64)
+    assert np.all(want["tiles"][..., 24:] == 0.0)  # the oracle's pad columns (no longer stored)
+    err = np.abs(x - want["tiles"][..., :24])
     assert err.max() <= 4e-6, err.max()
     assert np.all(x[want["row_mask"] == 0] == 0.0)
-    assert np.all(x[..., 24:] == 0.0)
 
 
 def test_positional_encoding_matches_reference():
