@@ -147,19 +147,24 @@ __global__ void bucket_scatter_kernel(const int64_t* __restrict__ leaf_off, int6
   __shared__ int warp_cnt[kScatterBlock / 32][kMaxL + 1];
   __shared__ int bucket_off[kMaxL + 2], tile_off[kMaxL + 2];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {  // bucket and tile offsets from the bucket sizes
-    int b = 0, t = 0;
-    for (int L = 1; L <= n_leaf_max; ++L) {
-      bucket_off[L] = b;
-      tile_off[L] = t;
-      const int c = cnt[L], A = R / L;
-      b += c;
-      t += (c + A - 1) / A;
+  if (w == 0) {  // bucket and tile offsets from the bucket sizes: lane L, warp scans
+    const int L = lane;
+    const int c = (L >= 1 && L <= n_leaf_max) ? cnt[L] : 0;
+    const int tl = (L >= 1 && L <= n_leaf_max) ? (c + R / L - 1) / (R / L) : 0;
+    int b = c, t = tl;  // inclusive prefix over lanes 1..L
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int bb = __shfl_up_sync(0xffffffffu, b, o), tt = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) {
+        b += bb;
+        t += tt;
+      }
     }
-    bucket_off[0] = tile_off[0] = 0;
-    bucket_off[n_leaf_max + 1] = b;
-    tile_off[n_leaf_max + 1] = t;
-    if (blockIdx.x == 0) *n_tiles_out = t < n_tiles_max ? t : n_tiles_max;
+    if (L <= n_leaf_max + 1) {  // exclusive prefix = offset of bucket L
+      bucket_off[L] = b - c;
+      tile_off[L] = t - tl;
+    }
+    if (L == n_leaf_max && blockIdx.x == 0) *n_tiles_out = t < n_tiles_max ? t : n_tiles_max;
   }
   __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x <= n_leaf_max + 1)
@@ -244,75 +249,92 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
   constexpr int kChunks = TPCB_FEAT_PAD / 4;  // 6 float4 per packed row
   const int rshift = R == 32 ? 5 : (R == 64 ? 6 : 7);
   const int64_t rows = (int64_t)(*n_tiles) << rshift;
-  for (int64_t base = (int64_t)blockIdx.x * kPackThreads; base < rows;
-       base += (int64_t)gridDim.x * kPackThreads) {
-    const int64_t gr = base + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * kPackThreads;
+  // the row header (tile record + row → token, then token → position) of the
+  // NEXT row is loaded while this row's vector is fetched: the two dependent
+  // header levels overlap the third instead of preceding it
+  struct Hdr {
+    int live;  // 1: a real row, 0: a pad row of a tile, -1: past the end
+    int tok;
+  };
+  auto header = [&](int64_t g) {
+    Hdr h{-1, 0};
+    if (g < rows) {
+      const int t = (int)(g >> rshift), r = (int)(g & (R - 1));
+      const int L = tile_L[t], cnt = tile_count[t];
+      const int tok_r = row_tok[g];  // in flight with the tile record
+      h.live = r / L < cnt ? 1 : 0;
+      h.tok = tok_r;
+    }
+    return h;
+  };
+  int64_t gr = (int64_t)blockIdx.x * kPackThreads + threadIdx.x;
+  Hdr cur = header(gr);
+  int ipos = (PE && cur.live == 1) ? ordering[cur.tok] : 0;
+  for (int64_t base = (int64_t)blockIdx.x * kPackThreads; base < rows; base += stride) {
+    const Hdr nxt = header(gr + stride);
     float4 out[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) out[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gr < rows) {
-      const int t = (int)(gr >> rshift), r = (int)(gr & (R - 1));
-      const int L = tile_L[t], cnt = tile_count[t];
-      const int tok_r = row_tok[gr];  // in flight with the tile record
-      if (r / L < cnt) {
-        const int64_t tok = tok_r;
-        const int ipos = PE ? ordering[tok] : 0;
-        const bool table = ipos >= 0 && ipos < kPeRows;
-        // two halves of 12 columns: half the live registers, 3-6 loads in flight each
+    if (cur.live == 1) {
+      const int64_t tok = cur.tok;
+      const bool table = ipos >= 0 && ipos < kPeRows;
+      // two halves of 12 columns: half the live registers, 3-6 loads in flight each
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double v[12];
-          if (F64) {
-            const double2* src = reinterpret_cast<const double2*>(
-                static_cast<const double*>(vectors_) + tok * TPCB_FEAT + h * 12);
+      for (int h = 0; h < 2; ++h) {
+        double v[12];
+        if (F64) {
+          const double2* src = reinterpret_cast<const double2*>(
+              static_cast<const double*>(vectors_) + tok * TPCB_FEAT + h * 12);
+#pragma unroll
+          for (int q = 0; q < 6; ++q) {
+            const double2 p = __ldg(src + q);
+            v[2 * q] = p.x;
+            v[2 * q + 1] = p.y;
+          }
+        } else {
+          const float4* src = reinterpret_cast<const float4*>(
+              static_cast<const float*>(vectors_) + tok * TPCB_FEAT + h * 12);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const float4 p = __ldg(src + q);
+            v[4 * q] = p.x; v[4 * q + 1] = p.y; v[4 * q + 2] = p.z; v[4 * q + 3] = p.w;
+          }
+        }
+        if (PE) {  // column 2δ: sin(pos/θ^(2δ/24)); 2δ+1: cos (features.py:255-262)
+          if (ipos >= 0 && ipos < kPeSmem) {  // shared-memory rows
+            const double2* tp =
+                reinterpret_cast<const double2*>(pe_s + ipos * TPCB_FEAT + h * 12);
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
-              const double2 p = __ldg(src + q);
-              v[2 * q] = p.x;
-              v[2 * q + 1] = p.y;
+              const double2 p = tp[q];
+              v[2 * q] += p.x;
+              v[2 * q + 1] += p.y;
+            }
+          } else if (table) {  // table row (L1/L2 resident)
+            const double2* tp =
+                reinterpret_cast<const double2*>(pe_table + ipos * TPCB_FEAT + h * 12);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+              const double2 p = __ldg(tp + q);
+              v[2 * q] += p.x;
+              v[2 * q + 1] += p.y;
             }
           } else {
-            const float4* src = reinterpret_cast<const float4*>(
-                static_cast<const float*>(vectors_) + tok * TPCB_FEAT + h * 12);
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-              const float4 p = __ldg(src + q);
-              v[4 * q] = p.x; v[4 * q + 1] = p.y; v[4 * q + 2] = p.z; v[4 * q + 3] = p.w;
-            }
+            for (int q = 0; q < 12; ++q) v[q] += pe_term((double)ipos, den.v[h * 6 + q / 2], q & 1);
           }
-          if (PE) {  // column 2δ: sin(pos/θ^(2δ/24)); 2δ+1: cos (features.py:255-262)
-            if (ipos >= 0 && ipos < kPeSmem) {  // shared-memory rows
-              const double2* tp =
-                  reinterpret_cast<const double2*>(pe_s + ipos * TPCB_FEAT + h * 12);
-#pragma unroll
-              for (int q = 0; q < 6; ++q) {
-                const double2 p = tp[q];
-                v[2 * q] += p.x;
-                v[2 * q + 1] += p.y;
-              }
-            } else if (table) {  // table row (L1/L2 resident)
-              const double2* tp =
-                  reinterpret_cast<const double2*>(pe_table + ipos * TPCB_FEAT + h * 12);
-#pragma unroll
-              for (int q = 0; q < 6; ++q) {
-                const double2 p = __ldg(tp + q);
-                v[2 * q] += p.x;
-                v[2 * q + 1] += p.y;
-              }
-            } else {
-#pragma unroll
-              for (int q = 0; q < 12; ++q) v[q] += pe_term((double)ipos, den.v[h * 6 + q / 2], q & 1);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 3; ++q)
-            out[3 * h + q] = make_float4((float)v[4 * q], (float)v[4 * q + 1],
-                                         (float)v[4 * q + 2], (float)v[4 * q + 3]);
         }
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          out[3 * h + q] = make_float4((float)v[4 * q], (float)v[4 * q + 1],
+                                       (float)v[4 * q + 2], (float)v[4 * q + 3]);
       }
-      else
-        row_ast[gr] = -1;  // pad row (real rows were written by bucket_scatter)
+    } else if (cur.live == 0) {
+      row_ast[gr] = -1;  // pad row (real rows were written by bucket_scatter)
     }
+    // the next row's position (its token arrived during this row's loads)
+    const int ipos_n = (PE && nxt.live == 1) ? ordering[nxt.tok] : 0;
     float4* my = reinterpret_cast<float4*>(stage + threadIdx.x * kStagePitch);
 #pragma unroll
     for (int q = 0; q < kChunks; ++q) my[q] = out[q];
@@ -324,6 +346,9 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
       dst[e] = reinterpret_cast<const float4*>(stage + rr * kStagePitch)[ch];
     }
     __syncthreads();
+    cur = nxt;
+    ipos = ipos_n;
+    gr += stride;
   }
 }
 
