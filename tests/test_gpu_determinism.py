@@ -39,7 +39,8 @@ def test_forward_and_pack_bitwise_repeatable():
     st = engine.Status(rows.device)
     a = engine.pack(rows, ordering, leaf_off, rag.n_ast, 16, False, st, 128)
     nt = int(a.n_tiles.item())
-    used = nt * 128 * 32  # tiles the plan uses (the buffer tail is never read)
+    from paper_2311_09690_b200 import _lib
+    used = nt * 128 * _lib.FEAT_PAD  # tiles the plan uses (the buffer tail is never read)
     for _ in range(3):
         b = engine.pack(rows, ordering, leaf_off, rag.n_ast, 16, False, st, 128)
         assert int(b.n_tiles.item()) == nt
