@@ -312,6 +312,55 @@ __global__ void prep_weights_kernel(const Model M, const float* __restrict__ P,
   }
 }
 
+// attention of one query row over its AST's LL keys (head columns hc..hc+31
+// of the K|V rows), LL a compile-time count: every score first (independent
+// dot products, registers), then the weights and the context
+template <int LL>
+__device__ __forceinline__ void attn_fixed(const uint8_t* __restrict__ sKV, int r0, int hc,
+                                           const float* q, float scale, float* c) {
+  float sc[LL];
+#pragma unroll
+  for (int j = 0; j < LL; ++j) {
+    const uint4* kr = reinterpret_cast<const uint4*>(sKV + ((r0 + j) * kKVLd + hc) * 2);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < DH / 8; ++i) {
+      const uint4 u = kr[i];
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+        acc[e] = fmaf(q[8 * i + 2 * e], kf.x, fmaf(q[8 * i + 2 * e + 1], kf.y, acc[e]));
+      }
+    }
+    sc[j] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) * scale;
+  }
+  float m = sc[0];
+#pragma unroll
+  for (int j = 1; j < LL; ++j) m = fmaxf(m, sc[j]);
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < LL; ++j) {
+    const float pj = LL == 1 ? 1.f : expf(sc[j] - m);
+    sum += pj;
+    const uint4* vr = reinterpret_cast<const uint4*>(sKV + ((r0 + j) * kKVLd + D + hc) * 2);
+#pragma unroll
+    for (int i = 0; i < DH / 8; ++i) {
+      const uint4 u = vr[i];
+      const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[e]));
+        c[8 * i + 2 * e] = fmaf(pj, vf.x, c[8 * i + 2 * e]);
+        c[8 * i + 2 * e + 1] = fmaf(pj, vf.y, c[8 * i + 2 * e + 1]);
+      }
+    }
+  }
+  const float inv = 1.f / sum;
+#pragma unroll
+  for (int i = 0; i < DH; ++i) c[i] *= inv;
+}
+
 __device__ long long* g_trace_tc = nullptr;
 // debug: per-phase timestamps of CTA 0 / thread 0 for its last 8 tiles (ring)
 #define TT(id)                                                                   \
@@ -502,7 +551,17 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       float c[DH];
 #pragma unroll
       for (int i = 0; i < DH; ++i) c[i] = 0.f;
-      if (live) {
+      if (live && L <= 6) {  // the common small leaf counts: unrolled per L
+        const int r0 = (r / L) * L;
+        switch (L) {
+          case 1: attn_fixed<1>(sKV, r0, hc, q, scale, c); break;
+          case 2: attn_fixed<2>(sKV, r0, hc, q, scale, c); break;
+          case 3: attn_fixed<3>(sKV, r0, hc, q, scale, c); break;
+          case 4: attn_fixed<4>(sKV, r0, hc, q, scale, c); break;
+          case 5: attn_fixed<5>(sKV, r0, hc, q, scale, c); break;
+          default: attn_fixed<6>(sKV, r0, hc, q, scale, c); break;
+        }
+      } else if (live) {
         // one pass over the keys with a running max (no score array, so no
         // stack frame): the context is rescaled only when the max grows
         const int r0 = (r / L) * L;
