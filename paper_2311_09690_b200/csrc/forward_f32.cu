@@ -170,6 +170,50 @@ __device__ long long* g_trace_f32 = nullptr;
       g_trace_f32[(tcount & 7) * 32 + (id)] = clock64();                         \
   } while (0)
 
+// attention of one query row over its AST's LL keys (fp32 K|V rows, head
+// columns DH·wg ..), LL a compile-time count: every score first
+// (independent dot products), then the weights and the context
+template <int LL>
+__device__ __forceinline__ void attn_f32_fixed(const float* __restrict__ sKV, int r0, int wg,
+                                               const float* q, float scale, float* c) {
+  float sc[LL];
+#pragma unroll
+  for (int jj = 0; jj < LL; ++jj) {
+    const float* kr = sKV + (r0 + jj) * LDK + DH * wg;
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < DH; i += 4) {
+      const float4 k4 = *reinterpret_cast<const float4*>(kr + i);
+      a4[0] = fmaf(q[i], k4.x, a4[0]);
+      a4[1] = fmaf(q[i + 1], k4.y, a4[1]);
+      a4[2] = fmaf(q[i + 2], k4.z, a4[2]);
+      a4[3] = fmaf(q[i + 3], k4.w, a4[3]);
+    }
+    sc[jj] = ((a4[0] + a4[1]) + (a4[2] + a4[3])) * scale;
+  }
+  float m = sc[0];
+#pragma unroll
+  for (int jj = 1; jj < LL; ++jj) m = fmaxf(m, sc[jj]);
+  float sum = 0.f;
+#pragma unroll
+  for (int jj = 0; jj < LL; ++jj) {
+    const float pj = LL == 1 ? 1.f : expf(sc[jj] - m);
+    sum += pj;
+    const float* vr = sKV + (r0 + jj) * LDK + D + DH * wg;
+#pragma unroll
+    for (int i = 0; i < DH; i += 4) {
+      const float4 v4 = *reinterpret_cast<const float4*>(vr + i);
+      c[i] = fmaf(pj, v4.x, c[i]);
+      c[i + 1] = fmaf(pj, v4.y, c[i + 1]);
+      c[i + 2] = fmaf(pj, v4.z, c[i + 2]);
+      c[i + 3] = fmaf(pj, v4.w, c[i + 3]);
+    }
+  }
+  const float inv = 1.f / sum;
+#pragma unroll
+  for (int i = 0; i < DH; ++i) c[i] *= inv;
+}
+
 __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
     const __grid_constant__ Model M, const float* __restrict__ P, const float* __restrict__ x,
     const int32_t* __restrict__ tile_L, const int32_t* __restrict__ tile_first,
@@ -350,7 +394,17 @@ __global__ void __launch_bounds__(NTH, 1) forward_f32_kernel(
       float c[DH];
 #pragma unroll
       for (int j = 0; j < DH; ++j) c[j] = 0.f;
-      if (live) {
+      if (live && L <= 6) {  // the common small leaf counts: unrolled per L
+        const int r0 = (r / L) * L;
+        switch (L) {
+          case 1: attn_f32_fixed<1>(sKV, r0, wg, q, scale, c); break;
+          case 2: attn_f32_fixed<2>(sKV, r0, wg, q, scale, c); break;
+          case 3: attn_f32_fixed<3>(sKV, r0, wg, q, scale, c); break;
+          case 4: attn_f32_fixed<4>(sKV, r0, wg, q, scale, c); break;
+          case 5: attn_f32_fixed<5>(sKV, r0, wg, q, scale, c); break;
+          default: attn_f32_fixed<6>(sKV, r0, wg, q, scale, c); break;
+        }
+      } else if (live) {
         // one pass over the keys with a running max (no score array, so no
         // stack frame): the context is rescaled only when the max grows
         const int r0 = (r / L) * L;
