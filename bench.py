@@ -491,6 +491,30 @@ def run_large_batch(cfg, train, targets, norm, dv, dev, flush_l2, batch: int = 6
         out[name] = {"samples_per_s": train.n / t, "ms_per_step": t * 1e3 / len(steps),
                      "optimizer_steps": int(len(steps))}
         del tr
+    # the A/B at the headline batch (64): the same fused trainer with the
+    # encoder weight gradients on tcgen05 (the bs-64 fused number is `value`)
+    cfg64 = pb.desk_config(seed=0, batch_size=64)
+    tr = Trainer(cfg64, params.tensors, rag_of(train, dv), targets, loss, device=dev,
+                 wgrad_tc=True)
+    rng = np.random.default_rng(0)
+    flat, steps = tr.plan(rng)
+    with torch.cuda.stream(tr.stream):
+        tr.run_epoch(cfg64.lr, flat, steps[:8])
+    torch.cuda.synchronize()
+    flat, steps = tr.plan(rng)
+    flush_l2()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(tr.stream):
+        a.record()
+        tr.run_epoch(cfg64.lr, flat, steps)
+        b.record()
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / 1e3
+    out["bs64_fused_ffma_wgrad_tcgen05"] = {"samples_per_s": train.n / t,
+                                            "ms_per_step": t * 1e3 / len(steps),
+                                            "optimizer_steps": int(len(steps))}
+    del tr
     return out
 
 
