@@ -22,7 +22,10 @@
 // measures it at 262,144 × 1024, d = 24 and 32).  G = 32 for κ ≥ 512; below
 // that G = 1 — every score enters the top-4 (exact fp32 top-4, unquantised),
 // which costs 20 ALU operations per score but keeps the candidate set robust
-// to two near-tied centres falling in one group.
+// to two near-tied centres falling in one group.  For d ≤ 30 the two spare K
+// columns carry ‖c‖² and X (centres −2c | ‖c‖² | 1, points x | 1 | X), so the
+// GEMM forms q itself and the scan starts from the TMEM values (d = 24: 0.50 →
+// 0.44 ms per 1 M × 1024 pass).
 //
 // Why this shape (profiles/r02/ncu_kmeans_tc_summary.txt): the epilogue, not
 // the tensor core, bounds the pass.  The round-1 kernel kept an exact fp32
@@ -116,25 +119,34 @@ __device__ double exact_sq(const double* a, const double* b, int d) {
 // centres → per-chunk operand image: chunk c = [hi tile (16 KB) | lo tile (16 KB)],
 // fp32 norms ‖c‖² (padding centres: zero rows, norm kPadNorm) and their maximum
 // (float bits; norms ≥ 0, so the unsigned order is the float order)
+// fold (d ≤ 30): the image holds −2·c in columns < d, ‖c‖² in column d and 1
+// in column d + 1, so the GEMM itself forms ‖c‖² − 2x·c + X (the points carry
+// 1 and X in those columns) and the scan reads scores straight from TMEM
 __global__ void prep_centers_kernel(const double* __restrict__ c, int kappa, int d, int nchunks,
-                                    uint8_t* __restrict__ img, float* __restrict__ norms,
-                                    unsigned* __restrict__ max_norm) {
+                                    int fold, uint8_t* __restrict__ img,
+                                    float* __restrict__ norms, unsigned* __restrict__ max_norm) {
   const int total = nchunks * CN * 32;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     const int row = e / 32, k = e - row * 32;  // row = centre index
     const int ch = row / CN, r = row - ch * CN;
-    const double v = (row < kappa && k < d) ? c[(size_t)row * d + k] : 0.0;
+    const bool live = row < kappa;
+    double s = 0.0;  // ‖c‖² (the thread of column 0 or, folded, of column d)
+    if (k == (fold ? d : 0) && live)
+      for (int i = 0; i < d; ++i) s += c[(size_t)row * d + i] * c[(size_t)row * d + i];
+    double v = (live && k < d) ? c[(size_t)row * d + k] : 0.0;
+    if (fold) {
+      if (k < d) v *= -2.0;  // exact
+      else if (k == d) v = live ? (double)(float)s : (double)kPadNorm;
+      else if (k == d + 1) v = 1.0;
+    }
     const float hi = tf32_hi((float)v);
     const float lo = tf32_hi((float)(v - (double)hi));
     uint8_t* base = img + (size_t)ch * 2 * kCtTile;
     *reinterpret_cast<float*>(base + sw128f(r, k)) = hi;
     *reinterpret_cast<float*>(base + kCtTile + sw128f(r, k)) = lo;
-    if (k == 0) {
-      double s = 0.0;
-      if (row < kappa)
-        for (int i = 0; i < d; ++i) s += c[(size_t)row * d + i] * c[(size_t)row * d + i];
-      norms[row] = row < kappa ? (float)s : kPadNorm;
-      if (row < kappa) atomicMax(max_norm, __float_as_uint((float)s));
+    if (k == (fold ? d : 0)) {
+      norms[row] = live ? (float)s : kPadNorm;
+      if (live) atomicMax(max_norm, __float_as_uint((float)s));
     }
   }
 }
@@ -203,7 +215,7 @@ __device__ __forceinline__ float group_min(const float* k) {  // G = 1, 8 or 32
   }
 }
 
-template <int G>
+template <int G, bool FOLD>
 __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
     const double* __restrict__ x, int64_t n, int d, const double* __restrict__ centers,
     int kappa, int nchunks, const uint8_t* __restrict__ img, const float* __restrict__ norms,
@@ -288,9 +300,15 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
         for (int k = 0; k < 32; ++k) xf[k] = (live && k < d) ? (float)x[i * d + k] : 0.f;
       }
 #pragma unroll
+      for (int k = 0; k < 32; ++k) xx = fmaf(xf[k], xf[k], xx);  // columns ≥ d are 0
+      const float Xp = fmaf(xx, kBias, xx) + bias_c;
+      if (FOLD) {  // 1 and X in columns d, d + 1 (selects: d is not a constant)
+#pragma unroll
+        for (int k = 0; k < 32; ++k) xf[k] = k == d ? 1.f : (k == d + 1 ? Xp : xf[k]);
+      }
+#pragma unroll
       for (int k = 0; k < 32; ++k) {  // fp32 split: the 2^-24 rounding of x is below 3xTF32's
         const float vf = xf[k];
-        xx = fmaf(vf, vf, xx);
         hv[k] = tf32_hi(vf);
         lv[k] = tf32_hi(vf - hv[k]);
       }
@@ -304,7 +322,7 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&pts);
-      return fmaf(xx, kBias, xx) + bias_c;
+      return Xp;
     };
     float X = ntiles > 0 ? stage(first + t) : 0.f;
     int gc = 0;
@@ -324,7 +342,7 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
       for (int c = 0; c < nchunks; ++c, ++gc) {
         const int b = gc & 1;
         mbar_wait(&done[b], (gc >> 1) & 1);
-        mbar_wait(&nld[b], (gc >> 1) & 1);
+        if (!FOLD) mbar_wait(&nld[b], (gc >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const float4* nrm4 = reinterpret_cast<const float4*>(s_norm + b * CN);
 #pragma unroll 1
@@ -341,10 +359,16 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
                 "=r"(r[30]), "=r"(r[31])
               : "r"(tmem + lane_off + b * CN + j0));
           float4 nv[8];
+          if (!FOLD) {
 #pragma unroll
-          for (int v = 0; v < 8; ++v) nv[v] = nrm4[j0 / 4 + v];
+            for (int v = 0; v < 8; ++v) nv[v] = nrm4[j0 / 4 + v];
+          }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           float key[32];
+          if (FOLD) {  // the GEMM formed the scores
+#pragma unroll
+            for (int u = 0; u < 32; ++u) key[u] = __uint_as_float(pack_key(r[u], kmask, u % G));
+          } else {
 #pragma unroll
           for (int v = 0; v < 8; ++v) {
             const uint64_t s01 =
@@ -360,6 +384,7 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
               const int u = 4 * v + e;
               key[u] = __uint_as_float(pack_key(w[e], kmask, u % G));
             }
+          }
           }
 #pragma unroll
           for (int g = 0; g < 32 / G; ++g) {
@@ -463,19 +488,19 @@ __global__ void __launch_bounds__(TP + 32, 2) assign_tc_kernel(
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-template <int G>
+template <int G, bool FOLD>
 int launch_assign(const double* x, int64_t n, int d, const double* c, int kappa, int nchunks,
                    const uint8_t* img, const float* norms, const unsigned* max_norm,
                    int64_t* assign, double* own, int32_t* counts, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
-    TPCB_CUDA_CHECK(cudaFuncSetAttribute(assign_tc_kernel<G>,
+    TPCB_CUDA_CHECK(cudaFuncSetAttribute(assign_tc_kernel<G, FOLD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmTotal));
     attr = true;
   }
   const int64_t tiles = (n + TP - 1) / TP;
   const int grid = (int)std::min<int64_t>(tiles, 2 * kNumSMs);
-  assign_tc_kernel<G><<<grid, TP + 32, kSmTotal, stream>>>(x, n, d, c, kappa, nchunks, img, norms,
+  assign_tc_kernel<G, FOLD><<<grid, TP + 32, kSmTotal, stream>>>(x, n, d, c, kappa, nchunks, img, norms,
                                                       max_norm, assign, own, counts);
   return TPCB_OK;
 }
@@ -508,14 +533,16 @@ extern "C" int tpcb_kmeans_assign_tc(const double* d_x, int64_t n, int32_t d,
   unsigned* max_norm = reinterpret_cast<unsigned*>(norms + nchunks * CN);
   TPCB_CUDA_CHECK(cudaMemsetAsync(d_counts, 0, sizeof(int32_t) * kappa, stream));
   TPCB_CUDA_CHECK(cudaMemsetAsync(max_norm, 0, sizeof(unsigned), stream));
+  const bool fold = d <= 30;  // two spare K columns carry the norms and X
   prep_centers_kernel<<<std::min(nchunks * CN * 32 / 256 + 1, 4 * kNumSMs), 256, 0, stream>>>(
-      d_centers, kappa, d, nchunks, img, norms, max_norm);
+      d_centers, kappa, d, nchunks, fold ? 1 : 0, img, norms, max_norm);
   TPCB_LAUNCH_CHECK("prep_centers");
-  const int rc = kappa >= 512
-                     ? launch_assign<32>(d_x, n, d, d_centers, kappa, nchunks, img, norms,
-                                         max_norm, d_assign, d_own, d_counts, stream)
-                     : launch_assign<1>(d_x, n, d, d_centers, kappa, nchunks, img, norms,
-                                        max_norm, d_assign, d_own, d_counts, stream);
+#define TPCB_ASSIGN(G, F)                                                                    \
+  launch_assign<G, F>(d_x, n, d, d_centers, kappa, nchunks, img, norms, max_norm, d_assign, \
+                      d_own, d_counts, stream)
+  const int rc = kappa >= 512 ? (fold ? TPCB_ASSIGN(32, true) : TPCB_ASSIGN(32, false))
+                              : (fold ? TPCB_ASSIGN(1, true) : TPCB_ASSIGN(1, false));
+#undef TPCB_ASSIGN
   if (rc != TPCB_OK) return rc;
   TPCB_LAUNCH_CHECK("kmeans_assign_tc");
   return TPCB_OK;
