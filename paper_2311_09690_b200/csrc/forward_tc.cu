@@ -464,6 +464,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     }
   };
   load_x(blockIdx.x);
+  bool a_staged = false;  // warpgroup 1 already wrote this tile's A rows
   int tcount = -1;
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     ++tcount;
@@ -476,12 +477,15 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
 
     float h[DH];  // this row's residual stream, columns 32·wg .. 32·wg+31 (fp32)
     if (wg == 1) {  // prefetched input rows → A operand (24 features, zero-padded to 64)
-      float v[D];
+      if (!a_staged) {  // (from the second tile on, staged under the previous decoder)
+        float v[D];
 #pragma unroll
-      for (int i = 0; i < D; ++i) v[i] = (live && i < TPCB_FEAT) ? xn[i < TPCB_FEAT ? i : 0] : 0.f;
-      store_row_bf16(sA, r, v);
+        for (int i = 0; i < D; ++i) v[i] = (live && i < TPCB_FEAT) ? xn[i < TPCB_FEAT ? i : 0] : 0.f;
+        store_row_bf16(sA, r, v);
+      }
       if (r < A) cp_async4(s_idx + r, perm + first + r);  // lands under the input projection
     }
+    a_staged = false;
     sync_for_mma();
     TT(1);
     if (t == 0) {
@@ -795,6 +799,16 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
           if (bad) raise_status(status, TPCB_ERR_DOMAIN);
         }
       }
+    } else if (tile + (int)gridDim.x < n_tiles) {
+      // warpgroup 1 is idle in the decoder's last epilogue and the A operand
+      // is dead once the dec1 MMA has completed: stage the next tile's rows now
+      const int nt = tile + gridDim.x;
+      const bool live_n = r < tile_count[nt] * tile_L[nt];
+      float v[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) v[i] = (live_n && i < TPCB_FEAT) ? xn[i < TPCB_FEAT ? i : 0] : 0.f;
+      store_row_bf16(sA, r, v);
+      a_staged = true;
     }
     TT(31);
     __syncthreads();
