@@ -766,13 +766,12 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     }
     wait_mma(&bars[1], phase);
     TT(27);
-    if (wg == 0) {
-      float u[DEC];
-      tmem_ld32(tlane, u);
-      tmem_ld32(tlane + 32, u + 32);
+    {  // dec0 epilogue split by column half (warpgroup wg: columns 32·wg ..)
+      float u[DH];
+      tmem_ld32(tlane + DH * wg, u);
 #pragma unroll
-      for (int j = 0; j < DEC; ++j) u[j] = fmaxf(u[j] + hv[kVHDecB0 + j], 0.f);
-      store_row_bf16(sA, t, u);
+      for (int j = 0; j < DH; ++j) u[j] = fmaxf(u[j] + hv[kVHDecB0 + DH * wg + j], 0.f);
+      store_half_row_bf16(sA, r, wg, u);
     }
     sync_for_mma();
     if (t == 0) {
