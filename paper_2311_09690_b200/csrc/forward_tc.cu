@@ -123,6 +123,15 @@ __device__ __forceinline__ void mma_chain(uint32_t tmem, const uint32_t* a_tiles
     }
 }
 
+// one lane of a converged warp (elect.sync): MMA issue from a warp-uniform
+// context, so the descriptors stay in uniform registers
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+               : "=r"(e));
+  return e != 0;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
       smem_u32(bar)));
@@ -488,7 +497,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     a_staged = false;
     sync_for_mma();
     TT(1);
-    if (t == 0) {
+    if (warp == 0 && elect_one()) {
       const uint32_t at[1] = {a_addr}, bt[1] = {w_addr + kImgIn};
       mma_chain(tmem, at, bt, 1, D);
       mma_commit(&bars[1]);
@@ -513,7 +522,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     for (int li = 0; li < NLAY; ++li) {
       const float* b = sv + kVecLayer + li * kVecLStride;
       const uint32_t wl = w_addr + kImgLayer + li * kImgLStride;
-      if (t == 0) {  // Q | K | V
+      if (warp == 0 && elect_one()) {  // Q | K | V
         const uint32_t at[1] = {a_addr}, bt[1] = {wl + kQKV};
         mma_chain(tmem, at, bt, 1, 3 * D);
         mma_commit(&bars[1]);
@@ -613,7 +622,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       store_half_row_bf16(sA, r, wg, c);
       sync_for_mma();
       TT(5 + li * 12);
-      if (t == 0) {  // output projection
+      if (warp == 0 && elect_one()) {  // output projection
         const uint32_t at[1] = {a_addr}, bt[1] = {wl + kWO};
         mma_chain(tmem, at, bt, 1, D);
         mma_commit(&bars[1]);
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       }
       sync_for_mma();
       TT(7 + li * 12);
-      if (t == 0) {  // FFN hidden (N = 128)
+      if (warp == 0 && elect_one()) {  // FFN hidden (N = 128)
         const uint32_t at[1] = {a_addr}, bt[1] = {wl + kFH};
         mma_chain(tmem, at, bt, 1, FF);
         mma_commit(&bars[1]);
@@ -648,7 +657,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       if (li + 1 == NLAY) load_x(tile + gridDim.x);
       sync_for_mma();
       TT(9 + li * 12);
-      if (t == 0) {  // FFN out (K = 128)
+      if (warp == 0 && elect_one()) {  // FFN out (K = 128)
         const uint32_t at[2] = {kv_addr, kv_addr + TR * 128},
                        bt[2] = {wl + kFO0, wl + kFO1};
         mma_chain(tmem, at, bt, 2, D);
@@ -684,7 +693,8 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     // W_L's l-th 64-row block, so D[a] = Σ_l h[a·L+l] · W_L[l] = z_x[a] − b_L
     // accumulates over the L chunks in TMEM (columns 0..31, one AST per lane).
     sync_for_mma();
-    if (t == 0) {
+    TT(12);
+    if (warp == 0 && elect_one()) {
       const int cb = leaf_chunk_a(L), boff = L * cb;
       const int G = min(L, (kLeafRegion - boff) / kLeafChunkB);
       const uint32_t id = idesc_bf16(TR, DE);
@@ -701,6 +711,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
         }
         mbar_wait(&bars[2], phase_b);
         phase_b ^= 1;
+        TT(13);
         for (int j = 0; j < g; ++j) {
           const uint32_t ab = a_addr + (uint32_t)((l0 + j) * cb),
                          bb = a_addr + (uint32_t)(boff + j * kLeafChunkB);
@@ -714,6 +725,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
           }
         }
       }
+      TT(14);
       mma_commit(&bars[1]);
     }
     wait_mma(&bars[1], phase);
@@ -759,7 +771,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
     sync_for_mma();
     TT(26);
     // decoder on the tensor cores, one AST per row / TMEM lane / thread
-    if (t == 0) {
+    if (warp == 0 && elect_one()) {
       const uint32_t at[1] = {a_addr}, bt[1] = {w_addr + kImgDec0};
       mma_chain(tmem, at, bt, 1, DEC);
       mma_commit(&bars[1]);
@@ -774,7 +786,7 @@ __global__ void __launch_bounds__(NTH, 1) forward_tc_kernel(
       store_half_row_bf16(sA, r, wg, u);
     }
     sync_for_mma();
-    if (t == 0) {
+    if (warp == 0 && elect_one()) {
       const uint32_t at[1] = {a_addr}, bt[1] = {w_addr + kImgDec1};
       mma_chain(tmem, at, bt, 1, DEC);
       mma_commit(&bars[1]);

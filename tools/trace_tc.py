@@ -31,7 +31,10 @@ for li in range(2):
     for k, nm in enumerate(["qkv mma", "qkv epi+attn", "wo mma", "ln1 epi", "ffn1 mma", "ffn1 epi",
                             "ffn2 mma", "ln2 epi"]):
         names[base + k] = f"L{li} {nm}"
-names[25] = "leaf mma"
+names[12] = "leaf sync"
+names[13] = "leaf B wait"
+names[14] = "leaf mma issue"
+names[25] = "leaf mma wait"
 names[26] = "zx+dev mlp+gate->A"
 names[27] = "dec0 mma"
 names[28] = "dec0 epi+dec1 mma"
