@@ -229,7 +229,7 @@ __device__ __noinline__ double pe_term(double pos, double den, int is_cos) {
 constexpr int kStagePitch = 36;  // floats per staged row (144 B: spreads banks)
 
 template <bool F64, bool PE>
-__global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
+__global__ void __launch_bounds__(kPackThreads, 2) pack_rows_kernel(
     const void* __restrict__ vectors_, const int32_t* __restrict__ ordering,
     const int64_t* __restrict__ leaf_off, const int32_t* __restrict__ perm,
     const int32_t* __restrict__ tile_L, const int32_t* __restrict__ tile_first,
@@ -268,9 +268,21 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
     }
     return h;
   };
+  // f32 rows: the next row's vector is loaded too, right after its token
+  // arrives (under this row's staging and stores) — two rows in flight
+  auto load_vec = [&](const Hdr& h, float4* dst) {
+    if (!F64 && h.live == 1) {
+      const float4* src =
+          reinterpret_cast<const float4*>(static_cast<const float*>(vectors_) + (int64_t)h.tok * TPCB_FEAT);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) dst[q] = __ldg(src + q);
+    }
+  };
   int64_t gr = (int64_t)blockIdx.x * kPackThreads + threadIdx.x;
   Hdr cur = header(gr);
   int ipos = (PE && cur.live == 1) ? ordering[cur.tok] : 0;
+  float4 vr[6];
+  load_vec(cur, vr);
   for (int64_t base = (int64_t)blockIdx.x * kPackThreads; base < rows; base += stride) {
     const Hdr nxt = header(gr + stride);
     float4 out[6];
@@ -293,11 +305,9 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
             v[2 * q + 1] = p.y;
           }
         } else {
-          const float4* src = reinterpret_cast<const float4*>(
-              static_cast<const float*>(vectors_) + tok * TPCB_FEAT + h * 12);
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
-            const float4 p = __ldg(src + q);
+            const float4 p = vr[3 * h + q];
             v[4 * q] = p.x; v[4 * q + 1] = p.y; v[4 * q + 2] = p.z; v[4 * q + 3] = p.w;
           }
         }
@@ -333,8 +343,10 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
     } else if (cur.live == 0) {
       row_ast[gr] = -1;  // pad row (real rows were written by bucket_scatter)
     }
-    // the next row's position (its token arrived during this row's loads)
+    // the next row's position and vector (its token arrived during this row)
     const int ipos_n = (PE && nxt.live == 1) ? ordering[nxt.tok] : 0;
+    float4 vn[6];
+    load_vec(nxt, vn);
     float4* my = reinterpret_cast<float4*>(stage + threadIdx.x * kStagePitch);
 #pragma unroll
     for (int q = 0; q < kChunks; ++q) my[q] = out[q];
@@ -348,6 +360,8 @@ __global__ void __launch_bounds__(kPackThreads, 3) pack_rows_kernel(
     __syncthreads();
     cur = nxt;
     ipos = ipos_n;
+#pragma unroll
+    for (int q = 0; q < 6; ++q) vr[q] = vn[q];
     gr += stride;
   }
 }
