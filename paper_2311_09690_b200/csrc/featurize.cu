@@ -226,7 +226,7 @@ __device__ __noinline__ double pe_term(double pos, double den, int is_cos) {
   sincos(pos / den, &sn, &cs);
   return is_cos ? cs : sn;
 }
-constexpr int kStagePitch = 36;  // floats per staged row (144 B: spreads banks)
+constexpr int kStagePitch = 28;  // floats per staged row (112 B: 16-B accesses conflict-free)
 
 template <bool F64, bool PE>
 __global__ void __launch_bounds__(kPackThreads, 2) pack_rows_kernel(
@@ -241,9 +241,14 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_rows_kernel(
   // ordering) in shared memory — the L1 path served them from L2 (ncu: L2
   // sectors ~2x the DRAM traffic)
   constexpr int kPeSmem = 64;
-  __shared__ __align__(16) double pe_s[PE ? kPeSmem * TPCB_FEAT : 2];
+  // rows padded to 26 doubles: a 24-double (192-B) pitch put every even
+  // position on the same 4 banks (16-way conflicts on the row reads); 208 B
+  // spreads the rows over all 8 16-byte bank groups
+  constexpr int kPePitch = TPCB_FEAT + 2;
+  __shared__ __align__(16) double pe_s[PE ? kPeSmem * kPePitch : 2];
   if (PE) {
-    for (int i = threadIdx.x; i < kPeSmem * TPCB_FEAT; i += kPackThreads) pe_s[i] = pe_table[i];
+    for (int i = threadIdx.x; i < kPeSmem * TPCB_FEAT; i += kPackThreads)
+      pe_s[(i / TPCB_FEAT) * kPePitch + i % TPCB_FEAT] = pe_table[i];
     __syncthreads();
   }
   constexpr int kChunks = TPCB_FEAT_PAD / 4;  // 6 float4 per packed row
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_rows_kernel(
         if (PE) {  // column 2δ: sin(pos/θ^(2δ/24)); 2δ+1: cos (features.py:255-262)
           if (ipos >= 0 && ipos < kPeSmem) {  // shared-memory rows
             const double2* tp =
-                reinterpret_cast<const double2*>(pe_s + ipos * TPCB_FEAT + h * 12);
+                reinterpret_cast<const double2*>(pe_s + ipos * kPePitch + h * 12);
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
               const double2 p = tp[q];
