@@ -1210,6 +1210,7 @@ struct ColDst {
 // two-stage deterministic column sums: chunks of 64 rows → partial[chunk][c],
 // then the chunks in order
 constexpr int kColChunk = 64;
+constexpr int kColCntMax = 256;  // column-sum stripe counters per backward workspace
 
 __global__ void colsum_partial_kernel(const float* __restrict__ x, const float* __restrict__ x_lo,
                                       int rows, int cols, int ld, float* __restrict__ part) {
@@ -1242,6 +1243,70 @@ __global__ void colsum_partial_kernel(const float* __restrict__ x, const float* 
     for (int k = 1; k < 8; ++k) s += red[k][threadIdx.x];
     part[(size_t)blockIdx.y * cols + c] = s;
   }
+}
+
+// one launch: the chunk partials of colsum_partial_kernel, then the last chunk
+// block of each 32-column stripe (a counter per stripe, reset for the next
+// call) sums the stripe's partials in chunk order — colsum_final_kernel's fold
+__global__ void colsum_fused_kernel(const float* __restrict__ x, const float* __restrict__ x_lo,
+                                    int rows, int cols, int ld, float* __restrict__ part,
+                                    unsigned* __restrict__ cnt, ColDst dst,
+                                    float* __restrict__ grad) {
+  __shared__ float red[8][33];
+  __shared__ bool last;
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = blockIdx.y * kColChunk, r1 = min(r0 + kColChunk, rows);
+  float acc = 0.f;
+  if (c < cols) {  // the chunk's rows for this thread: loads first, adds in row order
+    constexpr int kPer = kColChunk / 8;
+    float xv[kPer], xl[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int r = r0 + threadIdx.y + 8 * u;
+      xv[u] = r < r1 ? x[(size_t)r * ld + c] : 0.f;
+      xl[u] = (r < r1 && x_lo) ? x_lo[(size_t)r * ld + c] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int r = r0 + threadIdx.y + 8 * u;
+      if (r < r1) {
+        acc += xv[u];
+        if (x_lo) acc += xl[u];
+      }
+    }
+  }
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0) {
+    if (c < cols) {
+      float s = red[0][threadIdx.x];
+      for (int k = 1; k < 8; ++k) s += red[k][threadIdx.x];
+      part[(size_t)blockIdx.y * cols + c] = s;
+    }
+    __threadfence();
+    __syncwarp();
+    if (threadIdx.x == 0) last = atomicAdd(&cnt[blockIdx.x], 1u) == gridDim.y - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.y != 0) return;
+  __threadfence();
+  if (c < cols) {
+    const int chunks = gridDim.y;
+    float s = __ldcg(part + c);
+    int k = 1;
+    for (; k + 8 <= chunks; k += 8) {  // 8 loads in flight, added in chunk order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldcg(part + (size_t)(k + u) * cols + c);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; k < chunks; ++k) s += __ldcg(part + (size_t)k * cols + c);
+    const int t = c / dst.colw;
+    float* g = grad + dst.d[t] + (c - t * dst.colw);
+    *g = dst.acc ? *g + s : s;
+  }
+  if (threadIdx.x == 0) cnt[blockIdx.x] = 0;
 }
 
 __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, int cols,
@@ -1581,6 +1646,7 @@ struct Bwd {
   float *tWp, *tbp, *tWh, *tbh;
   float* dpred;
   float* colpart;            // column-sum partials [chunks][cols]
+  unsigned* colcnt;          // column-sum stripe counters [kColCntMax]
   size_t part_floats;
 };
 
@@ -1624,6 +1690,7 @@ Bwd carve_bwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, 
   b.dpred = cv->take(A);
   b.colpart = cv->take((size_t)ceil_div(max(T, A), kColChunk) *
                        max(max(M.d_dev * M.d_e, p.qkvp), max(p.ffp, dmax)));
+  b.colcnt = reinterpret_cast<unsigned*>(cv->take(kColCntMax));
   return b;
 }
 
@@ -1636,6 +1703,7 @@ int transpose_into(const float* hi, const float* lo, int rows, int cols, int ld,
 }
 
 thread_local float* g_colsum_part = nullptr;  // column-sum scratch (set per call)
+thread_local unsigned* g_colsum_cnt = nullptr;  // per-stripe counters (zeroed per call)
 
 // the weight-gradient branch runs on a side stream: dW = Xᵀ·dY only needs
 // dY, so it overlaps the main stream's dX chain; the main stream waits only
@@ -1665,10 +1733,15 @@ int stream_wait(cudaStream_t waiter, cudaStream_t on) {
 int colsum(const float* x, const float* x_lo, int rows, int cols, int ld, ColDst dst, float* grad,
            cudaStream_t st) {
   const int chunks = max(1, ceil_div(rows, kColChunk));
-  colsum_partial_kernel<<<dim3(ceil_div(cols, 32), chunks), dim3(32, 8), 0, st>>>(
-      x, x_lo, rows, cols, ld, g_colsum_part);
-  colsum_final_kernel<<<ceil_div(cols, 128), 128, 0, st>>>(g_colsum_part, chunks, cols, dst,
-                                                            grad);
+  if (g_colsum_cnt && ceil_div(cols, 32) <= kColCntMax) {
+    colsum_fused_kernel<<<dim3(ceil_div(cols, 32), chunks), dim3(32, 8), 0, st>>>(
+        x, x_lo, rows, cols, ld, g_colsum_part, g_colsum_cnt, dst, grad);
+  } else {
+    colsum_partial_kernel<<<dim3(ceil_div(cols, 32), chunks), dim3(32, 8), 0, st>>>(
+        x, x_lo, rows, cols, ld, g_colsum_part);
+    colsum_final_kernel<<<ceil_div(cols, 128), 128, 0, st>>>(g_colsum_part, chunks, cols, dst,
+                                                              grad);
+  }
   TPCB_LAUNCH_CHECK("large_colsum");
   return TPCB_OK;
 }
@@ -1955,8 +2028,13 @@ extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_para
   const int nt = (int)n_tok, nb = (int)n_batch;
   (void)nt;
   g_colsum_part = b.colpart;
+  g_colsum_cnt = b.colcnt;
+  struct CntGuard {  // the counters belong to this call's workspace
+    ~CntGuard() { g_colsum_cnt = nullptr; }
+  } cnt_guard;
   if ((rc = side_init())) return rc;
   TPCB_CUDA_CHECK(cudaMemsetAsync(G, 0, sizeof(float) * (size_t)M.total, st));
+  TPCB_CUDA_CHECK(cudaMemsetAsync(b.colcnt, 0, sizeof(unsigned) * kColCntMax, st));
   loss_kernel<<<1, 1024, 0, st>>>(f.pred, d_y, f.idx, nb, loss->mode, loss->lambda_hybrid,
                                   loss->offset, loss->original_space, loss->norm, n_norm, b.dpred,
                                   d_loss);
