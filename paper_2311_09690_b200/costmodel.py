@@ -19,6 +19,7 @@ import hashlib
 import io
 import json
 import math
+import threading
 import zipfile
 from dataclasses import asdict, dataclass, replace
 
@@ -265,11 +266,23 @@ class Predictor:
             return cpu(pred), cpu(zx), cpu(zv), cpu(z), cpu(lat)
         return self._forward_pipelined(batch, normalizer, latents)
 
+    def _pipe_state(self):
+        """Per-thread pipeline state (buffers + copy stream): concurrent
+        forward_batch calls on one Predictor from different threads never
+        share a staging buffer."""
+        tls = self.__dict__.get("_tls")
+        if tls is None:
+            tls = self.__dict__.setdefault("_tls", threading.local())
+        if not hasattr(tls, "bufs"):
+            tls.bufs = {}
+            tls.copy = None
+        return tls
+
     def _buf(self, name, numel, dtype, device=None):
         """Cached pipeline buffer (device, or pinned host when device is None),
         grown on demand; every call synchronises before returning, so a buffer
         is never resized under in-flight work."""
-        cache = self.__dict__.setdefault("_pipe_bufs", {})
+        cache = self._pipe_state().bufs
         buf = cache.get(name)
         if buf is None or buf.numel() < numel or buf.dtype != dtype:
             buf = (torch.empty(max(numel, 1), dtype=dtype, device=device) if device is not None
@@ -315,7 +328,10 @@ class Predictor:
         outs_lat = [self._buf(f"out_{w}_{i}", n * w, torch.float32).view(n, w)
                     for i, w in enumerate((de, ddev, de))] if latents else None
         compute = torch.cuda.current_stream(dev)
-        copy = self.__dict__.setdefault("_copy_stream", torch.cuda.Stream(device=dev))
+        st = self._pipe_state()
+        if st.copy is None:
+            st.copy = torch.cuda.Stream(device=dev)
+        copy = st.copy
         free = [None, None]  # compute finished with input buffer set k
         keep = []
         tb = 0

@@ -270,3 +270,37 @@ def test_forward_batch_pipelined_equals_one_shot(precision):
                                 nl, batch.device_index, devs)
     with pytest.raises(LeafCountExceeded, match=f"input {bad} "):
         p.forward_batch(bad_batch, None)
+
+
+def test_forward_batch_concurrent_threads_on_one_predictor():
+    """Two threads running the pipelined bulk path on one Predictor (shared
+    read-only params, disjoint batches — SURVEY 8(b) threading): each gets its
+    own staging buffers and copy stream, so the results equal the serial ones."""
+    import threading
+    import paper_2311_09690_b200 as pb
+    from paper_2311_09690_b200 import synth
+    import torch
+    devs = [pb.DeviceSpec("a", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0)]
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
+    batches = []
+    for seed in (21, 22):
+        d = synth.generate(12000, seed=seed)
+        batches.append(pb.CompactBatch(pin(d.vectors.astype(np.float32)),
+                                       pin(d.ordering.astype(np.int32)), pin(d.n_leaf),
+                                       np.zeros(d.n, np.int32), devs))
+    p = pb.Predictor(pb.init_params(pb.desk_config(seed=6)), precision="bf16")
+    p.CHUNK = 2500
+    serial = [p.forward_batch(b, None)[0] for b in batches]
+    out = [None, None]
+
+    def run(i):
+        for _ in range(3):
+            out[i] = p.forward_batch(batches[i], None)[0]
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for a, b in zip(serial, out):
+        assert np.array_equal(a, b)
