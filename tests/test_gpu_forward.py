@@ -304,3 +304,28 @@ def test_forward_batch_concurrent_threads_on_one_predictor():
         t.join()
     for a, b in zip(serial, out):
         assert np.array_equal(a, b)
+
+
+def test_pack_positional_table_cache_per_theta():
+    """K1 keeps one PE table per (device, θ): packs alternating between two θ
+    values each match the float64 oracle rows (rounded to f32) for their own
+    θ (within K1's 4e-6 row bar) — a cached table is never reused for another θ."""
+    import paper_2311_09690_b200 as pb
+    from paper_2311_09690_b200 import _lib, engine, synth
+    data = synth.generate(3000, seed=31)
+    dv = pb.device_vector(pb.DeviceSpec("a", 1000.0, 16.0, 1024.0, 16, 2048.0, 4.0))
+    rag = engine.RaggedHost(rows=data.vectors.astype(np.float32), ordering=data.ordering,
+                            n_leaf=data.n_leaf, devfeat=np.tile(dv, (data.n, 1)).astype(np.float32),
+                            encoded=False)
+    rows, ordering, leaf_off, _ = engine.upload_ragged(rag)
+    st = engine.Status(rows.device)
+    off = np.concatenate([[0], np.cumsum(data.n_leaf)])
+    for theta in (10000.0, 777.0, 10000.0, 777.0):
+        pk = engine.pack(rows, ordering, leaf_off, data.n, 16, False, st, 128, theta)
+        x = pk.x.cpu().numpy().reshape(-1, _lib.FEAT_PAD)
+        ast_row = pk.ast_row.cpu().numpy()
+        for i in (0, 1, 777, 2999):
+            want = of.encode_rows(data.vectors[off[i]:off[i + 1]].astype(np.float32),
+                                  data.ordering[off[i]:off[i + 1]], theta)
+            got = x[ast_row[i]:ast_row[i] + data.n_leaf[i], :24]
+            assert np.abs(got - want).max() <= 4e-6, (theta, i)  # K1's own bar (see above)
