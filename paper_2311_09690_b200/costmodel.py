@@ -323,10 +323,13 @@ class Predictor:
                 None if one_dev else self._buf(f"di{k}", cap_ast, torch.int32, dev))
                for k in range(2)]
         de, ddev = self.config.d_embed, self.config.d_device
-        out_pred = self._buf("out_pred", n, torch.float32)  # pinned staging, copied out
-        out_lat = self._buf("out_lat", n, torch.float64) if normalizer is not None else None
-        outs_lat = [self._buf(f"out_{w}_{i}", n * w, torch.float32).view(n, w)
-                    for i, w in enumerate((de, ddev, de))] if latents else None
+        # outputs: fresh pinned arrays handed to the caller (no host copy; the
+        # caching host allocator recycles them once the caller drops them)
+        pinned = lambda *shape, dt=torch.float32: torch.empty(  # noqa: E731
+            shape, dtype=dt, pin_memory=True)
+        out_pred = pinned(n)
+        out_lat = pinned(n, dt=torch.float64) if normalizer is not None else None
+        outs_lat = [pinned(n, w) for w in (de, ddev, de)] if latents else None
         compute = torch.cuda.current_stream(dev)
         st = self._pipe_state()
         if st.copy is None:
@@ -377,10 +380,9 @@ class Predictor:
             keep.append((pred, zx, zv, z, lat))  # alive until the D2H copies ran
         compute.synchronize()
         self.status.check("forward")
-        cp = lambda x: x.numpy().copy()  # noqa: E731  (the staging buffers are reused)
-        res = (cp(out_pred),) + (tuple(cp(o) for o in outs_lat) if latents
-                                 else (None, None, None))
-        return res + (cp(out_lat) if out_lat is not None else None,)
+        res = (out_pred.numpy(),) + (tuple(o.numpy() for o in outs_lat) if latents
+                                     else (None, None, None))
+        return res + (out_lat.numpy() if out_lat is not None else None,)
 
 
 def forward(params: CostModelParams, inputs: list) -> tuple:
