@@ -148,8 +148,18 @@ __global__ void bucket_scatter_kernel(const int64_t* __restrict__ leaf_off, int6
                                       int32_t* __restrict__ row_tok,
                                       int32_t* __restrict__ row_ast) {
   __shared__ int warp_cnt[kScatterBlock / 32][kMaxL + 1];
-  __shared__ int bucket_off[kMaxL + 2], tile_off[kMaxL + 2];
+  __shared__ int bucket_off[kMaxL + 2], tile_off[kMaxL + 2], s_base[kMaxL + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // every independent global load first (this AST's leaf range, the block's
+  // bucket bases), so their latencies overlap the bucket-offset scan below
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t lo_i = 0, hi_i = 0;
+  if (i < n_ast) {
+    lo_i = leaf_off[i];
+    hi_i = leaf_off[i + 1];
+  }
+  if (threadIdx.x >= 32 && threadIdx.x < 32 + kMaxL + 1)
+    s_base[threadIdx.x - 32] = blk_base[(int64_t)blockIdx.x * (kMaxL + 1) + threadIdx.x - 32];
   if (w == 0) {  // bucket and tile offsets from the bucket sizes: lane L, warp scans
     const int L = lane;
     const int c = (L >= 1 && L <= n_leaf_max) ? cnt[L] : 0;
@@ -187,10 +197,9 @@ __global__ void bucket_scatter_kernel(const int64_t* __restrict__ leaf_off, int6
   for (int k = threadIdx.x; k < (kScatterBlock / 32) * (kMaxL + 1); k += blockDim.x)
     (&warp_cnt[0][0])[k] = 0;
   __syncthreads();
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int L = 0;
   if (i < n_ast) {
-    int64_t l64 = leaf_off[i + 1] - leaf_off[i];
+    const int64_t l64 = hi_i - lo_i;
     L = (l64 >= 1 && l64 <= n_leaf_max) ? (int)l64 : 0;
   }
   unsigned peers = __match_any_sync(0xffffffffu, L);
@@ -201,14 +210,14 @@ __global__ void bucket_scatter_kernel(const int64_t* __restrict__ leaf_off, int6
   if (i < n_ast && L > 0) {
     int pre = 0;
     for (int ww = 0; ww < w; ++ww) pre += warp_cnt[ww][L];
-    int pos = bucket_off[L] + blk_base[(int64_t)blockIdx.x * (kMaxL + 1) + L] + pre + rank;
+    int pos = bucket_off[L] + s_base[L] + pre + rank;
     perm[pos] = (int32_t)i;
     int r = pos - bucket_off[L];
     int A = R / L;
     int tile = tile_off[L] + r / A;
     const int row0 = tile * R + (r % A) * L;
     ast_row[i] = row0;
-    const int tok0 = (int)leaf_off[i];  // n_tok < 2^31 (tpcb_pack_sizes)
+    const int tok0 = (int)lo_i;  // n_tok < 2^31 (tpcb_pack_sizes)
     for (int l = 0; l < L; ++l) {  // the packed rows of AST i: source token + owner
       row_tok[row0 + l] = tok0 + l;
       row_ast[row0 + l] = (int32_t)i;
