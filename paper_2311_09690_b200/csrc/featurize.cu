@@ -364,17 +364,23 @@ __global__ void __launch_bounds__(kPackThreads, 2) pack_rows_kernel(
     const int ipos_n = (PE && nxt.live == 1) ? ordering[nxt.tok] : 0;
     float4 vn[6];
     load_vec(nxt, vn);
+    // each warp stages its own 32 consecutive rows and writes them out as one
+    // contiguous 3 KB run (coalesced 16-byte stores): warp barriers only
     float4* my = reinterpret_cast<float4*>(stage + threadIdx.x * kStagePitch);
 #pragma unroll
     for (int q = 0; q < kChunks; ++q) my[q] = out[q];
-    __syncthreads();
-    const int n_rows = rows - base < kPackThreads ? (int)(rows - base) : kPackThreads;
-    float4* dst = reinterpret_cast<float4*>(x) + base * kChunks;
-    for (int e = threadIdx.x; e < n_rows * kChunks; e += kPackThreads) {
-      const int rr = e / kChunks, ch = e - rr * kChunks;
-      dst[e] = reinterpret_cast<const float4*>(stage + rr * kStagePitch)[ch];
+    __syncwarp();
+    {
+      const int lane = threadIdx.x & 31, w0 = threadIdx.x & ~31;
+      const int64_t wbase = base + w0;
+      const int n_rows = rows - wbase < 32 ? (int)(rows - wbase) : 32;
+      float4* dst = reinterpret_cast<float4*>(x) + wbase * kChunks;
+      for (int e = lane; e < n_rows * kChunks; e += 32) {
+        const int rr = e / kChunks, ch = e - rr * kChunks;
+        dst[e] = reinterpret_cast<const float4*>(stage + (w0 + rr) * kStagePitch)[ch];
+      }
     }
-    __syncthreads();
+    __syncwarp();
     cur = nxt;
     ipos = ipos_n;
 #pragma unroll
