@@ -181,7 +181,7 @@ struct GlobalTree {  // one program's arrays in global memory
 // with coalesced 8-byte stores (the vectors of a block are contiguous).
 constexpr int kProgsPerBlock = 64;
 constexpr int kThreads = 256;
-constexpr int kNodeCap = 2048;   // nodes staged per block
+constexpr int kNodeCap = 1280;   // nodes staged per block (3 blocks per SM; 64 programs average ~740)
 constexpr int kVecPitch = 25;    // doubles per staged vector (bank spread)
 
 struct SmemTree {  // block-local ids; base = first node of the program
@@ -321,14 +321,17 @@ __global__ void __launch_bounds__(kThreads) build_compact_kernel(
       const int n_leaf = (int)(sm.leaf_off[p + 1] - sm.leaf_off[p]);
       leaf_vector(ch, stats + (gl0 + g) * 9, k, n_leaf, sm.vec + t * kVecPitch);
     }
-    __syncthreads();
-    const int n = min(kThreads, leaves - c);
-    double* dst = out.vectors + (gl0 + c) * TPCB_FEAT;
-    for (int e = t; e < n * TPCB_FEAT; e += kThreads) {
+    // each warp writes its own 32 consecutive leaves (a contiguous 6 KB run,
+    // coalesced) from its part of the staging tile: warp barriers only
+    __syncwarp();
+    const int w0 = c + 32 * warp;
+    const int n = max(0, min(32, leaves - w0));
+    double* dst = out.vectors + (gl0 + w0) * TPCB_FEAT;
+    for (int e = lane; e < n * TPCB_FEAT; e += 32) {
       const int r = e / TPCB_FEAT, col = e - r * TPCB_FEAT;
-      dst[e] = sm.vec[r * kVecPitch + col];
+      dst[e] = sm.vec[(32 * warp + r) * kVecPitch + col];
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 
