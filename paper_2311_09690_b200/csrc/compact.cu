@@ -272,12 +272,31 @@ __global__ void __launch_bounds__(kThreads) build_compact_kernel(
       program_warp(node_off, parent, extent, annot, leaf_off, stats, p0 + q, out);
     return;
   }
-  // stage the node arrays (coalesced), parents as block-local indices
-  for (int j = t; j < nodes; j += kThreads) {
-    sm.ext[j] = extent[gn0 + j];
-    sm.ann[j] = annot[gn0 + j];
+  // stage the node arrays (coalesced), parents as block-local indices: four
+  // nodes per thread per round with every load issued before any store
+  for (int j0 = t; j0 < nodes; j0 += 4 * kThreads) {
+    int64_t e[4];
+    int32_t pa[4];
+    uint8_t an[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * kThreads;
+      if (j < nodes) {
+        e[u] = extent[gn0 + j];
+        an[u] = annot[gn0 + j];
+        pa[u] = parent[gn0 + j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * kThreads;
+      if (j < nodes) {
+        sm.ext[j] = e[u];
+        sm.ann[j] = an[u];
+        sm.par[j] = (int16_t)pa[u];  // local ids
+      }
+    }
   }
-  for (int j = t; j < nodes; j += kThreads) sm.par[j] = (int16_t)parent[gn0 + j];  // local ids
   // block-wide exclusive scan of is_leaf, 256 nodes per round
   int carry = 0;
   for (int c = 0; c < nodes; c += kThreads) {
