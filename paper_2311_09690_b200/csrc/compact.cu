@@ -179,7 +179,7 @@ struct GlobalTree {  // one program's arrays in global memory
 // position, then one thread per leaf walks its chain in shared memory and
 // writes its vector into a padded staging tile that the block streams out
 // with coalesced 8-byte stores (the vectors of a block are contiguous).
-constexpr int kProgsPerBlock = 64;
+constexpr int kProgsPerBlock = 64;  // (≤ 255: the node → program map is uint8)
 constexpr int kThreads = 256;
 constexpr int kNodeCap = 1280;   // nodes staged per block (3 blocks per SM; 64 programs average ~740)
 constexpr int kVecPitch = 25;    // doubles per staged vector (bank spread)
@@ -204,16 +204,9 @@ struct TileSmem {
   int64_t node_off[kProgsPerBlock + 1], leaf_off[kProgsPerBlock + 1];
   int warp_sum[kThreads / 32];
   uint8_t ann[kNodeCap];
+  uint8_t prog[kNodeCap];  // block-local program of every staged node
 };
 
-__device__ __forceinline__ int find_prog(const int64_t* off, int n, int64_t x) {
-  int lo = 0, hi = n;  // largest p with off[p] <= x
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (off[mid] <= x) lo = mid; else hi = mid;
-  }
-  return lo;
-}
 
 // warp-per-program path for blocks whose programs exceed the node cap
 __device__ void program_warp(const int64_t* __restrict__ node_off,
@@ -297,6 +290,9 @@ __global__ void __launch_bounds__(kThreads) build_compact_kernel(
       }
     }
   }
+  if (t < np)  // node → program map (replaces a binary search per node and per leaf)
+    for (int j = (int)(sm.node_off[t] - gn0); j < (int)(sm.node_off[t + 1] - gn0); ++j)
+      sm.prog[j] = (uint8_t)t;
   // block-wide exclusive scan of is_leaf, 256 nodes per round
   int carry = 0;
   for (int c = 0; c < nodes; c += kThreads) {
@@ -311,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) build_compact_kernel(
     for (int w = 0; w < kThreads / 32; ++w) total += sm.warp_sum[w];
     const int g = before + __popc(ball & ((1u << lane) - 1u));  // block-local leaf rank
     if (j < nodes) {
-      const int p = find_prog(sm.node_off, np, gn0 + j);
+      const int p = sm.prog[j];
       const int64_t pn0 = sm.node_off[p], pl0 = sm.leaf_off[p];
       const int i = (int)(gn0 + j - pn0);              // program-local node id
       const int k = (int)(gl0 + g - pl0);              // leaves before it in the program
@@ -331,7 +327,7 @@ __global__ void __launch_bounds__(kThreads) build_compact_kernel(
     const int g = c + t;
     if (g < leaves) {
       const int j = sm.leaf_node[g];
-      const int p = find_prog(sm.node_off, np, gn0 + j);
+      const int p = sm.prog[j];
       const int base = (int)(sm.node_off[p] - gn0);
       const SmemTree tree{sm.par, sm.ext, sm.ann, base};
       const Chain ch = walk_chain(tree, j - base);
