@@ -85,7 +85,20 @@ __device__ __forceinline__ double log2_1p_int(u128 v) {
   return log2(u128_to_double(v + 1));
 }
 
-constexpr u128 kProductLimit = ((u128)1) << 62;  // features.py:26
+constexpr uint64_t kProductLimit = 1ull << 62;  // features.py:26
+
+// a * e clamped at kProductLimit, exact: a <= 2^62 and e < 2^63, so the full
+// product fits 128 bits and "exceeds the limit" is hi != 0 || lo > limit
+__device__ __forceinline__ uint64_t sat_mul(uint64_t a, uint64_t e, bool& over) {
+  const uint64_t lo = a * e, hi = __umul64hi(a, e);
+  over = hi != 0 || lo > kProductLimit;
+  return over ? kProductLimit : lo;
+}
+
+__device__ __forceinline__ double log2_1p_u64(uint64_t v) {
+  if (v < (uint64_t)kLog2Table) return __ldg(&g_log2_table[(int)v]);
+  return log2(u128_to_double((u128)v + 1));
+}
 
 struct CompactOut {
   double* vectors;
@@ -98,7 +111,7 @@ struct CompactOut {
 // first); Tree gives parent(i) / extent(i) / annot(i) in program-local ids.
 struct Chain {
   int depth;
-  u128 prod, tprod[3];
+  uint64_t prod, tprod[3];  // clamped at kProductLimit (< 2^64)
   int tcount[3];
   int64_t inner, outer;
   bool overflow;
@@ -118,14 +131,16 @@ __device__ __forceinline__ Chain walk_chain(const Tree& t, int32_t leaf) {
     if (c.depth == 0) c.inner = e;
     c.outer = e;
     ++c.depth;
-    c.prod *= (u128)e;
-    if (c.prod > kProductLimit) { c.overflow = true; c.prod = kProductLimit; }
-    for (int q = 0; q < 3; ++q)
-      if (bits >> q & 1u) {
-        ++c.tcount[q];
-        c.tprod[q] *= (u128)e;
-        if (c.tprod[q] > kProductLimit) c.tprod[q] = kProductLimit;
-      }
+    bool over;
+    c.prod = sat_mul(c.prod, (uint64_t)e, over);
+    c.overflow |= over;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {  // branch-free: select the annotated products
+      const bool on = bits >> q & 1u;
+      const uint64_t tp = sat_mul(c.tprod[q], (uint64_t)e, over);
+      c.tcount[q] += on;
+      c.tprod[q] = on ? tp : c.tprod[q];
+    }
   }
   return c;
 }
@@ -133,35 +148,30 @@ __device__ __forceinline__ Chain walk_chain(const Tree& t, int32_t leaf) {
 // compute_vector (features.py:172-206) into v[0..23] (any address space)
 __device__ __forceinline__ void leaf_vector(const Chain& c, const int64_t* __restrict__ st,
                                             int k, int n_leaf, double* v) {
-  const u128 iters = c.depth ? c.prod : (u128)1;
-  v[0] = (double)c.depth;
-  v[1] = c.depth ? log2_1p_int(c.prod) : 0.0;
-  v[2] = c.depth ? log2_1p_int((u128)c.inner) : 0.0;
-  v[3] = c.depth ? log2_1p_int((u128)c.outer) : 0.0;
-  for (int q = 0; q < 3; ++q) {
-    v[4 + q] = (double)c.tcount[q];
-    v[7 + q] = c.tcount[q] ? log2_1p_int(c.tprod[q]) : 0.0;
-  }
+  // stats first: st may be this leaf's own staging row (columns 16..24 of v)
   int64_t s[9];
 #pragma unroll
   for (int q = 0; q < 9; ++q) s[q] = st[q];
-  u128 per_iter = 2 * (u128)s[0];
-#pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    v[10 + q] = log2_1p_int((u128)s[q]);
-    if (q) per_iter += (u128)s[q];
-  }
+  const u128 iters = c.depth ? (u128)c.prod : (u128)1;
+  double2* v2 = reinterpret_cast<double2*>(v);  // 16-byte aligned; pairs stored as they are ready
+  const auto lg = [](uint64_t x, bool on) { return on ? log2_1p_u64(x) : 0.0; };
+  v2[0] = make_double2((double)c.depth, lg(c.prod, c.depth));
+  v2[1] = make_double2(lg((uint64_t)c.inner, c.depth), lg((uint64_t)c.outer, c.depth));
+  v2[2] = make_double2((double)c.tcount[0], (double)c.tcount[1]);
+  v2[3] = make_double2((double)c.tcount[2], lg(c.tprod[0], c.tcount[0]));
+  v2[4] = make_double2(lg(c.tprod[1], c.tcount[1]), lg(c.tprod[2], c.tcount[2]));
+  v2[5] = make_double2(log2_1p_u64((uint64_t)s[0]), log2_1p_u64((uint64_t)s[1]));
+  v2[6] = make_double2(log2_1p_u64((uint64_t)s[2]), log2_1p_u64((uint64_t)s[3]));
+  const u128 per_iter = 2 * (u128)s[0] + (u128)s[1] + (u128)s[2] + (u128)s[3] + (u128)s[4];
   const u128 tot_flops = per_iter * iters;
   const u128 tot_read = (u128)s[5] * iters, tot_written = (u128)s[6] * iters;
-  v[15] = log2_1p_int(tot_flops);
-  v[16] = log2_1p_int((u128)s[5]);
-  v[17] = log2_1p_int((u128)s[6]);
-  v[18] = log2_1p_int(tot_read);
-  v[19] = log2_1p_int(tot_written);
-  v[20] = u128_to_double((u128)s[7]);
-  v[21] = u128_to_double((u128)s[8]);
-  v[22] = div_u128(tot_flops, tot_read + tot_written + 1);
-  v[23] = (double)k / (double)n_leaf;
+  v2[7] = make_double2(log2_1p_u64((uint64_t)s[4]), log2_1p_int(tot_flops));
+  v2[8] = make_double2(log2_1p_u64((uint64_t)s[5]), log2_1p_u64((uint64_t)s[6]));
+  v2[9] = make_double2(log2_1p_int(tot_read), log2_1p_int(tot_written));
+  v2[10] = make_double2(__ull2double_rn((unsigned long long)s[7]),
+                        __ull2double_rn((unsigned long long)s[8]));
+  v2[11] = make_double2(div_u128(tot_flops, tot_read + tot_written + 1),
+                        (double)k / (double)n_leaf);
 }
 
 struct GlobalTree {  // one program's arrays in global memory
@@ -182,7 +192,8 @@ struct GlobalTree {  // one program's arrays in global memory
 constexpr int kProgsPerBlock = 64;  // (≤ 255: the node → program map is uint8)
 constexpr int kThreads = 256;
 constexpr int kNodeCap = 1280;   // nodes staged per block (3 blocks per SM; 64 programs average ~740)
-constexpr int kVecPitch = 25;    // doubles per staged vector (bank spread)
+constexpr int kVecPitch = 26;    // doubles per staged row: 16-byte rows, conflict-free v2 stores
+constexpr int kStatsCol = 16;    // prefetched stats (9 × int64) at columns 16..24 of a row
 
 struct SmemTree {  // block-local ids; base = first node of the program
   const int16_t* par;
@@ -242,7 +253,7 @@ __device__ void program_warp(const int64_t* __restrict__ node_off,
   }
 }
 
-__global__ void __launch_bounds__(kThreads) build_compact_kernel(
+__global__ void __launch_bounds__(kThreads, 3) build_compact_kernel(
     const int64_t* __restrict__ node_off, const int32_t* __restrict__ parent,
     const int64_t* __restrict__ extent, const uint8_t* __restrict__ annot,
     const int64_t* __restrict__ leaf_off, const int64_t* __restrict__ stats, int64_t n_prog,
@@ -290,6 +301,17 @@ __global__ void __launch_bounds__(kThreads) build_compact_kernel(
       }
     }
   }
+  // this block's first 256 leaf stats rows → columns 16..24 of the staging
+  // rows of the threads that will own them (coalesced 8-byte cp.async; each
+  // thread reads its own row's stats before it writes the vector over them)
+  const int pre = min(leaves, kThreads) * 9;
+  for (int e = t; e < pre; e += kThreads) {
+    const int r = e / 9, q = e - r * 9;
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(sm.vec + r * kVecPitch + kStatsCol + q);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                 "l"(stats + (gl0 * 9 + e)) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
   if (t < np)  // node → program map (replaces a binary search per node and per leaf)
     for (int j = (int)(sm.node_off[t] - gn0); j < (int)(sm.node_off[t + 1] - gn0); ++j)
       sm.prog[j] = (uint8_t)t;
@@ -322,6 +344,8 @@ __global__ void __launch_bounds__(kThreads) build_compact_kernel(
     carry += total;
     __syncthreads();  // warp_sum reuse
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
   // one thread per leaf, staged vectors, coalesced stores
   for (int c = 0; c < leaves; c += kThreads) {
     const int g = c + t;
@@ -334,17 +358,22 @@ __global__ void __launch_bounds__(kThreads) build_compact_kernel(
       if (ch.overflow) atomicMin(out.first_bad, (unsigned long long)(p0 + p));
       const int k = (int)(gl0 + g - sm.leaf_off[p]);
       const int n_leaf = (int)(sm.leaf_off[p + 1] - sm.leaf_off[p]);
-      leaf_vector(ch, stats + (gl0 + g) * 9, k, n_leaf, sm.vec + t * kVecPitch);
+      double* row = sm.vec + t * kVecPitch;
+      const int64_t* st = c == 0 ? reinterpret_cast<const int64_t*>(row + kStatsCol)
+                                 : stats + (gl0 + g) * 9;
+      leaf_vector(ch, st, k, n_leaf, row);
     }
     // each warp writes its own 32 consecutive leaves (a contiguous 6 KB run,
     // coalesced) from its part of the staging tile: warp barriers only
     __syncwarp();
     const int w0 = c + 32 * warp;
     const int n = max(0, min(32, leaves - w0));
-    double* dst = out.vectors + (gl0 + w0) * TPCB_FEAT;
-    for (int e = lane; e < n * TPCB_FEAT; e += 32) {
-      const int r = e / TPCB_FEAT, col = e - r * TPCB_FEAT;
-      dst[e] = sm.vec[(32 * warp + r) * kVecPitch + col];
+    double2* dst = reinterpret_cast<double2*>(out.vectors + (gl0 + w0) * TPCB_FEAT);
+    const double2* src = reinterpret_cast<const double2*>(sm.vec + 32 * warp * kVecPitch);
+    // 12 double2 per row; lane + 32 i walks 8 rows every 3 steps
+    for (int e = lane; e < n * (TPCB_FEAT / 2); e += 32) {
+      const int r = e / (TPCB_FEAT / 2), col = e - r * (TPCB_FEAT / 2);
+      dst[e] = src[r * (kVecPitch / 2) + col];
     }
     __syncwarp();
   }
