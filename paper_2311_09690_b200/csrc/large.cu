@@ -252,12 +252,22 @@ __global__ void __launch_bounds__(192, 1)
     // once `done` fired); pass 2: 8 lanes per row, float4 per lane — residual,
     // ReLU / mask and the output stores as 128-byte row segments (coalesced),
     // instead of one 16-byte store per thread per row.  Same arithmetic.
-    mbar_wait(&done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     float* stile = reinterpret_cast<float*>(smem);
     constexpr int kLd = 36;  // floats per staged row (16-byte aligned, spreads banks)
+    constexpr int kRows = kTileM / 16;  // pass-2 rows per thread per chunk
     const int r_loc = 32 * warp + lane;
     const int sub = lane & 7, rq = lane >> 3;  // pass 2: column quad, row in the group
+    // residual (hi, lo) and ReLU-mask quads of a chunk: all of a thread's
+    // loads issued before the first is used (not one dependent round trip
+    // per staged row)
+    const bool vec_ok = ((e.ldr | e.ldm) & 3) == 0 &&
+                        (((uintptr_t)e.r_hi | (uintptr_t)e.r_lo | (uintptr_t)e.mask) & 15) == 0;
+    constexpr int kHalf = kRows / 2;  // rows whose loads are in flight together (measured: 2 > 4, 8 rows)
+    float4 rh[kHalf], rl[kHalf], mk[kHalf];
+    const bool epi_loads = e.r_hi || e.mask;
+    mbar_wait(&done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
     for (int ch = 0; ch < NT / 32; ++ch) {
       const int c0 = n0 + 32 * ch;
       if (c0 >= e.ldc) break;  // warp-uniform
@@ -279,35 +289,61 @@ __global__ void __launch_bounds__(192, 1)
       }
       group_bar(1, 128);
       const int col = c0 + 4 * sub;
-      for (int rr = 4 * warp + rq; rr < kTileM; rr += 16) {
-        const int row = m0 + rr;
-        if (row >= e.M) break;
-        float4 x = *reinterpret_cast<const float4*>(stile + rr * kLd + 4 * sub);
-        float* xs = &x.x;
+#pragma unroll 1
+      for (int i0 = 0; i0 < kRows; i0 += kHalf) {
+        if (epi_loads) {  // issue kHalf rows' loads together
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int cc = col + u;
-          float t = xs[u];
-          if (cc < e.N) {
-            if (e.r_hi) {
-              const size_t ri = (size_t)row * e.ldr + cc;
-              t += e.r_hi[ri] + (e.r_lo ? e.r_lo[ri] : 0.f);
+          for (int q = 0; q < kHalf; ++q) {
+            const int row = m0 + 4 * warp + rq + 16 * (i0 + q);
+            const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            rh[q] = z; rl[q] = z; mk[q] = make_float4(1.f, 1.f, 1.f, 1.f);
+            if (row < e.M && col < e.N) {
+              const size_t ri = (size_t)row * e.ldr + col, mi = (size_t)row * e.ldm + col;
+              if (vec_ok && col + 4 <= e.N) {
+                if (e.r_hi) rh[q] = __ldg(reinterpret_cast<const float4*>(e.r_hi + ri));
+                if (e.r_lo) rl[q] = __ldg(reinterpret_cast<const float4*>(e.r_lo + ri));
+                if (e.mask) mk[q] = __ldg(reinterpret_cast<const float4*>(e.mask + mi));
+              } else {
+                float* h = &rh[q].x; float* l = &rl[q].x; float* m = &mk[q].x;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  if (col + u < e.N) {
+                    if (e.r_hi) h[u] = e.r_hi[ri + u];
+                    if (e.r_lo) l[u] = e.r_lo[ri + u];
+                    if (e.mask) m[u] = e.mask[mi + u];
+                  }
+              }
             }
-            if (e.relu) t = fmaxf(t, 0.f);
-            if (e.mask && !(e.mask[(size_t)row * e.ldm + cc] > 0.f)) t = 0.f;
-          } else {
-            t = 0.f;
           }
-          xs[u] = t;
         }
-        if (e.c) {
-          *reinterpret_cast<float4*>(e.c + blockIdx.z * e.split_stride + (size_t)row * e.ldc + col) = x;
-        } else {
-          float4 h, l;
-          h.x = tf32_hi(x.x); h.y = tf32_hi(x.y); h.z = tf32_hi(x.z); h.w = tf32_hi(x.w);
-          l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
-          *reinterpret_cast<float4*>(e.c_hi + (size_t)row * e.ldc + col) = h;
-          *reinterpret_cast<float4*>(e.c_lo + (size_t)row * e.ldc + col) = l;
+#pragma unroll
+        for (int ih = 0; ih < kHalf; ++ih) {
+          const int rr = 4 * warp + rq + 16 * (i0 + ih), row = m0 + rr;
+          float4 x = *reinterpret_cast<const float4*>(stile + rr * kLd + 4 * sub);
+          float* xs = &x.x;
+          const float* h = &rh[ih].x; const float* l = &rl[ih].x; const float* m = &mk[ih].x;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float t = xs[u];
+            if (col + u < e.N) {
+              if (e.r_hi) t += h[u] + l[u];
+              if (e.relu) t = fmaxf(t, 0.f);
+              if (e.mask && !(m[u] > 0.f)) t = 0.f;
+            } else {
+              t = 0.f;
+            }
+            xs[u] = t;
+          }
+          if (row >= e.M) continue;
+          if (e.c) {
+            *reinterpret_cast<float4*>(e.c + blockIdx.z * e.split_stride + (size_t)row * e.ldc + col) = x;
+          } else {
+            float4 hh, ll;
+            hh.x = tf32_hi(x.x); hh.y = tf32_hi(x.y); hh.z = tf32_hi(x.z); hh.w = tf32_hi(x.w);
+            ll.x = x.x - hh.x; ll.y = x.y - hh.y; ll.z = x.z - hh.z; ll.w = x.w - hh.w;
+            *reinterpret_cast<float4*>(e.c_hi + (size_t)row * e.ldc + col) = hh;
+            *reinterpret_cast<float4*>(e.c_lo + (size_t)row * e.ldc + col) = ll;
+          }
         }
       }
       group_bar(1, 128);
