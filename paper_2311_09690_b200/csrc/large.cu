@@ -105,7 +105,7 @@ struct Epi {
   const float* mask = nullptr;  // ReLU backward: keep x where mask[row, col] > 0
   int ldm = 0;
   int64_t split_stride = 0;     // split-K: split z writes c + z * split_stride
-  int dbg = 0;                  // probe: 1 = skip the MMAs (TMA stream only)
+  int dbg = 0;                  // probe: 1 = skip the MMAs (TMA stream only), 2 = skip both
 };
 
 constexpr int kTileM = 128;
@@ -199,6 +199,10 @@ __global__ void __launch_bounds__(192, 1)
       const int s = it % S;
       if (it >= S) mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
       uint8_t* st = smem + s * Cfg::kStage;
+      if (e.dbg == 2) {  // probe: no operand traffic (epilogue + pipeline skeleton)
+        mbar_arrive_expect_tx(&full[s], 0);
+        continue;
+      }
       mbar_arrive_expect_tx(&full[s], Cfg::kStage);
       const int kx = (k0 + it) * BK;
       if constexpr (CN == 1) {
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t a_lo = a_hi + kSlabA, b_hi = a_hi + 2 * kSlabA, b_lo = b_hi + Cfg::kSlabB;
 #pragma unroll
       for (int kk = 0; kk < BK / 8; ++kk) {
-        if (e.dbg == 1) break;
+        if (e.dbg != 0) break;
         const uint32_t o = kk * 32;
         // the two correction products accumulate in their own TMEM tile
         // (columns NT..2NT): the main accumulator then takes K/8 rounding
@@ -374,35 +378,60 @@ struct ImgEntry {
   int plain, dst_ld, ncols_real;
 };
 
+// segment map of the k index: image position q → W row (−1: zero pad)
+__device__ __forceinline__ int image_k(const ImgEntry& E, int q) {
+  if (E.seg) {
+    const int sgi = q / E.segp, j = q - sgi * E.segp;
+    return j < E.seg ? sgi * E.seg + j : -1;
+  }
+  return q < E.k_real ? q : -1;
+}
+
+// 32 × 32 tiles of one entry per block iteration (blockDim 32 × 8): plain
+// entries copy rows (coalesced both ways); transposed ones read 32 W rows ×
+// 32 consecutive columns and write 32 image rows × 32 consecutive k through a
+// padded shared tile (the per-element transposed read of round 1 touched a
+// 32-byte sector per float)
 __global__ void build_image_kernel(const float* __restrict__ P, const ImgEntry* __restrict__ ents,
                                    int n_ents, float* __restrict__ img_hi,
                                    float* __restrict__ img_lo) {
+  __shared__ float tile[32][33];
   const ImgEntry E = ents[blockIdx.y];
-  const int64_t total = (int64_t)E.n * E.kp;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int n = (int)(i / E.kp), kq = (int)(i - (int64_t)n * E.kp);
-    // transposed: segment mapping on the k (column) index; plain: on the row
-    const int q = E.plain ? n : kq;
-    int k = -1;
-    if (E.seg) {
-      const int sgi = q / E.segp, j = q - sgi * E.segp;
-      if (j < E.seg) k = sgi * E.seg + j;
-    } else if (q < E.k_real) {
-      k = q;
-    }
-    float v;
-    int64_t o;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tk = (E.kp + 31) / 32, tiles = ((E.n + 31) / 32) * tk;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int n0 = (t / tk) * 32, k0 = (t % tk) * 32;
     if (E.plain) {
-      v = (k >= 0 && kq < E.ncols_real) ? P[E.src + (int64_t)k * E.n_src + E.col0 + kq] : 0.f;
-      o = E.dst + (int64_t)n * E.dst_ld + kq;
-    } else {
-      v = k >= 0 ? P[E.src + (int64_t)k * E.n_src + E.col0 + n] : 0.f;
-      o = E.dst + i;
+      for (int r = ty; r < 32; r += 8) {
+        const int n = n0 + r, kq = k0 + tx;
+        if (n >= E.n || kq >= E.kp) continue;
+        const int k = image_k(E, n);
+        const float v =
+            (k >= 0 && kq < E.ncols_real) ? P[E.src + (int64_t)k * E.n_src + E.col0 + kq] : 0.f;
+        const int64_t o = E.dst + (int64_t)n * E.dst_ld + kq;
+        const float h = tf32_hi(v);
+        img_hi[o] = h;
+        img_lo[o] = v - h;
+      }
+      continue;
     }
-    const float h = tf32_hi(v);
-    img_hi[o] = h;
-    img_lo[o] = v - h;
+    for (int r = ty; r < 32; r += 8) {
+      const int kq = k0 + r, n = n0 + tx;
+      const int k = kq < E.kp ? image_k(E, kq) : -1;
+      tile[r][tx] = (k >= 0 && n < E.n) ? P[E.src + (int64_t)k * E.n_src + E.col0 + n] : 0.f;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int n = n0 + r, kq = k0 + tx;
+      if (n < E.n && kq < E.kp) {
+        const float v = tile[tx][r];
+        const int64_t o = E.dst + (int64_t)n * E.kp + kq;
+        const float h = tf32_hi(v);
+        img_hi[o] = h;
+        img_lo[o] = v - h;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -1098,7 +1127,7 @@ extern "C" int tpcb_large_prepare(const tpcb_model* m, const float* d_params, vo
                                     cudaMemcpyHostToDevice, st));
   }
   const int n_ents = (with_backward & 1) ? (int)p.ents.size() : p.n_ents_fwd;
-  build_image_kernel<<<dim3(64, (unsigned)n_ents), 256, 0, st>>>(d_params, im.ents, n_ents, im.hi,
+  build_image_kernel<<<dim3(64, (unsigned)n_ents), dim3(32, 8), 0, st>>>(d_params, im.ents, n_ents, im.hi,
                                                                  im.lo);
   qkv_bias_kernel<<<dim3(8, m->dev.n_layers), 256, 0, st>>>(d_params, m->dev, d_off, im.bias);
   TPCB_LAUNCH_CHECK("large_prepare");
