@@ -198,6 +198,39 @@ def test_gpu_builder_oversized_blocks_take_the_warp_path(rng):
 
 
 @pytest.mark.gpu
+def test_gpu_builder_extent_products_at_the_guard(rng):
+    """64-bit saturating chain products (compact.cu sat_mul): products that
+    land exactly on 2^62, single extents up to 2^62, annotated sub-products,
+    and huge per-leaf counts (flop totals beyond 2^64) — bit-exact integer
+    entries and <= 2 ulp log2 against the oracle; one step past the guard
+    raises like the reference."""
+    from paper_2311_09690_b200 import ir
+    from paper_2311_09690_b200.forest import FlatForest, build_compact
+    st = lambda: ir.ComputeStats(*(int(x) for x in rng.integers(2 ** 50, 2 ** 55, 9)))  # noqa: E731
+    ann = frozenset({"unroll", "parallel"})
+    chains = [[2 ** 62], [2 ** 31, 2 ** 31], [2 ** 20, 2 ** 21, 2 ** 21], [3, 2 ** 60],
+              [2 ** 61 - 1, 2], [7, 11, 13, 2 ** 40], [1, 1, 2 ** 62], [2 ** 32 - 1, 2 ** 30]]
+    progs = []
+    for i, ch in enumerate(chains):
+        node = ir.leaf(f"x{i}", st())
+        for j, e in enumerate(ch):
+            node = ir.loop(ir.LoopInfo(f"l{j}", e, ann if j % 2 else frozenset({"vectorize"})),
+                           [node])
+        progs.append(ir.make_program(f"p{i}", node))
+    f = FlatForest.from_programs(progs)
+    want = oc.build_forest(f.node_off, f.parent, f.extent, f.annot, f.leaf_off, f.stats)
+    hosts = build_compact(f).to_host()
+    gv = np.concatenate([h.leaf_vectors for h in hosts])
+    wv = np.concatenate([w[0] for w in want])
+    assert np.array_equal(gv[:, INT_COLS + [22, 23]], wv[:, INT_COLS + [22, 23]])
+    assert _ulps(gv, wv).max() <= 2
+    over = ir.make_program("over", ir.loop(ir.LoopInfo("a", 2 ** 31 + 1), [
+        ir.loop(ir.LoopInfo("b", 2 ** 31), [ir.leaf("y", st())])]))
+    with pytest.raises(OverflowError):
+        build_compact(FlatForest.from_programs(progs[:3] + [over]))
+
+
+@pytest.mark.gpu
 def test_gpu_builder_errors_follow_reference_order():
     from paper_2311_09690_b200 import ir
     from paper_2311_09690_b200.errors import LeafCountExceeded
