@@ -190,6 +190,7 @@ struct GlobalTree {  // one program's arrays in global memory
 // writes its vector into a padded staging tile that the block streams out
 // with coalesced 8-byte stores (the vectors of a block are contiguous).
 constexpr int kProgsPerBlock = 64;  // (≤ 255: the node → program map is uint8)
+static_assert(4 * kProgsPerBlock <= 256, "four map-filling threads per program");
 constexpr int kThreads = 256;
 constexpr int kNodeCap = 1280;   // nodes staged per block (3 blocks per SM; 64 programs average ~740)
 constexpr int kVecPitch = 26;    // doubles per staged row: 16-byte rows, conflict-free v2 stores
@@ -312,9 +313,14 @@ __global__ void __launch_bounds__(kThreads, 3) build_compact_kernel(
                  "l"(stats + (gl0 * 9 + e)) : "memory");
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
-  if (t < np)  // node → program map (replaces a binary search per node and per leaf)
-    for (int j = (int)(sm.node_off[t] - gn0); j < (int)(sm.node_off[t + 1] - gn0); ++j)
-      sm.prog[j] = (uint8_t)t;
+  {  // node → program map (replaces a binary search per node and per leaf):
+     // four threads per program, interleaved over its nodes
+    const int q = t >> 2;
+    if (q < np) {
+      const int j0 = (int)(sm.node_off[q] - gn0), j1 = (int)(sm.node_off[q + 1] - gn0);
+      for (int j = j0 + (t & 3); j < j1; j += 4) sm.prog[j] = (uint8_t)q;
+    }
+  }
   // block-wide exclusive scan of is_leaf, 256 nodes per round
   int carry = 0;
   for (int c = 0; c < nodes; c += kThreads) {
