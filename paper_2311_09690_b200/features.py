@@ -110,6 +110,33 @@ def encode_input(compact: CompactAst, device: DeviceSpec,
     return EncodedInput(matrix=matrix, device_vector=device_vector(device))
 
 
+def compute_vector(leaf, enclosing, leaf_index: int, n_leaf: int) -> np.ndarray:
+    """The 24-entry computation vector of one leaf under its enclosing loops,
+    outermost first (features.py:168-203), float64.  Computed by the device
+    builder K0 on a one-leaf chain program — the same kernel and arithmetic
+    as build_compact_ast (exact integer entries, exact quotient, table /
+    device log2) —; entry 23 is the caller's position leaf_index / n_leaf.
+    Raises OverflowError when the extent product exceeds 2^62."""
+    from . import ir
+    from .forest import COUNT_LIMIT, FlatForest, build_compact
+    enclosing = list(enclosing)
+    # no tree validation here (the reference's helper has none: an all-zero
+    # leaf is fine); only what K0's exact arithmetic needs — extents >= 1
+    # (0 marks a leaf in the node arrays) and counts in 0..2^56
+    if any(int(lp.extent) < 1 for lp in enclosing):
+        raise ValidationError("loop extents must be >= 1")
+    if any(not 0 <= int(getattr(leaf, f)) < COUNT_LIMIT for f in ir.ComputeStats.FIELDS):
+        raise ValidationError("ComputeStats counts must be in 0..2^56")
+    node = ir.leaf("leaf", leaf)
+    for lp in reversed(enclosing):
+        node = ir.loop(lp, [node])
+    prog = ir.ProgramAst(root=node, name="compute_vector", n_leaf=1)
+    dc = build_compact(FlatForest.from_programs([prog]), validate=False)
+    v = dc.to_host()[0].leaf_vectors[0].copy()
+    v[23] = leaf_index / n_leaf
+    return v
+
+
 def build_compact_ast(ast, max_leaves: int | None = None) -> CompactAst:
     """Serialize a program tree pre-order (marker after each leaf) and build
     its leaf computation vectors (features.py:209-245) — one program through

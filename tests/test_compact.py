@@ -198,6 +198,39 @@ def test_gpu_builder_oversized_blocks_take_the_warp_path(rng):
 
 
 @pytest.mark.gpu
+def test_gpu_compute_vector_matches_oracle(rng):
+    """features.compute_vector (features.py:168-203) through K0: the
+    reference test_features.py examples plus random chains, vs the oracle's
+    leaf_vector; loop-free leaves, annotations, leaf position, overflow."""
+    import math
+    from paper_2311_09690_b200 import ir
+    from paper_2311_09690_b200.features import compute_vector
+    st = ir.ComputeStats(fma_count=2, bytes_read=16, bytes_written=8)
+    v = compute_vector(st, [ir.LoopInfo("i", 4)], 0, 1)
+    assert v[0] == 1 and v[1] == math.log2(5) and v[15] == math.log2(1 + 16)
+    v0 = compute_vector(ir.ComputeStats(), [], 1, 2)
+    want = np.zeros(24)
+    want[23] = 0.5
+    assert np.array_equal(v0, want)
+    with pytest.raises(OverflowError):
+        compute_vector(ir.ComputeStats(fma_count=1), [ir.LoopInfo("a", 2 ** 32),
+                                                      ir.LoopInfo("b", 2 ** 31)], 0, 1)
+    bits = {"vectorize": 1, "unroll": 2, "parallel": 4}
+    for _ in range(40):
+        counts = [int(x) for x in rng.integers(0, 2 ** 30, 9)]
+        loops = [ir.LoopInfo(f"l{j}", int(rng.integers(1, 2 ** 12)),
+                             frozenset(a for a in bits if rng.random() < .4))
+                 for j in range(int(rng.integers(0, 5)))]
+        n = int(rng.integers(1, 9))
+        k = int(rng.integers(0, n))
+        got = compute_vector(ir.ComputeStats(*counts), loops, k, n)
+        exp = oc.leaf_vector(counts, [(lp.extent, sum(bits[a] for a in lp.annotations))
+                                      for lp in loops], k, n)
+        assert np.array_equal(got[INT_COLS + [22, 23]], exp[INT_COLS + [22, 23]])
+        assert _ulps(got[None], exp[None]).max() <= 2
+
+
+@pytest.mark.gpu
 def test_gpu_builder_extent_products_at_the_guard(rng):
     """64-bit saturating chain products (compact.cu sat_mul): products that
     land exactly on 2^62, single extents up to 2^62, annotated sub-products,
