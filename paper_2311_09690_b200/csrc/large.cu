@@ -456,6 +456,20 @@ __global__ void gather_tokens_kernel(const float* __restrict__ px, const int32_t
 
 // per (AST, head): ctx = softmax(q kᵀ / sqrt(dh)) v over the AST's own L rows
 // (nn.py:79-96); writes the (hi, lo) pair, zeroes the pad columns
+// lanes per score pair in the attention kernels: the L² dot products over
+// the head dimension are split across groups of g lanes (g a power of two,
+// g · L² <= 128 threads) and summed by an xor tree — at the typical L of
+// 3–4 a thread used to walk all dh = 179 products of its pair alone
+__device__ __forceinline__ int score_group(int L) {
+  int g = 32;
+  while (g > 1 && g * L * L > 128) g >>= 1;
+  return g;
+}
+__device__ __forceinline__ float group_sum(float v, int g) {
+  for (int o = g >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __global__ void attention_kernel(const float* __restrict__ qkv, int ldq,
                                  const int32_t* __restrict__ tok_off, int d, int nh, int dh,
                                  float scale, int ldc, float* __restrict__ c_hi,
@@ -476,11 +490,16 @@ __global__ void attention_kernel(const float* __restrict__ qkv, int ldq,
     v[l * dhp + j] = row[2 * d];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
-    const int i = e / L, j = e - i * L;
-    float acc = 0.f;
-    for (int c = 0; c < dh; ++c) acc = fmaf(q[i * dhp + c], k[j * dhp + c], acc);
-    p[i * 17 + j] = acc * scale;
+  {
+    const int g = score_group(L), sl = threadIdx.x & (g - 1), ng = blockDim.x / g;
+    for (int e0 = 0; e0 < L * L; e0 += ng) {  // uniform trip count: full-warp shuffles
+      const int e = e0 + threadIdx.x / g, i = e / L, j = e - i * L;
+      float acc = 0.f;
+      if (e < L * L)
+        for (int c = sl; c < dh; c += g) acc = fmaf(q[i * dhp + c], k[j * dhp + c], acc);
+      acc = group_sum(acc, g);
+      if (e < L * L && sl == 0) p[i * 17 + j] = acc * scale;
+    }
   }
   __syncthreads();
   if (threadIdx.x < L) {
@@ -1514,15 +1533,23 @@ __global__ void attention_back_kernel(const float* __restrict__ qkv, int ldq,
     dc[l * dhp + j] = dctx[(size_t)(t0 + l) * ldc + h * dh + j];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < L * L; e += blockDim.x) {
-    const int i = e / L, j = e - i * L;
-    float acc = 0.f, acc2 = 0.f;
-    for (int c = 0; c < dh; ++c) {
-      acc = fmaf(q[i * dhp + c], k[j * dhp + c], acc);
-      acc2 = fmaf(dc[i * dhp + c], v[j * dhp + c], acc2);
+  {
+    const int g = score_group(L), sl = threadIdx.x & (g - 1), ng = blockDim.x / g;
+    for (int e0 = 0; e0 < L * L; e0 += ng) {  // uniform trip count: full-warp shuffles
+      const int e = e0 + threadIdx.x / g, i = e / L, j = e - i * L;
+      float acc = 0.f, acc2 = 0.f;
+      if (e < L * L)
+        for (int c = sl; c < dh; c += g) {
+          acc = fmaf(q[i * dhp + c], k[j * dhp + c], acc);
+          acc2 = fmaf(dc[i * dhp + c], v[j * dhp + c], acc2);
+        }
+      acc = group_sum(acc, g);
+      acc2 = group_sum(acc2, g);
+      if (e < L * L && sl == 0) {
+        p[i * 17 + j] = acc * scale;
+        dp[i * 17 + j] = acc2;
+      }
     }
-    p[i * 17 + j] = acc * scale;
-    dp[i * 17 + j] = acc2;
   }
   __syncthreads();
   if (threadIdx.x < L) {
