@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(192, 1)
                                              ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full[S], empty[S], done;
   __shared__ uint32_t tmem_base;
+  __shared__ float sbias[NT];  // the tile's bias columns (epilogue)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * NT, m0 = blockIdx.y * kTileM;
   const int k0 = blockIdx.z * kc;
@@ -269,6 +270,10 @@ __global__ void __launch_bounds__(192, 1)
     constexpr int kHalf = kRows / 2;  // rows whose loads are in flight together (measured: 2 > 4, 8 rows)
     float4 rh[kHalf], rl[kHalf], mk[kHalf];
     const bool epi_loads = e.r_hi || e.mask;
+    if (e.bias) {  // staged while the k-loop runs (was a global load per element)
+      for (int c = threadIdx.x; c < NT; c += 128) sbias[c] = n0 + c < e.N ? e.bias[n0 + c] : 0.f;
+      group_bar(1, 128);
+    }
     mbar_wait(&done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int u = 0; u < 4; ++u) {
           const int j = 4 * q + u;
           float t = v[j] + w[j];
-          if (e.bias && c0 + j < e.N) t += __ldg(e.bias + c0 + j);
+          if (e.bias && c0 + j < e.N) t += sbias[32 * ch + j];
           xs[u] = t;
         }
         *reinterpret_cast<float4*>(stile + r_loc * kLd + 4 * q) = x;
