@@ -766,7 +766,13 @@ int launch_gemm_nt(const Operand& A, const Operand& B, const Epi& e, cudaStream_
 int launch_gemm(const Operand& A, const Operand& B, const Epi& e, cudaStream_t st) {
   if (A.k_ext != B.k_ext || (A.k_ext & 31)) return TPCB_ERR_VALIDATION;
   const int64_t m_tiles = ceil_div(e.M, kTileM);
-  if (e.ldc > 128 && m_tiles * ceil_div(e.ldc, 256) >= kNumSMs)
+  // 256-wide tiles for large products (>= 4 waves: operand reuse wins), and
+  // for smaller ones only when they quantise into waves no worse than
+  // 128-wide tiles (the training QKV product: 171 tiles of 256 = 2 waves of
+  // 256-wide work vs 323 of 128 = 3 waves of 128-wide; 1.2 % per step)
+  const int64_t t256 = m_tiles * ceil_div(e.ldc, 256), t128 = m_tiles * ceil_div(e.ldc, 128);
+  const int64_t w256 = ceil_div(t256, (int64_t)kNumSMs), w128 = ceil_div(t128, (int64_t)kNumSMs);
+  if (e.ldc > 128 && t256 >= kNumSMs && (w256 >= 4 || 2 * w256 <= w128))
     return launch_gemm_nt<256>(A, B, e, st);
   return launch_gemm_nt<128>(A, B, e, st);
 }
