@@ -1741,7 +1741,9 @@ struct Bwd {
   float* dctx;               // [T, dp]
   float *dq_hi, *dq_lo;      // [T, qkvp]
   float* prod;               // [T, max(dp, dmax)]
-  float *xt_hi, *xt_lo, *yt_hi, *yt_lo;
+  // transposed weight-gradient operands, a ring of kXtRing sets: the main
+  // stream fills set k while the side stream's GEMMs still read the others
+  float *xt_hi[3], *xt_lo[3], *yt_hi[3], *yt_lo[3];
   float* part;
   float *dd_hi[2], *dd_lo[2];  // decoder grads [A, dmax]
   float* dz;                 // [A, dep]
@@ -1771,10 +1773,12 @@ Bwd carve_bwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, 
   b.prod = cv->take(max(T * p.dp, A * (int64_t)dmax));
   const int64_t wmax = max(max(p.qkvp, p.ffp), max(p.dp, dmax));
   const int64_t xt = max(wmax * (T + 32), (int64_t)p.dp * (T + 32 * TPCB_MAX_LEAF + 32));
-  b.xt_hi = cv->take(xt);
-  b.xt_lo = cv->take(xt);
-  b.yt_hi = cv->take(xt);
-  b.yt_lo = cv->take(xt);
+  for (int k = 0; k < 3; ++k) {
+    b.xt_hi[k] = cv->take(xt);
+    b.xt_lo[k] = cv->take(xt);
+    b.yt_hi[k] = cv->take(xt);
+    b.yt_lo[k] = cv->take(xt);
+  }
   const int64_t pm = max(max((int64_t)M.d * p.qkvp, (int64_t)M.d_ff * p.dp),
                          max((int64_t)M.d * p.ffp, (int64_t)TPCB_MAX_LEAF * p.dp * p.dep));
   b.part_floats = 8 * max(pm, (int64_t)dmax * dmax);
@@ -1811,10 +1815,14 @@ thread_local unsigned* g_colsum_cnt = nullptr;  // per-stripe counters (zeroed p
 // the weight-gradient branch runs on a side stream: dW = Xᵀ·dY only needs
 // dY, so it overlaps the main stream's dX chain; the main stream waits only
 // for the transposes (after which dY may be overwritten)
+constexpr int kXtRing = 3;
 struct SideStream {
   cudaStream_t s = nullptr;
   cudaEvent_t ev[4] = {};
   int k = 0;
+  cudaEvent_t xt_ev[kXtRing] = {};  // the side GEMM that last read transposed set k
+  bool xt_used[kXtRing] = {};
+  int xt_slot = 0;
   cudaEvent_t next() { return ev[k++ & 3]; }
 };
 thread_local SideStream g_side;
@@ -1823,6 +1831,7 @@ int side_init() {
   if (g_side.s) return TPCB_OK;
   TPCB_CUDA_CHECK(cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking));
   for (auto& e : g_side.ev) TPCB_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (auto& e : g_side.xt_ev) TPCB_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   return TPCB_OK;
 }
 
@@ -1852,17 +1861,25 @@ int colsum(const float* x, const float* x_lo, int rows, int cols, int ld, ColDst
 ColDst one(int64_t off, int colw, int acc = 0) { return ColDst{colw, {off, off, off}, acc}; }
 
 // dW[M_in, N_out] = Xᵀ·dY over K = kp rows: X given as [rows, M_in] (ld_x),
-// dY as [rows, N_out] (ld_y) — both transposed + split here
+// dY as [rows, N_out] (ld_y) — both transposed + split on the main stream
+// into the next set of the transposed-operand ring, the GEMM + reduction
+// forked to the side stream.  The main stream never waits for the side
+// stream's GEMMs except before refilling a ring set the side stream may
+// still be reading (kXtRing wgrads later) and at the final join.
 int wgrad(const Ctx& c, Bwd& b, const float* x_hi, const float* x_lo, int ld_x, int m_in,
           const float* y_hi, const float* y_lo, int ld_y, int n_out, int rows, int seg, int segp,
           ColDst dst, float* grad) {
   const cudaStream_t st = g_side.s;
   const int kp = pad32(rows);
   int rc;
-  if ((rc = stream_wait(st, c.st))) return rc;  // fork: dY is ready on the main stream
-  if ((rc = transpose_into(x_hi, x_lo, rows, m_in, ld_x, b.xt_hi, b.xt_lo, kp, st))) return rc;
-  if ((rc = transpose_into(y_hi, y_lo, rows, n_out, ld_y, b.yt_hi, b.yt_lo, kp, st))) return rc;
-  if ((rc = stream_wait(c.st, st))) return rc;  // main may overwrite dY after the copies
+  const int k = g_side.xt_slot;
+  g_side.xt_slot = (k + 1) % kXtRing;
+  if (g_side.xt_used[k]) TPCB_CUDA_CHECK(cudaStreamWaitEvent(c.st, g_side.xt_ev[k], 0));
+  if ((rc = transpose_into(x_hi, x_lo, rows, m_in, ld_x, b.xt_hi[k], b.xt_lo[k], kp, c.st)))
+    return rc;
+  if ((rc = transpose_into(y_hi, y_lo, rows, n_out, ld_y, b.yt_hi[k], b.yt_lo[k], kp, c.st)))
+    return rc;
+  if ((rc = stream_wait(st, c.st))) return rc;  // fork: the transposed operands are ready
   const int ldc = pad32(n_out);
   const int tiles = ceil_div(m_in, kTileM) * ceil_div(ldc, 128);
   const int k_total = kp / 32;
@@ -1870,8 +1887,10 @@ int wgrad(const Ctx& c, Bwd& b, const float* x_hi, const float* x_lo, int ld_x, 
   if ((size_t)splits * m_in * ldc > b.part_floats) return TPCB_ERR_VALIDATION;
   Epi e{m_in, n_out, ldc, nullptr, 0, nullptr, nullptr, 0, b.part, nullptr, nullptr};
   e.split_stride = (int64_t)m_in * ldc;
-  Operand A{b.xt_hi, b.xt_lo, m_in, kp, kp}, B{b.yt_hi, b.yt_lo, n_out, kp, kp};
+  Operand A{b.xt_hi[k], b.xt_lo[k], m_in, kp, kp}, B{b.yt_hi[k], b.yt_lo[k], n_out, kp, kp};
   if ((rc = launch_gemm_nt<128>(A, B, e, st, splits, &splits))) return rc;
+  TPCB_CUDA_CHECK(cudaEventRecord(g_side.xt_ev[k], st));
+  g_side.xt_used[k] = true;
   const int64_t total = (int64_t)m_in * n_out;
   reduce_grad_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, kNumSMs * 8), 256, 0, st>>>(
       b.part, splits, e.split_stride, m_in, n_out, ldc, seg, segp, dst, grad);
