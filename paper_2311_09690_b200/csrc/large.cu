@@ -1269,24 +1269,29 @@ namespace {
 
 // [rows, cols] (row stride ld; pair or fp32 when a_lo == null) → pair
 // [cols][ldo], zero for rows <= r < ldo
+// ones_col >= 0: that output row is all ones over the real rows (the bias
+// gradient folded into the weight-gradient GEMM as one more product row)
 __global__ void transpose_pair_kernel(const float* __restrict__ a_hi, const float* __restrict__ a_lo,
                                       int rows, int cols, int ld, float* __restrict__ o_hi,
-                                      float* __restrict__ o_lo, int ldo) {
+                                      float* __restrict__ o_lo, int ldo, int ones_col) {
   __shared__ float t[32][33];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
     float v = 0.f;
-    if (r < rows && c < cols) {
+    if (c == ones_col) {
+      v = r < rows ? 1.f : 0.f;
+    } else if (r < rows && c < cols) {
       v = a_hi[(size_t)r * ld + c];
       if (a_lo) v += a_lo[(size_t)r * ld + c];
     }
     t[i][threadIdx.x] = v;
   }
   __syncthreads();
+  const int cols_out = ones_col >= 0 ? ones_col + 1 : cols;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int c = c0 + i, r = r0 + threadIdx.x;
-    if (c < cols && r < ldo) {
+    if (c < cols_out && r < ldo) {
       const float v = t[threadIdx.x][i];
       const float h = tf32_hi(v);
       o_hi[(size_t)c * ldo + r] = h;
@@ -1425,13 +1430,23 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int chunks, 
 
 // split-K partials [splits][rows][ldc] → grad, rows through the leaf segment
 // map (seg > 0), columns split into ≤ 3 tensors of width colw
+// bias (has_bias): product row `rows` is the column sum of dY (the ones row
+// of the transposed X), written through bdst like colsum's final pass
 __global__ void reduce_grad_kernel(const float* __restrict__ part, int splits, int64_t sstride,
                                    int rows, int cols, int ldc, int seg, int segp, ColDst dst,
-                                   float* __restrict__ grad) {
-  const int64_t total = (int64_t)rows * cols;
+                                   float* __restrict__ grad, int has_bias, ColDst bdst) {
+  const int64_t total = (int64_t)(rows + has_bias) * cols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(e / cols), c = (int)(e - (int64_t)r * cols);
+    if (r == rows) {
+      float v = part[(size_t)r * ldc + c];
+      for (int z = 1; z < splits; ++z) v += part[z * sstride + (size_t)r * ldc + c];
+      const int t = c / bdst.colw;
+      float* g = grad + bdst.d[t] + (c - t * bdst.colw);
+      *g = bdst.acc ? *g + v : v;
+      continue;
+    }
     int rr = r;
     if (seg) {
       const int j = r % segp;
@@ -1781,7 +1796,7 @@ Bwd carve_bwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, 
   }
   const int64_t pm = max(max((int64_t)M.d * p.qkvp, (int64_t)M.d_ff * p.dp),
                          max((int64_t)M.d * p.ffp, (int64_t)TPCB_MAX_LEAF * p.dp * p.dep));
-  b.part_floats = 8 * max(pm, (int64_t)dmax * dmax);
+  b.part_floats = 8 * (max(pm, (int64_t)dmax * dmax) + max(wmax, (int64_t)p.dep));  // + bias row
   b.part = cv->take(b.part_floats);
   for (int k = 0; k < 2; ++k) {
     b.dd_hi[k] = cv->take(A * dmax);
@@ -1802,9 +1817,10 @@ Bwd carve_bwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, 
 }
 
 int transpose_into(const float* hi, const float* lo, int rows, int cols, int ld, float* o_hi,
-                   float* o_lo, int ldo, cudaStream_t st) {
-  const dim3 grid((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(ldo, 32));
-  transpose_pair_kernel<<<grid, dim3(32, 8), 0, st>>>(hi, lo, rows, cols, ld, o_hi, o_lo, ldo);
+                   float* o_lo, int ldo, cudaStream_t st, bool ones_row = false) {
+  const dim3 grid((unsigned)ceil_div(cols + (ones_row ? 1 : 0), 32), (unsigned)ceil_div(ldo, 32));
+  transpose_pair_kernel<<<grid, dim3(32, 8), 0, st>>>(hi, lo, rows, cols, ld, o_hi, o_lo, ldo,
+                                                      ones_row ? cols : -1);
   TPCB_LAUNCH_CHECK("large_transpose");
   return TPCB_OK;
 }
@@ -1868,32 +1884,36 @@ ColDst one(int64_t off, int colw, int acc = 0) { return ColDst{colw, {off, off, 
 // still be reading (kXtRing wgrads later) and at the final join.
 int wgrad(const Ctx& c, Bwd& b, const float* x_hi, const float* x_lo, int ld_x, int m_in,
           const float* y_hi, const float* y_lo, int ld_y, int n_out, int rows, int seg, int segp,
-          ColDst dst, float* grad) {
+          ColDst dst, float* grad, const ColDst* bias = nullptr) {
   const cudaStream_t st = g_side.s;
   const int kp = pad32(rows);
   int rc;
   const int k = g_side.xt_slot;
   g_side.xt_slot = (k + 1) % kXtRing;
   if (g_side.xt_used[k]) TPCB_CUDA_CHECK(cudaStreamWaitEvent(c.st, g_side.xt_ev[k], 0));
-  if ((rc = transpose_into(x_hi, x_lo, rows, m_in, ld_x, b.xt_hi[k], b.xt_lo[k], kp, c.st)))
+  // bias: X gets a ones row (product row m_in = the column sums of dY)
+  const int hb = bias ? 1 : 0, m_all = m_in + hb;
+  if ((rc = transpose_into(x_hi, x_lo, rows, m_in, ld_x, b.xt_hi[k], b.xt_lo[k], kp, c.st,
+                           bias != nullptr)))
     return rc;
   if ((rc = transpose_into(y_hi, y_lo, rows, n_out, ld_y, b.yt_hi[k], b.yt_lo[k], kp, c.st)))
     return rc;
   if ((rc = stream_wait(st, c.st))) return rc;  // fork: the transposed operands are ready
   const int ldc = pad32(n_out);
-  const int tiles = ceil_div(m_in, kTileM) * ceil_div(ldc, 128);
+  const int tiles = ceil_div(m_all, kTileM) * ceil_div(ldc, 128);
   const int k_total = kp / 32;
   int splits = max(1, min(min(2 * kNumSMs / max(tiles, 1), k_total / 4), 8));
-  if ((size_t)splits * m_in * ldc > b.part_floats) return TPCB_ERR_VALIDATION;
-  Epi e{m_in, n_out, ldc, nullptr, 0, nullptr, nullptr, 0, b.part, nullptr, nullptr};
-  e.split_stride = (int64_t)m_in * ldc;
-  Operand A{b.xt_hi[k], b.xt_lo[k], m_in, kp, kp}, B{b.yt_hi[k], b.yt_lo[k], n_out, kp, kp};
+  if ((size_t)splits * m_all * ldc > b.part_floats) return TPCB_ERR_VALIDATION;
+  Epi e{m_all, n_out, ldc, nullptr, 0, nullptr, nullptr, 0, b.part, nullptr, nullptr};
+  e.split_stride = (int64_t)m_all * ldc;
+  Operand A{b.xt_hi[k], b.xt_lo[k], m_all, kp, kp}, B{b.yt_hi[k], b.yt_lo[k], n_out, kp, kp};
   if ((rc = launch_gemm_nt<128>(A, B, e, st, splits, &splits))) return rc;
   TPCB_CUDA_CHECK(cudaEventRecord(g_side.xt_ev[k], st));
   g_side.xt_used[k] = true;
-  const int64_t total = (int64_t)m_in * n_out;
+  const int64_t total = (int64_t)m_all * n_out;
   reduce_grad_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, kNumSMs * 8), 256, 0, st>>>(
-      b.part, splits, e.split_stride, m_in, n_out, ldc, seg, segp, dst, grad);
+      b.part, splits, e.split_stride, m_in, n_out, ldc, seg, segp, dst, grad, hb,
+      bias ? *bias : ColDst{1, {0, 0, 0}, 0});
   TPCB_LAUNCH_CHECK("large_reduce_grad");
   return TPCB_OK;
 }
@@ -1934,12 +1954,10 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     Operand B{c.im.hi + p.leaf_b[Lb], c.im.lo + p.leaf_b[Lb], w, p.dep, p.dep};
     Epi e{nbk, w, w, nullptr, 0, nullptr, nullptr, 0, b.dh + t0 * p.dp, nullptr, nullptr};
     if ((rc = launch_gemm(A, B, e, st))) return rc;
+    const ColDst lb = one(M.leafb[Lb], M.d_e, acc);  // bias: the GEMM's ones row
     if ((rc = wgrad(c, b, hf.hi + t0 * p.dp, hf.lo + t0 * p.dp, w, w, b.dzx_hi + s0 * p.dep,
                     b.dzx_lo + s0 * p.dep, p.dep, M.d_e, nbk, M.d, p.dp, one(M.leafW[Lb], M.d_e, acc),
-                    G)))
-      return rc;
-    if ((rc = colsum(b.dzx_hi + s0 * p.dep, b.dzx_lo + s0 * p.dep, nbk, M.d_e, p.dep,
-                     one(M.leafb[Lb], M.d_e, acc), G, st)))
+                    G, &lb)))
       return rc;
     s0 = s1;
   }
@@ -1960,10 +1978,10 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     if ((rc = colsum(b.prod, nullptr, nt, M.d, p.dp, one(L.ln2g, M.d, acc), G, st))) return rc;
     if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln2b, M.d, acc), G, st))) return rc;
     // FFN out
+    const ColDst fob = one(L.fob, M.d, acc), fhb = one(L.fhb, M.d_ff, acc), bo = one(L.bo, M.d, acc);
     if ((rc = wgrad(c, b, ff.hi, ff.lo, p.ffp, M.d_ff, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
-                    one(L.foW, M.d, acc), G)))
+                    one(L.foW, M.d, acc), G, &fob)))
       return rc;
-    if ((rc = colsum(b.ds_hi, b.ds_lo, nt, M.d, p.dp, one(L.fob, M.d, acc), G, st))) return rc;
     {
       Epi e{nt, M.d_ff, p.ffp, nullptr, 0, nullptr, nullptr, 0, nullptr, b.df_hi, b.df_lo};
       e.mask = ff.hi;
@@ -1973,9 +1991,8 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     }
     // FFN hidden
     if ((rc = wgrad(c, b, h1.hi, h1.lo, p.dp, M.d, b.df_hi, b.df_lo, p.ffp, M.d_ff, nt, 0, 0,
-                    one(L.fhW, M.d_ff, acc), G)))
+                    one(L.fhW, M.d_ff, acc), G, &fhb)))
       return rc;
-    if ((rc = colsum(b.df_hi, b.df_lo, nt, M.d_ff, p.ffp, one(L.fhb, M.d_ff, acc), G, st))) return rc;
     {
       Epi e{nt, M.d, p.dp, nullptr, 0, b.ds_hi, b.ds_lo, p.dp, b.dh, nullptr, nullptr};
       Operand B{c.im.hi + p.layer_b[li][2], c.im.lo + p.layer_b[li][2], M.d, p.ffp, p.ffp};
@@ -1989,9 +2006,8 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln1b, M.d, acc), G, st))) return rc;
     // attention output projection
     if ((rc = wgrad(c, b, ctx.hi, ctx.lo, p.dp, M.d, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
-                    one(L.Wo, M.d, acc), G)))
+                    one(L.Wo, M.d, acc), G, &bo)))
       return rc;
-    if ((rc = colsum(b.ds_hi, b.ds_lo, nt, M.d, p.dp, one(L.bo, M.d, acc), G, st))) return rc;
     {
       Epi e{nt, M.d, p.dp, nullptr, 0, nullptr, nullptr, 0, b.dctx, nullptr, nullptr};
       Operand B{c.im.hi + p.layer_b[li][1], c.im.lo + p.layer_b[li][1], M.d, p.dp, p.dp};
@@ -2005,9 +2021,8 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     const ColDst qkv_dst{M.d, {(int64_t)L.Wq, (int64_t)L.Wk, (int64_t)L.Wv}, acc};
     const ColDst qkvb_dst{M.d, {(int64_t)L.bq, (int64_t)L.bk, (int64_t)L.bv}, acc};
     if ((rc = wgrad(c, b, h.hi, h.lo, p.dp, M.d, b.dq_hi, b.dq_lo, p.qkvp, p.qkv, nt, 0, 0,
-                    qkv_dst, G)))
+                    qkv_dst, G, &qkvb_dst)))
       return rc;
-    if ((rc = colsum(b.dq_hi, b.dq_lo, nt, p.qkv, p.qkvp, qkvb_dst, G, st))) return rc;
     {
       Epi e{nt, M.d, p.dp, nullptr, 0, b.ds_hi, b.ds_lo, p.dp, b.dh, nullptr, nullptr};
       Operand B{c.im.hi + p.layer_b[li][0], c.im.lo + p.layer_b[li][0], M.d, p.qkvp, p.qkvp};
@@ -2015,10 +2030,10 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     }
   }
   // input projection
+  const ColDst inb = one(M.inb, M.d, acc);
   if ((rc = wgrad(c, b, f.x_hi, f.x_lo, 32, TPCB_FEAT, b.dh, nullptr, p.dp, M.d, nt, 0, 0,
-                  one(M.inW, M.d, acc), G)))
+                  one(M.inW, M.d, acc), G, &inb)))
     return rc;
-  if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(M.inb, M.d, acc), G, st))) return rc;
   return TPCB_OK;
 }
 
@@ -2179,10 +2194,9 @@ extern "C" int tpcb_large_loss_backward(const tpcb_model* m, const float* d_para
     const int wi = i ? M.dec[i - 1] : M.d_e, ldi = pad32(wi);
     const float* in_hi = i ? f.dec_hi[i - 1] : f.z_hi;
     const float* in_lo = i ? f.dec_lo[i - 1] : f.z_lo;
+    const ColDst db = one(M.decb[i], wo);
     if ((rc = wgrad(c, b, in_hi, in_lo, ldi, wi, b.dd_hi[cur], b.dd_lo[cur], ldo, wo, nb, 0, 0,
-                    one(M.decW[i], wo), G)))
-      return rc;
-    if ((rc = colsum(b.dd_hi[cur], b.dd_lo[cur], nb, wo, ldo, one(M.decb[i], wo), G, st)))
+                    one(M.decW[i], wo), G, &db)))
       return rc;
     Operand A = act_op(b.dd_hi[cur], b.dd_lo[cur], nb, ldo);
     Operand B{c.im.hi + p.dec_b[i], c.im.lo + p.dec_b[i], wi, ldo, ldo};
