@@ -1269,33 +1269,45 @@ namespace {
 
 // [rows, cols] (row stride ld; pair or fp32 when a_lo == null) → pair
 // [cols][ldo], zero for rows <= r < ldo
-// ones_col >= 0: that output row is all ones over the real rows (the bias
-// gradient folded into the weight-gradient GEMM as one more product row)
-__global__ void transpose_pair_kernel(const float* __restrict__ a_hi, const float* __restrict__ a_lo,
-                                      int rows, int cols, int ld, float* __restrict__ o_hi,
-                                      float* __restrict__ o_lo, int ldo, int ones_col) {
-  __shared__ float t[32][33];
+// One transposed (hi, lo) operand: out[c][r] = split(in_hi[r][c] + in_lo[r][c])
+// for c < cols, r < ldo (zero beyond `rows`); ones_col >= 0: that output row
+// is all ones over the real rows (the bias gradient folded into the
+// weight-gradient GEMM as one more product row).
+struct TJob {
+  const float* hi;
+  const float* lo;
+  int rows, cols, ld;
+  float* o_hi;
+  float* o_lo;
+  int ldo, ones_col;
+};
+
+// both operands of a weight-gradient product in one launch (blockIdx.z)
+__global__ void transpose_pair_kernel(TJob j0, TJob j1) {
+  const TJob J = blockIdx.z ? j1 : j0;
+  const int cols_out = J.ones_col >= 0 ? J.ones_col + 1 : J.cols;
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  if (c0 >= cols_out || r0 >= J.ldo) return;  // the grid covers the larger job
+  __shared__ float t[32][33];
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
     float v = 0.f;
-    if (c == ones_col) {
-      v = r < rows ? 1.f : 0.f;
-    } else if (r < rows && c < cols) {
-      v = a_hi[(size_t)r * ld + c];
-      if (a_lo) v += a_lo[(size_t)r * ld + c];
+    if (c == J.ones_col) {
+      v = r < J.rows ? 1.f : 0.f;
+    } else if (r < J.rows && c < J.cols) {
+      v = J.hi[(size_t)r * J.ld + c];
+      if (J.lo) v += J.lo[(size_t)r * J.ld + c];
     }
     t[i][threadIdx.x] = v;
   }
   __syncthreads();
-  const int cols_out = ones_col >= 0 ? ones_col + 1 : cols;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int c = c0 + i, r = r0 + threadIdx.x;
-    if (c < cols_out && r < ldo) {
+    if (c < cols_out && r < J.ldo) {
       const float v = t[threadIdx.x][i];
       const float h = tf32_hi(v);
-      o_hi[(size_t)c * ldo + r] = h;
-      o_lo[(size_t)c * ldo + r] = v - h;
+      J.o_hi[(size_t)c * J.ldo + r] = h;
+      J.o_lo[(size_t)c * J.ldo + r] = v - h;
     }
   }
 }
@@ -1816,11 +1828,10 @@ Bwd carve_bwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, 
   return b;
 }
 
-int transpose_into(const float* hi, const float* lo, int rows, int cols, int ld, float* o_hi,
-                   float* o_lo, int ldo, cudaStream_t st, bool ones_row = false) {
-  const dim3 grid((unsigned)ceil_div(cols + (ones_row ? 1 : 0), 32), (unsigned)ceil_div(ldo, 32));
-  transpose_pair_kernel<<<grid, dim3(32, 8), 0, st>>>(hi, lo, rows, cols, ld, o_hi, o_lo, ldo,
-                                                      ones_row ? cols : -1);
+int transpose_pair(const TJob& a, const TJob& b, cudaStream_t st) {
+  const int ca = a.ones_col >= 0 ? a.ones_col + 1 : a.cols, cb = b.ones_col >= 0 ? b.ones_col + 1 : b.cols;
+  const dim3 grid((unsigned)ceil_div(max(ca, cb), 32), (unsigned)ceil_div(max(a.ldo, b.ldo), 32), 2);
+  transpose_pair_kernel<<<grid, dim3(32, 8), 0, st>>>(a, b);
   TPCB_LAUNCH_CHECK("large_transpose");
   return TPCB_OK;
 }
@@ -1893,10 +1904,10 @@ int wgrad(const Ctx& c, Bwd& b, const float* x_hi, const float* x_lo, int ld_x, 
   if (g_side.xt_used[k]) TPCB_CUDA_CHECK(cudaStreamWaitEvent(c.st, g_side.xt_ev[k], 0));
   // bias: X gets a ones row (product row m_in = the column sums of dY)
   const int hb = bias ? 1 : 0, m_all = m_in + hb;
-  if ((rc = transpose_into(x_hi, x_lo, rows, m_in, ld_x, b.xt_hi[k], b.xt_lo[k], kp, c.st,
-                           bias != nullptr)))
-    return rc;
-  if ((rc = transpose_into(y_hi, y_lo, rows, n_out, ld_y, b.yt_hi[k], b.yt_lo[k], kp, c.st)))
+  if ((rc = transpose_pair(TJob{x_hi, x_lo, rows, m_in, ld_x, b.xt_hi[k], b.xt_lo[k], kp,
+                                bias ? m_in : -1},
+                           TJob{y_hi, y_lo, rows, n_out, ld_y, b.yt_hi[k], b.yt_lo[k], kp, -1},
+                           c.st)))
     return rc;
   if ((rc = stream_wait(st, c.st))) return rc;  // fork: the transposed operands are ready
   const int ldc = pad32(n_out);
