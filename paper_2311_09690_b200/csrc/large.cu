@@ -1360,12 +1360,22 @@ __global__ void colsum_partial_kernel(const float* __restrict__ x, const float* 
 // one launch: the chunk partials of colsum_partial_kernel, then the last chunk
 // block of each 32-column stripe (a counter per stripe, reset for the next
 // call) sums the stripe's partials in chunk order — colsum_final_kernel's fold
+// gridDim.z == 2: a second job (x2, no lo part, dst2) over the same shape —
+// its own partials and stripe counters (the LayerNorm γ / β pair)
 __global__ void colsum_fused_kernel(const float* __restrict__ x, const float* __restrict__ x_lo,
                                     int rows, int cols, int ld, float* __restrict__ part,
                                     unsigned* __restrict__ cnt, ColDst dst,
-                                    float* __restrict__ grad) {
+                                    float* __restrict__ grad, const float* __restrict__ x2 = nullptr,
+                                    ColDst dst2 = ColDst{1, {0, 0, 0}, 0}) {
   __shared__ float red[8][33];
   __shared__ bool last;
+  if (blockIdx.z) {
+    x = x2;
+    x_lo = nullptr;
+    dst = dst2;
+    part += (size_t)gridDim.y * cols;
+    cnt += kColCntMax / 2;
+  }
   const int c = blockIdx.x * 32 + threadIdx.x;
   const int r0 = blockIdx.y * kColChunk, r1 = min(r0 + kColChunk, rows);
   float acc = 0.f;
@@ -1822,7 +1832,7 @@ Bwd carve_bwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, 
   b.tWh = cv->take(A * TPCB_DEV_FEAT * M.d_dev);
   b.tbh = cv->take(A * M.d_dev);
   b.dpred = cv->take(A);
-  b.colpart = cv->take((size_t)ceil_div(max(T, A), kColChunk) *
+  b.colpart = cv->take(2 * (size_t)ceil_div(max(T, A), kColChunk) *  // 2: colsum2's jobs
                        max(max(M.d_dev * M.d_e, p.qkvp), max(p.ffp, dmax)));
   b.colcnt = reinterpret_cast<unsigned*>(cv->take(kColCntMax));
   return b;
@@ -1866,6 +1876,17 @@ int stream_wait(cudaStream_t waiter, cudaStream_t on) {
   cudaEvent_t e = g_side.next();
   TPCB_CUDA_CHECK(cudaEventRecord(e, on));
   TPCB_CUDA_CHECK(cudaStreamWaitEvent(waiter, e, 0));
+  return TPCB_OK;
+}
+
+// γ / β of a LayerNorm backward: the column sums of prod and dy in one launch
+int colsum2(const float* x, ColDst dst, const float* x2, ColDst dst2, int rows, int cols, int ld,
+            float* grad, cudaStream_t st) {
+  const int chunks = max(1, ceil_div(rows, kColChunk));
+  if (!g_colsum_cnt || ceil_div(cols, 32) > kColCntMax / 2) return TPCB_ERR_VALIDATION;
+  colsum_fused_kernel<<<dim3(ceil_div(cols, 32), chunks, 2), dim3(32, 8), 0, st>>>(
+      x, nullptr, rows, cols, ld, g_colsum_part, g_colsum_cnt, dst, grad, x2, dst2);
+  TPCB_LAUNCH_CHECK("large_colsum2");
   return TPCB_OK;
 }
 
@@ -1986,8 +2007,9 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S2(li), p.dp, nt, M.d, P + L.ln2g,
                                                     b.ds_hi, b.ds_lo, b.prod);
     TPCB_LAUNCH_CHECK("large_ln_back");
-    if ((rc = colsum(b.prod, nullptr, nt, M.d, p.dp, one(L.ln2g, M.d, acc), G, st))) return rc;
-    if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln2b, M.d, acc), G, st))) return rc;
+    if ((rc = colsum2(b.prod, one(L.ln2g, M.d, acc), b.dh, one(L.ln2b, M.d, acc), nt, M.d, p.dp, G,
+                      st)))
+      return rc;
     // FFN out
     const ColDst fob = one(L.fob, M.d, acc), fhb = one(L.fhb, M.d_ff, acc), bo = one(L.bo, M.d, acc);
     if ((rc = wgrad(c, b, ff.hi, ff.lo, p.ffp, M.d_ff, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
@@ -2013,8 +2035,9 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S1(li), p.dp, nt, M.d, P + L.ln1g,
                                                     b.ds_hi, b.ds_lo, b.prod);
     TPCB_LAUNCH_CHECK("large_ln_back");
-    if ((rc = colsum(b.prod, nullptr, nt, M.d, p.dp, one(L.ln1g, M.d, acc), G, st))) return rc;
-    if ((rc = colsum(b.dh, nullptr, nt, M.d, p.dp, one(L.ln1b, M.d, acc), G, st))) return rc;
+    if ((rc = colsum2(b.prod, one(L.ln1g, M.d, acc), b.dh, one(L.ln1b, M.d, acc), nt, M.d, p.dp, G,
+                      st)))
+      return rc;
     // attention output projection
     if ((rc = wgrad(c, b, ctx.hi, ctx.lo, p.dp, M.d, b.ds_hi, b.ds_lo, p.dp, M.d, nt, 0, 0,
                     one(L.Wo, M.d, acc), G, &bo)))
