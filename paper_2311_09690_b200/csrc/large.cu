@@ -478,15 +478,15 @@ __device__ __forceinline__ float group_sum(float v, int g) {
 __global__ void attention_kernel(const float* __restrict__ qkv, int ldq,
                                  const int32_t* __restrict__ tok_off, int d, int nh, int dh,
                                  float scale, int ldc, float* __restrict__ c_hi,
-                                 float* __restrict__ c_lo) {
-  extern __shared__ float sm[];
+                                 float* __restrict__ c_lo, int lcap) {
+  extern __shared__ float sm[];  // q, k, v: lcap rows each (lcap = the launch's max L)
   const int s = blockIdx.x, h = blockIdx.y;
   const int t0 = tok_off[s], L = tok_off[s + 1] - t0;
   const int dhp = dh + 1;  // odd stride: conflict-free row reads
   float* q = sm;
-  float* k = q + TPCB_MAX_LEAF * dhp;
-  float* v = k + TPCB_MAX_LEAF * dhp;
-  float* p = v + TPCB_MAX_LEAF * dhp;  // [16][17]
+  float* k = q + lcap * dhp;
+  float* v = k + lcap * dhp;
+  float* p = v + lcap * dhp;  // [16][17]
   for (int e = threadIdx.x; e < L * dh; e += blockDim.x) {
     const int l = e / dh, j = e - l * dh;
     const float* row = qkv + (size_t)(t0 + l) * ldq + h * dh + j;
@@ -1021,6 +1021,16 @@ Operand act_op(const float* hi, const float* lo, int64_t rows, int ld) {
 // the forward over the sorted tokens already gathered into f.x (host-side
 // bucket structure h_tok_off); latents / pred scattered by f.idx unless
 // `train` (then pred stays in sorted order in f.pred)
+// the largest leaf count of a batch (attention's shared-memory rows; the
+// training batches are single-bucket, so this is usually their L); long
+// inference batches keep the cap instead of scanning
+int max_leaf_count(const int32_t* h_tok_off, int64_t n) {
+  if (n > 65536) return TPCB_MAX_LEAF;
+  int m = 1;
+  for (int64_t s = 0; s < n; ++s) m = std::max(m, h_tok_off[s + 1] - h_tok_off[s]);
+  return std::min(m, TPCB_MAX_LEAF);
+}
+
 int run_forward(const Ctx& c, const Fwd& f, int64_t n_ast, const int32_t* h_tok_off,
                 const float* d_devfeat, bool train, const tpcb_boxcox& bc, float* d_pred,
                 float* d_zx, float* d_zv, float* d_z, double* d_lat, int32_t* d_status) {
@@ -1042,6 +1052,8 @@ int run_forward(const Ctx& c, const Fwd& f, int64_t n_ast, const int32_t* h_tok_
     TPCB_CUDA_CHECK(cudaFuncSetAttribute(attention_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)att_smem));
+  const int lcap = max_leaf_count(h_tok_off, n_ast);
+  const size_t att_used = (size_t)(3 * lcap * (M.dh + 1) + 16 * 17) * 4;
   for (int li = 0; li < M.n_layers; ++li) {
     const LayerOff& L = M.layer[li];
     const Pair h = f.H(li), hn = f.H(li + 1), ctx = f.C(li), h1 = f.H1(li), ff = f.F(li);
@@ -1053,8 +1065,8 @@ int run_forward(const Ctx& c, const Fwd& f, int64_t n_ast, const int32_t* h_tok_
                             st)))
         return rc;
     }
-    attention_kernel<<<dim3((unsigned)n_ast, M.n_heads), 128, att_smem, st>>>(
-        qkv, p.qkvp, f.tok_off, M.d, M.n_heads, M.dh, scale, p.dp, ctx.hi, ctx.lo);
+    attention_kernel<<<dim3((unsigned)n_ast, M.n_heads), 128, att_used, st>>>(
+        qkv, p.qkvp, f.tok_off, M.d, M.n_heads, M.dh, scale, p.dp, ctx.hi, ctx.lo, lcap);
     TPCB_LAUNCH_CHECK("large_attention");
     {
       Epi e{(int)n_tok, M.d, p.dp, P + L.bo, 0, h.hi, h.lo, p.dp, f.S1(li), nullptr, nullptr};
@@ -1561,16 +1573,16 @@ __global__ void attention_back_kernel(const float* __restrict__ qkv, int ldq,
                                       const float* __restrict__ dctx, int ldc,
                                       const int32_t* __restrict__ tok_off, int d, int nh, int dh,
                                       float scale, float* __restrict__ g_hi,
-                                      float* __restrict__ g_lo) {
-  extern __shared__ float sm[];
+                                      float* __restrict__ g_lo, int lcap) {
+  extern __shared__ float sm[];  // q, k, v, dctx: lcap rows each
   const int s = blockIdx.x, h = blockIdx.y;
   const int t0 = tok_off[s], L = tok_off[s + 1] - t0;
   const int dhp = dh + 1;
   float* q = sm;
-  float* k = q + TPCB_MAX_LEAF * dhp;
-  float* v = k + TPCB_MAX_LEAF * dhp;
-  float* dc = v + TPCB_MAX_LEAF * dhp;
-  float* p = dc + TPCB_MAX_LEAF * dhp;  // [16][17]
+  float* k = q + lcap * dhp;
+  float* v = k + lcap * dhp;
+  float* dc = v + lcap * dhp;
+  float* p = dc + lcap * dhp;  // [16][17]
   float* dp = p + 16 * 17;              // [16][17]
   for (int e = threadIdx.x; e < L * dh; e += blockDim.x) {
     const int l = e / dh, j = e - l * dh;
@@ -2000,6 +2012,8 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     TPCB_CUDA_CHECK(cudaFuncSetAttribute(attention_back_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)att_smem));
+  const int lcap = max_leaf_count(h_tok_off, n_batch);
+  const size_t att_used = (size_t)(4 * lcap * (M.dh + 1) + 2 * 16 * 17) * 4;
   for (int li = M.n_layers - 1; li >= 0; --li) {
     const LayerOff& L = M.layer[li];
     const Pair h = f.H(li), h1 = f.H1(li), ff = f.F(li), ctx = f.C(li);
@@ -2047,9 +2061,9 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
       Operand B{c.im.hi + p.layer_b[li][1], c.im.lo + p.layer_b[li][1], M.d, p.dp, p.dp};
       if ((rc = launch_gemm(act_op(b.ds_hi, b.ds_lo, nt, p.dp), B, e, st))) return rc;
     }
-    attention_back_kernel<<<dim3((unsigned)n_batch, M.n_heads), 128, att_smem, st>>>(
+    attention_back_kernel<<<dim3((unsigned)n_batch, M.n_heads), 128, att_used, st>>>(
         f.QKV(li), p.qkvp, b.dctx, p.dp, f.tok_off, M.d, M.n_heads, M.dh, scale, b.dq_hi,
-        b.dq_lo);
+        b.dq_lo, lcap);
     TPCB_LAUNCH_CHECK("large_attention_back");
     // Q | K | V projections
     const ColDst qkv_dst{M.d, {(int64_t)L.Wq, (int64_t)L.Wk, (int64_t)L.Wv}, acc};
