@@ -1946,7 +1946,8 @@ int wgrad(const Ctx& c, Bwd& b, const float* x_hi, const float* x_lo, int ld_x, 
   const int ldc = pad32(n_out);
   const int tiles = ceil_div(m_all, kTileM) * ceil_div(ldc, 128);
   const int k_total = kp / 32;
-  int splits = max(1, min(min(2 * kNumSMs / max(tiles, 1), k_total / 4), 8));
+  // one wave: gemm3 runs one CTA per SM (197 KB of operand ring)
+  int splits = max(1, min(min(kNumSMs / max(tiles, 1), k_total / 4), 8));
   if ((size_t)splits * m_all * ldc > b.part_floats) return TPCB_ERR_VALIDATION;
   Epi e{m_all, n_out, ldc, nullptr, 0, nullptr, nullptr, 0, b.part, nullptr, nullptr};
   e.split_stride = (int64_t)m_all * ldc;
