@@ -1294,32 +1294,50 @@ struct TJob {
   int ldo, ones_col;
 };
 
-// both operands of a weight-gradient product in one launch (blockIdx.z)
-__global__ void transpose_pair_kernel(TJob j0, TJob j1) {
+// both operands of a weight-gradient product in one launch (blockIdx.z);
+// 64 × 64 tiles, 32 elements of each half per thread in flight.  A (hi, lo)
+// input is an exact split (lo = x − tf32(x)), so re-splitting hi + lo gives
+// the same pair back: the halves are transposed as they are; a plain input
+// (lo == null) is split here.
+__global__ void __launch_bounds__(256) transpose_pair_kernel(TJob j0, TJob j1) {
   const TJob J = blockIdx.z ? j1 : j0;
   const int cols_out = J.ones_col >= 0 ? J.ones_col + 1 : J.cols;
-  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int c0 = blockIdx.x * 64, r0 = blockIdx.y * 64;
   if (c0 >= cols_out || r0 >= J.ldo) return;  // the grid covers the larger job
-  __shared__ float t[32][33];
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int r = r0 + i, c = c0 + threadIdx.x;
-    float v = 0.f;
+  __shared__ float th[64][65], tl[64][65];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  float vh[16], vl[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = r0 + ty + 8 * (i >> 1), c = c0 + tx + 32 * (i & 1);
+    vh[i] = 0.f;
+    vl[i] = 0.f;
     if (c == J.ones_col) {
-      v = r < J.rows ? 1.f : 0.f;
+      vh[i] = r < J.rows ? 1.f : 0.f;
     } else if (r < J.rows && c < J.cols) {
-      v = J.hi[(size_t)r * J.ld + c];
-      if (J.lo) v += J.lo[(size_t)r * J.ld + c];
+      vh[i] = J.hi[(size_t)r * J.ld + c];
+      if (J.lo) vl[i] = J.lo[(size_t)r * J.ld + c];
     }
-    t[i][threadIdx.x] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int rr = ty + 8 * (i >> 1), cc = tx + 32 * (i & 1);
+    float h = vh[i], l = vl[i];
+    if (!J.lo) {
+      h = tf32_hi(vh[i]);
+      l = vh[i] - h;
+    }
+    th[rr][cc] = h;
+    tl[rr][cc] = l;
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int c = c0 + i, r = r0 + threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int cc = ty + 8 * (i >> 1), rr = tx + 32 * (i & 1);
+    const int c = c0 + cc, r = r0 + rr;
     if (c < cols_out && r < J.ldo) {
-      const float v = t[threadIdx.x][i];
-      const float h = tf32_hi(v);
-      J.o_hi[(size_t)c * J.ldo + r] = h;
-      J.o_lo[(size_t)c * J.ldo + r] = v - h;
+      J.o_hi[(size_t)c * J.ldo + r] = th[rr][cc];
+      J.o_lo[(size_t)c * J.ldo + r] = tl[rr][cc];
     }
   }
 }
@@ -1852,7 +1870,7 @@ Bwd carve_bwd(const LargePlan& p, const Model& M, int64_t n_tok, int64_t n_ast, 
 
 int transpose_pair(const TJob& a, const TJob& b, cudaStream_t st) {
   const int ca = a.ones_col >= 0 ? a.ones_col + 1 : a.cols, cb = b.ones_col >= 0 ? b.ones_col + 1 : b.cols;
-  const dim3 grid((unsigned)ceil_div(max(ca, cb), 32), (unsigned)ceil_div(max(a.ldo, b.ldo), 32), 2);
+  const dim3 grid((unsigned)ceil_div(max(ca, cb), 64), (unsigned)ceil_div(max(a.ldo, b.ldo), 64), 2);
   transpose_pair_kernel<<<grid, dim3(32, 8), 0, st>>>(a, b);
   TPCB_LAUNCH_CHECK("large_transpose");
   return TPCB_OK;
