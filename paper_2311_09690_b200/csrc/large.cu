@@ -1547,6 +1547,65 @@ __global__ void add_cmd_kernel(double* loss, const double* cmd, double alpha, do
 
 // LayerNorm backward (nn.py:57-66), one warp per row: dx = rstd·(dŷ − mean(dŷ)
 // − x̂·mean(dŷ·x̂)), dŷ = dy·g; prod = dy·x̂ (→ dg by column sums)
+// the row in registers (ld <= 32·PER): one load of x, dy and γ per element,
+// all in flight together; same passes and order as ln_back_kernel
+template <int PER>
+__global__ void ln_back_reg_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+                                   int ld, int rows, int d, const float* __restrict__ g,
+                                   float* __restrict__ dx_hi, float* __restrict__ dx_lo,
+                                   float* __restrict__ prod) {
+  const int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const float* xr = x + (size_t)r * ld;
+  const float* dr = dy + (size_t)r * ld;
+  float xv[PER], dv[PER], gv[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int j = lane + 32 * u;
+    xv[u] = j < d ? xr[j] : 0.f;
+    dv[u] = j < d ? dr[j] : 0.f;
+    gv[u] = j < d ? g[j] : 0.f;
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int u = 0; u < PER; ++u)
+    if (lane + 32 * u < d) s += xv[u];
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int u = 0; u < PER; ++u)
+    if (lane + 32 * u < d) {
+      const float t = xv[u] - mean;
+      q = fmaf(t, t, q);
+    }
+  const float rstd = rsqrtf(warp_sum(q) / d + 1e-5f);
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int u = 0; u < PER; ++u)
+    if (lane + 32 * u < d) {
+      const float xh = (xv[u] - mean) * rstd, dxh = dv[u] * gv[u];
+      s1 += dxh;
+      s2 = fmaf(dxh, xh, s2);
+    }
+  const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) / d;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int j = lane + 32 * u;
+    if (j >= ld) break;
+    float o = 0.f, pr = 0.f;
+    if (j < d) {
+      const float xh = (xv[u] - mean) * rstd, dxh = dv[u] * gv[u];
+      o = rstd * (dxh - m1 - xh * m2);
+      pr = dv[u] * xh;
+    }
+    const float h = tf32_hi(o);
+    dx_hi[(size_t)r * ld + j] = h;
+    dx_lo[(size_t)r * ld + j] = o - h;
+    prod[(size_t)r * ld + j] = pr;
+  }
+}
+
 __global__ void ln_back_kernel(const float* __restrict__ dy, const float* __restrict__ x, int ld,
                                int rows, int d, const float* __restrict__ g,
                                float* __restrict__ dx_hi, float* __restrict__ dx_lo,
@@ -2037,8 +2096,12 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
     const LayerOff& L = M.layer[li];
     const Pair h = f.H(li), h1 = f.H1(li), ff = f.F(li), ctx = f.C(li);
     // LN2
-    ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S2(li), p.dp, nt, M.d, P + L.ln2g,
-                                                    b.ds_hi, b.ds_lo, b.prod);
+    if (p.dp <= 768)
+      ln_back_reg_kernel<24><<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S2(li), p.dp, nt, M.d,
+                                                              P + L.ln2g, b.ds_hi, b.ds_lo, b.prod);
+    else
+      ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S2(li), p.dp, nt, M.d, P + L.ln2g,
+                                                      b.ds_hi, b.ds_lo, b.prod);
     TPCB_LAUNCH_CHECK("large_ln_back");
     if ((rc = colsum2(b.prod, one(L.ln2g, M.d, acc), b.dh, one(L.ln2b, M.d, acc), nt, M.d, p.dp, G,
                       st)))
@@ -2065,8 +2128,12 @@ int large_tail(const Ctx& c, const Fwd& f, Bwd& b, const int32_t* h_tok_off, int
       if ((rc = launch_gemm(act_op(b.df_hi, b.df_lo, nt, p.ffp), B, e, st))) return rc;
     }
     // LN1
-    ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S1(li), p.dp, nt, M.d, P + L.ln1g,
-                                                    b.ds_hi, b.ds_lo, b.prod);
+    if (p.dp <= 768)
+      ln_back_reg_kernel<24><<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S1(li), p.dp, nt, M.d,
+                                                              P + L.ln1g, b.ds_hi, b.ds_lo, b.prod);
+    else
+      ln_back_kernel<<<ceil_div(nt, 8), 256, 0, st>>>(b.dh, f.S1(li), p.dp, nt, M.d, P + L.ln1g,
+                                                      b.ds_hi, b.ds_lo, b.prod);
     TPCB_LAUNCH_CHECK("large_ln_back");
     if ((rc = colsum2(b.prod, one(L.ln1g, M.d, acc), b.dh, one(L.ln1b, M.d, acc), nt, M.d, p.dp, G,
                       st)))
